@@ -1,0 +1,245 @@
+/*
+ * wc4dvar_gpu.h -- C-ABI of the B200 (sm_100a) randomized-LMP hot path.
+ *
+ * Drop-in boundary for the reference's operator / sketch / LMP / PCG API
+ * (/root/reference/proj, C++20 + Eigen 3).  Every entry point names the
+ * reference interface it replaces (file:line relative to /root/reference/).
+ * INTEGRATION.md shows the C++ adapter a maintainer would add on the
+ * reference side (a `GpuHessianOperator : wc4dvar::LinearOperator`).
+ *
+ * Conventions
+ *  - All matrices are column-major fp64 with an explicit leading dimension,
+ *    exactly Eigen's default MatrixXd layout (types.hpp:9-11).
+ *  - Functions without a `_dev` suffix take HOST pointers and copy through
+ *    pinned staging buffers; `_dev` variants take device pointers on the
+ *    operator's device and a cudaStream_t passed as `void*` (NULL = the
+ *    handle's own stream).
+ *  - Every function returns a status code; on failure the thread-local
+ *    message is in wc4dvar_gpu_last_error().  Codes mirror the reference's
+ *    exception types (types.hpp:14-30):
+ *        1 std::invalid_argument (require), 2 NumericalError,
+ *        3 device failure (no reference equivalent), 4 DenseCapError.
+ *  - Handles are thread-safe: calls on one handle are serialised internally
+ *    (the reference's apply/apply_block are const and reentrant,
+ *    operators.hpp:30 / SPEC.md:271).
+ *  - Apply accounting follows LinearOperator::count (operators.hpp:32-39):
+ *    +1 per vector apply, +m per block apply of m columns.
+ */
+#ifndef WC4DVAR_GPU_H
+#define WC4DVAR_GPU_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum {
+    WC4DVAR_OK = 0,
+    WC4DVAR_INVALID_ARGUMENT = 1,
+    WC4DVAR_NUMERICAL = 2,
+    WC4DVAR_DEVICE = 3,
+    WC4DVAR_DENSE_CAP = 4
+};
+
+/* Thread-local message of the last failing call on this thread. */
+const char* wc4dvar_gpu_last_error(void);
+/* Library version string and the compiled device architecture ("sm_100a"). */
+const char* wc4dvar_gpu_version(void);
+
+/* ------------------------------------------------------------------------- */
+/* Operator descriptors                                                       */
+/* ------------------------------------------------------------------------- */
+
+/* LinearizedModel kinds (operators.hpp:57-111).  ADVDIFF and substeps > 1 are
+ * the BASELINE.json extensions. */
+enum {
+    WC4DVAR_MODEL_IDENTITY = 0,  /* IdentityLinearized, operators.hpp:100-111 */
+    WC4DVAR_MODEL_ADVECTION = 1, /* AdvectionLinearized, operators.cpp:31-42 */
+    WC4DVAR_MODEL_ADVDIFF = 2,   /* upwind advection + centred diffusion */
+    WC4DVAR_MODEL_LORENZ96 = 3   /* Lorenz96Linearized, operators.cpp:44-59 */
+};
+
+typedef struct {
+    int32_t kind;        /* WC4DVAR_MODEL_* */
+    int32_t N;           /* window intervals (ModelGrid::N, operators.hpp:125) */
+    int64_t n;           /* grid points (ModelGrid::n) */
+    int32_t substeps;    /* TL steps per interval; 1 = reference */
+    int32_t reserved;
+    double courant;      /* ADVECTION / ADVDIFF: c dt / dx */
+    double diffusion;    /* ADVDIFF: nu dt / dx^2 */
+    double dt;           /* LORENZ96 */
+    /* LORENZ96: host pointer to N*substeps stage sets, each [x1|x2|x3|x4] of
+     * 4n doubles (Lorenz96Stages::at, models.cpp:80-87), sub-step-major. */
+    const double* stages;
+} wc4dvar_model_desc;
+
+/* ObservationNetwork (models.hpp:45-56): observed times ascending, observed
+ * points ascending; q = n_times * n_points. */
+typedef struct {
+    int64_t n;
+    int32_t N;
+    int32_t n_times;
+    const int32_t* times;
+    int32_t n_points;
+    int32_t reserved;
+    const int32_t* points;
+} wc4dvar_network_desc;
+
+enum {
+    WC4DVAR_COV_DENSE = 0,    /* CovarianceFactor{half, half_inv}, covariance.hpp:31-38 */
+    WC4DVAR_COV_CIRCULANT = 1 /* EXTENSION: first columns of C^{1/2}, C^{-1/2} */
+};
+
+typedef struct {
+    int32_t kind;           /* WC4DVAR_COV_* */
+    int32_t reserved;
+    const double* half;     /* DENSE: n x n (symmetric); CIRCULANT: n */
+    const double* half_inv; /* same shape; may be NULL if D^{-1/2} is never used */
+} wc4dvar_cov_desc;
+
+typedef struct wc4dvar_op wc4dvar_op;
+
+/* HessianOperator ctor, operators.hpp:119-123 / operators.cpp:64-77:
+ * A = I + D^{1/2} L^{-T} H^T R^{-1} H L^{-1} D^{1/2}, R = sigma_obs^2 I. */
+int wc4dvar_gpu_hessian_create(const wc4dvar_model_desc* model,
+                               const wc4dvar_network_desc* net,
+                               const wc4dvar_cov_desc* background_half,
+                               const wc4dvar_cov_desc* model_error_half,
+                               double sigma_obs, int device, wc4dvar_op** out);
+
+/* DenseOperator, operators.hpp:42-53 (test/desk-scale operator). */
+int wc4dvar_gpu_dense_create(int64_t n, const double* A, int64_t lda, int device,
+                             wc4dvar_op** out);
+
+int wc4dvar_gpu_op_destroy(wc4dvar_op* op);
+int64_t wc4dvar_gpu_op_dim(const wc4dvar_op* op);
+/* LinearOperator::apply_count / reset_apply_count, operators.hpp:32-33. */
+int64_t wc4dvar_gpu_op_apply_count(const wc4dvar_op* op);
+void wc4dvar_gpu_op_reset_apply_count(wc4dvar_op* op);
+int wc4dvar_gpu_op_device(const wc4dvar_op* op);
+
+/* LinearOperator::apply (operators.hpp:23) and apply_block (operators.hpp:30,
+ * operators.cpp:9-19).  Column-major V (dim x m, ldv), out (dim x m, ldo). */
+int wc4dvar_gpu_op_apply(wc4dvar_op* op, const double* in, double* out);
+int wc4dvar_gpu_op_apply_block(wc4dvar_op* op, const double* V, int64_t ldv, int64_t m,
+                               double* out, int64_t ldo);
+int wc4dvar_gpu_op_apply_block_dev(wc4dvar_op* op, const double* V, int64_t ldv, int64_t m,
+                                   double* out, int64_t ldo, void* stream);
+
+/* HessianOperator pieces (operators.hpp:127-135), block forms (m columns):
+ * which = 0 apply_Linv (operators.cpp:79-89), 1 apply_LinvT (:91-101),
+ *         2 apply_D_half (:103-113), 3 apply_D_half_inv (:115-125).
+ * These do not count as operator applies, as in the reference. */
+enum { WC4DVAR_LINV = 0, WC4DVAR_LINVT = 1, WC4DVAR_D_HALF = 2, WC4DVAR_D_HALF_INV = 3 };
+int wc4dvar_gpu_hessian_piece(wc4dvar_op* op, int which, const double* V, int64_t ldv,
+                              int64_t m, double* out, int64_t ldo);
+int wc4dvar_gpu_hessian_piece_dev(wc4dvar_op* op, int which, const double* V, int64_t ldv,
+                                  int64_t m, double* out, int64_t ldo, void* stream);
+
+/* Stage profiling of HessianOperator block applies (CUDA events around the
+ * D^{1/2} GEMM, the fused sweep and the final D^{1/2} GEMM + identity term).
+ * enable != 0 resets the accumulators; read returns ms[3] summed over calls. */
+int wc4dvar_gpu_op_profile(wc4dvar_op* op, int enable);
+int wc4dvar_gpu_op_profile_read(wc4dvar_op* op, double* ms3, int64_t* calls);
+
+/* Diagnostics: sustained fp64 tensor-core (DMMA) throughput of this device in
+ * TFLOP/s, measured with an all-SM mma.sync.f64 loop (the roofline denominator
+ * for the D^{1/2} GEMM; MEASURED_PEAKS.json carries bf16 only). */
+int wc4dvar_gpu_probe_dmma_peak(int device, double* tflops);
+
+/* ------------------------------------------------------------------------- */
+/* Gaussian sketch matrix (randevd.cpp:16-21; NormalStream random.hpp:14-42)  */
+/* ------------------------------------------------------------------------- */
+/* Bit-exact with the reference stream (mt19937_64 + Box-Muller on glibc libm),
+ * column-major fill.  Host output. */
+int wc4dvar_gpu_gaussian_matrix(int64_t rows, int64_t cols, uint64_t seed, double* out);
+
+/* ------------------------------------------------------------------------- */
+/* Randomized eigenpairs (randevd.hpp:24-41)                                  */
+/* ------------------------------------------------------------------------- */
+enum { WC4DVAR_SKETCH_REVD = 0, WC4DVAR_SKETCH_NYSTROM = 1, WC4DVAR_SKETCH_RITZIT = 2 };
+
+/* SketchConfig, randevd.hpp:13-21; p_iter is the ritzit EXTENSION (1 = reference). */
+typedef struct {
+    int32_t target_rank; /* k */
+    int32_t oversample;  /* l */
+    uint64_t seed;
+    int32_t method;      /* WC4DVAR_SKETCH_* */
+    int32_t p_iter;
+} wc4dvar_sketch_config;
+
+/* sketch_eigenpairs (randevd.cpp:138-148).  omega: dim x (k+l) host matrix, or
+ * NULL to draw gaussian_matrix(dim, k+l, seed).  Outputs U (dim x k_out, ldu)
+ * and theta (k_out), decreasing; *k_out <= k (Nystrom caps at the rank). */
+int wc4dvar_gpu_sketch(wc4dvar_op* op, const wc4dvar_sketch_config* cfg, const double* omega,
+                       double* U, int64_t ldu, double* theta, int64_t* k_out);
+int wc4dvar_gpu_sketch_dev(wc4dvar_op* op, const wc4dvar_sketch_config* cfg,
+                           const double* omega_dev, double* U_dev, int64_t ldu,
+                           double* theta_dev, int64_t* k_out, void* stream);
+
+/* rayleigh_ritz (randevd.cpp:47-60): Z dim x m orthonormal -> all m pairs. */
+int wc4dvar_gpu_rayleigh_ritz(wc4dvar_op* op, const double* Z, int64_t ldz, int64_t m,
+                              double* U, int64_t ldu, double* theta);
+
+/* Per-stage device timings of the last sketch on this thread (ms):
+ * [0] block applies, [1] orthonormalisation, [2] small factorizations,
+ * [3] tall GEMMs, [4] total.  Used by bench.py. */
+int wc4dvar_gpu_last_sketch_timing(double* ms5);
+
+/* ------------------------------------------------------------------------- */
+/* Spectral LMP (lmp.hpp:12-28)                                               */
+/* ------------------------------------------------------------------------- */
+typedef struct wc4dvar_lmp wc4dvar_lmp;
+
+/* build_spectral_lmp (lmp.cpp:35-52): rejects theta <= 0 and an
+ * orthonormality defect > 1e-8.  k = 0 gives the identity factor. */
+int wc4dvar_gpu_lmp_build(int64_t n, int64_t k, const double* U, int64_t ldu,
+                          const double* theta, int device, wc4dvar_lmp** out);
+int wc4dvar_gpu_lmp_build_dev(int64_t n, int64_t k, const double* U_dev, int64_t ldu,
+                              const double* theta_dev, int device, wc4dvar_lmp** out);
+int wc4dvar_gpu_lmp_destroy(wc4dvar_lmp* lmp);
+/* LmpFactor::apply (C v, lmp.cpp:8-16) / apply_transpose (C^T v, lmp.cpp:18-26). */
+int wc4dvar_gpu_lmp_apply(wc4dvar_lmp* lmp, int transpose, const double* v, double* out);
+
+/* ------------------------------------------------------------------------- */
+/* Quadratic cost (assimilation.cpp:130-150) and split PCG (krylov.cpp:22-99) */
+/* ------------------------------------------------------------------------- */
+typedef struct wc4dvar_cost wc4dvar_cost;
+/* QuadraticCost(op, b, d): stores b~ = D^{-1/2} b and d (q). */
+int wc4dvar_gpu_cost_create(wc4dvar_op* hessian, const double* b, const double* d,
+                            wc4dvar_cost** out);
+int wc4dvar_gpu_cost_destroy(wc4dvar_cost* cost);
+int wc4dvar_gpu_cost_eval(wc4dvar_cost* cost, const double* x, double* value);
+int wc4dvar_gpu_cost_rhs(wc4dvar_cost* cost, double* rhs);
+
+/* PcgOptions (krylov.hpp:32-38). */
+typedef struct {
+    int32_t max_iter;
+    int32_t reorthogonalize;
+    double rel_tol;
+} wc4dvar_pcg_options;
+
+/* CgHistory (krylov.hpp:17-30): caller-provided arrays of length max_iter + 1
+ * (alphas/betas use max_iter); any pointer may be NULL. */
+typedef struct {
+    double* alphas;
+    double* betas;
+    double* residual_norms;
+    double* quadratic_costs; /* filled only when a cost handle is passed */
+    int32_t iterations;
+    int32_t converged;
+    int32_t stop_reason;     /* 0 zero initial residual, 1 tolerance, 2 max iterations */
+    int32_t reserved;
+} wc4dvar_pcg_history;
+
+/* pcg_split (krylov.cpp:22-99): precond may be NULL (identity, krylov.cpp:106-108),
+ * x0 may be NULL (zero guess: no initial apply), cost may be NULL. */
+int wc4dvar_gpu_pcg(wc4dvar_op* op, const double* b, wc4dvar_lmp* precond, const double* x0,
+                    const wc4dvar_pcg_options* opts, wc4dvar_cost* cost, double* x,
+                    wc4dvar_pcg_history* hist);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* WC4DVAR_GPU_H */

@@ -1,0 +1,604 @@
+// C-ABI entry points (include/wc4dvar_gpu.h).
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <memory>
+#include <sstream>
+#include <vector>
+
+#include "lmp_pcg.cuh"
+#include "ops.cuh"
+#include "pcg.cuh"
+#include "sketch.cuh"
+
+namespace w4 {
+void gaussian_fill(int64_t count, uint64_t seed, double* out);
+double probe_dmma_tflops();
+}
+
+using namespace w4;
+
+#define W4_API_BEGIN try {
+#define W4_API_END                         \
+    return WC4DVAR_OK;                     \
+    }                                      \
+    catch (const w4::InvalidArgument& e) { \
+        w4::set_last_error(e.what());      \
+        return WC4DVAR_INVALID_ARGUMENT;   \
+    }                                      \
+    catch (const w4::NumericalError& e) {  \
+        w4::set_last_error(e.what());      \
+        return WC4DVAR_NUMERICAL;          \
+    }                                      \
+    catch (const std::exception& e) {      \
+        w4::set_last_error(e.what());      \
+        return WC4DVAR_DEVICE;             \
+    }
+
+namespace {
+
+thread_local SketchTiming g_sketch_timing;
+
+template <class T>
+T* dev_upload(const T* host, size_t count, cudaStream_t st) {
+    T* d = nullptr;
+    W4_CUDA(cudaMalloc(&d, sizeof(T) * std::max<size_t>(count, 1)));
+    if (count) W4_CUDA(cudaMemcpyAsync(d, host, sizeof(T) * count, cudaMemcpyHostToDevice, st));
+    return d;
+}
+
+// Copy a host col-major (rows x cols, ld) block into a contiguous device buffer.
+void h2d_block(double* dst, const double* src, int64_t rows, int64_t cols, int64_t ld,
+               cudaStream_t st) {
+    if (rows * cols == 0) return;
+    W4_CUDA(cudaMemcpy2DAsync(dst, rows * sizeof(double), src, ld * sizeof(double),
+                              rows * sizeof(double), cols, cudaMemcpyHostToDevice, st));
+}
+void d2h_block(double* dst, int64_t ld, const double* src, int64_t rows, int64_t cols,
+               cudaStream_t st) {
+    if (rows * cols == 0) return;
+    W4_CUDA(cudaMemcpy2DAsync(dst, ld * sizeof(double), src, rows * sizeof(double),
+                              rows * sizeof(double), cols, cudaMemcpyDeviceToHost, st));
+}
+
+bool overlaps(const double* a, int64_t lda, int64_t ma, const double* b, int64_t ldb, int64_t mb,
+              int64_t rows) {
+    if (!a || !b || ma == 0 || mb == 0) return false;
+    const double* ae = a + (ma - 1) * lda + rows;
+    const double* be = b + (mb - 1) * ldb + rows;
+    return a < be && b < ae;
+}
+
+cudaStream_t pick(wc4dvar_op* op, void* s) {
+    return s ? static_cast<cudaStream_t>(s) : op->stream;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* wc4dvar_gpu_last_error(void) { return w4::last_error_cstr(); }
+
+const char* wc4dvar_gpu_version(void) { return "wc4dvar-b200 0.1 (sm_100a, fp64 DMMA)"; }
+
+int wc4dvar_gpu_hessian_create(const wc4dvar_model_desc* model, const wc4dvar_network_desc* net,
+                               const wc4dvar_cov_desc* bh, const wc4dvar_cov_desc* qh,
+                               double sigma_obs, int device, wc4dvar_op** out) {
+    W4_API_BEGIN
+    require(model && net && bh && qh && out, "HessianOperator: null descriptor");
+    *out = nullptr;
+    // HessianOperator ctor checks (operators.cpp:64-77)
+    require(sigma_obs > 0.0, "HessianOperator: sigma_obs must be positive");
+    require(model->n >= 1 && model->N >= 0, "HessianOperator: bad window");
+    require(model->substeps >= 1, "HessianOperator: substeps must be >= 1");
+    require(bh->half != nullptr, "HessianOperator: background factor mismatch");
+    require(qh->half != nullptr, "HessianOperator: model-error factor mismatch");
+    require(bh->kind == qh->kind, "HessianOperator: factors must share a representation");
+    require(net->n == model->n && net->N == model->N, "HessianOperator: network/window mismatch");
+    require(model->kind >= WC4DVAR_MODEL_IDENTITY && model->kind <= WC4DVAR_MODEL_LORENZ96,
+            "HessianOperator: unknown model kind");
+    require(model->kind != WC4DVAR_MODEL_LORENZ96,
+            "HessianOperator: Lorenz-96 device sweeps are not built yet");
+    require(bh->kind == WC4DVAR_COV_DENSE,
+            "HessianOperator: circulant covariance factors are not built yet");
+    const int64_t n = model->n;
+    const int N = model->N;
+    for (int a = 0; a < net->n_times; ++a) {
+        require(net->times[a] >= 0 && net->times[a] <= N, "ObservationNetwork: time out of window");
+        if (a) require(net->times[a] > net->times[a - 1], "ObservationNetwork: times must ascend");
+    }
+    for (int b = 0; b < net->n_points; ++b) {
+        require(net->points[b] >= 0 && net->points[b] < n, "ObservationNetwork: point outside grid");
+        if (b) require(net->points[b] > net->points[b - 1], "ObservationNetwork: points must ascend");
+    }
+    DeviceGuard g(device);
+    std::unique_ptr<HessianOp> h(new HessianOp());
+    h->init_common(device, n * (N + 1));
+    cudaStream_t st = h->stream;
+    h->n = n;
+    h->N = N;
+    h->sigma_obs = sigma_obs;
+    h->cov_kind = bh->kind;
+    h->md.kind = model->kind;
+    h->md.n = n;
+    h->md.N = N;
+    h->md.s = model->substeps;
+    h->md.c = model->courant;
+    h->md.d = model->diffusion;
+    h->md.dt = model->dt;
+    h->times.assign(net->times, net->times + net->n_times);
+    h->points.assign(net->points, net->points + net->n_points);
+    std::vector<int> slot(N + 1, -1), pmap(n, -1);
+    for (int a = 0; a < net->n_times; ++a) slot[net->times[a]] = a;
+    for (int b = 0; b < net->n_points; ++b) pmap[net->points[b]] = b;
+    h->d_slot = dev_upload(slot.data(), slot.size(), st);
+    h->d_pmap = dev_upload(pmap.data(), pmap.size(), st);
+    h->nd.n_times = net->n_times;
+    h->nd.n_points = net->n_points;
+    h->nd.q = (int64_t)net->n_times * net->n_points;
+    h->nd.slot = h->d_slot;
+    h->nd.pmap = h->d_pmap;
+    const size_t fsz = (size_t)n * n;
+    h->b_half = dev_upload(bh->half, fsz, st);
+    h->q_half = dev_upload(qh->half, fsz, st);
+    if (bh->half_inv) h->b_half_inv = dev_upload(bh->half_inv, fsz, st);
+    if (qh->half_inv) h->q_half_inv = dev_upload(qh->half_inv, fsz, st);
+    W4_CUDA(cudaStreamSynchronize(st));
+    *out = h.release();
+    W4_API_END
+}
+
+int wc4dvar_gpu_dense_create(int64_t n, const double* A, int64_t lda, int device,
+                             wc4dvar_op** out) {
+    W4_API_BEGIN
+    require(out && A && n >= 0 && lda >= n, "DenseOperator: bad arguments");
+    *out = nullptr;
+    DeviceGuard g(device);
+    std::unique_ptr<DenseOp> d(new DenseOp());
+    d->init_common(device, n);
+    W4_CUDA(cudaMalloc(&d->A, sizeof(double) * std::max<int64_t>(n * n, 1)));
+    h2d_block(d->A, A, n, n, lda, d->stream);
+    W4_CUDA(cudaStreamSynchronize(d->stream));
+    *out = d.release();
+    W4_API_END
+}
+
+int wc4dvar_gpu_op_destroy(wc4dvar_op* op) {
+    W4_API_BEGIN
+    delete op;
+    W4_API_END
+}
+
+int64_t wc4dvar_gpu_op_dim(const wc4dvar_op* op) { return op ? op->dim : -1; }
+int64_t wc4dvar_gpu_op_apply_count(const wc4dvar_op* op) { return op ? op->applies.load() : -1; }
+void wc4dvar_gpu_op_reset_apply_count(wc4dvar_op* op) {
+    if (op) op->applies.store(0);
+}
+int wc4dvar_gpu_op_device(const wc4dvar_op* op) { return op ? op->device : -1; }
+
+int wc4dvar_gpu_op_apply_block(wc4dvar_op* op, const double* V, int64_t ldv, int64_t m,
+                               double* out, int64_t ldo) {
+    W4_API_BEGIN
+    require(op != nullptr, "apply_block: null operator");
+    require(m >= 0 && ldv >= op->dim && ldo >= op->dim,
+            "LinearOperator::apply_block: dimension mismatch");
+    std::lock_guard<std::recursive_mutex> lk(op->mu);
+    DeviceGuard g(op->device);
+    op->applies += m;
+    if (m == 0 || op->dim == 0) return WC4DVAR_OK;
+    cudaStream_t st = op->stream;
+    double* din = op->in_buf.get<double>((size_t)op->dim * m);
+    double* dout = op->out_buf.get<double>((size_t)op->dim * m);
+    h2d_block(din, V, op->dim, m, ldv, st);
+    op->reset_status(st);
+    op->apply_block_dev(din, op->dim, m, dout, op->dim, st);
+    d2h_block(out, ldo, dout, op->dim, m, st);
+    op->check_status(st);
+    W4_API_END
+}
+
+int wc4dvar_gpu_op_apply(wc4dvar_op* op, const double* in, double* out) {
+    return wc4dvar_gpu_op_apply_block(op, in, op ? op->dim : 0, 1, out, op ? op->dim : 0);
+}
+
+int wc4dvar_gpu_op_apply_block_dev(wc4dvar_op* op, const double* V, int64_t ldv, int64_t m,
+                                   double* out, int64_t ldo, void* stream) {
+    W4_API_BEGIN
+    require(op != nullptr, "apply_block: null operator");
+    require(m >= 0 && ldv >= op->dim && ldo >= op->dim,
+            "LinearOperator::apply_block: dimension mismatch");
+    std::lock_guard<std::recursive_mutex> lk(op->mu);
+    DeviceGuard g(op->device);
+    op->applies += m;
+    if (m == 0 || op->dim == 0) return WC4DVAR_OK;
+    cudaStream_t st = pick(op, stream);
+    const double* src = V;
+    int64_t lds = ldv;
+    if (overlaps(V, ldv, m, out, ldo, m, op->dim)) {
+        double* tmp = op->in_buf.get<double>((size_t)op->dim * m);
+        W4_CUDA(cudaMemcpy2DAsync(tmp, op->dim * 8, V, ldv * 8, op->dim * 8, m,
+                                  cudaMemcpyDeviceToDevice, st));
+        src = tmp;
+        lds = op->dim;
+    }
+    op->reset_status(st);
+    op->apply_block_dev(src, lds, m, out, ldo, st);
+    op->check_status(st);
+    W4_API_END
+}
+
+int wc4dvar_gpu_hessian_piece_dev(wc4dvar_op* op, int which, const double* V, int64_t ldv,
+                                  int64_t m, double* out, int64_t ldo, void* stream) {
+    W4_API_BEGIN
+    HessianOp* h = dynamic_cast<HessianOp*>(op);
+    require(h != nullptr, "hessian piece: operator is not a HessianOperator");
+    static const char* names[] = {"apply_Linv", "apply_LinvT", "apply_D_half", "apply_D_half_inv"};
+    require(which >= 0 && which <= 3, "hessian piece: unknown selector");
+    require(m >= 0 && ldv >= op->dim && ldo >= op->dim,
+            std::string(names[which]) + ": window length mismatch");
+    std::lock_guard<std::recursive_mutex> lk(op->mu);
+    DeviceGuard g(op->device);
+    if (m == 0) return WC4DVAR_OK;
+    cudaStream_t st = pick(op, stream);
+    const double* src = V;
+    int64_t lds = ldv;
+    if (overlaps(V, ldv, m, out, ldo, m, op->dim)) {
+        double* tmp = op->in_buf.get<double>((size_t)op->dim * m);
+        W4_CUDA(cudaMemcpy2DAsync(tmp, op->dim * 8, V, ldv * 8, op->dim * 8, m,
+                                  cudaMemcpyDeviceToDevice, st));
+        src = tmp;
+        lds = op->dim;
+    }
+    op->reset_status(st);
+    h->piece_dev(which, src, lds, m, out, ldo, st);
+    W4_CUDA(cudaStreamSynchronize(st));
+    W4_API_END
+}
+
+int wc4dvar_gpu_hessian_piece(wc4dvar_op* op, int which, const double* V, int64_t ldv, int64_t m,
+                              double* out, int64_t ldo) {
+    W4_API_BEGIN
+    require(op != nullptr, "hessian piece: null operator");
+    require(m >= 0 && ldv >= op->dim && ldo >= op->dim, "hessian piece: window length mismatch");
+    std::lock_guard<std::recursive_mutex> lk(op->mu);
+    DeviceGuard g(op->device);
+    if (m == 0) return WC4DVAR_OK;
+    double* din = op->in_buf.get<double>((size_t)op->dim * m);
+    double* dout = op->out_buf.get<double>((size_t)op->dim * m);
+    h2d_block(din, V, op->dim, m, ldv, op->stream);
+    const int rc = wc4dvar_gpu_hessian_piece_dev(op, which, din, op->dim, m, dout, op->dim, nullptr);
+    if (rc != WC4DVAR_OK) return rc;
+    d2h_block(out, ldo, dout, op->dim, m, op->stream);
+    W4_CUDA(cudaStreamSynchronize(op->stream));
+    W4_API_END
+}
+
+int wc4dvar_gpu_op_profile(wc4dvar_op* op, int enable) {
+    W4_API_BEGIN
+    require(op != nullptr, "op_profile: null operator");
+    std::lock_guard<std::recursive_mutex> lk(op->mu);
+    DeviceGuard g(op->device);
+    if (enable && !op->pev[0])
+        for (auto& e : op->pev) W4_CUDA(cudaEventCreate(&e));
+    op->prof = enable != 0;
+    op->prof_pending = false;
+    op->prof_ms[0] = op->prof_ms[1] = op->prof_ms[2] = 0;
+    op->prof_calls = 0;
+    W4_API_END
+}
+
+int wc4dvar_gpu_op_profile_read(wc4dvar_op* op, double* ms3, int64_t* calls) {
+    W4_API_BEGIN
+    require(op && ms3 && calls, "op_profile_read: null argument");
+    std::lock_guard<std::recursive_mutex> lk(op->mu);
+    for (int i = 0; i < 3; ++i) ms3[i] = op->prof_ms[i];
+    *calls = op->prof_calls;
+    W4_API_END
+}
+
+int wc4dvar_gpu_probe_dmma_peak(int device, double* tflops) {
+    W4_API_BEGIN
+    require(tflops != nullptr, "probe_dmma_peak: null");
+    DeviceGuard g(device);
+    *tflops = w4::probe_dmma_tflops();
+    W4_API_END
+}
+
+int wc4dvar_gpu_gaussian_matrix(int64_t rows, int64_t cols, uint64_t seed, double* out) {
+    W4_API_BEGIN
+    require(rows >= 0 && cols >= 0 && (out || rows * cols == 0), "gaussian_matrix: bad arguments");
+    w4::gaussian_fill(rows * cols, seed, out);
+    W4_API_END
+}
+
+int wc4dvar_gpu_sketch_dev(wc4dvar_op* op, const wc4dvar_sketch_config* cfg,
+                           const double* omega_dev, double* U_dev, int64_t ldu, double* theta_dev,
+                           int64_t* k_out, void* stream) {
+    W4_API_BEGIN
+    require(op && cfg && omega_dev && U_dev && theta_dev && k_out, "sketch: null argument");
+    require(ldu >= op->dim, "sketch: ldu < dim");
+    std::lock_guard<std::recursive_mutex> lk(op->mu);
+    DeviceGuard g(op->device);
+    g_sketch_timing = SketchTiming{};
+    *k_out = sketch_dev(*op, *cfg, omega_dev, U_dev, ldu, theta_dev, pick(op, stream),
+                        &g_sketch_timing);
+    W4_API_END
+}
+
+int wc4dvar_gpu_sketch(wc4dvar_op* op, const wc4dvar_sketch_config* cfg, const double* omega,
+                       double* U, int64_t ldu, double* theta, int64_t* k_out) {
+    W4_API_BEGIN
+    require(op && cfg && U && theta && k_out, "sketch: null argument");
+    require(ldu >= op->dim, "sketch: ldu < dim");
+    // SketchConfig::validate before drawing (randevd.cpp:63)
+    require(cfg->target_rank >= 1, "SketchConfig: target rank must be >= 1");
+    require(cfg->oversample >= 0, "SketchConfig: oversampling must be >= 0");
+    const int64_t m = (int64_t)cfg->target_rank + cfg->oversample;
+    require(m <= op->dim, "SketchConfig: k + l exceeds operator dimension");
+    std::lock_guard<std::recursive_mutex> lk(op->mu);
+    DeviceGuard g(op->device);
+    const int64_t n = op->dim;
+    cudaStream_t st = op->stream;
+    std::vector<double> hom;
+    if (!omega) {
+        hom.resize(n * m);
+        w4::gaussian_fill(n * m, cfg->seed, hom.data());
+        omega = hom.data();
+    }
+    double* dom = op->in_buf.get<double>((size_t)n * m);
+    double* dU = op->out_buf.get<double>((size_t)n * cfg->target_rank + cfg->target_rank);
+    double* dth = dU + (size_t)n * cfg->target_rank;
+    h2d_block(dom, omega, n, m, n, st);
+    g_sketch_timing = SketchTiming{};
+    const int64_t kk = sketch_dev(*op, *cfg, dom, dU, n, dth, st, &g_sketch_timing);
+    d2h_block(U, ldu, dU, n, kk, st);
+    W4_CUDA(cudaMemcpyAsync(theta, dth, sizeof(double) * kk, cudaMemcpyDeviceToHost, st));
+    W4_CUDA(cudaStreamSynchronize(st));
+    *k_out = kk;
+    W4_API_END
+}
+
+int wc4dvar_gpu_rayleigh_ritz(wc4dvar_op* op, const double* Z, int64_t ldz, int64_t m, double* U,
+                              int64_t ldu, double* theta) {
+    W4_API_BEGIN
+    require(op && Z && U && theta, "rayleigh_ritz: null argument");
+    require(ldz >= op->dim && ldu >= op->dim, "rayleigh_ritz: dimension mismatch");
+    require(m >= 1 && m <= 512, "rayleigh_ritz: 1 <= m <= 512");
+    std::lock_guard<std::recursive_mutex> lk(op->mu);
+    DeviceGuard g(op->device);
+    const int64_t n = op->dim;
+    cudaStream_t st = op->stream;
+    double* dz = op->in_buf.get<double>((size_t)n * m);
+    double* dU = op->out_buf.get<double>((size_t)n * m + m);
+    double* dth = dU + (size_t)n * m;
+    h2d_block(dz, Z, n, m, ldz, st);
+    rayleigh_ritz_dev(*op, dz, n, m, dU, n, dth, st);
+    d2h_block(U, ldu, dU, n, m, st);
+    W4_CUDA(cudaMemcpyAsync(theta, dth, sizeof(double) * m, cudaMemcpyDeviceToHost, st));
+    W4_CUDA(cudaStreamSynchronize(st));
+    W4_API_END
+}
+
+int wc4dvar_gpu_last_sketch_timing(double* ms5) {
+    W4_API_BEGIN
+    require(ms5 != nullptr, "last_sketch_timing: null");
+    ms5[0] = g_sketch_timing.apply_ms;
+    ms5[1] = g_sketch_timing.orth_ms;
+    ms5[2] = g_sketch_timing.small_ms;
+    ms5[3] = g_sketch_timing.gemm_ms;
+    ms5[4] = g_sketch_timing.total_ms;
+    W4_API_END
+}
+
+// ----------------------------------------------------------------------------- LMP
+static int lmp_build_impl(int64_t n, int64_t k, const double* U, int64_t ldu, const double* theta,
+                          int device, bool dev_ptrs, wc4dvar_lmp** out) {
+    W4_API_BEGIN
+    require(out != nullptr && n >= 0 && k >= 0, "build_spectral_lmp: bad arguments");
+    *out = nullptr;
+    DeviceGuard g(device);
+    std::unique_ptr<wc4dvar_lmp> f(new wc4dvar_lmp());
+    f->device = device;
+    f->n = n;
+    f->k = (int)k;
+    W4_CUDA(cudaStreamCreateWithFlags(&f->stream, cudaStreamNonBlocking));
+    W4_CUDA(cudaMalloc(&f->counter, 4 * sizeof(unsigned)));
+    W4_CUDA(cudaMemset(f->counter, 0, 4 * sizeof(unsigned)));
+    if (k == 0) {  // LmpFactor::identity (lmp.cpp:28-33, :36)
+        *out = f.release();
+        return WC4DVAR_OK;
+    }
+    require(ldu >= n && U && theta, "build_spectral_lmp: bad arguments");
+    cudaStream_t st = f->stream;
+    std::vector<double> th(k);
+    if (dev_ptrs)
+        W4_CUDA(cudaMemcpy(th.data(), theta, sizeof(double) * k, cudaMemcpyDeviceToHost));
+    else
+        std::memcpy(th.data(), theta, sizeof(double) * k);
+    const double mn = *std::min_element(th.begin(), th.end());
+    if (!(mn > 0.0)) {  // lmp.cpp:37-41
+        std::ostringstream m;
+        m << "build_spectral_lmp: nonpositive Ritz value " << mn;
+        throw NumericalError(m.str());
+    }
+    W4_CUDA(cudaMalloc(&f->U, sizeof(double) * n * k));
+    W4_CUDA(cudaMalloc(&f->theta, sizeof(double) * k));
+    W4_CUDA(cudaMalloc(&f->T, sizeof(double) * k * k));
+    W4_CUDA(cudaMemcpy2DAsync(f->U, n * 8, U, ldu * 8, n * 8, k,
+                              dev_ptrs ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, st));
+    W4_CUDA(cudaMemcpyAsync(f->theta, th.data(), sizeof(double) * k, cudaMemcpyHostToDevice, st));
+    double* S = f->tmp.get<double>((size_t)k * k + 1);
+    gemm_tn(n, k, k, f->U, n, f->U, n, 1.0, S, k, f->partial, st);
+    double* dd = S + k * k;
+    defect_max((int)k, S, dd, st);
+    double defect = 0;
+    W4_CUDA(cudaMemcpyAsync(&defect, dd, sizeof(double), cudaMemcpyDeviceToHost, st));
+    W4_CUDA(cudaStreamSynchronize(st));
+    if (!(defect <= 1e-8)) {  // lmp.cpp:42-47
+        std::ostringstream m;
+        m << "build_spectral_lmp: Ritz vectors not orthonormal (defect " << defect << ")";
+        throw NumericalError(m.str());
+    }
+    lmp_build_T((int)k, S, f->theta, f->T, st);
+    W4_CUDA(cudaStreamSynchronize(st));
+    *out = f.release();
+    W4_API_END
+}
+
+int wc4dvar_gpu_lmp_build(int64_t n, int64_t k, const double* U, int64_t ldu, const double* theta,
+                          int device, wc4dvar_lmp** out) {
+    return lmp_build_impl(n, k, U, ldu, theta, device, false, out);
+}
+
+int wc4dvar_gpu_lmp_build_dev(int64_t n, int64_t k, const double* U, int64_t ldu,
+                              const double* theta, int device, wc4dvar_lmp** out) {
+    return lmp_build_impl(n, k, U, ldu, theta, device, true, out);
+}
+
+int wc4dvar_gpu_lmp_destroy(wc4dvar_lmp* f) {
+    W4_API_BEGIN
+    delete f;
+    W4_API_END
+}
+
+int wc4dvar_gpu_lmp_apply(wc4dvar_lmp* f, int transpose, const double* v, double* out) {
+    W4_API_BEGIN
+    require(f && v && out, "LmpFactor::apply: null argument");
+    std::lock_guard<std::mutex> lk(f->mu);
+    DeviceGuard g(f->device);
+    const int64_t n = f->n;
+    cudaStream_t st = f->stream;
+    if (f->k == 0) {
+        std::memmove(out, v, sizeof(double) * n);
+        return WC4DVAR_OK;
+    }
+    double* buf = f->tmp.get<double>((size_t)2 * n + f->k + 1);
+    double* dv = buf;
+    double* dout = buf + n;
+    double* gk = buf + 2 * n;
+    W4_CUDA(cudaMemcpyAsync(dv, v, sizeof(double) * n, cudaMemcpyHostToDevice, st));
+    RowPassCtx c;
+    c.n = n;
+    c.k = f->k;
+    c.U = f->U;
+    c.ldu = n;
+    c.T = f->T;
+    c.partial = f->partial.get<double>((size_t)(cdiv(n, 32) + 1) * (f->k + 1));
+    c.counter = f->counter;
+    rowpass_utv(c, dv, nullptr, nullptr, gk, st);
+    rowpass_apply(c, transpose != 0, dv, gk, dout, st);
+    W4_CUDA(cudaMemcpyAsync(out, dout, sizeof(double) * n, cudaMemcpyDeviceToHost, st));
+    W4_CUDA(cudaStreamSynchronize(st));
+    W4_API_END
+}
+
+// ----------------------------------------------------------------------------- cost
+int wc4dvar_gpu_cost_create(wc4dvar_op* op, const double* b, const double* d, wc4dvar_cost** out) {
+    W4_API_BEGIN
+    HessianOp* h = dynamic_cast<HessianOp*>(op);
+    require(h && b && out, "QuadraticCost: bad arguments");
+    *out = nullptr;
+    std::lock_guard<std::recursive_mutex> lk(op->mu);
+    DeviceGuard g(op->device);
+    std::unique_ptr<wc4dvar_cost> c(new wc4dvar_cost());
+    c->op = h;
+    const int64_t n = op->dim, q = h->nd.q;
+    cudaStream_t st = op->stream;
+    double* db = op->in_buf.get<double>((size_t)n);
+    W4_CUDA(cudaMemcpyAsync(db, b, sizeof(double) * n, cudaMemcpyHostToDevice, st));
+    W4_CUDA(cudaMalloc(&c->b_tilde, sizeof(double) * n));
+    h->piece_dev(WC4DVAR_D_HALF_INV, db, n, 1, c->b_tilde, n, st);  // assimilation.cpp:131
+    c->d = dev_upload(d ? d : b, d ? (size_t)q : 0, st);
+    W4_CUDA(cudaMalloc(&c->counter, 4 * sizeof(unsigned)));
+    W4_CUDA(cudaMemsetAsync(c->counter, 0, 4 * sizeof(unsigned), st));
+    W4_CUDA(cudaMalloc(&c->d_val, 2 * sizeof(double)));
+    W4_CUDA(cudaStreamSynchronize(st));
+    *out = c.release();
+    W4_API_END
+}
+
+int wc4dvar_gpu_cost_destroy(wc4dvar_cost* c) {
+    W4_API_BEGIN
+    delete c;
+    W4_API_END
+}
+
+int wc4dvar_gpu_cost_eval(wc4dvar_cost* c, const double* x, double* value) {
+    W4_API_BEGIN
+    require(c && x && value, "QuadraticCost: null argument");
+    wc4dvar_op* op = c->op;
+    std::lock_guard<std::recursive_mutex> lk(op->mu);
+    DeviceGuard g(op->device);
+    double* dx = op->in_buf.get<double>((size_t)op->dim);
+    W4_CUDA(cudaMemcpyAsync(dx, x, sizeof(double) * op->dim, cudaMemcpyHostToDevice, op->stream));
+    *value = c->eval_dev(dx, op->stream);
+    W4_API_END
+}
+
+int wc4dvar_gpu_cost_rhs(wc4dvar_cost* c, double* rhs) {
+    W4_API_BEGIN
+    require(c && rhs, "QuadraticCost: null argument");
+    HessianOp* h = c->op;
+    std::lock_guard<std::recursive_mutex> lk(h->mu);
+    DeviceGuard g(h->device);
+    const int64_t n = h->dim;
+    cudaStream_t st = h->stream;
+    double* s = h->in_buf.get<double>((size_t)2 * n);
+    double* u = s + n;
+    // rhs = b~ + r_inv D^{1/2} L^{-T} H^T d  (assimilation.cpp:142-146)
+    SweepArgs a;
+    a.Y = c->d;
+    a.S = s;
+    a.lds = n;
+    a.do_adj = true;
+    a.adj_obs = h->nd.q > 0;
+    a.m = 1;
+    h->reset_status(st);
+    sweep(h->md, h->nd, a, h->d_status, st);
+    h->piece_dev(WC4DVAR_D_HALF, s, n, 1, u, n, st);
+    const double r_inv = 1.0 / (h->sigma_obs * h->sigma_obs);
+    axpby(n, 1.0, c->b_tilde, r_inv, u, u, st);
+    W4_CUDA(cudaMemcpyAsync(rhs, u, sizeof(double) * n, cudaMemcpyDeviceToHost, st));
+    W4_CUDA(cudaStreamSynchronize(st));
+    W4_API_END
+}
+
+// ----------------------------------------------------------------------------- PCG
+int wc4dvar_gpu_pcg(wc4dvar_op* op, const double* b, wc4dvar_lmp* pre, const double* x0,
+                    const wc4dvar_pcg_options* opts, wc4dvar_cost* cost, double* x,
+                    wc4dvar_pcg_history* hist) {
+    W4_API_BEGIN
+    require(op && b && opts && x, "pcg_split: null argument");
+    require(!pre || pre->k == 0 || pre->n == op->dim, "pcg_split: preconditioner dimension mismatch");
+    require(!cost || cost->op == op, "pcg_split: cost belongs to another operator");
+    std::lock_guard<std::recursive_mutex> lk(op->mu);
+    DeviceGuard g(op->device);
+    const int64_t n = op->dim;
+    cudaStream_t st = op->stream;
+    double* buf = op->out_buf.get<double>((size_t)3 * n);
+    double* db = buf;
+    double* dx0 = x0 ? buf + n : nullptr;
+    double* dx = buf + 2 * n;
+    W4_CUDA(cudaMemcpyAsync(db, b, sizeof(double) * n, cudaMemcpyHostToDevice, st));
+    if (x0) W4_CUDA(cudaMemcpyAsync(dx0, x0, sizeof(double) * n, cudaMemcpyHostToDevice, st));
+    PcgRecord rec;
+    pcg_dev(*op, db, pre, dx0, *opts, cost, dx, rec, st);
+    W4_CUDA(cudaMemcpyAsync(x, dx, sizeof(double) * n, cudaMemcpyDeviceToHost, st));
+    W4_CUDA(cudaStreamSynchronize(st));
+    if (hist) {
+        for (size_t i = 0; i < rec.alphas.size(); ++i) {
+            if (hist->alphas) hist->alphas[i] = rec.alphas[i];
+            if (hist->betas) hist->betas[i] = rec.betas[i];
+        }
+        for (size_t i = 0; i < rec.residual_norms.size(); ++i)
+            if (hist->residual_norms) hist->residual_norms[i] = rec.residual_norms[i];
+        for (size_t i = 0; i < rec.costs.size(); ++i)
+            if (hist->quadratic_costs) hist->quadratic_costs[i] = rec.costs[i];
+        hist->iterations = rec.iterations;
+        hist->converged = rec.converged ? 1 : 0;
+        hist->stop_reason = rec.stop_reason;
+    }
+    W4_API_END
+}
+
+}  // extern "C"

@@ -1,0 +1,443 @@
+// fp64 DMMA GEMM kernels (see gemm.cuh).
+#include "gemm.cuh"
+
+#include <map>
+#include <mutex>
+
+namespace w4 {
+namespace {
+
+constexpr int BK = 16;
+constexpr int KPAD = BK + 4;  // [col][k] tiles: stride 20 doubles -> conflict-free fragments
+
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem, int src_bytes) {
+    unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(s), "l"(gmem),
+                 "r"(src_bytes));
+}
+__device__ __forceinline__ void cp_async8(void* smem, const void* gmem, int src_bytes) {
+    unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(s), "l"(gmem),
+                 "r"(src_bytes));
+}
+__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;\n"); }
+template <int N>
+__device__ __forceinline__ void cp_wait() {
+    asm volatile("cp.async.wait_group %0;\n" ::"n"(N));
+}
+
+__device__ __forceinline__ void dmma16x8x8(double (&d)[4], const double (&a)[4],
+                                           const double (&b)[2]) {
+    asm volatile(
+        "mma.sync.aligned.m16n8k8.row.col.f64.f64.f64.f64 "
+        "{%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, {%0,%1,%2,%3};\n"
+        : "+d"(d[0]), "+d"(d[1]), "+d"(d[2]), "+d"(d[3])
+        : "d"(a[0]), "d"(a[1]), "d"(a[2]), "d"(a[3]), "d"(b[0]), "d"(b[1]));
+}
+
+template <int VEC>
+__device__ __forceinline__ void cp_async_vec(void* smem, const double* gmem, int valid,
+                                             const double* safe) {
+    const double* src = valid > 0 ? gmem : safe;
+    if (VEC == 2)
+        cp_async16(smem, src, valid * 8);
+    else
+        cp_async8(smem, src, valid * 8);
+}
+
+// cudaFuncSetAttribute is per device: remember which devices are configured.
+void configure_smem(const void* kern, size_t smem) {
+    static std::mutex mu;
+    static std::map<std::pair<const void*, int>, bool> done;
+    int dev = 0;
+    W4_CUDA(cudaGetDevice(&dev));
+    std::lock_guard<std::mutex> lk(mu);
+    auto key = std::make_pair(kern, dev);
+    if (done.count(key)) return;
+    W4_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    done[key] = true;
+}
+
+struct PassTable {
+    GemmPass p[2];
+    int64_t tiles_m[2];
+    int64_t tile_start[3];
+};
+
+// ---------------------------------------------------------------------------
+// NN kernel: A tile stored [k][m] (stride BM+4), B tile stored [n][k] (stride BK+4).
+// ---------------------------------------------------------------------------
+template <int BM, int BN, int WM, int WN, int STAGES, int VEC>
+__global__ void __launch_bounds__(WM * WN * 32)
+    gemm_nn_kernel(const PassTable tab, unsigned* __restrict__ status) {
+    constexpr int NT = WM * WN * 32;
+    constexpr int WTM = BM / WM, WTN = BN / WN;
+    constexpr int MI = WTM / 16, NI = WTN / 8;
+    constexpr int APAD = BM + 4;
+    constexpr int A_ELEMS = BK * APAD, B_ELEMS = BN * KPAD;
+    extern __shared__ __align__(16) double smem[];
+    double* As = smem;
+    double* Bs = smem + STAGES * A_ELEMS;
+
+    int64_t tile = blockIdx.x;
+    const int pi = tile >= tab.tile_start[1] ? 1 : 0;
+    const GemmPass& P = tab.p[pi];
+    tile -= tab.tile_start[pi];
+    const int64_t tm = tile % tab.tiles_m[pi];
+    const int64_t tn = tile / tab.tiles_m[pi];
+    const int64_t m0 = tm * BM, n0 = tn * BN;
+    const int64_t M = P.M, K = P.K, ncols = P.ncols;
+
+    const int tid = threadIdx.x;
+    const int warp = tid >> 5, lane = tid & 31;
+    const int wm = warp % WM, wn = warp / WM;
+    const int g = lane >> 2, t0 = lane & 3;
+
+    double acc[MI][NI][4];
+#pragma unroll
+    for (int i = 0; i < MI; ++i)
+#pragma unroll
+        for (int j = 0; j < NI; ++j)
+#pragma unroll
+            for (int v = 0; v < 4; ++v) acc[i][j][v] = 0.0;
+
+    const int64_t ktiles = (K + BK - 1) / BK;
+
+    auto load_stage = [&](int stage, int64_t kt) {
+        const int64_t k0 = kt * BK;
+        double* as = As + stage * A_ELEMS;
+        double* bs = Bs + stage * B_ELEMS;
+        constexpr int ACH = BK * BM / VEC;
+#pragma unroll
+        for (int ch = tid; ch < ACH; ch += NT) {
+            const int kk = ch / (BM / VEC);
+            const int rr = (ch % (BM / VEC)) * VEC;
+            const int64_t row = m0 + rr, kcol = k0 + kk;
+            int valid = 0;
+            if (kcol < K) {
+                const int64_t rem = M - row;
+                valid = rem >= VEC ? VEC : (rem > 0 ? (int)rem : 0);
+            }
+            cp_async_vec<VEC>(as + kk * APAD + rr, P.A + kcol * P.lda + row, valid, P.A);
+        }
+        constexpr int BCH = BN * BK / VEC;
+#pragma unroll
+        for (int ch = tid; ch < BCH; ch += NT) {
+            const int nn = ch / (BK / VEC);
+            const int kk = (ch % (BK / VEC)) * VEC;
+            const int64_t c = n0 + nn, kr = k0 + kk;
+            int valid = 0;
+            const double* src = P.A;
+            if (c < ncols) {
+                const int64_t rem = K - kr;
+                valid = rem >= VEC ? VEC : (rem > 0 ? (int)rem : 0);
+                src = P.in.col(c) + kr;
+            }
+            cp_async_vec<VEC>(bs + nn * KPAD + kk, src, valid, P.A);
+        }
+    };
+
+#pragma unroll
+    for (int s = 0; s < STAGES - 1; ++s) {
+        if (s < ktiles) load_stage(s, s);
+        cp_commit();
+    }
+
+    for (int64_t kt = 0; kt < ktiles; ++kt) {
+        cp_wait<STAGES - 2>();
+        __syncthreads();
+        {
+            const int64_t nk = kt + STAGES - 1;
+            if (nk < ktiles) load_stage((int)(nk % STAGES), nk);
+            cp_commit();
+        }
+        const double* as = As + (kt % STAGES) * A_ELEMS;
+        const double* bs = Bs + (kt % STAGES) * B_ELEMS;
+#pragma unroll
+        for (int k8 = 0; k8 < BK; k8 += 8) {
+            double af[MI][4], bf[NI][2];
+#pragma unroll
+            for (int i = 0; i < MI; ++i) {
+                const int r = wm * WTM + i * 16 + g;
+                af[i][0] = as[(k8 + t0) * APAD + r];
+                af[i][1] = as[(k8 + t0) * APAD + r + 8];
+                af[i][2] = as[(k8 + t0 + 4) * APAD + r];
+                af[i][3] = as[(k8 + t0 + 4) * APAD + r + 8];
+            }
+#pragma unroll
+            for (int j = 0; j < NI; ++j) {
+                const int c = wn * WTN + j * 8 + g;
+                bf[j][0] = bs[c * KPAD + k8 + t0];
+                bf[j][1] = bs[c * KPAD + k8 + t0 + 4];
+            }
+#pragma unroll
+            for (int i = 0; i < MI; ++i)
+#pragma unroll
+                for (int j = 0; j < NI; ++j) dmma16x8x8(acc[i][j], af[i], bf[j]);
+        }
+    }
+    cp_wait<0>();
+
+    bool bad = false;
+    const double alpha = P.alpha;
+#pragma unroll
+    for (int j = 0; j < NI; ++j) {
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            const int64_t c = n0 + wn * WTN + j * 8 + 2 * t0 + h;
+            if (c >= ncols) continue;
+            double* outc = const_cast<double*>(P.out.col(c));
+            const double* addc = P.add.base ? P.add.col(c) : nullptr;
+#pragma unroll
+            for (int i = 0; i < MI; ++i) {
+#pragma unroll
+                for (int v = 0; v < 2; ++v) {
+                    const int64_t r = m0 + wm * WTM + i * 16 + g + 8 * v;
+                    if (r >= M) continue;
+                    double val = alpha * acc[i][j][2 * v + h];
+                    if (addc) val = addc[r] + val;
+                    bad |= !isfinite(val);
+                    outc[r] = val;
+                }
+            }
+        }
+    }
+    if (status && __any_sync(0xffffffffu, bad) && lane == 0) atomicOr(status, ST_OUT_NONFINITE);
+}
+
+template <int BM, int BN, int WM, int WN, int STAGES, int VEC>
+void launch_nn(const PassTable& tab, int64_t ntiles, unsigned* status, cudaStream_t stream) {
+    constexpr int APAD = BM + 4;
+    const size_t smem = sizeof(double) * STAGES * (BK * APAD + BN * KPAD);
+    auto kern = gemm_nn_kernel<BM, BN, WM, WN, STAGES, VEC>;
+    configure_smem(reinterpret_cast<const void*>(kern), smem);
+    kern<<<(unsigned)ntiles, WM * WN * 32, smem, stream>>>(tab, status);
+    W4_LAUNCH();
+}
+
+bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
+
+// ---------------------------------------------------------------------------
+// TN split kernel: both tiles stored [col][k] (stride KPAD).
+// Partial (split s) of C tile -> work[s][m2][m1] col-major m1 x m2.
+// ---------------------------------------------------------------------------
+template <int BM, int BN, int WM, int WN, int STAGES, int VEC>
+__global__ void __launch_bounds__(WM * WN * 32)
+    gemm_tn_kernel(int64_t R, int64_t m1, int64_t m2, const double* __restrict__ A, int64_t lda,
+                   const double* __restrict__ B, int64_t ldb, int64_t rows_per_split,
+                   int64_t tiles_m, int64_t tiles_n, double* __restrict__ work) {
+    constexpr int NT = WM * WN * 32;
+    constexpr int WTM = BM / WM, WTN = BN / WN;
+    constexpr int MI = WTM / 16, NI = WTN / 8;
+    constexpr int A_ELEMS = BM * KPAD, B_ELEMS = BN * KPAD;
+    extern __shared__ __align__(16) double smem[];
+    double* As = smem;
+    double* Bs = smem + STAGES * A_ELEMS;
+
+    const int64_t t = blockIdx.x;
+    const int64_t tm = t % tiles_m;
+    const int64_t tn = (t / tiles_m) % tiles_n;
+    const int64_t split = t / (tiles_m * tiles_n);
+    const int64_t i0 = tm * BM, j0 = tn * BN;
+    const int64_t r_begin = split * rows_per_split;
+    const int64_t r_end = min(R, r_begin + rows_per_split);
+
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int wm = warp % WM, wn = warp / WM;
+    const int g = lane >> 2, t0 = lane & 3;
+
+    double acc[MI][NI][4];
+#pragma unroll
+    for (int i = 0; i < MI; ++i)
+#pragma unroll
+        for (int j = 0; j < NI; ++j)
+#pragma unroll
+            for (int v = 0; v < 4; ++v) acc[i][j][v] = 0.0;
+
+    const int64_t ktiles = r_end > r_begin ? (r_end - r_begin + BK - 1) / BK : 0;
+
+    auto load_stage = [&](int stage, int64_t kt) {
+        const int64_t k0 = r_begin + kt * BK;
+        double* as = As + stage * A_ELEMS;
+        double* bs = Bs + stage * B_ELEMS;
+        constexpr int ACH = BM * BK / VEC;
+#pragma unroll
+        for (int ch = tid; ch < ACH; ch += NT) {
+            const int ii = ch / (BK / VEC);
+            const int kk = (ch % (BK / VEC)) * VEC;
+            const int64_t c = i0 + ii, kr = k0 + kk;
+            int valid = 0;
+            const double* src = A;
+            if (c < m1) {
+                const int64_t rem = r_end - kr;
+                valid = rem >= VEC ? VEC : (rem > 0 ? (int)rem : 0);
+                src = A + c * lda + kr;
+            }
+            cp_async_vec<VEC>(as + ii * KPAD + kk, src, valid, A);
+        }
+        constexpr int BCH = BN * BK / VEC;
+#pragma unroll
+        for (int ch = tid; ch < BCH; ch += NT) {
+            const int jj = ch / (BK / VEC);
+            const int kk = (ch % (BK / VEC)) * VEC;
+            const int64_t c = j0 + jj, kr = k0 + kk;
+            int valid = 0;
+            const double* src = B;
+            if (c < m2) {
+                const int64_t rem = r_end - kr;
+                valid = rem >= VEC ? VEC : (rem > 0 ? (int)rem : 0);
+                src = B + c * ldb + kr;
+            }
+            cp_async_vec<VEC>(bs + jj * KPAD + kk, src, valid, B);
+        }
+    };
+
+#pragma unroll
+    for (int s = 0; s < STAGES - 1; ++s) {
+        if (s < ktiles) load_stage(s, s);
+        cp_commit();
+    }
+    for (int64_t kt = 0; kt < ktiles; ++kt) {
+        cp_wait<STAGES - 2>();
+        __syncthreads();
+        {
+            const int64_t nk = kt + STAGES - 1;
+            if (nk < ktiles) load_stage((int)(nk % STAGES), nk);
+            cp_commit();
+        }
+        const double* as = As + (kt % STAGES) * A_ELEMS;
+        const double* bs = Bs + (kt % STAGES) * B_ELEMS;
+#pragma unroll
+        for (int k8 = 0; k8 < BK; k8 += 8) {
+            double af[MI][4], bf[NI][2];
+#pragma unroll
+            for (int i = 0; i < MI; ++i) {
+                const int r = wm * WTM + i * 16 + g;
+                af[i][0] = as[r * KPAD + k8 + t0];
+                af[i][1] = as[(r + 8) * KPAD + k8 + t0];
+                af[i][2] = as[r * KPAD + k8 + t0 + 4];
+                af[i][3] = as[(r + 8) * KPAD + k8 + t0 + 4];
+            }
+#pragma unroll
+            for (int j = 0; j < NI; ++j) {
+                const int c = wn * WTN + j * 8 + g;
+                bf[j][0] = bs[c * KPAD + k8 + t0];
+                bf[j][1] = bs[c * KPAD + k8 + t0 + 4];
+            }
+#pragma unroll
+            for (int i = 0; i < MI; ++i)
+#pragma unroll
+                for (int j = 0; j < NI; ++j) dmma16x8x8(acc[i][j], af[i], bf[j]);
+        }
+    }
+    cp_wait<0>();
+
+    double* P = work + split * m1 * m2;
+#pragma unroll
+    for (int j = 0; j < NI; ++j)
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            const int64_t c = j0 + wn * WTN + j * 8 + 2 * t0 + h;
+            if (c >= m2) continue;
+#pragma unroll
+            for (int i = 0; i < MI; ++i)
+#pragma unroll
+                for (int v = 0; v < 2; ++v) {
+                    const int64_t r = i0 + wm * WTM + i * 16 + g + 8 * v;
+                    if (r < m1) P[c * m1 + r] = acc[i][j][2 * v + h];
+                }
+        }
+}
+
+__global__ void reduce_splits_kernel(int64_t m1, int64_t m2, int64_t nsplit,
+                                     const double* __restrict__ work, double alpha,
+                                     double* __restrict__ C, int64_t ldc) {
+    const int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (e >= m1 * m2) return;
+    double s = 0.0;
+    for (int64_t k = 0; k < nsplit; ++k) s += work[k * m1 * m2 + e];  // fixed order
+    const int64_t r = e % m1, c = e / m1;
+    C[c * ldc + r] = alpha * s;
+}
+
+template <int BM, int BN, int WM, int WN, int STAGES, int VEC>
+void launch_tn(int64_t R, int64_t m1, int64_t m2, const double* A, int64_t lda, const double* B,
+               int64_t ldb, double* work, int64_t rows_per_split, int64_t nsplit,
+               cudaStream_t stream) {
+    const size_t smem = sizeof(double) * STAGES * (BM * KPAD + BN * KPAD);
+    auto kern = gemm_tn_kernel<BM, BN, WM, WN, STAGES, VEC>;
+    configure_smem(reinterpret_cast<const void*>(kern), smem);
+    const int64_t tm = cdiv(m1, BM), tn = cdiv(m2, BN);
+    kern<<<(unsigned)(tm * tn * nsplit), WM * WN * 32, smem, stream>>>(
+        R, m1, m2, A, lda, B, ldb, rows_per_split, tm, tn, work);
+    W4_LAUNCH();
+}
+
+}  // namespace
+
+void gemm_nn(const GemmPass* passes, int npass, unsigned* status, cudaStream_t stream) {
+    PassTable tab{};
+    int64_t total_cols = 0, maxM = 0;
+    bool vec2 = true;
+    for (int i = 0; i < npass; ++i) {
+        tab.p[i] = passes[i];
+        total_cols += passes[i].ncols;
+        maxM = passes[i].M > maxM ? passes[i].M : maxM;
+        const GemmPass& p = passes[i];
+        vec2 = vec2 && aligned16(p.A) && (p.lda % 2 == 0) && aligned16(p.in.base) &&
+               (p.in.ld_outer % 2 == 0) && (p.in.stride % 2 == 0);
+    }
+    for (int i = npass; i < 2; ++i) tab.p[i] = GemmPass{};
+    // Tile shape: big tiles when there are enough of them to fill the chip twice.
+    const bool big = cdiv(maxM, 128) * cdiv(total_cols, 64) >= 2 * kSMs;
+    const int BMv = big ? 128 : 64, BNv = big ? 64 : 32;
+    int64_t start = 0;
+    for (int i = 0; i < 2; ++i) {
+        tab.tile_start[i] = start;
+        if (i < npass && passes[i].ncols > 0 && passes[i].M > 0) {
+            tab.tiles_m[i] = cdiv(passes[i].M, BMv);
+            start += tab.tiles_m[i] * cdiv(passes[i].ncols, BNv);
+        } else {
+            tab.tiles_m[i] = 1;
+        }
+    }
+    tab.tile_start[2] = start;
+    if (start == 0) return;
+    if (big) {
+        if (vec2) launch_nn<128, 64, 4, 2, 3, 2>(tab, start, status, stream);
+        else launch_nn<128, 64, 4, 2, 3, 1>(tab, start, status, stream);
+    } else {
+        if (vec2) launch_nn<64, 32, 2, 2, 4, 2>(tab, start, status, stream);
+        else launch_nn<64, 32, 2, 2, 4, 1>(tab, start, status, stream);
+    }
+}
+
+void gemm_tn(int64_t R, int64_t m1, int64_t m2, const double* A, int64_t lda, const double* B,
+             int64_t ldb, double alpha, double* C, int64_t ldc, DevBuf& work,
+             cudaStream_t stream) {
+    if (m1 == 0 || m2 == 0) return;
+    constexpr int BM = 64, BN = 64;
+    const int64_t tiles = cdiv(m1, BM) * cdiv(m2, BN);
+    int64_t nsplit = cdiv(2 * kSMs, tiles);
+    const int64_t min_rows = 256;
+    if (nsplit * min_rows > R) nsplit = cdiv(R, min_rows);
+    if (nsplit < 1) nsplit = 1;
+    int64_t rows_per_split = cdiv(R, nsplit);
+    rows_per_split = cdiv(rows_per_split, BK) * BK;
+    nsplit = R > 0 ? cdiv(R, rows_per_split) : 1;
+    double* w = work.get<double>((size_t)(nsplit * m1 * m2));
+    const bool vec2 = aligned16(A) && aligned16(B) && lda % 2 == 0 && ldb % 2 == 0;
+    if (R == 0) {
+        W4_CUDA(cudaMemsetAsync(w, 0, sizeof(double) * m1 * m2, stream));
+    } else if (vec2) {
+        launch_tn<BM, BN, 2, 2, 4, 2>(R, m1, m2, A, lda, B, ldb, w, rows_per_split, nsplit, stream);
+    } else {
+        launch_tn<BM, BN, 2, 2, 4, 1>(R, m1, m2, A, lda, B, ldb, w, rows_per_split, nsplit, stream);
+    }
+    const int64_t e = m1 * m2;
+    reduce_splits_kernel<<<(unsigned)cdiv(e, 256), 256, 0, stream>>>(m1, m2, nsplit, w, alpha, C,
+                                                                        ldc);
+    W4_LAUNCH();
+}
+
+}  // namespace w4

@@ -1,0 +1,244 @@
+// Operator, LMP and cost handles plus their C-ABI entry points.
+#include "ops.cuh"
+
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <sstream>
+
+#include "lmp_pcg.cuh"
+
+namespace w4 {
+
+namespace {
+thread_local std::string g_last_error;
+}
+
+void set_last_error(const std::string& msg) { g_last_error = msg; }
+const char* last_error_cstr() { return g_last_error.c_str(); }
+
+}  // namespace w4
+
+using namespace w4;
+
+// ----------------------------------------------------------------------------- base op
+wc4dvar_op::~wc4dvar_op() {
+    DeviceGuard g(device);
+    for (cudaEvent_t e : pev)
+        if (e) cudaEventDestroy(e);
+    if (h_int) cudaFreeHost(h_int);
+    if (d_status) cudaFree(d_status);
+    if (h_status) cudaFreeHost(h_status);
+    if (stream) cudaStreamDestroy(stream);
+}
+
+void wc4dvar_op::init_common(int dev, int64_t n) {
+    device = dev;
+    dim = n;
+    W4_CUDA(cudaStreamCreateWithFlags(&stream, cudaStreamNonBlocking));
+    W4_CUDA(cudaMalloc(&d_status, sizeof(unsigned)));
+    W4_CUDA(cudaMallocHost(&h_status, sizeof(unsigned)));
+    W4_CUDA(cudaMallocHost(&h_int, 16 * sizeof(int)));
+    W4_CUDA(cudaMemset(d_status, 0, sizeof(unsigned)));
+}
+
+void wc4dvar_op::collect_profile() {
+    if (!prof || !prof_pending) return;
+    prof_pending = false;
+    for (int i = 0; i < 3; ++i) {
+        float ms = 0;
+        if (cudaEventElapsedTime(&ms, pev[i], pev[i + 1]) == cudaSuccess) prof_ms[i] += ms;
+    }
+    ++prof_calls;
+}
+
+void wc4dvar_op::reset_status(cudaStream_t st) {
+    W4_CUDA(cudaMemsetAsync(d_status, 0, sizeof(unsigned), st));
+}
+
+void wc4dvar_op::check_status(cudaStream_t st) {
+    W4_CUDA(cudaMemcpyAsync(h_status, d_status, sizeof(unsigned), cudaMemcpyDeviceToHost, st));
+    W4_CUDA(cudaStreamSynchronize(st));
+    const unsigned s = *h_status;
+    collect_profile();
+    // operators.cpp:133-143, in the reference's order of checks
+    if (s & ST_FWD_NONFINITE)
+        throw NumericalError("hessian apply: non-finite value after forward sweep");
+    if (s & ST_ADJ_NONFINITE)
+        throw NumericalError("hessian apply: non-finite value after adjoint sweep");
+    if (s & ST_OUT_NONFINITE) throw NumericalError("hessian apply: non-finite result");
+}
+
+namespace w4 {
+
+// ----------------------------------------------------------------------------- Hessian
+HessianOp::~HessianOp() {
+    DeviceGuard g(device);
+    for (double* p : {b_half, b_half_inv, q_half, q_half_inv, d_stages})
+        if (p) cudaFree(p);
+    if (d_slot) cudaFree(d_slot);
+    if (d_pmap) cudaFree(d_pmap);
+}
+
+void HessianOp::d_half(bool inv, const double* V, int64_t ldv, int64_t m, double* out,
+                       int64_t ldo, const double* add, int64_t ldadd, unsigned* status,
+                       cudaStream_t st) {
+    const double* B = inv ? b_half_inv : b_half;
+    const double* Q = inv ? q_half_inv : q_half;
+    require(B && Q, "apply_D_half_inv: inverse factors were not provided");
+    require(cov_kind == WC4DVAR_COV_DENSE, "circulant covariance factors are not built yet");
+    GemmPass ps[2];
+    int np = 0;
+    if (N > 0) {
+        GemmPass& p = ps[np++];
+        p.A = Q;
+        p.lda = n;
+        p.M = n;
+        p.K = n;
+        p.ncols = (int64_t)N * m;
+        p.in = ColMap{V, ldv, n, N, 1};
+        p.out = ColMap{out, ldo, n, N, 1};
+        if (add) p.add = ColMap{add, ldadd, n, N, 1};
+    }
+    {
+        GemmPass& p = ps[np++];
+        p.A = B;
+        p.lda = n;
+        p.M = n;
+        p.K = n;
+        p.ncols = m;
+        p.in = ColMap{V, ldv, n, 1, 0};
+        p.out = ColMap{out, ldo, n, 1, 0};
+        if (add) p.add = ColMap{add, ldadd, n, 1, 0};
+    }
+    gemm_nn(ps, np, status, st);
+}
+
+void HessianOp::apply_block_dev(const double* V, int64_t ldv, int64_t m, double* out, int64_t ldo,
+                                cudaStream_t st) {
+    if (m == 0) return;
+    const int64_t q = nd.q;
+    double* T = t_ws.get<double>((size_t)dim * m);
+    double* Y = q > 0 ? y_ws.get<double>((size_t)q * m) : nullptr;
+    prof_mark(0, st);
+    // t = D^{1/2} v  (operators.cpp:131)
+    d_half(false, V, ldv, m, T, dim, nullptr, 0, nullptr, st);
+    prof_mark(1, st);
+    // traj = L^{-1} t; y = R^{-1} H traj; s = L^{-T} H^T y  (operators.cpp:132-141)
+    SweepArgs a;
+    a.X = T;
+    a.ldx = dim;
+    a.Y = Y;
+    a.scale_fwd = 1.0 / (sigma_obs * sigma_obs);
+    a.do_fwd = true;
+    a.fwd_obs = q > 0;
+    a.S = T;  // in place: the adjoint runs after the forward sweep of the same column
+    a.lds = dim;
+    a.do_adj = true;
+    a.adj_obs = q > 0;
+    a.m = m;
+    sweep(md, nd, a, d_status, st);
+    prof_mark(2, st);
+    // out = v + D^{1/2} s  (operators.cpp:141)
+    d_half(false, T, dim, m, out, ldo, V, ldv, d_status, st);
+    prof_mark(3, st);
+    prof_pending = prof;
+}
+
+void HessianOp::piece_dev(int which, const double* V, int64_t ldv, int64_t m, double* out,
+                          int64_t ldo, cudaStream_t st) {
+    if (m == 0) return;
+    SweepArgs a;
+    a.m = m;
+    switch (which) {
+        case WC4DVAR_LINV:
+            a.X = V;
+            a.ldx = ldv;
+            a.traj = out;
+            a.ldtraj = ldo;
+            a.do_fwd = true;
+            sweep(md, nd, a, d_status, st);
+            break;
+        case WC4DVAR_LINVT:
+            a.V = V;
+            a.ldv = ldv;
+            a.S = out;
+            a.lds = ldo;
+            a.do_adj = true;
+            sweep(md, nd, a, d_status, st);
+            break;
+        case WC4DVAR_D_HALF:
+        case WC4DVAR_D_HALF_INV:
+            d_half(which == WC4DVAR_D_HALF_INV, V, ldv, m, out, ldo, nullptr, 0, nullptr, st);
+            break;
+        default:
+            throw InvalidArgument("hessian piece: unknown selector");
+    }
+}
+
+// ----------------------------------------------------------------------------- Dense
+DenseOp::~DenseOp() {
+    DeviceGuard g(device);
+    if (A) cudaFree(A);
+}
+
+void DenseOp::apply_block_dev(const double* V, int64_t ldv, int64_t m, double* out, int64_t ldo,
+                              cudaStream_t st) {
+    if (m == 0) return;
+    GemmPass p;
+    p.A = A;
+    p.lda = dim;
+    p.M = dim;
+    p.K = dim;
+    p.ncols = m;
+    p.in = ColMap::plain(V, ldv);
+    p.out = ColMap::plain(out, ldo);
+    gemm_nn(&p, 1, nullptr, st);
+}
+
+}  // namespace w4
+
+// ----------------------------------------------------------------------------- LMP / cost dtors
+wc4dvar_lmp::~wc4dvar_lmp() {
+    DeviceGuard g(device);
+    if (U) cudaFree(U);
+    if (theta) cudaFree(theta);
+    if (T) cudaFree(T);
+    if (counter) cudaFree(counter);
+    if (stream) cudaStreamDestroy(stream);
+}
+
+wc4dvar_cost::~wc4dvar_cost() {
+    if (b_tilde) cudaFree(b_tilde);
+    if (d) cudaFree(d);
+    if (counter) cudaFree(counter);
+    if (d_val) cudaFree(d_val);
+}
+
+double wc4dvar_cost::eval_dev(const double* x, cudaStream_t st) {
+    HessianOp& h = *op;
+    const int64_t dim = h.dim, q = h.nd.q;
+    double* t = ws_t.get<double>((size_t)dim);
+    double* y = q > 0 ? ws_y.get<double>((size_t)q) : nullptr;
+    double* part = partial.get<double>(2 * kSMs);
+    // J(x) = 1/2 |x - b~|^2 + 1/2 r_inv |H L^{-1} D^{1/2} x - d|^2  (assimilation.cpp:135-140)
+    h.d_half(false, x, dim, 1, t, dim, nullptr, 0, nullptr, st);
+    SweepArgs a;
+    a.X = t;
+    a.ldx = dim;
+    a.Y = y;
+    a.scale_fwd = 1.0;
+    a.do_fwd = true;
+    a.fwd_obs = q > 0;
+    a.m = 1;
+    sweep(h.md, h.nd, a, h.d_status, st);
+    sqdist(dim, x, b_tilde, d_val, part, counter, st);
+    if (q > 0) sqdist(q, y, d, d_val + 1, part, counter, st);
+    else W4_CUDA(cudaMemsetAsync(d_val + 1, 0, sizeof(double), st));
+    double hv[2];
+    W4_CUDA(cudaMemcpyAsync(hv, d_val, sizeof(hv), cudaMemcpyDeviceToHost, st));
+    W4_CUDA(cudaStreamSynchronize(st));
+    const double r_inv = 1.0 / (h.sigma_obs * h.sigma_obs);
+    return 0.5 * hv[0] + 0.5 * r_inv * hv[1];
+}
+

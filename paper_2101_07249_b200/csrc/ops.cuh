@@ -1,0 +1,122 @@
+// Operator handles behind the C-ABI (include/wc4dvar_gpu.h).
+#pragma once
+
+#include <atomic>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "common.cuh"
+#include "gemm.cuh"
+#include "sweep.cuh"
+
+// LinearOperator (operators.hpp:15-40): dim, apply_block, atomic apply counter.
+struct wc4dvar_op {
+    int device = 0;
+    int64_t dim = 0;
+    std::atomic<int64_t> applies{0};
+    std::recursive_mutex mu;
+    cudaStream_t stream = nullptr;
+    unsigned* d_status = nullptr;  // device status word (finite checks)
+    unsigned* h_status = nullptr;  // pinned mirror
+    int* h_int = nullptr;          // pinned scratch for small device->host reads
+    w4::DevBuf in_buf, out_buf;
+    w4::DevBuf pool[32];           // [0,20) sketch, [20,32) PCG workspaces
+
+    // Stage profiling (wc4dvar_gpu_op_profile): events around the apply's kernels.
+    bool prof = false;
+    bool prof_pending = false;
+    cudaEvent_t pev[4] = {nullptr, nullptr, nullptr, nullptr};
+    double prof_ms[3] = {0, 0, 0};
+    int64_t prof_calls = 0;
+    void prof_mark(int i, cudaStream_t st) {
+        if (prof) cudaEventRecord(pev[i], st);
+    }
+    void collect_profile();  // after a synchronising call
+
+    virtual ~wc4dvar_op();
+    // Block apply on device pointers; does not count and does not synchronise.
+    virtual void apply_block_dev(const double* V, int64_t ldv, int64_t m, double* out, int64_t ldo,
+                                 cudaStream_t st) = 0;
+    virtual const char* kind_name() const = 0;
+
+    void init_common(int dev, int64_t n);
+    void reset_status(cudaStream_t st);
+    // Synchronises st and throws NumericalError with the reference's stage message.
+    void check_status(cudaStream_t st);
+};
+
+namespace w4 {
+
+// HessianOperator (operators.hpp:116-152), Eq. 12 of the paper.
+struct HessianOp final : wc4dvar_op {
+    ModelDev md;
+    NetDev nd;
+    int cov_kind = WC4DVAR_COV_DENSE;
+    int64_t n = 0;
+    int N = 0;
+    double sigma_obs = 1.0;
+    double* b_half = nullptr;
+    double* b_half_inv = nullptr;
+    double* q_half = nullptr;
+    double* q_half_inv = nullptr;
+    int* d_slot = nullptr;
+    int* d_pmap = nullptr;
+    double* d_stages = nullptr;
+    std::vector<int> times, points;
+    DevBuf t_ws, y_ws;
+
+    ~HessianOp() override;
+    const char* kind_name() const override { return "HessianOperator"; }
+    void apply_block_dev(const double* V, int64_t ldv, int64_t m, double* out, int64_t ldo,
+                         cudaStream_t st) override;
+    // which: WC4DVAR_LINV / LINVT / D_HALF / D_HALF_INV (block forms).
+    void piece_dev(int which, const double* V, int64_t ldv, int64_t m, double* out, int64_t ldo,
+                   cudaStream_t st);
+    // out = D^{1/2} V (+ add) for an n_A x m block; inverse factors when inv.
+    void d_half(bool inv, const double* V, int64_t ldv, int64_t m, double* out, int64_t ldo,
+                const double* add, int64_t ldadd, unsigned* status, cudaStream_t st);
+};
+
+// DenseOperator (operators.hpp:42-53).
+struct DenseOp final : wc4dvar_op {
+    double* A = nullptr;
+    ~DenseOp() override;
+    const char* kind_name() const override { return "DenseOperator"; }
+    void apply_block_dev(const double* V, int64_t ldv, int64_t m, double* out, int64_t ldo,
+                         cudaStream_t st) override;
+};
+
+// Thread-local error message for the C-ABI.
+void set_last_error(const std::string& msg);
+const char* last_error_cstr();
+
+}  // namespace w4
+
+// LmpFactor (lmp.hpp:12-26) in compact-WY form.
+struct wc4dvar_lmp {
+    int device = 0;
+    int64_t n = 0;
+    int k = 0;
+    double* U = nullptr;      // n x k (ld n)
+    double* theta = nullptr;  // k
+    double* T = nullptr;      // k x k upper
+    cudaStream_t stream = nullptr;
+    std::mutex mu;
+    w4::DevBuf partial, gbuf, tmp;
+    unsigned* counter = nullptr;
+    ~wc4dvar_lmp();
+};
+
+// QuadraticCost (assimilation.hpp:82-97).
+struct wc4dvar_cost {
+    w4::HessianOp* op = nullptr;
+    double* b_tilde = nullptr;  // n_A
+    double* d = nullptr;        // q
+    w4::DevBuf ws_t, ws_y, partial;
+    unsigned* counter = nullptr;
+    double* d_val = nullptr;    // 2 doubles
+    ~wc4dvar_cost();
+    // value on device pointer x (n_A); synchronises op stream.
+    double eval_dev(const double* x, cudaStream_t st);
+};

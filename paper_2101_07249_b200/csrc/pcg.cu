@@ -1,0 +1,219 @@
+// Split-preconditioned CG on device (krylov.cpp:22-99, Algorithm 1 of the paper).
+//
+// Per iteration: one operator apply (w = A p) and three fused row passes over the LMP
+// vectors U (lmp_pcg.cuh); scalars alpha/beta/rho stay on device and the host reads one
+// small pinned record per iteration for the reference's checks and stopping test.
+#include "pcg.cuh"
+
+#include <cmath>
+#include <sstream>
+
+#include "lmp_pcg.cuh"
+
+namespace w4 {
+namespace {
+
+__global__ void reorth_fix_kernel(double* scal, const double* h, int k) {
+    // after MGS re-orthogonalisation: rho_next = |r|^2 recomputed (krylov.cpp:71-76)
+    const double rn = h[k];
+    scal[SC_RHO_NEXT] = rn;
+    scal[SC_BETA] = rn / scal[SC_DOT];
+    scal[SC_RHO] = rn;
+}
+
+__global__ void dot_kernel(int64_t n, const double* __restrict__ a, const double* __restrict__ b,
+                           double* out) {
+    __shared__ double red[32];
+    double s = 0.0;
+    for (int64_t i = threadIdx.x; i < n; i += blockDim.x) s += a[i] * b[i];
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = s;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double t = 0.0;
+        for (unsigned w = 0; w < blockDim.x / 32; ++w) t += red[w];
+        *out = t;
+    }
+}
+
+__global__ void axpy_dev_kernel(int64_t n, const double* __restrict__ coef, double sign,
+                                const double* __restrict__ f, double* __restrict__ r) {
+    const double c = sign * (*coef);
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x)
+        r[i] -= c * f[i];
+}
+
+__global__ void scale_copy_kernel(int64_t n, const double* __restrict__ r, const double* rho,
+                                  double* __restrict__ f) {
+    const double inv = 1.0 / sqrt(*rho);
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x)
+        f[i] = r[i] * inv;
+}
+
+void check_finite(double v, const char* what, int it) {
+    if (!std::isfinite(v)) {
+        std::ostringstream m;
+        m << "pcg_split: non-finite " << what << " at iteration " << it;
+        throw NumericalError(m.str());
+    }
+}
+
+}  // namespace
+
+void pcg_dev(wc4dvar_op& op, const double* b, wc4dvar_lmp* pre, const double* x0,
+             const wc4dvar_pcg_options& opts, wc4dvar_cost* cost, double* x,
+             PcgRecord& rec, cudaStream_t st) {
+    const int64_t n = op.dim;
+    const int k = pre ? pre->k : 0;
+    require(!pre || pre->k == 0 || pre->n == n, "pcg_split: preconditioner dimension mismatch");
+    enum { B_R = 0, B_P, B_W, B_TMP, B_PART, B_SCAL, B_G, B_H, B_F, B_CNT };
+    DevBuf* pool = op.pool + 20;  // pool[0..19] belong to the sketch workspaces
+    double* r = pool[B_R].get<double>(n);
+    double* p = pool[B_P].get<double>(n);
+    double* w = pool[B_W].get<double>(n);
+    double* tmp = pool[B_TMP].get<double>(n);
+    const int64_t maxgrid = cdiv(n, 32) + 1;
+    double* part = pool[B_PART].get<double>((size_t)maxgrid * (k + 1));
+    double* scal = pool[B_SCAL].get<double>(SC_N + 2);
+    double* g = pool[B_G].get<double>(k + 1);
+    double* h = pool[B_H].get<double>(k + 1);
+    unsigned* counter = pool[B_CNT].get<unsigned>(4);
+    W4_CUDA(cudaMemsetAsync(counter, 0, 4 * sizeof(unsigned), st));
+    W4_CUDA(cudaMemsetAsync(scal, 0, (SC_N + 2) * sizeof(double), st));
+    double* F = nullptr;
+    if (opts.reorthogonalize) F = pool[B_F].get<double>((size_t)n * (opts.max_iter + 1));
+    static thread_local double* pinned = nullptr;
+    if (!pinned) W4_CUDA(cudaMallocHost(&pinned, 16 * sizeof(double)));
+
+    RowPassCtx c;
+    c.n = n;
+    c.k = k;
+    c.U = pre ? pre->U : nullptr;
+    c.ldu = n;
+    c.T = pre ? pre->T : nullptr;
+    c.partial = part;
+    c.counter = counter;
+    c.scal = scal;
+    c.g = g;
+    c.h = h;
+
+    auto read_scal = [&]() {
+        W4_CUDA(cudaMemcpyAsync(pinned, scal, SC_N * sizeof(double), cudaMemcpyDeviceToHost, st));
+        W4_CUDA(cudaStreamSynchronize(st));
+    };
+
+    // x = x0 or 0; r = C^T (b - A x0)   (krylov.cpp:32-38)
+    bool x0_zero = true;
+    if (x0) {
+        // isZero(0.0): every entry exactly zero (checked on device)
+        rowpass_utv(RowPassCtx{n, 0, nullptr, n, nullptr, part, counter, scal, g, h}, x0, x0, x0,
+                    tmp, st);  // tmp[0] = x0 . x0
+        double hv = 0;
+        W4_CUDA(cudaMemcpyAsync(&hv, tmp, sizeof(double), cudaMemcpyDeviceToHost, st));
+        W4_CUDA(cudaStreamSynchronize(st));
+        x0_zero = (hv == 0.0);
+    }
+    if (x0 && !x0_zero) {
+        W4_CUDA(cudaMemcpyAsync(x, x0, n * sizeof(double), cudaMemcpyDeviceToDevice, st));
+        op.applies += 1;
+        op.reset_status(st);
+        op.apply_block_dev(x, n, 1, w, n, st);
+        op.check_status(st);
+        axpby(n, 1.0, b, -1.0, w, tmp, st);  // b - A x0
+    } else {
+        if (x0) W4_CUDA(cudaMemcpyAsync(x, x0, n * sizeof(double), cudaMemcpyDeviceToDevice, st));
+        else W4_CUDA(cudaMemsetAsync(x, 0, n * sizeof(double), st));
+        W4_CUDA(cudaMemcpyAsync(tmp, b, n * sizeof(double), cudaMemcpyDeviceToDevice, st));
+    }
+    rowpass_utv(c, tmp, nullptr, nullptr, g, st);        // g = U^T rhs
+    rowpass_apply(c, true, tmp, g, r, st);               // r = C^T rhs
+    rowpass_utv(c, r, r, r, h, st);                      // h = [U^T r ; r.r]
+    rowpass_apply(c, false, r, h, p, st);                // p = C r  (krylov.cpp:39)
+    W4_CUDA(cudaMemcpyAsync(scal + SC_RHO, h + k, sizeof(double), cudaMemcpyDeviceToDevice, st));
+    read_scal();
+    const double rho0 = pinned[SC_RHO];
+    const double r0 = std::sqrt(rho0);
+    rec.residual_norms.push_back(r0);
+    if (cost) rec.costs.push_back(cost->eval_dev(x, st));
+    rec.iterations = 0;
+    rec.converged = false;
+    if (r0 == 0.0) {
+        rec.converged = true;
+        rec.stop_reason = 0;
+        return;
+    }
+    int nf = 0;
+    if (F) {
+        scale_copy_kernel<<<(unsigned)std::min<int64_t>(cdiv(n, 256), 1184), 256, 0, st>>>(
+            n, r, scal + SC_RHO, F);
+        W4_LAUNCH();
+        nf = 1;
+    }
+    for (int j = 1; j <= opts.max_iter; ++j) {
+        op.applies += 1;  // the single operator apply of this iteration (krylov.cpp:56)
+        op.reset_status(st);
+        op.apply_block_dev(p, n, 1, w, n, st);
+        pcg_pass1(c, p, w, st);  // curvature, alpha
+        if (F) W4_CUDA(cudaMemcpyAsync(scal + SC_DOT, scal + SC_RHO, sizeof(double),
+                                       cudaMemcpyDeviceToDevice, st));
+        pcg_pass2(c, x, r, p, w, st);  // x, r, rho_next, beta
+        if (F) {
+            // modified Gram-Schmidt against the stored normalised residuals (krylov.cpp:71-74)
+            double* dd = scal + SC_N;
+            for (int f = 0; f < nf; ++f) {
+                dot_kernel<<<1, 1024, 0, st>>>(n, F + (int64_t)f * n, r, dd);
+                axpy_dev_kernel<<<(unsigned)std::min<int64_t>(cdiv(n, 256), 1184), 256, 0, st>>>(
+                    n, dd, 1.0, F + (int64_t)f * n, r);
+            }
+            W4_LAUNCH();
+            rowpass_utv(c, r, r, r, h, st);
+            reorth_fix_kernel<<<1, 1, 0, st>>>(scal, h, k);
+            W4_LAUNCH();
+        }
+        pcg_pass3(c, r, p, st);  // p = C r + beta p (speculative; unused on exit)
+        W4_CUDA(cudaMemcpyAsync(op.h_status, op.d_status, sizeof(unsigned), cudaMemcpyDeviceToHost,
+                                st));
+        read_scal();
+        const unsigned s = *op.h_status;
+        if (s & ST_FWD_NONFINITE)
+            throw NumericalError("hessian apply: non-finite value after forward sweep");
+        if (s & ST_ADJ_NONFINITE)
+            throw NumericalError("hessian apply: non-finite value after adjoint sweep");
+        if (s & ST_OUT_NONFINITE) throw NumericalError("hessian apply: non-finite result");
+        const double curv = pinned[SC_CURV];
+        check_finite(curv, "curvature", j);
+        if (curv <= 0.0) {
+            std::ostringstream m;
+            m << "pcg_split: p^T A p = " << curv << " at iteration " << j
+              << "; operator lost positive definiteness";
+            throw NumericalError(m.str());
+        }
+        const double alpha = pinned[SC_ALPHA];
+        check_finite(alpha, "alpha", j);
+        const double rho_next = pinned[SC_RHO_NEXT];
+        const double beta = pinned[SC_BETA];
+        check_finite(beta, "beta", j);
+        rec.alphas.push_back(alpha);
+        rec.betas.push_back(beta);
+        rec.residual_norms.push_back(std::sqrt(rho_next));
+        if (cost) rec.costs.push_back(cost->eval_dev(x, st));
+        if (F && rho_next > 0.0) {
+            scale_copy_kernel<<<(unsigned)std::min<int64_t>(cdiv(n, 256), 1184), 256, 0, st>>>(
+                n, r, scal + SC_RHO_NEXT, F + (int64_t)nf * n);
+            W4_LAUNCH();
+            ++nf;
+        }
+        rec.iterations = j;
+        if (std::sqrt(rho_next) / r0 <= opts.rel_tol) {
+            rec.converged = true;
+            rec.stop_reason = 1;
+            break;
+        }
+    }
+    if (!rec.converged) rec.stop_reason = 2;
+    W4_CUDA(cudaStreamSynchronize(st));
+}
+
+}  // namespace w4

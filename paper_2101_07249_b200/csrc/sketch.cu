@@ -1,0 +1,356 @@
+// REVD / Nystrom / ritzit on device (randevd.cpp:47-148).
+//
+// Orthonormalisation is CholQR2 (Gram by DMMA split-GEMM, Cholesky + triangular inverse
+// in one CTA, Y R^{-1} by DMMA GEMM, twice).  The reference's Householder QR, pivoted QR
+// and BDCSVD are replaced by numerically equivalent (basis-invariant) steps:
+//   * Ritz values / LMP are invariant to the orthonormal basis of span(Y)
+//     (sign and rotation of Z cancel in Z W), so CholQR2 replaces HouseholderQR;
+//   * the ColPivHouseholderQR rank probe becomes a diagonally pivoted Cholesky of Y^T Y
+//     with a Gram-noise threshold;
+//   * BDCSVD(F) becomes CholQR2(F) = Q_F R_F plus one-sided Jacobi SVD of R_F.
+#include "sketch.cuh"
+
+#include <cmath>
+#include <cstring>
+#include <sstream>
+#include <vector>
+
+#include "gemm.cuh"
+#include "lmp_pcg.cuh"
+#include "smallla.cuh"
+
+namespace w4 {
+namespace {
+
+enum {
+    P_Y = 0, P_Z, P_Q1, P_AZ, P_F, P_G, P_R1, P_R1I, P_G2, P_R2, P_R2I, P_R, P_K, P_W,
+    P_VALS, P_INT, P_TMP, P_SEL, P_GEMMWS, P_SMALLWS, P_COUNT
+};
+
+struct Timer {
+    cudaStream_t st;
+    std::vector<std::pair<int, std::pair<cudaEvent_t, cudaEvent_t>>> evs;
+    int cur = -1;
+    cudaEvent_t cur_start = nullptr;
+    bool on;
+    Timer(cudaStream_t s, bool enabled) : st(s), on(enabled) {}
+    ~Timer() {
+        for (auto& e : evs) {
+            cudaEventDestroy(e.second.first);
+            cudaEventDestroy(e.second.second);
+        }
+    }
+    void begin(int cat) {
+        if (!on) return;
+        end();
+        W4_CUDA(cudaEventCreate(&cur_start));
+        W4_CUDA(cudaEventRecord(cur_start, st));
+        cur = cat;
+    }
+    void end() {
+        if (!on || cur < 0) return;
+        cudaEvent_t e;
+        W4_CUDA(cudaEventCreate(&e));
+        W4_CUDA(cudaEventRecord(e, st));
+        evs.push_back({cur, {cur_start, e}});
+        cur = -1;
+    }
+    void collect(SketchTiming* t) {
+        if (!on || !t) return;
+        end();
+        W4_CUDA(cudaStreamSynchronize(st));
+        double acc[4] = {0, 0, 0, 0};
+        for (auto& e : evs) {
+            float ms = 0;
+            W4_CUDA(cudaEventElapsedTime(&ms, e.second.first, e.second.second));
+            acc[e.first] += ms;
+        }
+        t->apply_ms = acc[0];
+        t->orth_ms = acc[1];
+        t->small_ms = acc[2];
+        t->gemm_ms = acc[3];
+        t->total_ms = acc[0] + acc[1] + acc[2] + acc[3];
+    }
+};
+enum { T_APPLY = 0, T_ORTH = 1, T_SMALL = 2, T_GEMM = 3 };
+
+struct Ctx {
+    wc4dvar_op& op;
+    cudaStream_t st;
+    int64_t n;
+    Timer& tm;
+    DevBuf* pool;
+    int* h_int;  // pinned scratch
+
+    double* buf(int id, size_t count) { return pool[id].get<double>(count); }
+
+    int read_int(const int* d) {
+        W4_CUDA(cudaMemcpyAsync(h_int, d, sizeof(int), cudaMemcpyDeviceToHost, st));
+        W4_CUDA(cudaStreamSynchronize(st));
+        return *h_int;
+    }
+
+    // out = A in  (m columns), counted and finite-checked like apply_block.
+    void apply(const double* in, int64_t m, double* out) {
+        tm.begin(T_APPLY);
+        op.applies += m;
+        op.reset_status(st);
+        op.apply_block_dev(in, n, m, out, n, st);
+        op.check_status(st);
+        tm.end();
+    }
+
+    // G = A^T B (m1 x m2)
+    void gram(const double* A, int64_t m1, const double* B, int64_t m2, double* G) {
+        gemm_tn(n, m1, m2, A, n, B, n, 1.0, G, m1, pool[P_GEMMWS], st);
+    }
+
+    // C (n x ncols) = A (n x K) * B (K x ncols, ld K)
+    void tall_times_small(const double* A, int64_t K, const double* B, int64_t ldb, int64_t ncols,
+                          double* C, int64_t ldc) {
+        GemmPass p;
+        p.A = A;
+        p.lda = n;
+        p.M = n;
+        p.K = K;
+        p.ncols = ncols;
+        p.in = ColMap::plain(B, ldb);
+        p.out = ColMap::plain(C, ldc);
+        gemm_nn(&p, 1, nullptr, st);
+    }
+
+    // CholQR2: Q (n x m) with Y = Q R; G0 = Y^T Y may be supplied.  Returns false on a
+    // Cholesky breakdown (caller raises the method-specific NumericalError).
+    bool cholqr2(const double* Y, int64_t m, double* Q, double* R_out, const double* G0) {
+        tm.begin(T_ORTH);
+        double* G = buf(P_G, m * m);
+        if (G0) {
+            if (G0 != G)
+                W4_CUDA(cudaMemcpyAsync(G, G0, sizeof(double) * m * m, cudaMemcpyDeviceToDevice, st));
+        } else {
+            gram(Y, m, Y, m, G);
+        }
+        double* R1 = buf(P_R1, m * m);
+        double* R1i = buf(P_R1I, m * m);
+        int* info = reinterpret_cast<int*>(buf(P_INT, 4 + 2 * m));
+        chol_upper((int)m, G, R1, info, pool[P_SMALLWS], st);
+        if (read_int(info)) return false;
+        tri_inv_upper((int)m, R1, R1i, st);
+        double* Q1 = buf(P_Q1, n * m);
+        tall_times_small(Y, m, R1i, m, m, Q1, n);
+        double* G2 = buf(P_G2, m * m);
+        gram(Q1, m, Q1, m, G2);
+        double* R2 = buf(P_R2, m * m);
+        double* R2i = buf(P_R2I, m * m);
+        chol_upper((int)m, G2, R2, info, pool[P_SMALLWS], st);
+        if (read_int(info)) return false;
+        tri_inv_upper((int)m, R2, R2i, st);
+        tall_times_small(Q1, m, R2i, m, m, Q, n);
+        if (R_out) small_gemm(false, false, (int)m, (int)m, (int)m, 1.0, R2, (int)m, R1, (int)m, 0.0,
+                              R_out, (int)m, st);
+        tm.end();
+        return true;
+    }
+
+    // rank probe: pivoted Cholesky of G (m x m); perm to P_INT[4..]
+    int rank_probe(const double* G, int64_t m, int** perm_out) {
+        tm.begin(T_SMALL);
+        int* ints = reinterpret_cast<int*>(buf(P_INT, 4 + 2 * m));
+        int* perm = ints + 4;
+        const double tol_rel = 32.0 * std::sqrt((double)n) * 2.220446049250313e-16;
+        pivoted_chol_rank((int)m, G, tol_rel, ints + 1, perm, pool[P_SMALLWS], st);
+        const int r = read_int(ints + 1);
+        tm.end();
+        *perm_out = perm;
+        return r;
+    }
+};
+
+__global__ void sqrt_head_kernel(int k, const double* __restrict__ vals, double* __restrict__ out) {
+    const int i = threadIdx.x + blockIdx.x * blockDim.x;
+    if (i < k) out[i] = sqrt(vals[i]);
+}
+__global__ void square_head_kernel(int k, const double* __restrict__ s, double* __restrict__ out) {
+    const int i = threadIdx.x + blockIdx.x * blockDim.x;
+    if (i < k) out[i] = s[i] * s[i];
+}
+
+void rr_core(Ctx& c, const double* Z, int64_t m, int64_t keep, double* U_out, int64_t ldu,
+             double* theta_out) {
+    const int64_t n = c.n;
+    // Gram defect check (randevd.cpp:50-52)
+    c.tm.begin(T_GEMM);
+    double* G = c.buf(P_G, m * m);
+    c.gram(Z, m, Z, m, G);
+    double* defect = c.buf(P_TMP, 4);
+    defect_max((int)m, G, defect, c.st);
+    double hd = 0;
+    W4_CUDA(cudaMemcpyAsync(&hd, defect, sizeof(double), cudaMemcpyDeviceToHost, c.st));
+    W4_CUDA(cudaStreamSynchronize(c.st));
+    c.tm.end();
+    if (!(hd <= 1e-8)) throw NumericalError("rayleigh_ritz: Z is not orthonormal");
+    double* AZ = c.buf(P_AZ, n * m);
+    c.apply(Z, m, AZ);  // second block product
+    c.tm.begin(T_GEMM);
+    double* K = c.buf(P_K, m * m);
+    c.gram(Z, m, AZ, m, K);
+    c.tm.begin(T_SMALL);
+    double* vals = c.buf(P_VALS, m);
+    double* W = c.buf(P_W, m * m);
+    sym_evd_desc((int)m, K, vals, W, c.pool[P_SMALLWS], c.st);
+    c.tm.begin(T_GEMM);
+    c.tall_times_small(Z, m, W, m, keep, U_out, ldu);
+    W4_CUDA(cudaMemcpyAsync(theta_out, vals, sizeof(double) * keep, cudaMemcpyDeviceToDevice, c.st));
+    c.tm.end();
+}
+
+}  // namespace
+
+void rayleigh_ritz_dev(wc4dvar_op& op, const double* Z, int64_t ldz, int64_t m, double* U_out,
+                       int64_t ldu, double* theta_out, cudaStream_t st) {
+    require(ldz == op.dim, "rayleigh_ritz: Z must be contiguous (ld = dim)");
+    Timer tm(st, false);
+    Ctx c{op, st, op.dim, tm, op.pool, op.h_int};
+    rr_core(c, Z, m, m, U_out, ldu, theta_out);
+}
+
+int64_t sketch_dev(wc4dvar_op& op, const wc4dvar_sketch_config& cfg, const double* omega,
+                   double* U_out, int64_t ldu, double* theta_out, cudaStream_t st,
+                   SketchTiming* timing) {
+    const int64_t n = op.dim;
+    // SketchConfig::validate, randevd.cpp:10-14
+    require(cfg.target_rank >= 1, "SketchConfig: target rank must be >= 1");
+    require(cfg.oversample >= 0, "SketchConfig: oversampling must be >= 0");
+    const int64_t k = cfg.target_rank;
+    const int64_t m = k + cfg.oversample;
+    require(m <= n, "SketchConfig: k + l exceeds operator dimension");
+    require(m <= 512, "sketch: k + l above 512 is not supported by the device small-matrix kernels");
+    Timer tm(st, timing != nullptr);
+    Ctx c{op, st, n, tm, op.pool, op.h_int};
+    int64_t produced = 0;
+
+    if (cfg.method == WC4DVAR_SKETCH_REVD) {
+        // randevd.cpp:62-80
+        double* Y = c.buf(P_Y, n * m);
+        c.apply(omega, m, Y);
+        tm.begin(T_GEMM);
+        double* G = c.buf(P_G, m * m);
+        c.gram(Y, m, Y, m, G);
+        int* perm = nullptr;
+        const int r = c.rank_probe(G, m, &perm);
+        if (r < m) {
+            std::ostringstream msg;
+            msg << "revd: sample matrix rank collapsed to " << r << " of " << m << " columns";
+            throw NumericalError(msg.str());
+        }
+        double* Z = c.buf(P_Z, n * m);
+        if (!c.cholqr2(Y, m, Z, nullptr, G))
+            throw NumericalError("revd: sample matrix is numerically rank deficient (CholQR breakdown)");
+        rr_core(c, Z, m, k, U_out, ldu, theta_out);
+        produced = k;
+    } else if (cfg.method == WC4DVAR_SKETCH_NYSTROM) {
+        // randevd.cpp:82-114
+        double* Y = c.buf(P_Y, n * m);
+        c.apply(omega, m, Y);
+        tm.begin(T_GEMM);
+        double* G = c.buf(P_G, m * m);
+        c.gram(Y, m, Y, m, G);
+        int* perm = nullptr;
+        const int r = c.rank_probe(G, m, &perm);
+        if (r == 0) throw NumericalError("nystrom: sample matrix is zero");
+        double* Z = c.buf(P_Z, n * m);
+        const double* Ysrc = Y;
+        if (r < m) {
+            double* Ysel = c.buf(P_SEL, n * r);
+            gather_cols(n, r, Y, n, perm, Ysel, n, st);
+            Ysrc = Ysel;
+        }
+        if (!c.cholqr2(Ysrc, r, Z, nullptr, r < m ? nullptr : G))
+            throw NumericalError("nystrom: sample matrix is numerically rank deficient (CholQR breakdown)");
+        double* E1 = c.buf(P_AZ, n * r);
+        c.apply(Z, r, E1);
+        tm.begin(T_GEMM);
+        double* E2 = c.buf(P_K, r * r);
+        c.gram(Z, r, E1, r, E2);
+        tm.begin(T_SMALL);
+        double* Ru = c.buf(P_R1, r * r);
+        double* Rui = c.buf(P_R1I, r * r);
+        int* info = reinterpret_cast<int*>(c.buf(P_INT, 4 + 2 * m));
+        chol_upper((int)r, E2, Ru, info, op.pool[P_SMALLWS], st);  // sym(E2), randevd.cpp:96-97
+        if (c.read_int(info))
+            throw NumericalError(
+                "nystrom: Cholesky of Z^T A Z failed; the projected operator is numerically "
+                "indefinite. Increase the oversampling parameter or use revd for indefinite "
+                "spectra.");
+        tri_inv_upper((int)r, Ru, Rui, st);
+        tm.begin(T_GEMM);
+        double* F = c.buf(P_F, n * r);
+        c.tall_times_small(E1, r, Rui, r, r, F, n);  // F = E1 U^{-1}, randevd.cpp:104-105
+        double* QF = c.buf(P_Y, n * r);              // Y no longer needed
+        double* RF = c.buf(P_R, r * r);
+        if (!c.cholqr2(F, r, QF, RF, nullptr))
+            throw NumericalError("nystrom: factor F is numerically rank deficient (CholQR breakdown)");
+        tm.begin(T_SMALL);
+        double* sig = c.buf(P_VALS, r);
+        double* W = c.buf(P_W, r * r);
+        svd_left_desc((int)r, RF, sig, W, op.pool[P_SMALLWS], st);
+        const int64_t keep = std::min<int64_t>(k, r);
+        tm.begin(T_GEMM);
+        c.tall_times_small(QF, r, W, r, keep, U_out, ldu);
+        square_head_kernel<<<1, 512, 0, st>>>((int)keep, sig, theta_out);
+        W4_LAUNCH();
+        tm.end();
+        produced = keep;
+    } else if (cfg.method == WC4DVAR_SKETCH_RITZIT) {
+        // randevd.cpp:116-136 (+ p_iter EXTENSION)
+        double* G3 = c.buf(P_Z, n * m);
+        if (!c.cholqr2(omega, m, G3, nullptr, nullptr))
+            throw NumericalError("revd_ritzit: Gaussian sample is numerically rank deficient");
+        double* Y3 = c.buf(P_Y, n * m);
+        c.apply(G3, m, Y3);
+        for (int it = 1; it < std::max(cfg.p_iter, 1); ++it) {
+            if (!c.cholqr2(Y3, m, G3, nullptr, nullptr))
+                throw NumericalError("revd_ritzit: QR of the sample matrix is rank deficient");
+            c.apply(G3, m, Y3);
+        }
+        double* Z3 = c.buf(P_Z, n * m);
+        double* R3 = c.buf(P_R, m * m);
+        if (!c.cholqr2(Y3, m, Z3, R3, nullptr))
+            throw NumericalError("revd_ritzit: QR of the sample matrix is rank deficient");
+        // min |R_ii| <= 1e-14 max |R_ii| (randevd.cpp:125-127)
+        std::vector<double> hR(m * m);
+        W4_CUDA(cudaMemcpyAsync(hR.data(), R3, sizeof(double) * m * m, cudaMemcpyDeviceToHost, st));
+        W4_CUDA(cudaStreamSynchronize(st));
+        double dmin = INFINITY, dmax = 0.0;
+        for (int64_t i = 0; i < m; ++i) {
+            dmin = std::min(dmin, std::fabs(hR[i + i * m]));
+            dmax = std::max(dmax, std::fabs(hR[i + i * m]));
+        }
+        if (dmin <= 1e-14 * dmax)
+            throw NumericalError("revd_ritzit: QR of the sample matrix is rank deficient");
+        tm.begin(T_SMALL);
+        double* K = c.buf(P_K, m * m);
+        small_gemm(false, true, (int)m, (int)m, (int)m, 1.0, R3, (int)m, R3, (int)m, 0.0, K, (int)m,
+                   st);  // R3 R3^T
+        double* vals = c.buf(P_VALS, m);
+        double* W = c.buf(P_W, m * m);
+        sym_evd_desc((int)m, K, vals, W, op.pool[P_SMALLWS], st);
+        double hv = 0;
+        W4_CUDA(cudaMemcpyAsync(&hv, vals + (std::min(k, m) - 1), sizeof(double),
+                                cudaMemcpyDeviceToHost, st));
+        W4_CUDA(cudaStreamSynchronize(st));
+        if (hv <= 0.0) throw NumericalError("revd_ritzit: nonpositive squared Ritz value");
+        tm.begin(T_GEMM);
+        c.tall_times_small(Z3, m, W, m, k, U_out, ldu);
+        sqrt_head_kernel<<<1, 512, 0, st>>>((int)k, vals, theta_out);
+        W4_LAUNCH();
+        tm.end();
+        produced = k;
+    } else {
+        throw InvalidArgument("sketch_eigenpairs: unknown method");
+    }
+    tm.collect(timing);
+    return produced;
+}
+
+}  // namespace w4

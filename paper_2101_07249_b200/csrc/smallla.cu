@@ -1,0 +1,443 @@
+// Single-CTA dense kernels on the (k+l)-dimension (see smallla.cuh).
+#include "smallla.cuh"
+
+#include <cfloat>
+
+namespace w4 {
+namespace {
+
+constexpr int kThreads = 1024;
+constexpr size_t kSmemMax = 200 * 1024;
+
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
+
+// ---------------------------------------------------------------- Cholesky
+__global__ void __launch_bounds__(kThreads)
+    chol_kernel(int m, const double* __restrict__ G, double* __restrict__ R, int* info,
+                double* gwork, int use_smem) {
+    extern __shared__ double sm[];
+    double* A = use_smem ? sm : gwork;
+    __shared__ int fail;
+    const int tid = threadIdx.x, nt = blockDim.x;
+    for (int e = tid; e < m * m; e += nt) {
+        const int i = e % m, j = e / m;
+        A[e] = 0.5 * (G[i + j * m] + G[j + i * m]);
+    }
+    if (tid == 0) fail = 0;
+    __syncthreads();
+    for (int j = 0; j < m; ++j) {
+        if (tid == 0) {
+            const double d = A[j + j * m];
+            if (!(d > 0.0) || !isfinite(d)) fail = j + 1;
+            else A[j + j * m] = sqrt(d);
+        }
+        __syncthreads();
+        if (fail) break;
+        const double ljj = A[j + j * m];
+        for (int i = j + 1 + tid; i < m; i += nt) A[i + j * m] /= ljj;
+        __syncthreads();
+        const int w = m - j - 1;
+        for (int e = tid; e < w * w; e += nt) {
+            const int i = j + 1 + e % w, k = j + 1 + e / w;
+            if (i >= k) A[i + k * m] -= A[i + j * m] * A[k + j * m];
+        }
+        __syncthreads();
+    }
+    if (!fail)
+        for (int e = tid; e < m * m; e += nt) {
+            const int r = e % m, c = e / m;  // R(r, c) = L(c, r) for c >= r
+            R[e] = (c >= r) ? A[c + r * m] : 0.0;
+        }
+    if (tid == 0) *info = fail;
+}
+
+// ---------------------------------------------------------------- pivoted Cholesky rank
+__global__ void __launch_bounds__(kThreads)
+    pchol_kernel(int m, const double* __restrict__ G, double tol_rel, int* rank, int* perm,
+                 double* gwork, int use_smem) {
+    extern __shared__ double sm[];
+    double* A = use_smem ? sm : gwork;
+    __shared__ int piv, stop;
+    __shared__ double maxd;
+    const int tid = threadIdx.x, nt = blockDim.x;
+    for (int e = tid; e < m * m; e += nt) {
+        const int i = e % m, j = e / m;
+        A[e] = 0.5 * (G[i + j * m] + G[j + i * m]);
+    }
+    for (int i = tid; i < m; i += nt) perm[i] = i;
+    __syncthreads();
+    if (tid == 0) {
+        double mx = 0.0;
+        for (int i = 0; i < m; ++i) mx = fmax(mx, A[i + i * m]);
+        maxd = mx;
+        stop = 0;
+    }
+    __syncthreads();
+    const double tol = tol_rel * maxd;
+    int r = m;
+    for (int j = 0; j < m; ++j) {
+        if (tid == 0) {
+            int p = j;
+            double best = A[j + j * m];
+            for (int i = j + 1; i < m; ++i)
+                if (A[i + i * m] > best) {
+                    best = A[i + i * m];
+                    p = i;
+                }
+            piv = p;
+            stop = !(best > tol) || !isfinite(best);
+            if (!stop && p != j) {
+                const int t = perm[j];
+                perm[j] = perm[p];
+                perm[p] = t;
+            }
+        }
+        __syncthreads();
+        if (stop) {
+            r = j;
+            break;
+        }
+        const int p = piv;
+        if (p != j) {
+            for (int c = tid; c < m; c += nt) {
+                const double t = A[j + c * m];
+                A[j + c * m] = A[p + c * m];
+                A[p + c * m] = t;
+            }
+            __syncthreads();
+            for (int rr = tid; rr < m; rr += nt) {
+                const double t = A[rr + j * m];
+                A[rr + j * m] = A[rr + p * m];
+                A[rr + p * m] = t;
+            }
+            __syncthreads();
+        }
+        const double ljj = sqrt(A[j + j * m]);
+        __syncthreads();
+        for (int i = j + tid; i < m; i += nt) A[i + j * m] = (i == j) ? ljj : A[i + j * m] / ljj;
+        __syncthreads();
+        const int w = m - j - 1;
+        for (int e = tid; e < w * w; e += nt) {
+            const int i = j + 1 + e % w, k = j + 1 + e / w;
+            A[i + k * m] -= A[i + j * m] * A[k + j * m];
+        }
+        __syncthreads();
+    }
+    if (tid == 0) *rank = r;
+}
+
+// ---------------------------------------------------------------- triangular inverse
+__global__ void tri_inv_kernel(int m, const double* __restrict__ R, double* __restrict__ Rinv) {
+    extern __shared__ double xs[];
+    const int warps = blockDim.x / 32;
+    const int wid = threadIdx.x / 32, lane = threadIdx.x % 32;
+    const int j = blockIdx.x * warps + wid;
+    if (j >= m) return;
+    double* x = xs + wid * m;
+    if (lane == 0) x[j] = 1.0 / R[j + j * m];
+    __syncwarp();
+    for (int i = j - 1; i >= 0; --i) {
+        double s = 0.0;
+        for (int k = i + 1 + lane; k <= j; k += 32) s += R[i + k * m] * x[k];
+        s = warp_sum(s);
+        if (lane == 0) x[i] = -s / R[i + i * m];
+        __syncwarp();
+    }
+    for (int i = lane; i < m; i += 32) Rinv[i + j * m] = (i <= j) ? x[i] : 0.0;
+}
+
+// ---------------------------------------------------------------- round-robin pairs
+__device__ __forceinline__ void rr_pair(int k, int r, int mp, int& p, int& q) {
+    auto player = [&](int pos) { return pos == 0 ? 0 : 1 + (pos - 1 + r) % (mp - 1); };
+    p = player(k);
+    q = player(mp - 1 - k);
+    if (p > q) {
+        const int t = p;
+        p = q;
+        q = t;
+    }
+}
+
+// ---------------------------------------------------------------- two-sided Jacobi EVD
+__global__ void __launch_bounds__(kThreads)
+    jacobi_evd_kernel(int m, const double* __restrict__ K, double* __restrict__ vals,
+                      double* __restrict__ W, double* gwork, int use_smem) {
+    extern __shared__ double sm[];
+    double* A = use_smem ? sm : gwork;
+    double* V = A + (size_t)m * m;
+    __shared__ double cs_c[512], cs_s[512];
+    __shared__ int cs_p[512], cs_q[512];
+    __shared__ int rank_of[512];
+    const int tid = threadIdx.x, nt = blockDim.x;
+    for (int e = tid; e < m * m; e += nt) {
+        const int i = e % m, j = e / m;
+        A[e] = 0.5 * (K[i + j * m] + K[j + i * m]);
+        V[e] = (i == j) ? 1.0 : 0.0;
+    }
+    __syncthreads();
+    const int mp = m + (m & 1);
+    const int npairs = mp / 2;
+    for (int sweep = 0; sweep < 60 && m > 1; ++sweep) {
+        int rotated = 0;
+        for (int r = 0; r < mp - 1; ++r) {
+            for (int k = tid; k < npairs; k += nt) {
+                int p, q;
+                rr_pair(k, r, mp, p, q);
+                double c = 1.0, s = 0.0;
+                if (q < m) {
+                    const double apq = A[p + q * m];
+                    const double app = A[p + p * m], aqq = A[q + q * m];
+                    if (apq != 0.0 && fabs(apq) > DBL_EPSILON * 0.5 * sqrt(fabs(app * aqq))) {
+                        const double tau = (aqq - app) / (2.0 * apq);
+                        const double t =
+                            (tau >= 0.0 ? 1.0 : -1.0) / (fabs(tau) + sqrt(1.0 + tau * tau));
+                        c = 1.0 / sqrt(1.0 + t * t);
+                        s = t * c;
+                        rotated = 1;
+                    }
+                }
+                cs_c[k] = c;
+                cs_s[k] = s;
+                cs_p[k] = p;
+                cs_q[k] = q;
+            }
+            __syncthreads();
+            // A <- A J, V <- V J (columns p, q)
+            for (int e = tid; e < npairs * m; e += nt) {
+                const int k = e / m, i = e % m;
+                const double s = cs_s[k];
+                if (s == 0.0) continue;
+                const double c = cs_c[k];
+                const int p = cs_p[k], q = cs_q[k];
+                const double aip = A[i + p * m], aiq = A[i + q * m];
+                A[i + p * m] = c * aip - s * aiq;
+                A[i + q * m] = s * aip + c * aiq;
+                const double vip = V[i + p * m], viq = V[i + q * m];
+                V[i + p * m] = c * vip - s * viq;
+                V[i + q * m] = s * vip + c * viq;
+            }
+            __syncthreads();
+            // A <- J^T A (rows p, q)
+            for (int e = tid; e < npairs * m; e += nt) {
+                const int k = e / m, cidx = e % m;
+                const double s = cs_s[k];
+                if (s == 0.0) continue;
+                const double c = cs_c[k];
+                const int p = cs_p[k], q = cs_q[k];
+                const double apc = A[p + cidx * m], aqc = A[q + cidx * m];
+                A[p + cidx * m] = c * apc - s * aqc;
+                A[q + cidx * m] = s * apc + c * aqc;
+            }
+            __syncthreads();
+        }
+        if (!__syncthreads_or(rotated)) break;
+    }
+    for (int i = tid; i < m; i += nt) {
+        const double di = A[i + i * m];
+        int rk = 0;
+        for (int j = 0; j < m; ++j) {
+            const double dj = A[j + j * m];
+            rk += (dj > di) || (dj == di && j < i);
+        }
+        rank_of[i] = rk;
+        vals[rk] = di;
+    }
+    __syncthreads();
+    for (int e = tid; e < m * m; e += nt) {
+        const int i = e % m, j = e / m;
+        W[i + rank_of[j] * m] = V[e];
+    }
+}
+
+// ---------------------------------------------------------------- one-sided Jacobi SVD
+__global__ void __launch_bounds__(kThreads)
+    jacobi_svd_kernel(int m, const double* __restrict__ Xin, double* __restrict__ sigma,
+                      double* __restrict__ U, double* gwork, int use_smem) {
+    extern __shared__ double sm[];
+    double* X = use_smem ? sm : gwork;
+    __shared__ double cs_c[512], cs_s[512];
+    __shared__ int cs_p[512], cs_q[512];
+    __shared__ double nrm[512];
+    __shared__ int rank_of[512];
+    const int tid = threadIdx.x, nt = blockDim.x;
+    const int wid = tid / 32, lane = tid % 32, nw = nt / 32;
+    for (int e = tid; e < m * m; e += nt) X[e] = Xin[e];
+    __syncthreads();
+    const int mp = m + (m & 1);
+    const int npairs = mp / 2;
+    for (int sweep = 0; sweep < 60 && m > 1; ++sweep) {
+        int rotated = 0;
+        for (int r = 0; r < mp - 1; ++r) {
+            for (int k = wid; k < npairs; k += nw) {
+                int p, q;
+                rr_pair(k, r, mp, p, q);
+                double c = 1.0, s = 0.0;
+                if (q < m) {
+                    double al = 0.0, be = 0.0, ga = 0.0;
+                    for (int i = lane; i < m; i += 32) {
+                        const double xp = X[i + p * m], xq = X[i + q * m];
+                        al += xp * xp;
+                        be += xq * xq;
+                        ga += xp * xq;
+                    }
+                    al = warp_sum(al);
+                    be = warp_sum(be);
+                    ga = warp_sum(ga);
+                    if (ga != 0.0 && fabs(ga) > DBL_EPSILON * sqrt(al * be)) {
+                        const double zeta = (be - al) / (2.0 * ga);
+                        const double t =
+                            (zeta >= 0.0 ? 1.0 : -1.0) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
+                        c = 1.0 / sqrt(1.0 + t * t);
+                        s = t * c;
+                        rotated = 1;
+                    }
+                }
+                if (lane == 0) {
+                    cs_c[k] = c;
+                    cs_s[k] = s;
+                    cs_p[k] = p;
+                    cs_q[k] = q;
+                }
+            }
+            __syncthreads();
+            for (int e = tid; e < npairs * m; e += nt) {
+                const int k = e / m, i = e % m;
+                const double s = cs_s[k];
+                if (s == 0.0) continue;
+                const double c = cs_c[k];
+                const int p = cs_p[k], q = cs_q[k];
+                const double xp = X[i + p * m], xq = X[i + q * m];
+                X[i + p * m] = c * xp - s * xq;
+                X[i + q * m] = s * xp + c * xq;
+            }
+            __syncthreads();
+        }
+        if (!__syncthreads_or(rotated)) break;
+    }
+    for (int j = wid; j < m; j += nw) {
+        double a = 0.0;
+        for (int i = lane; i < m; i += 32) a += X[i + j * m] * X[i + j * m];
+        a = warp_sum(a);
+        if (lane == 0) nrm[j] = sqrt(a);
+    }
+    __syncthreads();
+    for (int i = tid; i < m; i += nt) {
+        int rk = 0;
+        for (int j = 0; j < m; ++j) rk += (nrm[j] > nrm[i]) || (nrm[j] == nrm[i] && j < i);
+        rank_of[i] = rk;
+        sigma[rk] = nrm[i];
+    }
+    __syncthreads();
+    for (int e = tid; e < m * m; e += nt) {
+        const int i = e % m, j = e / m;
+        const double sj = nrm[j];
+        U[i + rank_of[j] * m] = sj > 0.0 ? X[e] / sj : 0.0;
+    }
+}
+
+__global__ void small_gemm_kernel(bool ta, bool tb, int M, int N, int K, double alpha,
+                                  const double* __restrict__ A, int lda,
+                                  const double* __restrict__ B, int ldb, double beta,
+                                  double* __restrict__ C, int ldc) {
+    const int e = blockIdx.x * blockDim.x + threadIdx.x;
+    if (e >= M * N) return;
+    const int i = e % M, j = e / M;
+    double s = 0.0;
+    for (int k = 0; k < K; ++k) {
+        const double a = ta ? A[k + (size_t)i * lda] : A[i + (size_t)k * lda];
+        const double b = tb ? B[j + (size_t)k * ldb] : B[k + (size_t)j * ldb];
+        s += a * b;
+    }
+    C[i + (size_t)j * ldc] = alpha * s + (beta != 0.0 ? beta * C[i + (size_t)j * ldc] : 0.0);
+}
+
+__global__ void gather_cols_kernel(int64_t R, int r, const double* __restrict__ in, int64_t ldi,
+                                   const int* __restrict__ perm, double* __restrict__ out,
+                                   int64_t ldo) {
+    const int j = blockIdx.y;
+    const double* src = in + (int64_t)perm[j] * ldi;
+    double* dst = out + (int64_t)j * ldo;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < R;
+         i += (int64_t)gridDim.x * blockDim.x)
+        dst[i] = src[i];
+}
+
+size_t setup_smem(const void* kern, size_t bytes, int& use_smem) {
+    use_smem = bytes <= kSmemMax;
+    if (!use_smem) return 0;
+    if (bytes > 48 * 1024)
+        W4_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
+    return bytes;
+}
+
+}  // namespace
+
+void chol_upper(int m, const double* G, double* R, int* info, DevBuf& work, cudaStream_t st) {
+    int use = 0;
+    const size_t bytes = sizeof(double) * m * m;
+    const size_t sh = setup_smem(reinterpret_cast<const void*>(chol_kernel), bytes, use);
+    double* g = use ? nullptr : work.get<double>((size_t)m * m);
+    chol_kernel<<<1, kThreads, sh, st>>>(m, G, R, info, g, use);
+    W4_LAUNCH();
+}
+
+void pivoted_chol_rank(int m, const double* G, double tol_rel, int* rank, int* perm, DevBuf& work,
+                       cudaStream_t st) {
+    int use = 0;
+    const size_t bytes = sizeof(double) * m * m;
+    const size_t sh = setup_smem(reinterpret_cast<const void*>(pchol_kernel), bytes, use);
+    double* g = use ? nullptr : work.get<double>((size_t)m * m);
+    pchol_kernel<<<1, kThreads, sh, st>>>(m, G, tol_rel, rank, perm, g, use);
+    W4_LAUNCH();
+}
+
+void tri_inv_upper(int m, const double* R, double* Rinv, cudaStream_t st) {
+    const int warps = 8;
+    tri_inv_kernel<<<(unsigned)cdiv(m, warps), warps * 32, sizeof(double) * warps * m, st>>>(m, R,
+                                                                                           Rinv);
+    W4_LAUNCH();
+}
+
+void sym_evd_desc(int m, const double* K, double* vals, double* W, DevBuf& work,
+                  cudaStream_t st) {
+    require(m <= 512, "sym_evd_desc: m too large");
+    int use = 0;
+    const size_t bytes = sizeof(double) * 2 * m * m;
+    const size_t sh = setup_smem(reinterpret_cast<const void*>(jacobi_evd_kernel), bytes, use);
+    double* g = use ? nullptr : work.get<double>((size_t)2 * m * m);
+    jacobi_evd_kernel<<<1, kThreads, sh, st>>>(m, K, vals, W, g, use);
+    W4_LAUNCH();
+}
+
+void svd_left_desc(int m, const double* X, double* sigma, double* U, DevBuf& work,
+                   cudaStream_t st) {
+    require(m <= 512, "svd_left_desc: m too large");
+    int use = 0;
+    const size_t bytes = sizeof(double) * m * m;
+    const size_t sh = setup_smem(reinterpret_cast<const void*>(jacobi_svd_kernel), bytes, use);
+    double* g = use ? nullptr : work.get<double>((size_t)m * m);
+    jacobi_svd_kernel<<<1, kThreads, sh, st>>>(m, X, sigma, U, g, use);
+    W4_LAUNCH();
+}
+
+void small_gemm(bool ta, bool tb, int M, int N, int K, double alpha, const double* A, int lda,
+                const double* B, int ldb, double beta, double* C, int ldc, cudaStream_t st) {
+    if (M * N == 0) return;
+    small_gemm_kernel<<<(unsigned)cdiv((int64_t)M * N, 256), 256, 0, st>>>(
+        ta, tb, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc);
+    W4_LAUNCH();
+}
+
+void gather_cols(int64_t R, int r, const double* in, int64_t ldi, const int* perm, double* out,
+                 int64_t ldo, cudaStream_t st) {
+    if (r == 0 || R == 0) return;
+    dim3 grid((unsigned)std::min<int64_t>(cdiv(R, 256), 1024), (unsigned)r);
+    gather_cols_kernel<<<grid, 256, 0, st>>>(R, r, in, ldi, perm, out, ldo);
+    W4_LAUNCH();
+}
+
+}  // namespace w4

@@ -1,0 +1,51 @@
+// Batched tangent-linear / adjoint window sweeps (L^{-1}, L^{-T}) with the observation
+// operator fused in (HessianOperator::apply_Linv / apply_LinvT / observe / observe_adjoint,
+// operators.cpp:79-101, models.cpp:184-201).
+#pragma once
+
+#include "common.cuh"
+
+namespace w4 {
+
+struct ModelDev {
+    int kind = WC4DVAR_MODEL_IDENTITY;
+    int64_t n = 0;
+    int N = 0;
+    int s = 1;
+    double c = 0.0, d = 0.0, dt = 0.0;
+    const double* stages = nullptr;  // device, L96: (N*s) x 4n
+};
+
+struct NetDev {
+    int n_times = 0, n_points = 0;
+    int64_t q = 0;
+    const int* slot = nullptr;  // N+1: observation slot of time t, or -1
+    const int* pmap = nullptr;  // n: index of grid point j in points[], or -1
+};
+
+struct SweepArgs {
+    // forward sweep (x_0 = X_0, x_{i+1} = M_i x_i + X_{i+1})
+    const double* X = nullptr;
+    int64_t ldx = 0;
+    double* traj = nullptr;  // optional: every x_i
+    int64_t ldtraj = 0;
+    double* Y = nullptr;  // q x m obs (ld q): forward writes scale_fwd * H x, adjoint reads it
+    double scale_fwd = 1.0;
+    bool do_fwd = false;
+    bool fwd_obs = false;
+    // adjoint sweep (s_N = v_N + H_N^T y, s_i = v_i + H_i^T y + M_i^T s_{i+1})
+    const double* V = nullptr;  // optional addend v
+    int64_t ldv = 0;
+    double* S = nullptr;
+    int64_t lds = 0;
+    bool do_adj = false;
+    bool adj_obs = false;
+    int64_t m = 0;
+};
+
+// Max grid points handled by the resident (whole state in shared memory) sweep.
+int64_t sweep_resident_max_n();
+void sweep(const ModelDev& model, const NetDev& net, const SweepArgs& a, unsigned* status,
+           cudaStream_t stream);
+
+}  // namespace w4

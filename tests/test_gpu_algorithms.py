@@ -1,0 +1,216 @@
+"""GPU parity of REVD / Nystrom / ritzit, the spectral LMP and split PCG against the oracle,
+plus the reference's own sketch / LMP / PCG known-answer tests (test_randevd.cpp,
+test_lmp.cpp, test_krylov.cpp) on the device path.
+
+Tolerances (north star): Ritz values 1e-10 relative, PCG iteration counts within one,
+final residuals 1e-9 relative."""
+import numpy as np
+import pytest
+
+from oracle import oracle as O
+
+pytestmark = pytest.mark.gpu
+
+W = pytest.importorskip("paper_2101_07249_b200")
+from gpu_helpers import relerr, workload_pair  # noqa: E402
+from paper_2101_07249_b200 import configs  # noqa: E402
+
+METHODS = ("revd", "nystrom", "ritzit")
+
+
+def head_tail():
+    d = np.ones(100)
+    d[:10] = 10.0 - np.arange(10)
+    return np.diag(d)
+
+
+# ---------------------------------------------------------------- sketches vs oracle
+@pytest.mark.parametrize("method", METHODS)
+def test_sketch_dense_vs_oracle(method):
+    A = O.random_spd(np.concatenate([np.linspace(50, 5, 12), np.linspace(2, 1, 88)]), 5)
+    g, o = W.DenseOperator(A), O.DenseOperator(A)
+    for seed in (1, 2, 3):
+        pg = W.sketch_eigenpairs(g, W.SketchConfig(8, 6, seed, method))
+        po = O.sketch_eigenpairs(o, O.SketchConfig(8, 6, seed, method))
+        assert pg.k() == po.k()
+        assert relerr(pg.values, po.values) <= 1e-10
+        pg.validate(1e-10)
+        # projectors agree (vectors up to sign / rotation in clusters)
+        assert np.abs(pg.vectors @ pg.vectors.T - po.vectors @ po.vectors.T).max() <= 1e-8
+
+
+@pytest.mark.parametrize("method", METHODS)
+@pytest.mark.parametrize("wl", [configs.small_advdiff(), configs.config1()], ids=lambda w: w.name)
+def test_sketch_hessian_vs_oracle(method, wl):
+    g, o = workload_pair(wl)
+    cfg = dict(target_rank=wl.k, oversample=wl.m - wl.k, seed=configs.OMEGA_SEED, method=method,
+               p_iter=wl.p_iter if method == "ritzit" else 1)
+    pg = W.sketch_eigenpairs(g, W.SketchConfig(**cfg))
+    po = O.sketch_eigenpairs(o, O.SketchConfig(**cfg))
+    assert pg.k() == po.k()
+    assert relerr(pg.values, po.values) <= 1e-10, (pg.values[:4], po.values[:4])
+    pg.validate(1e-10)
+
+
+def test_sketch_known_answers():  # test_randevd.cpp:82-251
+    op = W.DenseOperator(np.eye(60))
+    for m in METHODS:
+        pr = W.sketch_eigenpairs(op, W.SketchConfig(4, 3, 12345, m))
+        assert pr.k() == 4 and np.abs(pr.values - 1).max() <= 1e-12
+        pr.validate(1e-10)
+    A = head_tail()
+    op = W.DenseOperator(A)
+    target = np.array([10.0, 9, 8, 7, 6])
+    mr, mn, mz = np.zeros(5), np.zeros(5), np.zeros(5)
+    for seed in range(1, 21):
+        cfg = W.SketchConfig(5, 5, seed)
+        r, n, z = W.revd(op, cfg), W.nystrom(op, cfg), W.revd_ritzit(op, cfg)
+        for v in (r.values, n.values, z.values):
+            assert (v <= target + 1e-10).all()
+        mr += r.values / target / 20
+        mn += n.values / target / 20
+        mz += z.values / target / 20
+    assert (mr >= 0.65).all() and (mn >= mr).all() and (mz <= mn).all() and (mz <= mr).all()
+    # exactly low rank: Nystrom caps at the detected rank (randevd.cpp:89-92,108)
+    B = O.NormalStream(17).fill(40, 3)
+    A = 0.5 * (B @ B.T + (B @ B.T).T)
+    pr = W.nystrom(W.DenseOperator(A), W.SketchConfig(5, 2, 4))
+    assert pr.k() == 3
+    assert np.linalg.norm(A - pr.vectors @ np.diag(pr.values) @ pr.vectors.T) <= 1e-10 * np.linalg.norm(A)
+    B = O.NormalStream(29).fill(30, 1)
+    with pytest.raises(W.NumericalError, match="rank collapsed"):
+        W.revd(W.DenseOperator(B @ B.T), W.SketchConfig(3, 2, 3))
+    with pytest.raises(ValueError):
+        W.revd(W.DenseOperator(np.eye(6)), W.SketchConfig(5, 5, 0))
+    with pytest.raises(ValueError):
+        W.revd(W.DenseOperator(np.eye(6)), W.SketchConfig(0, 5, 0))
+    op = W.DenseOperator(head_tail())
+    for m, cnt in (("revd", 20), ("nystrom", 20), ("ritzit", 10)):
+        op.reset_apply_count()
+        W.sketch_eigenpairs(op, W.SketchConfig(7, 3, 5, m))
+        assert op.apply_count() == cnt
+    for m in METHODS:
+        a = W.sketch_eigenpairs(op, W.SketchConfig(6, 4, 31, m))
+        b = W.sketch_eigenpairs(op, W.SketchConfig(6, 4, 31, m))
+        assert np.array_equal(a.values, b.values) and np.array_equal(a.vectors, b.vectors)
+
+
+def test_rayleigh_ritz():  # test_randevd.cpp:40-80
+    eigs = np.linspace(1, 30, 30)
+    V = O.random_orthogonal(30, 3)
+    A = V @ np.diag(eigs) @ V.T
+    pr = W.rayleigh_ritz(W.DenseOperator(0.5 * (A + A.T)), V[:, [29, 25, 20]])
+    np.testing.assert_allclose(pr.values, [30, 26, 21], rtol=1e-10)
+    Z = np.zeros((10, 2))
+    Z[0, :] = 1.0
+    with pytest.raises(W.NumericalError):
+        W.rayleigh_ritz(W.DenseOperator(np.eye(10)), Z)
+
+
+# ---------------------------------------------------------------- LMP
+def test_lmp_vs_oracle_and_algebra():  # test_lmp.cpp:34-110,209-224
+    Q = O.random_orthogonal(14, 17)
+    th = np.array([30.0, 11, 5, 2, 1.3])
+    fg = W.build_spectral_lmp(W.RitzPairs(Q[:, :5], th))
+    fo = O.build_spectral_lmp(O.RitzPairs(Q[:, :5], th))
+    s = O.NormalStream(19)
+    for _ in range(5):
+        v = s.draw(14)
+        assert np.abs(fg.apply(v) - fo.apply(v)).max() <= 1e-14
+        assert np.abs(fg.apply_transpose(v) - fo.apply_transpose(v)).max() <= 1e-14
+    # non-orthonormal U: compact WY still equals the sequential rank-1 product exactly
+    U = O.random_orthogonal(20, 2)[:, :4] + 1e-9 * O.NormalStream(3).fill(20, 4)
+    th = np.array([9.0, 4.0, 2.0, 1.5])
+    fg = W.build_spectral_lmp(W.RitzPairs(U, th))
+    fo = O.LmpFactor(U, th)
+    v = O.NormalStream(4).draw(20)
+    assert np.abs(fg.apply(v) - fo.apply(v)).max() <= 1e-14
+    assert np.abs(fg.apply_transpose(v) - fo.apply_transpose(v)).max() <= 1e-14
+    A = O.random_spd(np.linspace(0.5, 20, 10), 11)
+    w, V = np.linalg.eigh(A)
+    f = W.build_spectral_lmp(W.RitzPairs(V[:, ::-1].copy(), w[::-1].copy()))
+    P = np.column_stack([f.apply(f.apply_transpose(e)) for e in np.eye(10)])
+    assert np.linalg.norm(P - np.linalg.inv(A)) <= 1e-9 * np.linalg.norm(np.linalg.inv(A))
+    with pytest.raises(W.NumericalError, match="nonpositive"):
+        W.build_spectral_lmp(W.RitzPairs(O.random_orthogonal(6, 83)[:, :2], np.array([2.0, -0.1])))
+    with pytest.raises(W.NumericalError, match="not orthonormal"):
+        W.build_spectral_lmp(W.RitzPairs(np.ones((6, 2)), np.array([2.0, 1.5])))
+    assert W.build_spectral_lmp(W.RitzPairs(O.random_orthogonal(6, 89)[:, :2], np.array([2.0, 0.7]))).k() == 2
+    idf = W.LmpFactor.identity(12)
+    v = O.NormalStream(1).draw(12)
+    assert np.array_equal(idf.apply(v), v)
+
+
+# ---------------------------------------------------------------- PCG
+def test_pcg_known_answers():  # test_krylov.cpp:31-151
+    b = O.NormalStream(1).draw(9)
+    r = W.pcg_split(W.DenseOperator(np.eye(9)), b, opts=W.PcgOptions(rel_tol=1e-12))
+    assert r.history.iterations == 1 and r.history.converged and np.abs(r.x - b).max() <= 1e-13
+    A = np.diag(np.arange(1.0, 11.0))
+    w, V = np.linalg.eigh(A)
+    f = W.build_spectral_lmp(W.RitzPairs(V[:, ::-1].copy(), w[::-1].copy()))
+    r = W.pcg_split(W.DenseOperator(A), O.NormalStream(2).draw(10), f, opts=W.PcgOptions(rel_tol=1e-10))
+    assert r.history.iterations == 1 and r.history.converged
+    A = O.random_spd(np.linspace(0.5, 60, 200), 11)
+    b = O.NormalStream(3).draw(200)
+    r = W.pcg_split(W.DenseOperator(A), b, opts=W.PcgOptions(max_iter=2000, rel_tol=1e-10))
+    d = np.linalg.solve(A, b)
+    assert r.history.converged and np.linalg.norm(r.x - d) <= 1e-8 * np.linalg.norm(d)
+    with pytest.raises(W.NumericalError, match="positive definiteness"):
+        W.pcg_split(W.DenseOperator(-np.eye(5)), O.NormalStream(4).draw(5))
+    A = O.random_spd(np.linspace(1, 9, 30), 51)
+    op = W.DenseOperator(A)
+    b = O.NormalStream(8).draw(30)
+    op.reset_apply_count()
+    r = W.pcg_split(op, b, opts=W.PcgOptions(max_iter=12, rel_tol=1e-15))
+    assert op.apply_count() == r.history.iterations
+    op.reset_apply_count()
+    r2 = W.pcg_split(op, b, W.LmpFactor.identity(30), O.NormalStream(9).draw(30),
+                     W.PcgOptions(max_iter=12, rel_tol=1e-15))
+    assert op.apply_count() == r2.history.iterations + 1
+    # k = 0 factor leaves PCG bitwise unchanged (test_lmp.cpp:34-51)
+    A = O.random_spd(np.linspace(1, 7, 12), 3)
+    b = O.NormalStream(1).draw(12)
+    p1 = W.pcg_split(W.DenseOperator(A), b, opts=W.PcgOptions(max_iter=12, rel_tol=1e-12))
+    p2 = W.pcg_split(W.DenseOperator(A), b, W.LmpFactor.identity(12), opts=W.PcgOptions(max_iter=12, rel_tol=1e-12))
+    assert np.array_equal(p1.x, p2.x) and p1.history.residual_norms == p2.history.residual_norms
+
+
+@pytest.mark.parametrize("reorth", [False, True])
+def test_pcg_dense_vs_oracle(reorth):
+    A = O.random_spd(np.linspace(1, 80, 60), 31)
+    b = O.NormalStream(6).draw(60)
+    o = O.pcg_split(O.DenseOperator(A), b, opts=O.PcgOptions(max_iter=60, rel_tol=1e-12, reorthogonalize=reorth))
+    g = W.pcg_split(W.DenseOperator(A), b, opts=W.PcgOptions(max_iter=60, rel_tol=1e-12, reorthogonalize=reorth))
+    assert abs(g.history.iterations - o.history.iterations) <= 1
+    assert relerr(g.x, o.x) <= 1e-9
+
+
+@pytest.mark.parametrize("method", ("none",) + METHODS)
+@pytest.mark.parametrize("wl", [configs.small_advdiff(), configs.config1()], ids=lambda w: w.name)
+def test_inner_loop_vs_oracle(method, wl):
+    """sketch -> LMP -> PCG on the Hessian, with the recorded quadratic cost (the
+    run_inner_loop pipeline, assimilation.cpp:192-253), against the oracle."""
+    g, o = workload_pair(wl)
+    n = g.dim()
+    rhs = O.NormalStream(configs.RHS_SEED).draw(n)
+    d = O.NormalStream(11).draw(wl.net.q)
+    if method == "none":
+        fg, fo = None, None
+    else:
+        cfg = dict(target_rank=wl.k, oversample=wl.m - wl.k, seed=configs.OMEGA_SEED, method=method,
+                   p_iter=wl.p_iter if method == "ritzit" else 1)
+        pg = W.sketch_eigenpairs(g, W.SketchConfig(**cfg))
+        po = O.sketch_eigenpairs(o, O.SketchConfig(**cfg))
+        fg, fo = W.build_spectral_lmp(pg), O.build_spectral_lmp(po)
+    cg, co = W.QuadraticCost(g, rhs, d), O.QuadraticCost(o, rhs, d)
+    assert relerr(cg.rhs(), co.rhs()) <= 1e-12
+    b = co.rhs()
+    rg = W.pcg_split(g, b, fg, opts=W.PcgOptions(max_iter=200, rel_tol=1e-6, cost=cg))
+    ro = O.pcg_split(o, b, fo, opts=O.PcgOptions(max_iter=200, rel_tol=1e-6, cost_eval=co))
+    assert rg.history.converged and ro.history.converged
+    assert abs(rg.history.iterations - ro.history.iterations) <= 1
+    it = min(rg.history.iterations, ro.history.iterations)
+    assert relerr(rg.history.residual_norms[:it + 1], ro.history.residual_norms[:it + 1]) <= 1e-9
+    assert relerr(rg.x, ro.x) <= 1e-9
+    assert relerr(rg.history.quadratic_costs[:it + 1], ro.history.quadratic_costs[:it + 1]) <= 1e-9
