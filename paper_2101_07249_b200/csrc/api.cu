@@ -139,6 +139,19 @@ int wc4dvar_gpu_hessian_create(const wc4dvar_model_desc* model, const wc4dvar_ne
     h->nd.slot = h->d_slot;
     h->nd.pmap = h->d_pmap;
     const size_t fsz = (size_t)n * n;
+    // sym_sqrt symmetrises its factors exactly (covariance.cpp:101-102); when a factor is
+    // bitwise symmetric the D^{1/2} GEMM may read its columns as rows.
+    auto is_sym = [n](const double* F) {
+        if (!F) return false;
+        for (int64_t j = 0; j < n; ++j)
+            for (int64_t i = j + 1; i < n; ++i)
+                if (F[i + j * n] != F[j + i * n]) return false;
+        return true;
+    };
+    h->sym[0] = is_sym(bh->half);
+    h->sym[1] = is_sym(qh->half);
+    h->sym[2] = is_sym(bh->half_inv);
+    h->sym[3] = is_sym(qh->half_inv);
     h->b_half = dev_upload(bh->half, fsz, st);
     h->q_half = dev_upload(qh->half, fsz, st);
     if (bh->half_inv) h->b_half_inv = dev_upload(bh->half_inv, fsz, st);

@@ -9,6 +9,12 @@ namespace {
 
 constexpr int BK = 16;
 constexpr int KPAD = BK + 4;  // [col][k] tiles: stride 20 doubles -> conflict-free fragments
+// [col][k] tiles read with LDS.128 under the permuted k order (see gemm_sym_kernel):
+// stride 24 doubles keeps 16-byte fragment loads bank-conflict free.
+constexpr int KS = BK + 8;
+// Every DMMA kernel feeds the MMA's logical k = t0 with physical k = 2 t0 and logical
+// k = t0 + 4 with physical 2 t0 + 1, so all kernels accumulate each output element in the
+// same order (block apply == column-wise apply bitwise, whichever tile shape runs).
 
 __device__ __forceinline__ void cp_async16(void* smem, const void* gmem, int src_bytes) {
     unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
@@ -33,6 +39,28 @@ __device__ __forceinline__ void dmma16x8x8(double (&d)[4], const double (&a)[4],
         "{%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, {%0,%1,%2,%3};\n"
         : "+d"(d[0]), "+d"(d[1]), "+d"(d[2]), "+d"(d[3])
         : "d"(a[0]), "d"(a[1]), "d"(a[2]), "d"(a[3]), "d"(b[0]), "d"(b[1]));
+}
+
+__device__ __forceinline__ void dmma16x8x4(double (&d)[4], double a0, double a1, double b0) {
+    asm volatile(
+        "mma.sync.aligned.m16n8k4.row.col.f64.f64.f64.f64 "
+        "{%0,%1,%2,%3}, {%4,%5}, {%6}, {%0,%1,%2,%3};\n"
+        : "+d"(d[0]), "+d"(d[1]), "+d"(d[2]), "+d"(d[3])
+        : "d"(a0), "d"(a1), "d"(b0));
+}
+
+// One k8 step of a warp tile as two m16n8k4 sweeps (physical k = 2 t0, then 2 t0 + 1):
+// consecutive MMAs are independent, so no DMMA waits on the one just issued, and every
+// element accumulates in the same order as the m16n8k8 form.
+template <int MI, int NI>
+__device__ __forceinline__ void mma_k8(double (&acc)[MI][NI][4], const double (&af)[MI][4],
+                                       const double (&bf)[NI][2]) {
+#pragma unroll
+    for (int h = 0; h < 2; ++h)
+#pragma unroll
+        for (int i = 0; i < MI; ++i)
+#pragma unroll
+            for (int j = 0; j < NI; ++j) dmma16x8x4(acc[i][j], af[i][2 * h], af[i][2 * h + 1], bf[j][h]);
 }
 
 template <int VEC>
@@ -73,8 +101,8 @@ __global__ void __launch_bounds__(WM * WN * 32)
     constexpr int NT = WM * WN * 32;
     constexpr int WTM = BM / WM, WTN = BN / WN;
     constexpr int MI = WTM / 16, NI = WTN / 8;
-    constexpr int APAD = BM + 4;
-    constexpr int A_ELEMS = BK * APAD, B_ELEMS = BN * KPAD;
+    constexpr int APAD = BM + 2;  // rows 2t0 apart by 2*APAD == 4 (mod 16): conflict-free
+    constexpr int A_ELEMS = BK * APAD, B_ELEMS = BN * KS;
     extern __shared__ __align__(16) double smem[];
     double* As = smem;
     double* Bs = smem + STAGES * A_ELEMS;
@@ -133,7 +161,7 @@ __global__ void __launch_bounds__(WM * WN * 32)
                 valid = rem >= VEC ? VEC : (rem > 0 ? (int)rem : 0);
                 src = P.in.col(c) + kr;
             }
-            cp_async_vec<VEC>(bs + nn * KPAD + kk, src, valid, P.A);
+            cp_async_vec<VEC>(bs + nn * KS + kk, src, valid, P.A);
         }
     };
 
@@ -159,21 +187,19 @@ __global__ void __launch_bounds__(WM * WN * 32)
 #pragma unroll
             for (int i = 0; i < MI; ++i) {
                 const int r = wm * WTM + i * 16 + g;
-                af[i][0] = as[(k8 + t0) * APAD + r];
-                af[i][1] = as[(k8 + t0) * APAD + r + 8];
-                af[i][2] = as[(k8 + t0 + 4) * APAD + r];
-                af[i][3] = as[(k8 + t0 + 4) * APAD + r + 8];
+                af[i][0] = as[(k8 + 2 * t0) * APAD + r];
+                af[i][1] = as[(k8 + 2 * t0) * APAD + r + 8];
+                af[i][2] = as[(k8 + 2 * t0 + 1) * APAD + r];
+                af[i][3] = as[(k8 + 2 * t0 + 1) * APAD + r + 8];
             }
 #pragma unroll
             for (int j = 0; j < NI; ++j) {
                 const int c = wn * WTN + j * 8 + g;
-                bf[j][0] = bs[c * KPAD + k8 + t0];
-                bf[j][1] = bs[c * KPAD + k8 + t0 + 4];
+                const double2 bb = *reinterpret_cast<const double2*>(bs + c * KS + k8 + 2 * t0);
+                bf[j][0] = bb.x;
+                bf[j][1] = bb.y;
             }
-#pragma unroll
-            for (int i = 0; i < MI; ++i)
-#pragma unroll
-                for (int j = 0; j < NI; ++j) dmma16x8x8(acc[i][j], af[i], bf[j]);
+            mma_k8(acc, af, bf);
         }
     }
     cp_wait<0>();
@@ -207,8 +233,8 @@ __global__ void __launch_bounds__(WM * WN * 32)
 
 template <int BM, int BN, int WM, int WN, int STAGES, int VEC>
 void launch_nn(const PassTable& tab, int64_t ntiles, unsigned* status, cudaStream_t stream) {
-    constexpr int APAD = BM + 4;
-    const size_t smem = sizeof(double) * STAGES * (BK * APAD + BN * KPAD);
+    constexpr int APAD = BM + 2;
+    const size_t smem = sizeof(double) * STAGES * (BK * APAD + BN * KS);
     auto kern = gemm_nn_kernel<BM, BN, WM, WN, STAGES, VEC>;
     configure_smem(reinterpret_cast<const void*>(kern), smem);
     kern<<<(unsigned)ntiles, WM * WN * 32, smem, stream>>>(tab, status);
@@ -216,6 +242,160 @@ void launch_nn(const PassTable& tab, int64_t ntiles, unsigned* status, cudaStrea
 }
 
 bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
+
+// ---------------------------------------------------------------------------
+// Symmetric-A kernel (the D^{1/2} factors): because A = A^T, the A tile can be loaded as
+// [m][k] rows straight from A's columns, so BOTH operands sit k-contiguous in SMEM.  The
+// MMA's logical k index is permuted (logical t0 <-> physical 2 t0, logical t0+4 <->
+// physical 2 t0 + 1) so each thread's (a0,a2), (a1,a3) and (b0,b1) fragment pairs are
+// adjacent doubles: one LDS.128 each.  Row stride 24 doubles keeps the 16-byte loads
+// bank-conflict free.  Warp tile 64 x 32 (16 MMAs per k8 per warp).
+// ---------------------------------------------------------------------------
+template <int BM, int BN, int WM, int WN, int STAGES>
+__global__ void __launch_bounds__(WM * WN * 32, 1)
+    gemm_sym_kernel(const PassTable tab, unsigned* __restrict__ status) {
+    constexpr int NT = WM * WN * 32;
+    constexpr int WTM = BM / WM, WTN = BN / WN;
+    constexpr int MI = WTM / 16, NI = WTN / 8;
+    constexpr int A_ELEMS = BM * KS, B_ELEMS = BN * KS;
+    extern __shared__ __align__(16) double smem[];
+    double* As = smem;
+    double* Bs = smem + STAGES * A_ELEMS;
+
+    int64_t tile = blockIdx.x;
+    const int pi = tile >= tab.tile_start[1] ? 1 : 0;
+    const GemmPass& P = tab.p[pi];
+    tile -= tab.tile_start[pi];
+    const int64_t tm = tile % tab.tiles_m[pi];
+    const int64_t tn = tile / tab.tiles_m[pi];
+    const int64_t m0 = tm * BM, n0 = tn * BN;
+    const int64_t M = P.M, K = P.K, ncols = P.ncols;
+
+    const int tid = threadIdx.x;
+    const int warp = tid >> 5, lane = tid & 31;
+    const int wm = warp % WM, wn = warp / WM;
+    const int g = lane >> 2, t0 = lane & 3;
+
+    double acc[MI][NI][4];
+#pragma unroll
+    for (int i = 0; i < MI; ++i)
+#pragma unroll
+        for (int j = 0; j < NI; ++j)
+#pragma unroll
+            for (int v = 0; v < 4; ++v) acc[i][j][v] = 0.0;
+
+    const int64_t ktiles = (K + BK - 1) / BK;
+    auto load_stage = [&](int stage, int64_t kt) {
+        const int64_t k0 = kt * BK;
+        double* as = As + stage * A_ELEMS;
+        double* bs = Bs + stage * B_ELEMS;
+        constexpr int ACH = BM * BK / 2;
+#pragma unroll
+        for (int ch = tid; ch < ACH; ch += NT) {
+            const int mm = ch / (BK / 2);
+            const int kk = (ch % (BK / 2)) * 2;
+            const int64_t row = m0 + mm, kr = k0 + kk;
+            int valid = 0;
+            const double* src = P.A;
+            if (row < M) {
+                const int64_t rem = K - kr;
+                valid = rem >= 2 ? 2 : (rem > 0 ? (int)rem : 0);
+                src = P.A + row * P.lda + kr;  // column `row` of A == row `row` (symmetric)
+            }
+            cp_async_vec<2>(as + mm * KS + kk, src, valid, P.A);
+        }
+        constexpr int BCH = BN * BK / 2;
+#pragma unroll
+        for (int ch = tid; ch < BCH; ch += NT) {
+            const int nn = ch / (BK / 2);
+            const int kk = (ch % (BK / 2)) * 2;
+            const int64_t c = n0 + nn, kr = k0 + kk;
+            int valid = 0;
+            const double* src = P.A;
+            if (c < ncols) {
+                const int64_t rem = K - kr;
+                valid = rem >= 2 ? 2 : (rem > 0 ? (int)rem : 0);
+                src = P.in.col(c) + kr;
+            }
+            cp_async_vec<2>(bs + nn * KS + kk, src, valid, P.A);
+        }
+    };
+
+#pragma unroll
+    for (int s = 0; s < STAGES - 1; ++s) {
+        if (s < ktiles) load_stage(s, s);
+        cp_commit();
+    }
+    for (int64_t kt = 0; kt < ktiles; ++kt) {
+        cp_wait<STAGES - 2>();
+        __syncthreads();
+        {
+            const int64_t nk = kt + STAGES - 1;
+            if (nk < ktiles) load_stage((int)(nk % STAGES), nk);
+            cp_commit();
+        }
+        const double* as = As + (kt % STAGES) * A_ELEMS;
+        const double* bs = Bs + (kt % STAGES) * B_ELEMS;
+#pragma unroll
+        for (int k8 = 0; k8 < BK; k8 += 8) {
+            double af[MI][4], bf[NI][2];
+#pragma unroll
+            for (int i = 0; i < MI; ++i) {
+                const int r = wm * WTM + i * 16 + g;
+                const double2 lo = *reinterpret_cast<const double2*>(as + r * KS + k8 + 2 * t0);
+                const double2 hi = *reinterpret_cast<const double2*>(as + (r + 8) * KS + k8 + 2 * t0);
+                af[i][0] = lo.x;
+                af[i][2] = lo.y;
+                af[i][1] = hi.x;
+                af[i][3] = hi.y;
+            }
+#pragma unroll
+            for (int j = 0; j < NI; ++j) {
+                const int c = wn * WTN + j * 8 + g;
+                const double2 bb = *reinterpret_cast<const double2*>(bs + c * KS + k8 + 2 * t0);
+                bf[j][0] = bb.x;
+                bf[j][1] = bb.y;
+            }
+            mma_k8(acc, af, bf);
+        }
+    }
+    cp_wait<0>();
+
+    bool bad = false;
+    const double alpha = P.alpha;
+#pragma unroll
+    for (int j = 0; j < NI; ++j) {
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            const int64_t c = n0 + wn * WTN + j * 8 + 2 * t0 + h;
+            if (c >= ncols) continue;
+            double* outc = const_cast<double*>(P.out.col(c));
+            const double* addc = P.add.base ? P.add.col(c) : nullptr;
+#pragma unroll
+            for (int i = 0; i < MI; ++i) {
+#pragma unroll
+                for (int v = 0; v < 2; ++v) {
+                    const int64_t r = m0 + wm * WTM + i * 16 + g + 8 * v;
+                    if (r >= M) continue;
+                    double val = alpha * acc[i][j][2 * v + h];
+                    if (addc) val = addc[r] + val;
+                    bad |= !isfinite(val);
+                    outc[r] = val;
+                }
+            }
+        }
+    }
+    if (status && __any_sync(0xffffffffu, bad) && lane == 0) atomicOr(status, ST_OUT_NONFINITE);
+}
+
+template <int BM, int BN, int WM, int WN, int STAGES>
+void launch_sym(const PassTable& tab, int64_t ntiles, unsigned* status, cudaStream_t stream) {
+    const size_t smem = sizeof(double) * STAGES * (BM * KS + BN * KS);
+    auto kern = gemm_sym_kernel<BM, BN, WM, WN, STAGES>;
+    configure_smem(reinterpret_cast<const void*>(kern), smem);
+    kern<<<(unsigned)ntiles, WM * WN * 32, smem, stream>>>(tab, status);
+    W4_LAUNCH();
+}
 
 // ---------------------------------------------------------------------------
 // TN split kernel: both tiles stored [col][k] (stride KPAD).
@@ -229,7 +409,7 @@ __global__ void __launch_bounds__(WM * WN * 32)
     constexpr int NT = WM * WN * 32;
     constexpr int WTM = BM / WM, WTN = BN / WN;
     constexpr int MI = WTM / 16, NI = WTN / 8;
-    constexpr int A_ELEMS = BM * KPAD, B_ELEMS = BN * KPAD;
+    constexpr int A_ELEMS = BM * KS, B_ELEMS = BN * KS;
     extern __shared__ __align__(16) double smem[];
     double* As = smem;
     double* Bs = smem + STAGES * A_ELEMS;
@@ -273,7 +453,7 @@ __global__ void __launch_bounds__(WM * WN * 32)
                 valid = rem >= VEC ? VEC : (rem > 0 ? (int)rem : 0);
                 src = A + c * lda + kr;
             }
-            cp_async_vec<VEC>(as + ii * KPAD + kk, src, valid, A);
+            cp_async_vec<VEC>(as + ii * KS + kk, src, valid, A);
         }
         constexpr int BCH = BN * BK / VEC;
 #pragma unroll
@@ -288,7 +468,7 @@ __global__ void __launch_bounds__(WM * WN * 32)
                 valid = rem >= VEC ? VEC : (rem > 0 ? (int)rem : 0);
                 src = B + c * ldb + kr;
             }
-            cp_async_vec<VEC>(bs + jj * KPAD + kk, src, valid, B);
+            cp_async_vec<VEC>(bs + jj * KS + kk, src, valid, B);
         }
     };
 
@@ -313,21 +493,21 @@ __global__ void __launch_bounds__(WM * WN * 32)
 #pragma unroll
             for (int i = 0; i < MI; ++i) {
                 const int r = wm * WTM + i * 16 + g;
-                af[i][0] = as[r * KPAD + k8 + t0];
-                af[i][1] = as[(r + 8) * KPAD + k8 + t0];
-                af[i][2] = as[r * KPAD + k8 + t0 + 4];
-                af[i][3] = as[(r + 8) * KPAD + k8 + t0 + 4];
+                const double2 lo = *reinterpret_cast<const double2*>(as + r * KS + k8 + 2 * t0);
+                const double2 hi = *reinterpret_cast<const double2*>(as + (r + 8) * KS + k8 + 2 * t0);
+                af[i][0] = lo.x;
+                af[i][2] = lo.y;
+                af[i][1] = hi.x;
+                af[i][3] = hi.y;
             }
 #pragma unroll
             for (int j = 0; j < NI; ++j) {
                 const int c = wn * WTN + j * 8 + g;
-                bf[j][0] = bs[c * KPAD + k8 + t0];
-                bf[j][1] = bs[c * KPAD + k8 + t0 + 4];
+                const double2 bb = *reinterpret_cast<const double2*>(bs + c * KS + k8 + 2 * t0);
+                bf[j][0] = bb.x;
+                bf[j][1] = bb.y;
             }
-#pragma unroll
-            for (int i = 0; i < MI; ++i)
-#pragma unroll
-                for (int j = 0; j < NI; ++j) dmma16x8x8(acc[i][j], af[i], bf[j]);
+            mma_k8(acc, af, bf);
         }
     }
     cp_wait<0>();
@@ -364,7 +544,7 @@ template <int BM, int BN, int WM, int WN, int STAGES, int VEC>
 void launch_tn(int64_t R, int64_t m1, int64_t m2, const double* A, int64_t lda, const double* B,
                int64_t ldb, double* work, int64_t rows_per_split, int64_t nsplit,
                cudaStream_t stream) {
-    const size_t smem = sizeof(double) * STAGES * (BM * KPAD + BN * KPAD);
+    const size_t smem = sizeof(double) * STAGES * (BM * KS + BN * KS);
     auto kern = gemm_tn_kernel<BM, BN, WM, WN, STAGES, VEC>;
     configure_smem(reinterpret_cast<const void*>(kern), smem);
     const int64_t tm = cdiv(m1, BM), tn = cdiv(m2, BN);
@@ -388,6 +568,23 @@ void gemm_nn(const GemmPass* passes, int npass, unsigned* status, cudaStream_t s
                (p.in.ld_outer % 2 == 0) && (p.in.stride % 2 == 0);
     }
     for (int i = npass; i < 2; ++i) tab.p[i] = GemmPass{};
+    bool sym = vec2;
+    for (int i = 0; i < npass; ++i) sym = sym && passes[i].symA && passes[i].M == passes[i].K;
+    if (sym && cdiv(maxM, 128) * cdiv(total_cols, 128) >= kSMs) {
+        int64_t start = 0;
+        for (int i = 0; i < 2; ++i) {
+            tab.tile_start[i] = start;
+            if (i < npass && passes[i].ncols > 0 && passes[i].M > 0) {
+                tab.tiles_m[i] = cdiv(passes[i].M, 128);
+                start += tab.tiles_m[i] * cdiv(passes[i].ncols, 128);
+            } else {
+                tab.tiles_m[i] = 1;
+            }
+        }
+        tab.tile_start[2] = start;
+        if (start > 0) launch_sym<128, 128, 4, 4, 3>(tab, start, status, stream);
+        return;
+    }
     // Tile shape: big tiles when there are enough of them to fill the chip twice.
     const bool big = cdiv(maxM, 128) * cdiv(total_cols, 64) >= 2 * kSMs;
     const int BMv = big ? 128 : 64, BNv = big ? 64 : 32;

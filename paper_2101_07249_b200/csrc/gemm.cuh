@@ -44,6 +44,7 @@ struct GemmPass {
     ColMap in;    // K-long columns
     ColMap out;   // M-long columns
     ColMap add;   // optional addend (base == nullptr: none)
+    bool symA = false;  // A == A^T bitwise (enables the k-contiguous LDS.128 kernel)
 };
 
 // Launch one or two passes in a single kernel.  status (optional) gets

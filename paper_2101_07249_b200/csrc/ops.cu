@@ -99,6 +99,7 @@ void HessianOp::d_half(bool inv, const double* V, int64_t ldv, int64_t m, double
         p.in = ColMap{V, ldv, n, N, 1};
         p.out = ColMap{out, ldo, n, N, 1};
         if (add) p.add = ColMap{add, ldadd, n, N, 1};
+        p.symA = sym[inv ? 3 : 1];
     }
     {
         GemmPass& p = ps[np++];
@@ -110,6 +111,7 @@ void HessianOp::d_half(bool inv, const double* V, int64_t ldv, int64_t m, double
         p.in = ColMap{V, ldv, n, 1, 0};
         p.out = ColMap{out, ldo, n, 1, 0};
         if (add) p.add = ColMap{add, ldadd, n, 1, 0};
+        p.symA = sym[inv ? 2 : 0];
     }
     gemm_nn(ps, np, status, st);
 }

@@ -60,6 +60,7 @@ struct HessianOp final : wc4dvar_op {
     double* b_half_inv = nullptr;
     double* q_half = nullptr;
     double* q_half_inv = nullptr;
+    bool sym[4] = {false, false, false, false};  // b_half, q_half, b_half_inv, q_half_inv == ^T
     int* d_slot = nullptr;
     int* d_pmap = nullptr;
     double* d_stages = nullptr;

@@ -253,6 +253,100 @@ __global__ void __launch_bounds__(kThreads)
     }
 }
 
+// ---------------------------------------------------------------- two-sided Jacobi EVD, 2x2 blocks
+// Parallel cyclic Jacobi (round-robin pairs).  All m/2 rotations of a round act on
+// disjoint index pairs, so A' = J^T A J factors into independent 2x2 blocks
+// A'_{PQ} = J_P^T A_{PQ} J_Q: each thread reads, rotates and writes whole blocks, and a
+// round costs two barriers (rotation parameters, block update) instead of three.  The
+// matrix is padded to even order with a zero row/column that no rotation ever touches.
+constexpr int kEvdThreads = 512;
+
+__global__ void __launch_bounds__(kEvdThreads)
+    jacobi_evd_blk_kernel(int m, const double* __restrict__ K, double* __restrict__ vals,
+                          double* __restrict__ W, double* gwork, int use_smem) {
+    extern __shared__ double sm[];
+    const int mp = m + (m & 1);
+    double* A = use_smem ? sm : gwork;
+    double* V = A + (size_t)mp * mp;
+    __shared__ double cs_c[256], cs_s[256];
+    __shared__ int cs_p[256], cs_q[256];
+    __shared__ int rank_of[512];
+    const int tid = threadIdx.x, nt = blockDim.x;
+    for (int e = tid; e < mp * mp; e += nt) {
+        const int i = e % mp, j = e / mp;
+        A[e] = (i < m && j < m) ? 0.5 * (K[i + j * m] + K[j + i * m]) : 0.0;
+        V[e] = (i == j) ? 1.0 : 0.0;
+    }
+    __syncthreads();
+    const int npairs = mp / 2;
+    for (int sweep = 0; sweep < 60 && m > 1; ++sweep) {
+        int rotated = 0;
+        for (int r = 0; r < mp - 1; ++r) {
+            for (int k = tid; k < npairs; k += nt) {
+                int p, q;
+                rr_pair(k, r, mp, p, q);
+                double c = 1.0, s = 0.0;
+                const double apq = A[p + q * mp];
+                const double app = A[p + p * mp], aqq = A[q + q * mp];
+                if (apq != 0.0 && fabs(apq) > DBL_EPSILON * 0.5 * sqrt(fabs(app * aqq))) {
+                    const double tau = (aqq - app) / (2.0 * apq);
+                    const double t = (tau >= 0.0 ? 1.0 : -1.0) / (fabs(tau) + sqrt(1.0 + tau * tau));
+                    c = 1.0 / sqrt(1.0 + t * t);
+                    s = t * c;
+                    rotated = 1;
+                }
+                cs_c[k] = c;
+                cs_s[k] = s;
+                cs_p[k] = p;
+                cs_q[k] = q;
+            }
+            __syncthreads();
+            for (int e = tid; e < npairs * npairs; e += nt) {
+                const int P = e % npairs, Q = e / npairs;
+                const double sP = cs_s[P], sQ = cs_s[Q];
+                if (sP == 0.0 && sQ == 0.0) continue;
+                const double cP = cs_c[P], cQ = cs_c[Q];
+                const int p1 = cs_p[P], p2 = cs_q[P], q1 = cs_p[Q], q2 = cs_q[Q];
+                const double a11 = A[p1 + q1 * mp], a12 = A[p1 + q2 * mp];
+                const double a21 = A[p2 + q1 * mp], a22 = A[p2 + q2 * mp];
+                const double b11 = cQ * a11 - sQ * a12, b12 = sQ * a11 + cQ * a12;
+                const double b21 = cQ * a21 - sQ * a22, b22 = sQ * a21 + cQ * a22;
+                A[p1 + q1 * mp] = cP * b11 - sP * b21;
+                A[p2 + q1 * mp] = sP * b11 + cP * b21;
+                A[p1 + q2 * mp] = cP * b12 - sP * b22;
+                A[p2 + q2 * mp] = sP * b12 + cP * b22;
+            }
+            for (int e = tid; e < mp * npairs; e += nt) {
+                const int i = e % mp, Q = e / mp;
+                const double sQ = cs_s[Q];
+                if (sQ == 0.0) continue;
+                const double cQ = cs_c[Q];
+                const int q1 = cs_p[Q], q2 = cs_q[Q];
+                const double v1 = V[i + q1 * mp], v2 = V[i + q2 * mp];
+                V[i + q1 * mp] = cQ * v1 - sQ * v2;
+                V[i + q2 * mp] = sQ * v1 + cQ * v2;
+            }
+            __syncthreads();
+        }
+        if (!__syncthreads_or(rotated)) break;
+    }
+    for (int i = tid; i < m; i += nt) {
+        const double di = A[i + i * mp];
+        int rk = 0;
+        for (int j = 0; j < m; ++j) {
+            const double dj = A[j + j * mp];
+            rk += (dj > di) || (dj == di && j < i);
+        }
+        rank_of[i] = rk;
+        vals[rk] = di;
+    }
+    __syncthreads();
+    for (int e = tid; e < m * m; e += nt) {
+        const int i = e % m, j = e / m;
+        W[i + rank_of[j] * m] = V[i + j * mp];
+    }
+}
+
 // ---------------------------------------------------------------- one-sided Jacobi SVD
 __global__ void __launch_bounds__(kThreads)
     jacobi_svd_kernel(int m, const double* __restrict__ Xin, double* __restrict__ sigma,
@@ -407,9 +501,12 @@ void sym_evd_desc(int m, const double* K, double* vals, double* W, DevBuf& work,
     require(m <= 512, "sym_evd_desc: m too large");
     int use = 0;
     const size_t bytes = sizeof(double) * 2 * m * m;
-    const size_t sh = setup_smem(reinterpret_cast<const void*>(jacobi_evd_kernel), bytes, use);
-    double* g = use ? nullptr : work.get<double>((size_t)2 * m * m);
-    jacobi_evd_kernel<<<1, kThreads, sh, st>>>(m, K, vals, W, g, use);
+    const int mp = m + (m & 1);
+    const size_t bytes2 = sizeof(double) * 2 * mp * mp;
+    (void)bytes;
+    const size_t sh = setup_smem(reinterpret_cast<const void*>(jacobi_evd_blk_kernel), bytes2, use);
+    double* g = use ? nullptr : work.get<double>((size_t)2 * mp * mp);
+    jacobi_evd_blk_kernel<<<1, kEvdThreads, sh, st>>>(m, K, vals, W, g, use);
     W4_LAUNCH();
 }
 

@@ -168,9 +168,226 @@ __global__ void __launch_bounds__(1024)
         atomicOr(status, (any_f ? ST_FWD_NONFINITE : 0u) | (any_a ? ST_ADJ_NONFINITE : 0u));
 }
 
+// ---------------------------------------------------------------------------
+// Register-blocked variant (temporal blocking): each thread owns P consecutive grid
+// points and gathers a halo of S points per side from shared memory once per window
+// interval, then advances all S sub-steps in registers (valid region shrinking by one
+// point per side per sub-step).  One __syncthreads per interval instead of one per
+// sub-step; redundant halo work is 2S/P.  Radius-1 stencils (identity, upwind
+// advection, advection-diffusion).
+// ---------------------------------------------------------------------------
+template <int KIND>
+__device__ __forceinline__ double tl3(double l, double c, double r, double cc, double dd) {
+    if (KIND == WC4DVAR_MODEL_IDENTITY) return c;
+    if (KIND == WC4DVAR_MODEL_ADVECTION) return c - cc * (c - l);
+    return c - cc * (c - l) + dd * (r - 2.0 * c + l);
+}
+template <int KIND>
+__device__ __forceinline__ double adj3(double l, double c, double r, double cc, double dd) {
+    if (KIND == WC4DVAR_MODEL_IDENTITY) return c;
+    if (KIND == WC4DVAR_MODEL_ADVECTION) return (1.0 - cc) * c + cc * r;
+    return c - cc * (c - r) + dd * (l - 2.0 * c + r);
+}
+
+template <int KIND, int S, int P, bool ADJ>
+__device__ __forceinline__ void advance_interval(const double* __restrict__ cur, int b, int n,
+                                                 double cc, double dd, double (&v)[P + 2 * S]) {
+    constexpr int L = P + 2 * S;
+    int j = (b - S) % n;
+    if (j < 0) j += n;
+#pragma unroll
+    for (int u = 0; u < L; ++u) {
+        v[u] = cur[j];
+        j = (j + 1 == n) ? 0 : j + 1;
+    }
+#pragma unroll
+    for (int k = 0; k < S; ++k) {
+        double prev = v[k];
+#pragma unroll
+        for (int u = k + 1; u < L - k - 1; ++u) {
+            const double c = v[u];
+            v[u] = ADJ ? adj3<KIND>(prev, c, v[u + 1], cc, dd) : tl3<KIND>(prev, c, v[u + 1], cc, dd);
+            prev = c;
+        }
+    }
+}
+
+template <int KIND, int S, int P>
+__global__ void __launch_bounds__(512)
+    sweep_blocked_kernel(const ModelDev md, const NetDev net, const SweepArgs a,
+                         unsigned* __restrict__ status) {
+    extern __shared__ double sm[];
+    const int n = (int)md.n;
+    const int N = md.N;
+    const double c = md.c, d = md.d;
+    double* buf0 = sm;
+    double* buf1 = sm + n;
+    int* pmap = reinterpret_cast<int*>(sm + 2 * n);  // observation tables staged in SMEM
+    int* slot = pmap + n;
+    const int64_t col = blockIdx.x;
+    const int tid = threadIdx.x, nt = blockDim.x;
+    const int b = tid * P;
+    const bool owner = b < n;
+    const int np = net.n_points;
+    bool bad_f = false, bad_a = false;
+    double v[P + 2 * S];
+    for (int j = tid; j < n; j += nt) pmap[j] = net.pmap[j];
+    for (int t = tid; t <= N; t += nt) slot[t] = net.slot[t];
+    __syncthreads();
+
+    if (a.do_fwd) {
+        const double* X = a.X + col * a.ldx;
+        double* Yc = a.Y ? a.Y + col * net.q : nullptr;
+        double* tr = a.traj ? a.traj + col * a.ldtraj : nullptr;
+        {
+            const int sl = slot[0];
+            for (int j = tid; j < n; j += nt) {
+                const double x = X[j];
+                buf0[j] = x;
+                bad_f |= !isfinite(x);
+                if (tr) tr[j] = x;
+                if (a.fwd_obs && sl >= 0) {
+                    const int bb = pmap[j];
+                    if (bb >= 0) Yc[(int64_t)sl * np + bb] = a.scale_fwd * x;
+                }
+            }
+        }
+        // forcing of the next interval, prefetched one interval ahead into registers
+        double xin[P];
+#pragma unroll
+        for (int p = 0; p < P; ++p) xin[p] = (owner && N > 0 && b + p < n) ? X[(int64_t)n + b + p] : 0.0;
+        __syncthreads();
+        double* cur = buf0;
+        double* nxt = buf1;
+        for (int i = 0; i < N; ++i) {
+            const int sl = slot[i + 1];
+            double* trn = tr ? tr + (int64_t)(i + 1) * n : nullptr;
+            double xnx[P];
+            const double* Xnn = X + (int64_t)(i + 2) * n;
+#pragma unroll
+            for (int p = 0; p < P; ++p) xnx[p] = (owner && i + 1 < N && b + p < n) ? Xnn[b + p] : 0.0;
+            if (owner) {
+                advance_interval<KIND, S, P, false>(cur, b, n, c, d, v);
+#pragma unroll
+                for (int p = 0; p < P; ++p) {
+                    const int j = b + p;
+                    if (j < n) {
+                        const double x = v[S + p] + xin[p];
+                        nxt[j] = x;
+                        bad_f |= !isfinite(x);
+                        if (trn) trn[j] = x;
+                        if (a.fwd_obs && sl >= 0) {
+                            const int bb = pmap[j];
+                            if (bb >= 0) Yc[(int64_t)sl * np + bb] = a.scale_fwd * x;
+                        }
+                    }
+                }
+            }
+#pragma unroll
+            for (int p = 0; p < P; ++p) xin[p] = xnx[p];
+            __syncthreads();
+            double* t = cur;
+            cur = nxt;
+            nxt = t;
+        }
+    }
+
+    if (a.do_adj) {
+        const double* V = a.V ? a.V + col * a.ldv : nullptr;
+        const double* Yc = a.Y ? a.Y + col * net.q : nullptr;
+        double* Sv = a.S + col * a.lds;
+        // s_i = v_i + H_i^T y + M_i^T s_{i+1}: the addend of interval i, prefetched
+        auto addend = [&](int i, int j) -> double {
+            double x = V ? V[(int64_t)i * n + j] : 0.0;
+            if (a.adj_obs) {
+                const int sl = slot[i];
+                if (sl >= 0) {
+                    const int bb = pmap[j];
+                    if (bb >= 0) x = V ? x + Yc[(int64_t)sl * np + bb] : Yc[(int64_t)sl * np + bb];
+                }
+            }
+            return x;
+        };
+        {
+            const int64_t off = (int64_t)N * n;
+            for (int j = tid; j < n; j += nt) {
+                const double x = addend(N, j);
+                buf0[j] = x;
+                Sv[off + j] = x;
+                bad_a |= !isfinite(x);
+            }
+        }
+        double ain[P];
+#pragma unroll
+        for (int p = 0; p < P; ++p) ain[p] = (owner && N > 0 && b + p < n) ? addend(N - 1, b + p) : 0.0;
+        __syncthreads();
+        double* cur = buf0;
+        double* nxt = buf1;
+        for (int i = N - 1; i >= 0; --i) {
+            const int64_t off = (int64_t)i * n;
+            double anx[P];
+#pragma unroll
+            for (int p = 0; p < P; ++p) anx[p] = (owner && i > 0 && b + p < n) ? addend(i - 1, b + p) : 0.0;
+            if (owner) {
+                advance_interval<KIND, S, P, true>(cur, b, n, c, d, v);
+#pragma unroll
+                for (int p = 0; p < P; ++p) {
+                    const int j = b + p;
+                    if (j < n) {
+                        const double x = ain[p] + v[S + p];  // operators.cpp:99 (v_i + back)
+                        nxt[j] = x;
+                        Sv[off + j] = x;
+                        bad_a |= !isfinite(x);
+                    }
+                }
+            }
+#pragma unroll
+            for (int p = 0; p < P; ++p) ain[p] = anx[p];
+            __syncthreads();
+            double* t = cur;
+            cur = nxt;
+            nxt = t;
+        }
+    }
+
+    const int any_f = __syncthreads_or(bad_f);
+    const int any_a = __syncthreads_or(bad_a);
+    if (tid == 0 && (any_f || any_a))
+        atomicOr(status, (any_f ? ST_FWD_NONFINITE : 0u) | (any_a ? ST_ADJ_NONFINITE : 0u));
+}
+
+template <int KIND, int S>
+bool launch_blocked_s(const ModelDev& md, const NetDev& net, const SweepArgs& a, unsigned* status,
+                      cudaStream_t stream) {
+    constexpr int P = 8;
+    const int64_t owners = (md.n + P - 1) / P;
+    if (owners > 512) return false;
+    int nt = (int)((owners + 31) / 32) * 32;
+    const size_t smem = sizeof(double) * 2 * md.n + sizeof(int) * (md.n + md.N + 1);
+    if (smem > 200 * 1024) return false;
+    auto kern = sweep_blocked_kernel<KIND, S, P>;
+    if (smem > 48 * 1024)
+        W4_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    kern<<<(unsigned)a.m, nt, smem, stream>>>(md, net, a, status);
+    W4_LAUNCH();
+    return true;
+}
+
+template <int KIND>
+bool launch_blocked(const ModelDev& md, const NetDev& net, const SweepArgs& a, unsigned* status,
+                    cudaStream_t stream) {
+    switch (md.s) {
+        case 1: return launch_blocked_s<KIND, 1>(md, net, a, status, stream);
+        case 5: return launch_blocked_s<KIND, 5>(md, net, a, status, stream);
+        case 10: return launch_blocked_s<KIND, 10>(md, net, a, status, stream);
+        default: return false;
+    }
+}
+
 template <int KIND>
 void launch_resident(const ModelDev& md, const NetDev& net, const SweepArgs& a, unsigned* status,
                      cudaStream_t stream) {
+    if (launch_blocked<KIND>(md, net, a, status, stream)) return;
     const size_t smem = sizeof(double) * 2 * md.n;
     auto kern = sweep_resident_kernel<KIND>;
     if (smem > 48 * 1024)
