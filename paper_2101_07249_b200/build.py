@@ -59,7 +59,9 @@ def build(verbose: bool = False) -> str:
                 print(f"== {os.path.basename(o)}\n{log}")
     newest = max(os.path.getmtime(o) for o in objs)
     if not os.path.exists(LIB) or os.path.getmtime(LIB) < newest:
-        cmd = [NVCC] + ARCH + ["-shared", "-o", LIB] + objs + ["--cudart", "static"]
+        cmd = [NVCC] + ARCH + ["-shared", "-o", LIB] + objs + [
+            "--cudart", "static", "-L/usr/local/cuda/lib64", "-lcufft",
+            "-Xlinker", "-rpath=/usr/local/cuda/lib64"]
         p = subprocess.run(cmd, capture_output=True, text=True)
         if p.returncode != 0:
             raise RuntimeError(f"link failed: {' '.join(cmd)}\n{p.stdout}\n{p.stderr}")

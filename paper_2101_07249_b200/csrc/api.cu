@@ -97,10 +97,11 @@ int wc4dvar_gpu_hessian_create(const wc4dvar_model_desc* model, const wc4dvar_ne
     require(net->n == model->n && net->N == model->N, "HessianOperator: network/window mismatch");
     require(model->kind >= WC4DVAR_MODEL_IDENTITY && model->kind <= WC4DVAR_MODEL_LORENZ96,
             "HessianOperator: unknown model kind");
-    require(model->kind != WC4DVAR_MODEL_LORENZ96,
-            "HessianOperator: Lorenz-96 device sweeps are not built yet");
-    require(bh->kind == WC4DVAR_COV_DENSE,
-            "HessianOperator: circulant covariance factors are not built yet");
+    require(model->kind != WC4DVAR_MODEL_LORENZ96 || (model->stages && model->dt > 0.0),
+            "Lorenz96Linearized: stages and dt are required");
+    require(model->kind != WC4DVAR_MODEL_LORENZ96 || model->n >= 4, "Lorenz96Model: n must be >= 4");
+    require(bh->kind == WC4DVAR_COV_DENSE || bh->kind == WC4DVAR_COV_CIRCULANT,
+            "HessianOperator: unknown covariance representation");
     const int64_t n = model->n;
     const int N = model->N;
     for (int a = 0; a < net->n_times; ++a) {
@@ -126,6 +127,10 @@ int wc4dvar_gpu_hessian_create(const wc4dvar_model_desc* model, const wc4dvar_ne
     h->md.c = model->courant;
     h->md.d = model->diffusion;
     h->md.dt = model->dt;
+    if (model->kind == WC4DVAR_MODEL_LORENZ96) {
+        h->d_stages = dev_upload(model->stages, (size_t)N * model->substeps * 4 * n, st);
+        h->md.stages = h->d_stages;
+    }
     h->times.assign(net->times, net->times + net->n_times);
     h->points.assign(net->points, net->points + net->n_points);
     std::vector<int> slot(N + 1, -1), pmap(n, -1);
@@ -138,6 +143,13 @@ int wc4dvar_gpu_hessian_create(const wc4dvar_model_desc* model, const wc4dvar_ne
     h->nd.q = (int64_t)net->n_times * net->n_points;
     h->nd.slot = h->d_slot;
     h->nd.pmap = h->d_pmap;
+    if (bh->kind == WC4DVAR_COV_CIRCULANT) {
+        h->circ = new CirculantPlan();
+        h->circ->init(n, bh->half, qh->half, bh->half_inv, qh->half_inv, st);
+        W4_CUDA(cudaStreamSynchronize(st));
+        *out = h.release();
+        return WC4DVAR_OK;
+    }
     const size_t fsz = (size_t)n * n;
     // sym_sqrt symmetrises its factors exactly (covariance.cpp:101-102); when a factor is
     // bitwise symmetric the D^{1/2} GEMM may read its columns as rows.
@@ -567,7 +579,7 @@ int wc4dvar_gpu_cost_rhs(wc4dvar_cost* c, double* rhs) {
     a.adj_obs = h->nd.q > 0;
     a.m = 1;
     h->reset_status(st);
-    sweep(h->md, h->nd, a, h->d_status, st);
+    sweep(h->md, h->nd, a, h->d_status, st, &h->sweep_ws);
     h->piece_dev(WC4DVAR_D_HALF, s, n, 1, u, n, st);
     const double r_inv = 1.0 / (h->sigma_obs * h->sigma_obs);
     axpby(n, 1.0, c->b_tilde, r_inv, u, u, st);

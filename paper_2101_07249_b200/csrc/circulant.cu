@@ -1,0 +1,169 @@
+// Circulant covariance factors (EXTENSION): on the periodic grid SOAR
+// with chordal distance is circulant (covariance.cpp:36-41, test_covariance.cpp:41-43), so
+// its symmetric square root is the circulant matrix whose eigenvalues are the square
+// roots of the DFT of the first column.  D^{1/2} of an n_A x m block is then a batched
+// real FFT over the (N+1)m n-columns, a pointwise product with the B^{1/2} or Q^{1/2}
+// spectrum (picked per column; the 1/n normalisation and the optional identity term
+// v + D^{1/2}s fused into the product / final pass), and a batched inverse FFT.
+// The FFTs are cuFFT (library); the spectrum product and epilogues are our kernels.
+#include "circulant.cuh"
+
+#include <cufft.h>
+
+#include <map>
+#include <mutex>
+
+namespace w4 {
+namespace {
+
+#define W4_CUFFT(expr)                                                                      \
+    do {                                                                                    \
+        cufftResult _r = (expr);                                                            \
+        if (_r != CUFFT_SUCCESS)                                                            \
+            throw DeviceError(std::string(#expr) + ": cuFFT error " + std::to_string((int)_r)); \
+    } while (0)
+
+__global__ void spectrum_mul_kernel(int64_t nh, int64_t ncols, int per, const double2* __restrict__ sb,
+                                    const double2* __restrict__ sq, double scale, double2* __restrict__ Z) {
+    // column c of the (N+1)m view: block i = c % per; i == 0 -> B spectrum, else Q
+    const int64_t total = nh * ncols;
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
+         e += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t c = e / nh, f = e % nh;
+        const double2 h = ((c % per) == 0) ? sb[f] : sq[f];
+        const double2 z = Z[e];
+        Z[e] = make_double2(scale * (z.x * h.x - z.y * h.y), scale * (z.x * h.y + z.y * h.x));
+    }
+}
+
+__global__ void add_cols_kernel(int64_t rows, int64_t m, const double* __restrict__ a, int64_t lda,
+                                const double* __restrict__ b, int64_t ldb, double* __restrict__ out,
+                                int64_t ldo, unsigned* status) {
+    bool bad = false;
+    const int64_t total = rows * m;
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
+         e += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t c = e / rows, r = e % rows;
+        const double v = a[c * lda + r] + b[c * ldb + r];  // out = v + D^{1/2} s
+        out[c * ldo + r] = v;
+        bad |= !isfinite(v);
+    }
+    if (status && __syncthreads_or(bad) && threadIdx.x == 0) atomicOr(status, ST_OUT_NONFINITE);
+}
+
+__global__ void copy_cols_kernel(int64_t rows, int64_t m, const double* __restrict__ a, int64_t lda,
+                                 double* __restrict__ out, int64_t ldo) {
+    const int64_t total = rows * m;
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
+         e += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t c = e / rows, r = e % rows;
+        out[c * ldo + r] = a[c * lda + r];
+    }
+}
+
+unsigned grid_for(int64_t total) {
+    int64_t g = cdiv(total, 256);
+    if (g > 16 * kSMs) g = 16 * kSMs;
+    return (unsigned)std::max<int64_t>(g, 1);
+}
+
+}  // namespace
+
+struct CirculantPlan::Impl {
+    int64_t n = 0;
+    std::mutex mu;
+    std::map<int64_t, std::pair<cufftHandle, cufftHandle>> plans;  // batch -> (R2C, C2R)
+    ~Impl() {
+        for (auto& kv : plans) {
+            cufftDestroy(kv.second.first);
+            cufftDestroy(kv.second.second);
+        }
+    }
+    std::pair<cufftHandle, cufftHandle> get(int64_t batch) {
+        std::lock_guard<std::mutex> lk(mu);
+        auto it = plans.find(batch);
+        if (it != plans.end()) return it->second;
+        cufftHandle f, b;
+        long long nn = n;
+        W4_CUFFT(cufftCreate(&f));
+        W4_CUFFT(cufftCreate(&b));
+        size_t ws = 0;
+        long long inembed = n, onembed = n / 2 + 1;
+        W4_CUFFT(cufftMakePlanMany64(f, 1, &nn, &inembed, 1, n, &onembed, 1, n / 2 + 1, CUFFT_D2Z, batch, &ws));
+        W4_CUFFT(cufftMakePlanMany64(b, 1, &nn, &onembed, 1, n / 2 + 1, &inembed, 1, n, CUFFT_Z2D, batch, &ws));
+        plans[batch] = {f, b};
+        return plans[batch];
+    }
+};
+
+CirculantPlan::CirculantPlan() : impl(new Impl) {}
+CirculantPlan::~CirculantPlan() {
+    for (double2*& p : spec)
+        if (p) cudaFree(p);
+    delete impl;
+}
+
+void CirculantPlan::init(int64_t n, const double* h_b, const double* h_q, const double* h_bi,
+                         const double* h_qi, cudaStream_t st) {
+    impl->n = n;
+    const int64_t nh = n / 2 + 1;
+    auto spectrum = [&](const double* host_col, double2*& dst) {
+        if (!host_col) {
+            dst = nullptr;
+            return;
+        }
+        double* d = nullptr;
+        W4_CUDA(cudaMalloc(&d, sizeof(double) * n));
+        W4_CUDA(cudaMalloc(&dst, sizeof(double2) * nh));
+        W4_CUDA(cudaMemcpyAsync(d, host_col, sizeof(double) * n, cudaMemcpyHostToDevice, st));
+        auto pl = impl->get(1);
+        W4_CUFFT(cufftSetStream(pl.first, st));
+        W4_CUFFT(cufftExecD2Z(pl.first, d, reinterpret_cast<cufftDoubleComplex*>(dst)));
+        W4_CUDA(cudaStreamSynchronize(st));
+        cudaFree(d);
+    };
+    spectrum(h_b, spec[0]);
+    spectrum(h_q, spec[1]);
+    spectrum(h_bi, spec[2]);
+    spectrum(h_qi, spec[3]);
+}
+
+void CirculantPlan::apply(bool inv, int N, const double* V, int64_t ldv, int64_t m, double* out,
+                          int64_t ldo, const double* add, int64_t ldadd, unsigned* status,
+                          DevBuf& zbuf, DevBuf& xbuf, cudaStream_t st) {
+    const int64_t n = impl->n, nh = n / 2 + 1;
+    const double2* sb = spec[inv ? 2 : 0];
+    const double2* sq = spec[inv ? 3 : 1];
+    require(sb && sq, "apply_D_half_inv: inverse factors were not provided");
+    const int64_t dim = n * (N + 1);
+    const int64_t ncols = (int64_t)(N + 1) * m;
+    // contiguous real input (the FFT plan assumes column distance n)
+    const double* X = V;
+    if (ldv != dim) {
+        double* xb = xbuf.get<double>((size_t)dim * m);
+        copy_cols_kernel<<<grid_for(dim * m), 256, 0, st>>>(dim, m, V, ldv, xb, dim);
+        W4_LAUNCH();
+        X = xb;
+    }
+    double2* Z = zbuf.get<double2>((size_t)nh * ncols);
+    auto pl = impl->get(ncols);
+    W4_CUFFT(cufftSetStream(pl.first, st));
+    W4_CUFFT(cufftSetStream(pl.second, st));
+    W4_CUFFT(cufftExecD2Z(pl.first, const_cast<double*>(X), reinterpret_cast<cufftDoubleComplex*>(Z)));
+    spectrum_mul_kernel<<<grid_for(nh * ncols), 256, 0, st>>>(nh, ncols, N + 1, sb, sq, 1.0 / (double)n, Z);
+    W4_LAUNCH();
+    if (!add && ldo == dim) {
+        W4_CUFFT(cufftExecZ2D(pl.second, reinterpret_cast<cufftDoubleComplex*>(Z), out));
+        return;
+    }
+    double* tmp = xbuf.get<double>((size_t)dim * m);
+    W4_CUFFT(cufftExecZ2D(pl.second, reinterpret_cast<cufftDoubleComplex*>(Z), tmp));
+    if (add) {
+        add_cols_kernel<<<grid_for(dim * m), 256, 0, st>>>(dim, m, add, ldadd, tmp, dim, out, ldo, status);
+    } else {
+        copy_cols_kernel<<<grid_for(dim * m), 256, 0, st>>>(dim, m, tmp, dim, out, ldo);
+    }
+    W4_LAUNCH();
+}
+
+}  // namespace w4

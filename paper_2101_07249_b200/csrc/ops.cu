@@ -78,15 +78,19 @@ HessianOp::~HessianOp() {
         if (p) cudaFree(p);
     if (d_slot) cudaFree(d_slot);
     if (d_pmap) cudaFree(d_pmap);
+    delete circ;
 }
 
 void HessianOp::d_half(bool inv, const double* V, int64_t ldv, int64_t m, double* out,
                        int64_t ldo, const double* add, int64_t ldadd, unsigned* status,
                        cudaStream_t st) {
+    if (cov_kind == WC4DVAR_COV_CIRCULANT) {
+        circ->apply(inv, N, V, ldv, m, out, ldo, add, ldadd, status, circ_z, circ_x, st);
+        return;
+    }
     const double* B = inv ? b_half_inv : b_half;
     const double* Q = inv ? q_half_inv : q_half;
     require(B && Q, "apply_D_half_inv: inverse factors were not provided");
-    require(cov_kind == WC4DVAR_COV_DENSE, "circulant covariance factors are not built yet");
     GemmPass ps[2];
     int np = 0;
     if (N > 0) {
@@ -139,7 +143,7 @@ void HessianOp::apply_block_dev(const double* V, int64_t ldv, int64_t m, double*
     a.do_adj = true;
     a.adj_obs = q > 0;
     a.m = m;
-    sweep(md, nd, a, d_status, st);
+    sweep(md, nd, a, d_status, st, &sweep_ws);
     prof_mark(2, st);
     // out = v + D^{1/2} s  (operators.cpp:141)
     d_half(false, T, dim, m, out, ldo, V, ldv, d_status, st);
@@ -159,7 +163,7 @@ void HessianOp::piece_dev(int which, const double* V, int64_t ldv, int64_t m, do
             a.traj = out;
             a.ldtraj = ldo;
             a.do_fwd = true;
-            sweep(md, nd, a, d_status, st);
+            sweep(md, nd, a, d_status, st, &sweep_ws);
             break;
         case WC4DVAR_LINVT:
             a.V = V;
@@ -167,7 +171,7 @@ void HessianOp::piece_dev(int which, const double* V, int64_t ldv, int64_t m, do
             a.S = out;
             a.lds = ldo;
             a.do_adj = true;
-            sweep(md, nd, a, d_status, st);
+            sweep(md, nd, a, d_status, st, &sweep_ws);
             break;
         case WC4DVAR_D_HALF:
         case WC4DVAR_D_HALF_INV:
@@ -233,7 +237,7 @@ double wc4dvar_cost::eval_dev(const double* x, cudaStream_t st) {
     a.do_fwd = true;
     a.fwd_obs = q > 0;
     a.m = 1;
-    sweep(h.md, h.nd, a, h.d_status, st);
+    sweep(h.md, h.nd, a, h.d_status, st, &h.sweep_ws);
     sqdist(dim, x, b_tilde, d_val, part, counter, st);
     if (q > 0) sqdist(q, y, d, d_val + 1, part, counter, st);
     else W4_CUDA(cudaMemsetAsync(d_val + 1, 0, sizeof(double), st));

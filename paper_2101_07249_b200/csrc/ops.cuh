@@ -6,6 +6,7 @@
 #include <string>
 #include <vector>
 
+#include "circulant.cuh"
 #include "common.cuh"
 #include "gemm.cuh"
 #include "sweep.cuh"
@@ -65,7 +66,9 @@ struct HessianOp final : wc4dvar_op {
     int* d_pmap = nullptr;
     double* d_stages = nullptr;
     std::vector<int> times, points;
-    DevBuf t_ws, y_ws;
+    DevBuf t_ws, y_ws, sweep_ws;
+    CirculantPlan* circ = nullptr;  // WC4DVAR_COV_CIRCULANT factors
+    DevBuf circ_z, circ_x;
 
     ~HessianOp() override;
     const char* kind_name() const override { return "HessianOperator"; }

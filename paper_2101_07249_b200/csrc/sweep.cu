@@ -8,6 +8,8 @@
 // with the observation selection (models.cpp:184-201) fused into the sweeps.
 #include "sweep.cuh"
 
+#include <cstdlib>
+
 namespace w4 {
 namespace {
 
@@ -405,10 +407,19 @@ void launch_resident(const ModelDev& md, const NetDev& net, const SweepArgs& a, 
 int64_t sweep_resident_max_n() { return (227 * 1024) / (2 * sizeof(double)); }
 
 void sweep(const ModelDev& md, const NetDev& net, const SweepArgs& a, unsigned* status,
-           cudaStream_t stream) {
+           cudaStream_t stream, DevBuf* ws) {
     if (a.m == 0) return;
-    require(md.n <= sweep_resident_max_n(),
-            "sweep: n exceeds the resident-sweep limit (tiled sweep not built yet)");
+    // WC4DVAR_SWEEP_TILE=T forces the tiled path with tile size T (test hook: lets the
+    // halo / multi-launch logic run on problem sizes the oracle can check quickly).
+    static const int forced_tile = [] {
+        const char* e = std::getenv("WC4DVAR_SWEEP_TILE");
+        return e ? std::atoi(e) : 0;
+    }();
+    if (md.kind == WC4DVAR_MODEL_LORENZ96 || md.n > sweep_resident_max_n() || forced_tile > 0) {
+        static thread_local DevBuf local;
+        sweep_tiled(md, net, a, status, stream, ws ? *ws : local, forced_tile);
+        return;
+    }
     switch (md.kind) {
         case WC4DVAR_MODEL_IDENTITY:
             launch_resident<WC4DVAR_MODEL_IDENTITY>(md, net, a, status, stream);

@@ -45,7 +45,12 @@ struct SweepArgs {
 
 // Max grid points handled by the resident (whole state in shared memory) sweep.
 int64_t sweep_resident_max_n();
+// ws: scratch for the tiled path's launch-boundary states (grown as needed).
 void sweep(const ModelDev& model, const NetDev& net, const SweepArgs& a, unsigned* status,
-           cudaStream_t stream);
+           cudaStream_t stream, DevBuf* ws = nullptr);
+// Tiled window sweeps (large n, Lorenz-96); see sweep_tiled.cu.
+// tile_override > 0 forces tiled mode with that tile size (tests).
+void sweep_tiled(const ModelDev& model, const NetDev& net, const SweepArgs& a, unsigned* status,
+                 cudaStream_t stream, DevBuf& ws, int tile_override = 0);
 
 }  // namespace w4

@@ -1,0 +1,431 @@
+// Tiled window sweeps for large n and for Lorenz-96 (any n).
+//
+// One CTA owns a tile of T grid points of one sketch column and advances K window
+// intervals per launch on a shared-memory region [t0 - HL, t0 + T + HR) whose halos
+// (HL = K s rl, HR = K s rr for a stencil of radius (rl, rr) per sub-step) are recomputed
+// redundantly, so tiles never communicate inside a launch; the valid region shrinks by
+// (rl, rr) per sub-step and the tile centre stays valid.  State crossing a launch boundary
+// goes through a ping-pong buffer.  When the whole periodic domain fits (n <= T) the tile
+// is the domain itself ("resident" mode: indices wrap, nothing shrinks, one launch).
+//
+// Models: identity / upwind advection / advection-diffusion (1 stencil phase per
+// sub-step) and the exact TL / adjoint of the RK4 Lorenz-96 step with stored stages
+// (4 stencil phases per sub-step, models.cpp:92-148).
+#include "sweep.cuh"
+
+#include <algorithm>
+
+namespace w4 {
+namespace {
+
+constexpr int kThreads = 512;
+
+struct TileGeom {
+    int T;        // tile centre size
+    int HL, HR;   // halos (tiled mode)
+    int R;        // region size in SMEM
+    bool resident;
+    int64_t ntiles;
+};
+
+// Stencil radius (left, right) of one TL sub-step (adjoint mirrors it).
+__host__ __device__ inline void model_radius(int kind, int& rl, int& rr) {
+    if (kind == WC4DVAR_MODEL_LORENZ96) {
+        rl = 8;
+        rr = 4;
+    } else if (kind == WC4DVAR_MODEL_IDENTITY) {
+        rl = 0;
+        rr = 0;
+    } else {
+        rl = 1;
+        rr = 1;
+    }
+}
+
+struct Region {
+    int R;
+    bool resident;
+    int64_t origin;  // global grid index of region element 0
+    int64_t n;
+    __device__ __forceinline__ int nb(int e, int d) const {  // neighbour index in SMEM
+        if (!resident) return e + d;
+        int x = e + d;
+        if (x < 0) x += R;
+        else if (x >= R) x -= R;
+        return x;
+    }
+    __device__ __forceinline__ int64_t gidx(int e) const {
+        int64_t g = origin + e;
+        g %= n;
+        if (g < 0) g += n;
+        return g;
+    }
+};
+
+// ---------------------------------------------------------------- single-phase stencils
+template <int KIND, bool ADJ>
+__device__ __forceinline__ double stencil1(const double* __restrict__ u, const Region& rg, int e,
+                                           double c, double d) {
+    if (KIND == WC4DVAR_MODEL_IDENTITY) return u[e];
+    const double um = u[rg.nb(e, -1)], uc = u[e], up = u[rg.nb(e, 1)];
+    if (!ADJ) {
+        if (KIND == WC4DVAR_MODEL_ADVECTION) return uc - c * (uc - um);          // models.cpp:32
+        return uc - c * (uc - um) + d * (up - 2.0 * uc + um);
+    }
+    if (KIND == WC4DVAR_MODEL_ADVECTION) return (1.0 - c) * uc + c * up;        // models.cpp:42
+    return uc - c * (uc - up) + d * (um - 2.0 * uc + up);
+}
+
+// Lorenz-96 Jacobian (models.cpp:92-102) and its transpose (models.cpp:105-116) at e,
+// with the stage x given as a global pointer indexed by grid point and the vector in SMEM.
+__device__ __forceinline__ double l96_jac(const double* __restrict__ x, const double* __restrict__ v,
+                                          const Region& rg, int e) {
+    const int64_t g = rg.gidx(e);
+    const int64_t n = rg.n;
+    const int64_t gm2 = (g + n - 2) % n, gm1 = (g + n - 1) % n, gp1 = (g + 1) % n;
+    const double vm2 = v[rg.nb(e, -2)], vm1 = v[rg.nb(e, -1)], vp1 = v[rg.nb(e, 1)], vc = v[e];
+    return -vm2 * x[gm1] - x[gm2] * vm1 + vm1 * x[gp1] + x[gm1] * vp1 - vc;
+}
+__device__ __forceinline__ double l96_jac_t(const double* __restrict__ x, const double* __restrict__ l,
+                                            const Region& rg, int e, double scale) {
+    const int64_t g = rg.gidx(e);
+    const int64_t n = rg.n;
+    const int64_t gm2 = (g + n - 2) % n, gm1 = (g + n - 1) % n, gp1 = (g + 1) % n, gp2 = (g + 2) % n;
+    const double lp2 = scale * l[rg.nb(e, 2)], lp1 = scale * l[rg.nb(e, 1)];
+    const double lm1 = scale * l[rg.nb(e, -1)], lc = scale * l[e];
+    return -x[gp1] * lp2 + (x[gp2] - x[gm1]) * lp1 + x[gm2] * lm1 - lc;
+}
+
+struct TiledArgs {
+    ModelDev md;
+    NetDev net;
+    SweepArgs a;
+    TileGeom geo;
+    int i0, i1;             // forward: intervals [i0, i1); adjoint: from state s_{i1} down to s_{i0}
+    const double* bin;      // boundary state in (n x m, ld n) or null (start of window)
+    double* bout;           // boundary state out
+};
+
+// ---------------------------------------------------------------- forward
+template <int KIND>
+__global__ void __launch_bounds__(kThreads) tiled_fwd_kernel(const TiledArgs ta, unsigned* status) {
+    extern __shared__ double sm[];
+    const ModelDev& md = ta.md;
+    const NetDev& net = ta.net;
+    const SweepArgs& a = ta.a;
+    const TileGeom& geo = ta.geo;
+    const int R = geo.R;
+    double* cur = sm;
+    double* nxt = sm + R;
+    double* t1 = sm + 2 * R;  // L96 temporaries
+    double* t2 = sm + 3 * R;
+    double* acc = sm + 4 * R;
+    const int64_t n = md.n;
+    const int64_t col = blockIdx.x;
+    const int64_t tile = blockIdx.y;
+    const int64_t t0 = tile * geo.T;
+    const int tid = threadIdx.x, nt = blockDim.x;
+    Region rg{R, geo.resident, geo.resident ? 0 : t0 - geo.HL, n};
+    const int c_lo = geo.resident ? 0 : geo.HL;                   // tile centre in SMEM
+    const int c_hi = geo.resident ? R : geo.HL + (int)(n - t0 < (int64_t)geo.T ? n - t0 : (int64_t)geo.T);
+    int rl, rr;
+    model_radius(md.kind, rl, rr);
+    const int s = md.s;
+    const double* X = a.X + col * a.ldx;
+    double* Yc = a.Y ? a.Y + col * net.q : nullptr;
+    double* tr = a.traj ? a.traj + col * a.ldtraj : nullptr;
+    const int np = net.n_points;
+    bool bad = false;
+
+    // state x_{i0} on the region
+    const double* src = ta.bin ? ta.bin + col * n : X;  // x_0 = X_0
+    for (int e = tid; e < R; e += nt) {
+        const int64_t g = rg.gidx(e);
+        cur[e] = src[g];
+    }
+    if (ta.i0 == 0) {  // x_0 is part of the trajectory (finite check, traj, obs at t_0)
+        const int sl = net.slot[0];
+        for (int e = c_lo + tid; e < c_hi; e += nt) {
+            const int64_t g = rg.gidx(e);
+            const double x = cur[e];
+            bad |= !isfinite(x);
+            if (tr) tr[g] = x;
+            if (a.fwd_obs && sl >= 0) {
+                const int bb = net.pmap[g];
+                if (bb >= 0) Yc[(int64_t)sl * np + bb] = a.scale_fwd * x;
+            }
+        }
+    }
+    __syncthreads();
+    int lo = 0, hi = R;  // valid region
+    for (int i = ta.i0; i < ta.i1; ++i) {
+        for (int k = 0; k < s; ++k) {
+            if (!geo.resident) {
+                lo += rl;
+                hi -= rr;
+            }
+            const bool last = (k + 1 == s);
+            if (KIND != WC4DVAR_MODEL_LORENZ96) {
+                for (int e = lo + tid; e < hi; e += nt) nxt[e] = stencil1<KIND, false>(cur, rg, e, md.c, md.d);
+            } else {
+                // RK4 TL step (models.cpp:120-128), stages of sub-step i*s+k
+                const double* st = md.stages + ((int64_t)i * s + k) * 4 * n;
+                const double dt = md.dt;
+                const int l1 = geo.resident ? 0 : lo - 6, h1 = geo.resident ? R : hi + 3;
+                for (int e = max(l1, 0) + tid; e < min(h1, R); e += nt) {
+                    const double a1 = l96_jac(st, cur, rg, e);
+                    acc[e] = a1;
+                    t1[e] = cur[e] + 0.5 * dt * a1;
+                }
+                __syncthreads();
+                const int l2 = geo.resident ? 0 : lo - 4, h2 = geo.resident ? R : hi + 2;
+                for (int e = max(l2, 0) + tid; e < min(h2, R); e += nt) {
+                    const double a2 = l96_jac(st + n, t1, rg, e);
+                    acc[e] = acc[e] + 2.0 * a2;
+                    t2[e] = cur[e] + 0.5 * dt * a2;
+                }
+                __syncthreads();
+                const int l3 = geo.resident ? 0 : lo - 2, h3 = geo.resident ? R : hi + 1;
+                for (int e = max(l3, 0) + tid; e < min(h3, R); e += nt) {
+                    const double a3 = l96_jac(st + 2 * n, t2, rg, e);
+                    acc[e] = acc[e] + 2.0 * a3;
+                    t1[e] = cur[e] + dt * a3;
+                }
+                __syncthreads();
+                for (int e = lo + tid; e < hi; e += nt) {
+                    const double a4 = l96_jac(st + 3 * n, t1, rg, e);
+                    nxt[e] = cur[e] + (dt / 6.0) * (acc[e] + a4);
+                }
+            }
+            if (last) {
+                // x_{i+1} = M_i x_i + X_{i+1}  (operators.cpp:88)
+                const double* Xn = X + (int64_t)(i + 1) * n;
+                const int sl = net.slot[i + 1];
+                double* trn = tr ? tr + (int64_t)(i + 1) * n : nullptr;
+                for (int e = lo + tid; e < hi; e += nt) {
+                    const int64_t g = rg.gidx(e);
+                    const double x = nxt[e] + Xn[g];
+                    nxt[e] = x;
+                    if (e >= c_lo && e < c_hi) {
+                        bad |= !isfinite(x);
+                        if (trn) trn[g] = x;
+                        if (a.fwd_obs && sl >= 0) {
+                            const int bb = net.pmap[g];
+                            if (bb >= 0) Yc[(int64_t)sl * np + bb] = a.scale_fwd * x;
+                        }
+                    }
+                }
+            }
+            __syncthreads();
+            double* t = cur;
+            cur = nxt;
+            nxt = t;
+        }
+    }
+    if (ta.bout)
+        for (int e = c_lo + tid; e < c_hi; e += nt) ta.bout[col * n + rg.gidx(e)] = cur[e];
+    if (__syncthreads_or(bad) && tid == 0) atomicOr(status, ST_FWD_NONFINITE);
+}
+
+// ---------------------------------------------------------------- adjoint
+template <int KIND>
+__global__ void __launch_bounds__(kThreads) tiled_adj_kernel(const TiledArgs ta, unsigned* status) {
+    extern __shared__ double sm[];
+    const ModelDev& md = ta.md;
+    const NetDev& net = ta.net;
+    const SweepArgs& a = ta.a;
+    const TileGeom& geo = ta.geo;
+    const int R = geo.R;
+    double* cur = sm;
+    double* nxt = sm + R;
+    double* t1 = sm + 2 * R;
+    double* t2 = sm + 3 * R;
+    double* acc = sm + 4 * R;
+    const int64_t n = md.n;
+    const int64_t col = blockIdx.x;
+    const int64_t tile = blockIdx.y;
+    const int64_t t0 = tile * geo.T;
+    const int tid = threadIdx.x, nt = blockDim.x;
+    // adjoint radius mirrors the TL one: (rr, rl)
+    int rl, rr;
+    model_radius(md.kind, rr, rl);
+    const int HL = geo.resident ? 0 : geo.HR, HRr = geo.resident ? 0 : geo.HL;
+    (void)HRr;
+    Region rg{R, geo.resident, geo.resident ? 0 : t0 - HL, n};
+    const int c_lo = geo.resident ? 0 : HL;
+    const int c_hi = geo.resident ? R : HL + (int)(n - t0 < (int64_t)geo.T ? n - t0 : (int64_t)geo.T);
+    const int s = md.s;
+    const double* V = a.V ? a.V + col * a.ldv : nullptr;
+    const double* Yc = a.Y ? a.Y + col * net.q : nullptr;
+    double* Sv = a.S + col * a.lds;
+    const int np = net.n_points;
+    bool bad = false;
+
+    auto addend = [&](int i, int64_t g) -> double {
+        double x = V ? V[(int64_t)i * n + g] : 0.0;
+        if (a.adj_obs) {
+            const int sl = net.slot[i];
+            if (sl >= 0) {
+                const int bb = net.pmap[g];
+                if (bb >= 0) x = V ? x + Yc[(int64_t)sl * np + bb] : Yc[(int64_t)sl * np + bb];
+            }
+        }
+        return x;
+    };
+
+    // state s_{i1}
+    if (ta.bin) {
+        for (int e = tid; e < R; e += nt) cur[e] = ta.bin[col * n + rg.gidx(e)];
+    } else {  // s_N = v_N + H_N^T y
+        for (int e = tid; e < R; e += nt) {
+            const int64_t g = rg.gidx(e);
+            const double x = addend(ta.i1, g);
+            cur[e] = x;
+            if (e >= c_lo && e < c_hi) {
+                Sv[(int64_t)ta.i1 * n + g] = x;
+                bad |= !isfinite(x);
+            }
+        }
+    }
+    __syncthreads();
+    int lo = 0, hi = R;
+    for (int i = ta.i1 - 1; i >= ta.i0; --i) {
+        for (int kk = 0; kk < s; ++kk) {
+            const int k = s - 1 - kk;  // sub-steps in reverse
+            if (!geo.resident) {
+                lo += rl;
+                hi -= rr;
+            }
+            const bool last = (kk + 1 == s);
+            if (KIND != WC4DVAR_MODEL_LORENZ96) {
+                for (int e = lo + tid; e < hi; e += nt) nxt[e] = stencil1<KIND, true>(cur, rg, e, md.c, md.d);
+            } else {
+                // RK4 adjoint step (models.cpp:130-148)
+                const double* st = md.stages + ((int64_t)i * s + k) * 4 * n;
+                const double dt = md.dt, ee = dt / 6.0;
+                const int l1 = geo.resident ? 0 : lo - 3, h1 = geo.resident ? R : hi + 6;
+                for (int e = max(l1, 0) + tid; e < min(h1, R); e += nt) {
+                    const double w = l96_jac_t(st + 3 * n, cur, rg, e, ee);
+                    acc[e] = cur[e] + w;
+                    t1[e] = 2.0 * ee * cur[e] + dt * w;
+                }
+                __syncthreads();
+                const int l2 = geo.resident ? 0 : lo - 2, h2 = geo.resident ? R : hi + 4;
+                for (int e = max(l2, 0) + tid; e < min(h2, R); e += nt) {
+                    const double w = l96_jac_t(st + 2 * n, t1, rg, e, 1.0);
+                    acc[e] = acc[e] + w;
+                    t2[e] = 2.0 * ee * cur[e] + 0.5 * dt * w;
+                }
+                __syncthreads();
+                const int l3 = geo.resident ? 0 : lo - 1, h3 = geo.resident ? R : hi + 2;
+                for (int e = max(l3, 0) + tid; e < min(h3, R); e += nt) {
+                    const double w = l96_jac_t(st + n, t2, rg, e, 1.0);
+                    acc[e] = acc[e] + w;
+                    t1[e] = ee * cur[e] + 0.5 * dt * w;
+                }
+                __syncthreads();
+                for (int e = lo + tid; e < hi; e += nt) {
+                    const double w = l96_jac_t(st, t1, rg, e, 1.0);
+                    nxt[e] = acc[e] + w;
+                }
+            }
+            if (last) {
+                // s_i = v_i + H_i^T y + M_i^T s_{i+1}  (operators.cpp:99)
+                for (int e = lo + tid; e < hi; e += nt) {
+                    const int64_t g = rg.gidx(e);
+                    const double x = addend(i, g) + nxt[e];
+                    nxt[e] = x;
+                    if (e >= c_lo && e < c_hi) {
+                        Sv[(int64_t)i * n + g] = x;
+                        bad |= !isfinite(x);
+                    }
+                }
+            }
+            __syncthreads();
+            double* t = cur;
+            cur = nxt;
+            nxt = t;
+        }
+    }
+    if (ta.bout)
+        for (int e = c_lo + tid; e < c_hi; e += nt) ta.bout[col * n + rg.gidx(e)] = cur[e];
+    if (__syncthreads_or(bad) && tid == 0) atomicOr(status, ST_ADJ_NONFINITE);
+}
+
+template <int KIND>
+void launch_tiled(const ModelDev& md, const NetDev& net, const SweepArgs& a, unsigned* status,
+                  cudaStream_t st, DevBuf& ws, int tile_override) {
+    int rl, rr;
+    model_radius(md.kind, rl, rr);
+    const int nbuf = (KIND == WC4DVAR_MODEL_LORENZ96) ? 5 : 2;
+    const int64_t smem_cap = 200 * 1024 / (8 * nbuf);  // region doubles per buffer
+    TileGeom geo{};
+    int K = md.N;  // intervals per launch
+    if (md.n <= smem_cap && (tile_override <= 0 || tile_override >= md.n)) {
+        geo.resident = true;
+        geo.T = (int)md.n;
+        geo.R = (int)md.n;
+        geo.HL = geo.HR = 0;
+        geo.ntiles = 1;
+    } else {
+        geo.resident = false;
+        // tile: 4096 points (L96) / 8192 (stencils) when it fits, halo <= T/4
+        int T = (int)std::min<int64_t>(smem_cap * 3 / 4, KIND == WC4DVAR_MODEL_LORENZ96 ? 4096 : 8192);
+        if (tile_override > 0) T = tile_override;
+        const int per = md.s * (rl + rr);
+        K = std::max(1, std::min<int>(md.N, (int)((smem_cap - T) / std::max(per, 1))));
+        while (K > 1 && per * K > std::max(T / 4, per)) --K;
+        geo.T = T;
+        geo.HL = K * md.s * rl;
+        geo.HR = K * md.s * rr;
+        geo.R = T + geo.HL + geo.HR;
+        require(geo.R <= smem_cap, "tiled sweep: halo does not fit shared memory");
+        geo.ntiles = cdiv(md.n, T);
+    }
+    const size_t smem = sizeof(double) * (size_t)nbuf * geo.R;
+    auto fk = tiled_fwd_kernel<KIND>;
+    auto ak = tiled_adj_kernel<KIND>;
+    W4_CUDA(cudaFuncSetAttribute(fk, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    W4_CUDA(cudaFuncSetAttribute(ak, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    const int nl = geo.resident ? 1 : (int)cdiv(md.N, K);
+    double* bbuf = nullptr;
+    if (nl > 1) bbuf = ws.get<double>((size_t)2 * md.n * a.m);
+    const dim3 grid((unsigned)a.m, (unsigned)geo.ntiles);
+    TiledArgs ta{md, net, a, geo, 0, 0, nullptr, nullptr};
+    if (a.do_fwd) {
+        for (int l = 0; l < nl; ++l) {
+            ta.i0 = l * K;
+            ta.i1 = std::min(md.N, (l + 1) * K);
+            ta.bin = l == 0 ? nullptr : bbuf + (size_t)((l + 1) % 2) * md.n * a.m;
+            ta.bout = l + 1 < nl ? bbuf + (size_t)(l % 2) * md.n * a.m : nullptr;
+            fk<<<grid, kThreads, smem, st>>>(ta, status);
+            W4_LAUNCH();
+        }
+    }
+    if (a.do_adj) {  // mirrored radius: same region size, origin shifted (see kernel)
+        for (int l = 0; l < nl; ++l) {
+            ta.i1 = md.N - l * K;
+            ta.i0 = std::max(0, md.N - (l + 1) * K);
+            ta.bin = l == 0 ? nullptr : bbuf + (size_t)((l + 1) % 2) * md.n * a.m;
+            ta.bout = l + 1 < nl ? bbuf + (size_t)(l % 2) * md.n * a.m : nullptr;
+            ak<<<grid, kThreads, smem, st>>>(ta, status);
+            W4_LAUNCH();
+        }
+    }
+}
+
+}  // namespace
+
+void sweep_tiled(const ModelDev& md, const NetDev& net, const SweepArgs& a, unsigned* status,
+                 cudaStream_t st, DevBuf& ws, int tov) {
+    if (a.m == 0) return;
+    switch (md.kind) {
+        case WC4DVAR_MODEL_IDENTITY: launch_tiled<WC4DVAR_MODEL_IDENTITY>(md, net, a, status, st, ws, tov); break;
+        case WC4DVAR_MODEL_ADVECTION: launch_tiled<WC4DVAR_MODEL_ADVECTION>(md, net, a, status, st, ws, tov); break;
+        case WC4DVAR_MODEL_ADVDIFF: launch_tiled<WC4DVAR_MODEL_ADVDIFF>(md, net, a, status, st, ws, tov); break;
+        case WC4DVAR_MODEL_LORENZ96: launch_tiled<WC4DVAR_MODEL_LORENZ96>(md, net, a, status, st, ws, tov); break;
+        default: throw InvalidArgument("sweep: unknown model kind");
+    }
+}
+
+}  // namespace w4

@@ -244,6 +244,54 @@ def AdvDiffLinearized(n: int, N: int, courant: float, diffusion: float, substeps
     return LinearizedModel("advdiff", n, N, substeps, courant, diffusion)
 
 
+def lorenz96_rhs(x: np.ndarray, forcing: float) -> np.ndarray:
+    """models.cpp:59-70 (same evaluation order, vectorised)."""
+    xm2, xm1, xp1 = np.roll(x, 2), np.roll(x, 1), np.roll(x, -1)
+    return -xm2 * xm1 + xm1 * xp1 - x + forcing
+
+
+def lorenz96_step(x: np.ndarray, forcing: float, dt: float) -> np.ndarray:
+    """models.cpp:72-78 (RK4)."""
+    k1 = lorenz96_rhs(x, forcing)
+    k2 = lorenz96_rhs(x + 0.5 * dt * k1, forcing)
+    k3 = lorenz96_rhs(x + 0.5 * dt * k2, forcing)
+    k4 = lorenz96_rhs(x + dt * k3, forcing)
+    return x + (dt / 6.0) * (k1 + 2.0 * k2 + 2.0 * k3 + k4)
+
+
+def lorenz96_stages(x: np.ndarray, forcing: float, dt: float) -> np.ndarray:
+    """Lorenz96Stages::at, models.cpp:80-87 -> [x1 | x2 | x3 | x4]."""
+    x1 = x
+    x2 = x + 0.5 * dt * lorenz96_rhs(x1, forcing)
+    x3 = x + 0.5 * dt * lorenz96_rhs(x2, forcing)
+    x4 = x + dt * lorenz96_rhs(x3, forcing)
+    return np.concatenate([x1, x2, x3, x4])
+
+
+def Lorenz96Linearized(trajectory: np.ndarray, forcing: float, dt: float, substeps: int = 1):
+    """operators.cpp:44-51: stages precomputed on the host at construction, as in the
+    reference.  ``trajectory`` holds N*s + 1 states (n x (N*s+1)); s = 1 is the reference."""
+    trajectory = np.asarray(trajectory, dtype=np.float64)
+    require(trajectory.ndim == 2 and trajectory.shape[1] >= 2, "Lorenz96Linearized: trajectory too short")
+    n, total = trajectory.shape[0], trajectory.shape[1] - 1
+    require(total % substeps == 0, "Lorenz96Linearized: trajectory/sub-step mismatch")
+    stages = np.concatenate([lorenz96_stages(trajectory[:, c], forcing, dt) for c in range(total)])
+    return LinearizedModel("l96", n, total // substeps, substeps, dt=dt, stages=stages)
+
+
+def lorenz96_trajectory(x0: np.ndarray, forcing: float, dt: float, spinup: int, steps: int) -> np.ndarray:
+    """Spin x0 up for `spinup` RK4 steps, then return the next `steps` + 1 states (n x (steps+1))."""
+    x = np.asarray(x0, dtype=np.float64)
+    for _ in range(spinup):
+        x = lorenz96_step(x, forcing, dt)
+    traj = np.empty((len(x), steps + 1))
+    traj[:, 0] = x
+    for c in range(steps):
+        x = lorenz96_step(x, forcing, dt)
+        traj[:, c + 1] = x
+    return traj
+
+
 _MODEL_KIND = {"identity": 0, "advection": 1, "advdiff": 2, "l96": 3}
 
 
