@@ -45,8 +45,8 @@ __host__ __device__ inline void model_radius(int kind, int& rl, int& rr) {
 struct Region {
     int R;
     bool resident;
-    int64_t origin;  // global grid index of region element 0
-    int64_t n;
+    int origin;  // global grid index of region element 0 (|origin| < n)
+    int n;       // grid points (n < 2^31)
     __device__ __forceinline__ int nb(int e, int d) const {  // neighbour index in SMEM
         if (!resident) return e + d;
         int x = e + d;
@@ -54,12 +54,9 @@ struct Region {
         else if (x >= R) x -= R;
         return x;
     }
-    __device__ __forceinline__ int64_t gidx(int e) const {
-        int64_t g = origin + e;
-        g %= n;
-        if (g < 0) g += n;
-        return g;
-    }
+    // division-free periodic wrap of a grid index in (-n, 2n)
+    __device__ __forceinline__ int wrap(int g) const { return g < 0 ? g + n : (g >= n ? g - n : g); }
+    __device__ __forceinline__ int gidx(int e) const { return wrap(origin + e); }
 };
 
 // ---------------------------------------------------------------- single-phase stencils
@@ -80,17 +77,15 @@ __device__ __forceinline__ double stencil1(const double* __restrict__ u, const R
 // with the stage x given as a global pointer indexed by grid point and the vector in SMEM.
 __device__ __forceinline__ double l96_jac(const double* __restrict__ x, const double* __restrict__ v,
                                           const Region& rg, int e) {
-    const int64_t g = rg.gidx(e);
-    const int64_t n = rg.n;
-    const int64_t gm2 = (g + n - 2) % n, gm1 = (g + n - 1) % n, gp1 = (g + 1) % n;
+    const int g = rg.gidx(e);
+    const int gm2 = rg.wrap(g - 2), gm1 = rg.wrap(g - 1), gp1 = rg.wrap(g + 1);
     const double vm2 = v[rg.nb(e, -2)], vm1 = v[rg.nb(e, -1)], vp1 = v[rg.nb(e, 1)], vc = v[e];
     return -vm2 * x[gm1] - x[gm2] * vm1 + vm1 * x[gp1] + x[gm1] * vp1 - vc;
 }
 __device__ __forceinline__ double l96_jac_t(const double* __restrict__ x, const double* __restrict__ l,
                                             const Region& rg, int e, double scale) {
-    const int64_t g = rg.gidx(e);
-    const int64_t n = rg.n;
-    const int64_t gm2 = (g + n - 2) % n, gm1 = (g + n - 1) % n, gp1 = (g + 1) % n, gp2 = (g + 2) % n;
+    const int g = rg.gidx(e);
+    const int gm2 = rg.wrap(g - 2), gm1 = rg.wrap(g - 1), gp1 = rg.wrap(g + 1), gp2 = rg.wrap(g + 2);
     const double lp2 = scale * l[rg.nb(e, 2)], lp1 = scale * l[rg.nb(e, 1)];
     const double lm1 = scale * l[rg.nb(e, -1)], lc = scale * l[e];
     return -x[gp1] * lp2 + (x[gp2] - x[gm1]) * lp1 + x[gm2] * lm1 - lc;
@@ -125,7 +120,7 @@ __global__ void __launch_bounds__(kThreads) tiled_fwd_kernel(const TiledArgs ta,
     const int64_t tile = blockIdx.y;
     const int64_t t0 = tile * geo.T;
     const int tid = threadIdx.x, nt = blockDim.x;
-    Region rg{R, geo.resident, geo.resident ? 0 : t0 - geo.HL, n};
+    Region rg{R, geo.resident, geo.resident ? 0 : (int)(t0 - geo.HL), (int)n};
     const int c_lo = geo.resident ? 0 : geo.HL;                   // tile centre in SMEM
     const int c_hi = geo.resident ? R : geo.HL + (int)(n - t0 < (int64_t)geo.T ? n - t0 : (int64_t)geo.T);
     int rl, rr;
@@ -140,13 +135,13 @@ __global__ void __launch_bounds__(kThreads) tiled_fwd_kernel(const TiledArgs ta,
     // state x_{i0} on the region
     const double* src = ta.bin ? ta.bin + col * n : X;  // x_0 = X_0
     for (int e = tid; e < R; e += nt) {
-        const int64_t g = rg.gidx(e);
+        const int g = rg.gidx(e);
         cur[e] = src[g];
     }
     if (ta.i0 == 0) {  // x_0 is part of the trajectory (finite check, traj, obs at t_0)
         const int sl = net.slot[0];
         for (int e = c_lo + tid; e < c_hi; e += nt) {
-            const int64_t g = rg.gidx(e);
+            const int g = rg.gidx(e);
             const double x = cur[e];
             bad |= !isfinite(x);
             if (tr) tr[g] = x;
@@ -203,7 +198,7 @@ __global__ void __launch_bounds__(kThreads) tiled_fwd_kernel(const TiledArgs ta,
                 const int sl = net.slot[i + 1];
                 double* trn = tr ? tr + (int64_t)(i + 1) * n : nullptr;
                 for (int e = lo + tid; e < hi; e += nt) {
-                    const int64_t g = rg.gidx(e);
+                    const int g = rg.gidx(e);
                     const double x = nxt[e] + Xn[g];
                     nxt[e] = x;
                     if (e >= c_lo && e < c_hi) {
@@ -251,7 +246,7 @@ __global__ void __launch_bounds__(kThreads) tiled_adj_kernel(const TiledArgs ta,
     model_radius(md.kind, rr, rl);
     const int HL = geo.resident ? 0 : geo.HR, HRr = geo.resident ? 0 : geo.HL;
     (void)HRr;
-    Region rg{R, geo.resident, geo.resident ? 0 : t0 - HL, n};
+    Region rg{R, geo.resident, geo.resident ? 0 : (int)(t0 - HL), (int)n};
     const int c_lo = geo.resident ? 0 : HL;
     const int c_hi = geo.resident ? R : HL + (int)(n - t0 < (int64_t)geo.T ? n - t0 : (int64_t)geo.T);
     const int s = md.s;
@@ -261,7 +256,7 @@ __global__ void __launch_bounds__(kThreads) tiled_adj_kernel(const TiledArgs ta,
     const int np = net.n_points;
     bool bad = false;
 
-    auto addend = [&](int i, int64_t g) -> double {
+    auto addend = [&](int i, int g) -> double {
         double x = V ? V[(int64_t)i * n + g] : 0.0;
         if (a.adj_obs) {
             const int sl = net.slot[i];
@@ -278,7 +273,7 @@ __global__ void __launch_bounds__(kThreads) tiled_adj_kernel(const TiledArgs ta,
         for (int e = tid; e < R; e += nt) cur[e] = ta.bin[col * n + rg.gidx(e)];
     } else {  // s_N = v_N + H_N^T y
         for (int e = tid; e < R; e += nt) {
-            const int64_t g = rg.gidx(e);
+            const int g = rg.gidx(e);
             const double x = addend(ta.i1, g);
             cur[e] = x;
             if (e >= c_lo && e < c_hi) {
@@ -332,7 +327,7 @@ __global__ void __launch_bounds__(kThreads) tiled_adj_kernel(const TiledArgs ta,
             if (last) {
                 // s_i = v_i + H_i^T y + M_i^T s_{i+1}  (operators.cpp:99)
                 for (int e = lo + tid; e < hi; e += nt) {
-                    const int64_t g = rg.gidx(e);
+                    const int g = rg.gidx(e);
                     const double x = addend(i, g) + nxt[e];
                     nxt[e] = x;
                     if (e >= c_lo && e < c_hi) {
@@ -352,6 +347,253 @@ __global__ void __launch_bounds__(kThreads) tiled_adj_kernel(const TiledArgs ta,
     if (__syncthreads_or(bad) && tid == 0) atomicOr(status, ST_ADJ_NONFINITE);
 }
 
+// ---------------------------------------------------------------- register-blocked tiles
+// Radius-1 models with S sub-steps per interval: each thread owns P consecutive region
+// points, gathers them with an S-point halo from SMEM once per interval and advances the
+// S sub-steps in registers (one barrier per interval instead of per sub-step).  Region
+// R = nt * P = T + 2 K S; the valid region shrinks by S per side per interval.
+template <int KIND>
+__device__ __forceinline__ double tl3t(double l, double c, double r, double cc, double dd) {
+    if (KIND == WC4DVAR_MODEL_IDENTITY) return c;
+    if (KIND == WC4DVAR_MODEL_ADVECTION) return c - cc * (c - l);
+    return c - cc * (c - l) + dd * (r - 2.0 * c + l);
+}
+template <int KIND>
+__device__ __forceinline__ double adj3t(double l, double c, double r, double cc, double dd) {
+    if (KIND == WC4DVAR_MODEL_IDENTITY) return c;
+    if (KIND == WC4DVAR_MODEL_ADVECTION) return (1.0 - cc) * c + cc * r;
+    return c - cc * (c - r) + dd * (l - 2.0 * c + r);
+}
+
+template <int KIND, int S, int P, bool ADJ>
+__device__ __forceinline__ void blk_advance(const double* __restrict__ cur, int b, int R, double cc,
+                                            double dd, double (&v)[P + 2 * S]) {
+    constexpr int L = P + 2 * S;
+#pragma unroll
+    for (int u = 0; u < L; ++u) {
+        int j = b - S + u;
+        j = j < 0 ? 0 : (j >= R ? R - 1 : j);  // clamped lanes feed only discarded points
+        v[u] = cur[j];
+    }
+#pragma unroll
+    for (int k = 0; k < S; ++k) {
+        double prev = v[k];
+#pragma unroll
+        for (int u = k + 1; u < L - k - 1; ++u) {
+            const double c = v[u];
+            v[u] = ADJ ? adj3t<KIND>(prev, c, v[u + 1], cc, dd) : tl3t<KIND>(prev, c, v[u + 1], cc, dd);
+            prev = c;
+        }
+    }
+}
+
+template <int KIND, int S, int P>
+__global__ void __launch_bounds__(512) tiled_blk_fwd_kernel(const TiledArgs ta, unsigned* status) {
+    extern __shared__ double sm[];
+    const ModelDev& md = ta.md;
+    const NetDev& net = ta.net;
+    const SweepArgs& a = ta.a;
+    const TileGeom& geo = ta.geo;
+    const int R = geo.R;
+    double* cur = sm;
+    double* nxt = sm + R;
+    const int n = (int)md.n;
+    const int64_t col = blockIdx.x;
+    const int64_t t0 = (int64_t)blockIdx.y * geo.T;
+    const int tid = threadIdx.x, nt = blockDim.x;
+    const Region rg{R, false, (int)(t0 - geo.HL), n};
+    const int c_lo = geo.HL;
+    const int c_hi = geo.HL + (int)((int64_t)n - t0 < geo.T ? (int64_t)n - t0 : geo.T);
+    const double* X = a.X + col * a.ldx;
+    double* Yc = a.Y ? a.Y + col * net.q : nullptr;
+    double* tr = a.traj ? a.traj + col * a.ldtraj : nullptr;
+    const int np = net.n_points;
+    const int b = tid * P;
+    bool bad = false;
+    double v[P + 2 * S];
+
+    const double* src = ta.bin ? ta.bin + col * n : X;
+    for (int e = tid; e < R; e += nt) cur[e] = src[rg.gidx(e)];
+    if (ta.i0 == 0) {
+        const int sl = net.slot[0];
+        for (int e = c_lo + tid; e < c_hi; e += nt) {
+            const int g = rg.gidx(e);
+            const double x = cur[e];
+            bad |= !isfinite(x);
+            if (tr) tr[g] = x;
+            if (a.fwd_obs && sl >= 0) {
+                const int bb = net.pmap[g];
+                if (bb >= 0) Yc[(int64_t)sl * np + bb] = a.scale_fwd * x;
+            }
+        }
+    }
+    __syncthreads();
+    int lo = 0, hi = R;
+    for (int i = ta.i0; i < ta.i1; ++i) {
+        lo += S;
+        hi -= S;
+        const double* Xn = X + (int64_t)(i + 1) * n;
+        const int sl = net.slot[i + 1];
+        double* trn = tr ? tr + (int64_t)(i + 1) * n : nullptr;
+        if (b + P > lo && b < hi) {
+            blk_advance<KIND, S, P, false>(cur, b, R, md.c, md.d, v);
+#pragma unroll
+            for (int p = 0; p < P; ++p) {
+                const int e = b + p;
+                if (e >= lo && e < hi) {
+                    const int g = rg.gidx(e);
+                    const double x = v[S + p] + Xn[g];  // operators.cpp:88
+                    nxt[e] = x;
+                    if (e >= c_lo && e < c_hi) {
+                        bad |= !isfinite(x);
+                        if (trn) trn[g] = x;
+                        if (a.fwd_obs && sl >= 0) {
+                            const int bb = net.pmap[g];
+                            if (bb >= 0) Yc[(int64_t)sl * np + bb] = a.scale_fwd * x;
+                        }
+                    }
+                }
+            }
+        }
+        __syncthreads();
+        double* t = cur;
+        cur = nxt;
+        nxt = t;
+    }
+    if (ta.bout)
+        for (int e = c_lo + tid; e < c_hi; e += nt) ta.bout[col * n + rg.gidx(e)] = cur[e];
+    if (__syncthreads_or(bad) && tid == 0) atomicOr(status, ST_FWD_NONFINITE);
+}
+
+template <int KIND, int S, int P>
+__global__ void __launch_bounds__(512) tiled_blk_adj_kernel(const TiledArgs ta, unsigned* status) {
+    extern __shared__ double sm[];
+    const ModelDev& md = ta.md;
+    const NetDev& net = ta.net;
+    const SweepArgs& a = ta.a;
+    const TileGeom& geo = ta.geo;
+    const int R = geo.R;
+    double* cur = sm;
+    double* nxt = sm + R;
+    const int n = (int)md.n;
+    const int64_t col = blockIdx.x;
+    const int64_t t0 = (int64_t)blockIdx.y * geo.T;
+    const int tid = threadIdx.x, nt = blockDim.x;
+    const Region rg{R, false, (int)(t0 - geo.HR), n};
+    const int c_lo = geo.HR;
+    const int c_hi = geo.HR + (int)((int64_t)n - t0 < geo.T ? (int64_t)n - t0 : geo.T);
+    const double* V = a.V ? a.V + col * a.ldv : nullptr;
+    const double* Yc = a.Y ? a.Y + col * net.q : nullptr;
+    double* Sv = a.S + col * a.lds;
+    const int np = net.n_points;
+    const int b = tid * P;
+    bool bad = false;
+    double v[P + 2 * S];
+    auto addend = [&](int i, int g) -> double {
+        double x = V ? V[(int64_t)i * n + g] : 0.0;
+        if (a.adj_obs) {
+            const int sl = net.slot[i];
+            if (sl >= 0) {
+                const int bb = net.pmap[g];
+                if (bb >= 0) x = V ? x + Yc[(int64_t)sl * np + bb] : Yc[(int64_t)sl * np + bb];
+            }
+        }
+        return x;
+    };
+    if (ta.bin) {
+        for (int e = tid; e < R; e += nt) cur[e] = ta.bin[col * n + rg.gidx(e)];
+    } else {
+        for (int e = tid; e < R; e += nt) {
+            const int g = rg.gidx(e);
+            const double x = addend(ta.i1, g);
+            cur[e] = x;
+            if (e >= c_lo && e < c_hi) {
+                Sv[(int64_t)ta.i1 * n + g] = x;
+                bad |= !isfinite(x);
+            }
+        }
+    }
+    __syncthreads();
+    int lo = 0, hi = R;
+    for (int i = ta.i1 - 1; i >= ta.i0; --i) {
+        lo += S;
+        hi -= S;
+        if (b + P > lo && b < hi) {
+            blk_advance<KIND, S, P, true>(cur, b, R, md.c, md.d, v);
+#pragma unroll
+            for (int p = 0; p < P; ++p) {
+                const int e = b + p;
+                if (e >= lo && e < hi) {
+                    const int g = rg.gidx(e);
+                    const double x = addend(i, g) + v[S + p];  // operators.cpp:99
+                    nxt[e] = x;
+                    if (e >= c_lo && e < c_hi) {
+                        Sv[(int64_t)i * n + g] = x;
+                        bad |= !isfinite(x);
+                    }
+                }
+            }
+        }
+        __syncthreads();
+        double* t = cur;
+        cur = nxt;
+        nxt = t;
+    }
+    if (ta.bout)
+        for (int e = c_lo + tid; e < c_hi; e += nt) ta.bout[col * n + rg.gidx(e)] = cur[e];
+    if (__syncthreads_or(bad) && tid == 0) atomicOr(status, ST_ADJ_NONFINITE);
+}
+
+// Register-blocked tiled launch (radius-1 models, S in {1,5,10}); false if not applicable.
+template <int KIND, int S>
+bool launch_tiled_blk(const ModelDev& md, const NetDev& net, const SweepArgs& a, unsigned* status,
+                      cudaStream_t st, DevBuf& ws, int tile_override) {
+    constexpr int P = 8;
+    int nt = 512;
+    int K = md.N;
+    int R = nt * P;
+    while (K > 1 && 2 * K * S > R / 4) --K;
+    int T = R - 2 * K * S;
+    if (tile_override > 0) {
+        T = tile_override;
+        K = std::max(1, std::min(md.N, std::max(T / (8 * S), 1)));
+        R = T + 2 * K * S;
+        nt = (int)cdiv(R, P);
+        R = nt * P;
+        T = R - 2 * K * S;
+    }
+    if (nt > 512 || T <= 0 || R > md.n) return false;
+    TileGeom geo{T, K * S, K * S, R, false, cdiv(md.n, T)};
+    const size_t smem = sizeof(double) * 2 * (size_t)R;
+    auto fk = tiled_blk_fwd_kernel<KIND, S, P>;
+    auto ak = tiled_blk_adj_kernel<KIND, S, P>;
+    W4_CUDA(cudaFuncSetAttribute(fk, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    W4_CUDA(cudaFuncSetAttribute(ak, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    const int nl = (int)cdiv(md.N, K);
+    double* bbuf = nl > 1 ? ws.get<double>((size_t)2 * md.n * a.m) : nullptr;
+    const dim3 grid((unsigned)a.m, (unsigned)geo.ntiles);
+    TiledArgs ta{md, net, a, geo, 0, 0, nullptr, nullptr};
+    if (a.do_fwd)
+        for (int l = 0; l < nl; ++l) {
+            ta.i0 = l * K;
+            ta.i1 = std::min(md.N, (l + 1) * K);
+            ta.bin = l == 0 ? nullptr : bbuf + (size_t)((l + 1) % 2) * md.n * a.m;
+            ta.bout = l + 1 < nl ? bbuf + (size_t)(l % 2) * md.n * a.m : nullptr;
+            fk<<<grid, nt, smem, st>>>(ta, status);
+            W4_LAUNCH();
+        }
+    if (a.do_adj)
+        for (int l = 0; l < nl; ++l) {
+            ta.i1 = md.N - l * K;
+            ta.i0 = std::max(0, md.N - (l + 1) * K);
+            ta.bin = l == 0 ? nullptr : bbuf + (size_t)((l + 1) % 2) * md.n * a.m;
+            ta.bout = l + 1 < nl ? bbuf + (size_t)(l % 2) * md.n * a.m : nullptr;
+            ak<<<grid, nt, smem, st>>>(ta, status);
+            W4_LAUNCH();
+        }
+    return true;
+}
+
 template <int KIND>
 void launch_tiled(const ModelDev& md, const NetDev& net, const SweepArgs& a, unsigned* status,
                   cudaStream_t st, DevBuf& ws, int tile_override) {
@@ -368,6 +610,16 @@ void launch_tiled(const ModelDev& md, const NetDev& net, const SweepArgs& a, uns
         geo.HL = geo.HR = 0;
         geo.ntiles = 1;
     } else {
+        if (KIND != WC4DVAR_MODEL_LORENZ96) {
+            bool done = false;
+            switch (md.s) {
+                case 1: done = launch_tiled_blk<KIND, 1>(md, net, a, status, st, ws, tile_override); break;
+                case 5: done = launch_tiled_blk<KIND, 5>(md, net, a, status, st, ws, tile_override); break;
+                case 10: done = launch_tiled_blk<KIND, 10>(md, net, a, status, st, ws, tile_override); break;
+                default: break;
+            }
+            if (done) return;
+        }
         geo.resident = false;
         // tile: 4096 points (L96) / 8192 (stencils) when it fits, halo <= T/4
         int T = (int)std::min<int64_t>(smem_cap * 3 / 4, KIND == WC4DVAR_MODEL_LORENZ96 ? 4096 : 8192);
@@ -380,6 +632,7 @@ void launch_tiled(const ModelDev& md, const NetDev& net, const SweepArgs& a, uns
         geo.HR = K * md.s * rr;
         geo.R = T + geo.HL + geo.HR;
         require(geo.R <= smem_cap, "tiled sweep: halo does not fit shared memory");
+        require(geo.R <= md.n, "tiled sweep: tile plus halo exceeds the periodic domain");
         geo.ntiles = cdiv(md.n, T);
     }
     const size_t smem = sizeof(double) * (size_t)nbuf * geo.R;
