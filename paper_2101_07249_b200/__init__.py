@@ -10,5 +10,6 @@ from .wc4dvar import (  # noqa: F401
     QuadraticCost, RitzPairs, SketchConfig, assemble_dense, build_spectral_lmp, gaussian_matrix,
     last_sketch_timing, nystrom, pcg_split, probe_dmma_peak, rayleigh_ritz, revd, revd_ritzit,
     sketch_eigenpairs, version, LIB_PATH, SIGNATURES, Lorenz96Linearized, lorenz96_rhs,
-    lorenz96_stages, lorenz96_step, lorenz96_trajectory,
+    lorenz96_stages, lorenz96_step, lorenz96_trajectory, InnerLoopReport, PrecondSpec, SolverSpec,
+    run_inner_loop,
 )

@@ -1,6 +1,7 @@
 // fp64 DMMA GEMM kernels (see gemm.cuh).
 #include "gemm.cuh"
 
+#include <cstdlib>
 #include <map>
 #include <mutex>
 
@@ -398,6 +399,196 @@ void launch_sym(const PassTable& tab, int64_t ntiles, unsigned* status, cudaStre
 }
 
 // ---------------------------------------------------------------------------
+// Warp-specialised symmetric-A kernel: one producer warp streams the A / B tiles with
+// cp.async into a STAGES-deep ring and signals per-stage "full" mbarriers
+// (cp.async.mbarrier.arrive.noinc); 16 consumer warps wait on "full", run the DMMA k-steps
+// and release the stage through "empty" mbarriers.  No block-wide barrier in the main
+// loop, so the tensor pipe is not drained every k-tile.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ unsigned smem_u32(const void* p) {
+    return static_cast<unsigned>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* b, unsigned count) {
+    asm volatile("mbarrier.init.shared.b64 [%0], %1;\n" ::"r"(smem_u32(b)), "r"(count));
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* b) {
+    asm volatile("mbarrier.arrive.shared.b64 _, [%0];\n" ::"r"(smem_u32(b)) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_cp_async(uint64_t* b) {
+    asm volatile("cp.async.mbarrier.arrive.noinc.shared.b64 [%0];\n" ::"r"(smem_u32(b)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* b, unsigned parity) {
+    asm volatile(
+        "{\n"
+        ".reg .pred P1;\n"
+        "WAIT_%=:\n"
+        "mbarrier.try_wait.parity.shared.b64 P1, [%0], %1;\n"
+        "@!P1 bra WAIT_%=;\n"
+        "}\n" ::"r"(smem_u32(b)),
+        "r"(parity)
+        : "memory");
+}
+
+template <int BM, int BN, int WM, int WN, int STAGES>
+__global__ void __launch_bounds__(WM * WN * 32 + 32, 1)
+    gemm_sym_ws_kernel(const PassTable tab, unsigned* __restrict__ status) {
+    constexpr int NC = WM * WN * 32;  // consumer threads
+    constexpr int WTM = BM / WM, WTN = BN / WN;
+    constexpr int MI = WTM / 16, NI = WTN / 8;
+    constexpr int A_ELEMS = BM * KS, B_ELEMS = BN * KS;
+    static_assert(BM % 32 == 0 && BN % 32 == 0, "tile");
+    extern __shared__ __align__(16) double smem[];
+    double* As = smem;
+    double* Bs = smem + STAGES * A_ELEMS;
+    uint64_t* full = reinterpret_cast<uint64_t*>(Bs + STAGES * B_ELEMS);
+    uint64_t* empty = full + STAGES;
+
+    int64_t tile = blockIdx.x;
+    const int pi = tile >= tab.tile_start[1] ? 1 : 0;
+    const GemmPass& P = tab.p[pi];
+    tile -= tab.tile_start[pi];
+    const int64_t tm = tile % tab.tiles_m[pi];
+    const int64_t tn = tile / tab.tiles_m[pi];
+    const int64_t m0 = tm * BM, n0 = tn * BN;
+    const int64_t M = P.M, K = P.K, ncols = P.ncols;
+    const int64_t ktiles = (K + BK - 1) / BK;
+
+    const int tid = threadIdx.x;
+    const int warp = tid >> 5, lane = tid & 31;
+    if (tid == 0) {
+        for (int s = 0; s < STAGES; ++s) {
+            mbar_init(&full[s], 32);
+            mbar_init(&empty[s], WM * WN);
+        }
+    }
+    __syncthreads();
+
+    if (warp == WM * WN) {
+        // ===== producer warp =====
+        // Each warp instruction copies 4 rows x 128 B (8 lanes per row, lane owns chunk
+        // lane & 7 of rows (lane >> 3) + 4u), so a quarter-warp's 16-byte SMEM writes cover
+        // one contiguous 128 B row.  Row pointers are arithmetic; the column map's division
+        // is done once per lane and advanced incrementally.
+        const int ch = lane & 7, r0 = lane >> 3;
+        constexpr int U = BM / 4;
+        static_assert(BM == BN, "producer assumes square tiles");
+        const int64_t ld = P.lda;
+        const ColMap& im = P.in;
+        for (int64_t kt = 0; kt < ktiles; ++kt) {
+            const int s = (int)(kt % STAGES);
+            const unsigned ph = (unsigned)((kt / STAGES) & 1);
+            mbar_wait(&empty[s], ph ^ 1u);
+            const int64_t k0 = kt * BK;
+            const int64_t kr = k0 + 2 * ch;
+            const int64_t rem = K - kr;
+            const int kval = rem >= 2 ? 2 : (rem > 0 ? (int)rem : 0);
+            double* as = As + s * A_ELEMS + r0 * KS + 2 * ch;
+            double* bs = Bs + s * B_ELEMS + r0 * KS + 2 * ch;
+            int64_t row = m0 + r0;
+            const double* ap = P.A + row * ld + kr;  // column `row` of A == row (symmetric)
+            int64_t c = n0 + r0;
+            int64_t cq = c / im.per, cr = c % im.per;
+#pragma unroll 4
+            for (int u = 0; u < U; ++u) {
+                cp_async_vec<2>(as + u * 4 * KS, ap, row < M ? kval : 0, P.A);
+                const double* bp = im.base + cq * im.ld_outer + (im.off + cr) * im.stride + kr;
+                cp_async_vec<2>(bs + u * 4 * KS, bp, c < ncols ? kval : 0, P.A);
+                row += 4;
+                ap += 4 * ld;
+                c += 4;
+                cr += 4;
+                while (cr >= im.per) {
+                    cr -= im.per;
+                    ++cq;
+                }
+            }
+            mbar_arrive_cp_async(&full[s]);
+        }
+        cp_wait<0>();
+        return;
+    }
+
+    // ===== consumer warps =====
+    const int wm = warp % WM, wn = warp / WM;
+    const int g = lane >> 2, t0 = lane & 3;
+    double acc[MI][NI][4];
+#pragma unroll
+    for (int i = 0; i < MI; ++i)
+#pragma unroll
+        for (int j = 0; j < NI; ++j)
+#pragma unroll
+            for (int v = 0; v < 4; ++v) acc[i][j][v] = 0.0;
+
+    for (int64_t kt = 0; kt < ktiles; ++kt) {
+        const int s = (int)(kt % STAGES);
+        const unsigned ph = (unsigned)((kt / STAGES) & 1);
+        mbar_wait(&full[s], ph);
+        const double* as = As + s * A_ELEMS;
+        const double* bs = Bs + s * B_ELEMS;
+#pragma unroll
+        for (int k8 = 0; k8 < BK; k8 += 8) {
+            double af[MI][4], bf[NI][2];
+#pragma unroll
+            for (int i = 0; i < MI; ++i) {
+                const int r = wm * WTM + i * 16 + g;
+                const double2 lo = *reinterpret_cast<const double2*>(as + r * KS + k8 + 2 * t0);
+                const double2 hi = *reinterpret_cast<const double2*>(as + (r + 8) * KS + k8 + 2 * t0);
+                af[i][0] = lo.x;
+                af[i][2] = lo.y;
+                af[i][1] = hi.x;
+                af[i][3] = hi.y;
+            }
+#pragma unroll
+            for (int j = 0; j < NI; ++j) {
+                const int c = wn * WTN + j * 8 + g;
+                const double2 bb = *reinterpret_cast<const double2*>(bs + c * KS + k8 + 2 * t0);
+                bf[j][0] = bb.x;
+                bf[j][1] = bb.y;
+            }
+            mma_k8(acc, af, bf);
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[s]);
+    }
+
+    bool bad = false;
+    const double alpha = P.alpha;
+#pragma unroll
+    for (int j = 0; j < NI; ++j) {
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            const int64_t c = n0 + wn * WTN + j * 8 + 2 * t0 + h;
+            if (c >= ncols) continue;
+            double* outc = const_cast<double*>(P.out.col(c));
+            const double* addc = P.add.base ? P.add.col(c) : nullptr;
+#pragma unroll
+            for (int i = 0; i < MI; ++i) {
+#pragma unroll
+                for (int v = 0; v < 2; ++v) {
+                    const int64_t r = m0 + wm * WTM + i * 16 + g + 8 * v;
+                    if (r >= M) continue;
+                    double val = alpha * acc[i][j][2 * v + h];
+                    if (addc) val = addc[r] + val;
+                    bad |= !isfinite(val);
+                    outc[r] = val;
+                }
+            }
+        }
+    }
+    if (status && __any_sync(0xffffffffu, bad) && lane == 0) atomicOr(status, ST_OUT_NONFINITE);
+    (void)NC;
+}
+
+template <int BM, int BN, int WM, int WN, int STAGES>
+void launch_sym_ws(const PassTable& tab, int64_t ntiles, unsigned* status, cudaStream_t stream) {
+    const size_t smem = sizeof(double) * STAGES * (BM * KS + BN * KS) + 2 * STAGES * sizeof(uint64_t);
+    auto kern = gemm_sym_ws_kernel<BM, BN, WM, WN, STAGES>;
+    configure_smem(reinterpret_cast<const void*>(kern), smem);
+    kern<<<(unsigned)ntiles, WM * WN * 32 + 32, smem, stream>>>(tab, status);
+    W4_LAUNCH();
+}
+
+// ---------------------------------------------------------------------------
 // TN split kernel: both tiles stored [col][k] (stride KPAD).
 // Partial (split s) of C tile -> work[s][m2][m1] col-major m1 x m2.
 // ---------------------------------------------------------------------------
@@ -582,7 +773,14 @@ void gemm_nn(const GemmPass* passes, int npass, unsigned* status, cudaStream_t s
             }
         }
         tab.tile_start[2] = start;
-        if (start > 0) launch_sym<128, 128, 4, 4, 3>(tab, start, status, stream);
+        static const int ws_mode = [] {
+            const char* e = std::getenv("WC4DVAR_GEMM_WS");
+            return e ? std::atoi(e) : 1;
+        }();
+        if (start > 0) {
+            if (ws_mode) launch_sym_ws<128, 128, 4, 4, 4>(tab, start, status, stream);
+            else launch_sym<128, 128, 4, 4, 3>(tab, start, status, stream);
+        }
         return;
     }
     // Tile shape: big tiles when there are enough of them to fill the chip twice.

@@ -29,24 +29,25 @@ __global__ void __launch_bounds__(kThreads)
     }
     if (tid == 0) fail = 0;
     __syncthreads();
+    const int wid = tid >> 5, lane = tid & 31, nw = nt >> 5;
     for (int j = 0; j < m; ++j) {
-        if (tid == 0) {
-            const double d = A[j + j * m];
-            if (!(d > 0.0) || !isfinite(d)) fail = j + 1;
-            else A[j + j * m] = sqrt(d);
+        // every thread reads the pivot after the previous barrier: uniform decision
+        const double d = A[j + j * m];
+        if (!(d > 0.0) || !isfinite(d)) {
+            if (tid == 0) fail = j + 1;
+            break;
         }
-        __syncthreads();
-        if (fail) break;
-        const double ljj = A[j + j * m];
+        const double ljj = sqrt(d);
         for (int i = j + 1 + tid; i < m; i += nt) A[i + j * m] /= ljj;
         __syncthreads();
-        const int w = m - j - 1;
-        for (int e = tid; e < w * w; e += nt) {
-            const int i = j + 1 + e % w, k = j + 1 + e / w;
-            if (i >= k) A[i + k * m] -= A[i + j * m] * A[k + j * m];
+        for (int k = j + 1 + wid; k < m; k += nw) {
+            const double lk = A[k + j * m];
+            for (int i = k + lane; i < m; i += 32) A[i + k * m] -= A[i + j * m] * lk;
         }
+        if (tid == 0) A[j + j * m] = ljj;  // the trailing update never reads the diagonal
         __syncthreads();
     }
+    __syncthreads();
     if (!fail)
         for (int e = tid; e < m * m; e += nt) {
             const int r = e % m, c = e / m;  // R(r, c) = L(c, r) for c >= r
@@ -131,6 +132,31 @@ __global__ void __launch_bounds__(kThreads)
 }
 
 // ---------------------------------------------------------------- triangular inverse
+// Single CTA, R staged in SMEM: warp w solves R x = e_j for columns j = w, w + 32, ...
+__global__ void __launch_bounds__(1024)
+    tri_inv_smem_kernel(int m, const double* __restrict__ R, double* __restrict__ Rinv) {
+    extern __shared__ double sm[];
+    double* Rs = sm;                           // m x m
+    const int tid = threadIdx.x, nt = blockDim.x;
+    const int wid = tid >> 5, lane = tid & 31, nw = nt >> 5;
+    double* x = sm + (size_t)m * m + (size_t)wid * m;
+    for (int e = tid; e < m * m; e += nt) Rs[e] = R[e];
+    __syncthreads();
+    for (int j = wid; j < m; j += nw) {
+        if (lane == 0) x[j] = 1.0 / Rs[j + j * m];
+        __syncwarp();
+        for (int i = j - 1; i >= 0; --i) {
+            double s = 0.0;
+            for (int k = i + 1 + lane; k <= j; k += 32) s += Rs[i + k * m] * x[k];
+            s = warp_sum(s);
+            if (lane == 0) x[i] = -s / Rs[i + i * m];
+            __syncwarp();
+        }
+        for (int i = lane; i < m; i += 32) Rinv[i + j * m] = (i <= j) ? x[i] : 0.0;
+        __syncwarp();
+    }
+}
+
 __global__ void tri_inv_kernel(int m, const double* __restrict__ R, double* __restrict__ Rinv) {
     extern __shared__ double xs[];
     const int warps = blockDim.x / 32;
@@ -288,7 +314,10 @@ __global__ void __launch_bounds__(kEvdThreads)
                 double c = 1.0, s = 0.0;
                 const double apq = A[p + q * mp];
                 const double app = A[p + p * mp], aqq = A[q + q * mp];
-                if (apq != 0.0 && fabs(apq) > DBL_EPSILON * 0.5 * sqrt(fabs(app * aqq))) {
+                // Rotation threshold m*eps*sqrt|a_pp a_qq| (relative accuracy m*eps); a
+                // pure eps threshold lets roundoff re-create above-threshold entries so the
+                // sweep never goes quiet.
+                if (apq != 0.0 && fabs(apq) > mp * DBL_EPSILON * sqrt(fabs(app * aqq))) {
                     const double tau = (aqq - app) / (2.0 * apq);
                     const double t = (tau >= 0.0 ? 1.0 : -1.0) / (fabs(tau) + sqrt(1.0 + tau * tau));
                     c = 1.0 / sqrt(1.0 + t * t);
@@ -301,8 +330,9 @@ __global__ void __launch_bounds__(kEvdThreads)
                 cs_q[k] = q;
             }
             __syncthreads();
-            for (int e = tid; e < npairs * npairs; e += nt) {
-                const int P = e % npairs, Q = e / npairs;
+            const int wid = tid >> 5, lane = tid & 31, nw = nt >> 5;
+            for (int Q = wid; Q < npairs; Q += nw)
+            for (int P = lane; P < npairs; P += 32) {
                 const double sP = cs_s[P], sQ = cs_s[Q];
                 if (sP == 0.0 && sQ == 0.0) continue;
                 const double cP = cs_c[P], cQ = cs_c[Q];
@@ -316,8 +346,8 @@ __global__ void __launch_bounds__(kEvdThreads)
                 A[p1 + q2 * mp] = cP * b12 - sP * b22;
                 A[p2 + q2 * mp] = sP * b12 + cP * b22;
             }
-            for (int e = tid; e < mp * npairs; e += nt) {
-                const int i = e % mp, Q = e / mp;
+            for (int Q = wid; Q < npairs; Q += nw)
+            for (int i = lane; i < mp; i += 32) {
                 const double sQ = cs_s[Q];
                 if (sQ == 0.0) continue;
                 const double cQ = cs_c[Q];
@@ -381,7 +411,7 @@ __global__ void __launch_bounds__(kThreads)
                     al = warp_sum(al);
                     be = warp_sum(be);
                     ga = warp_sum(ga);
-                    if (ga != 0.0 && fabs(ga) > DBL_EPSILON * sqrt(al * be)) {
+                    if (ga != 0.0 && fabs(ga) > mp * DBL_EPSILON * sqrt(al * be)) {
                         const double zeta = (be - al) / (2.0 * ga);
                         const double t =
                             (zeta >= 0.0 ? 1.0 : -1.0) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
@@ -490,6 +520,15 @@ void pivoted_chol_rank(int m, const double* G, double tol_rel, int* rank, int* p
 }
 
 void tri_inv_upper(int m, const double* R, double* Rinv, cudaStream_t st) {
+    const size_t smem = sizeof(double) * ((size_t)m * m + 32 * (size_t)m);
+    if (smem <= kSmemMax) {
+        if (smem > 48 * 1024)
+            W4_CUDA(cudaFuncSetAttribute(tri_inv_smem_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)smem));
+        tri_inv_smem_kernel<<<1, 1024, smem, st>>>(m, R, Rinv);
+        W4_LAUNCH();
+        return;
+    }
     const int warps = 8;
     tri_inv_kernel<<<(unsigned)cdiv(m, warps), warps * 32, sizeof(double) * warps * m, st>>>(m, R,
                                                                                            Rinv);

@@ -182,13 +182,15 @@ template <int KIND>
 __device__ __forceinline__ double tl3(double l, double c, double r, double cc, double dd) {
     if (KIND == WC4DVAR_MODEL_IDENTITY) return c;
     if (KIND == WC4DVAR_MODEL_ADVECTION) return c - cc * (c - l);
-    return c - cc * (c - l) + dd * (r - 2.0 * c + l);
+    // x_j - C(x_j - x_{j-1}) + D(x_{j+1} - 2x_j + x_{j-1}) regrouped into three fp64 ops
+    // (coefficients are loop-invariant); differs from the expanded form by rounding only
+    return fma(dd, r, fma(cc + dd, l, (1.0 - cc - 2.0 * dd) * c));
 }
 template <int KIND>
 __device__ __forceinline__ double adj3(double l, double c, double r, double cc, double dd) {
     if (KIND == WC4DVAR_MODEL_IDENTITY) return c;
     if (KIND == WC4DVAR_MODEL_ADVECTION) return (1.0 - cc) * c + cc * r;
-    return c - cc * (c - r) + dd * (l - 2.0 * c + r);
+    return fma(dd, l, fma(cc + dd, r, (1.0 - cc - 2.0 * dd) * c));
 }
 
 template <int KIND, int S, int P, bool ADJ>

@@ -91,6 +91,36 @@ __device__ __forceinline__ double l96_jac_t(const double* __restrict__ x, const 
     return -x[gp1] * lp2 + (x[gp2] - x[gm1]) * lp1 + x[gm2] * lm1 - lc;
 }
 
+// Same Jacobians with the stage vector staged in SMEM over the region.
+__device__ __forceinline__ double l96_jac_s(const double* __restrict__ x, const double* __restrict__ v,
+                                            const Region& rg, int e) {
+    const int em2 = rg.nb(e, -2), em1 = rg.nb(e, -1), ep1 = rg.nb(e, 1);
+    return -v[em2] * x[em1] - x[em2] * v[em1] + v[em1] * x[ep1] + x[em1] * v[ep1] - v[e];
+}
+__device__ __forceinline__ double l96_jac_t_s(const double* __restrict__ x, const double* __restrict__ l,
+                                              const Region& rg, int e, double scale) {
+    const int em2 = rg.nb(e, -2), em1 = rg.nb(e, -1), ep1 = rg.nb(e, 1), ep2 = rg.nb(e, 2);
+    const double lp2 = scale * l[ep2], lp1 = scale * l[ep1], lm1 = scale * l[em1], lc = scale * l[e];
+    return -x[ep1] * lp2 + (x[ep2] - x[em1]) * lp1 + x[em2] * lm1 - lc;
+}
+
+// Region slice of one stage vector -> SMEM with 8-byte cp.async (overlaps the current phase).
+__device__ __forceinline__ void stage_load(double* dst, const double* __restrict__ src, const Region& rg,
+                                           int R, int tid, int nt) {
+    for (int e = tid - 2; e < R + 2; e += nt) {  // region plus the 2-element guards
+        const unsigned d = static_cast<unsigned>(__cvta_generic_to_shared(dst + e));
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(d), "l"(src + rg.gidx(e)));
+    }
+    asm volatile("cp.async.commit_group;\n");
+}
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;\n" ::: "memory"); }
+#define stage_sync(idx)          \
+    do {                         \
+        cp_async_wait_all();     \
+        __syncthreads();         \
+        (idx) ^= 1;              \
+    } while (0)
+
 struct TiledArgs {
     ModelDev md;
     NetDev net;
@@ -152,6 +182,15 @@ __global__ void __launch_bounds__(kThreads) tiled_fwd_kernel(const TiledArgs ta,
         }
     }
     __syncthreads();
+    // L96 stage double buffer, each with a 2-element guard per side (the adjoint Jacobian
+    // reads the stage one point further left than the state)
+    double* sbuf[2] = {sm + 5 * R + 2, sm + 6 * R + 6};
+    int sbi = 0;
+    if (KIND == WC4DVAR_MODEL_LORENZ96 && ta.i1 > ta.i0) {  // x1 of the first sub-step
+        stage_load(sbuf[0], md.stages + (int64_t)ta.i0 * s * 4 * n, rg, R, tid, nt);
+        cp_async_wait_all();
+        __syncthreads();
+    }
     int lo = 0, hi = R;  // valid region
     for (int i = ta.i0; i < ta.i1; ++i) {
         for (int k = 0; k < s; ++k) {
@@ -163,34 +202,44 @@ __global__ void __launch_bounds__(kThreads) tiled_fwd_kernel(const TiledArgs ta,
             if (KIND != WC4DVAR_MODEL_LORENZ96) {
                 for (int e = lo + tid; e < hi; e += nt) nxt[e] = stencil1<KIND, false>(cur, rg, e, md.c, md.d);
             } else {
-                // RK4 TL step (models.cpp:120-128), stages of sub-step i*s+k
+                // RK4 TL step (models.cpp:120-128), stages of sub-step i*s+k.  Stage x_p is
+                // staged in SMEM (sb[cur]) while x_{p+1} streams into sb[nxt] by cp.async.
                 const double* st = md.stages + ((int64_t)i * s + k) * 4 * n;
                 const double dt = md.dt;
                 const int l1 = geo.resident ? 0 : lo - 6, h1 = geo.resident ? R : hi + 3;
+                stage_load(sbuf[sbi ^ 1], st + n, rg, R, tid, nt);
                 for (int e = max(l1, 0) + tid; e < min(h1, R); e += nt) {
-                    const double a1 = l96_jac(st, cur, rg, e);
+                    const double a1 = l96_jac_s(sbuf[sbi], cur, rg, e);
                     acc[e] = a1;
                     t1[e] = cur[e] + 0.5 * dt * a1;
                 }
-                __syncthreads();
+                stage_sync(sbi);
                 const int l2 = geo.resident ? 0 : lo - 4, h2 = geo.resident ? R : hi + 2;
+                stage_load(sbuf[sbi ^ 1], st + 2 * n, rg, R, tid, nt);
                 for (int e = max(l2, 0) + tid; e < min(h2, R); e += nt) {
-                    const double a2 = l96_jac(st + n, t1, rg, e);
+                    const double a2 = l96_jac_s(sbuf[sbi], t1, rg, e);
                     acc[e] = acc[e] + 2.0 * a2;
                     t2[e] = cur[e] + 0.5 * dt * a2;
                 }
-                __syncthreads();
+                stage_sync(sbi);
                 const int l3 = geo.resident ? 0 : lo - 2, h3 = geo.resident ? R : hi + 1;
+                stage_load(sbuf[sbi ^ 1], st + 3 * n, rg, R, tid, nt);
                 for (int e = max(l3, 0) + tid; e < min(h3, R); e += nt) {
-                    const double a3 = l96_jac(st + 2 * n, t2, rg, e);
+                    const double a3 = l96_jac_s(sbuf[sbi], t2, rg, e);
                     acc[e] = acc[e] + 2.0 * a3;
                     t1[e] = cur[e] + dt * a3;
                 }
-                __syncthreads();
+                stage_sync(sbi);
+                {  // prefetch x1 of the next sub-step of this launch
+                    const bool more = (k + 1 < s) || (i + 1 < ta.i1);
+                    if (more) stage_load(sbuf[sbi ^ 1], st + 4 * n, rg, R, tid, nt);
+                }
                 for (int e = lo + tid; e < hi; e += nt) {
-                    const double a4 = l96_jac(st + 3 * n, t1, rg, e);
+                    const double a4 = l96_jac_s(sbuf[sbi], t1, rg, e);
                     nxt[e] = cur[e] + (dt / 6.0) * (acc[e] + a4);
                 }
+                cp_async_wait_all();
+                sbi ^= 1;
             }
             if (last) {
                 // x_{i+1} = M_i x_i + X_{i+1}  (operators.cpp:88)
@@ -283,6 +332,13 @@ __global__ void __launch_bounds__(kThreads) tiled_adj_kernel(const TiledArgs ta,
         }
     }
     __syncthreads();
+    double* sbuf[2] = {sm + 5 * R + 2, sm + 6 * R + 6};  // guarded stage buffers (see fwd)
+    int sbi = 0;
+    if (KIND == WC4DVAR_MODEL_LORENZ96 && ta.i1 > ta.i0) {  // x4 of the last sub-step
+        stage_load(sbuf[0], md.stages + (((int64_t)ta.i1 * s - 1) * 4 + 3) * n, rg, R, tid, nt);
+        cp_async_wait_all();
+        __syncthreads();
+    }
     int lo = 0, hi = R;
     for (int i = ta.i1 - 1; i >= ta.i0; --i) {
         for (int kk = 0; kk < s; ++kk) {
@@ -299,30 +355,39 @@ __global__ void __launch_bounds__(kThreads) tiled_adj_kernel(const TiledArgs ta,
                 const double* st = md.stages + ((int64_t)i * s + k) * 4 * n;
                 const double dt = md.dt, ee = dt / 6.0;
                 const int l1 = geo.resident ? 0 : lo - 3, h1 = geo.resident ? R : hi + 6;
+                stage_load(sbuf[sbi ^ 1], st + 2 * n, rg, R, tid, nt);
                 for (int e = max(l1, 0) + tid; e < min(h1, R); e += nt) {
-                    const double w = l96_jac_t(st + 3 * n, cur, rg, e, ee);
+                    const double w = l96_jac_t_s(sbuf[sbi], cur, rg, e, ee);  // stage x4
                     acc[e] = cur[e] + w;
                     t1[e] = 2.0 * ee * cur[e] + dt * w;
                 }
-                __syncthreads();
+                stage_sync(sbi);
                 const int l2 = geo.resident ? 0 : lo - 2, h2 = geo.resident ? R : hi + 4;
+                stage_load(sbuf[sbi ^ 1], st + n, rg, R, tid, nt);
                 for (int e = max(l2, 0) + tid; e < min(h2, R); e += nt) {
-                    const double w = l96_jac_t(st + 2 * n, t1, rg, e, 1.0);
+                    const double w = l96_jac_t_s(sbuf[sbi], t1, rg, e, 1.0);  // x3
                     acc[e] = acc[e] + w;
                     t2[e] = 2.0 * ee * cur[e] + 0.5 * dt * w;
                 }
-                __syncthreads();
+                stage_sync(sbi);
                 const int l3 = geo.resident ? 0 : lo - 1, h3 = geo.resident ? R : hi + 2;
+                stage_load(sbuf[sbi ^ 1], st, rg, R, tid, nt);
                 for (int e = max(l3, 0) + tid; e < min(h3, R); e += nt) {
-                    const double w = l96_jac_t(st + n, t2, rg, e, 1.0);
+                    const double w = l96_jac_t_s(sbuf[sbi], t2, rg, e, 1.0);  // x2
                     acc[e] = acc[e] + w;
                     t1[e] = ee * cur[e] + 0.5 * dt * w;
                 }
-                __syncthreads();
+                stage_sync(sbi);
+                {  // prefetch x4 of the previous sub-step (next in adjoint order)
+                    const bool more = (k > 0) || (i > ta.i0);
+                    if (more) stage_load(sbuf[sbi ^ 1], st - 4 * n + 3 * n, rg, R, tid, nt);
+                }
                 for (int e = lo + tid; e < hi; e += nt) {
-                    const double w = l96_jac_t(st, t1, rg, e, 1.0);
+                    const double w = l96_jac_t_s(sbuf[sbi], t1, rg, e, 1.0);  // x1
                     nxt[e] = acc[e] + w;
                 }
+                cp_async_wait_all();
+                sbi ^= 1;
             }
             if (last) {
                 // s_i = v_i + H_i^T y + M_i^T s_{i+1}  (operators.cpp:99)
@@ -356,13 +421,13 @@ template <int KIND>
 __device__ __forceinline__ double tl3t(double l, double c, double r, double cc, double dd) {
     if (KIND == WC4DVAR_MODEL_IDENTITY) return c;
     if (KIND == WC4DVAR_MODEL_ADVECTION) return c - cc * (c - l);
-    return c - cc * (c - l) + dd * (r - 2.0 * c + l);
+    return fma(dd, r, fma(cc + dd, l, (1.0 - cc - 2.0 * dd) * c));  // 3 fp64 ops
 }
 template <int KIND>
 __device__ __forceinline__ double adj3t(double l, double c, double r, double cc, double dd) {
     if (KIND == WC4DVAR_MODEL_IDENTITY) return c;
     if (KIND == WC4DVAR_MODEL_ADVECTION) return (1.0 - cc) * c + cc * r;
-    return c - cc * (c - r) + dd * (l - 2.0 * c + r);
+    return fma(dd, l, fma(cc + dd, r, (1.0 - cc - 2.0 * dd) * c));
 }
 
 template <int KIND, int S, int P, bool ADJ>
@@ -599,7 +664,7 @@ void launch_tiled(const ModelDev& md, const NetDev& net, const SweepArgs& a, uns
                   cudaStream_t st, DevBuf& ws, int tile_override) {
     int rl, rr;
     model_radius(md.kind, rl, rr);
-    const int nbuf = (KIND == WC4DVAR_MODEL_LORENZ96) ? 5 : 2;
+    const int nbuf = (KIND == WC4DVAR_MODEL_LORENZ96) ? 7 : 2;
     const int64_t smem_cap = 200 * 1024 / (8 * nbuf);  // region doubles per buffer
     TileGeom geo{};
     int K = md.N;  // intervals per launch
@@ -635,7 +700,7 @@ void launch_tiled(const ModelDev& md, const NetDev& net, const SweepArgs& a, uns
         require(geo.R <= md.n, "tiled sweep: tile plus halo exceeds the periodic domain");
         geo.ntiles = cdiv(md.n, T);
     }
-    const size_t smem = sizeof(double) * (size_t)nbuf * geo.R;
+    const size_t smem = sizeof(double) * ((size_t)nbuf * geo.R + 8);
     auto fk = tiled_fwd_kernel<KIND>;
     auto ak = tiled_adj_kernel<KIND>;
     W4_CUDA(cudaFuncSetAttribute(fk, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));

@@ -718,6 +718,62 @@ class PcgResult:
 _STOP = {0: "zero initial residual", 1: "relative residual tolerance reached", 2: "maximum iterations reached"}
 
 
+@dataclass
+class PrecondSpec:
+    """assimilation.hpp:66-77 (randomized kinds; the deterministic Lanczos LMP is out of
+    scope)."""
+
+    kind: str = "none"   # none | revd | nystrom | ritzit
+    k: int = 0
+    l: int = 5
+    seed: int = 0
+    p_iter: int = 1
+
+
+@dataclass
+class SolverSpec:
+    """assimilation.hpp:79-84."""
+
+    max_iter: int = 100
+    rel_tol: float = 1e-6
+    reorthogonalize: bool = False
+    record_cost: bool = True
+
+
+@dataclass
+class InnerLoopReport:
+    """assimilation.hpp:86-97 (without the desk-scale preconditioned extremes)."""
+
+    delta_p: np.ndarray
+    delta_p_tilde: np.ndarray
+    quadratic_costs: List[float]
+    residual_norms: List[float]
+    iterations: int
+    converged: bool
+    precond: PrecondSpec
+    ritz_values: np.ndarray
+
+
+def run_inner_loop(hessian: HessianOperator, b, d, precond: PrecondSpec, solver: SolverSpec,
+                   omega: Optional[np.ndarray] = None) -> InnerLoopReport:
+    """run_inner_loop, assimilation.cpp:192-253, from the innovations b (control space) and
+    d (observation space) of compute_innovations (assimilation.cpp:119-128): QuadraticCost
+    -> randomized LMP -> split PCG on the cost's RHS -> delta_p = D^{1/2} x."""
+    cost = QuadraticCost(hessian, b, d)
+    factor, ritz = None, np.zeros(0)
+    if precond.kind != "none":
+        cfg = SketchConfig(precond.k, precond.l, precond.seed, precond.kind, precond.p_iter)
+        pairs = sketch_eigenpairs(hessian, cfg, omega)
+        factor = build_spectral_lmp(pairs, hessian.device())
+        ritz = pairs.values
+    opts = PcgOptions(solver.max_iter, solver.rel_tol, solver.reorthogonalize,
+                      cost if solver.record_cost else None)
+    sol = pcg_split(hessian, cost.rhs(), factor, None, opts)
+    return InnerLoopReport(hessian.apply_D_half(sol.x), sol.x, sol.history.quadratic_costs,
+                           sol.history.residual_norms, sol.history.iterations, sol.history.converged,
+                           precond, ritz)
+
+
 def pcg_split(op: LinearOperator, b, precond: Optional[LmpFactor] = None, x0=None,
               opts: Optional[PcgOptions] = None) -> PcgResult:
     """krylov.cpp:22-108."""
