@@ -465,42 +465,46 @@ __global__ void __launch_bounds__(WM * WN * 32 + 32, 1)
 
     if (warp == WM * WN) {
         // ===== producer warp =====
-        // Each warp instruction copies 4 rows x 128 B (8 lanes per row, lane owns chunk
-        // lane & 7 of rows (lane >> 3) + 4u), so a quarter-warp's 16-byte SMEM writes cover
-        // one contiguous 128 B row.  Row pointers are arithmetic; the column map's division
-        // is done once per lane and advanced incrementally.
-        const int ch = lane & 7, r0 = lane >> 3;
-        constexpr int U = BM / 4;
-        static_assert(BM == BN, "producer assumes square tiles");
-        const int64_t ld = P.lda;
-        const ColMap& im = P.in;
+        // Lane l owns A rows l + 32u and B columns l + 32u (pointers computed once per
+        // tile).  It copies the 8 16-byte chunks of each row in the lane-rotated order
+        // (ch + l) & 7: with the 192-byte row stride the 8 lanes of a quarter-warp then hit
+        // 8 distinct 4-bank groups, so the SMEM writes are conflict-free.
+        constexpr int AU = BM / 32, BU = BN / 32;
+        const double* arow[AU];
+        bool aok[AU];
+        const double* bcol[BU];
+        bool bok[BU];
+#pragma unroll
+        for (int u = 0; u < AU; ++u) {
+            const int64_t row = m0 + lane + 32 * u;
+            aok[u] = row < M;
+            arow[u] = P.A + (aok[u] ? row : 0) * P.lda;  // column `row` of A == row (symmetric)
+        }
+#pragma unroll
+        for (int u = 0; u < BU; ++u) {
+            const int64_t c = n0 + lane + 32 * u;
+            bok[u] = c < ncols;
+            bcol[u] = bok[u] ? P.in.col(c) : P.A;
+        }
         for (int64_t kt = 0; kt < ktiles; ++kt) {
             const int s = (int)(kt % STAGES);
             const unsigned ph = (unsigned)((kt / STAGES) & 1);
             mbar_wait(&empty[s], ph ^ 1u);
             const int64_t k0 = kt * BK;
-            const int64_t kr = k0 + 2 * ch;
-            const int64_t rem = K - kr;
-            const int kval = rem >= 2 ? 2 : (rem > 0 ? (int)rem : 0);
-            double* as = As + s * A_ELEMS + r0 * KS + 2 * ch;
-            double* bs = Bs + s * B_ELEMS + r0 * KS + 2 * ch;
-            int64_t row = m0 + r0;
-            const double* ap = P.A + row * ld + kr;  // column `row` of A == row (symmetric)
-            int64_t c = n0 + r0;
-            int64_t cq = c / im.per, cr = c % im.per;
-#pragma unroll 4
-            for (int u = 0; u < U; ++u) {
-                cp_async_vec<2>(as + u * 4 * KS, ap, row < M ? kval : 0, P.A);
-                const double* bp = im.base + cq * im.ld_outer + (im.off + cr) * im.stride + kr;
-                cp_async_vec<2>(bs + u * 4 * KS, bp, c < ncols ? kval : 0, P.A);
-                row += 4;
-                ap += 4 * ld;
-                c += 4;
-                cr += 4;
-                while (cr >= im.per) {
-                    cr -= im.per;
-                    ++cq;
-                }
+            double* as = As + s * A_ELEMS + lane * KS;
+            double* bs = Bs + s * B_ELEMS + lane * KS;
+#pragma unroll
+            for (int cc = 0; cc < BK / 2; ++cc) {
+                const int ch = (cc + lane) & 7;
+                const int64_t kr = k0 + 2 * ch;
+                const int64_t rem = K - kr;
+                const int kval = rem >= 2 ? 2 : (rem > 0 ? (int)rem : 0);
+#pragma unroll
+                for (int u = 0; u < AU; ++u)
+                    cp_async_vec<2>(as + u * 32 * KS + 2 * ch, arow[u] + kr, aok[u] ? kval : 0, P.A);
+#pragma unroll
+                for (int u = 0; u < BU; ++u)
+                    cp_async_vec<2>(bs + u * 32 * KS + 2 * ch, bcol[u] + kr, bok[u] ? kval : 0, P.A);
             }
             mbar_arrive_cp_async(&full[s]);
         }

@@ -2,6 +2,8 @@
 #include "smallla.cuh"
 
 #include <cfloat>
+#include <cstdio>
+#include <cstdlib>
 
 namespace w4 {
 namespace {
@@ -289,7 +291,7 @@ constexpr int kEvdThreads = 512;
 
 __global__ void __launch_bounds__(kEvdThreads)
     jacobi_evd_blk_kernel(int m, const double* __restrict__ K, double* __restrict__ vals,
-                          double* __restrict__ W, double* gwork, int use_smem) {
+                          double* __restrict__ W, double* gwork, int use_smem, int debug) {
     extern __shared__ double sm[];
     const int mp = m + (m & 1);
     double* A = use_smem ? sm : gwork;
@@ -358,7 +360,9 @@ __global__ void __launch_bounds__(kEvdThreads)
             }
             __syncthreads();
         }
-        if (!__syncthreads_or(rotated)) break;
+        const int any = __syncthreads_or(rotated);
+        if (debug && tid == 0) printf("jacobi_evd m=%d sweep %d rotated %d\n", m, sweep, any);
+        if (!any) break;
     }
     for (int i = tid; i < m; i += nt) {
         const double di = A[i + i * mp];
@@ -545,7 +549,8 @@ void sym_evd_desc(int m, const double* K, double* vals, double* W, DevBuf& work,
     (void)bytes;
     const size_t sh = setup_smem(reinterpret_cast<const void*>(jacobi_evd_blk_kernel), bytes2, use);
     double* g = use ? nullptr : work.get<double>((size_t)2 * mp * mp);
-    jacobi_evd_blk_kernel<<<1, kEvdThreads, sh, st>>>(m, K, vals, W, g, use);
+    static const int debug = std::getenv("WC4DVAR_DEBUG_JACOBI") ? 1 : 0;
+    jacobi_evd_blk_kernel<<<1, kEvdThreads, sh, st>>>(m, K, vals, W, g, use, debug);
     W4_LAUNCH();
 }
 
