@@ -14,6 +14,7 @@
 #include "sweep.cuh"
 
 #include <algorithm>
+#include <cstdlib>
 
 namespace w4 {
 namespace {
@@ -659,6 +660,479 @@ bool launch_tiled_blk(const ModelDev& md, const NetDev& net, const SweepArgs& a,
     return true;
 }
 
+// ---------------------------------------------------------------- Lorenz-96, register-blocked
+// CB sketch columns share one CTA and one SMEM copy of each RK4 stage slice; each thread
+// keeps P consecutive region points of one column in registers.  One phase = one Jacobian
+// product (models.cpp:92-116): the thread publishes its P values to an SMEM exchange row,
+// one barrier, then reads its 2+1 (TL) / 1+2 (adjoint) halo values and the stage slice
+// around its points (LDS.128).  Exchange rows and stage buffers are double-buffered, so a
+// phase costs a single barrier while the next stage streams in by cp.async.  Arithmetic is
+// written in the same order as the SMEM kernels above (and the oracle).
+constexpr int kL96Threads = 512;
+constexpr int kL96P = 8;
+constexpr int kL96G = 0;  // (rows carry their guards inside the interleaved layout)
+
+// SMEM rows use an interleaved layout so every per-thread access is a conflict-free LDS.128
+// / STS.128 across the warp: point pair (2k, 2k+1) of thread j lives at double2 slot
+// k (NTC + 2) + j + 1; slots j = -1 and j = NTC are the left / right guards.
+template <int CB, int NTC_>
+struct L96Lay {
+    static constexpr int NTC = NTC_;              // threads per column
+    static constexpr int NT = CB * NTC;           // threads per CTA
+    static constexpr int R = NTC * kL96P;         // region points
+    static constexpr int LD = kL96P * (NTC + 2);  // row size in doubles
+    // 4 stage ring buffers + 2 x CB exchange rows
+    static constexpr size_t smem_bytes = sizeof(double) * (4 * LD + 2 * CB * LD);
+};
+template <int NTC>
+__device__ __forceinline__ int l96_slot(int k, int j) { return k * (NTC + 2) + j + 1; }
+
+// Region slice [-2, R+2) of one stage vector -> interleaved SMEM row (8-byte cp.async).
+template <int P, int NTC>
+__device__ __forceinline__ void stage_load_il(double* dst, const double* __restrict__ src, const Region& rg,
+                                              int R, int tid, int nt) {
+    // consecutive threads take consecutive point pairs, so the global reads coalesce
+    for (int pi = tid; pi < R / 2 + 2; pi += nt) {
+        const int e = 2 * pi - 2;
+        const int jj = (e + P) / P - 1;  // floor(e / P) for e >= -P
+        const int k = (e - jj * P) >> 1;
+        const unsigned d = static_cast<unsigned>(__cvta_generic_to_shared(dst + 2 * l96_slot<NTC>(k, jj)));
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(d), "l"(src + rg.gidx(e)));
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(d + 8), "l"(src + rg.gidx(e + 1)));
+    }
+    asm volatile("cp.async.commit_group;\n");
+}
+
+template <int P, int NTC>
+__device__ __forceinline__ void l96_publish(double* exr, int b, const double (&v)[P]) {
+    double2* r2 = reinterpret_cast<double2*>(exr);
+    const int j = b / P;
+#pragma unroll
+    for (int k = 0; k < P / 2; ++k) r2[l96_slot<NTC>(k, j)] = make_double2(v[2 * k], v[2 * k + 1]);
+}
+
+template <int P, int NTC>
+__device__ __forceinline__ void l96_stage_regs(const double* xs, int j, double (&xv)[P + 4]) {
+    const double2* r2 = reinterpret_cast<const double2*>(xs);
+    const double2 lft = r2[l96_slot<NTC>(P / 2 - 1, j - 1)], rgt = r2[l96_slot<NTC>(0, j + 1)];
+    xv[0] = lft.x;  // x[b-2 .. b+P+1]
+    xv[1] = lft.y;
+#pragma unroll
+    for (int k = 0; k < P / 2; ++k) {
+        const double2 q = r2[l96_slot<NTC>(k, j)];
+        xv[2 + 2 * k] = q.x;
+        xv[3 + 2 * k] = q.y;
+    }
+    xv[P + 2] = rgt.x;
+    xv[P + 3] = rgt.y;
+}
+
+// a = J(x) v on the thread's points (l96_jac_s order)
+template <int P, int NTC>
+__device__ __forceinline__ void l96_tl_phase(const double* xs, const double* exr, int b, const double (&v)[P],
+                                             double (&out)[P]) {
+    const int j = b / P;
+    double xv[P + 4];
+    l96_stage_regs<P, NTC>(xs, j, xv);
+    const double2* e2 = reinterpret_cast<const double2*>(exr);
+    double w[P + 3];  // v[b-2 .. b+P]
+    const double2 h = e2[l96_slot<NTC>(P / 2 - 1, j - 1)];
+    w[0] = h.x;
+    w[1] = h.y;
+#pragma unroll
+    for (int p = 0; p < P; ++p) w[p + 2] = v[p];
+    w[P + 2] = e2[l96_slot<NTC>(0, j + 1)].x;
+#pragma unroll
+    for (int p = 0; p < P; ++p)
+        out[p] = -w[p] * xv[p + 1] - xv[p] * w[p + 1] + w[p + 1] * xv[p + 3] + xv[p + 1] * w[p + 3] - w[p + 2];
+}
+
+// w = J(x)^T (scale l) on the thread's points (l96_jac_t_s order)
+template <int P, int NTC>
+__device__ __forceinline__ void l96_adj_phase(const double* xs, const double* exr, int b, const double (&l)[P],
+                                              double scale, double (&out)[P]) {
+    const int j = b / P;
+    double xv[P + 4];
+    l96_stage_regs<P, NTC>(xs, j, xv);
+    const double2* e2 = reinterpret_cast<const double2*>(exr);
+    double w[P + 3];  // l[b-1 .. b+P+1]
+    w[0] = e2[l96_slot<NTC>(P / 2 - 1, j - 1)].y;
+#pragma unroll
+    for (int p = 0; p < P; ++p) w[p + 1] = l[p];
+    const double2 h = e2[l96_slot<NTC>(0, j + 1)];
+    w[P + 1] = h.x;
+    w[P + 2] = h.y;
+#pragma unroll
+    for (int p = 0; p < P; ++p) {
+        const double lp2 = scale * w[p + 3], lp1 = scale * w[p + 2], lm1 = scale * w[p], lc = scale * w[p + 1];
+        out[p] = -xv[p + 3] * lp2 + (xv[p + 4] - xv[p + 1]) * lp1 + xv[p] * lm1 - lc;
+    }
+}
+
+// Stage sg (global RK4 stage index (interval * s + sub-step) * 4 + stage; one per phase)
+// -> ring buffer sg & 3.  Each phase issues exactly one commit group (empty outside
+// [lo, hi)) so that the phase barrier's wait_group 2 leaves the next two stages in flight.
+template <int P, int NTC>
+__device__ __forceinline__ void l96_prefetch(double* sx, int LD, const double* __restrict__ stages, int64_t sg,
+                                             int64_t lo, int64_t hi, int n, const Region& rg, int R, int tid,
+                                             int nt) {
+    if (sg >= lo && sg < hi)
+        stage_load_il<P, NTC>(sx + (int)(sg & 3) * LD, stages + sg * n, rg, R, tid, nt);
+    else
+        asm volatile("cp.async.commit_group;\n");
+}
+
+// barrier of one phase: this thread's copies of the current stage land (two newer stages
+// may stay in flight), everyone's exchange row and stage copies are visible
+#define L96_PHASE_SYNC()                                          \
+    do {                                                          \
+        asm volatile("cp.async.wait_group 2;\n" ::: "memory"); \
+        __syncthreads();                                          \
+    } while (0)
+#define L96_PREFETCH() \
+    l96_prefetch<P, Lay::NTC>(sx, LD, md.stages, sg + 3 * kDir, sg_lo, sg_hi, n, rg, R, tid, nt)
+
+template <int CB, int NTC>
+__global__ void __launch_bounds__(CB * NTC, 65536 / (CB * NTC * 128)) l96_blk_fwd_kernel(const TiledArgs ta, unsigned* status) {
+    using Lay = L96Lay<CB, NTC>;
+    constexpr int P = kL96P, R = Lay::R, LD = Lay::LD, G = kL96G;
+    extern __shared__ __align__(16) double l96sm[];
+    double* sx = l96sm;           // [2][LD] stage slices
+    double* ex = l96sm + 4 * LD;  // [2][CB][LD] exchange rows
+    const ModelDev& md = ta.md;
+    const NetDev& net = ta.net;
+    const SweepArgs& a = ta.a;
+    const TileGeom& geo = ta.geo;
+    const int n = (int)md.n;
+    const int tid = threadIdx.x, nt = blockDim.x;
+    const int cg = tid / Lay::NTC, b = (tid % Lay::NTC) * P;
+    const int64_t col = (int64_t)blockIdx.x * CB + cg;
+    const bool live = col < a.m;
+    const int64_t t0 = (int64_t)blockIdx.y * geo.T;
+    const Region rg{R, false, (int)(t0 - geo.HL), n};
+    const int c_lo = geo.HL;
+    const int c_hi = geo.HL + (int)((int64_t)n - t0 < geo.T ? (int64_t)n - t0 : geo.T);
+    const int s = md.s;
+    const double dt = md.dt;
+    const double* X = a.X + (live ? col : 0) * a.ldx;
+    double* Yc = a.Y ? a.Y + col * net.q : nullptr;
+    double* tr = a.traj ? a.traj + col * a.ldtraj : nullptr;
+    const int np = net.n_points;
+    bool bad = false;
+
+    for (int r = tid; r < 2 * CB * P; r += nt) {  // exchange-row guard slots: finite, never written
+        const int row = r / P, k = (r % P) >> 1, side = r & 1;
+        reinterpret_cast<double2*>(ex + row * LD)[l96_slot<Lay::NTC>(k, side ? Lay::NTC : -1)] =
+            make_double2(0.0, 0.0);
+    }
+    constexpr int kDir = 1;  // stages consumed in increasing order
+    const int64_t sg_lo = (int64_t)ta.i0 * s * 4, sg_hi = (int64_t)ta.i1 * s * 4;
+    int64_t sg = sg_lo;
+    for (int u = 0; u < 3; ++u) l96_prefetch<P, Lay::NTC>(sx, LD, md.stages, sg + u, sg_lo, sg_hi, n, rg, R, tid, nt);
+
+    double cur[P], t[P], acc[P], av[P];
+    {
+        const double* src = ta.bin ? ta.bin + col * n : X;
+#pragma unroll
+        for (int p = 0; p < P; ++p) cur[p] = live ? src[rg.gidx(b + p)] : 0.0;
+    }
+    if (ta.i0 == 0 && live) {
+        const int sl = net.slot[0];
+#pragma unroll
+        for (int p = 0; p < P; ++p) {
+            const int e = b + p;
+            if (e >= c_lo && e < c_hi) {
+                const int g = rg.gidx(e);
+                bad |= !isfinite(cur[p]);
+                if (tr) tr[g] = cur[p];
+                if (a.fwd_obs && sl >= 0) {
+                    const int bb = net.pmap[g];
+                    if (bb >= 0) Yc[(int64_t)sl * np + bb] = a.scale_fwd * cur[p];
+                }
+            }
+        }
+    }
+    int pb = 0;
+    for (int i = ta.i0; i < ta.i1; ++i) {
+        for (int k = 0; k < s; ++k) {
+            // RK4 TL step (models.cpp:120-128)
+            l96_publish<P, Lay::NTC>(ex + (pb * CB + cg) * LD + G, b, cur);
+            L96_PHASE_SYNC();
+            L96_PREFETCH();
+            l96_tl_phase<P, Lay::NTC>(sx + (int)(sg & 3) * LD, ex + (pb * CB + cg) * LD + G, b, cur, av);
+#pragma unroll
+            for (int p = 0; p < P; ++p) {
+                acc[p] = av[p];
+                t[p] = cur[p] + 0.5 * dt * av[p];
+            }
+            sg += kDir;
+            pb ^= 1;
+            l96_publish<P, Lay::NTC>(ex + (pb * CB + cg) * LD + G, b, t);
+            L96_PHASE_SYNC();
+            L96_PREFETCH();
+            l96_tl_phase<P, Lay::NTC>(sx + (int)(sg & 3) * LD, ex + (pb * CB + cg) * LD + G, b, t, av);
+#pragma unroll
+            for (int p = 0; p < P; ++p) {
+                acc[p] = acc[p] + 2.0 * av[p];
+                t[p] = cur[p] + 0.5 * dt * av[p];
+            }
+            sg += kDir;
+            pb ^= 1;
+            l96_publish<P, Lay::NTC>(ex + (pb * CB + cg) * LD + G, b, t);
+            L96_PHASE_SYNC();
+            L96_PREFETCH();
+            l96_tl_phase<P, Lay::NTC>(sx + (int)(sg & 3) * LD, ex + (pb * CB + cg) * LD + G, b, t, av);
+#pragma unroll
+            for (int p = 0; p < P; ++p) {
+                acc[p] = acc[p] + 2.0 * av[p];
+                t[p] = cur[p] + dt * av[p];
+            }
+            sg += kDir;
+            pb ^= 1;
+            l96_publish<P, Lay::NTC>(ex + (pb * CB + cg) * LD + G, b, t);
+            L96_PHASE_SYNC();
+            L96_PREFETCH();
+            l96_tl_phase<P, Lay::NTC>(sx + (int)(sg & 3) * LD, ex + (pb * CB + cg) * LD + G, b, t, av);
+#pragma unroll
+            for (int p = 0; p < P; ++p) cur[p] = cur[p] + (dt / 6.0) * (acc[p] + av[p]);
+            sg += kDir;
+            pb ^= 1;
+        }
+        // x_{i+1} = M_i x_i + X_{i+1}  (operators.cpp:88)
+        if (live) {
+            const double* Xn = X + (int64_t)(i + 1) * n;
+            const int sl = net.slot[i + 1];
+            double* trn = tr ? tr + (int64_t)(i + 1) * n : nullptr;
+#pragma unroll
+            for (int p = 0; p < P; ++p) {
+                const int e = b + p;
+                const int g = rg.gidx(e);
+                cur[p] = cur[p] + Xn[g];
+                if (e >= c_lo && e < c_hi) {
+                    bad |= !isfinite(cur[p]);
+                    if (trn) trn[g] = cur[p];
+                    if (a.fwd_obs && sl >= 0) {
+                        const int bb = net.pmap[g];
+                        if (bb >= 0) Yc[(int64_t)sl * np + bb] = a.scale_fwd * cur[p];
+                    }
+                }
+            }
+        }
+    }
+    if (ta.bout && live) {
+#pragma unroll
+        for (int p = 0; p < P; ++p) {
+            const int e = b + p;
+            if (e >= c_lo && e < c_hi) ta.bout[col * n + rg.gidx(e)] = cur[p];
+        }
+    }
+    if (__syncthreads_or(bad) && tid == 0) atomicOr(status, ST_FWD_NONFINITE);
+}
+
+template <int CB, int NTC>
+__global__ void __launch_bounds__(CB * NTC, 65536 / (CB * NTC * 128)) l96_blk_adj_kernel(const TiledArgs ta, unsigned* status) {
+    using Lay = L96Lay<CB, NTC>;
+    constexpr int P = kL96P, R = Lay::R, LD = Lay::LD, G = kL96G;
+    extern __shared__ __align__(16) double l96sm[];
+    double* sx = l96sm;
+    double* ex = l96sm + 4 * LD;
+    const ModelDev& md = ta.md;
+    const NetDev& net = ta.net;
+    const SweepArgs& a = ta.a;
+    const TileGeom& geo = ta.geo;
+    const int n = (int)md.n;
+    const int tid = threadIdx.x, nt = blockDim.x;
+    const int cg = tid / Lay::NTC, b = (tid % Lay::NTC) * P;
+    const int64_t col = (int64_t)blockIdx.x * CB + cg;
+    const bool live = col < a.m;
+    const int64_t t0 = (int64_t)blockIdx.y * geo.T;
+    const Region rg{R, false, (int)(t0 - geo.HR), n};  // adjoint: mirrored halos
+    const int c_lo = geo.HR;
+    const int c_hi = geo.HR + (int)((int64_t)n - t0 < geo.T ? (int64_t)n - t0 : geo.T);
+    const int s = md.s;
+    const double dt = md.dt, ee = dt / 6.0;
+    const double* V = a.V ? a.V + col * a.ldv : nullptr;
+    const double* Yc = a.Y ? a.Y + col * net.q : nullptr;
+    double* Sv = a.S + col * a.lds;
+    const int np = net.n_points;
+    bool bad = false;
+    auto addend = [&](int i, int g) -> double {
+        double x = V ? V[(int64_t)i * n + g] : 0.0;
+        if (a.adj_obs) {
+            const int sl = net.slot[i];
+            if (sl >= 0) {
+                const int bb = net.pmap[g];
+                if (bb >= 0) x = V ? x + Yc[(int64_t)sl * np + bb] : Yc[(int64_t)sl * np + bb];
+            }
+        }
+        return x;
+    };
+
+    for (int r = tid; r < 2 * CB * P; r += nt) {
+        const int row = r / P, k = (r % P) >> 1, side = r & 1;
+        reinterpret_cast<double2*>(ex + row * LD)[l96_slot<Lay::NTC>(k, side ? Lay::NTC : -1)] =
+            make_double2(0.0, 0.0);
+    }
+    constexpr int kDir = -1;  // stages consumed in decreasing order (x4 of the last sub-step first)
+    const int64_t sg_lo = (int64_t)ta.i0 * s * 4, sg_hi = (int64_t)ta.i1 * s * 4;
+    int64_t sg = sg_hi - 1;
+    for (int u = 0; u < 3; ++u) l96_prefetch<P, Lay::NTC>(sx, LD, md.stages, sg - u, sg_lo, sg_hi, n, rg, R, tid, nt);
+
+    double cur[P], t[P], acc[P], w[P];
+    if (!live) {
+#pragma unroll
+        for (int p = 0; p < P; ++p) cur[p] = 0.0;
+    } else if (ta.bin) {
+#pragma unroll
+        for (int p = 0; p < P; ++p) cur[p] = ta.bin[col * n + rg.gidx(b + p)];
+    } else {  // s_N = v_N + H_N^T y
+#pragma unroll
+        for (int p = 0; p < P; ++p) {
+            const int e = b + p;
+            const int g = rg.gidx(e);
+            cur[p] = addend(ta.i1, g);
+            if (e >= c_lo && e < c_hi) {
+                Sv[(int64_t)ta.i1 * n + g] = cur[p];
+                bad |= !isfinite(cur[p]);
+            }
+        }
+    }
+    int pb = 0;
+    for (int i = ta.i1 - 1; i >= ta.i0; --i) {
+        for (int kk = 0; kk < s; ++kk) {
+            const int k = s - 1 - kk;
+            // RK4 adjoint step (models.cpp:130-148)
+            l96_publish<P, Lay::NTC>(ex + (pb * CB + cg) * LD + G, b, cur);
+            L96_PHASE_SYNC();
+            L96_PREFETCH();
+            l96_adj_phase<P, Lay::NTC>(sx + (int)(sg & 3) * LD, ex + (pb * CB + cg) * LD + G, b, cur, ee, w);  // x4
+#pragma unroll
+            for (int p = 0; p < P; ++p) {
+                acc[p] = cur[p] + w[p];
+                t[p] = 2.0 * ee * cur[p] + dt * w[p];
+            }
+            sg += kDir;
+            pb ^= 1;
+            l96_publish<P, Lay::NTC>(ex + (pb * CB + cg) * LD + G, b, t);
+            L96_PHASE_SYNC();
+            L96_PREFETCH();
+            l96_adj_phase<P, Lay::NTC>(sx + (int)(sg & 3) * LD, ex + (pb * CB + cg) * LD + G, b, t, 1.0, w);  // x3
+#pragma unroll
+            for (int p = 0; p < P; ++p) {
+                acc[p] = acc[p] + w[p];
+                t[p] = 2.0 * ee * cur[p] + 0.5 * dt * w[p];
+            }
+            sg += kDir;
+            pb ^= 1;
+            l96_publish<P, Lay::NTC>(ex + (pb * CB + cg) * LD + G, b, t);
+            L96_PHASE_SYNC();
+            L96_PREFETCH();
+            l96_adj_phase<P, Lay::NTC>(sx + (int)(sg & 3) * LD, ex + (pb * CB + cg) * LD + G, b, t, 1.0, w);  // x2
+#pragma unroll
+            for (int p = 0; p < P; ++p) {
+                acc[p] = acc[p] + w[p];
+                t[p] = ee * cur[p] + 0.5 * dt * w[p];
+            }
+            sg += kDir;
+            pb ^= 1;
+            l96_publish<P, Lay::NTC>(ex + (pb * CB + cg) * LD + G, b, t);
+            L96_PHASE_SYNC();
+            L96_PREFETCH();
+            l96_adj_phase<P, Lay::NTC>(sx + (int)(sg & 3) * LD, ex + (pb * CB + cg) * LD + G, b, t, 1.0, w);  // x1
+#pragma unroll
+            for (int p = 0; p < P; ++p) cur[p] = acc[p] + w[p];
+            sg += kDir;
+            pb ^= 1;
+        }
+        // s_i = v_i + H_i^T y + M_i^T s_{i+1}  (operators.cpp:99)
+        if (live) {
+#pragma unroll
+            for (int p = 0; p < P; ++p) {
+                const int e = b + p;
+                const int g = rg.gidx(e);
+                cur[p] = addend(i, g) + cur[p];
+                if (e >= c_lo && e < c_hi) {
+                    Sv[(int64_t)i * n + g] = cur[p];
+                    bad |= !isfinite(cur[p]);
+                }
+            }
+        }
+    }
+    if (ta.bout && live) {
+#pragma unroll
+        for (int p = 0; p < P; ++p) {
+            const int e = b + p;
+            if (e >= c_lo && e < c_hi) ta.bout[col * n + rg.gidx(e)] = cur[p];
+        }
+    }
+    if (__syncthreads_or(bad) && tid == 0) atomicOr(status, ST_ADJ_NONFINITE);
+}
+
+// Register-blocked Lorenz-96 launch; false if the region does not fit the domain.
+template <int CB, int NTC>
+bool launch_l96_blk(const ModelDev& md, const NetDev& net, const SweepArgs& a, unsigned* status,
+                    cudaStream_t st, DevBuf& ws) {
+    using Lay = L96Lay<CB, NTC>;
+    const int per = md.s * 12;  // (8 + 4) halo points per sub-step
+    int K = 1;                  // intervals per launch: redundant halo work 12 s K / R
+    while (K < md.N && (K + 1) * per <= Lay::R / 16) ++K;
+    const int T = Lay::R - K * per;
+    if (T < Lay::R / 2 || Lay::R > md.n) return false;
+    TileGeom geo{T, K * md.s * 8, K * md.s * 4, Lay::R, false, cdiv(md.n, T)};
+    if (geo.ntiles > 65535) return false;
+    auto fk = l96_blk_fwd_kernel<CB, NTC>;
+    auto ak = l96_blk_adj_kernel<CB, NTC>;
+    W4_CUDA(cudaFuncSetAttribute(fk, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Lay::smem_bytes));
+    W4_CUDA(cudaFuncSetAttribute(ak, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Lay::smem_bytes));
+    const int nl = (int)cdiv(md.N, K);
+    double* bbuf = nl > 1 ? ws.get<double>((size_t)2 * md.n * a.m) : nullptr;
+    const dim3 grid((unsigned)cdiv(a.m, CB), (unsigned)geo.ntiles);
+    TiledArgs ta{md, net, a, geo, 0, 0, nullptr, nullptr};
+    if (a.do_fwd)
+        for (int l = 0; l < nl; ++l) {
+            ta.i0 = l * K;
+            ta.i1 = std::min(md.N, (l + 1) * K);
+            ta.bin = l == 0 ? nullptr : bbuf + (size_t)((l + 1) % 2) * md.n * a.m;
+            ta.bout = l + 1 < nl ? bbuf + (size_t)(l % 2) * md.n * a.m : nullptr;
+            fk<<<grid, Lay::NT, Lay::smem_bytes, st>>>(ta, status);
+            W4_LAUNCH();
+        }
+    if (a.do_adj)
+        for (int l = 0; l < nl; ++l) {
+            ta.i1 = md.N - l * K;
+            ta.i0 = std::max(0, md.N - (l + 1) * K);
+            ta.bin = l == 0 ? nullptr : bbuf + (size_t)((l + 1) % 2) * md.n * a.m;
+            ta.bout = l + 1 < nl ? bbuf + (size_t)(l % 2) * md.n * a.m : nullptr;
+            ak<<<grid, Lay::NT, Lay::smem_bytes, st>>>(ta, status);
+            W4_LAUNCH();
+        }
+    return true;
+}
+
+// WC4DVAR_L96_BLK: 0 = SMEM phase kernels only, 1 = register-blocked whenever the region
+// fits the domain (tests), unset = register-blocked for the tiled (large-n) regime.
+// WC4DVAR_L96_CB: CTA shape of the register-blocked kernel as columns x threads per column
+// (1: 2x256, 2: 4x128, 4: 4x64, 8: 8x64 (default), 16: 16x32).
+bool try_l96_blk(const ModelDev& md, const NetDev& net, const SweepArgs& a, unsigned* status, cudaStream_t st,
+                 DevBuf& ws, bool tiled_regime) {
+    static const int mode = [] {
+        const char* e = std::getenv("WC4DVAR_L96_BLK");
+        return e ? std::atoi(e) : -1;
+    }();
+    static const int cb = [] {
+        const char* e = std::getenv("WC4DVAR_L96_CB");
+        return e ? std::atoi(e) : 8;
+    }();
+    if (mode == 0 || (mode < 0 && !tiled_regime)) return false;
+    switch (cb) {
+        case 1: return launch_l96_blk<2, 256>(md, net, a, status, st, ws);
+        case 2: return launch_l96_blk<4, 128>(md, net, a, status, st, ws);
+        case 4: return launch_l96_blk<4, 64>(md, net, a, status, st, ws);
+        case 16: return launch_l96_blk<16, 32>(md, net, a, status, st, ws);
+        default: return launch_l96_blk<8, 64>(md, net, a, status, st, ws);
+    }
+}
+
 template <int KIND>
 void launch_tiled(const ModelDev& md, const NetDev& net, const SweepArgs& a, unsigned* status,
                   cudaStream_t st, DevBuf& ws, int tile_override) {
@@ -666,6 +1140,9 @@ void launch_tiled(const ModelDev& md, const NetDev& net, const SweepArgs& a, uns
     model_radius(md.kind, rl, rr);
     const int nbuf = (KIND == WC4DVAR_MODEL_LORENZ96) ? 7 : 2;
     const int64_t smem_cap = 200 * 1024 / (8 * nbuf);  // region doubles per buffer
+    if (KIND == WC4DVAR_MODEL_LORENZ96 && tile_override <= 0 &&
+        try_l96_blk(md, net, a, status, st, ws, md.n > smem_cap))
+        return;
     TileGeom geo{};
     int K = md.N;  // intervals per launch
     if (md.n <= smem_cap && (tile_override <= 0 || tile_override >= md.n)) {

@@ -40,6 +40,11 @@ def main():
         traj = W.lorenz96_trajectory(x0, 8.0, dt, 50, N * s)
         res[f"l96_s{s}"] = case(W.Lorenz96Linearized(traj, 8.0, dt, s), W.ObservationNetwork.build(n, N, 2, 1), n,
                                 sigma_o=0.2)
+    # a domain wider than one register-blocked region (WC4DVAR_L96_BLK=1 engages it)
+    nb, N, s, dt = 1500, 4, 5, 0.025
+    traj = W.lorenz96_trajectory(8.0 + O.NormalStream(5).draw(nb), 8.0, dt, 20, N * s)
+    res["l96_n1500"] = case(W.Lorenz96Linearized(traj, 8.0, dt, s), W.ObservationNetwork.build(nb, N, 3, 2), nb,
+                            sigma_o=0.2, m=6)
     print(json.dumps(res))
 
 
