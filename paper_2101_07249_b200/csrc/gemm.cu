@@ -87,6 +87,23 @@ void configure_smem(const void* kern, size_t smem) {
     done[key] = true;
 }
 
+// The stream-K scratch comes from the device's default stream-ordered pool; keep what the
+// pool has reserved across synchronisations (default threshold 0 returns it to the driver
+// at every sync, turning each call's cudaMallocAsync into a fresh mapping).
+void keep_pool_reserved() {
+    static std::mutex mu;
+    static std::map<int, bool> done;
+    int dev = 0;
+    W4_CUDA(cudaGetDevice(&dev));
+    std::lock_guard<std::mutex> lk(mu);
+    if (done.count(dev)) return;
+    cudaMemPool_t pool;
+    W4_CUDA(cudaDeviceGetDefaultMemPool(&pool, dev));
+    uint64_t keep = 64ull << 20;  // the scratch is ~19 MB per concurrent GEMM
+    W4_CUDA(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep));
+    done[dev] = true;
+}
+
 struct PassTable {
     GemmPass p[2];
     int64_t tiles_m[2];
@@ -429,9 +446,85 @@ __device__ __forceinline__ void mbar_wait(uint64_t* b, unsigned parity) {
         : "memory");
 }
 
+// Stream-K schedule that keeps every output element's accumulation order identical to the
+// one-CTA-per-tile kernel (so block apply == column apply stays bitwise): the T tiles x KT
+// k-tiles are cut into G equal contiguous ranges, one per CTA.  With T >= G every range
+// spans >= KT k-tiles, so each tile is split in at most two pieces: a "start" piece
+// (k-tiles [0, c)) at the end of range b and an "end" piece ([c, KT)) at the beginning of
+// range b+1.  CTA b runs its start piece FIRST and publishes the raw DMMA accumulators,
+// then its full tiles, then its end piece, which resumes from CTA b-1's published
+// accumulators -- by then CTA b-1 has long finished its own first piece (no waits when
+// the range is >= KT).  With G = T this is the plain one-tile-per-CTA grid.
+struct SkSched {
+    int64_t s, e, KT, full0, full1;
+    bool has_start, has_end;
+    __device__ SkSched(int64_t b, int64_t G, int64_t T, int64_t kt) : KT(kt) {
+        const int64_t I = T * KT;
+        s = b * I / G;
+        e = (b + 1) * I / G;
+        has_start = (e % KT) != 0;
+        has_end = (s % KT) != 0;
+        full0 = (s + KT - 1) / KT;
+        full1 = e / KT;
+    }
+    __device__ int64_t count() const { return (int64_t)has_start + (full1 - full0) + (int64_t)has_end; }
+    // kind: 0 full tile, 1 start piece (publish), 2 end piece (resume)
+    __device__ void get(int64_t i, int64_t& tile, int64_t& kb, int64_t& ke, int& kind) const {
+        if (has_start) {
+            if (i == 0) {
+                tile = e / KT;
+                kb = 0;
+                ke = e - tile * KT;
+                kind = 1;
+                return;
+            }
+            --i;
+        }
+        if (i < full1 - full0) {
+            tile = full0 + i;
+            kb = 0;
+            ke = KT;
+            kind = 0;
+            return;
+        }
+        tile = s / KT;
+        kb = s - tile * KT;
+        ke = KT;
+        kind = 2;
+    }
+};
+
+struct TileXY {
+    int pi;
+    int64_t m0, n0;
+};
+template <int BM, int BN>
+__device__ __forceinline__ TileXY tile_xy(const PassTable& tab, int64_t tile) {
+    const int pi = tile >= tab.tile_start[1] ? 1 : 0;
+    tile -= tab.tile_start[pi];
+    return TileXY{pi, (tile % tab.tiles_m[pi]) * BM, (tile / tab.tiles_m[pi]) * BN};
+}
+
+__device__ __forceinline__ int ld_acquire(const int* p) {
+    int v;
+    asm volatile("ld.acquire.gpu.global.b32 %0, [%1];\n" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void st_release(int* p, int v) {
+    asm volatile("st.release.gpu.global.b32 [%0], %1;\n" ::"l"(p), "r"(v) : "memory");
+}
+
+constexpr int kSkMaxPieces = 64;  // pieces per CTA (host falls back to one tile per CTA beyond)
+
+struct SkArgs {
+    int64_t KT;        // k-tiles per tile (all passes share K)
+    double* partial;   // [G][32 * NC] published accumulators (null: plain grid)
+    int* flags;        // [G], zeroed before the launch
+};
+
 template <int BM, int BN, int WM, int WN, int STAGES>
 __global__ void __launch_bounds__(WM * WN * 32 + 32, 1)
-    gemm_sym_ws_kernel(const PassTable tab, unsigned* __restrict__ status) {
+    gemm_sym_ws_kernel(const PassTable tab, unsigned* __restrict__ status, const SkArgs sk) {
     constexpr int NC = WM * WN * 32;  // consumer threads
     constexpr int WTM = BM / WM, WTN = BN / WN;
     constexpr int MI = WTM / 16, NI = WTN / 8;
@@ -443,17 +536,24 @@ __global__ void __launch_bounds__(WM * WN * 32 + 32, 1)
     uint64_t* full = reinterpret_cast<uint64_t*>(Bs + STAGES * B_ELEMS);
     uint64_t* empty = full + STAGES;
 
-    int64_t tile = blockIdx.x;
-    const int pi = tile >= tab.tile_start[1] ? 1 : 0;
-    const GemmPass& P = tab.p[pi];
-    tile -= tab.tile_start[pi];
-    const int64_t tm = tile % tab.tiles_m[pi];
-    const int64_t tn = tile / tab.tiles_m[pi];
-    const int64_t m0 = tm * BM, n0 = tn * BN;
-    const int64_t M = P.M, K = P.K, ncols = P.ncols;
-    const int64_t ktiles = (K + BK - 1) / BK;
+    // pass table and this CTA's piece list in SMEM (dynamic indexing without local copies)
+    __shared__ PassTable s_tab;
+    __shared__ int4 s_piece[kSkMaxPieces];  // {tile, kb, ke, kind}
+    __shared__ int s_np;
 
     const int tid = threadIdx.x;
+    if (tid == 0) {
+        s_tab = tab;
+        const SkSched sched(blockIdx.x, gridDim.x, tab.tile_start[2], sk.KT);
+        const int np = (int)sched.count();
+        for (int i = 0; i < np; ++i) {
+            int64_t tl, kb, ke;
+            int kind;
+            sched.get(i, tl, kb, ke, kind);
+            s_piece[i] = make_int4((int)tl, (int)kb, (int)ke, kind);
+        }
+        s_np = np;
+    }
     const int warp = tid >> 5, lane = tid & 31;
     if (tid == 0) {
         for (int s = 0; s < STAGES; ++s) {
@@ -470,43 +570,53 @@ __global__ void __launch_bounds__(WM * WN * 32 + 32, 1)
         // (ch + l) & 7: with the 192-byte row stride the 8 lanes of a quarter-warp then hit
         // 8 distinct 4-bank groups, so the SMEM writes are conflict-free.
         constexpr int AU = BM / 32, BU = BN / 32;
-        const double* arow[AU];
-        bool aok[AU];
-        const double* bcol[BU];
-        bool bok[BU];
+        unsigned it = 0;  // ring position, continuous across pieces
+        const int npieces = s_np;
+        for (int pc = 0; pc < npieces; ++pc) {
+            const int4 pe = s_piece[pc];
+            const int64_t tile = pe.x, kb = pe.y, ke = pe.z;
+            const TileXY xy = tile_xy<BM, BN>(s_tab, tile);
+            const GemmPass& P = s_tab.p[xy.pi];
+            const int64_t K = P.K;
+            const double* const safe = P.A;  // register copy: cp.async asm would force reloads
+            const double* arow[AU];
+            bool aok[AU];
+            const double* bcol[BU];
+            bool bok[BU];
 #pragma unroll
-        for (int u = 0; u < AU; ++u) {
-            const int64_t row = m0 + lane + 32 * u;
-            aok[u] = row < M;
-            arow[u] = P.A + (aok[u] ? row : 0) * P.lda;  // column `row` of A == row (symmetric)
-        }
-#pragma unroll
-        for (int u = 0; u < BU; ++u) {
-            const int64_t c = n0 + lane + 32 * u;
-            bok[u] = c < ncols;
-            bcol[u] = bok[u] ? P.in.col(c) : P.A;
-        }
-        for (int64_t kt = 0; kt < ktiles; ++kt) {
-            const int s = (int)(kt % STAGES);
-            const unsigned ph = (unsigned)((kt / STAGES) & 1);
-            mbar_wait(&empty[s], ph ^ 1u);
-            const int64_t k0 = kt * BK;
-            double* as = As + s * A_ELEMS + lane * KS;
-            double* bs = Bs + s * B_ELEMS + lane * KS;
-#pragma unroll
-            for (int cc = 0; cc < BK / 2; ++cc) {
-                const int ch = (cc + lane) & 7;
-                const int64_t kr = k0 + 2 * ch;
-                const int64_t rem = K - kr;
-                const int kval = rem >= 2 ? 2 : (rem > 0 ? (int)rem : 0);
-#pragma unroll
-                for (int u = 0; u < AU; ++u)
-                    cp_async_vec<2>(as + u * 32 * KS + 2 * ch, arow[u] + kr, aok[u] ? kval : 0, P.A);
-#pragma unroll
-                for (int u = 0; u < BU; ++u)
-                    cp_async_vec<2>(bs + u * 32 * KS + 2 * ch, bcol[u] + kr, bok[u] ? kval : 0, P.A);
+            for (int u = 0; u < AU; ++u) {
+                const int64_t row = xy.m0 + lane + 32 * u;
+                aok[u] = row < P.M;
+                arow[u] = P.A + (aok[u] ? row : 0) * P.lda;  // column `row` of A == row (symmetric)
             }
-            mbar_arrive_cp_async(&full[s]);
+#pragma unroll
+            for (int u = 0; u < BU; ++u) {
+                const int64_t c = xy.n0 + lane + 32 * u;
+                bok[u] = c < P.ncols;
+                bcol[u] = bok[u] ? P.in.col(c) : P.A;
+            }
+            for (int kt = (int)kb; kt < (int)ke; ++kt, ++it) {
+                const int s = (int)(it % STAGES);
+                const unsigned ph = (it / STAGES) & 1u;
+                mbar_wait(&empty[s], ph ^ 1u);
+                const int64_t k0 = kt * BK;
+                double* as = As + s * A_ELEMS + lane * KS;
+                double* bs = Bs + s * B_ELEMS + lane * KS;
+#pragma unroll
+                for (int cc = 0; cc < BK / 2; ++cc) {
+                    const int ch = (cc + lane) & 7;
+                    const int64_t kr = k0 + 2 * ch;
+                    const int64_t rem = K - kr;
+                    const int kval = rem >= 2 ? 2 : (rem > 0 ? (int)rem : 0);
+#pragma unroll
+                    for (int u = 0; u < AU; ++u)
+                        cp_async_vec<2>(as + u * 32 * KS + 2 * ch, arow[u] + kr, aok[u] ? kval : 0, safe);
+#pragma unroll
+                    for (int u = 0; u < BU; ++u)
+                        cp_async_vec<2>(bs + u * 32 * KS + 2 * ch, bcol[u] + kr, bok[u] ? kval : 0, safe);
+                }
+                mbar_arrive_cp_async(&full[s]);
+            }
         }
         cp_wait<0>();
         return;
@@ -515,17 +625,36 @@ __global__ void __launch_bounds__(WM * WN * 32 + 32, 1)
     // ===== consumer warps =====
     const int wm = warp % WM, wn = warp / WM;
     const int g = lane >> 2, t0 = lane & 3;
+    bool bad = false;
+    unsigned it = 0;
+    const int npieces = s_np;
+    for (int pc = 0; pc < npieces; ++pc) {
+    const int4 pe = s_piece[pc];
+    const int kb = pe.y, ke = pe.z, kind = pe.w;
     double acc[MI][NI][4];
+    if (kind == 2) {  // resume CTA b-1's accumulators (published by its first piece)
+        if (tid == 0)
+            while (ld_acquire(sk.flags + blockIdx.x - 1) == 0) __nanosleep(64);
+        asm volatile("bar.sync 1, %0;\n" ::"n"(NC) : "memory");
+        const double* src = sk.partial + (size_t)(blockIdx.x - 1) * (MI * NI * 4) * NC + tid;
 #pragma unroll
-    for (int i = 0; i < MI; ++i)
+        for (int i = 0; i < MI; ++i)
 #pragma unroll
-        for (int j = 0; j < NI; ++j)
+            for (int j = 0; j < NI; ++j)
 #pragma unroll
-            for (int v = 0; v < 4; ++v) acc[i][j][v] = 0.0;
+                for (int v = 0; v < 4; ++v) acc[i][j][v] = __ldcg(src + ((i * NI + j) * 4 + v) * NC);
+    } else {
+#pragma unroll
+        for (int i = 0; i < MI; ++i)
+#pragma unroll
+            for (int j = 0; j < NI; ++j)
+#pragma unroll
+                for (int v = 0; v < 4; ++v) acc[i][j][v] = 0.0;
+    }
 
-    for (int64_t kt = 0; kt < ktiles; ++kt) {
-        const int s = (int)(kt % STAGES);
-        const unsigned ph = (unsigned)((kt / STAGES) & 1);
+    for (int kt = (int)kb; kt < (int)ke; ++kt, ++it) {
+        const int s = (int)(it % STAGES);
+        const unsigned ph = (it / STAGES) & 1u;
         mbar_wait(&full[s], ph);
         const double* as = As + s * A_ELEMS;
         const double* bs = Bs + s * B_ELEMS;
@@ -555,40 +684,88 @@ __global__ void __launch_bounds__(WM * WN * 32 + 32, 1)
         if (lane == 0) mbar_arrive(&empty[s]);
     }
 
-    bool bad = false;
-    const double alpha = P.alpha;
+    if (kind == 1) {  // publish the raw accumulators of this tile's first k-tiles
+        double* dst = sk.partial + (size_t)blockIdx.x * (MI * NI * 4) * NC + tid;
+#pragma unroll
+        for (int i = 0; i < MI; ++i)
+#pragma unroll
+            for (int j = 0; j < NI; ++j)
+#pragma unroll
+                for (int v = 0; v < 4; ++v) __stcg(dst + ((i * NI + j) * 4 + v) * NC, acc[i][j][v]);
+        __threadfence();
+        asm volatile("bar.sync 1, %0;\n" ::"n"(NC) : "memory");
+        if (tid == 0) st_release(sk.flags + blockIdx.x, 1);
+        continue;
+    }
+    const TileXY xy = tile_xy<BM, BN>(s_tab, s_piece[pc].x);
+    // stores go through st.global (__stcg): a generic-pointer store could alias SMEM and
+    // would force a reload of the s_tab fields after each one
+    const ColMap& omap = s_tab.p[xy.pi].out;
+    const ColMap& amap = s_tab.p[xy.pi].add;
+    const int64_t Mrows = s_tab.p[xy.pi].M, ncols = s_tab.p[xy.pi].ncols;
+    const double alpha = s_tab.p[xy.pi].alpha;
 #pragma unroll
     for (int j = 0; j < NI; ++j) {
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
-            const int64_t c = n0 + wn * WTN + j * 8 + 2 * t0 + h;
+            const int64_t c = xy.n0 + wn * WTN + j * 8 + 2 * t0 + h;
             if (c >= ncols) continue;
-            double* outc = const_cast<double*>(P.out.col(c));
-            const double* addc = P.add.base ? P.add.col(c) : nullptr;
+            double* outc = const_cast<double*>(omap.col(c));
+            const double* addc = amap.base ? amap.col(c) : nullptr;
 #pragma unroll
             for (int i = 0; i < MI; ++i) {
 #pragma unroll
                 for (int v = 0; v < 2; ++v) {
-                    const int64_t r = m0 + wm * WTM + i * 16 + g + 8 * v;
-                    if (r >= M) continue;
+                    const int64_t r = xy.m0 + wm * WTM + i * 16 + g + 8 * v;
+                    if (r >= Mrows) continue;
                     double val = alpha * acc[i][j][2 * v + h];
                     if (addc) val = addc[r] + val;
                     bad |= !isfinite(val);
-                    outc[r] = val;
+                    __stcg(outc + r, val);
                 }
             }
         }
     }
+    }  // pieces
     if (status && __any_sync(0xffffffffu, bad) && lane == 0) atomicOr(status, ST_OUT_NONFINITE);
-    (void)NC;
 }
 
+// Grid: one CTA per SM in stream-K mode when the tile count is not a multiple of the SM
+// count (WC4DVAR_GEMM_SK=0 forces one CTA per tile).  Partials / flags come from the
+// stream-ordered pool, so concurrent GEMMs on different streams never share them.
 template <int BM, int BN, int WM, int WN, int STAGES>
 void launch_sym_ws(const PassTable& tab, int64_t ntiles, unsigned* status, cudaStream_t stream) {
+    constexpr int NC = WM * WN * 32;
     const size_t smem = sizeof(double) * STAGES * (BM * KS + BN * KS) + 2 * STAGES * sizeof(uint64_t);
     auto kern = gemm_sym_ws_kernel<BM, BN, WM, WN, STAGES>;
     configure_smem(reinterpret_cast<const void*>(kern), smem);
-    kern<<<(unsigned)ntiles, WM * WN * 32 + 32, smem, stream>>>(tab, status);
+    static const int sk_mode = [] {
+        const char* e = std::getenv("WC4DVAR_GEMM_SK");
+        return e ? std::atoi(e) : 1;
+    }();
+    const int first = tab.tile_start[1] > 0 ? 0 : 1;
+    SkArgs sk{cdiv(tab.p[first].K, BK), nullptr, nullptr};
+    bool same_k = true;
+    for (int i = 0; i < 2; ++i)
+        if (tab.tile_start[i + 1] > tab.tile_start[i]) same_k = same_k && tab.p[i].K == tab.p[first].K;
+    int64_t grid = ntiles;
+    if (sk_mode && same_k && ntiles > kSMs && ntiles % kSMs != 0 && ntiles / kSMs + 3 <= kSkMaxPieces &&
+        ntiles < (int64_t)1 << 31 && sk.KT < (int64_t)1 << 31)
+        grid = kSMs;
+    if (grid != ntiles) {
+        keep_pool_reserved();
+        const size_t pbytes = sizeof(double) * (size_t)grid * NC * (BM * BN / NC);
+        char* buf = nullptr;
+        W4_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&buf), pbytes + sizeof(int) * grid, stream));
+        sk.partial = reinterpret_cast<double*>(buf);
+        sk.flags = reinterpret_cast<int*>(buf + pbytes);
+        W4_CUDA(cudaMemsetAsync(sk.flags, 0, sizeof(int) * grid, stream));
+        kern<<<(unsigned)grid, NC + 32, smem, stream>>>(tab, status, sk);
+        W4_LAUNCH();
+        W4_CUDA(cudaFreeAsync(buf, stream));
+        return;
+    }
+    kern<<<(unsigned)grid, NC + 32, smem, stream>>>(tab, status, sk);
     W4_LAUNCH();
 }
 

@@ -115,6 +115,18 @@ def test_block_equals_columns_bitwise_and_counts():  # :188-221
         assert np.array_equal(B[:, j], g2.apply(V[:, j]))
 
 
+def test_stream_k_block_equals_columns_bitwise():
+    """At C2 size the D^1/2 GEMM runs stream-K (272 tiles on 148 SMs, tiles split across
+    CTAs); the split resumes the published DMMA accumulators, so the block apply still equals
+    the column-wise apply (one-CTA-per-tile kernels) bit for bit (test_operators.cpp:188-211)."""
+    g = configs.config2().hessian(0)
+    V = O.gaussian_matrix(g.dim(), 100, 5)
+    B = g.apply_block(V)
+    for j in (0, 37, 63, 99):
+        assert np.array_equal(B[:, j], g.apply(V[:, j])), j
+    assert np.array_equal(g.apply_block(V), B)  # run-to-run deterministic
+
+
 def test_errors():  # :263-277
     g, _ = pair(W.IdentityLinearized(4, 2), W.ObservationNetwork.build(4, 2, 2, 1), identity_factor(4),
                 identity_factor(4), 1.0)
