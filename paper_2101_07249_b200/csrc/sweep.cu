@@ -193,15 +193,22 @@ __device__ __forceinline__ double adj3(double l, double c, double r, double cc, 
     return fma(dd, l, fma(cc + dd, r, (1.0 - cc - 2.0 * dd) * c));
 }
 
+// SMEM state rows use a point-major ("transposed") layout: grid point j lives at
+// (j % P) * ntp + j / P, ntp = ceil(n / P).  Thread t owns points [tP, tP + P), so when a warp
+// reads its u-th halo/centre value the 32 addresses are consecutive -- conflict-free -- where
+// the natural layout (stride P doubles between threads) is a 16-way bank conflict.
+template <int P>
+__device__ __forceinline__ int pm_slot(int j, int ntp) { return (j % P) * ntp + j / P; }
+
 template <int KIND, int S, int P, bool ADJ>
-__device__ __forceinline__ void advance_interval(const double* __restrict__ cur, int b, int n,
+__device__ __forceinline__ void advance_interval(const double* __restrict__ cur, int b, int n, int ntp,
                                                  double cc, double dd, double (&v)[P + 2 * S]) {
     constexpr int L = P + 2 * S;
     int j = (b - S) % n;
     if (j < 0) j += n;
 #pragma unroll
     for (int u = 0; u < L; ++u) {
-        v[u] = cur[j];
+        v[u] = cur[pm_slot<P>(j, ntp)];
         j = (j + 1 == n) ? 0 : j + 1;
     }
 #pragma unroll
@@ -224,9 +231,10 @@ __global__ void __launch_bounds__(512)
     const int n = (int)md.n;
     const int N = md.N;
     const double c = md.c, d = md.d;
+    const int ntp = (n + P - 1) / P;  // point-major rows (see pm_slot)
     double* buf0 = sm;
-    double* buf1 = sm + n;
-    int* pmap = reinterpret_cast<int*>(sm + 2 * n);  // observation tables staged in SMEM
+    double* buf1 = sm + P * ntp;
+    int* pmap = reinterpret_cast<int*>(sm + 2 * P * ntp);  // observation tables staged in SMEM
     int* slot = pmap + n;
     const int64_t col = blockIdx.x;
     const int tid = threadIdx.x, nt = blockDim.x;
@@ -247,7 +255,7 @@ __global__ void __launch_bounds__(512)
             const int sl = slot[0];
             for (int j = tid; j < n; j += nt) {
                 const double x = X[j];
-                buf0[j] = x;
+                buf0[pm_slot<P>(j, ntp)] = x;
                 bad_f |= !isfinite(x);
                 if (tr) tr[j] = x;
                 if (a.fwd_obs && sl >= 0) {
@@ -271,13 +279,13 @@ __global__ void __launch_bounds__(512)
 #pragma unroll
             for (int p = 0; p < P; ++p) xnx[p] = (owner && i + 1 < N && b + p < n) ? Xnn[b + p] : 0.0;
             if (owner) {
-                advance_interval<KIND, S, P, false>(cur, b, n, c, d, v);
+                advance_interval<KIND, S, P, false>(cur, b, n, ntp, c, d, v);
 #pragma unroll
                 for (int p = 0; p < P; ++p) {
                     const int j = b + p;
                     if (j < n) {
                         const double x = v[S + p] + xin[p];
-                        nxt[j] = x;
+                        nxt[p * ntp + tid] = x;
                         bad_f |= !isfinite(x);
                         if (trn) trn[j] = x;
                         if (a.fwd_obs && sl >= 0) {
@@ -316,7 +324,7 @@ __global__ void __launch_bounds__(512)
             const int64_t off = (int64_t)N * n;
             for (int j = tid; j < n; j += nt) {
                 const double x = addend(N, j);
-                buf0[j] = x;
+                buf0[pm_slot<P>(j, ntp)] = x;
                 Sv[off + j] = x;
                 bad_a |= !isfinite(x);
             }
@@ -333,13 +341,13 @@ __global__ void __launch_bounds__(512)
 #pragma unroll
             for (int p = 0; p < P; ++p) anx[p] = (owner && i > 0 && b + p < n) ? addend(i - 1, b + p) : 0.0;
             if (owner) {
-                advance_interval<KIND, S, P, true>(cur, b, n, c, d, v);
+                advance_interval<KIND, S, P, true>(cur, b, n, ntp, c, d, v);
 #pragma unroll
                 for (int p = 0; p < P; ++p) {
                     const int j = b + p;
                     if (j < n) {
                         const double x = ain[p] + v[S + p];  // operators.cpp:99 (v_i + back)
-                        nxt[j] = x;
+                        nxt[p * ntp + tid] = x;
                         Sv[off + j] = x;
                         bad_a |= !isfinite(x);
                     }
@@ -367,7 +375,7 @@ bool launch_blocked_s(const ModelDev& md, const NetDev& net, const SweepArgs& a,
     const int64_t owners = (md.n + P - 1) / P;
     if (owners > 512) return false;
     int nt = (int)((owners + 31) / 32) * 32;
-    const size_t smem = sizeof(double) * 2 * md.n + sizeof(int) * (md.n + md.N + 1);
+    const size_t smem = sizeof(double) * 2 * P * owners + sizeof(int) * (md.n + md.N + 1);
     if (smem > 200 * 1024) return false;
     auto kern = sweep_blocked_kernel<KIND, S, P>;
     if (smem > 48 * 1024)

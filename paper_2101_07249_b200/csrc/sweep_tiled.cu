@@ -439,7 +439,7 @@ __device__ __forceinline__ void blk_advance(const double* __restrict__ cur, int 
     for (int u = 0; u < L; ++u) {
         int j = b - S + u;
         j = j < 0 ? 0 : (j >= R ? R - 1 : j);  // clamped lanes feed only discarded points
-        v[u] = cur[j];
+        v[u] = cur[(j % P) * (R / P) + j / P];  // point-major row (pm_slot in sweep.cu)
     }
 #pragma unroll
     for (int k = 0; k < S; ++k) {
@@ -479,12 +479,14 @@ __global__ void __launch_bounds__(512) tiled_blk_fwd_kernel(const TiledArgs ta, 
     double v[P + 2 * S];
 
     const double* src = ta.bin ? ta.bin + col * n : X;
-    for (int e = tid; e < R; e += nt) cur[e] = src[rg.gidx(e)];
+    // SMEM rows are point-major: region point e at (e % P) * nt + e / P (conflict-free
+    // per-thread gathers, see blk_advance)
+    for (int e = tid; e < R; e += nt) cur[(e % P) * nt + e / P] = src[rg.gidx(e)];
     if (ta.i0 == 0) {
         const int sl = net.slot[0];
         for (int e = c_lo + tid; e < c_hi; e += nt) {
             const int g = rg.gidx(e);
-            const double x = cur[e];
+            const double x = cur[(e % P) * nt + e / P];
             bad |= !isfinite(x);
             if (tr) tr[g] = x;
             if (a.fwd_obs && sl >= 0) {
@@ -509,7 +511,7 @@ __global__ void __launch_bounds__(512) tiled_blk_fwd_kernel(const TiledArgs ta, 
                 if (e >= lo && e < hi) {
                     const int g = rg.gidx(e);
                     const double x = v[S + p] + Xn[g];  // operators.cpp:88
-                    nxt[e] = x;
+                    nxt[p * nt + tid] = x;
                     if (e >= c_lo && e < c_hi) {
                         bad |= !isfinite(x);
                         if (trn) trn[g] = x;
@@ -527,7 +529,7 @@ __global__ void __launch_bounds__(512) tiled_blk_fwd_kernel(const TiledArgs ta, 
         nxt = t;
     }
     if (ta.bout)
-        for (int e = c_lo + tid; e < c_hi; e += nt) ta.bout[col * n + rg.gidx(e)] = cur[e];
+        for (int e = c_lo + tid; e < c_hi; e += nt) ta.bout[col * n + rg.gidx(e)] = cur[(e % P) * nt + e / P];
     if (__syncthreads_or(bad) && tid == 0) atomicOr(status, ST_FWD_NONFINITE);
 }
 
@@ -567,12 +569,12 @@ __global__ void __launch_bounds__(512) tiled_blk_adj_kernel(const TiledArgs ta, 
         return x;
     };
     if (ta.bin) {
-        for (int e = tid; e < R; e += nt) cur[e] = ta.bin[col * n + rg.gidx(e)];
+        for (int e = tid; e < R; e += nt) cur[(e % P) * nt + e / P] = ta.bin[col * n + rg.gidx(e)];
     } else {
         for (int e = tid; e < R; e += nt) {
             const int g = rg.gidx(e);
             const double x = addend(ta.i1, g);
-            cur[e] = x;
+            cur[(e % P) * nt + e / P] = x;
             if (e >= c_lo && e < c_hi) {
                 Sv[(int64_t)ta.i1 * n + g] = x;
                 bad |= !isfinite(x);
@@ -592,7 +594,7 @@ __global__ void __launch_bounds__(512) tiled_blk_adj_kernel(const TiledArgs ta, 
                 if (e >= lo && e < hi) {
                     const int g = rg.gidx(e);
                     const double x = addend(i, g) + v[S + p];  // operators.cpp:99
-                    nxt[e] = x;
+                    nxt[p * nt + tid] = x;
                     if (e >= c_lo && e < c_hi) {
                         Sv[(int64_t)i * n + g] = x;
                         bad |= !isfinite(x);
@@ -606,7 +608,7 @@ __global__ void __launch_bounds__(512) tiled_blk_adj_kernel(const TiledArgs ta, 
         nxt = t;
     }
     if (ta.bout)
-        for (int e = c_lo + tid; e < c_hi; e += nt) ta.bout[col * n + rg.gidx(e)] = cur[e];
+        for (int e = c_lo + tid; e < c_hi; e += nt) ta.bout[col * n + rg.gidx(e)] = cur[(e % P) * nt + e / P];
     if (__syncthreads_or(bad) && tid == 0) atomicOr(status, ST_ADJ_NONFINITE);
 }
 
