@@ -432,14 +432,14 @@ __device__ __forceinline__ double adj3t(double l, double c, double r, double cc,
 }
 
 template <int KIND, int S, int P, bool ADJ>
-__device__ __forceinline__ void blk_advance(const double* __restrict__ cur, int b, int R, double cc,
+__device__ __forceinline__ void blk_advance(const double* __restrict__ cur, int b, int R, int ns, double cc,
                                             double dd, double (&v)[P + 2 * S]) {
     constexpr int L = P + 2 * S;
 #pragma unroll
     for (int u = 0; u < L; ++u) {
         int j = b - S + u;
         j = j < 0 ? 0 : (j >= R ? R - 1 : j);  // clamped lanes feed only discarded points
-        v[u] = cur[(j % P) * (R / P) + j / P];  // point-major row (pm_slot in sweep.cu)
+        v[u] = cur[(j % P) * ns + j / P];       // point-major row, stride ns (see blk kernels)
     }
 #pragma unroll
     for (int k = 0; k < S; ++k) {
@@ -453,7 +453,21 @@ __device__ __forceinline__ void blk_advance(const double* __restrict__ cur, int 
     }
 }
 
-template <int KIND, int S, int P>
+// SMEM rows of the blocked tiles are point-major with a padded stride ns = nt + 2: region
+// point e lives at (e % P) * ns + e / P.  Per-thread gathers (blk_advance) and the owner's
+// P results then hit 32 consecutive slots per warp (conflict-free), and the coalesced
+// row passes (loads, trajectory / state emits) see at most 2-way conflicts.
+__device__ __forceinline__ void cp8(double* dst, const double* src) {
+    const unsigned d = static_cast<unsigned>(__cvta_generic_to_shared(dst));
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(d), "l"(src));
+}
+
+// Each CTA runs intervals i0..i1 of one tile of one column.  Per interval: one barrier,
+// then (a) a coalesced pass that emits the previous state's tile centre (finite check,
+// trajectory, observations -- stores coalesced instead of stride-P per thread), (b) the
+// next interval's forcing row issued by cp.async into a double buffer (lands while the S
+// sub-steps compute), (c) the register-blocked advance.
+template <int KIND, int S, int SB, int P>
 __global__ void __launch_bounds__(512) tiled_blk_fwd_kernel(const TiledArgs ta, unsigned* status) {
     extern __shared__ double sm[];
     const ModelDev& md = ta.md;
@@ -461,12 +475,15 @@ __global__ void __launch_bounds__(512) tiled_blk_fwd_kernel(const TiledArgs ta, 
     const SweepArgs& a = ta.a;
     const TileGeom& geo = ta.geo;
     const int R = geo.R;
+    const int tid = threadIdx.x, nt = blockDim.x;
+    const int ns = nt + 2, RS = P * ns;
     double* cur = sm;
-    double* nxt = sm + R;
+    double* nxt = sm + RS;
+    double* const fx0 = sm + 2 * RS;  // forcing X_{i+1}, prefetched (double buffer)
+    double* const fx1 = sm + 3 * RS;
     const int n = (int)md.n;
     const int64_t col = blockIdx.x;
     const int64_t t0 = (int64_t)blockIdx.y * geo.T;
-    const int tid = threadIdx.x, nt = blockDim.x;
     const Region rg{R, false, (int)(t0 - geo.HL), n};
     const int c_lo = geo.HL;
     const int c_hi = geo.HL + (int)((int64_t)n - t0 < geo.T ? (int64_t)n - t0 : geo.T);
@@ -476,64 +493,66 @@ __global__ void __launch_bounds__(512) tiled_blk_fwd_kernel(const TiledArgs ta, 
     const int np = net.n_points;
     const int b = tid * P;
     bool bad = false;
-    double v[P + 2 * S];
+    double v[P + 2 * SB];
+    auto slot = [&](int e) { return (e % P) * ns + e / P; };
+    auto load_row = [&](double* dst, const double* row) {
+        for (int e = tid; e < R; e += nt) cp8(dst + slot(e), row + rg.gidx(e));
+        asm volatile("cp.async.commit_group;\n");
+    };
 
-    const double* src = ta.bin ? ta.bin + col * n : X;
-    // SMEM rows are point-major: region point e at (e % P) * nt + e / P (conflict-free
-    // per-thread gathers, see blk_advance)
-    for (int e = tid; e < R; e += nt) cur[(e % P) * nt + e / P] = src[rg.gidx(e)];
-    if (ta.i0 == 0) {
-        const int sl = net.slot[0];
-        for (int e = c_lo + tid; e < c_hi; e += nt) {
-            const int g = rg.gidx(e);
-            const double x = cur[(e % P) * nt + e / P];
-            bad |= !isfinite(x);
-            if (tr) tr[g] = x;
-            if (a.fwd_obs && sl >= 0) {
-                const int bb = net.pmap[g];
-                if (bb >= 0) Yc[(int64_t)sl * np + bb] = a.scale_fwd * x;
-            }
-        }
-    }
-    __syncthreads();
+    if (ta.i1 > ta.i0) load_row(fx0, X + (int64_t)(ta.i0 + 1) * n);
+    const double* src = ta.bin ? ta.bin + col * n : X;  // x_0 = X_0
+    for (int e = tid; e < R; e += nt) cur[slot(e)] = src[rg.gidx(e)];
     int lo = 0, hi = R;
-    for (int i = ta.i0; i < ta.i1; ++i) {
-        lo += S;
-        hi -= S;
-        const double* Xn = X + (int64_t)(i + 1) * n;
-        const int sl = net.slot[i + 1];
-        double* trn = tr ? tr + (int64_t)(i + 1) * n : nullptr;
-        if (b + P > lo && b < hi) {
-            blk_advance<KIND, S, P, false>(cur, b, R, md.c, md.d, v);
-#pragma unroll
-            for (int p = 0; p < P; ++p) {
-                const int e = b + p;
-                if (e >= lo && e < hi) {
-                    const int g = rg.gidx(e);
-                    const double x = v[S + p] + Xn[g];  // operators.cpp:88
-                    nxt[p * nt + tid] = x;
-                    if (e >= c_lo && e < c_hi) {
-                        bad |= !isfinite(x);
-                        if (trn) trn[g] = x;
-                        if (a.fwd_obs && sl >= 0) {
-                            const int bb = net.pmap[g];
-                            if (bb >= 0) Yc[(int64_t)sl * np + bb] = a.scale_fwd * x;
-                        }
-                    }
+    for (int i = ta.i0;; ++i) {
+        cp_async_wait_all();
+        __syncthreads();
+        // emit x_i on the tile centre (x_{i0} only at the window start: otherwise the
+        // previous launch emitted it)
+        if (i > ta.i0 || ta.i0 == 0) {
+            const int sl = net.slot[i];
+            double* tri = tr ? tr + (int64_t)i * n : nullptr;
+            for (int e = c_lo + tid; e < c_hi; e += nt) {
+                const int g = rg.gidx(e);
+                const double x = cur[slot(e)];
+                bad |= !isfinite(x);
+                if (tri) tri[g] = x;
+                if (a.fwd_obs && sl >= 0) {
+                    const int bb = net.pmap[g];
+                    if (bb >= 0) Yc[(int64_t)sl * np + bb] = a.scale_fwd * x;
                 }
             }
         }
-        __syncthreads();
-        double* t = cur;
-        cur = nxt;
-        nxt = t;
+        if (i == ta.i1) break;
+        const int k = i - ta.i0;
+        if (i + 2 <= ta.i1) load_row((k & 1) ? fx0 : fx1, X + (int64_t)(i + 2) * n);
+        // S sub-steps in S / SB register blocks of SB sub-steps (one barrier between blocks)
+        for (int blk = 0; blk < S / SB; ++blk) {
+            const bool last = blk + 1 == S / SB;
+            if (blk > 0) __syncthreads();
+            lo += SB;
+            hi -= SB;
+            if (b + P > lo && b < hi) {
+                blk_advance<KIND, SB, P, false>(cur, b, R, ns, md.c, md.d, v);
+                const double* f = (k & 1) ? fx1 : fx0;
+#pragma unroll
+                for (int p = 0; p < P; ++p) {
+                    const int e = b + p;
+                    if (e >= lo && e < hi)  // x_{i+1} = M_i x_i + X_{i+1}  (operators.cpp:88)
+                        nxt[p * ns + tid] = last ? v[SB + p] + f[p * ns + tid] : v[SB + p];
+                }
+            }
+            double* t = cur;
+            cur = nxt;
+            nxt = t;
+        }
     }
     if (ta.bout)
-        for (int e = c_lo + tid; e < c_hi; e += nt) ta.bout[col * n + rg.gidx(e)] = cur[(e % P) * nt + e / P];
+        for (int e = c_lo + tid; e < c_hi; e += nt) ta.bout[col * n + rg.gidx(e)] = cur[slot(e)];
     if (__syncthreads_or(bad) && tid == 0) atomicOr(status, ST_FWD_NONFINITE);
 }
 
-template <int KIND, int S, int P>
+template <int KIND, int S, int SB, int P>
 __global__ void __launch_bounds__(512) tiled_blk_adj_kernel(const TiledArgs ta, unsigned* status) {
     extern __shared__ double sm[];
     const ModelDev& md = ta.md;
@@ -541,12 +560,15 @@ __global__ void __launch_bounds__(512) tiled_blk_adj_kernel(const TiledArgs ta, 
     const SweepArgs& a = ta.a;
     const TileGeom& geo = ta.geo;
     const int R = geo.R;
+    const int tid = threadIdx.x, nt = blockDim.x;
+    const int ns = nt + 2, RS = P * ns;
     double* cur = sm;
-    double* nxt = sm + R;
+    double* nxt = sm + RS;
+    double* const vb0 = sm + 2 * RS;  // v_{i-1} rows, prefetched (double buffer)
+    double* const vb1 = sm + 3 * RS;
     const int n = (int)md.n;
     const int64_t col = blockIdx.x;
     const int64_t t0 = (int64_t)blockIdx.y * geo.T;
-    const int tid = threadIdx.x, nt = blockDim.x;
     const Region rg{R, false, (int)(t0 - geo.HR), n};
     const int c_lo = geo.HR;
     const int c_hi = geo.HR + (int)((int64_t)n - t0 < geo.T ? (int64_t)n - t0 : geo.T);
@@ -556,9 +578,14 @@ __global__ void __launch_bounds__(512) tiled_blk_adj_kernel(const TiledArgs ta, 
     const int np = net.n_points;
     const int b = tid * P;
     bool bad = false;
-    double v[P + 2 * S];
-    auto addend = [&](int i, int g) -> double {
-        double x = V ? V[(int64_t)i * n + g] : 0.0;
+    double v[P + 2 * SB];
+    auto slot = [&](int e) { return (e % P) * ns + e / P; };
+    auto load_row = [&](double* dst, const double* row) {
+        for (int e = tid; e < R; e += nt) cp8(dst + slot(e), row + rg.gidx(e));
+        asm volatile("cp.async.commit_group;\n");
+    };
+    // H_i^T y part of the addend (sparse: observed points of observed times)
+    auto obs_add = [&](int i, int g, double x) -> double {
         if (a.adj_obs) {
             const int sl = net.slot[i];
             if (sl >= 0) {
@@ -568,52 +595,65 @@ __global__ void __launch_bounds__(512) tiled_blk_adj_kernel(const TiledArgs ta, 
         }
         return x;
     };
+
+    if (V && ta.i1 > ta.i0) load_row(vb0, V + (int64_t)(ta.i1 - 1) * n);
     if (ta.bin) {
-        for (int e = tid; e < R; e += nt) cur[(e % P) * nt + e / P] = ta.bin[col * n + rg.gidx(e)];
-    } else {
+        for (int e = tid; e < R; e += nt) cur[slot(e)] = ta.bin[col * n + rg.gidx(e)];
+    } else {  // s_N = v_N + H_N^T y
         for (int e = tid; e < R; e += nt) {
             const int g = rg.gidx(e);
-            const double x = addend(ta.i1, g);
-            cur[(e % P) * nt + e / P] = x;
-            if (e >= c_lo && e < c_hi) {
-                Sv[(int64_t)ta.i1 * n + g] = x;
+            cur[slot(e)] = obs_add(ta.i1, g, V ? V[(int64_t)ta.i1 * n + g] : 0.0);
+        }
+    }
+    int lo = 0, hi = R;
+    for (int i = ta.i1;; --i) {  // cur = s_i
+        cp_async_wait_all();
+        __syncthreads();
+        if (i < ta.i1 || !ta.bin) {  // emit s_i on the tile centre
+            for (int e = c_lo + tid; e < c_hi; e += nt) {
+                const double x = cur[slot(e)];
+                Sv[(int64_t)i * n + rg.gidx(e)] = x;
                 bad |= !isfinite(x);
             }
         }
-    }
-    __syncthreads();
-    int lo = 0, hi = R;
-    for (int i = ta.i1 - 1; i >= ta.i0; --i) {
-        lo += S;
-        hi -= S;
-        if (b + P > lo && b < hi) {
-            blk_advance<KIND, S, P, true>(cur, b, R, md.c, md.d, v);
+        if (i == ta.i0) break;
+        const int k = ta.i1 - i;
+        if (V && i - 2 >= ta.i0) load_row((k & 1) ? vb0 : vb1, V + (int64_t)(i - 2) * n);
+        for (int blk = 0; blk < S / SB; ++blk) {  // S / SB register blocks (see fwd)
+            const bool last = blk + 1 == S / SB;
+            if (blk > 0) __syncthreads();
+            lo += SB;
+            hi -= SB;
+            if (b + P > lo && b < hi) {
+                blk_advance<KIND, SB, P, true>(cur, b, R, ns, md.c, md.d, v);
+                const double* vr = (k & 1) ? vb1 : vb0;
 #pragma unroll
-            for (int p = 0; p < P; ++p) {
-                const int e = b + p;
-                if (e >= lo && e < hi) {
-                    const int g = rg.gidx(e);
-                    const double x = addend(i, g) + v[S + p];  // operators.cpp:99
-                    nxt[p * nt + tid] = x;
-                    if (e >= c_lo && e < c_hi) {
-                        Sv[(int64_t)i * n + g] = x;
-                        bad |= !isfinite(x);
+                for (int p = 0; p < P; ++p) {
+                    const int e = b + p;
+                    if (e >= lo && e < hi) {
+                        if (last) {
+                            // s_{i-1} = v_{i-1} + H^T y + M^T s_i  (operators.cpp:99)
+                            const double ad = obs_add(i - 1, rg.gidx(e), V ? vr[p * ns + tid] : 0.0);
+                            nxt[p * ns + tid] = ad + v[SB + p];
+                        } else {
+                            nxt[p * ns + tid] = v[SB + p];
+                        }
                     }
                 }
             }
+            double* t = cur;
+            cur = nxt;
+            nxt = t;
         }
-        __syncthreads();
-        double* t = cur;
-        cur = nxt;
-        nxt = t;
     }
     if (ta.bout)
-        for (int e = c_lo + tid; e < c_hi; e += nt) ta.bout[col * n + rg.gidx(e)] = cur[(e % P) * nt + e / P];
+        for (int e = c_lo + tid; e < c_hi; e += nt) ta.bout[col * n + rg.gidx(e)] = cur[slot(e)];
     if (__syncthreads_or(bad) && tid == 0) atomicOr(status, ST_ADJ_NONFINITE);
 }
 
-// Register-blocked tiled launch (radius-1 models, S in {1,5,10}); false if not applicable.
-template <int KIND, int S>
+// Register-blocked tiled launch (radius-1 models, S in {1,5,10}, SB sub-steps per register
+// block); false if not applicable.
+template <int KIND, int S, int SB>
 bool launch_tiled_blk(const ModelDev& md, const NetDev& net, const SweepArgs& a, unsigned* status,
                       cudaStream_t st, DevBuf& ws, int tile_override) {
     constexpr int P = 8;
@@ -632,9 +672,9 @@ bool launch_tiled_blk(const ModelDev& md, const NetDev& net, const SweepArgs& a,
     }
     if (nt > 512 || T <= 0 || R > md.n) return false;
     TileGeom geo{T, K * S, K * S, R, false, cdiv(md.n, T)};
-    const size_t smem = sizeof(double) * 2 * (size_t)R;
-    auto fk = tiled_blk_fwd_kernel<KIND, S, P>;
-    auto ak = tiled_blk_adj_kernel<KIND, S, P>;
+    const size_t smem = sizeof(double) * 4 * (size_t)P * (nt + 2);  // cur, nxt, 2 prefetch rows
+    auto fk = tiled_blk_fwd_kernel<KIND, S, SB, P>;
+    auto ak = tiled_blk_adj_kernel<KIND, S, SB, P>;
     W4_CUDA(cudaFuncSetAttribute(fk, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     W4_CUDA(cudaFuncSetAttribute(ak, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     const int nl = (int)cdiv(md.N, K);
@@ -1155,11 +1195,23 @@ void launch_tiled(const ModelDev& md, const NetDev& net, const SweepArgs& a, uns
         geo.ntiles = 1;
     } else {
         if (KIND != WC4DVAR_MODEL_LORENZ96) {
+            // WC4DVAR_SWEEP_SB: sub-steps per register block (default 5; s=10 also 2 / 10)
+            static const int sb = [] {
+                const char* e = std::getenv("WC4DVAR_SWEEP_SB");
+                return e ? std::atoi(e) : 5;
+            }();
             bool done = false;
             switch (md.s) {
-                case 1: done = launch_tiled_blk<KIND, 1>(md, net, a, status, st, ws, tile_override); break;
-                case 5: done = launch_tiled_blk<KIND, 5>(md, net, a, status, st, ws, tile_override); break;
-                case 10: done = launch_tiled_blk<KIND, 10>(md, net, a, status, st, ws, tile_override); break;
+                case 1: done = launch_tiled_blk<KIND, 1, 1>(md, net, a, status, st, ws, tile_override); break;
+                case 5:
+                    done = sb == 1 ? launch_tiled_blk<KIND, 5, 1>(md, net, a, status, st, ws, tile_override)
+                                   : launch_tiled_blk<KIND, 5, 5>(md, net, a, status, st, ws, tile_override);
+                    break;
+                case 10:
+                    done = sb == 2    ? launch_tiled_blk<KIND, 10, 2>(md, net, a, status, st, ws, tile_override)
+                           : sb == 10 ? launch_tiled_blk<KIND, 10, 10>(md, net, a, status, st, ws, tile_override)
+                                      : launch_tiled_blk<KIND, 10, 5>(md, net, a, status, st, ws, tile_override);
+                    break;
                 default: break;
             }
             if (done) return;
