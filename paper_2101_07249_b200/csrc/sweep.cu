@@ -223,10 +223,35 @@ __device__ __forceinline__ void advance_interval(const double* __restrict__ cur,
     }
 }
 
+// One interval as the fused (2S+1)-tap stencil (see StencilTaps); results land in
+// v[S .. S+P) like advance_interval's.
+template <int S, int P>
+__device__ __forceinline__ void conv_interval(const double* __restrict__ cur, int b, int n, int ntp,
+                                              const StencilTaps& tp, double (&v)[P + 2 * S]) {
+    constexpr int L = P + 2 * S;
+    int j = (b - S) % n;
+    if (j < 0) j += n;
+#pragma unroll
+    for (int u = 0; u < L; ++u) {
+        v[u] = cur[pm_slot<P>(j, ntp)];
+        j = (j + 1 == n) ? 0 : j + 1;
+    }
+    double o[P];
+#pragma unroll
+    for (int p = 0; p < P; ++p) {
+        double acc = tp.t[0] * v[p];
+#pragma unroll
+        for (int k = 1; k <= 2 * S; ++k) acc = fma(tp.t[k], v[p + k], acc);
+        o[p] = acc;
+    }
+#pragma unroll
+    for (int p = 0; p < P; ++p) v[S + p] = o[p];
+}
+
 template <int KIND, int S, int P>
 __global__ void __launch_bounds__(512)
-    sweep_blocked_kernel(const ModelDev md, const NetDev net, const SweepArgs a,
-                         unsigned* __restrict__ status) {
+    sweep_blocked_kernel(const ModelDev md, const NetDev net, const SweepArgs a, const StencilTaps tf,
+                         const StencilTaps tb, unsigned* __restrict__ status) {
     extern __shared__ double sm[];
     const int n = (int)md.n;
     const int N = md.N;
@@ -279,7 +304,7 @@ __global__ void __launch_bounds__(512)
 #pragma unroll
             for (int p = 0; p < P; ++p) xnx[p] = (owner && i + 1 < N && b + p < n) ? Xnn[b + p] : 0.0;
             if (owner) {
-                advance_interval<KIND, S, P, false>(cur, b, n, ntp, c, d, v);
+                conv_interval<S, P>(cur, b, n, ntp, tf, v);
 #pragma unroll
                 for (int p = 0; p < P; ++p) {
                     const int j = b + p;
@@ -341,7 +366,7 @@ __global__ void __launch_bounds__(512)
 #pragma unroll
             for (int p = 0; p < P; ++p) anx[p] = (owner && i > 0 && b + p < n) ? addend(i - 1, b + p) : 0.0;
             if (owner) {
-                advance_interval<KIND, S, P, true>(cur, b, n, ntp, c, d, v);
+                conv_interval<S, P>(cur, b, n, ntp, tb, v);
 #pragma unroll
                 for (int p = 0; p < P; ++p) {
                     const int j = b + p;
@@ -380,7 +405,9 @@ bool launch_blocked_s(const ModelDev& md, const NetDev& net, const SweepArgs& a,
     auto kern = sweep_blocked_kernel<KIND, S, P>;
     if (smem > 48 * 1024)
         W4_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    kern<<<(unsigned)a.m, nt, smem, stream>>>(md, net, a, status);
+    const StencilTaps tf = stencil_power(KIND, md.c, md.d, S, false);
+    const StencilTaps tb = stencil_power(KIND, md.c, md.d, S, true);
+    kern<<<(unsigned)a.m, nt, smem, stream>>>(md, net, a, tf, tb, status);
     W4_LAUNCH();
     return true;
 }
@@ -415,6 +442,36 @@ void launch_resident(const ModelDev& md, const NetDev& net, const SweepArgs& a, 
 }  // namespace
 
 int64_t sweep_resident_max_n() { return (227 * 1024) / (2 * sizeof(double)); }
+
+StencilTaps stencil_power(int kind, double c, double d, int s, bool adjoint) {
+    require(s >= 1 && s <= kMaxFusedS, "stencil_power: sub-steps out of range");
+    // one step: coefficients of x_{j-1}, x_j, x_{j+1} (models.cpp:27-45; adjoint mirrored)
+    long double lft = 0, mid = 1, rgt = 0;
+    if (kind == WC4DVAR_MODEL_ADVECTION) {
+        lft = c;
+        mid = 1.0L - c;
+    } else if (kind == WC4DVAR_MODEL_ADVDIFF) {
+        lft = (long double)c + d;
+        mid = 1.0L - c - 2.0L * d;
+        rgt = d;
+    }
+    if (adjoint) std::swap(lft, rgt);
+    long double poly[2 * kMaxFusedS + 1] = {1.0L};
+    int len = 1;
+    for (int k = 0; k < s; ++k) {  // poly <- poly * (lft z^-1 + mid + rgt z)
+        long double nx[2 * kMaxFusedS + 1] = {};
+        for (int i = 0; i < len; ++i) {
+            nx[i] += poly[i] * lft;
+            nx[i + 1] += poly[i] * mid;
+            nx[i + 2] += poly[i] * rgt;
+        }
+        len += 2;
+        for (int i = 0; i < len; ++i) poly[i] = nx[i];
+    }
+    StencilTaps t{};
+    for (int i = 0; i < len; ++i) t.t[i] = (double)poly[i];
+    return t;
+}
 
 void sweep(const ModelDev& md, const NetDev& net, const SweepArgs& a, unsigned* status,
            cudaStream_t stream, DevBuf* ws) {

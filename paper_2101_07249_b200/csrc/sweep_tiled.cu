@@ -130,6 +130,7 @@ struct TiledArgs {
     int i0, i1;             // forward: intervals [i0, i1); adjoint: from state s_{i1} down to s_{i0}
     const double* bin;      // boundary state in (n x m, ld n) or null (start of window)
     double* bout;           // boundary state out
+    StencilTaps tp{};       // fused S-step stencil of this direction (blocked stencil kernels)
 };
 
 // ---------------------------------------------------------------- forward
@@ -453,6 +454,30 @@ __device__ __forceinline__ void blk_advance(const double* __restrict__ cur, int 
     }
 }
 
+// Gather P + 2S region values (clamped lanes feed only discarded points) and apply the fused
+// S-step stencil; results in v[S .. S+P).
+template <int S, int P>
+__device__ __forceinline__ void blk_conv(const double* __restrict__ cur, int b, int R, int ns,
+                                         const StencilTaps& tp, double (&v)[P + 2 * S]) {
+    constexpr int L = P + 2 * S;
+#pragma unroll
+    for (int u = 0; u < L; ++u) {
+        int j = b - S + u;
+        j = j < 0 ? 0 : (j >= R ? R - 1 : j);
+        v[u] = cur[(j % P) * ns + j / P];
+    }
+    double o[P];
+#pragma unroll
+    for (int p = 0; p < P; ++p) {
+        double acc = tp.t[0] * v[p];
+#pragma unroll
+        for (int k = 1; k <= 2 * S; ++k) acc = fma(tp.t[k], v[p + k], acc);
+        o[p] = acc;
+    }
+#pragma unroll
+    for (int p = 0; p < P; ++p) v[S + p] = o[p];
+}
+
 // SMEM rows of the blocked tiles are point-major with a padded stride ns = nt + 2: region
 // point e lives at (e % P) * ns + e / P.  Per-thread gathers (blk_advance) and the owner's
 // P results then hit 32 consecutive slots per warp (conflict-free), and the coalesced
@@ -467,7 +492,7 @@ __device__ __forceinline__ void cp8(double* dst, const double* src) {
 // trajectory, observations -- stores coalesced instead of stride-P per thread), (b) the
 // next interval's forcing row issued by cp.async into a double buffer (lands while the S
 // sub-steps compute), (c) the register-blocked advance.
-template <int KIND, int S, int SB, int P>
+template <int KIND, int S, int P>
 __global__ void __launch_bounds__(512) tiled_blk_fwd_kernel(const TiledArgs ta, unsigned* status) {
     extern __shared__ double sm[];
     const ModelDev& md = ta.md;
@@ -493,7 +518,7 @@ __global__ void __launch_bounds__(512) tiled_blk_fwd_kernel(const TiledArgs ta, 
     const int np = net.n_points;
     const int b = tid * P;
     bool bad = false;
-    double v[P + 2 * SB];
+    double v[P + 2 * S];
     auto slot = [&](int e) { return (e % P) * ns + e / P; };
     auto load_row = [&](double* dst, const double* row) {
         for (int e = tid; e < R; e += nt) cp8(dst + slot(e), row + rg.gidx(e));
@@ -526,33 +551,28 @@ __global__ void __launch_bounds__(512) tiled_blk_fwd_kernel(const TiledArgs ta, 
         if (i == ta.i1) break;
         const int k = i - ta.i0;
         if (i + 2 <= ta.i1) load_row((k & 1) ? fx0 : fx1, X + (int64_t)(i + 2) * n);
-        // S sub-steps in S / SB register blocks of SB sub-steps (one barrier between blocks)
-        for (int blk = 0; blk < S / SB; ++blk) {
-            const bool last = blk + 1 == S / SB;
-            if (blk > 0) __syncthreads();
-            lo += SB;
-            hi -= SB;
-            if (b + P > lo && b < hi) {
-                blk_advance<KIND, SB, P, false>(cur, b, R, ns, md.c, md.d, v);
-                const double* f = (k & 1) ? fx1 : fx0;
+        lo += S;
+        hi -= S;
+        if (b + P > lo && b < hi) {
+            blk_conv<S, P>(cur, b, R, ns, ta.tp, v);  // M_i = the S-step TL as one stencil
+            const double* f = (k & 1) ? fx1 : fx0;
 #pragma unroll
-                for (int p = 0; p < P; ++p) {
-                    const int e = b + p;
-                    if (e >= lo && e < hi)  // x_{i+1} = M_i x_i + X_{i+1}  (operators.cpp:88)
-                        nxt[p * ns + tid] = last ? v[SB + p] + f[p * ns + tid] : v[SB + p];
-                }
+            for (int p = 0; p < P; ++p) {
+                const int e = b + p;
+                if (e >= lo && e < hi)  // x_{i+1} = M_i x_i + X_{i+1}  (operators.cpp:88)
+                    nxt[p * ns + tid] = v[S + p] + f[p * ns + tid];
             }
-            double* t = cur;
-            cur = nxt;
-            nxt = t;
         }
+        double* t = cur;
+        cur = nxt;
+        nxt = t;
     }
     if (ta.bout)
         for (int e = c_lo + tid; e < c_hi; e += nt) ta.bout[col * n + rg.gidx(e)] = cur[slot(e)];
     if (__syncthreads_or(bad) && tid == 0) atomicOr(status, ST_FWD_NONFINITE);
 }
 
-template <int KIND, int S, int SB, int P>
+template <int KIND, int S, int P>
 __global__ void __launch_bounds__(512) tiled_blk_adj_kernel(const TiledArgs ta, unsigned* status) {
     extern __shared__ double sm[];
     const ModelDev& md = ta.md;
@@ -578,7 +598,7 @@ __global__ void __launch_bounds__(512) tiled_blk_adj_kernel(const TiledArgs ta, 
     const int np = net.n_points;
     const int b = tid * P;
     bool bad = false;
-    double v[P + 2 * SB];
+    double v[P + 2 * S];
     auto slot = [&](int e) { return (e % P) * ns + e / P; };
     auto load_row = [&](double* dst, const double* row) {
         for (int e = tid; e < R; e += nt) cp8(dst + slot(e), row + rg.gidx(e));
@@ -619,41 +639,33 @@ __global__ void __launch_bounds__(512) tiled_blk_adj_kernel(const TiledArgs ta, 
         if (i == ta.i0) break;
         const int k = ta.i1 - i;
         if (V && i - 2 >= ta.i0) load_row((k & 1) ? vb0 : vb1, V + (int64_t)(i - 2) * n);
-        for (int blk = 0; blk < S / SB; ++blk) {  // S / SB register blocks (see fwd)
-            const bool last = blk + 1 == S / SB;
-            if (blk > 0) __syncthreads();
-            lo += SB;
-            hi -= SB;
-            if (b + P > lo && b < hi) {
-                blk_advance<KIND, SB, P, true>(cur, b, R, ns, md.c, md.d, v);
-                const double* vr = (k & 1) ? vb1 : vb0;
+        lo += S;
+        hi -= S;
+        if (b + P > lo && b < hi) {
+            blk_conv<S, P>(cur, b, R, ns, ta.tp, v);  // M_i^T as one stencil
+            const double* vr = (k & 1) ? vb1 : vb0;
 #pragma unroll
-                for (int p = 0; p < P; ++p) {
-                    const int e = b + p;
-                    if (e >= lo && e < hi) {
-                        if (last) {
-                            // s_{i-1} = v_{i-1} + H^T y + M^T s_i  (operators.cpp:99)
-                            const double ad = obs_add(i - 1, rg.gidx(e), V ? vr[p * ns + tid] : 0.0);
-                            nxt[p * ns + tid] = ad + v[SB + p];
-                        } else {
-                            nxt[p * ns + tid] = v[SB + p];
-                        }
-                    }
+            for (int p = 0; p < P; ++p) {
+                const int e = b + p;
+                if (e >= lo && e < hi) {
+                    // s_{i-1} = v_{i-1} + H^T y + M^T s_i  (operators.cpp:99)
+                    const double ad = obs_add(i - 1, rg.gidx(e), V ? vr[p * ns + tid] : 0.0);
+                    nxt[p * ns + tid] = ad + v[S + p];
                 }
             }
-            double* t = cur;
-            cur = nxt;
-            nxt = t;
         }
+        double* t = cur;
+        cur = nxt;
+        nxt = t;
     }
     if (ta.bout)
         for (int e = c_lo + tid; e < c_hi; e += nt) ta.bout[col * n + rg.gidx(e)] = cur[slot(e)];
     if (__syncthreads_or(bad) && tid == 0) atomicOr(status, ST_ADJ_NONFINITE);
 }
 
-// Register-blocked tiled launch (radius-1 models, S in {1,5,10}, SB sub-steps per register
-// block); false if not applicable.
-template <int KIND, int S, int SB>
+// Register-blocked tiled launch (radius-1 models, S in {1,5,10}, one fused S-step stencil
+// per interval); false if not applicable.
+template <int KIND, int S>
 bool launch_tiled_blk(const ModelDev& md, const NetDev& net, const SweepArgs& a, unsigned* status,
                       cudaStream_t st, DevBuf& ws, int tile_override) {
     constexpr int P = 8;
@@ -673,8 +685,8 @@ bool launch_tiled_blk(const ModelDev& md, const NetDev& net, const SweepArgs& a,
     if (nt > 512 || T <= 0 || R > md.n) return false;
     TileGeom geo{T, K * S, K * S, R, false, cdiv(md.n, T)};
     const size_t smem = sizeof(double) * 4 * (size_t)P * (nt + 2);  // cur, nxt, 2 prefetch rows
-    auto fk = tiled_blk_fwd_kernel<KIND, S, SB, P>;
-    auto ak = tiled_blk_adj_kernel<KIND, S, SB, P>;
+    auto fk = tiled_blk_fwd_kernel<KIND, S, P>;
+    auto ak = tiled_blk_adj_kernel<KIND, S, P>;
     W4_CUDA(cudaFuncSetAttribute(fk, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     W4_CUDA(cudaFuncSetAttribute(ak, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     const int nl = (int)cdiv(md.N, K);
@@ -687,6 +699,7 @@ bool launch_tiled_blk(const ModelDev& md, const NetDev& net, const SweepArgs& a,
             ta.i1 = std::min(md.N, (l + 1) * K);
             ta.bin = l == 0 ? nullptr : bbuf + (size_t)((l + 1) % 2) * md.n * a.m;
             ta.bout = l + 1 < nl ? bbuf + (size_t)(l % 2) * md.n * a.m : nullptr;
+            ta.tp = stencil_power(KIND, md.c, md.d, S, false);
             fk<<<grid, nt, smem, st>>>(ta, status);
             W4_LAUNCH();
         }
@@ -696,6 +709,7 @@ bool launch_tiled_blk(const ModelDev& md, const NetDev& net, const SweepArgs& a,
             ta.i0 = std::max(0, md.N - (l + 1) * K);
             ta.bin = l == 0 ? nullptr : bbuf + (size_t)((l + 1) % 2) * md.n * a.m;
             ta.bout = l + 1 < nl ? bbuf + (size_t)(l % 2) * md.n * a.m : nullptr;
+            ta.tp = stencil_power(KIND, md.c, md.d, S, true);
             ak<<<grid, nt, smem, st>>>(ta, status);
             W4_LAUNCH();
         }
@@ -1195,23 +1209,11 @@ void launch_tiled(const ModelDev& md, const NetDev& net, const SweepArgs& a, uns
         geo.ntiles = 1;
     } else {
         if (KIND != WC4DVAR_MODEL_LORENZ96) {
-            // WC4DVAR_SWEEP_SB: sub-steps per register block (default 5; s=10 also 2 / 10)
-            static const int sb = [] {
-                const char* e = std::getenv("WC4DVAR_SWEEP_SB");
-                return e ? std::atoi(e) : 5;
-            }();
             bool done = false;
             switch (md.s) {
-                case 1: done = launch_tiled_blk<KIND, 1, 1>(md, net, a, status, st, ws, tile_override); break;
-                case 5:
-                    done = sb == 1 ? launch_tiled_blk<KIND, 5, 1>(md, net, a, status, st, ws, tile_override)
-                                   : launch_tiled_blk<KIND, 5, 5>(md, net, a, status, st, ws, tile_override);
-                    break;
-                case 10:
-                    done = sb == 2    ? launch_tiled_blk<KIND, 10, 2>(md, net, a, status, st, ws, tile_override)
-                           : sb == 10 ? launch_tiled_blk<KIND, 10, 10>(md, net, a, status, st, ws, tile_override)
-                                      : launch_tiled_blk<KIND, 10, 5>(md, net, a, status, st, ws, tile_override);
-                    break;
+                case 1: done = launch_tiled_blk<KIND, 1>(md, net, a, status, st, ws, tile_override); break;
+                case 5: done = launch_tiled_blk<KIND, 5>(md, net, a, status, st, ws, tile_override); break;
+                case 10: done = launch_tiled_blk<KIND, 10>(md, net, a, status, st, ws, tile_override); break;
                 default: break;
             }
             if (done) return;

@@ -22,7 +22,7 @@ from gpu_helpers import factor, oracle_model, pair, relerr  # noqa: E402
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 
-@pytest.mark.parametrize("tile", ["0", "64", "37", "l96cb1", "l96cb4", "l96cb8", "l96cb16", "sb2", "sb10"])
+@pytest.mark.parametrize("tile", ["0", "64", "37", "l96cb1", "l96cb4", "l96cb8", "l96cb16"])
 def test_tiled_sweeps_vs_oracle(tile):
     """l96cbX: the register-blocked Lorenz-96 kernels (X columns per CTA) forced on every
     domain at least one region wide."""
@@ -30,9 +30,6 @@ def test_tiled_sweeps_vs_oracle(tile):
     if tile.startswith("l96cb"):
         env["WC4DVAR_L96_BLK"] = "1"
         env["WC4DVAR_L96_CB"] = tile[5:]
-    elif tile.startswith("sb"):  # register-block depth of the stencil sweeps, small tiles
-        env["WC4DVAR_SWEEP_SB"] = tile[2:]
-        env["WC4DVAR_SWEEP_TILE"] = "64"
     elif tile != "0":
         env["WC4DVAR_SWEEP_TILE"] = tile
     p = subprocess.run([sys.executable, os.path.join(ROOT, "tools", "tiled_check.py")], env=env,
