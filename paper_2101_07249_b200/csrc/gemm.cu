@@ -770,6 +770,106 @@ void launch_sym_ws(const PassTable& tab, int64_t ntiles, unsigned* status, cudaS
 }
 
 // ---------------------------------------------------------------------------
+// Few-column symmetric GEMM: one warp per 16 x 8 output tile ("unit"), fragments loaded
+// straight from global/L2 into a D-deep register ring (no SMEM, no barriers).  With the
+// bitwise-order constraint every output element is one sequential chain over K, so the
+// only parallelism is across tiles; one warp per tile maximises it (PCG: n/16 x (N+1)/8
+// warps) and the prefetch ring keeps each chain fed.  Same fragment k-permutation and the
+// same two-phase m16n8k4 order as mma_k8.
+// ---------------------------------------------------------------------------
+template <int D>
+__global__ void __launch_bounds__(128) gemm_chain_kernel(const PassTable tab, unsigned* __restrict__ status) {
+    const int lane = threadIdx.x & 31;
+    const int64_t unit = (int64_t)blockIdx.x * 4 + (threadIdx.x >> 5);
+    if (unit >= tab.tile_start[2]) return;
+    const int pi = unit >= tab.tile_start[1] ? 1 : 0;
+    const GemmPass& P = tab.p[pi];
+    const int64_t u = unit - tab.tile_start[pi];
+    const int64_t m0 = (u % tab.tiles_m[pi]) * 16, n0 = (u / tab.tiles_m[pi]) * 8;
+    const int64_t M = P.M, K = P.K, ncols = P.ncols;
+    const int g = lane >> 2, t0 = lane & 3;
+    const int64_t r_lo = m0 + g, r_hi = m0 + g + 8, cb = n0 + g;
+    const bool ok_lo = r_lo < M, ok_hi = r_hi < M, ok_b = cb < ncols;
+    // symmetric A: row r of A is column r (contiguous in k)
+    const double* a_lo = P.A + (ok_lo ? r_lo : 0) * P.lda + 2 * t0;
+    const double* a_hi = P.A + (ok_hi ? r_hi : 0) * P.lda + 2 * t0;
+    const double* bp = (ok_b ? P.in.col(cb) : P.A) + 2 * t0;
+    const int KB = (int)(K / 8);  // full k8 blocks; a K tail is handled after the loop
+    // main loop: unconditional loads from clamped rows / columns, invalid lanes zeroed by
+    // a select (branch-free, so the ring of D loads really is in flight)
+    // running pointers advanced once per D-chunk; ring loads use constant offsets
+    const double2* pl = reinterpret_cast<const double2*>(a_lo);
+    const double2* ph = reinterpret_cast<const double2*>(a_hi);
+    const double2* pb = reinterpret_cast<const double2*>(bp);
+    auto load = [&](int kb, double2& al, double2& ah, double2& b) {  // kb relative to the pointers
+        al = __ldg(pl + 4 * kb);
+        ah = __ldg(ph + 4 * kb);
+        b = __ldg(pb + 4 * kb);
+    };
+    auto fix = [&](double2& al, double2& ah, double2& b) {
+        if (!ok_lo) al = make_double2(0.0, 0.0);
+        if (!ok_hi) ah = make_double2(0.0, 0.0);
+        if (!ok_b) b = make_double2(0.0, 0.0);
+    };
+    double acc[4] = {0.0, 0.0, 0.0, 0.0};
+    double2 ra[D], rh[D], rb[D];
+#pragma unroll
+    for (int d = 0; d < D; ++d)
+        if (d < KB) load(d, ra[d], rh[d], rb[d]);
+    int kb = 0;
+    for (; kb + D <= KB; kb += D) {
+        const bool more = kb + 2 * D <= KB;  // whole next chunk in range: unpredicated loads
+#pragma unroll
+        for (int d = 0; d < D; ++d) {
+            double2 al = ra[d], ah = rh[d], b = rb[d];
+            if (more || kb + d + D < KB) load(d + D, ra[d], rh[d], rb[d]);
+            fix(al, ah, b);
+            dmma16x8x4(acc, al.x, ah.x, b.x);  // physical k = 2 t0
+            dmma16x8x4(acc, al.y, ah.y, b.y);  // physical k = 2 t0 + 1
+        }
+        pl += 4 * D;
+        ph += 4 * D;
+        pb += 4 * D;
+    }
+#pragma unroll
+    for (int d = 0; d < D; ++d) {  // remaining (< D) full blocks, already loaded
+        if (kb + d < KB) {
+            double2 al = ra[d], ah = rh[d], b = rb[d];
+            fix(al, ah, b);
+            dmma16x8x4(acc, al.x, ah.x, b.x);
+            dmma16x8x4(acc, al.y, ah.y, b.y);
+        }
+    }
+    if ((int64_t)KB * 8 < K) {  // K tail: zero-fill like the cp.async kernels
+        const int64_t k = (int64_t)KB * 8;
+        const bool v0 = k + 2 * t0 < K, v1 = k + 2 * t0 + 1 < K;
+        const double2 al = make_double2(ok_lo && v0 ? a_lo[k] : 0.0, ok_lo && v1 ? a_lo[k + 1] : 0.0);
+        const double2 ah = make_double2(ok_hi && v0 ? a_hi[k] : 0.0, ok_hi && v1 ? a_hi[k + 1] : 0.0);
+        const double2 b = make_double2(ok_b && v0 ? bp[k] : 0.0, ok_b && v1 ? bp[k + 1] : 0.0);
+        dmma16x8x4(acc, al.x, ah.x, b.x);
+        dmma16x8x4(acc, al.y, ah.y, b.y);
+    }
+    bool bad = false;
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+        const int64_t c = n0 + 2 * t0 + h;
+        if (c >= ncols) continue;
+        double* outc = const_cast<double*>(P.out.col(c));
+        const double* addc = P.add.base ? P.add.col(c) : nullptr;
+#pragma unroll
+        for (int v = 0; v < 2; ++v) {
+            const int64_t r = m0 + g + 8 * v;
+            if (r >= M) continue;
+            double val = P.alpha * acc[2 * v + h];
+            if (addc) val = addc[r] + val;
+            bad |= !isfinite(val);
+            outc[r] = val;
+        }
+    }
+    if (status && __any_sync(0xffffffffu, bad) && lane == 0) atomicOr(status, ST_OUT_NONFINITE);
+}
+
+// ---------------------------------------------------------------------------
 // TN split kernel: both tiles stored [col][k] (stride KPAD).
 // Partial (split s) of C tile -> work[s][m2][m1] col-major m1 x m2.
 // ---------------------------------------------------------------------------
@@ -962,6 +1062,37 @@ void gemm_nn(const GemmPass* passes, int npass, unsigned* status, cudaStream_t s
             if (ws_mode) launch_sym_ws<128, 128, 4, 4, 4>(tab, start, status, stream);
             else launch_sym<128, 128, 4, 4, 3>(tab, start, status, stream);
         }
+        return;
+    }
+    // Few columns (the single-vector applies of PCG: n x (N+1) columns): 64 x 32 tiles would
+    // leave most SMs idle, so run one warp per 16 x 8 output tile with register-prefetched
+    // fragments (gemm_chain_kernel).  Every shape accumulates each element in the same DMMA
+    // order, so the choice never changes a bit of the result.
+    static const int chain_mode = [] {
+        const char* e = std::getenv("WC4DVAR_GEMM_CHAIN");
+        return e ? std::atoi(e) : 1;
+    }();
+    if (sym && chain_mode > 0 && cdiv(maxM, 64) * cdiv(total_cols, 32) < kSMs) {
+        int64_t units = 0;
+        for (int i = 0; i < 2; ++i) {
+            tab.tile_start[i] = units;
+            if (i < npass && passes[i].ncols > 0 && passes[i].M > 0) {
+                tab.tiles_m[i] = cdiv(passes[i].M, 16);
+                units += tab.tiles_m[i] * cdiv(passes[i].ncols, 8);
+            } else {
+                tab.tiles_m[i] = 1;
+            }
+        }
+        tab.tile_start[2] = units;
+        if (units == 0) return;
+        const unsigned grid = (unsigned)cdiv(units, 4);
+        switch (chain_mode) {  // prefetch depth in k8 steps
+            case 4: gemm_chain_kernel<4><<<grid, 128, 0, stream>>>(tab, status); break;
+            case 6: gemm_chain_kernel<6><<<grid, 128, 0, stream>>>(tab, status); break;
+            case 8: gemm_chain_kernel<8><<<grid, 128, 0, stream>>>(tab, status); break;
+            default: gemm_chain_kernel<10><<<grid, 128, 0, stream>>>(tab, status); break;
+        }
+        W4_LAUNCH();
         return;
     }
     // Tile shape: big tiles when there are enough of them to fill the chip twice.
