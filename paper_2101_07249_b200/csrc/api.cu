@@ -1,6 +1,7 @@
 // C-ABI entry points (include/wc4dvar_gpu.h).
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <memory>
 #include <sstream>
@@ -214,6 +215,38 @@ int wc4dvar_gpu_op_apply_block(wc4dvar_op* op, const double* V, int64_t ldv, int
     cudaStream_t st = op->stream;
     double* din = op->in_buf.get<double>((size_t)op->dim * m);
     double* dout = op->out_buf.get<double>((size_t)op->dim * m);
+    // Copy/compute overlap for wide blocks: the columns go in `nch` chunks; chunk c+1's
+    // host->device copy and chunk c-1's device->host copy run on their own streams while
+    // chunk c computes.  Each column's arithmetic is unchanged (bitwise).
+    // WC4DVAR_PIPELINE_CHUNKS (default 2; 1 = off), engaged for m >= 32.
+    static const int chunks_env = [] {
+        const char* e = std::getenv("WC4DVAR_PIPELINE_CHUNKS");
+        return e ? std::atoi(e) : 2;
+    }();
+    const int nch = (m >= 32 && !op->prof) ? std::max(1, std::min(chunks_env, 4)) : 1;
+    if (nch > 1) {
+        op->ensure_pipeline();
+        op->reset_status(st);
+        int64_t cb[5];
+        for (int c = 0; c <= nch; ++c) cb[c] = m * c / nch;
+        for (int c = 0; c < nch; ++c) {
+            h2d_block(din + cb[c] * op->dim, V + cb[c] * ldv, op->dim, cb[c + 1] - cb[c], ldv, op->pipe_in);
+            W4_CUDA(cudaEventRecord(op->pipe_ev[c], op->pipe_in));
+        }
+        for (int c = 0; c < nch; ++c) {
+            W4_CUDA(cudaStreamWaitEvent(st, op->pipe_ev[c], 0));
+            op->apply_block_dev(din + cb[c] * op->dim, op->dim, cb[c + 1] - cb[c], dout + cb[c] * op->dim,
+                                op->dim, st);
+            W4_CUDA(cudaEventRecord(op->pipe_ev[4 + c], st));
+        }
+        for (int c = 0; c < nch; ++c) {
+            W4_CUDA(cudaStreamWaitEvent(op->pipe_out, op->pipe_ev[4 + c], 0));
+            d2h_block(out + cb[c] * ldo, ldo, dout + cb[c] * op->dim, op->dim, cb[c + 1] - cb[c], op->pipe_out);
+        }
+        W4_CUDA(cudaStreamSynchronize(op->pipe_out));
+        op->check_status(st);
+        return WC4DVAR_OK;
+    }
     h2d_block(din, V, op->dim, m, ldv, st);
     op->reset_status(st);
     op->apply_block_dev(din, op->dim, m, dout, op->dim, st);

@@ -1042,7 +1042,9 @@ void gemm_nn(const GemmPass* passes, int npass, unsigned* status, cudaStream_t s
     for (int i = npass; i < 2; ++i) tab.p[i] = GemmPass{};
     bool sym = vec2;
     for (int i = 0; i < npass; ++i) sym = sym && passes[i].symA && passes[i].M == passes[i].K;
-    if (sym && cdiv(maxM, 128) * cdiv(total_cols, 128) >= kSMs) {
+    int64_t ws_tiles = 0;  // 128 x 128 tiles of the warp-specialised kernel, per pass
+    for (int i = 0; i < npass; ++i) ws_tiles += cdiv(passes[i].M, 128) * cdiv(passes[i].ncols, 128);
+    if (sym && 2 * ws_tiles >= kSMs) {
         int64_t start = 0;
         for (int i = 0; i < 2; ++i) {
             tab.tile_start[i] = start;

@@ -26,6 +26,10 @@ wc4dvar_op::~wc4dvar_op() {
     DeviceGuard g(device);
     for (cudaEvent_t e : pev)
         if (e) cudaEventDestroy(e);
+    for (cudaEvent_t e : pipe_ev)
+        if (e) cudaEventDestroy(e);
+    if (pipe_in) cudaStreamDestroy(pipe_in);
+    if (pipe_out) cudaStreamDestroy(pipe_out);
     if (h_int) cudaFreeHost(h_int);
     if (d_status) cudaFree(d_status);
     if (h_status) cudaFreeHost(h_status);
@@ -40,6 +44,13 @@ void wc4dvar_op::init_common(int dev, int64_t n) {
     W4_CUDA(cudaMallocHost(&h_status, sizeof(unsigned)));
     W4_CUDA(cudaMallocHost(&h_int, 16 * sizeof(int)));
     W4_CUDA(cudaMemset(d_status, 0, sizeof(unsigned)));
+}
+
+void wc4dvar_op::ensure_pipeline() {
+    if (pipe_in) return;
+    W4_CUDA(cudaStreamCreateWithFlags(&pipe_in, cudaStreamNonBlocking));
+    W4_CUDA(cudaStreamCreateWithFlags(&pipe_out, cudaStreamNonBlocking));
+    for (cudaEvent_t& e : pipe_ev) W4_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
 }
 
 void wc4dvar_op::collect_profile() {

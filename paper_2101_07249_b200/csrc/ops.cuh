@@ -35,6 +35,12 @@ struct wc4dvar_op {
     }
     void collect_profile();  // after a synchronising call
 
+    // Host-buffer block apply pipeline (api.cu): H2D of chunk c+1 and D2H of chunk c-1 run
+    // on their own streams while chunk c computes on `stream`.
+    cudaStream_t pipe_in = nullptr, pipe_out = nullptr;
+    cudaEvent_t pipe_ev[8] = {};
+    void ensure_pipeline();
+
     virtual ~wc4dvar_op();
     // Block apply on device pointers; does not count and does not synchronise.
     virtual void apply_block_dev(const double* V, int64_t ldv, int64_t m, double* out, int64_t ldo,
