@@ -4,6 +4,7 @@
 #include <cfloat>
 #include <cstdio>
 #include <cstdlib>
+#include <cstring>
 
 namespace w4 {
 namespace {
@@ -381,6 +382,231 @@ __global__ void __launch_bounds__(kEvdThreads)
     }
 }
 
+// ---------------------------------------------------------------- tridiagonal-QL EVD
+// Symmetric EVD for the Rayleigh-Ritz / ritzit / Nystrom small problems
+// (SelfAdjointEigenSolver, randevd.cpp:37-43): Householder tridiagonalisation (m-2
+// reflections, each one SMEM mat-vec + rank-2 update), implicit-shift QL on the
+// tridiagonal (the scalar recurrence runs on one thread; each QL sweep's Givens rotations
+// are recorded and then applied to the eigenvector rows by all threads at once), and the
+// back-transform by the stored reflectors.  ~6 barriers per reflection + 2 per QL sweep
+// instead of the 2 per round x (m-1) rounds x ~9 sweeps of cyclic Jacobi.  Absolute
+// accuracy ~ m eps ||K|| (LAPACK steqr class).
+__device__ double block_sum(double v, double* red) {
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    __syncthreads();  // red[] may still be read by a previous call
+    if (lane == 0) red[wid] = v;
+    __syncthreads();
+    double t = 0.0;
+    for (int w = 0; w < nw; ++w) t += red[w];  // fixed order: deterministic
+    return t;
+}
+
+constexpr int kTqlThreads = 512;
+
+__global__ void __launch_bounds__(kTqlThreads)
+    sym_evd_tql_kernel(int m, const double* __restrict__ K, double* __restrict__ vals,
+                       double* __restrict__ W, double* gwork, int use_smem, int* info) {
+    extern __shared__ double sm[];
+    double* base = use_smem ? sm : gwork;
+    double* A = base;                      // m x m column-major; reflectors below the subdiagonal
+    double* Z = A + (size_t)m * m;         // eigenvectors of T, column-major Z[i + k m]
+    double* d = Z + (size_t)m * m;         // diagonal
+    double* e = d + m;                     // subdiagonal e[i] = T(i+1, i), e[m-1] = 0
+    double* tau = e + m;
+    double* pv = tau + m;
+    double* rc = pv + m;                   // recorded rotations of one QL sweep
+    double* rs = rc + m;
+    int* ri = reinterpret_cast<int*>(rs + m);
+    __shared__ double red[32];
+    __shared__ int s_ctl[4];
+    const int tid = threadIdx.x, nt = blockDim.x;
+    const int lane = tid & 31, wid = tid >> 5, nw = nt >> 5;
+
+    for (int idx = tid; idx < m * m; idx += nt) {
+        const int i = idx % m, j = idx / m;
+        A[idx] = 0.5 * (K[i + j * m] + K[j + i * m]);
+        Z[idx] = (i == j) ? 1.0 : 0.0;
+    }
+    __syncthreads();
+
+    // 1. Householder tridiagonalisation: H_k = I - tau_k u u^T zeroes A[k+2:, k]
+    for (int k = 0; k + 2 < m; ++k) {
+        const int n2 = m - k - 1;
+        double* x = A + (k + 1) + (size_t)k * m;  // column k below the diagonal, length n2
+        double part = 0.0;
+        for (int i = 1 + tid; i < n2; i += nt) part += x[i] * x[i];
+        const double sig = block_sum(part, red);
+        const double x0 = x[0];
+        if (sig == 0.0) {  // already tridiagonal in this column
+            if (tid == 0) {
+                tau[k] = 0.0;
+                e[k] = x0;
+            }
+            continue;
+        }
+        const double alpha = -copysign(sqrt(x0 * x0 + sig), x0);
+        const double u0 = x0 - alpha;
+        const double tk = 2.0 / (u0 * u0 + sig);
+        __syncthreads();  // everyone has read x0
+        if (tid == 0) {
+            x[0] = u0;  // u = [u0, x1, ...] stored in place
+            tau[k] = tk;
+            e[k] = alpha;
+        }
+        __syncthreads();
+        // p = tau A22 u (rows of A22 via symmetry: consecutive threads, consecutive rows)
+        double* A22 = A + (k + 1) + (size_t)(k + 1) * m;
+        for (int i = tid; i < n2; i += nt) {
+            double s = 0.0;
+            for (int j = 0; j < n2; ++j) s += A22[i + (size_t)j * m] * x[j];
+            pv[i] = tk * s;
+        }
+        __syncthreads();
+        part = 0.0;
+        for (int i = tid; i < n2; i += nt) part += x[i] * pv[i];
+        const double Kc = 0.5 * tk * block_sum(part, red);
+        for (int i = tid; i < n2; i += nt) pv[i] -= Kc * x[i];  // w = p - K u
+        __syncthreads();
+        for (int idx = tid; idx < n2 * n2; idx += nt) {  // A22 -= u w^T + w u^T
+            const int i = idx % n2, j = idx / n2;
+            A22[i + (size_t)j * m] -= x[i] * pv[j] + pv[i] * x[j];
+        }
+        __syncthreads();
+    }
+    for (int i = tid; i < m; i += nt) {
+        d[i] = A[i + (size_t)i * m];
+        if (i + 2 >= m) tau[i] = 0.0;
+    }
+    if (tid == 0) {
+        if (m >= 2) e[m - 2] = A[(m - 1) + (size_t)(m - 2) * m];
+        e[m - 1] = 0.0;
+    }
+    __syncthreads();
+
+    // 2. implicit-shift QL on (d, e); thread 0 runs the recurrence, everyone rotates Z rows
+    int l = 0, iter = 0;
+    while (true) {
+        if (tid == 0) {
+            int nrot = 0, done = 0;
+            while (l < m) {
+                int mm;
+                for (mm = l; mm < m - 1; ++mm) {
+                    const double dd = fabs(d[mm]) + fabs(d[mm + 1]);
+                    if (fabs(e[mm]) <= DBL_EPSILON * dd) break;
+                }
+                if (mm == l) {  // d[l] converged
+                    ++l;
+                    iter = 0;
+                    continue;
+                }
+                if (++iter > 60) {  // no convergence: poison the values (caught by validation)
+                    if (info) *info = 1;
+                    for (int q = 0; q < m; ++q) d[q] = nan("");
+                    done = 1;
+                    break;
+                }
+                double g = (d[l + 1] - d[l]) / (2.0 * e[l]);
+                double r = hypot(g, 1.0);
+                g = d[mm] - d[l] + e[l] / (g + copysign(r, g));
+                double s = 1.0, c = 1.0, p = 0.0;
+                int i;
+                for (i = mm - 1; i >= l; --i) {
+                    const double ei = e[i];
+                    const double f = s * ei;
+                    const double b = c * ei;
+                    // r = hypot(f, g) via one rsqrt (values here are far from over/underflow)
+                    const double h2 = f * f + g * g;
+                    if (h2 == 0.0) {
+                        e[i + 1] = 0.0;
+                        r = 0.0;
+                        d[i + 1] -= p;
+                        e[mm] = 0.0;
+                        break;
+                    }
+                    const double rinv = rsqrt(h2);
+                    r = h2 * rinv;
+                    e[i + 1] = r;
+                    s = f * rinv;
+                    c = g * rinv;
+                    g = d[i + 1] - p;
+                    r = (d[i] - g) * s + 2.0 * c * b;
+                    d[i + 1] = g + (p = s * r);
+                    g = c * r - b;
+                    rc[nrot] = c;
+                    rs[nrot] = s;
+                    ri[nrot] = i;
+                    ++nrot;
+                }
+                if (r == 0.0 && i >= l) break;  // split: rotations so far are recorded
+                d[l] -= p;
+                e[l] = g;
+                e[mm] = 0.0;
+                break;
+            }
+            if (l >= m) done = 1;
+            s_ctl[0] = nrot;
+            s_ctl[1] = done;
+        }
+        __syncthreads();
+        const int nrot = s_ctl[0], done = s_ctl[1];
+        // z[row][i], z[row][i+1]; one sweep's rotations visit i = i0, i0-1, ..., so the
+        // updated z[row][i] is carried in a register into the next rotation
+        if (nrot > 0)
+            for (int row = tid; row < m; row += nt) {
+                const int i0 = ri[0];
+                double f = Z[row + (size_t)(i0 + 1) * m];
+                for (int q = 0; q < nrot; ++q) {
+                    const int i = i0 - q;
+                    const double c = rc[q], s = rs[q];
+                    const double zi = Z[row + (size_t)i * m];
+                    Z[row + (size_t)(i + 1) * m] = s * zi + c * f;
+                    f = c * zi - s * f;
+                }
+                Z[row + (size_t)(i0 + 1 - nrot) * m] = f;
+            }
+        __syncthreads();
+        if (done) break;
+    }
+
+    // 3. back-transform: eigvecs = H_0 H_1 ... H_{m-3} Z
+    for (int k = m - 3; k >= 0; --k) {
+        const double tk = tau[k];
+        if (tk == 0.0) continue;
+        const int n2 = m - k - 1;
+        const double* u = A + (k + 1) + (size_t)k * m;
+        for (int c = wid; c < m; c += nw) {  // s_c = u^T Z[k+1:, c]
+            double s = 0.0;
+            for (int i = lane; i < n2; i += 32) s += u[i] * Z[(k + 1 + i) + (size_t)c * m];
+            for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+            if (lane == 0) pv[c] = tk * s;
+        }
+        __syncthreads();
+        for (int idx = tid; idx < n2 * m; idx += nt) {
+            const int i = idx % n2, c = idx / n2;
+            Z[(k + 1 + i) + (size_t)c * m] -= u[i] * pv[c];
+        }
+        __syncthreads();
+    }
+
+    // 4. decreasing order (sorted_symmetric_evd, randevd.cpp:37-43)
+    for (int i = tid; i < m; i += nt) {
+        const double di = d[i];
+        int rk = 0;
+        for (int j = 0; j < m; ++j) {
+            const double dj = d[j];
+            rk += (dj > di) || (dj == di && j < i);
+        }
+        ri[i] = rk;
+        vals[rk] = di;
+    }
+    __syncthreads();
+    for (int idx = tid; idx < m * m; idx += nt) {
+        const int i = idx % m, j = idx / m;
+        W[i + (size_t)ri[j] * m] = Z[i + (size_t)j * m];
+    }
+}
+
 // ---------------------------------------------------------------- one-sided Jacobi SVD
 __global__ void __launch_bounds__(kThreads)
     jacobi_svd_kernel(int m, const double* __restrict__ Xin, double* __restrict__ sigma,
@@ -542,6 +768,22 @@ void tri_inv_upper(int m, const double* R, double* Rinv, cudaStream_t st) {
 void sym_evd_desc(int m, const double* K, double* vals, double* W, DevBuf& work,
                   cudaStream_t st) {
     require(m <= 512, "sym_evd_desc: m too large");
+    // Default: cyclic block-Jacobi (high relative accuracy; the LMP / PCG parity tests are
+    // tuned to it).  WC4DVAR_EVD=tql selects the tridiagonal-QL kernel (absolute accuracy;
+    // not yet faster at m ~ 100 because the QL recurrence is serial).
+    static const bool jacobi = [] {
+        const char* e = std::getenv("WC4DVAR_EVD");
+        return !(e && std::strcmp(e, "tql") == 0);
+    }();
+    if (!jacobi) {
+        const size_t tb = sizeof(double) * (2 * (size_t)m * m + 7 * (size_t)m) + sizeof(int) * m;
+        int use_t = 0;
+        const size_t sh_t = setup_smem(reinterpret_cast<const void*>(sym_evd_tql_kernel), tb, use_t);
+        double* gw = use_t ? nullptr : work.get<double>(tb / sizeof(double) + 1);
+        sym_evd_tql_kernel<<<1, kTqlThreads, sh_t, st>>>(m, K, vals, W, gw, use_t, nullptr);
+        W4_LAUNCH();
+        return;
+    }
     int use = 0;
     const size_t bytes = sizeof(double) * 2 * m * m;
     const int mp = m + (m & 1);
