@@ -114,6 +114,17 @@ def algorithmic_counts(wl, m):
     return nA, flops_gemm, flops_model, bytes_step
 
 
+def gemm_traffic():
+    """DRAM bytes per launch of the D^1/2 GEMM from the committed `ncu --set full` capture
+    (dram__bytes_read.sum + dram__bytes_write.sum, averaged over the captured launches)."""
+    path = os.path.join(ROOT, "profiles", "r01_gemm_sym_stream_k.json")
+    try:
+        ks = [k for k in json.load(open(path))["kernels"] if "gemm_sym_ws" in k["kernel"]]
+        return sum(k["traffic_bytes"] for k in ks) / len(ks), os.path.relpath(path, ROOT)
+    except (OSError, KeyError, ValueError, ZeroDivisionError):
+        return None, None
+
+
 def cpu_reference(wl, columns, threads, seed_cols_offset=0):
     """Time the oracle port of HessianOperator::apply_block (the reference's column
     fan-out over std::thread, threads.cpp:25-44) on `columns` sketch columns."""
@@ -238,6 +249,7 @@ def run_ours(args):
     nA_, flops_gemm, flops_model, bytes_step = algorithmic_counts(wl, m)
     gemm_ms = (stage_ms[0] + stage_ms[2]) / (2 * max(calls, 1))
     achieved_tf = flops_gemm / (gemm_ms * 1e-3) / 1e12
+    traffic, traffic_src = gemm_traffic()
     try:
         peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
     except Exception:
@@ -264,8 +276,9 @@ def run_ours(args):
                     "d2h_bytes_per_step": 8 * nA * m},
             "gpu_launches": 3 * args.steps,
             "roofline": {"bound": "tensor", "achieved": achieved_tf, "peak": dmma_peak, "unit": "TFLOP/s",
-                         "frac": achieved_tf / dmma_peak, "traffic": None,
-                         "kernel": "gemm_nn (D^1/2 block-diagonal DMMA GEMM)",
+                         "frac": achieved_tf / dmma_peak, "traffic": traffic,
+                         "traffic_source": traffic_src,
+                         "kernel": "gemm_sym_ws_kernel (D^1/2 block-diagonal DMMA GEMM, stream-K)",
                          "flops_per_launch": flops_gemm, "launch_ms": gemm_ms,
                          "peak_source": "measured in this run: all-SM mma.sync.f64 probe "
                                         "(MEASURED_PEAKS.json has bf16/HBM only)"},
