@@ -18,12 +18,17 @@ __device__ __forceinline__ double warp_sum(double v) {
     return v;
 }
 
+// The single-CTA kernels take their working matrix in SMEM when it fits, else in a global
+// work buffer.  SM is a template parameter so the SMEM variant compiles to LDS/STS instead
+// of generic loads (which cost extra latency on every access of these latency-bound loops).
+
 // ---------------------------------------------------------------- Cholesky
+template <bool SM>
 __global__ void __launch_bounds__(kThreads)
     chol_kernel(int m, const double* __restrict__ G, double* __restrict__ R, int* info,
                 double* gwork, int use_smem) {
     extern __shared__ double sm[];
-    double* A = use_smem ? sm : gwork;
+    double* A = SM ? sm : gwork;
     __shared__ int fail;
     const int tid = threadIdx.x, nt = blockDim.x;
     for (int e = tid; e < m * m; e += nt) {
@@ -60,11 +65,12 @@ __global__ void __launch_bounds__(kThreads)
 }
 
 // ---------------------------------------------------------------- pivoted Cholesky rank
+template <bool SM>
 __global__ void __launch_bounds__(kThreads)
     pchol_kernel(int m, const double* __restrict__ G, double tol_rel, int* rank, int* perm,
                  double* gwork, int use_smem) {
     extern __shared__ double sm[];
-    double* A = use_smem ? sm : gwork;
+    double* A = SM ? sm : gwork;
     __shared__ int piv, stop;
     __shared__ double maxd;
     const int tid = threadIdx.x, nt = blockDim.x;
@@ -192,11 +198,12 @@ __device__ __forceinline__ void rr_pair(int k, int r, int mp, int& p, int& q) {
 }
 
 // ---------------------------------------------------------------- two-sided Jacobi EVD
+template <bool SM>
 __global__ void __launch_bounds__(kThreads)
     jacobi_evd_kernel(int m, const double* __restrict__ K, double* __restrict__ vals,
                       double* __restrict__ W, double* gwork, int use_smem) {
     extern __shared__ double sm[];
-    double* A = use_smem ? sm : gwork;
+    double* A = SM ? sm : gwork;
     double* V = A + (size_t)m * m;
     __shared__ double cs_c[512], cs_s[512];
     __shared__ int cs_p[512], cs_q[512];
@@ -290,12 +297,13 @@ __global__ void __launch_bounds__(kThreads)
 // matrix is padded to even order with a zero row/column that no rotation ever touches.
 constexpr int kEvdThreads = 512;
 
+template <bool SM>
 __global__ void __launch_bounds__(kEvdThreads)
     jacobi_evd_blk_kernel(int m, const double* __restrict__ K, double* __restrict__ vals,
                           double* __restrict__ W, double* gwork, int use_smem, int debug) {
     extern __shared__ double sm[];
     const int mp = m + (m & 1);
-    double* A = use_smem ? sm : gwork;
+    double* A = SM ? sm : gwork;
     double* V = A + (size_t)mp * mp;
     __shared__ double cs_c[256], cs_s[256];
     __shared__ int cs_p[256], cs_q[256];
@@ -333,31 +341,73 @@ __global__ void __launch_bounds__(kEvdThreads)
                 cs_q[k] = q;
             }
             __syncthreads();
-            const int wid = tid >> 5, lane = tid & 31, nw = nt >> 5;
-            for (int Q = wid; Q < npairs; Q += nw)
-            for (int P = lane; P < npairs; P += 32) {
-                const double sP = cs_s[P], sQ = cs_s[Q];
-                if (sP == 0.0 && sQ == 0.0) continue;
-                const double cP = cs_c[P], cQ = cs_c[Q];
-                const int p1 = cs_p[P], p2 = cs_q[P], q1 = cs_p[Q], q2 = cs_q[Q];
-                const double a11 = A[p1 + q1 * mp], a12 = A[p1 + q2 * mp];
-                const double a21 = A[p2 + q1 * mp], a22 = A[p2 + q2 * mp];
-                const double b11 = cQ * a11 - sQ * a12, b12 = sQ * a11 + cQ * a12;
-                const double b21 = cQ * a21 - sQ * a22, b22 = sQ * a21 + cQ * a22;
-                A[p1 + q1 * mp] = cP * b11 - sP * b21;
-                A[p2 + q1 * mp] = sP * b11 + cP * b21;
-                A[p1 + q2 * mp] = cP * b12 - sP * b22;
-                A[p2 + q2 * mp] = sP * b12 + cP * b22;
+            // 2x2 block updates A <- J_P^T A J_Q for all pair blocks (P, Q) and V <- V J_Q.
+            // Items are processed in batches of JB per thread with all loads issued before
+            // any store: the blocks are disjoint, and the explicit batching removes the
+            // store->load ordering the compiler would otherwise keep between items.  A pair
+            // with (c, s) = (1, 0) leaves its entries bit-identical, so no skip is needed.
+            constexpr int JB = 4;
+            const int nblk = npairs * npairs;
+            for (int b0 = tid; b0 < nblk; b0 += JB * nt) {
+                int o11[JB], o12[JB], o21[JB], o22[JB];
+                double cP[JB], sP[JB], cQ[JB], sQ[JB], a11[JB], a12[JB], a21[JB], a22[JB];
+#pragma unroll
+                for (int u = 0; u < JB; ++u) {
+                    const int bi = b0 + u * nt < nblk ? b0 + u * nt : 0;  // tail slots: load only
+                    const int P = bi % npairs, Q = bi / npairs;
+                    const int p1 = cs_p[P], p2 = cs_q[P], q1 = cs_p[Q], q2 = cs_q[Q];
+                    cP[u] = cs_c[P];
+                    sP[u] = cs_s[P];
+                    cQ[u] = cs_c[Q];
+                    sQ[u] = cs_s[Q];
+                    o11[u] = p1 + q1 * mp;
+                    o12[u] = p1 + q2 * mp;
+                    o21[u] = p2 + q1 * mp;
+                    o22[u] = p2 + q2 * mp;
+                    a11[u] = A[o11[u]];
+                    a12[u] = A[o12[u]];
+                    a21[u] = A[o21[u]];
+                    a22[u] = A[o22[u]];
+                }
+#pragma unroll
+                for (int u = 0; u < JB; ++u) {
+                    const double b11 = cQ[u] * a11[u] - sQ[u] * a12[u], b12 = sQ[u] * a11[u] + cQ[u] * a12[u];
+                    const double b21 = cQ[u] * a21[u] - sQ[u] * a22[u], b22 = sQ[u] * a21[u] + cQ[u] * a22[u];
+                    a11[u] = cP[u] * b11 - sP[u] * b21;
+                    a21[u] = sP[u] * b11 + cP[u] * b21;
+                    a12[u] = cP[u] * b12 - sP[u] * b22;
+                    a22[u] = sP[u] * b12 + cP[u] * b22;
+                }
+#pragma unroll
+                for (int u = 0; u < JB; ++u) {
+                    if (b0 + u * nt >= nblk) continue;
+                    A[o11[u]] = a11[u];
+                    A[o21[u]] = a21[u];
+                    A[o12[u]] = a12[u];
+                    A[o22[u]] = a22[u];
+                }
             }
-            for (int Q = wid; Q < npairs; Q += nw)
-            for (int i = lane; i < mp; i += 32) {
-                const double sQ = cs_s[Q];
-                if (sQ == 0.0) continue;
-                const double cQ = cs_c[Q];
-                const int q1 = cs_p[Q], q2 = cs_q[Q];
-                const double v1 = V[i + q1 * mp], v2 = V[i + q2 * mp];
-                V[i + q1 * mp] = cQ * v1 - sQ * v2;
-                V[i + q2 * mp] = sQ * v1 + cQ * v2;
+            const int nv = npairs * mp;
+            for (int v0 = tid; v0 < nv; v0 += JB * nt) {
+                int o1[JB], o2[JB];
+                double c[JB], s[JB], v1[JB], v2[JB];
+#pragma unroll
+                for (int u = 0; u < JB; ++u) {
+                    const int vi = v0 + u * nt < nv ? v0 + u * nt : 0;
+                    const int Q = vi / mp, i = vi - Q * mp;
+                    c[u] = cs_c[Q];
+                    s[u] = cs_s[Q];
+                    o1[u] = i + cs_p[Q] * mp;
+                    o2[u] = i + cs_q[Q] * mp;
+                    v1[u] = V[o1[u]];
+                    v2[u] = V[o2[u]];
+                }
+#pragma unroll
+                for (int u = 0; u < JB; ++u) {
+                    if (v0 + u * nt >= nv) continue;
+                    V[o1[u]] = c[u] * v1[u] - s[u] * v2[u];
+                    V[o2[u]] = s[u] * v1[u] + c[u] * v2[u];
+                }
             }
             __syncthreads();
         }
@@ -404,11 +454,12 @@ __device__ double block_sum(double v, double* red) {
 
 constexpr int kTqlThreads = 512;
 
+template <bool SM>
 __global__ void __launch_bounds__(kTqlThreads)
     sym_evd_tql_kernel(int m, const double* __restrict__ K, double* __restrict__ vals,
                        double* __restrict__ W, double* gwork, int use_smem, int* info) {
     extern __shared__ double sm[];
-    double* base = use_smem ? sm : gwork;
+    double* base = SM ? sm : gwork;
     double* A = base;                      // m x m column-major; reflectors below the subdiagonal
     double* Z = A + (size_t)m * m;         // eigenvectors of T, column-major Z[i + k m]
     double* d = Z + (size_t)m * m;         // diagonal
@@ -608,11 +659,12 @@ __global__ void __launch_bounds__(kTqlThreads)
 }
 
 // ---------------------------------------------------------------- one-sided Jacobi SVD
+template <bool SM>
 __global__ void __launch_bounds__(kThreads)
     jacobi_svd_kernel(int m, const double* __restrict__ Xin, double* __restrict__ sigma,
                       double* __restrict__ U, double* gwork, int use_smem) {
     extern __shared__ double sm[];
-    double* X = use_smem ? sm : gwork;
+    double* X = SM ? sm : gwork;
     __shared__ double cs_c[512], cs_s[512];
     __shared__ int cs_p[512], cs_q[512];
     __shared__ double nrm[512];
@@ -733,9 +785,9 @@ size_t setup_smem(const void* kern, size_t bytes, int& use_smem) {
 void chol_upper(int m, const double* G, double* R, int* info, DevBuf& work, cudaStream_t st) {
     int use = 0;
     const size_t bytes = sizeof(double) * m * m;
-    const size_t sh = setup_smem(reinterpret_cast<const void*>(chol_kernel), bytes, use);
+    const size_t sh = setup_smem(reinterpret_cast<const void*>(chol_kernel<true>), bytes, use);
     double* g = use ? nullptr : work.get<double>((size_t)m * m);
-    chol_kernel<<<1, kThreads, sh, st>>>(m, G, R, info, g, use);
+    (use ? chol_kernel<true> : chol_kernel<false>)<<<1, kThreads, sh, st>>>(m, G, R, info, g, use);
     W4_LAUNCH();
 }
 
@@ -743,9 +795,10 @@ void pivoted_chol_rank(int m, const double* G, double tol_rel, int* rank, int* p
                        cudaStream_t st) {
     int use = 0;
     const size_t bytes = sizeof(double) * m * m;
-    const size_t sh = setup_smem(reinterpret_cast<const void*>(pchol_kernel), bytes, use);
+    const size_t sh = setup_smem(reinterpret_cast<const void*>(pchol_kernel<true>), bytes, use);
     double* g = use ? nullptr : work.get<double>((size_t)m * m);
-    pchol_kernel<<<1, kThreads, sh, st>>>(m, G, tol_rel, rank, perm, g, use);
+    (use ? pchol_kernel<true> : pchol_kernel<false>)<<<1, kThreads, sh, st>>>(m, G, tol_rel, rank, perm, g,
+                                                                              use);
     W4_LAUNCH();
 }
 
@@ -778,9 +831,10 @@ void sym_evd_desc(int m, const double* K, double* vals, double* W, DevBuf& work,
     if (!jacobi) {
         const size_t tb = sizeof(double) * (2 * (size_t)m * m + 7 * (size_t)m) + sizeof(int) * m;
         int use_t = 0;
-        const size_t sh_t = setup_smem(reinterpret_cast<const void*>(sym_evd_tql_kernel), tb, use_t);
+        const size_t sh_t = setup_smem(reinterpret_cast<const void*>(sym_evd_tql_kernel<true>), tb, use_t);
         double* gw = use_t ? nullptr : work.get<double>(tb / sizeof(double) + 1);
-        sym_evd_tql_kernel<<<1, kTqlThreads, sh_t, st>>>(m, K, vals, W, gw, use_t, nullptr);
+        (use_t ? sym_evd_tql_kernel<true> : sym_evd_tql_kernel<false>)<<<1, kTqlThreads, sh_t, st>>>(
+            m, K, vals, W, gw, use_t, nullptr);
         W4_LAUNCH();
         return;
     }
@@ -789,10 +843,11 @@ void sym_evd_desc(int m, const double* K, double* vals, double* W, DevBuf& work,
     const int mp = m + (m & 1);
     const size_t bytes2 = sizeof(double) * 2 * mp * mp;
     (void)bytes;
-    const size_t sh = setup_smem(reinterpret_cast<const void*>(jacobi_evd_blk_kernel), bytes2, use);
+    const size_t sh = setup_smem(reinterpret_cast<const void*>(jacobi_evd_blk_kernel<true>), bytes2, use);
     double* g = use ? nullptr : work.get<double>((size_t)2 * mp * mp);
     static const int debug = std::getenv("WC4DVAR_DEBUG_JACOBI") ? 1 : 0;
-    jacobi_evd_blk_kernel<<<1, kEvdThreads, sh, st>>>(m, K, vals, W, g, use, debug);
+    (use ? jacobi_evd_blk_kernel<true> : jacobi_evd_blk_kernel<false>)<<<1, kEvdThreads, sh, st>>>(
+        m, K, vals, W, g, use, debug);
     W4_LAUNCH();
 }
 
@@ -801,9 +856,9 @@ void svd_left_desc(int m, const double* X, double* sigma, double* U, DevBuf& wor
     require(m <= 512, "svd_left_desc: m too large");
     int use = 0;
     const size_t bytes = sizeof(double) * m * m;
-    const size_t sh = setup_smem(reinterpret_cast<const void*>(jacobi_svd_kernel), bytes, use);
+    const size_t sh = setup_smem(reinterpret_cast<const void*>(jacobi_svd_kernel<true>), bytes, use);
     double* g = use ? nullptr : work.get<double>((size_t)m * m);
-    jacobi_svd_kernel<<<1, kThreads, sh, st>>>(m, X, sigma, U, g, use);
+    (use ? jacobi_svd_kernel<true> : jacobi_svd_kernel<false>)<<<1, kThreads, sh, st>>>(m, X, sigma, U, g, use);
     W4_LAUNCH();
 }
 
