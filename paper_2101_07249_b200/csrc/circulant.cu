@@ -10,6 +10,7 @@
 
 #include <cufft.h>
 
+#include <cstdlib>
 #include <map>
 #include <mutex>
 
@@ -23,30 +24,36 @@ namespace {
             throw DeviceError(std::string(#expr) + ": cuFFT error " + std::to_string((int)_r)); \
     } while (0)
 
-__global__ void spectrum_mul_kernel(int64_t nh, int64_t ncols, int per, const double2* __restrict__ sb,
+__global__ void spectrum_mul_kernel(int64_t nh, int64_t ncols, int64_t c0, int per, const double2* __restrict__ sb,
                                     const double2* __restrict__ sq, double scale, double2* __restrict__ Z) {
-    // column c of the (N+1)m view: block i = c % per; i == 0 -> B spectrum, else Q
+    // column c0 + c of the (N+1)m view: block i = (c0 + c) % per; i == 0 -> B spectrum, else Q
     const int64_t total = nh * ncols;
     for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
          e += (int64_t)gridDim.x * blockDim.x) {
         const int64_t c = e / nh, f = e % nh;
-        const double2 h = ((c % per) == 0) ? sb[f] : sq[f];
+        const double2 h = (((c0 + c) % per) == 0) ? sb[f] : sq[f];
         const double2 z = Z[e];
         Z[e] = make_double2(scale * (z.x * h.x - z.y * h.y), scale * (z.x * h.y + z.y * h.x));
     }
 }
 
-__global__ void add_cols_kernel(int64_t rows, int64_t m, const double* __restrict__ a, int64_t lda,
-                                const double* __restrict__ b, int64_t ldb, double* __restrict__ out,
-                                int64_t ldo, unsigned* status) {
+// n-column chunk [c0, c0 + nc) of the (N+1)m view: view column c is window block
+// i = c % per of sketch column j = c / per, i.e. element j*ld + i*n + r of a block.
+__global__ void emit_chunk_kernel(int64_t n, int64_t nc, int64_t c0, int per, const double* __restrict__ tmp,
+                                  const double* __restrict__ add, int64_t ldadd, double* __restrict__ out,
+                                  int64_t ldo, unsigned* status) {
     bool bad = false;
-    const int64_t total = rows * m;
+    const int64_t total = n * nc;
     for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
          e += (int64_t)gridDim.x * blockDim.x) {
-        const int64_t c = e / rows, r = e % rows;
-        const double v = a[c * lda + r] + b[c * ldb + r];  // out = v + D^{1/2} s
-        out[c * ldo + r] = v;
-        bad |= !isfinite(v);
+        const int64_t c = c0 + e / n, r = e % n;
+        const int64_t j = c / per, i = c % per;
+        double v = tmp[e];
+        if (add) {
+            v = add[j * ldadd + i * n + r] + v;  // out = v + D^{1/2} s
+            bad |= !isfinite(v);
+        }
+        out[j * ldo + i * n + r] = v;
     }
     if (status && __syncthreads_or(bad) && threadIdx.x == 0) atomicOr(status, ST_OUT_NONFINITE);
 }
@@ -145,25 +152,36 @@ void CirculantPlan::apply(bool inv, int N, const double* V, int64_t ldv, int64_t
         W4_LAUNCH();
         X = xb;
     }
-    double2* Z = zbuf.get<double2>((size_t)nh * ncols);
-    auto pl = impl->get(ncols);
-    W4_CUFFT(cufftSetStream(pl.first, st));
-    W4_CUFFT(cufftSetStream(pl.second, st));
-    W4_CUFFT(cufftExecD2Z(pl.first, const_cast<double*>(X), reinterpret_cast<cufftDoubleComplex*>(Z)));
-    spectrum_mul_kernel<<<grid_for(nh * ncols), 256, 0, st>>>(nh, ncols, N + 1, sb, sq, 1.0 / (double)n, Z);
-    W4_LAUNCH();
-    if (!add && ldo == dim) {
-        W4_CUFFT(cufftExecZ2D(pl.second, reinterpret_cast<cufftDoubleComplex*>(Z), out));
-        return;
+    // WC4DVAR_FFT_CHUNK=c runs the columns in L2-sized chunks of c (D2Z -> product -> Z2D
+    // per chunk).  Measured at C4 (n = 1e6) this is SLOWER than one batched plan (chunk 1:
+    // 72 ms, 8: 31 ms, all 1088 columns: 25 ms per D^1/2): small batches leave cuFFT's
+    // kernels under-occupied.  Default: one chunk.
+    static const int64_t chunk_env = [] {
+        const char* e = std::getenv("WC4DVAR_FFT_CHUNK");
+        return e ? (int64_t)std::atoll(e) : (int64_t)0;
+    }();
+    const int64_t chunk = chunk_env > 0 ? std::min(chunk_env, ncols) : ncols;
+    const bool direct = !add && ldo == dim;  // Z2D straight into the output block
+    // spectrum chunk and (if needed) the real chunk before the epilogue share zbuf; xbuf may
+    // hold the contiguous copy of V
+    double2* Z = zbuf.get<double2>((size_t)nh * chunk + (direct ? 0 : (size_t)(n * chunk + 1) / 2));
+    double* tmp = direct ? nullptr : reinterpret_cast<double*>(Z + (size_t)nh * chunk);
+    for (int64_t c0 = 0; c0 < ncols; c0 += chunk) {
+        const int64_t nc = std::min(chunk, ncols - c0);
+        auto pl = impl->get(nc);
+        W4_CUFFT(cufftSetStream(pl.first, st));
+        W4_CUFFT(cufftSetStream(pl.second, st));
+        W4_CUFFT(cufftExecD2Z(pl.first, const_cast<double*>(X) + c0 * n, reinterpret_cast<cufftDoubleComplex*>(Z)));
+        spectrum_mul_kernel<<<grid_for(nh * nc), 256, 0, st>>>(nh, nc, c0, N + 1, sb, sq, 1.0 / (double)n, Z);
+        W4_LAUNCH();
+        if (direct) {
+            W4_CUFFT(cufftExecZ2D(pl.second, reinterpret_cast<cufftDoubleComplex*>(Z), out + c0 * n));
+            continue;
+        }
+        W4_CUFFT(cufftExecZ2D(pl.second, reinterpret_cast<cufftDoubleComplex*>(Z), tmp));
+        emit_chunk_kernel<<<grid_for(n * nc), 256, 0, st>>>(n, nc, c0, N + 1, tmp, add, ldadd, out, ldo, status);
+        W4_LAUNCH();
     }
-    double* tmp = xbuf.get<double>((size_t)dim * m);
-    W4_CUFFT(cufftExecZ2D(pl.second, reinterpret_cast<cufftDoubleComplex*>(Z), tmp));
-    if (add) {
-        add_cols_kernel<<<grid_for(dim * m), 256, 0, st>>>(dim, m, add, ldadd, tmp, dim, out, ldo, status);
-    } else {
-        copy_cols_kernel<<<grid_for(dim * m), 256, 0, st>>>(dim, m, tmp, dim, out, ldo);
-    }
-    W4_LAUNCH();
 }
 
 }  // namespace w4
