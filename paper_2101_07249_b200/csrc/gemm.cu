@@ -1061,7 +1061,9 @@ void gemm_nn(const GemmPass* passes, int npass, unsigned* status, cudaStream_t s
             return e ? std::atoi(e) : 1;
         }();
         if (start > 0) {
-            if (ws_mode) launch_sym_ws<128, 128, 4, 4, 4>(tab, start, status, stream);
+            // WC4DVAR_GEMM_WS: 1 = 16 consumer warps of 32x32, 2 = 8 consumer warps of 64x32
+            if (ws_mode == 2) launch_sym_ws<128, 128, 2, 4, 4>(tab, start, status, stream);
+            else if (ws_mode) launch_sym_ws<128, 128, 4, 4, 4>(tab, start, status, stream);
             else launch_sym<128, 128, 4, 4, 3>(tab, start, status, stream);
         }
         return;
