@@ -51,3 +51,40 @@ def test_circulant_lorenz96_sketch_vs_oracle():
         pg = W.sketch_eigenpairs(g, W.SketchConfig(**cfg))
         po = O.sketch_eigenpairs(o, O.SketchConfig(**cfg))
         assert relerr(pg.values, po.values) <= 1e-10, method
+
+
+def test_fused_four_step_fft_vs_oracle():
+    """The fused four-step FFT path (fft4.cu, opt-in via WC4DVAR_FFT4=1) against the oracle's
+    direct circulant convolution, on splits that exercise radices 8, 5, 4, 3 and 2 and both
+    paired and unpaired window columns (run in a fresh process: the knob is read once)."""
+    import os
+    import subprocess
+    import sys
+    code = r"""
+import math, sys, json
+sys.path.insert(0, 'tests'); sys.path.insert(0, '.')
+import numpy as np
+from oracle import oracle as O
+import paper_2101_07249_b200 as W
+from paper_2101_07249_b200 import configs
+from gpu_helpers import pair, relerr
+out = {}
+for n, N, m in ((1000, 3, 5), (300, 4, 3), (2000, 2, 4), (64, 5, 2)):
+    bh = configs.circulant_sqrt(configs.soar_first_column(1.0, 5.0, n))
+    qh = configs.circulant_sqrt(configs.soar_first_column(math.sqrt(0.05), 5.0, n))
+    g, o = pair(W.AdvDiffLinearized(n, N, 0.5, 0.2, 3), W.ObservationNetwork.build(n, N, 4, 1), bh, qh, 0.1)
+    V = O.gaussian_matrix(g.dim(), m, 1)
+    out[str(n)] = [relerr(g.apply_block(V), o.apply_block(V)),
+                   relerr(g.apply_D_half_inv(V[:, 0]), o.apply_D_half_inv(V[:, 0]))]
+print(json.dumps(out))
+"""
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, WC4DVAR_FFT4="1")
+    p = subprocess.run([sys.executable, "-c", code], cwd=root, env=env, capture_output=True, text=True,
+                       timeout=600)
+    assert p.returncode == 0, p.stderr[-2000:]
+    import json
+    res = json.loads(p.stdout.strip().splitlines()[-1])
+    for n, (e_apply, e_inv) in res.items():
+        assert e_apply <= 1e-12, (n, e_apply)
+        assert e_inv <= 1e-10, (n, e_inv)
