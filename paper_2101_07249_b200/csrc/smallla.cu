@@ -316,6 +316,13 @@ __global__ void __launch_bounds__(kEvdThreads)
     }
     __syncthreads();
     const int npairs = mp / 2;
+    // fixed per-thread roles of the block-update phase (see below)
+    const int aTQ = nt / npairs > 0 ? nt / npairs : 1;
+    const int aP = tid < aTQ * npairs ? tid % npairs : npairs;  // npairs: no A role
+    const int aQ0 = tid / npairs;
+    const int vTQ = nt / mp > 0 ? nt / mp : 1;
+    const int vI = tid < vTQ * mp ? tid % mp : mp;  // mp: no V role
+    const int vQ0 = tid / mp;
     for (int sweep = 0; sweep < 60 && m > 1; ++sweep) {
         int rotated = 0;
         for (int r = 0; r < mp - 1; ++r) {
@@ -328,10 +335,14 @@ __global__ void __launch_bounds__(kEvdThreads)
                 // Rotation threshold m*eps*sqrt|a_pp a_qq| (relative accuracy m*eps); a
                 // pure eps threshold lets roundoff re-create above-threshold entries so the
                 // sweep never goes quiet.
-                if (apq != 0.0 && fabs(apq) > mp * DBL_EPSILON * sqrt(fabs(app * aqq))) {
-                    const double tau = (aqq - app) / (2.0 * apq);
-                    const double t = (tau >= 0.0 ? 1.0 : -1.0) / (fabs(tau) + sqrt(1.0 + tau * tau));
-                    c = 1.0 / sqrt(1.0 + t * t);
+                // (squared test, no sqrt).  Rotation t = sgn(tau)/(|tau| + sqrt(1 + tau^2)),
+                // tau = h / g, rewritten as sgn(h) g / (|h| + sqrt(h^2 + g^2)): one division
+                // and one square root on this serial path, c = rsqrt(1 + t^2).
+                const double thr = mp * DBL_EPSILON;
+                if (apq != 0.0 && apq * apq > thr * thr * fabs(app * aqq)) {
+                    const double h = aqq - app, g = 2.0 * apq;
+                    const double t = (h >= 0.0 ? g : -g) / (fabs(h) + sqrt(h * h + g * g));
+                    c = rsqrt(1.0 + t * t);
                     s = t * c;
                     rotated = 1;
                 }
@@ -342,71 +353,68 @@ __global__ void __launch_bounds__(kEvdThreads)
             }
             __syncthreads();
             // 2x2 block updates A <- J_P^T A J_Q for all pair blocks (P, Q) and V <- V J_Q.
-            // Items are processed in batches of JB per thread with all loads issued before
-            // any store: the blocks are disjoint, and the explicit batching removes the
-            // store->load ordering the compiler would otherwise keep between items.  A pair
-            // with (c, s) = (1, 0) leaves its entries bit-identical, so no skip is needed.
-            constexpr int JB = 4;
-            const int nblk = npairs * npairs;
-            for (int b0 = tid; b0 < nblk; b0 += JB * nt) {
-                int o11[JB], o12[JB], o21[JB], o22[JB];
-                double cP[JB], sP[JB], cQ[JB], sQ[JB], a11[JB], a12[JB], a21[JB], a22[JB];
-#pragma unroll
-                for (int u = 0; u < JB; ++u) {
-                    const int bi = b0 + u * nt < nblk ? b0 + u * nt : 0;  // tail slots: load only
-                    const int P = bi % npairs, Q = bi / npairs;
-                    const int p1 = cs_p[P], p2 = cs_q[P], q1 = cs_p[Q], q2 = cs_q[Q];
-                    cP[u] = cs_c[P];
-                    sP[u] = cs_s[P];
-                    cQ[u] = cs_c[Q];
-                    sQ[u] = cs_s[Q];
-                    o11[u] = p1 + q1 * mp;
-                    o12[u] = p1 + q2 * mp;
-                    o21[u] = p2 + q1 * mp;
-                    o22[u] = p2 + q2 * mp;
-                    a11[u] = A[o11[u]];
-                    a12[u] = A[o12[u]];
-                    a21[u] = A[o21[u]];
-                    a22[u] = A[o22[u]];
+            // Each thread's roles were fixed before the sweep (no per-item index division):
+            // A blocks (P = aP, Q = aQ0 + k aTQ), V entries (row vI, pair Q = vQ0 + k vTQ).
+            // Two items per step with both loads issued before either store (the blocks are
+            // disjoint).  A pair with (c, s) = (1, 0) leaves its entries bit-identical.
+            if (aP < npairs) {
+                const int p1 = cs_p[aP], p2 = cs_q[aP];
+                const double cP = cs_c[aP], sP = cs_s[aP];
+                auto rot_blk = [&](int Q, double& a11, double& a12, double& a21, double& a22) {
+                    const double cQ = cs_c[Q], sQ = cs_s[Q];
+                    const double b11 = cQ * a11 - sQ * a12, b12 = sQ * a11 + cQ * a12;
+                    const double b21 = cQ * a21 - sQ * a22, b22 = sQ * a21 + cQ * a22;
+                    a11 = cP * b11 - sP * b21;
+                    a21 = sP * b11 + cP * b21;
+                    a12 = cP * b12 - sP * b22;
+                    a22 = sP * b12 + cP * b22;
+                };
+                int Q = aQ0;
+                for (; Q + aTQ < npairs; Q += 2 * aTQ) {
+                    const int Qb = Q + aTQ;
+                    const int qa1 = cs_p[Q] * mp, qa2 = cs_q[Q] * mp, qb1 = cs_p[Qb] * mp, qb2 = cs_q[Qb] * mp;
+                    double x11 = A[p1 + qa1], x12 = A[p1 + qa2], x21 = A[p2 + qa1], x22 = A[p2 + qa2];
+                    double y11 = A[p1 + qb1], y12 = A[p1 + qb2], y21 = A[p2 + qb1], y22 = A[p2 + qb2];
+                    rot_blk(Q, x11, x12, x21, x22);
+                    rot_blk(Qb, y11, y12, y21, y22);
+                    A[p1 + qa1] = x11;
+                    A[p1 + qa2] = x12;
+                    A[p2 + qa1] = x21;
+                    A[p2 + qa2] = x22;
+                    A[p1 + qb1] = y11;
+                    A[p1 + qb2] = y12;
+                    A[p2 + qb1] = y21;
+                    A[p2 + qb2] = y22;
                 }
-#pragma unroll
-                for (int u = 0; u < JB; ++u) {
-                    const double b11 = cQ[u] * a11[u] - sQ[u] * a12[u], b12 = sQ[u] * a11[u] + cQ[u] * a12[u];
-                    const double b21 = cQ[u] * a21[u] - sQ[u] * a22[u], b22 = sQ[u] * a21[u] + cQ[u] * a22[u];
-                    a11[u] = cP[u] * b11 - sP[u] * b21;
-                    a21[u] = sP[u] * b11 + cP[u] * b21;
-                    a12[u] = cP[u] * b12 - sP[u] * b22;
-                    a22[u] = sP[u] * b12 + cP[u] * b22;
-                }
-#pragma unroll
-                for (int u = 0; u < JB; ++u) {
-                    if (b0 + u * nt >= nblk) continue;
-                    A[o11[u]] = a11[u];
-                    A[o21[u]] = a21[u];
-                    A[o12[u]] = a12[u];
-                    A[o22[u]] = a22[u];
+                if (Q < npairs) {
+                    const int qa1 = cs_p[Q] * mp, qa2 = cs_q[Q] * mp;
+                    double x11 = A[p1 + qa1], x12 = A[p1 + qa2], x21 = A[p2 + qa1], x22 = A[p2 + qa2];
+                    rot_blk(Q, x11, x12, x21, x22);
+                    A[p1 + qa1] = x11;
+                    A[p1 + qa2] = x12;
+                    A[p2 + qa1] = x21;
+                    A[p2 + qa2] = x22;
                 }
             }
-            const int nv = npairs * mp;
-            for (int v0 = tid; v0 < nv; v0 += JB * nt) {
-                int o1[JB], o2[JB];
-                double c[JB], s[JB], v1[JB], v2[JB];
-#pragma unroll
-                for (int u = 0; u < JB; ++u) {
-                    const int vi = v0 + u * nt < nv ? v0 + u * nt : 0;
-                    const int Q = vi / mp, i = vi - Q * mp;
-                    c[u] = cs_c[Q];
-                    s[u] = cs_s[Q];
-                    o1[u] = i + cs_p[Q] * mp;
-                    o2[u] = i + cs_q[Q] * mp;
-                    v1[u] = V[o1[u]];
-                    v2[u] = V[o2[u]];
+            if (vI < mp) {
+                int Q = vQ0;
+                for (; Q + vTQ < npairs; Q += 2 * vTQ) {
+                    const int Qb = Q + vTQ;
+                    const int oa1 = vI + cs_p[Q] * mp, oa2 = vI + cs_q[Q] * mp;
+                    const int ob1 = vI + cs_p[Qb] * mp, ob2 = vI + cs_q[Qb] * mp;
+                    const double va1 = V[oa1], va2 = V[oa2], vb1 = V[ob1], vb2 = V[ob2];
+                    const double ca = cs_c[Q], sa = cs_s[Q], cb = cs_c[Qb], sb = cs_s[Qb];
+                    V[oa1] = ca * va1 - sa * va2;
+                    V[oa2] = sa * va1 + ca * va2;
+                    V[ob1] = cb * vb1 - sb * vb2;
+                    V[ob2] = sb * vb1 + cb * vb2;
                 }
-#pragma unroll
-                for (int u = 0; u < JB; ++u) {
-                    if (v0 + u * nt >= nv) continue;
-                    V[o1[u]] = c[u] * v1[u] - s[u] * v2[u];
-                    V[o2[u]] = s[u] * v1[u] + c[u] * v2[u];
+                if (Q < npairs) {
+                    const int oa1 = vI + cs_p[Q] * mp, oa2 = vI + cs_q[Q] * mp;
+                    const double va1 = V[oa1], va2 = V[oa2];
+                    const double ca = cs_c[Q], sa = cs_s[Q];
+                    V[oa1] = ca * va1 - sa * va2;
+                    V[oa2] = sa * va1 + ca * va2;
                 }
             }
             __syncthreads();
