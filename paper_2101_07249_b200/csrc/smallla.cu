@@ -683,6 +683,9 @@ __global__ void __launch_bounds__(kThreads)
     __syncthreads();
     const int mp = m + (m & 1);
     const int npairs = mp / 2;
+    const int uTK = nt / m > 0 ? nt / m : 1;  // update roles, fixed for all rounds
+    const int uI = tid < uTK * m ? tid % m : m;
+    const int uK0 = tid / m;
     for (int sweep = 0; sweep < 60 && m > 1; ++sweep) {
         int rotated = 0;
         for (int r = 0; r < mp - 1; ++r) {
@@ -701,11 +704,12 @@ __global__ void __launch_bounds__(kThreads)
                     al = warp_sum(al);
                     be = warp_sum(be);
                     ga = warp_sum(ga);
-                    if (ga != 0.0 && fabs(ga) > mp * DBL_EPSILON * sqrt(al * be)) {
-                        const double zeta = (be - al) / (2.0 * ga);
-                        const double t =
-                            (zeta >= 0.0 ? 1.0 : -1.0) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
-                        c = 1.0 / sqrt(1.0 + t * t);
+                    // |ga| > mp eps sqrt(al be), squared; t as in the two-sided kernel
+                    const double thr = mp * DBL_EPSILON;
+                    if (ga != 0.0 && ga * ga > thr * thr * (al * be)) {
+                        const double h = be - al, g = 2.0 * ga;
+                        const double t = (h >= 0.0 ? g : -g) / (fabs(h) + sqrt(h * h + g * g));
+                        c = rsqrt(1.0 + t * t);
                         s = t * c;
                         rotated = 1;
                     }
@@ -718,16 +722,16 @@ __global__ void __launch_bounds__(kThreads)
                 }
             }
             __syncthreads();
-            for (int e = tid; e < npairs * m; e += nt) {
-                const int k = e / m, i = e % m;
-                const double s = cs_s[k];
-                if (s == 0.0) continue;
-                const double c = cs_c[k];
-                const int p = cs_p[k], q = cs_q[k];
-                const double xp = X[i + p * m], xq = X[i + q * m];
-                X[i + p * m] = c * xp - s * xq;
-                X[i + q * m] = s * xp + c * xq;
-            }
+            if (uI < m)  // fixed roles: row uI of pairs k = uK0, uK0 + uTK, ...
+                for (int k = uK0; k < npairs; k += uTK) {
+                    const double s = cs_s[k];
+                    if (s == 0.0) continue;
+                    const double c = cs_c[k];
+                    const int op = uI + cs_p[k] * m, oq = uI + cs_q[k] * m;
+                    const double xp = X[op], xq = X[oq];
+                    X[op] = c * xp - s * xq;
+                    X[oq] = s * xp + c * xq;
+                }
             __syncthreads();
         }
         if (!__syncthreads_or(rotated)) break;
