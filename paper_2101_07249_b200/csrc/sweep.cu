@@ -393,10 +393,9 @@ __global__ void __launch_bounds__(512)
         atomicOr(status, (any_f ? ST_FWD_NONFINITE : 0u) | (any_a ? ST_ADJ_NONFINITE : 0u));
 }
 
-template <int KIND, int S>
-bool launch_blocked_s(const ModelDev& md, const NetDev& net, const SweepArgs& a, unsigned* status,
-                      cudaStream_t stream) {
-    constexpr int P = 8;
+template <int KIND, int S, int P>
+bool launch_blocked_sp(const ModelDev& md, const NetDev& net, const SweepArgs& a, unsigned* status,
+                       cudaStream_t stream) {
     const int64_t owners = (md.n + P - 1) / P;
     if (owners > 512) return false;
     int nt = (int)((owners + 31) / 32) * 32;
@@ -410,6 +409,20 @@ bool launch_blocked_s(const ModelDev& md, const NetDev& net, const SweepArgs& a,
     kern<<<(unsigned)a.m, nt, smem, stream>>>(md, net, a, tf, tb, status);
     W4_LAUNCH();
     return true;
+}
+
+// Points per thread: P = 4 when a column fits 512 threads that way (twice the warps per
+// column to hide the per-interval latency chain; the sweep is latency-bound at one CTA per
+// column), else P = 8.  WC4DVAR_SWEEP_P=8 forces the wider blocking.
+template <int KIND, int S>
+bool launch_blocked_s(const ModelDev& md, const NetDev& net, const SweepArgs& a, unsigned* status,
+                      cudaStream_t stream) {
+    static const int pref = [] {
+        const char* e = std::getenv("WC4DVAR_SWEEP_P");
+        return e ? std::atoi(e) : 4;
+    }();
+    if (pref == 4 && launch_blocked_sp<KIND, S, 4>(md, net, a, status, stream)) return true;
+    return launch_blocked_sp<KIND, S, 8>(md, net, a, status, stream);
 }
 
 template <int KIND>
