@@ -117,11 +117,13 @@ __global__ void __launch_bounds__(kBlock)
     if ((tid & 31) == 0) wred[tid >> 5] = d;
     __syncthreads();
     double* part = c.partial + (int64_t)blockIdx.x * (k + 1);
-    for (int i = tid; i < k; i += kBlock) {
+    // one warp per U column: lanes stride the CTA's rows, then a shuffle tree (fixed order)
+    for (int i = tid >> 5; i < k; i += kBlock / 32) {
         double s = 0.0;
         const double* col = Us + i * ks;
-        for (int rr = 0; rr < rows; ++rr) s += col[rr] * es[rr];
-        part[i] = s;
+        for (int rr = tid & 31; rr < rows; rr += 32) s += col[rr] * es[rr];
+        s = warp_sum(s);
+        if ((tid & 31) == 0) part[i] = s;
     }
     if (tid == 0) {
         double s = 0.0;
@@ -135,10 +137,13 @@ __global__ void __launch_bounds__(kBlock)
     if (!is_last) return;
     __threadfence();
     double* res = (MODE == M_UTV) ? A.out : (MODE == M_P1 ? c.g : c.h);
-    for (int i = tid; i <= k; i += kBlock) {
+    // final sums over the CTAs' partials: one warp per entry, lanes stride the CTAs (the
+    // loads of a lane are independent, so they pipeline instead of forming one long chain)
+    for (int i = tid >> 5; i <= k; i += kBlock / 32) {
         double s = 0.0;
-        for (unsigned b = 0; b < gridDim.x; ++b) s += __ldcg(c.partial + (int64_t)b * (k + 1) + i);
-        res[i] = s;
+        for (unsigned b = tid & 31; b < gridDim.x; b += 32) s += __ldcg(c.partial + (int64_t)b * (k + 1) + i);
+        s = warp_sum(s);
+        if ((tid & 31) == 0) res[i] = s;
     }
     __syncthreads();
     if (tid == 0) {
@@ -216,12 +221,15 @@ __global__ void sqdist_kernel(int64_t n, const double* __restrict__ a, const dou
         is_last = (atomicAdd(counter, 1u) == gridDim.x - 1);
     }
     __syncthreads();
-    if (is_last && threadIdx.x == 0) {
+    if (is_last && threadIdx.x < 32) {  // warp 0: lanes stride the partials, fixed-order tree
         __threadfence();
         double t = 0.0;
-        for (unsigned b2 = 0; b2 < gridDim.x; ++b2) t += __ldcg(partial + b2);
-        *out = t;
-        *counter = 0u;
+        for (unsigned b2 = threadIdx.x; b2 < gridDim.x; b2 += 32) t += __ldcg(partial + b2);
+        t = warp_sum(t);
+        if (threadIdx.x == 0) {
+            *out = t;
+            *counter = 0u;
+        }
     }
 }
 
