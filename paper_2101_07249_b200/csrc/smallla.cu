@@ -689,21 +689,30 @@ __global__ void __launch_bounds__(kThreads)
     for (int sweep = 0; sweep < 60 && m > 1; ++sweep) {
         int rotated = 0;
         for (int r = 0; r < mp - 1; ++r) {
-            for (int k = wid; k < npairs; k += nw) {
-                int p, q;
-                rr_pair(k, r, mp, p, q);
+            // 8-lane groups per column pair (4 pairs per warp, all pairs of a round at once);
+            // the warp iterates uniformly so the width-8 shuffles see every lane
+            const int gl = lane & 7, grp = lane >> 3;
+            for (int base = wid * 4; base < npairs; base += nw * 4) {
+                const int k = base + grp;
+                int p = 0, q = m;
+                if (k < npairs) rr_pair(k, r, mp, p, q);
                 double c = 1.0, s = 0.0;
-                if (q < m) {
-                    double al = 0.0, be = 0.0, ga = 0.0;
-                    for (int i = lane; i < m; i += 32) {
+                double al = 0.0, be = 0.0, ga = 0.0;
+                if (q < m)
+                    for (int i = gl; i < m; i += 8) {
                         const double xp = X[i + p * m], xq = X[i + q * m];
                         al += xp * xp;
                         be += xq * xq;
                         ga += xp * xq;
                     }
-                    al = warp_sum(al);
-                    be = warp_sum(be);
-                    ga = warp_sum(ga);
+#pragma unroll
+                for (int o = 4; o > 0; o >>= 1) {
+                    al += __shfl_xor_sync(0xffffffffu, al, o, 8);
+                    be += __shfl_xor_sync(0xffffffffu, be, o, 8);
+                    ga += __shfl_xor_sync(0xffffffffu, ga, o, 8);
+                }
+                if (k >= npairs) continue;
+                if (q < m) {
                     // |ga| > mp eps sqrt(al be), squared; t as in the two-sided kernel
                     const double thr = mp * DBL_EPSILON;
                     if (ga != 0.0 && ga * ga > thr * thr * (al * be)) {
@@ -714,7 +723,7 @@ __global__ void __launch_bounds__(kThreads)
                         rotated = 1;
                     }
                 }
-                if (lane == 0) {
+                if (gl == 0) {
                     cs_c[k] = c;
                     cs_s[k] = s;
                     cs_p[k] = p;
