@@ -314,11 +314,11 @@ def run_extras(W, configs, wl, op, Om, dev):
     pairs = {}
     for method in ("revd", "nystrom", "ritzit"):
         cfg = W.SketchConfig(k, l, configs.OMEGA_SEED, method, 1)
-        W.sketch_eigenpairs(op, cfg, Om)  # warm
-        t = W.last_sketch_timing()
+        W.sketch_eigenpairs(op, cfg, Om)  # warm (grows the sketch workspaces)
+        pairs[method] = W.sketch_eigenpairs(op, cfg, Om)
+        t = W.last_sketch_timing()  # the second, warm call
         out["lmp_build_ms"][method] = t["total_ms"]
         out["lmp_build_stage_ms"][method] = {kk: v for kk, v in t.items() if kk != "total_ms"}
-        pairs[method] = W.sketch_eigenpairs(op, cfg, Om)
     b = W.gaussian_matrix(nA, 1, configs.RHS_SEED)[:, 0]
     for method in ("none", "revd", "nystrom", "ritzit"):
         f = None if method == "none" else W.build_spectral_lmp(pairs[method])

@@ -6,6 +6,7 @@
 #include "pcg.cuh"
 
 #include <cmath>
+#include <cstdlib>
 #include <sstream>
 
 #include "lmp_pcg.cuh"
@@ -151,15 +152,61 @@ void pcg_dev(wc4dvar_op& op, const double* b, wc4dvar_lmp* pre, const double* x0
         W4_LAUNCH();
         nf = 1;
     }
-    for (int j = 1; j <= opts.max_iter; ++j) {
-        op.applies += 1;  // the single operator apply of this iteration (krylov.cpp:56)
+    // Without re-orthogonalisation every iteration issues the same device work on the same
+    // buffers: capture it once as a CUDA graph (apply + 3 row passes + the scalar read-back)
+    // and replay it, so the host's per-iteration sync is followed by one graph launch instead
+    // of ~10 kernel launches.  WC4DVAR_PCG_GRAPH=0 disables.
+    static const bool graph_env = [] {
+        const char* e = std::getenv("WC4DVAR_PCG_GRAPH");
+        return !(e && std::atoi(e) == 0);
+    }();
+    const bool use_graph = graph_env && !F && !op.prof;
+    cudaGraphExec_t gexec = nullptr;
+    struct GraphGuard {
+        cudaGraphExec_t& e;
+        ~GraphGuard() {
+            if (e) cudaGraphExecDestroy(e);
+        }
+    } gguard{gexec};
+    auto body = [&]() {
         op.reset_status(st);
         op.apply_block_dev(p, n, 1, w, n, st);
-        pcg_pass1(c, p, w, st);  // curvature, alpha
-        if (F) W4_CUDA(cudaMemcpyAsync(scal + SC_DOT, scal + SC_RHO, sizeof(double),
-                                       cudaMemcpyDeviceToDevice, st));
+        pcg_pass1(c, p, w, st);        // curvature, alpha
         pcg_pass2(c, x, r, p, w, st);  // x, r, rho_next, beta
-        if (F) {
+        pcg_pass3(c, r, p, st);        // p = C r + beta p (speculative; unused on exit)
+        W4_CUDA(cudaMemcpyAsync(op.h_status, op.d_status, sizeof(unsigned), cudaMemcpyDeviceToHost, st));
+        W4_CUDA(cudaMemcpyAsync(pinned, scal, SC_N * sizeof(double), cudaMemcpyDeviceToHost, st));
+    };
+    for (int j = 1; j <= opts.max_iter; ++j) {
+        op.applies += 1;  // the single operator apply of this iteration (krylov.cpp:56)
+        // iteration 1 runs eagerly (it grows the workspaces; no allocation under capture)
+        const bool graph_it = use_graph && j > 1;
+        if (graph_it) {
+            if (!gexec) {
+                cudaGraph_t graph = nullptr;
+                W4_CUDA(cudaStreamBeginCapture(st, cudaStreamCaptureModeRelaxed));
+                try {
+                    body();
+                } catch (...) {
+                    cudaStreamEndCapture(st, &graph);
+                    if (graph) cudaGraphDestroy(graph);
+                    throw;
+                }
+                W4_CUDA(cudaStreamEndCapture(st, &graph));
+                W4_CUDA(cudaGraphInstantiate(&gexec, graph, 0));
+                W4_CUDA(cudaGraphDestroy(graph));
+            }
+            W4_CUDA(cudaGraphLaunch(gexec, st));
+            W4_CUDA(cudaStreamSynchronize(st));
+        } else {
+            op.reset_status(st);
+            op.apply_block_dev(p, n, 1, w, n, st);
+            pcg_pass1(c, p, w, st);  // curvature, alpha
+            if (F) W4_CUDA(cudaMemcpyAsync(scal + SC_DOT, scal + SC_RHO, sizeof(double),
+                                           cudaMemcpyDeviceToDevice, st));
+            pcg_pass2(c, x, r, p, w, st);  // x, r, rho_next, beta
+        }
+        if (!graph_it && F) {
             // modified Gram-Schmidt against the stored normalised residuals (krylov.cpp:71-74)
             double* dd = scal + SC_N;
             for (int f = 0; f < nf; ++f) {
@@ -172,10 +219,12 @@ void pcg_dev(wc4dvar_op& op, const double* b, wc4dvar_lmp* pre, const double* x0
             reorth_fix_kernel<<<1, 1, 0, st>>>(scal, h, k);
             W4_LAUNCH();
         }
-        pcg_pass3(c, r, p, st);  // p = C r + beta p (speculative; unused on exit)
-        W4_CUDA(cudaMemcpyAsync(op.h_status, op.d_status, sizeof(unsigned), cudaMemcpyDeviceToHost,
-                                st));
-        read_scal();
+        if (!graph_it) {
+            pcg_pass3(c, r, p, st);  // p = C r + beta p (speculative; unused on exit)
+            W4_CUDA(cudaMemcpyAsync(op.h_status, op.d_status, sizeof(unsigned), cudaMemcpyDeviceToHost,
+                                    st));
+            read_scal();
+        }
         const unsigned s = *op.h_status;
         if (s & ST_FWD_NONFINITE)
             throw NumericalError("hessian apply: non-finite value after forward sweep");
