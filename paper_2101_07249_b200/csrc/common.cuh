@@ -37,7 +37,8 @@ inline void require(bool cond, const std::string& what) {
     do {                                                                                 \
         cudaError_t _e = cudaGetLastError();                                             \
         if (_e != cudaSuccess)                                                           \
-            throw ::w4::DeviceError(std::string("kernel launch: ") + cudaGetErrorString(_e)); \
+            throw ::w4::DeviceError(std::string("kernel launch (") + __FILE__ + ":" +       \
+                                    std::to_string(__LINE__) + "): " + cudaGetErrorString(_e)); \
     } while (0)
 
 // Status bits written by kernels into a device word (finite checks of

@@ -8,6 +8,8 @@
 // with the observation selection (models.cpp:184-201) fused into the sweeps.
 #include "sweep.cuh"
 
+#include <cooperative_groups.h>
+
 #include <cstdlib>
 
 namespace w4 {
@@ -393,6 +395,205 @@ __global__ void __launch_bounds__(512)
         atomicOr(status, (any_f ? ST_FWD_NONFINITE : 0u) | (any_a ? ST_ADJ_NONFINITE : 0u));
 }
 
+// ---------------------------------------------------------------------------
+// Cluster-split resident sweep for few columns (PCG's single-vector applies): the CL CTAs
+// of a thread-block cluster each own n/CL points of the column; per interval every CTA
+// pulls the S-point halos of its two neighbours from their SMEM over DSMEM after one
+// cluster barrier, then advances its segment with the fused stencil.  One column runs on
+// CL SMs instead of one (the resident sweep is latency-bound at one CTA per column).
+// Region layout per CTA: e in [0, Lseg + 2S), e = S + local point, point-major slots.
+// ---------------------------------------------------------------------------
+template <int KIND, int S, int P, int CL>
+__global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(512)
+    sweep_cluster_kernel(const ModelDev md, const NetDev net, const SweepArgs a, const StencilTaps tf,
+                         const StencilTaps tb, unsigned* __restrict__ status) {
+    namespace cg = cooperative_groups;
+    cg::cluster_group cluster = cg::this_cluster();
+    extern __shared__ double sm[];
+    const int n = (int)md.n;
+    const int N = md.N;
+    const int Lseg = n / CL;
+    const int R = Lseg + 2 * S;
+    const int ntp = (R + P - 1) / P;
+    double* buf0 = sm;
+    double* buf1 = sm + P * ntp;
+    int* pm = reinterpret_cast<int*>(sm + 2 * P * ntp);  // pmap of the own segment
+    int* slot = pm + Lseg;
+    const int rank = (int)cluster.block_rank();
+    const int64_t col = blockIdx.x / CL;
+    const int seg0 = rank * Lseg;
+    const int left = (rank + CL - 1) % CL, right = (rank + 1) % CL;
+    const int tid = threadIdx.x, nt = blockDim.x;
+    const int b = tid * P;  // own local points [b, b + P), region e = S + b + p
+    const bool owner = b < Lseg;
+    const int np = net.n_points;
+    bool bad_f = false, bad_a = false;
+    double v[P + 2 * S];
+    auto sl_of = [&](int e) { return (e % P) * ntp + e / P; };
+    for (int j = tid; j < Lseg; j += nt) pm[j] = net.pmap[seg0 + j];
+    for (int t = tid; t <= N; t += nt) slot[t] = net.slot[t];
+    __syncthreads();  // the staged tables are read by other threads below
+    // halos of buffer `cur`: e in [0, S) <- left's own tail, e in [Lseg + S, R) <- right's head
+    auto pull_halos = [&](double* cur) {
+        if (tid < 2 * S) {
+            const bool lft = tid < S;
+            const int e_dst = lft ? tid : Lseg + S + (tid - S);
+            const int e_src = lft ? Lseg + tid : S + (tid - S);
+            const double* nb = cluster.map_shared_rank(cur, lft ? left : right);
+            cur[sl_of(e_dst)] = nb[sl_of(e_src)];
+        }
+    };
+    auto advance = [&](const double* cur, const StencilTaps& tp) {
+#pragma unroll
+        for (int u = 0; u < P + 2 * S; ++u) v[u] = cur[sl_of(b + u)];
+        double o[P];
+#pragma unroll
+        for (int p = 0; p < P; ++p) {
+            double acc = tp.t[0] * v[p];
+#pragma unroll
+            for (int k = 1; k <= 2 * S; ++k) acc = fma(tp.t[k], v[p + k], acc);
+            o[p] = acc;
+        }
+#pragma unroll
+        for (int p = 0; p < P; ++p) v[S + p] = o[p];
+    };
+
+    if (a.do_fwd) {
+        const double* X = a.X + col * a.ldx;
+        double* Yc = a.Y ? a.Y + col * net.q : nullptr;
+        double* tr = a.traj ? a.traj + col * a.ldtraj : nullptr;
+        {
+            const int sl = slot[0];
+            for (int j = tid; j < Lseg; j += nt) {
+                const int g = seg0 + j;
+                const double x = X[g];
+                buf0[sl_of(S + j)] = x;
+                bad_f |= !isfinite(x);
+                if (tr) tr[g] = x;
+                if (a.fwd_obs && sl >= 0) {
+                    const int bb = pm[j];
+                    if (bb >= 0) Yc[(int64_t)sl * np + bb] = a.scale_fwd * x;
+                }
+            }
+        }
+        double xin[P];
+#pragma unroll
+        for (int p = 0; p < P; ++p) xin[p] = (owner && N > 0) ? X[(int64_t)n + seg0 + b + p] : 0.0;
+        double* cur = buf0;
+        double* nxt = buf1;
+        for (int i = 0; i < N; ++i) {
+            cluster.sync();  // every segment of x_i is in SMEM (and the old halos are read)
+            pull_halos(cur);
+            __syncthreads();
+            const int sl = slot[i + 1];
+            double* trn = tr ? tr + (int64_t)(i + 1) * n : nullptr;
+            double xnx[P];
+            const double* Xnn = X + (int64_t)(i + 2) * n + seg0;
+#pragma unroll
+            for (int p = 0; p < P; ++p) xnx[p] = (owner && i + 1 < N) ? Xnn[b + p] : 0.0;
+            if (owner) {
+                advance(cur, tf);
+#pragma unroll
+                for (int p = 0; p < P; ++p) {
+                    const int j = b + p;
+                    const double x = v[S + p] + xin[p];  // operators.cpp:88
+                    nxt[sl_of(S + j)] = x;
+                    bad_f |= !isfinite(x);
+                    if (trn) trn[seg0 + j] = x;
+                    if (a.fwd_obs && sl >= 0) {
+                        const int bb = pm[j];
+                        if (bb >= 0) Yc[(int64_t)sl * np + bb] = a.scale_fwd * x;
+                    }
+                }
+            }
+#pragma unroll
+            for (int p = 0; p < P; ++p) xin[p] = xnx[p];
+            double* t = cur;
+            cur = nxt;
+            nxt = t;
+        }
+    }
+
+    if (a.do_adj) {
+        cluster.sync();  // the forward's last halo reads of buf0 / buf1 are done
+        const double* V = a.V ? a.V + col * a.ldv : nullptr;
+        const double* Yc = a.Y ? a.Y + col * net.q : nullptr;
+        double* Sv = a.S + col * a.lds;
+        auto addend = [&](int i, int j) -> double {  // j: local point
+            double x = V ? V[(int64_t)i * n + seg0 + j] : 0.0;
+            if (a.adj_obs) {
+                const int sl = slot[i];
+                if (sl >= 0) {
+                    const int bb = pm[j];
+                    if (bb >= 0) x = V ? x + Yc[(int64_t)sl * np + bb] : Yc[(int64_t)sl * np + bb];
+                }
+            }
+            return x;
+        };
+        {
+            const int64_t off = (int64_t)N * n + seg0;
+            for (int j = tid; j < Lseg; j += nt) {
+                const double x = addend(N, j);
+                buf0[sl_of(S + j)] = x;
+                Sv[off + j] = x;
+                bad_a |= !isfinite(x);
+            }
+        }
+        double ain[P];
+#pragma unroll
+        for (int p = 0; p < P; ++p) ain[p] = (owner && N > 0) ? addend(N - 1, b + p) : 0.0;
+        double* cur = buf0;
+        double* nxt = buf1;
+        for (int i = N - 1; i >= 0; --i) {
+            cluster.sync();
+            pull_halos(cur);
+            __syncthreads();
+            const int64_t off = (int64_t)i * n + seg0;
+            double anx[P];
+#pragma unroll
+            for (int p = 0; p < P; ++p) anx[p] = (owner && i > 0) ? addend(i - 1, b + p) : 0.0;
+            if (owner) {
+                advance(cur, tb);
+#pragma unroll
+                for (int p = 0; p < P; ++p) {
+                    const int j = b + p;
+                    const double x = ain[p] + v[S + p];  // operators.cpp:99
+                    nxt[sl_of(S + j)] = x;
+                    Sv[off + j] = x;
+                    bad_a |= !isfinite(x);
+                }
+            }
+#pragma unroll
+            for (int p = 0; p < P; ++p) ain[p] = anx[p];
+            double* t = cur;
+            cur = nxt;
+            nxt = t;
+        }
+    }
+    cluster.sync();  // no CTA exits while a neighbour may still read its SMEM
+    const int any_f = __syncthreads_or(bad_f);
+    const int any_a = __syncthreads_or(bad_a);
+    if (tid == 0 && (any_f || any_a))
+        atomicOr(status, (any_f ? ST_FWD_NONFINITE : 0u) | (any_a ? ST_ADJ_NONFINITE : 0u));
+}
+
+template <int KIND, int S, int P, int CL>
+bool launch_cluster_sp(const ModelDev& md, const NetDev& net, const SweepArgs& a, unsigned* status,
+                       cudaStream_t stream) {
+    if (md.n % (CL * P) != 0) return false;
+    const int Lseg = (int)(md.n / CL);
+    if (Lseg < 2 * S || Lseg / P > 512) return false;
+    const int R = Lseg + 2 * S, ntp = (R + P - 1) / P;
+    const size_t smem = sizeof(double) * 2 * P * ntp + sizeof(int) * (Lseg + md.N + 1);
+    if (smem > 48 * 1024) return false;
+    const int nt = ((Lseg / P + 31) / 32) * 32;
+    const StencilTaps tf = stencil_power(KIND, md.c, md.d, S, false);
+    const StencilTaps tb = stencil_power(KIND, md.c, md.d, S, true);
+    sweep_cluster_kernel<KIND, S, P, CL><<<(unsigned)(a.m * CL), nt, smem, stream>>>(md, net, a, tf, tb, status);
+    W4_LAUNCH();
+    return true;
+}
+
 template <int KIND, int S, int P>
 bool launch_blocked_sp(const ModelDev& md, const NetDev& net, const SweepArgs& a, unsigned* status,
                        cudaStream_t stream) {
@@ -421,6 +622,12 @@ bool launch_blocked_s(const ModelDev& md, const NetDev& net, const SweepArgs& a,
         const char* e = std::getenv("WC4DVAR_SWEEP_P");
         return e ? std::atoi(e) : 4;
     }();
+    // few columns (PCG): split each column over a 4-CTA cluster (WC4DVAR_SWEEP_CLUSTER=0 off)
+    static const int clus = [] {
+        const char* e = std::getenv("WC4DVAR_SWEEP_CLUSTER");
+        return e ? std::atoi(e) : 4;
+    }();
+    if (clus == 4 && a.m * 4 <= kSMs && launch_cluster_sp<KIND, S, 4, 4>(md, net, a, status, stream)) return true;
     if (pref == 4 && launch_blocked_sp<KIND, S, 4>(md, net, a, status, stream)) return true;
     return launch_blocked_sp<KIND, S, 8>(md, net, a, status, stream);
 }
