@@ -1168,7 +1168,7 @@ bool launch_l96_blk(const ModelDev& md, const NetDev& net, const SweepArgs& a, u
 // WC4DVAR_L96_BLK: 0 = SMEM phase kernels only, 1 = register-blocked whenever the region
 // fits the domain (tests), unset = register-blocked for the tiled (large-n) regime.
 // WC4DVAR_L96_CB: CTA shape of the register-blocked kernel as columns x threads per column
-// (1: 2x256, 2: 4x128, 4: 4x64, 8: 8x64 (default), 16: 16x32).
+// (1: 2x256, 2: 4x128, 4: 4x64 (default, 2 CTAs per SM), 8: 8x64, 16: 16x32).
 bool try_l96_blk(const ModelDev& md, const NetDev& net, const SweepArgs& a, unsigned* status, cudaStream_t st,
                  DevBuf& ws, bool tiled_regime) {
     static const int mode = [] {
@@ -1177,7 +1177,7 @@ bool try_l96_blk(const ModelDev& md, const NetDev& net, const SweepArgs& a, unsi
     }();
     static const int cb = [] {
         const char* e = std::getenv("WC4DVAR_L96_CB");
-        return e ? std::atoi(e) : 8;
+        return e ? std::atoi(e) : 4;
     }();
     if (mode == 0 || (mode < 0 && !tiled_regime)) return false;
     switch (cb) {
