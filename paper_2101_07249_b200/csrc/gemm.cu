@@ -522,13 +522,22 @@ struct SkArgs {
     int* flags;        // [G], zeroed before the launch
 };
 
-template <int BM, int BN, int WM, int WN, int STAGES>
-__global__ void __launch_bounds__(WM * WN * 32 + 32, 1)
+// SMEM row stride RS: KS (= BK + 8, padded, conflict-free by padding) or BK (unpadded, the
+// 16-byte chunk index XOR-swizzled with bit 2 by the row parity: the two rows a quarter-warp
+// reads with LDS.128 then land in disjoint bank groups, and the producer's lane-rotated
+// chunk order stays conflict-free).  Unpadded stages are 2/3 the size, so 6 fit in SMEM.
+template <int RS>
+__device__ __forceinline__ int swz(int row, int chunk) {
+    return RS == BK ? (chunk ^ ((row & 1) << 2)) : chunk;
+}
+
+template <int BM, int BN, int WM, int WN, int STAGES, int RS, int NPW>
+__global__ void __launch_bounds__(WM * WN * 32 + 32 * NPW, 1)
     gemm_sym_ws_kernel(const PassTable tab, unsigned* __restrict__ status, const SkArgs sk) {
     constexpr int NC = WM * WN * 32;  // consumer threads
     constexpr int WTM = BM / WM, WTN = BN / WN;
     constexpr int MI = WTM / 16, NI = WTN / 8;
-    constexpr int A_ELEMS = BM * KS, B_ELEMS = BN * KS;
+    constexpr int A_ELEMS = BM * RS, B_ELEMS = BN * RS;
     static_assert(BM % 32 == 0 && BN % 32 == 0, "tile");
     extern __shared__ __align__(16) double smem[];
     double* As = smem;
@@ -557,14 +566,16 @@ __global__ void __launch_bounds__(WM * WN * 32 + 32, 1)
     const int warp = tid >> 5, lane = tid & 31;
     if (tid == 0) {
         for (int s = 0; s < STAGES; ++s) {
-            mbar_init(&full[s], 32);
+            mbar_init(&full[s], 32 * NPW);
             mbar_init(&empty[s], WM * WN);
         }
     }
     __syncthreads();
 
-    if (warp == WM * WN) {
-        // ===== producer warp =====
+    if (warp >= WM * WN) {
+        // ===== producer warp(s) =====  (NPW = 2: warp 0 streams A, warp 1 streams B)
+        const int pw = warp - WM * WN;
+        const bool doA = NPW == 1 || pw == 0, doB = NPW == 1 || pw == 1;
         // Lane l owns A rows l + 32u and B columns l + 32u (pointers computed once per
         // tile).  It copies the 8 16-byte chunks of each row in the lane-rotated order
         // (ch + l) & 7: with the 192-byte row stride the 8 lanes of a quarter-warp then hit
@@ -600,20 +611,42 @@ __global__ void __launch_bounds__(WM * WN * 32 + 32, 1)
                 const unsigned ph = (it / STAGES) & 1u;
                 mbar_wait(&empty[s], ph ^ 1u);
                 const int64_t k0 = kt * BK;
-                double* as = As + s * A_ELEMS + lane * KS;
-                double* bs = Bs + s * B_ELEMS + lane * KS;
+                double* as = As + s * A_ELEMS + lane * RS;
+                double* bs = Bs + s * B_ELEMS + lane * RS;
+                if (k0 + BK <= K) {
+                    // interior k-tile: no tail predicates (out-of-range rows / columns point at
+                    // valid memory and zero-fill through the src-size operand)
+#pragma unroll
+                    for (int cc = 0; cc < BK / 2; ++cc) {
+                        const int ch = (cc + lane) & 7;
+                        const int sc = 2 * swz<RS>(lane, ch);
+                        if (doA)
+#pragma unroll
+                            for (int u = 0; u < AU; ++u)
+                                cp_async16(as + u * 32 * RS + sc, arow[u] + k0 + 2 * ch, aok[u] ? 16 : 0);
+                        if (doB)
+#pragma unroll
+                            for (int u = 0; u < BU; ++u)
+                                cp_async16(bs + u * 32 * RS + sc, bcol[u] + k0 + 2 * ch, bok[u] ? 16 : 0);
+                    }
+                    mbar_arrive_cp_async(&full[s]);
+                    continue;
+                }
 #pragma unroll
                 for (int cc = 0; cc < BK / 2; ++cc) {
                     const int ch = (cc + lane) & 7;
+                    const int sc = 2 * swz<RS>(lane, ch);  // rows lane + 32 u share the parity
                     const int64_t kr = k0 + 2 * ch;
                     const int64_t rem = K - kr;
                     const int kval = rem >= 2 ? 2 : (rem > 0 ? (int)rem : 0);
+                    if (doA)
 #pragma unroll
-                    for (int u = 0; u < AU; ++u)
-                        cp_async_vec<2>(as + u * 32 * KS + 2 * ch, arow[u] + kr, aok[u] ? kval : 0, safe);
+                        for (int u = 0; u < AU; ++u)
+                            cp_async_vec<2>(as + u * 32 * RS + sc, arow[u] + kr, aok[u] ? kval : 0, safe);
+                    if (doB)
 #pragma unroll
-                    for (int u = 0; u < BU; ++u)
-                        cp_async_vec<2>(bs + u * 32 * KS + 2 * ch, bcol[u] + kr, bok[u] ? kval : 0, safe);
+                        for (int u = 0; u < BU; ++u)
+                            cp_async_vec<2>(bs + u * 32 * RS + sc, bcol[u] + kr, bok[u] ? kval : 0, safe);
                 }
                 mbar_arrive_cp_async(&full[s]);
             }
@@ -664,8 +697,9 @@ __global__ void __launch_bounds__(WM * WN * 32 + 32, 1)
 #pragma unroll
             for (int i = 0; i < MI; ++i) {
                 const int r = wm * WTM + i * 16 + g;
-                const double2 lo = *reinterpret_cast<const double2*>(as + r * KS + k8 + 2 * t0);
-                const double2 hi = *reinterpret_cast<const double2*>(as + (r + 8) * KS + k8 + 2 * t0);
+                const int sc = 2 * swz<RS>(r, k8 / 2 + t0);  // rows r and r + 8 share the parity
+                const double2 lo = *reinterpret_cast<const double2*>(as + r * RS + sc);
+                const double2 hi = *reinterpret_cast<const double2*>(as + (r + 8) * RS + sc);
                 af[i][0] = lo.x;
                 af[i][2] = lo.y;
                 af[i][1] = hi.x;
@@ -674,7 +708,7 @@ __global__ void __launch_bounds__(WM * WN * 32 + 32, 1)
 #pragma unroll
             for (int j = 0; j < NI; ++j) {
                 const int c = wn * WTN + j * 8 + g;
-                const double2 bb = *reinterpret_cast<const double2*>(bs + c * KS + k8 + 2 * t0);
+                const double2 bb = *reinterpret_cast<const double2*>(bs + c * RS + 2 * swz<RS>(c, k8 / 2 + t0));
                 bf[j][0] = bb.x;
                 bf[j][1] = bb.y;
             }
@@ -733,11 +767,11 @@ __global__ void __launch_bounds__(WM * WN * 32 + 32, 1)
 // Grid: one CTA per SM in stream-K mode when the tile count is not a multiple of the SM
 // count (WC4DVAR_GEMM_SK=0 forces one CTA per tile).  Partials / flags come from the
 // stream-ordered pool, so concurrent GEMMs on different streams never share them.
-template <int BM, int BN, int WM, int WN, int STAGES>
+template <int BM, int BN, int WM, int WN, int STAGES, int RS = KS, int NPW = 1>
 void launch_sym_ws(const PassTable& tab, int64_t ntiles, unsigned* status, cudaStream_t stream) {
     constexpr int NC = WM * WN * 32;
-    const size_t smem = sizeof(double) * STAGES * (BM * KS + BN * KS) + 2 * STAGES * sizeof(uint64_t);
-    auto kern = gemm_sym_ws_kernel<BM, BN, WM, WN, STAGES>;
+    const size_t smem = sizeof(double) * STAGES * (BM * RS + BN * RS) + 2 * STAGES * sizeof(uint64_t);
+    auto kern = gemm_sym_ws_kernel<BM, BN, WM, WN, STAGES, RS, NPW>;
     configure_smem(reinterpret_cast<const void*>(kern), smem);
     static const int sk_mode = [] {
         const char* e = std::getenv("WC4DVAR_GEMM_SK");
@@ -760,12 +794,12 @@ void launch_sym_ws(const PassTable& tab, int64_t ntiles, unsigned* status, cudaS
         sk.partial = reinterpret_cast<double*>(buf);
         sk.flags = reinterpret_cast<int*>(buf + pbytes);
         W4_CUDA(cudaMemsetAsync(sk.flags, 0, sizeof(int) * grid, stream));
-        kern<<<(unsigned)grid, NC + 32, smem, stream>>>(tab, status, sk);
+        kern<<<(unsigned)grid, NC + 32 * NPW, smem, stream>>>(tab, status, sk);
         W4_LAUNCH();
         W4_CUDA(cudaFreeAsync(buf, stream));
         return;
     }
-    kern<<<(unsigned)grid, NC + 32, smem, stream>>>(tab, status, sk);
+    kern<<<(unsigned)grid, NC + 32 * NPW, smem, stream>>>(tab, status, sk);
     W4_LAUNCH();
 }
 
@@ -1058,11 +1092,15 @@ void gemm_nn(const GemmPass* passes, int npass, unsigned* status, cudaStream_t s
         tab.tile_start[2] = start;
         static const int ws_mode = [] {
             const char* e = std::getenv("WC4DVAR_GEMM_WS");
-            return e ? std::atoi(e) : 1;
+            return e ? std::atoi(e) : 4;
         }();
         if (start > 0) {
-            // WC4DVAR_GEMM_WS: 1 = 16 consumer warps of 32x32, 2 = 8 consumer warps of 64x32
-            if (ws_mode == 2) launch_sym_ws<128, 128, 2, 4, 4>(tab, start, status, stream);
+            // WC4DVAR_GEMM_WS: 4 (default) = 16 consumer warps of 32x32 + 2 producer warps (A, B),
+            // 1 = one producer warp, 2 = 8 consumer warps of 64x32
+            // 3: unpadded swizzled stages, 6-deep ring
+            if (ws_mode == 3) launch_sym_ws<128, 128, 4, 4, 6, BK>(tab, start, status, stream);
+            else if (ws_mode == 4) launch_sym_ws<128, 128, 4, 4, 4, KS, 2>(tab, start, status, stream);
+            else if (ws_mode == 2) launch_sym_ws<128, 128, 2, 4, 4>(tab, start, status, stream);
             else if (ws_mode) launch_sym_ws<128, 128, 4, 4, 4>(tab, start, status, stream);
             else launch_sym<128, 128, 4, 4, 3>(tab, start, status, stream);
         }
