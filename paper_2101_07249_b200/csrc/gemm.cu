@@ -738,14 +738,51 @@ __global__ void __launch_bounds__(WM * WN * 32 + 32 * NPW, 1)
     const ColMap& amap = s_tab.p[xy.pi].add;
     const int64_t Mrows = s_tab.p[xy.pi].M, ncols = s_tab.p[xy.pi].ncols;
     const double alpha = s_tab.p[xy.pi].alpha;
+    if (!amap.base) {  // plain D^{1/2} v
+#pragma unroll
+        for (int j = 0; j < NI; ++j)
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+                const int64_t c = xy.n0 + wn * WTN + j * 8 + 2 * t0 + h;
+                if (c >= ncols) continue;
+                double* oc = const_cast<double*>(omap.col(c));
+#pragma unroll
+                for (int i = 0; i < MI; ++i)
+#pragma unroll
+                    for (int v = 0; v < 2; ++v) {
+                        const int64_t r = xy.m0 + wm * WTM + i * 16 + g + 8 * v;
+                        if (r >= Mrows) continue;
+                        const double val = alpha * acc[i][j][2 * v + h];
+                        bad |= !isfinite(val);
+                        __stcg(oc + r, val);
+                    }
+            }
+        continue;
+    }
 #pragma unroll
     for (int j = 0; j < NI; ++j) {
+        // the add term (v of out = v + D^{1/2}s) through the read-only path, all of this
+        // column block's loads issued before its stores (else each load waits on HBM in turn)
+        const double* addc[2];
+        double* outc[2];
+        double addv[2][MI][2];
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
             const int64_t c = xy.n0 + wn * WTN + j * 8 + 2 * t0 + h;
-            if (c >= ncols) continue;
-            double* outc = const_cast<double*>(omap.col(c));
-            const double* addc = amap.base ? amap.col(c) : nullptr;
+            const bool ok = c < ncols;
+            outc[h] = ok ? const_cast<double*>(omap.col(c)) : nullptr;
+            addc[h] = (ok && amap.base) ? amap.col(c) : nullptr;
+#pragma unroll
+            for (int i = 0; i < MI; ++i)
+#pragma unroll
+                for (int v = 0; v < 2; ++v) {
+                    const int64_t r = xy.m0 + wm * WTM + i * 16 + g + 8 * v;
+                    addv[h][i][v] = (addc[h] && r < Mrows) ? __ldg(addc[h] + r) : 0.0;
+                }
+        }
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            if (!outc[h]) continue;
 #pragma unroll
             for (int i = 0; i < MI; ++i) {
 #pragma unroll
@@ -753,9 +790,9 @@ __global__ void __launch_bounds__(WM * WN * 32 + 32 * NPW, 1)
                     const int64_t r = xy.m0 + wm * WTM + i * 16 + g + 8 * v;
                     if (r >= Mrows) continue;
                     double val = alpha * acc[i][j][2 * v + h];
-                    if (addc) val = addc[r] + val;
+                    if (addc[h]) val = addv[h][i][v] + val;
                     bad |= !isfinite(val);
-                    __stcg(outc + r, val);
+                    __stcg(outc[h] + r, val);
                 }
             }
         }
