@@ -9,7 +9,6 @@ namespace w4 {
 namespace {
 
 constexpr int BK = 16;
-constexpr int KPAD = BK + 4;  // [col][k] tiles: stride 20 doubles -> conflict-free fragments
 // [col][k] tiles read with LDS.128 under the permuted k order (see gemm_sym_kernel):
 // stride 24 doubles keeps 16-byte fragment loads bank-conflict free.
 constexpr int KS = BK + 8;
@@ -31,15 +30,6 @@ __device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_grou
 template <int N>
 __device__ __forceinline__ void cp_wait() {
     asm volatile("cp.async.wait_group %0;\n" ::"n"(N));
-}
-
-__device__ __forceinline__ void dmma16x8x8(double (&d)[4], const double (&a)[4],
-                                           const double (&b)[2]) {
-    asm volatile(
-        "mma.sync.aligned.m16n8k8.row.col.f64.f64.f64.f64 "
-        "{%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, {%0,%1,%2,%3};\n"
-        : "+d"(d[0]), "+d"(d[1]), "+d"(d[2]), "+d"(d[3])
-        : "d"(a[0]), "d"(a[1]), "d"(a[2]), "d"(a[3]), "d"(b[0]), "d"(b[1]));
 }
 
 __device__ __forceinline__ void dmma16x8x4(double (&d)[4], double a0, double a1, double b0) {

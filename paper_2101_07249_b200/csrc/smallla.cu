@@ -197,98 +197,6 @@ __device__ __forceinline__ void rr_pair(int k, int r, int mp, int& p, int& q) {
     }
 }
 
-// ---------------------------------------------------------------- two-sided Jacobi EVD
-template <bool SM>
-__global__ void __launch_bounds__(kThreads)
-    jacobi_evd_kernel(int m, const double* __restrict__ K, double* __restrict__ vals,
-                      double* __restrict__ W, double* gwork, int use_smem) {
-    extern __shared__ double sm[];
-    double* A = SM ? sm : gwork;
-    double* V = A + (size_t)m * m;
-    __shared__ double cs_c[512], cs_s[512];
-    __shared__ int cs_p[512], cs_q[512];
-    __shared__ int rank_of[512];
-    const int tid = threadIdx.x, nt = blockDim.x;
-    for (int e = tid; e < m * m; e += nt) {
-        const int i = e % m, j = e / m;
-        A[e] = 0.5 * (K[i + j * m] + K[j + i * m]);
-        V[e] = (i == j) ? 1.0 : 0.0;
-    }
-    __syncthreads();
-    const int mp = m + (m & 1);
-    const int npairs = mp / 2;
-    for (int sweep = 0; sweep < 60 && m > 1; ++sweep) {
-        int rotated = 0;
-        for (int r = 0; r < mp - 1; ++r) {
-            for (int k = tid; k < npairs; k += nt) {
-                int p, q;
-                rr_pair(k, r, mp, p, q);
-                double c = 1.0, s = 0.0;
-                if (q < m) {
-                    const double apq = A[p + q * m];
-                    const double app = A[p + p * m], aqq = A[q + q * m];
-                    if (apq != 0.0 && fabs(apq) > DBL_EPSILON * 0.5 * sqrt(fabs(app * aqq))) {
-                        const double tau = (aqq - app) / (2.0 * apq);
-                        const double t =
-                            (tau >= 0.0 ? 1.0 : -1.0) / (fabs(tau) + sqrt(1.0 + tau * tau));
-                        c = 1.0 / sqrt(1.0 + t * t);
-                        s = t * c;
-                        rotated = 1;
-                    }
-                }
-                cs_c[k] = c;
-                cs_s[k] = s;
-                cs_p[k] = p;
-                cs_q[k] = q;
-            }
-            __syncthreads();
-            // A <- A J, V <- V J (columns p, q)
-            for (int e = tid; e < npairs * m; e += nt) {
-                const int k = e / m, i = e % m;
-                const double s = cs_s[k];
-                if (s == 0.0) continue;
-                const double c = cs_c[k];
-                const int p = cs_p[k], q = cs_q[k];
-                const double aip = A[i + p * m], aiq = A[i + q * m];
-                A[i + p * m] = c * aip - s * aiq;
-                A[i + q * m] = s * aip + c * aiq;
-                const double vip = V[i + p * m], viq = V[i + q * m];
-                V[i + p * m] = c * vip - s * viq;
-                V[i + q * m] = s * vip + c * viq;
-            }
-            __syncthreads();
-            // A <- J^T A (rows p, q)
-            for (int e = tid; e < npairs * m; e += nt) {
-                const int k = e / m, cidx = e % m;
-                const double s = cs_s[k];
-                if (s == 0.0) continue;
-                const double c = cs_c[k];
-                const int p = cs_p[k], q = cs_q[k];
-                const double apc = A[p + cidx * m], aqc = A[q + cidx * m];
-                A[p + cidx * m] = c * apc - s * aqc;
-                A[q + cidx * m] = s * apc + c * aqc;
-            }
-            __syncthreads();
-        }
-        if (!__syncthreads_or(rotated)) break;
-    }
-    for (int i = tid; i < m; i += nt) {
-        const double di = A[i + i * m];
-        int rk = 0;
-        for (int j = 0; j < m; ++j) {
-            const double dj = A[j + j * m];
-            rk += (dj > di) || (dj == di && j < i);
-        }
-        rank_of[i] = rk;
-        vals[rk] = di;
-    }
-    __syncthreads();
-    for (int e = tid; e < m * m; e += nt) {
-        const int i = e % m, j = e / m;
-        W[i + rank_of[j] * m] = V[e];
-    }
-}
-
 // ---------------------------------------------------------------- two-sided Jacobi EVD, 2x2 blocks
 // Parallel cyclic Jacobi (round-robin pairs).  All m/2 rotations of a round act on
 // disjoint index pairs, so A' = J^T A J factors into independent 2x2 blocks

@@ -175,26 +175,10 @@ __global__ void __launch_bounds__(1024)
 // ---------------------------------------------------------------------------
 // Register-blocked variant (temporal blocking): each thread owns P consecutive grid
 // points and gathers a halo of S points per side from shared memory once per window
-// interval, then advances all S sub-steps in registers (valid region shrinking by one
-// point per side per sub-step).  One __syncthreads per interval instead of one per
-// sub-step; redundant halo work is 2S/P.  Radius-1 stencils (identity, upwind
-// advection, advection-diffusion).
+// interval, then applies all S sub-steps at once as one fused (2S+1)-tap stencil in
+// registers.  One __syncthreads per interval instead of one per sub-step; redundant halo
+// loads are 2S/P.  Radius-1 stencils (identity, upwind advection, advection-diffusion).
 // ---------------------------------------------------------------------------
-template <int KIND>
-__device__ __forceinline__ double tl3(double l, double c, double r, double cc, double dd) {
-    if (KIND == WC4DVAR_MODEL_IDENTITY) return c;
-    if (KIND == WC4DVAR_MODEL_ADVECTION) return c - cc * (c - l);
-    // x_j - C(x_j - x_{j-1}) + D(x_{j+1} - 2x_j + x_{j-1}) regrouped into three fp64 ops
-    // (coefficients are loop-invariant); differs from the expanded form by rounding only
-    return fma(dd, r, fma(cc + dd, l, (1.0 - cc - 2.0 * dd) * c));
-}
-template <int KIND>
-__device__ __forceinline__ double adj3(double l, double c, double r, double cc, double dd) {
-    if (KIND == WC4DVAR_MODEL_IDENTITY) return c;
-    if (KIND == WC4DVAR_MODEL_ADVECTION) return (1.0 - cc) * c + cc * r;
-    return fma(dd, l, fma(cc + dd, r, (1.0 - cc - 2.0 * dd) * c));
-}
-
 // SMEM state rows use a point-major ("transposed") layout: grid point j lives at
 // (j % P) * ntp + j / P, ntp = ceil(n / P).  Thread t owns points [tP, tP + P), so when a warp
 // reads its u-th halo/centre value the 32 addresses are consecutive -- conflict-free -- where
@@ -202,31 +186,8 @@ __device__ __forceinline__ double adj3(double l, double c, double r, double cc, 
 template <int P>
 __device__ __forceinline__ int pm_slot(int j, int ntp) { return (j % P) * ntp + j / P; }
 
-template <int KIND, int S, int P, bool ADJ>
-__device__ __forceinline__ void advance_interval(const double* __restrict__ cur, int b, int n, int ntp,
-                                                 double cc, double dd, double (&v)[P + 2 * S]) {
-    constexpr int L = P + 2 * S;
-    int j = (b - S) % n;
-    if (j < 0) j += n;
-#pragma unroll
-    for (int u = 0; u < L; ++u) {
-        v[u] = cur[pm_slot<P>(j, ntp)];
-        j = (j + 1 == n) ? 0 : j + 1;
-    }
-#pragma unroll
-    for (int k = 0; k < S; ++k) {
-        double prev = v[k];
-#pragma unroll
-        for (int u = k + 1; u < L - k - 1; ++u) {
-            const double c = v[u];
-            v[u] = ADJ ? adj3<KIND>(prev, c, v[u + 1], cc, dd) : tl3<KIND>(prev, c, v[u + 1], cc, dd);
-            prev = c;
-        }
-    }
-}
-
-// One interval as the fused (2S+1)-tap stencil (see StencilTaps); results land in
-// v[S .. S+P) like advance_interval's.
+// One interval as the fused (2S+1)-tap stencil (see StencilTaps, built by stencil_power from
+// the S-fold product of the 3-point step); results land in v[S .. S+P).
 template <int S, int P>
 __device__ __forceinline__ void conv_interval(const double* __restrict__ cur, int b, int n, int ntp,
                                               const StencilTaps& tp, double (&v)[P + 2 * S]) {
@@ -257,7 +218,6 @@ __global__ void __launch_bounds__(512)
     extern __shared__ double sm[];
     const int n = (int)md.n;
     const int N = md.N;
-    const double c = md.c, d = md.d;
     const int ntp = (n + P - 1) / P;  // point-major rows (see pm_slot)
     double* buf0 = sm;
     double* buf1 = sm + P * ntp;

@@ -75,24 +75,7 @@ __device__ __forceinline__ double stencil1(const double* __restrict__ u, const R
 }
 
 // Lorenz-96 Jacobian (models.cpp:92-102) and its transpose (models.cpp:105-116) at e,
-// with the stage x given as a global pointer indexed by grid point and the vector in SMEM.
-__device__ __forceinline__ double l96_jac(const double* __restrict__ x, const double* __restrict__ v,
-                                          const Region& rg, int e) {
-    const int g = rg.gidx(e);
-    const int gm2 = rg.wrap(g - 2), gm1 = rg.wrap(g - 1), gp1 = rg.wrap(g + 1);
-    const double vm2 = v[rg.nb(e, -2)], vm1 = v[rg.nb(e, -1)], vp1 = v[rg.nb(e, 1)], vc = v[e];
-    return -vm2 * x[gm1] - x[gm2] * vm1 + vm1 * x[gp1] + x[gm1] * vp1 - vc;
-}
-__device__ __forceinline__ double l96_jac_t(const double* __restrict__ x, const double* __restrict__ l,
-                                            const Region& rg, int e, double scale) {
-    const int g = rg.gidx(e);
-    const int gm2 = rg.wrap(g - 2), gm1 = rg.wrap(g - 1), gp1 = rg.wrap(g + 1), gp2 = rg.wrap(g + 2);
-    const double lp2 = scale * l[rg.nb(e, 2)], lp1 = scale * l[rg.nb(e, 1)];
-    const double lm1 = scale * l[rg.nb(e, -1)], lc = scale * l[e];
-    return -x[gp1] * lp2 + (x[gp2] - x[gm1]) * lp1 + x[gm2] * lm1 - lc;
-}
-
-// Same Jacobians with the stage vector staged in SMEM over the region.
+// with the stage vector staged in SMEM over the region.
 __device__ __forceinline__ double l96_jac_s(const double* __restrict__ x, const double* __restrict__ v,
                                             const Region& rg, int e) {
     const int em2 = rg.nb(e, -2), em1 = rg.nb(e, -1), ep1 = rg.nb(e, 1);
@@ -416,44 +399,11 @@ __global__ void __launch_bounds__(kThreads) tiled_adj_kernel(const TiledArgs ta,
 
 // ---------------------------------------------------------------- register-blocked tiles
 // Radius-1 models with S sub-steps per interval: each thread owns P consecutive region
-// points, gathers them with an S-point halo from SMEM once per interval and advances the
-// S sub-steps in registers (one barrier per interval instead of per sub-step).  Region
-// R = nt * P = T + 2 K S; the valid region shrinks by S per side per interval.
-template <int KIND>
-__device__ __forceinline__ double tl3t(double l, double c, double r, double cc, double dd) {
-    if (KIND == WC4DVAR_MODEL_IDENTITY) return c;
-    if (KIND == WC4DVAR_MODEL_ADVECTION) return c - cc * (c - l);
-    return fma(dd, r, fma(cc + dd, l, (1.0 - cc - 2.0 * dd) * c));  // 3 fp64 ops
-}
-template <int KIND>
-__device__ __forceinline__ double adj3t(double l, double c, double r, double cc, double dd) {
-    if (KIND == WC4DVAR_MODEL_IDENTITY) return c;
-    if (KIND == WC4DVAR_MODEL_ADVECTION) return (1.0 - cc) * c + cc * r;
-    return fma(dd, l, fma(cc + dd, r, (1.0 - cc - 2.0 * dd) * c));
-}
-
-template <int KIND, int S, int P, bool ADJ>
-__device__ __forceinline__ void blk_advance(const double* __restrict__ cur, int b, int R, int ns, double cc,
-                                            double dd, double (&v)[P + 2 * S]) {
-    constexpr int L = P + 2 * S;
-#pragma unroll
-    for (int u = 0; u < L; ++u) {
-        int j = b - S + u;
-        j = j < 0 ? 0 : (j >= R ? R - 1 : j);  // clamped lanes feed only discarded points
-        v[u] = cur[(j % P) * ns + j / P];       // point-major row, stride ns (see blk kernels)
-    }
-#pragma unroll
-    for (int k = 0; k < S; ++k) {
-        double prev = v[k];
-#pragma unroll
-        for (int u = k + 1; u < L - k - 1; ++u) {
-            const double c = v[u];
-            v[u] = ADJ ? adj3t<KIND>(prev, c, v[u + 1], cc, dd) : tl3t<KIND>(prev, c, v[u + 1], cc, dd);
-            prev = c;
-        }
-    }
-}
-
+// points, gathers them with an S-point halo from SMEM once per interval and applies the
+// S sub-steps in registers as one fused stencil (one barrier per interval instead of per
+// sub-step).  Region R = nt * P = T + 2 K S; the valid region shrinks by S per side per
+// interval.
+//
 // Gather P + 2S region values (clamped lanes feed only discarded points) and apply the fused
 // S-step stencil; results in v[S .. S+P).
 template <int S, int P>
@@ -479,7 +429,7 @@ __device__ __forceinline__ void blk_conv(const double* __restrict__ cur, int b, 
 }
 
 // SMEM rows of the blocked tiles are point-major with a padded stride ns = nt + 2: region
-// point e lives at (e % P) * ns + e / P.  Per-thread gathers (blk_advance) and the owner's
+// point e lives at (e % P) * ns + e / P.  Per-thread gathers (blk_conv) and the owner's
 // P results then hit 32 consecutive slots per warp (conflict-free), and the coalesced
 // row passes (loads, trajectory / state emits) see at most 2-way conflicts.
 __device__ __forceinline__ void cp8(double* dst, const double* src) {
@@ -724,7 +674,6 @@ bool launch_tiled_blk(const ModelDev& md, const NetDev& net, const SweepArgs& a,
 // around its points (LDS.128).  Exchange rows and stage buffers are double-buffered, so a
 // phase costs a single barrier while the next stage streams in by cp.async.  Arithmetic is
 // written in the same order as the SMEM kernels above (and the oracle).
-constexpr int kL96Threads = 512;
 constexpr int kL96P = 8;
 constexpr int kL96G = 0;  // (rows carry their guards inside the interleaved layout)
 
@@ -1056,7 +1005,6 @@ __global__ void __launch_bounds__(CB * NTC, 65536 / (CB * NTC * 128)) l96_blk_ad
     int pb = 0;
     for (int i = ta.i1 - 1; i >= ta.i0; --i) {
         for (int kk = 0; kk < s; ++kk) {
-            const int k = s - 1 - kk;
             // RK4 adjoint step (models.cpp:130-148)
             l96_publish<P, Lay::NTC>(ex + (pb * CB + cg) * LD + G, b, cur);
             L96_PHASE_SYNC();
