@@ -188,6 +188,56 @@ int wc4dvar_gpu_rayleigh_ritz(wc4dvar_op* op, const double* Z, int64_t ldz, int6
 int wc4dvar_gpu_last_sketch_timing(double* ms5);
 
 /* ------------------------------------------------------------------------- */
+/* Row-sharded building blocks (multi-GPU sketches)          */
+/* ------------------------------------------------------------------------- */
+/* The local halves of the dense steps of randevd.cpp for a ROW shard of the
+ * tall matrices; the caller all-reduces each m x m result across ranks
+ * (paper_2101_07249_b200/distributed.py) and runs the replicated small steps
+ * on every rank.  Same kernels as wc4dvar_gpu_sketch, so world size 1
+ * reproduces it.  Device pointers on `device`; stream as void* (NULL = the
+ * legacy default stream).  Sizes of the small factorizations: 1 <= m <= 512. */
+/* G (m1 x m2, ldg) = A^T B for A rows x m1, B rows x m2: the local Gram of
+ * householder_q / ColPivHouseholderQR (randevd.cpp:27-30,67), K = Z^T A Z
+ * (randevd.cpp:54) and Z^T E1 (randevd.cpp:95); fixed-order reduction. */
+int wc4dvar_gpu_la_gram_dev(int device, int64_t rows, int64_t m1, int64_t m2, const double* A,
+                            int64_t lda, const double* B, int64_t ldb, double* G, int64_t ldg,
+                            void* stream);
+/* C (rows x ncols) = A (rows x k) W (k x ncols): U = Z W (randevd.cpp:57,133),
+ * Y R^{-1} and F = E1 U^{-1} (randevd.cpp:105) with R^{-1} from tri_inv_upper.
+ * C must not alias A. */
+int wc4dvar_gpu_la_tall_times_small_dev(int device, int64_t rows, int64_t k, int64_t ncols,
+                                        const double* A, int64_t lda, const double* W,
+                                        int64_t ldw, double* C, int64_t ldc, void* stream);
+/* R = upper Cholesky factor of sym(G) (Eigen::LLT, randevd.cpp:96-102); status 2
+ * (NumericalError) when G is not positive definite. */
+int wc4dvar_gpu_la_chol_upper_dev(int device, int64_t m, const double* G, double* R, void* stream);
+/* Rinv = R^{-1} for upper-triangular R (triangular solve, randevd.cpp:105). */
+int wc4dvar_gpu_la_tri_inv_upper_dev(int device, int64_t m, const double* R, double* Rinv,
+                                     void* stream);
+/* Rank probe of ColPivHouseholderQR (randevd.cpp:67-73,89-92) as a diagonally
+ * pivoted Cholesky of the (all-reduced) Gram G: *rank (host) = pivots above
+ * tol_rel * max diag, perm (device, m int32) = pivot order. */
+int wc4dvar_gpu_la_pivoted_rank_dev(int device, int64_t m, const double* G, double tol_rel,
+                                    int64_t* rank, int32_t* perm, void* stream);
+/* sorted_symmetric_evd (randevd.cpp:37-43): values decreasing, W (m x m). */
+int wc4dvar_gpu_la_sym_evd_dev(int device, int64_t m, const double* K, double* vals, double* W,
+                               void* stream);
+/* Left singular vectors and values of a square X (BDCSVD thin U, randevd.cpp:106),
+ * sigma decreasing. */
+int wc4dvar_gpu_la_svd_left_dev(int device, int64_t m, const double* X, double* sigma, double* U,
+                                void* stream);
+/* C = alpha op(A) op(B) + beta C for small matrices (R2 R1, R3 R3^T of
+ * randevd.cpp:128); op = transpose when trans_* != 0. */
+int wc4dvar_gpu_la_small_gemm_dev(int device, int32_t trans_a, int32_t trans_b, int64_t M,
+                                  int64_t N, int64_t K, double alpha, const double* A, int64_t lda,
+                                  const double* B, int64_t ldb, double beta, double* C, int64_t ldc,
+                                  void* stream);
+/* out[:, j] = in[:, perm[j]], j < r: the pivoted Nystrom basis (randevd.cpp:89-92). */
+int wc4dvar_gpu_la_gather_cols_dev(int device, int64_t rows, int64_t r, const double* in,
+                                   int64_t ldi, const int32_t* perm, double* out, int64_t ldo,
+                                   void* stream);
+
+/* ------------------------------------------------------------------------- */
 /* Spectral LMP (lmp.hpp:12-28)                                               */
 /* ------------------------------------------------------------------------- */
 typedef struct wc4dvar_lmp wc4dvar_lmp;

@@ -5,24 +5,55 @@ CPU test ranks).  The data layout follows the path's natural sharding:
 
 * A*Omega shards by sketch COLUMNS with no communication (`column_range`): each rank
   applies the Hessian to its own columns (bench.py, weak scaling);
-* the tall-skinny algebra (CholQR2, Rayleigh-Ritz, Nystrom) works on ROW shards: an
-  all-to-all transposes column shards into row shards (`cols_to_rows` / `rows_to_cols`),
-  Gram matrices are summed with one all-reduce of m x m, the small factorizations are
+* the tall-skinny algebra of REVD, Nystrom and ritzit (randevd.cpp:47-136) works on ROW
+  shards: an all-to-all transposes column shards into row shards (`cols_to_rows` /
+  `rows_to_cols`), every Gram-type product is a local partial plus one all-reduce of an
+  m x m matrix, and the small factorizations (Cholesky, pivoted rank probe, EVD, SVD) are
   replicated on every rank;
 * PCG shards by rows with all-reduced dot products (`dist_pcg`).
 
-Local dense work goes through a `LocalOps` backend: `TorchOps` (torch tensors; used by the
-gloo CPU tests and as a reference) or the device library on GPU ranks.  The operator
-apply is a callback so each rank can use its own `HessianOperator` handle.
+Local dense work goes through an ops backend:
+
+* `DeviceOps` -- the library's own kernels (C-ABI "row-sharded building blocks",
+  include/wc4dvar_gpu.h) on the rank's GPU, on torch's current stream.  With one rank the
+  distributed methods run exactly the kernel sequence of `wc4dvar_gpu_sketch`.
+* `TorchOps` -- the same steps on torch tensors (float64), used by the gloo CPU tests.
+
+Tall matrices are torch tensors of shape (rows, cols) in COLUMN-major storage (strides
+(1, rows)), the layout of the C-ABI and of Eigen.  The operator apply is a callback so
+each rank can use its own `HessianOperator` handle (`hessian_apply_cols`).
 """
 from __future__ import annotations
 
+import ctypes
 import math
 from dataclasses import dataclass, field
 from typing import Callable, List, Optional
 
 import torch
 import torch.distributed as dist
+
+from .wc4dvar import NumericalError
+
+_EPS = 2.220446049250313e-16
+
+
+# ----------------------------------------------------------------------------- layout
+def fmat(rows: int, cols: int, like: torch.Tensor) -> torch.Tensor:
+    """Uninitialised column-major (rows x cols) tensor on like's device."""
+    return torch.empty((cols, rows), dtype=torch.float64, device=like.device).T
+
+
+def fcontig(t: torch.Tensor) -> torch.Tensor:
+    """Column-major contiguous copy of a 2-D tensor (no copy when it already is)."""
+    if t.dim() == 1:
+        t = t.reshape(-1, 1)
+    rows, cols = t.shape
+    if t.stride(0) == 1 and t.stride(1) == rows:
+        return t
+    if t.stride(0) == 1 and cols == 1:  # one dense column: restate its leading dimension
+        return t.as_strided((rows, 1), (1, max(rows, 1)))
+    return t.T.contiguous().T
 
 
 def column_range(m: int, world: int, rank: int):
@@ -36,41 +67,196 @@ def row_range(n: int, world: int, rank: int):
     return column_range(n, world, rank)
 
 
+def _world_rank():
+    if dist.is_available() and dist.is_initialized():
+        return dist.get_world_size(), dist.get_rank()
+    return 1, 0
+
+
+# ----------------------------------------------------------------------------- backends
 class TorchOps:
-    """Local dense kernels on torch tensors (float64)."""
+    """Local dense steps on torch tensors (float64); same contracts as DeviceOps."""
 
     @staticmethod
     def gram(A, B):
-        return A.T @ B
+        return fcontig(A.T @ B)
 
     @staticmethod
     def tall_times_small(A, W):
-        return A @ W
+        return fcontig(A @ W)
 
     @staticmethod
-    def chol_upper(G):
+    def chol_upper(G, what="cholqr"):
         G = 0.5 * (G + G.T)
         L, info = torch.linalg.cholesky_ex(G)
         if int(info) != 0:
-            raise RuntimeError(f"cholqr: Gram matrix not positive definite (pivot {int(info)})")
-        return L.T
+            raise NumericalError(f"{what}: matrix is not positive definite (pivot {int(info) - 1})")
+        return fcontig(L.T)
+
+    @staticmethod
+    def tri_inv_upper(R):
+        eye = torch.eye(R.shape[0], dtype=R.dtype, device=R.device)
+        return fcontig(torch.linalg.solve_triangular(R, eye, upper=True))
+
+    @staticmethod
+    def small_mm(A, B, ta=False, tb=False):
+        return fcontig((A.T if ta else A) @ (B.T if tb else B))
+
+    @staticmethod
+    def pivoted_rank(G, tol_rel):
+        """Diagonally pivoted Cholesky rank probe (the device rule of smallla.cu)."""
+        A = (0.5 * (G + G.T)).clone()
+        m = A.shape[0]
+        perm = list(range(m))
+        tol = tol_rel * float(torch.diagonal(A).max()) if m else 0.0
+        for j in range(m):
+            d = torch.diagonal(A)[j:]
+            p = j + int(torch.argmax(d))
+            best = float(A[p, p])
+            if not (best > tol) or not math.isfinite(best):
+                return j, torch.tensor(perm, dtype=torch.int32, device=G.device)
+            if p != j:
+                perm[j], perm[p] = perm[p], perm[j]
+                A[[j, p], :] = A[[p, j], :]
+                A[:, [j, p]] = A[:, [p, j]]
+            A[j, j] = math.sqrt(A[j, j])
+            A[j, j + 1:] /= A[j, j]
+            A[j + 1:, j + 1:] -= torch.outer(A[j, j + 1:], A[j, j + 1:])
+        return m, torch.tensor(perm, dtype=torch.int32, device=G.device)
 
     @staticmethod
     def eigh_desc(K):
         w, V = torch.linalg.eigh(0.5 * (K + K.T))
-        return torch.flip(w, [0]), torch.flip(V, [1])
+        return torch.flip(w, [0]).contiguous(), fcontig(torch.flip(V, [1]))
+
+    @staticmethod
+    def svd_left(X):
+        U, s, _ = torch.linalg.svd(X)
+        return s.contiguous(), fcontig(U)
+
+    @staticmethod
+    def gather_cols(Y, perm, r):
+        return fcontig(Y[:, perm[:r].long()])
 
 
+class DeviceOps:
+    """The library's kernels on this rank's GPU (include/wc4dvar_gpu.h, row-sharded
+    building blocks), issued on torch's current stream."""
+
+    def __init__(self, device: Optional[int] = None):
+        from . import wc4dvar as _w
+        self._w = _w
+        self.device = torch.cuda.current_device() if device is None else int(device)
+
+    def _st(self):
+        return ctypes.c_void_p(torch.cuda.current_stream(self.device).cuda_stream)
+
+    def _call(self, name, *args):
+        self._w._check(getattr(self._w.lib, name)(self.device, *args, self._st()))
+
+    def gram(self, A, B):
+        A, B = fcontig(A), fcontig(B)
+        G = fmat(A.shape[1], B.shape[1], A)
+        self._call("wc4dvar_gpu_la_gram_dev", A.shape[0], A.shape[1], B.shape[1], A.data_ptr(),
+                   max(A.stride(1), A.shape[0], 1), B.data_ptr(), max(B.stride(1), B.shape[0], 1),
+                   G.data_ptr(), max(A.shape[1], 1))
+        return G
+
+    def tall_times_small(self, A, W):
+        A, W = fcontig(A), fcontig(W)
+        C = fmat(A.shape[0], W.shape[1], A)
+        self._call("wc4dvar_gpu_la_tall_times_small_dev", A.shape[0], A.shape[1], W.shape[1],
+                   A.data_ptr(), max(A.shape[0], 1), W.data_ptr(), W.shape[0], C.data_ptr(),
+                   max(A.shape[0], 1))
+        return C
+
+    def chol_upper(self, G, what="cholqr"):
+        G = fcontig(G)
+        R = fmat(G.shape[0], G.shape[0], G)
+        try:
+            self._call("wc4dvar_gpu_la_chol_upper_dev", G.shape[0], G.data_ptr(), R.data_ptr())
+        except NumericalError as e:
+            raise NumericalError(f"{what}: {e}") from None
+        return R
+
+    def tri_inv_upper(self, R):
+        R = fcontig(R)
+        Ri = fmat(R.shape[0], R.shape[0], R)
+        self._call("wc4dvar_gpu_la_tri_inv_upper_dev", R.shape[0], R.data_ptr(), Ri.data_ptr())
+        return Ri
+
+    def small_mm(self, A, B, ta=False, tb=False):
+        A, B = fcontig(A), fcontig(B)
+        M = A.shape[1] if ta else A.shape[0]
+        K = A.shape[0] if ta else A.shape[1]
+        N = B.shape[0] if tb else B.shape[1]
+        C = fmat(M, N, A)
+        self._call("wc4dvar_gpu_la_small_gemm_dev", int(ta), int(tb), M, N, K, 1.0, A.data_ptr(),
+                   A.shape[0], B.data_ptr(), B.shape[0], 0.0, C.data_ptr(), M)
+        return C
+
+    def pivoted_rank(self, G, tol_rel):
+        G = fcontig(G)
+        m = G.shape[0]
+        perm = torch.empty(m, dtype=torch.int32, device=G.device)
+        r = ctypes.c_int64(0)
+        self._call("wc4dvar_gpu_la_pivoted_rank_dev", m, G.data_ptr(), float(tol_rel), ctypes.byref(r),
+                   perm.data_ptr())
+        return int(r.value), perm
+
+    def eigh_desc(self, K):
+        K = fcontig(K)
+        m = K.shape[0]
+        vals = torch.empty(m, dtype=torch.float64, device=K.device)
+        W = fmat(m, m, K)
+        self._call("wc4dvar_gpu_la_sym_evd_dev", m, K.data_ptr(), vals.data_ptr(), W.data_ptr())
+        return vals, W
+
+    def svd_left(self, X):
+        X = fcontig(X)
+        m = X.shape[0]
+        s = torch.empty(m, dtype=torch.float64, device=X.device)
+        U = fmat(m, m, X)
+        self._call("wc4dvar_gpu_la_svd_left_dev", m, X.data_ptr(), s.data_ptr(), U.data_ptr())
+        return s, U
+
+    def gather_cols(self, Y, perm, r):
+        Y = fcontig(Y)
+        out = fmat(Y.shape[0], r, Y)
+        self._call("wc4dvar_gpu_la_gather_cols_dev", Y.shape[0], r, Y.data_ptr(), max(Y.shape[0], 1),
+                   perm.data_ptr(), out.data_ptr(), max(Y.shape[0], 1))
+        return out
+
+
+def hessian_apply_cols(op) -> Callable[[torch.Tensor], torch.Tensor]:
+    """Column-block apply of a device operator handle on column-major CUDA tensors
+    (wc4dvar_gpu_op_apply_block_dev on torch's current stream; counts m applies)."""
+
+    def apply(X: torch.Tensor) -> torch.Tensor:
+        X = fcontig(X)
+        out = fmat(X.shape[0], X.shape[1], X)
+        if X.shape[1]:
+            op.apply_block_dev(X.T, out.T, ctypes.c_void_p(torch.cuda.current_stream().cuda_stream))
+        return out
+
+    return apply
+
+
+# ----------------------------------------------------------------------------- collectives
 def allreduce_sum(t: torch.Tensor) -> torch.Tensor:
-    if dist.is_available() and dist.is_initialized() and dist.get_world_size() > 1:
-        dist.all_reduce(t, op=dist.ReduceOp.SUM)
+    world, _ = _world_rank()
+    if world > 1:
+        t = t.contiguous() if t.dim() == 1 else fcontig(t)
+        flat = t.T if t.dim() == 2 else t  # row-major view of the same bytes
+        dist.all_reduce(flat, op=dist.ReduceOp.SUM)
     return t
 
 
 def all_gather_cat(t: torch.Tensor, sizes: List[int], dim: int = 0) -> torch.Tensor:
     """All-gather shards of unequal length along `dim` (padded to the largest, then trimmed;
     gloo requires equal sizes) and concatenate them in rank order."""
-    if not (dist.is_available() and dist.is_initialized()) or dist.get_world_size() == 1:
+    world, _ = _world_rank()
+    if world == 1:
         return t
     mx = max(sizes)
     pad_shape = list(t.shape)
@@ -91,8 +277,10 @@ def _alltoall(recv: List[torch.Tensor], send: List[torch.Tensor]) -> None:
         if r == rank:
             rv.copy_(sd)
             continue
-        ops.append(dist.P2POp(dist.isend, sd, r))
-        ops.append(dist.P2POp(dist.irecv, rv, r))
+        if sd.numel():
+            ops.append(dist.P2POp(dist.isend, sd, r))
+        if rv.numel():
+            ops.append(dist.P2POp(dist.irecv, rv, r))
     if ops:
         for w in dist.batch_isend_irecv(ops):
             w.wait()
@@ -100,67 +288,141 @@ def _alltoall(recv: List[torch.Tensor], send: List[torch.Tensor]) -> None:
 
 def cols_to_rows(Y_cols: torch.Tensor, n: int, m: int) -> torch.Tensor:
     """All-to-all transpose: this rank holds all n rows of its column shard; return all m
-    columns of its row shard.  Y_cols: (n, m_local) -> (n_local, m)."""
-    world = dist.get_world_size() if dist.is_initialized() else 1
-    rank = dist.get_rank() if dist.is_initialized() else 0
+    columns of its row shard.  Y_cols: (n, m_local) -> (n_local, m), column-major.
+    Messages travel as the row-major (cols, rows) image of each column-major block."""
+    world, rank = _world_rank()
     if world == 1:
-        return Y_cols
+        return fcontig(Y_cols)
     send = []
     for r in range(world):
         a, b = row_range(n, world, r)
-        send.append(Y_cols[a:b, :].contiguous())
-    recv = []
+        send.append(Y_cols[a:b, :].T.contiguous())
     ra, rb = row_range(n, world, rank)
+    recv = []
     for r in range(world):
         ca, cb = column_range(m, world, r)
-        recv.append(torch.empty((rb - ra, cb - ca), dtype=Y_cols.dtype, device=Y_cols.device))
+        recv.append(torch.empty((cb - ca, rb - ra), dtype=Y_cols.dtype, device=Y_cols.device))
     _alltoall(recv, send)
-    return torch.cat(recv, dim=1)
+    return torch.cat(recv, dim=0).T
 
 
 def rows_to_cols(Y_rows: torch.Tensor, n: int, m: int) -> torch.Tensor:
-    """Inverse of cols_to_rows: (n_local, m) -> (n, m_local)."""
-    world = dist.get_world_size() if dist.is_initialized() else 1
-    rank = dist.get_rank() if dist.is_initialized() else 0
+    """Inverse of cols_to_rows: (n_local, m) -> (n, m_local), column-major."""
+    world, rank = _world_rank()
     if world == 1:
-        return Y_rows
+        return fcontig(Y_rows)
     send = []
     for r in range(world):
         a, b = column_range(m, world, r)
-        send.append(Y_rows[:, a:b].contiguous())
+        send.append(Y_rows[:, a:b].T.contiguous())
     ca, cb = column_range(m, world, rank)
     recv = []
     for r in range(world):
         a, b = row_range(n, world, r)
-        recv.append(torch.empty((b - a, cb - ca), dtype=Y_rows.dtype, device=Y_rows.device))
+        recv.append(torch.empty((cb - ca, b - a), dtype=Y_rows.dtype, device=Y_rows.device))
     _alltoall(recv, send)
-    return torch.cat(recv, dim=0)
+    return torch.cat(recv, dim=1).T
 
 
-def dist_cholqr2(Y_rows: torch.Tensor, ops=TorchOps):
-    """Row-partitioned CholQR2: Gram all-reduce (m x m), replicated Cholesky, local Y R^{-1}.
-    Returns (Q_rows, R) with Y = Q R."""
-    G = allreduce_sum(ops.gram(Y_rows, Y_rows).contiguous())
-    R1 = ops.chol_upper(G)
-    Q1 = torch.linalg.solve_triangular(R1, Y_rows, upper=True, left=False)
-    G2 = allreduce_sum(ops.gram(Q1, Q1).contiguous())
-    R2 = ops.chol_upper(G2)
-    Q = torch.linalg.solve_triangular(R2, Q1, upper=True, left=False)
-    return Q, R2 @ R1
+# ----------------------------------------------------------------------------- sketches
+def dist_cholqr2(Y_rows: torch.Tensor, ops=TorchOps, G0: Optional[torch.Tensor] = None,
+                 want_r: bool = False, what: str = "cholqr"):
+    """Row-partitioned CholQR2 (replaces householder_q, randevd.cpp:27-30): Gram all-reduce
+    (m x m), replicated Cholesky and triangular inverse, local Y R^{-1}; twice.  G0 is an
+    already all-reduced Y^T Y.  Returns Q_rows, and R with Y = Q R when want_r."""
+    G = G0 if G0 is not None else allreduce_sum(ops.gram(Y_rows, Y_rows))
+    R1 = ops.chol_upper(G, what)
+    Q1 = ops.tall_times_small(Y_rows, ops.tri_inv_upper(R1))
+    G2 = allreduce_sum(ops.gram(Q1, Q1))
+    R2 = ops.chol_upper(G2, what)
+    Q = ops.tall_times_small(Q1, ops.tri_inv_upper(R2))
+    return (Q, ops.small_mm(R2, R1)) if want_r else Q
+
+
+def _rank_tol(n: int) -> float:
+    return 32.0 * math.sqrt(n) * _EPS  # sketch.cu rank_probe (DESIGN.md "Rank probe")
+
+
+def _apply_rows(apply_cols, Z_rows, n, m):
+    """A Z for row-sharded Z: rows -> cols, column-sharded apply, cols -> rows."""
+    return cols_to_rows(apply_cols(rows_to_cols(Z_rows, n, m)), n, m)
+
+
+def dist_rayleigh_ritz(apply_cols, Z_rows, n: int, keep: int, ops=TorchOps):
+    """rayleigh_ritz (randevd.cpp:47-60) on a row-sharded orthonormal Z."""
+    m = Z_rows.shape[1]
+    G = allreduce_sum(ops.gram(Z_rows, Z_rows))
+    eye = torch.eye(m, dtype=G.dtype, device=G.device)
+    if float((G - eye).abs().max()) > 1e-8:
+        raise NumericalError("rayleigh_ritz: Z is not orthonormal")
+    AZ_rows = _apply_rows(apply_cols, Z_rows, n, m)
+    K = allreduce_sum(ops.gram(Z_rows, AZ_rows))
+    vals, W = ops.eigh_desc(K)
+    return ops.tall_times_small(Z_rows, W[:, :keep]), vals[:keep].clone()
 
 
 def dist_revd(apply_cols: Callable[[torch.Tensor], torch.Tensor], omega_cols: torch.Tensor, n: int,
               m: int, k: int, ops=TorchOps):
-    """Distributed REVD (randevd.cpp:62-80): column-sharded applies, row-sharded CholQR2 and
-    Rayleigh-Ritz (randevd.cpp:47-60).  Returns (U_rows, theta) with U row-sharded."""
+    """Distributed REVD (randevd.cpp:62-80): column-sharded applies, row-sharded rank probe,
+    CholQR2 and Rayleigh-Ritz.  Transposes: 3.  Returns (U_rows, theta), U row-sharded."""
     Y_rows = cols_to_rows(apply_cols(omega_cols), n, m)
-    Z_rows, _ = dist_cholqr2(Y_rows, ops)
-    AZ_rows = cols_to_rows(apply_cols(rows_to_cols(Z_rows, n, m)), n, m)
-    K = allreduce_sum(ops.gram(Z_rows, AZ_rows).contiguous())
-    vals, W = ops.eigh_desc(K)
-    return ops.tall_times_small(Z_rows, W[:, :k]), vals[:k]
+    G = allreduce_sum(ops.gram(Y_rows, Y_rows))
+    r, _ = ops.pivoted_rank(G, _rank_tol(n))
+    if r < m:
+        raise NumericalError(f"revd: sample matrix rank collapsed to {r} of {m} columns")
+    Z_rows = dist_cholqr2(Y_rows, ops, G0=G,
+                          what="revd: sample matrix is numerically rank deficient (CholQR breakdown)")
+    return dist_rayleigh_ritz(apply_cols, Z_rows, n, k, ops)
 
 
+def dist_nystrom(apply_cols, omega_cols: torch.Tensor, n: int, m: int, k: int, ops=TorchOps):
+    """Distributed Nystrom (randevd.cpp:82-114): pivoted rank probe on the all-reduced Gram,
+    CholQR2 of the kept columns, E1 = A Z, E2 = Z^T E1 (all-reduced), Cholesky,
+    F = E1 U^{-1}, CholQR2(F) and the replicated SVD of R_F.  Transposes: 3."""
+    Y_rows = cols_to_rows(apply_cols(omega_cols), n, m)
+    G = allreduce_sum(ops.gram(Y_rows, Y_rows))
+    r, perm = ops.pivoted_rank(G, _rank_tol(n))
+    if r == 0:
+        raise NumericalError("nystrom: sample matrix is zero")
+    what = "nystrom: sample matrix is numerically rank deficient (CholQR breakdown)"
+    if r < m:
+        Z_rows = dist_cholqr2(ops.gather_cols(Y_rows, perm, r), ops, what=what)
+    else:
+        Z_rows = dist_cholqr2(Y_rows, ops, G0=G, what=what)
+    E1_rows = _apply_rows(apply_cols, Z_rows, n, r)
+    E2 = allreduce_sum(ops.gram(Z_rows, E1_rows))
+    Ru = ops.chol_upper(E2, "nystrom: Cholesky of Z^T A Z failed; the projected operator is "
+                            "numerically indefinite. Increase the oversampling parameter or use "
+                            "revd for indefinite spectra.")
+    F_rows = ops.tall_times_small(E1_rows, ops.tri_inv_upper(Ru))
+    QF_rows, RF = dist_cholqr2(F_rows, ops, want_r=True,
+                               what="nystrom: factor F is numerically rank deficient (CholQR breakdown)")
+    sig, W = ops.svd_left(RF)
+    keep = min(k, r)
+    return ops.tall_times_small(QF_rows, W[:, :keep]), (sig[:keep] * sig[:keep]).clone()
+
+
+def dist_ritzit(apply_cols, omega_rows: torch.Tensor, n: int, m: int, k: int, ops=TorchOps,
+                p_iter: int = 1):
+    """Distributed ritzit (randevd.cpp:116-136; p_iter > 1 is the BASELINE extension): the
+    sample is ROW-sharded from the start (QR(Omega) needs rows), so only 2 transposes per
+    apply.  Returns (U_rows, theta)."""
+    G3 = dist_cholqr2(omega_rows, ops, what="revd_ritzit: Gaussian sample is numerically rank deficient")
+    Y3 = _apply_rows(apply_cols, G3, n, m)
+    for _ in range(max(p_iter, 1) - 1):
+        G3 = dist_cholqr2(Y3, ops, what="revd_ritzit: QR of the sample matrix is rank deficient")
+        Y3 = _apply_rows(apply_cols, G3, n, m)
+    Z3, R3 = dist_cholqr2(Y3, ops, want_r=True, what="revd_ritzit: QR of the sample matrix is rank deficient")
+    d = torch.diagonal(R3).abs()
+    if float(d.min()) <= 1e-14 * float(d.max()):
+        raise NumericalError("revd_ritzit: QR of the sample matrix is rank deficient")
+    vals, W = ops.eigh_desc(ops.small_mm(R3, R3, tb=True))
+    if float(vals[min(k, m) - 1]) <= 0.0:
+        raise NumericalError("revd_ritzit: nonpositive squared Ritz value")
+    return ops.tall_times_small(Z3, W[:, :k]), torch.sqrt(vals[:k])
+
+
+# ----------------------------------------------------------------------------- PCG
 @dataclass
 class DistPcgResult:
     x_rows: torch.Tensor
@@ -171,13 +433,13 @@ class DistPcgResult:
 
 def dist_pcg(apply_rows: Callable[[torch.Tensor], torch.Tensor], b_rows: torch.Tensor,
              U_rows: Optional[torch.Tensor], theta: Optional[torch.Tensor], max_iter: int = 100,
-             rel_tol: float = 1e-6) -> DistPcgResult:
+             rel_tol: float = 1e-6, ops=TorchOps) -> DistPcgResult:
     """Row-sharded split PCG (krylov.cpp:22-99) with the compact-WY spectral LMP: every dot
-    product and every U^T v is one all-reduce of (k + 1) doubles."""
+    product and every U^T v of an iteration is one all-reduce of (k + 1) doubles."""
     k = 0 if U_rows is None else U_rows.shape[1]
     if k:
         c = 1.0 - 1.0 / torch.sqrt(theta)
-        S = allreduce_sum((U_rows.T @ U_rows).contiguous())
+        S = allreduce_sum(ops.gram(U_rows, U_rows))
         T = torch.zeros((k, k), dtype=b_rows.dtype, device=b_rows.device)
         for i in range(k):  # compact-WY recurrence (lmp_pcg.cuh)
             T[i, i] = c[i]
@@ -185,16 +447,16 @@ def dist_pcg(apply_rows: Callable[[torch.Tensor], torch.Tensor], b_rows: torch.T
                 T[:i, i] = -c[i] * (T[:i, :i] @ S[:i, i])
 
     def utv_dot(v, a=None):
-        parts = [U_rows.T @ v] if k else []
+        parts = [ops.gram(U_rows, v.reshape(-1, 1)).reshape(-1)] if k else []
         parts.append((a @ v).reshape(1) if a is not None else torch.zeros(1, dtype=v.dtype, device=v.device))
         red = allreduce_sum(torch.cat(parts).contiguous())
         return red[:k], red[k]
 
     def C(v, g):      # C v = v - U T (U^T v)
-        return v - U_rows @ (T @ g) if k else v.clone()
+        return v - ops.tall_times_small(U_rows, (T @ g).reshape(-1, 1)).reshape(-1) if k else v.clone()
 
     def Ct(v, g):     # C^T v = v - U T^T (U^T v)
-        return v - U_rows @ (T.T @ g) if k else v.clone()
+        return v - ops.tall_times_small(U_rows, (T.T @ g).reshape(-1, 1)).reshape(-1) if k else v.clone()
 
     x = torch.zeros_like(b_rows)
     g, _ = utv_dot(b_rows)
@@ -212,7 +474,7 @@ def dist_pcg(apply_rows: Callable[[torch.Tensor], torch.Tensor], b_rows: torch.T
         g, curv = utv_dot(w, p)
         curv = float(curv)
         if not math.isfinite(curv) or curv <= 0.0:
-            raise RuntimeError(f"pcg_split: p^T A p = {curv} at iteration {j}")
+            raise NumericalError(f"pcg_split: p^T A p = {curv} at iteration {j}")
         alpha = rho / curv
         x = x + alpha * p
         r = r - alpha * Ct(w, g)

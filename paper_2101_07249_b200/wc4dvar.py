@@ -109,6 +109,21 @@ SIGNATURES = {
                                               ctypes.POINTER(_i64), _vp]),
     "wc4dvar_gpu_rayleigh_ritz": (ctypes.c_int, [_vp, _dp, _i64, _i64, _dp, _i64, _dp]),
     "wc4dvar_gpu_last_sketch_timing": (ctypes.c_int, [_dp]),
+    "wc4dvar_gpu_la_gram_dev": (ctypes.c_int, [ctypes.c_int, _i64, _i64, _i64, _vp, _i64, _vp, _i64,
+                                               _vp, _i64, _vp]),
+    "wc4dvar_gpu_la_tall_times_small_dev": (ctypes.c_int, [ctypes.c_int, _i64, _i64, _i64, _vp, _i64,
+                                                           _vp, _i64, _vp, _i64, _vp]),
+    "wc4dvar_gpu_la_chol_upper_dev": (ctypes.c_int, [ctypes.c_int, _i64, _vp, _vp, _vp]),
+    "wc4dvar_gpu_la_tri_inv_upper_dev": (ctypes.c_int, [ctypes.c_int, _i64, _vp, _vp, _vp]),
+    "wc4dvar_gpu_la_pivoted_rank_dev": (ctypes.c_int, [ctypes.c_int, _i64, _vp, ctypes.c_double,
+                                                       ctypes.POINTER(_i64), _vp, _vp]),
+    "wc4dvar_gpu_la_sym_evd_dev": (ctypes.c_int, [ctypes.c_int, _i64, _vp, _vp, _vp, _vp]),
+    "wc4dvar_gpu_la_svd_left_dev": (ctypes.c_int, [ctypes.c_int, _i64, _vp, _vp, _vp, _vp]),
+    "wc4dvar_gpu_la_small_gemm_dev": (ctypes.c_int, [ctypes.c_int, ctypes.c_int32, ctypes.c_int32, _i64,
+                                                     _i64, _i64, ctypes.c_double, _vp, _i64, _vp, _i64,
+                                                     ctypes.c_double, _vp, _i64, _vp]),
+    "wc4dvar_gpu_la_gather_cols_dev": (ctypes.c_int, [ctypes.c_int, _i64, _i64, _vp, _i64, _vp, _vp,
+                                                      _i64, _vp]),
     "wc4dvar_gpu_lmp_build": (ctypes.c_int, [_i64, _i64, _dp, _i64, _dp, ctypes.c_int, ctypes.POINTER(_vp)]),
     "wc4dvar_gpu_lmp_build_dev": (ctypes.c_int, [_i64, _i64, _vp, _i64, _vp, ctypes.c_int, ctypes.POINTER(_vp)]),
     "wc4dvar_gpu_lmp_destroy": (ctypes.c_int, [_vp]),

@@ -1,7 +1,8 @@
 """World-size-2 gloo tests (CPU) of the multi-GPU host logic: column-sharded A*Omega,
-the all-to-all column<->row transposes, row-sharded CholQR2 / REVD with all-reduced Gram
-matrices and row-sharded PCG with all-reduced dots -- each against the single-process
-oracle on the same inputs."""
+the all-to-all column<->row transposes, row-sharded CholQR2 / REVD / Nystrom / ritzit with
+all-reduced Gram matrices and row-sharded PCG with all-reduced dots -- each against the
+single-process oracle on the same inputs (TorchOps backend; the device backend is
+tests/test_gpu_distributed.py)."""
 import os
 import socket
 
@@ -61,12 +62,19 @@ def _body_transposes(rank, world):
     assert torch.equal(back, full[:, a:b])
 
 
+def _spd_case():
+    from oracle import oracle as O
+    n_ = 80
+    A = O.random_spd(np.concatenate([np.linspace(40, 5, 10), np.linspace(2, 1, n_ - 10)]), 3)
+    return n_, A
+
+
 def _body_revd_pcg(rank, world):
     from oracle import oracle as O
     from paper_2101_07249_b200.distributed import (all_gather_cat, column_range, dist_cholqr2, dist_pcg,
                                                    dist_revd, row_range)
-    n_, k, l = 80, 6, 4
-    A = O.random_spd(np.concatenate([np.linspace(40, 5, 10), np.linspace(2, 1, n_ - 10)]), 3)
+    n_, A = _spd_case()
+    k, l = 6, 4
     m = k + l
     Om = O.gaussian_matrix(n_, m, 5)
     a, b = column_range(m, world, rank)
@@ -78,17 +86,19 @@ def _body_revd_pcg(rank, world):
     # U is row-sharded; gather and compare the projector
     ra, rb = row_range(n_, world, rank)
     rsz = [row_range(n_, world, r)[1] - row_range(n_, world, r)[0] for r in range(world)]
-    U = all_gather_cat(U_rows, rsz).numpy()
+    U = all_gather_cat(U_rows.contiguous(), rsz).numpy()
     assert np.abs(U @ U.T - ref.vectors @ ref.vectors.T).max() <= 1e-8
-    # CholQR2 orthonormality on row shards
-    Q, R = dist_cholqr2(torch.from_numpy(Om[ra:rb, :].copy()))
-    G = Q.T @ Q
+    # CholQR2 orthonormality and Y = Q R on row shards
+    Y = torch.from_numpy(Om[ra:rb, :].copy())
+    Q, R = dist_cholqr2(Y, want_r=True)
+    G = (Q.T @ Q).contiguous()
     dist.all_reduce(G)
     assert (G - torch.eye(m, dtype=torch.float64)).abs().max() <= 1e-13
+    assert (Q @ R - Y).abs().max() <= 1e-13 * Y.abs().max()
     # row-sharded PCG with the LMP vs the oracle
     b = O.NormalStream(2).draw(n_)
 
-    def apply_rows(p_rows):  # gather-apply-slice stand-in for the halo-exchange apply
+    def apply_rows(p_rows):  # replicated apply: gather p, apply, keep the own rows
         return (At @ all_gather_cat(p_rows, rsz))[ra:rb]
 
     res = dist_pcg(apply_rows, torch.from_numpy(b[ra:rb].copy()), U_rows, theta, 200, 1e-10)
@@ -98,7 +108,56 @@ def _body_revd_pcg(rank, world):
     assert np.abs(x - oref.x).max() <= 1e-9 * np.abs(oref.x).max()
 
 
-@pytest.mark.parametrize("body", ["_body_sharded_apply", "_body_transposes", "_body_revd_pcg"])
+def _gather_rows(U_rows, n_, world):
+    from paper_2101_07249_b200.distributed import all_gather_cat, row_range
+    rsz = [row_range(n_, world, r)[1] - row_range(n_, world, r)[0] for r in range(world)]
+    return all_gather_cat(U_rows.contiguous(), rsz).numpy()
+
+
+def _body_nystrom_ritzit(rank, world):
+    from oracle import oracle as O
+    from paper_2101_07249_b200.distributed import column_range, dist_nystrom, dist_ritzit, row_range
+    n_, A = _spd_case()
+    At = torch.from_numpy(A)
+    apply_cols = lambda X: At @ X  # noqa: E731
+    k, l = 6, 4
+    m = k + l
+    a, b = column_range(m, world, rank)
+    ra, rb = row_range(n_, world, rank)
+    for seed in (5, 6):
+        Om = O.gaussian_matrix(n_, m, seed)
+        U_rows, theta = dist_nystrom(apply_cols, torch.from_numpy(Om[:, a:b].copy()), n_, m, k)
+        ref = O.nystrom(O.DenseOperator(A), O.SketchConfig(k, l, seed, "nystrom"), Om)
+        assert np.abs(theta.numpy() - ref.values).max() <= 1e-10 * ref.values.max()
+        U = _gather_rows(U_rows, n_, world)
+        assert np.abs(U @ U.T - ref.vectors @ ref.vectors.T).max() <= 1e-8
+        for p_iter in (1, 3):
+            U_rows, theta = dist_ritzit(apply_cols, torch.from_numpy(Om[ra:rb, :].copy()), n_, m, k,
+                                        p_iter=p_iter)
+            ref = O.revd_ritzit(O.DenseOperator(A), O.SketchConfig(k, l, seed, "ritzit", p_iter), Om)
+            assert np.abs(theta.numpy() - ref.values).max() <= 1e-10 * ref.values.max()
+            U = _gather_rows(U_rows, n_, world)
+            assert np.abs(U @ U.T - ref.vectors @ ref.vectors.T).max() <= 1e-8
+
+
+def _body_nystrom_rank_cap(rank, world):
+    # test_randevd.cpp:153-168: a rank-3 operator; Nystrom caps k at the detected rank
+    from oracle import oracle as O
+    from paper_2101_07249_b200.distributed import column_range, dist_nystrom
+    n_ = 50
+    V = O.random_orthogonal(n_, 7)[:, :3]
+    A = V @ np.diag([5.0, 3.0, 2.0]) @ V.T
+    At = torch.from_numpy(A)
+    m = 8
+    a, b = column_range(m, world, rank)
+    Om = O.gaussian_matrix(n_, m, 11)
+    U_rows, theta = dist_nystrom(lambda X: At @ X, torch.from_numpy(Om[:, a:b].copy()), n_, m, 6)
+    assert theta.numel() == 3
+    assert np.abs(np.sort(theta.numpy())[::-1] - [5.0, 3.0, 2.0]).max() <= 1e-10 * 5.0
+
+
+@pytest.mark.parametrize("body", ["_body_sharded_apply", "_body_transposes", "_body_revd_pcg",
+                                  "_body_nystrom_ritzit", "_body_nystrom_rank_cap"])
 def test_world_size_2_gloo(body):
     _run(body, 2)
 

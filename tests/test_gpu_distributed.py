@@ -1,0 +1,102 @@
+"""Device backend of the multi-GPU sketches (paper_2101_07249_b200/distributed.py DeviceOps
+over the C-ABI row-sharded building blocks), on one rank: the distributed REVD / Nystrom /
+ritzit run the same kernel sequence as wc4dvar_gpu_sketch, so their Ritz pairs must be
+bitwise identical to it; row-sharded PCG must match pcg_split (iterations within one,
+solution 1e-9 relative).  The N>1 exchange logic is covered by the gloo tests
+(tests/test_distributed.py)."""
+import numpy as np
+import pytest
+import torch
+
+from oracle import oracle as O
+
+pytestmark = pytest.mark.gpu
+
+W = pytest.importorskip("paper_2101_07249_b200")
+from gpu_helpers import workload_pair  # noqa: E402
+from paper_2101_07249_b200 import configs  # noqa: E402
+from paper_2101_07249_b200 import distributed as D  # noqa: E402
+
+
+def _dev(a):
+    return D.fcontig(torch.from_numpy(np.asfortranarray(a)).cuda())
+
+
+def _ops_case():
+    wl = configs.config1()
+    g, _ = workload_pair(wl)
+    return wl, g
+
+
+@pytest.mark.parametrize("method", ["revd", "nystrom", "ritzit"])
+def test_device_ops_match_single_gpu_sketch_bitwise(method):
+    wl, g = _ops_case()
+    n, k, m = g.dim(), wl.k, wl.m
+    Om = W.gaussian_matrix(n, m, configs.OMEGA_SEED)
+    ops = D.DeviceOps(0)
+    apply_cols = D.hessian_apply_cols(g)
+    if method == "revd":
+        U, th = D.dist_revd(apply_cols, _dev(Om), n, m, k, ops)
+    elif method == "nystrom":
+        U, th = D.dist_nystrom(apply_cols, _dev(Om), n, m, k, ops)
+    else:
+        U, th = D.dist_ritzit(apply_cols, _dev(Om), n, m, k, ops, p_iter=1)
+    torch.cuda.synchronize()
+    ref = W.sketch_eigenpairs(g, W.SketchConfig(k, m - k, configs.OMEGA_SEED, method), Om)
+    assert np.array_equal(th.cpu().numpy(), ref.values)
+    assert np.array_equal(U.cpu().numpy(), ref.vectors)
+
+
+def test_device_ops_building_blocks_vs_torch():
+    rng = np.random.default_rng(3)
+    Y = rng.standard_normal((1001, 37))
+    Yd = _dev(Y)
+    dev, cpu = D.DeviceOps(0), D.TorchOps
+    Yc = D.fcontig(torch.from_numpy(Y))
+    G = dev.gram(Yd, Yd)
+    assert np.abs(G.cpu().numpy() - Y.T @ Y).max() <= 1e-12 * np.abs(Y.T @ Y).max()
+    R = dev.chol_upper(G)
+    Rc = cpu.chol_upper(D.fcontig(G.cpu()))
+    assert np.abs(R.cpu().numpy() - Rc.numpy()).max() <= 1e-12 * np.abs(Rc.numpy()).max()
+    Ri = dev.tri_inv_upper(R)
+    Q = dev.tall_times_small(Yd, Ri)
+    Qc = Yc @ cpu.tri_inv_upper(Rc)
+    assert np.abs(Q.cpu().numpy() - Qc.numpy()).max() <= 1e-11
+    K = dev.small_mm(R, R, tb=True)
+    assert np.abs(K.cpu().numpy() - (Rc @ Rc.T).numpy()).max() <= 1e-12 * float((Rc @ Rc.T).abs().max())
+    vals, V = dev.eigh_desc(K)
+    vc, _ = cpu.eigh_desc(D.fcontig(K.cpu()))
+    assert np.abs(vals.cpu().numpy() - vc.numpy()).max() <= 1e-10 * float(vc.abs().max())
+    s, U = dev.svd_left(R)
+    sc, _ = cpu.svd_left(D.fcontig(R.cpu()))
+    assert np.abs(s.cpu().numpy() - sc.numpy()).max() <= 1e-10 * float(sc.max())
+    # pivoted rank probe on a rank-5 Gram: same rank and pivot order as the torch rule
+    Z = rng.standard_normal((300, 5)) @ rng.standard_normal((5, 12))
+    Gz = _dev(Z.T @ Z)
+    r, perm = dev.pivoted_rank(Gz, 32 * np.sqrt(300) * 2.2e-16)
+    rc, permc = cpu.pivoted_rank(D.fcontig(Gz.cpu()), 32 * np.sqrt(300) * 2.2e-16)
+    assert r == rc == 5
+    assert perm.cpu().tolist()[:5] == permc.tolist()[:5]
+    Sel = dev.gather_cols(_dev(Z), perm, r)
+    assert np.array_equal(Sel.cpu().numpy(), Z[:, perm.cpu().numpy()[:5]])
+
+
+def test_device_ops_errors_are_typed():
+    ops = D.DeviceOps(0)
+    bad = _dev(-np.eye(4))
+    with pytest.raises(W.NumericalError):
+        ops.chol_upper(bad)
+
+
+def test_row_sharded_pcg_device_ops_vs_pcg_split():
+    wl, g = _ops_case()
+    n, k, m = g.dim(), wl.k, wl.m
+    pr = W.sketch_eigenpairs(g, W.SketchConfig(k, m - k, configs.OMEGA_SEED, "nystrom"))
+    b = O.NormalStream(configs.RHS_SEED).draw(n)
+    ref = W.pcg_split(g, b, W.build_spectral_lmp(pr), None, W.PcgOptions(200, 1e-8))
+    apply_cols = D.hessian_apply_cols(g)
+    res = D.dist_pcg(lambda p: apply_cols(p.reshape(-1, 1)).reshape(-1), _dev(b).reshape(-1),
+                     _dev(pr.vectors), torch.from_numpy(pr.values).cuda(), 200, 1e-8, ops=D.DeviceOps(0))
+    assert res.converged and abs(res.iterations - ref.history.iterations) <= 1
+    x = res.x_rows.cpu().numpy()
+    assert np.abs(x - ref.x).max() <= 1e-9 * np.abs(ref.x).max()
