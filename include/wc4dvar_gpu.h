@@ -211,6 +211,11 @@ int wc4dvar_gpu_la_tall_times_small_dev(int device, int64_t rows, int64_t k, int
 /* R = upper Cholesky factor of sym(G) (Eigen::LLT, randevd.cpp:96-102); status 2
  * (NumericalError) when G is not positive definite. */
 int wc4dvar_gpu_la_chol_upper_dev(int device, int64_t m, const double* G, double* R, void* stream);
+/* R = chol_upper(G) and Rinv = R^{-1} in one call (the CholQR step of
+ * householder_q, randevd.cpp:27-30, and the LLT + triangular solve of
+ * randevd.cpp:97-105); status 2 as chol_upper.  R may alias G. */
+int wc4dvar_gpu_la_chol_inv_upper_dev(int device, int64_t m, const double* G, double* R,
+                                      double* Rinv, void* stream);
 /* Rinv = R^{-1} for upper-triangular R (triangular solve, randevd.cpp:105). */
 int wc4dvar_gpu_la_tri_inv_upper_dev(int device, int64_t m, const double* R, double* Rinv,
                                      void* stream);

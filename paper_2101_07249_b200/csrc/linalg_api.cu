@@ -113,6 +113,21 @@ int wc4dvar_gpu_la_chol_upper_dev(int device, int64_t m, const double* G, double
     W4_LA_END
 }
 
+int wc4dvar_gpu_la_chol_inv_upper_dev(int device, int64_t m, const double* G, double* R,
+                                      double* Rinv, void* stream) {
+    W4_LA_BEGIN
+    require(m >= 1 && m <= 512, "chol_inv_upper: m must be in [1, 512]");
+    DeviceGuard g(device);
+    auto st = static_cast<cudaStream_t>(stream);
+    Scratch& s = scratch(device);
+    int* info = s.ints.get<int>(4);
+    chol_inv_upper((int)m, G, R, Rinv, info, s.small, st);
+    const int bad = read_int(s, info, st);
+    if (bad) throw NumericalError("chol_inv_upper: matrix is not positive definite (pivot " +
+                                  std::to_string(bad - 1) + ")");
+    W4_LA_END
+}
+
 int wc4dvar_gpu_la_tri_inv_upper_dev(int device, int64_t m, const double* R, double* Rinv,
                                      void* stream) {
     W4_LA_BEGIN

@@ -176,7 +176,7 @@ void launch_pass(const RowPassCtx& c, const PassArgs& a, cudaStream_t st) {
     const int RB = pick_rb(c.k);
     const size_t smem = sizeof(double) * ((size_t)c.k * (RB + 1) + RB + c.k);
     auto kern = rowpass_kernel<MODE>;
-    if (smem > 48 * 1024)
+    if (smem + 1024 > 48 * 1024)  // + the kernel's static reduction scratch
         W4_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     const int64_t grid = cdiv(c.n, RB);
     kern<<<(unsigned)grid, kBlock, smem, st>>>(c, a, RB);

@@ -133,18 +133,16 @@ struct Ctx {
         double* R1 = buf(P_R1, m * m);
         double* R1i = buf(P_R1I, m * m);
         int* info = reinterpret_cast<int*>(buf(P_INT, 4 + 2 * m));
-        chol_upper((int)m, G, R1, info, pool[P_SMALLWS], st);
+        chol_inv_upper((int)m, G, R1, R1i, info, pool[P_SMALLWS], st);
         if (read_int(info)) return false;
-        tri_inv_upper((int)m, R1, R1i, st);
         double* Q1 = buf(P_Q1, n * m);
         tall_times_small(Y, m, R1i, m, m, Q1, n);
         double* G2 = buf(P_G2, m * m);
         gram(Q1, m, Q1, m, G2);
         double* R2 = buf(P_R2, m * m);
         double* R2i = buf(P_R2I, m * m);
-        chol_upper((int)m, G2, R2, info, pool[P_SMALLWS], st);
+        chol_inv_upper((int)m, G2, R2, R2i, info, pool[P_SMALLWS], st);
         if (read_int(info)) return false;
-        tri_inv_upper((int)m, R2, R2i, st);
         tall_times_small(Q1, m, R2i, m, m, Q, n);
         if (R_out) small_gemm(false, false, (int)m, (int)m, (int)m, 1.0, R2, (int)m, R1, (int)m, 0.0,
                               R_out, (int)m, st);
@@ -276,13 +274,12 @@ int64_t sketch_dev(wc4dvar_op& op, const wc4dvar_sketch_config& cfg, const doubl
         double* Ru = c.buf(P_R1, r * r);
         double* Rui = c.buf(P_R1I, r * r);
         int* info = reinterpret_cast<int*>(c.buf(P_INT, 4 + 2 * m));
-        chol_upper((int)r, E2, Ru, info, op.pool[P_SMALLWS], st);  // sym(E2), randevd.cpp:96-97
+        chol_inv_upper((int)r, E2, Ru, Rui, info, op.pool[P_SMALLWS], st);  // sym(E2), randevd.cpp:96-97
         if (c.read_int(info))
             throw NumericalError(
                 "nystrom: Cholesky of Z^T A Z failed; the projected operator is numerically "
                 "indefinite. Increase the oversampling parameter or use revd for indefinite "
                 "spectra.");
-        tri_inv_upper((int)r, Ru, Rui, st);
         tm.begin(T_GEMM);
         double* F = c.buf(P_F, n * r);
         c.tall_times_small(E1, r, Rui, r, r, F, n);  // F = E1 U^{-1}, randevd.cpp:104-105

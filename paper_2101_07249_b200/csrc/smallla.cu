@@ -1,6 +1,7 @@
 // Single-CTA dense kernels on the (k+l)-dimension (see smallla.cuh).
 #include "smallla.cuh"
 
+#include <algorithm>
 #include <cfloat>
 #include <cstdio>
 #include <cstdlib>
@@ -62,6 +63,154 @@ __global__ void __launch_bounds__(kThreads)
             R[e] = (c >= r) ? A[c + r * m] : 0.0;
         }
     if (tid == 0) *info = fail;
+}
+
+// ---------------------------------------------------------------- Cholesky + inverse, fused
+// R (upper, R^T R = sym(G)) and R^{-1} in one pass for m <= 128: symmetric Gaussian
+// elimination of the augmented rows [G | I].  Step j subtracts m_ij = A(i,j) / A(j,j) times
+// pivot row j from every row i > j, on the trailing lower triangle of A (the Schur
+// complement) and on the lower triangle of X (which ends as L_unit^{-1}); then
+// L = L_unit D^{1/2}, L^{-1} = D^{-1/2} L_unit^{-1}, R = L^T, R^{-1} = L^{-T}.
+// Row i needs only i + 1 slots: slot c holds A(i,c) while c > j and X(i,c) once c <= j (the
+// A entry retires, as pivot-column value, at exactly the step its X entry is born), so
+// every update is v_c <- (c == j ? 0 : v_c) - m_ij p_c with p the compact pivot row
+// [X(j, 0..j-1), 1, A(j+1..m-1, j)].  Slots live in registers of fixed owners (TPR threads
+// per row, slot c at lane c % TPR); p is published to a double-buffered SMEM vector by its
+// owners, so a step costs one barrier and at most NE FMAs per thread, instead of the two
+// barriers and SMEM read-modify-writes of chol_kernel + tri_inv.
+template <int TPR, int NP>
+__global__ void __launch_bounds__(TPR * 128 < 1024 ? TPR * 128 : 1024)
+    chol_inv_reg_kernel(int m, const double* __restrict__ G, double* __restrict__ R,
+                        double* __restrict__ Rinv, int* info) {
+    static_assert((NP & (NP - 1)) == 0, "NP must be a power of two");
+    constexpr int SPAN = 2 * TPR;  // slots per register pair across a row's TPR threads
+    __shared__ __align__(16) double pv[2][128];
+    __shared__ double pd[2][2], rl_s[128];  // pd[b] = {sqrt(d_j), 1 / sqrt(d_j)}
+    __shared__ int fail;
+    const int tid = threadIdx.x;
+    const int i = tid / TPR, lane = tid % TPR;
+    const bool row_ok = i < m;
+    const int c0 = 2 * lane;
+    // Register pair s holds slots c0 + SPAN * ((s + k) % NP) + {0, 1} after k rotations: the
+    // pair whose slots transition in the current block of SPAN steps is always v[0], so every
+    // register index below is static.  Slots c > i are never read (no masks in the update).
+    double v[NP][2];
+#pragma unroll
+    for (int s = 0; s < NP; ++s)
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            const int c = c0 + SPAN * s + h;
+            v[s][h] = (row_ok && c <= i) ? 0.5 * (G[i + (size_t)c * m] + G[c + (size_t)i * m]) : 0.0;
+        }
+    // The owner of the next pivot publishes its square root and reciprocal, so the sqrt /
+    // division latency overlaps the other threads' updates.  A non-positive or non-finite
+    // pivot publishes rl = NaN (every thread then sees the same breakdown).
+    auto publish_pivot = [&](int b, double d) {
+        const bool ok = d > 0.0 && isfinite(d);
+        const double l = ok ? sqrt(d) : 0.0;
+        pd[b][0] = l;
+        pd[b][1] = ok ? 1.0 / l : __longlong_as_double(0x7ff8000000000000ll);
+    };
+    if (row_ok && lane == 0) {  // pivot row of step 0: p = [1, A(1..m-1, 0)], d = A(0, 0)
+        if (i == 0) {
+            pv[0][0] = 1.0;
+            publish_pivot(0, v[0][0]);
+        } else {
+            pv[0][i] = v[0][0];
+        }
+    }
+    if (tid == 0) fail = 0;
+    __syncthreads();  // G fully read: R / Rinv may alias it from here on
+    for (int e = tid; e < m * m; e += blockDim.x) {
+        const int r = e % m, c = e / m;
+        if (r > c) {
+            R[e] = 0.0;
+            Rinv[e] = 0.0;
+        }
+    }
+    int f = 0, k = 0;
+    for (int jb = 0; jb < m && !f; jb += SPAN, ++k) {
+#pragma unroll
+        for (int u = 0; u < SPAN; ++u) {
+            const int j = jb + u;
+            if (j >= m) break;
+            const int b = j & 1;
+            const double ljj = pd[b][0], rl = pd[b][1];
+            if (rl != rl) {  // NaN: breakdown at pivot j (uniform)
+                f = j + 1;
+                break;
+            }
+            if (tid == 0) rl_s[j] = rl;
+            if (row_ok && i >= j) {
+                const double aij = pv[b][i];
+                if (lane == 0) R[j + (size_t)i * m] = (i == j) ? ljj : aij * rl;
+                if (i > j) {
+                    const double mi = aij * (rl * rl);
+                    // slot j (v[0][u & 1] of lane u / 2) turns from A(i, j) into X(i, j)
+                    if (lane == (u >> 1)) v[0][u & 1] = 0.0;
+#pragma unroll
+                    for (int s = 0; s < NP; ++s) {
+                        const int c = c0 + SPAN * ((s + k) & (NP - 1));
+                        const double2 p2 = *reinterpret_cast<const double2*>(&pv[b][c]);
+                        v[s][0] = fma(-mi, p2.x, v[s][0]);
+                        v[s][1] = fma(-mi, p2.y, v[s][1]);
+                    }
+                    // publish the pivot row of step j + 1 into the other buffer
+                    const int jn = j + 1;
+                    if (i == jn) {  // X(jn, 0..j)
+#pragma unroll
+                        for (int s = 0; s < NP; ++s)
+#pragma unroll
+                            for (int h = 0; h < 2; ++h) {
+                                const int c = c0 + SPAN * ((s + k) & (NP - 1)) + h;
+                                if (c <= j) pv[b ^ 1][c] = v[s][h];
+                            }
+                    }
+                    // slot jn: v[0][(u + 1) & 1] of lane (u + 1) / 2, or v[1][0] of lane 0
+                    const int ln = (u + 1 < SPAN) ? ((u + 1) >> 1) : 0;
+                    if (lane == ln) {
+                        const double x = (u + 1 < SPAN) ? v[0][(u + 1) & 1] : v[1 % NP][0];
+                        if (i == jn) {
+                            pv[b ^ 1][jn] = 1.0;
+                            publish_pivot(b ^ 1, x);
+                        } else {
+                            pv[b ^ 1][i] = x;
+                        }
+                    }
+                }
+            }
+            __syncthreads();
+        }
+        // rotate: the finished pair moves to the back, the next block's pair to v[0]
+        double t0 = v[0][0], t1 = v[0][1];
+#pragma unroll
+        for (int s = 0; s + 1 < NP; ++s) {
+            v[s][0] = v[s + 1][0];
+            v[s][1] = v[s + 1][1];
+        }
+        v[NP - 1][0] = t0;
+        v[NP - 1][1] = t1;
+    }
+    if (tid == 0) {
+        fail = f;
+        *info = f;
+    }
+    __syncthreads();
+    if (fail || !row_ok) return;
+    const double ri = rl_s[i];
+#pragma unroll
+    for (int s = 0; s < NP; ++s)
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            const int c = c0 + SPAN * ((s + k) & (NP - 1)) + h;
+            if (c <= i) Rinv[c + (size_t)i * m] = (c == i ? 1.0 : v[s][h]) * ri;
+        }
+}
+
+template <int TPR, int NP>
+void launch_chol_inv(int m, const double* G, double* R, double* Rinv, int* info, cudaStream_t st) {
+    chol_inv_reg_kernel<TPR, NP><<<1, TPR * m, 0, st>>>(m, G, R, Rinv, info);
+    W4_LAUNCH();
 }
 
 // ---------------------------------------------------------------- pivoted Cholesky rank
@@ -704,7 +853,11 @@ __global__ void gather_cols_kernel(int64_t R, int r, const double* __restrict__ 
 size_t setup_smem(const void* kern, size_t bytes, int& use_smem) {
     use_smem = bytes <= kSmemMax;
     if (!use_smem) return 0;
-    if (bytes > 48 * 1024)
+    // the kernels' static SMEM counts toward the 48 KB default too, so opt in whenever the
+    // total exceeds it (e.g. the SVD's 18 KB of rotation tables + a 32 KB matrix at m = 64)
+    cudaFuncAttributes fa;
+    W4_CUDA(cudaFuncGetAttributes(&fa, kern));
+    if (bytes + fa.sharedSizeBytes > 48 * 1024)
         W4_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
     return bytes;
 }
@@ -718,6 +871,19 @@ void chol_upper(int m, const double* G, double* R, int* info, DevBuf& work, cuda
     double* g = use ? nullptr : work.get<double>((size_t)m * m);
     (use ? chol_kernel<true> : chol_kernel<false>)<<<1, kThreads, sh, st>>>(m, G, R, info, g, use);
     W4_LAUNCH();
+}
+
+void chol_inv_upper(int m, const double* G, double* R, double* Rinv, int* info, DevBuf& work,
+                    cudaStream_t st) {
+    if (m <= 32) return launch_chol_inv<16, 1>(m, G, R, Rinv, info, st);
+    if (m <= 64) return launch_chol_inv<16, 2>(m, G, R, Rinv, info, st);
+    if (m <= 128) {
+        static const int tpr = std::getenv("WC4DVAR_CHOLINV_TPR") ? std::atoi(std::getenv("WC4DVAR_CHOLINV_TPR")) : 8;
+        if (tpr == 4) return launch_chol_inv<4, 16>(m, G, R, Rinv, info, st);  // 512 threads
+        return launch_chol_inv<8, 8>(m, G, R, Rinv, info, st);
+    }
+    chol_upper(m, G, R, info, work, st);
+    tri_inv_upper(m, R, Rinv, st);  // garbage after a breakdown; callers check info first
 }
 
 void pivoted_chol_rank(int m, const double* G, double tol_rel, int* rank, int* perm, DevBuf& work,

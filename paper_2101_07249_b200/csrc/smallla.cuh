@@ -13,6 +13,10 @@ namespace w4 {
 // symmetric part; randevd.cpp:96-102).  G, R: m x m col-major (ld m); may alias.
 void chol_upper(int m, const double* G, double* R, int* info, DevBuf& work, cudaStream_t st);
 
+// R = chol_upper(G) and Rinv = R^{-1} together (one register-resident kernel for m <= 128).
+// R, Rinv: m x m (ld m); R may alias G.  *info as chol_upper.
+void chol_inv_upper(int m, const double* G, double* R, double* Rinv, int* info, DevBuf& work,
+                    cudaStream_t st);
 // Diagonally pivoted Cholesky rank probe of a Gram matrix: rank = number of pivots
 // above tol_rel * max(diag).  perm[0..m) = pivot order (device ints).
 void pivoted_chol_rank(int m, const double* G, double tol_rel, int* rank, int* perm, DevBuf& work,

@@ -99,6 +99,11 @@ class TorchOps:
         return fcontig(torch.linalg.solve_triangular(R, eye, upper=True))
 
     @staticmethod
+    def chol_inv(G, what="cholqr"):
+        R = TorchOps.chol_upper(G, what)
+        return R, TorchOps.tri_inv_upper(R)
+
+    @staticmethod
     def small_mm(A, B, ta=False, tb=False):
         return fcontig((A.T if ta else A) @ (B.T if tb else B))
 
@@ -178,6 +183,16 @@ class DeviceOps:
         except NumericalError as e:
             raise NumericalError(f"{what}: {e}") from None
         return R
+
+    def chol_inv(self, G, what="cholqr"):
+        G = fcontig(G)
+        R, Ri = fmat(G.shape[0], G.shape[0], G), fmat(G.shape[0], G.shape[0], G)
+        try:
+            self._call("wc4dvar_gpu_la_chol_inv_upper_dev", G.shape[0], G.data_ptr(), R.data_ptr(),
+                       Ri.data_ptr())
+        except NumericalError as e:
+            raise NumericalError(f"{what}: {e}") from None
+        return R, Ri
 
     def tri_inv_upper(self, R):
         R = fcontig(R)
@@ -331,11 +346,11 @@ def dist_cholqr2(Y_rows: torch.Tensor, ops=TorchOps, G0: Optional[torch.Tensor] 
     (m x m), replicated Cholesky and triangular inverse, local Y R^{-1}; twice.  G0 is an
     already all-reduced Y^T Y.  Returns Q_rows, and R with Y = Q R when want_r."""
     G = G0 if G0 is not None else allreduce_sum(ops.gram(Y_rows, Y_rows))
-    R1 = ops.chol_upper(G, what)
-    Q1 = ops.tall_times_small(Y_rows, ops.tri_inv_upper(R1))
+    R1, R1i = ops.chol_inv(G, what)
+    Q1 = ops.tall_times_small(Y_rows, R1i)
     G2 = allreduce_sum(ops.gram(Q1, Q1))
-    R2 = ops.chol_upper(G2, what)
-    Q = ops.tall_times_small(Q1, ops.tri_inv_upper(R2))
+    R2, R2i = ops.chol_inv(G2, what)
+    Q = ops.tall_times_small(Q1, R2i)
     return (Q, ops.small_mm(R2, R1)) if want_r else Q
 
 
@@ -391,10 +406,10 @@ def dist_nystrom(apply_cols, omega_cols: torch.Tensor, n: int, m: int, k: int, o
         Z_rows = dist_cholqr2(Y_rows, ops, G0=G, what=what)
     E1_rows = _apply_rows(apply_cols, Z_rows, n, r)
     E2 = allreduce_sum(ops.gram(Z_rows, E1_rows))
-    Ru = ops.chol_upper(E2, "nystrom: Cholesky of Z^T A Z failed; the projected operator is "
-                            "numerically indefinite. Increase the oversampling parameter or use "
-                            "revd for indefinite spectra.")
-    F_rows = ops.tall_times_small(E1_rows, ops.tri_inv_upper(Ru))
+    _, Rui = ops.chol_inv(E2, "nystrom: Cholesky of Z^T A Z failed; the projected operator is "
+                              "numerically indefinite. Increase the oversampling parameter or use "
+                              "revd for indefinite spectra.")
+    F_rows = ops.tall_times_small(E1_rows, Rui)
     QF_rows, RF = dist_cholqr2(F_rows, ops, want_r=True,
                                what="nystrom: factor F is numerically rank deficient (CholQR breakdown)")
     sig, W = ops.svd_left(RF)

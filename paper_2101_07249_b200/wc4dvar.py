@@ -114,6 +114,7 @@ SIGNATURES = {
     "wc4dvar_gpu_la_tall_times_small_dev": (ctypes.c_int, [ctypes.c_int, _i64, _i64, _i64, _vp, _i64,
                                                            _vp, _i64, _vp, _i64, _vp]),
     "wc4dvar_gpu_la_chol_upper_dev": (ctypes.c_int, [ctypes.c_int, _i64, _vp, _vp, _vp]),
+    "wc4dvar_gpu_la_chol_inv_upper_dev": (ctypes.c_int, [ctypes.c_int, _i64, _vp, _vp, _vp, _vp]),
     "wc4dvar_gpu_la_tri_inv_upper_dev": (ctypes.c_int, [ctypes.c_int, _i64, _vp, _vp, _vp]),
     "wc4dvar_gpu_la_pivoted_rank_dev": (ctypes.c_int, [ctypes.c_int, _i64, _vp, ctypes.c_double,
                                                        ctypes.POINTER(_i64), _vp, _vp]),

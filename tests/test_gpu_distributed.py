@@ -100,3 +100,18 @@ def test_row_sharded_pcg_device_ops_vs_pcg_split():
     assert res.converged and abs(res.iterations - ref.history.iterations) <= 1
     x = res.x_rows.cpu().numpy()
     assert np.abs(x - ref.x).max() <= 1e-9 * np.abs(ref.x).max()
+
+
+@pytest.mark.parametrize("m", [1, 2, 20, 37, 64, 100, 128, 129])
+def test_chol_inv_fused_vs_torch(m):
+    rng = np.random.default_rng(m)
+    Y = rng.standard_normal((4 * m + 8, m))
+    G = Y.T @ Y
+    R, Ri = D.DeviceOps(0).chol_inv(_dev(G))
+    R, Ri = R.cpu().numpy(), Ri.cpu().numpy()
+    Rc = np.linalg.cholesky(G).T
+    assert np.array_equal(np.tril(R, -1), np.zeros((m, m))) and np.array_equal(np.tril(Ri, -1), np.zeros((m, m)))
+    assert np.abs(R - Rc).max() <= 1e-12 * np.abs(Rc).max()
+    assert np.abs(Ri @ R - np.eye(m)).max() <= 1e-12
+    with pytest.raises(W.NumericalError):
+        D.DeviceOps(0).chol_inv(_dev(G - 2 * np.abs(G).max() * np.eye(m)))
