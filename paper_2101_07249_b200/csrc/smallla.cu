@@ -357,7 +357,9 @@ constexpr int kEvdThreads = 512;
 template <bool SM>
 __global__ void __launch_bounds__(kEvdThreads)
     jacobi_evd_blk_kernel(int m, const double* __restrict__ K, double* __restrict__ vals,
-                          double* __restrict__ W, double* gwork, int use_smem, int debug) {
+                          double* __restrict__ W, double* gwork, int use_smem, int debug,
+                          const int* __restrict__ gate) {
+    if (gate && *gate == 0) return;  // the Cholesky + one-sided path succeeded (sym_evd_desc)
     extern __shared__ double sm[];
     const int mp = m + (m & 1);
     double* A = SM ? sm : gwork;
@@ -823,6 +825,137 @@ __global__ void __launch_bounds__(kThreads)
     }
 }
 
+// ---------------------------------------------------------------- one-sided Jacobi, one barrier
+// Left singular vectors / values of X (m <= 128), or of X^T (trans), by cyclic one-sided
+// Jacobi in round-robin order.  One 8-lane group per column pair: the group loads both
+// columns into registers (lane l owns the row pairs 2l + 16t, 2l + 16t + 1: LDS.128, and a
+// group's 8 lanes cover 128 contiguous bytes, so the four groups of a warp hit disjoint bank
+// passes), reduces the three dot products with width-8 shuffles, rotates in registers and
+// stores back -- one barrier per round and no SMEM rotation tables (the two-phase
+// jacobi_svd_kernel needs two barriers, a table round trip and a second pass over X).
+// Rotation and threshold as jacobi_svd_kernel (m eps relative, squared test).
+// gate (optional): run only if *gate == 0 (the Cholesky feeding sym_evd_desc succeeded).
+// square: write sigma^2 (eigenvalues of X X^T) instead of sigma.
+template <int RP>  // row pairs per lane: rows covered = 16 RP >= m
+__global__ void __launch_bounds__(512)
+    svd_reg_kernel(int m, const double* __restrict__ Xin, int trans, double* __restrict__ sigma,
+                   double* __restrict__ U, const int* __restrict__ gate, int square, int debug) {
+    if (gate && *gate != 0) return;
+    extern __shared__ __align__(16) double X[];  // ld x mp column-major, ld = 16 RP, zero padded
+    constexpr int ld = 16 * RP;
+    __shared__ double nrm[128];
+    __shared__ int rank_of[128];
+    const int tid = threadIdx.x, nt = blockDim.x;
+    const int mp = m + (m & 1);
+    for (int e = tid; e < ld * mp; e += nt) {
+        const int i = e % ld, j = e / ld;
+        X[e] = (i < m && j < m) ? (trans ? Xin[j + (size_t)i * m] : Xin[i + (size_t)j * m]) : 0.0;
+    }
+    __syncthreads();
+    const int g = tid >> 3, gl = tid & 7;
+    int a = g, b = mp - 1 - g;  // round-robin players (rr_pair, r advancing by one per round)
+    const bool active = g < mp / 2;
+    for (int sweep = 0; sweep < 60 && m > 1; ++sweep) {
+        int rotated = 0;
+        for (int r = 0; r < mp - 1; ++r) {
+            const int p = a < b ? a : b, q = a < b ? b : a;
+            double2 xp[RP], xq[RP];
+            double al0 = 0.0, al1 = 0.0, be0 = 0.0, be1 = 0.0, ga0 = 0.0, ga1 = 0.0;
+            const double* cp = X + (size_t)p * ld + 2 * gl;
+            const double* cq = X + (size_t)q * ld + 2 * gl;
+#pragma unroll
+            for (int t = 0; t < RP; ++t) {
+                xp[t] = active ? *reinterpret_cast<const double2*>(cp + 16 * t) : make_double2(0.0, 0.0);
+                xq[t] = active ? *reinterpret_cast<const double2*>(cq + 16 * t) : make_double2(0.0, 0.0);
+                al0 = fma(xp[t].x, xp[t].x, al0);
+                al1 = fma(xp[t].y, xp[t].y, al1);
+                be0 = fma(xq[t].x, xq[t].x, be0);
+                be1 = fma(xq[t].y, xq[t].y, be1);
+                ga0 = fma(xp[t].x, xq[t].x, ga0);
+                ga1 = fma(xp[t].y, xq[t].y, ga1);
+            }
+            double al = al0 + al1, be = be0 + be1, ga = ga0 + ga1;
+#pragma unroll
+            for (int o = 4; o > 0; o >>= 1) {
+                al += __shfl_xor_sync(0xffffffffu, al, o, 8);
+                be += __shfl_xor_sync(0xffffffffu, be, o, 8);
+                ga += __shfl_xor_sync(0xffffffffu, ga, o, 8);
+            }
+            const double thr = mp * DBL_EPSILON;
+            if (active && q < m && ga != 0.0 && ga * ga > thr * thr * (al * be)) {
+                const double h = be - al, g2 = 2.0 * ga;
+                const double tt = (h >= 0.0 ? g2 : -g2) / (fabs(h) + sqrt(h * h + g2 * g2));
+                const double c = rsqrt(1.0 + tt * tt);
+                const double sn = tt * c;
+                rotated = 1;
+                double* wp = X + (size_t)p * ld + 2 * gl;
+                double* wq = X + (size_t)q * ld + 2 * gl;
+#pragma unroll
+                for (int t = 0; t < RP; ++t) {
+                    double2 np, nq;
+                    np.x = c * xp[t].x - sn * xq[t].x;
+                    np.y = c * xp[t].y - sn * xq[t].y;
+                    nq.x = sn * xp[t].x + c * xq[t].x;
+                    nq.y = sn * xp[t].y + c * xq[t].y;
+                    *reinterpret_cast<double2*>(wp + 16 * t) = np;
+                    *reinterpret_cast<double2*>(wq + 16 * t) = nq;
+                }
+            }
+            a = a == 0 ? 0 : (a == mp - 1 ? 1 : a + 1);
+            b = b == 0 ? 0 : (b == mp - 1 ? 1 : b + 1);
+            __syncthreads();
+        }
+        const int any = __syncthreads_or(rotated);
+        if (debug && tid == 0) printf("svd_reg m=%d sweep %d rotated %d\n", m, sweep, any);
+        if (!any) break;
+    }
+    const int wid = tid >> 5, lane = tid & 31, nw = nt >> 5;
+    for (int j = wid; j < m; j += nw) {
+        double s2 = 0.0;
+        for (int i = lane; i < m; i += 32) s2 += X[i + j * ld] * X[i + j * ld];
+        s2 = warp_sum(s2);
+        if (lane == 0) nrm[j] = sqrt(s2);
+    }
+    __syncthreads();
+    for (int i = tid; i < m; i += nt) {
+        int rk = 0;
+        for (int j = 0; j < m; ++j) rk += (nrm[j] > nrm[i]) || (nrm[j] == nrm[i] && j < i);
+        rank_of[i] = rk;
+        sigma[rk] = square ? nrm[i] * nrm[i] : nrm[i];
+    }
+    __syncthreads();
+    for (int e = tid; e < m * m; e += nt) {
+        const int i = e % m, j = e / m;
+        const double sj = nrm[j];
+        U[i + rank_of[j] * m] = sj > 0.0 ? X[i + j * ld] / sj : 0.0;
+    }
+}
+
+template <int RP>
+void launch_svd_reg(int m, const double* X, int trans, double* sigma, double* U, const int* gate,
+                    int square, cudaStream_t st) {
+    const int mp = m + (m & 1);
+    const size_t smem = sizeof(double) * (size_t)(16 * RP) * mp;
+    auto kern = svd_reg_kernel<RP>;
+    cudaFuncAttributes fa;
+    W4_CUDA(cudaFuncGetAttributes(&fa, kern));
+    if (smem + fa.sharedSizeBytes > 48 * 1024)
+        W4_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    const int threads = std::max(32, ((mp / 2) * 8 + 31) / 32 * 32);
+    static const int debug = std::getenv("WC4DVAR_DEBUG_JACOBI") ? 1 : 0;
+    kern<<<1, threads, smem, st>>>(m, X, trans, sigma, U, gate, square, debug);
+    W4_LAUNCH();
+}
+
+void svd_reg(int m, const double* X, int trans, double* sigma, double* U, const int* gate, int square,
+             cudaStream_t st) {
+    const int rp = (m + 15) / 16;
+    if (rp <= 2) return launch_svd_reg<2>(m, X, trans, sigma, U, gate, square, st);
+    if (rp <= 4) return launch_svd_reg<4>(m, X, trans, sigma, U, gate, square, st);
+    if (rp <= 7) return launch_svd_reg<7>(m, X, trans, sigma, U, gate, square, st);
+    return launch_svd_reg<8>(m, X, trans, sigma, U, gate, square, st);
+}
+
 __global__ void small_gemm_kernel(bool ta, bool tb, int M, int N, int K, double alpha,
                                   const double* __restrict__ A, int lda,
                                   const double* __restrict__ B, int ldb, double beta,
@@ -933,22 +1066,45 @@ void sym_evd_desc(int m, const double* K, double* vals, double* W, DevBuf& work,
         W4_LAUNCH();
         return;
     }
-    int use = 0;
-    const size_t bytes = sizeof(double) * 2 * m * m;
+    // Default for m <= 128 and SPD K (every sketch: Z^T A Z with A >= I, R R^T): K = R^T R by
+    // the fused Cholesky, then the register one-sided Jacobi on R^T gives the eigenvectors as
+    // its left singular vectors and the eigenvalues as sigma^2, with no eigenvector
+    // accumulation and one barrier per round.  If the Cholesky breaks down (indefinite K) the
+    // two-sided block-Jacobi kernel runs instead; the device info word gates both kernels, so
+    // there is no host round trip.  WC4DVAR_EVD=jacobi forces the two-sided kernel.
+    static const bool two_sided = [] {
+        const char* e = std::getenv("WC4DVAR_EVD");
+        return e && std::strcmp(e, "jacobi") == 0;
+    }();
     const int mp = m + (m & 1);
     const size_t bytes2 = sizeof(double) * 2 * mp * mp;
-    (void)bytes;
+    int use = 0;
     const size_t sh = setup_smem(reinterpret_cast<const void*>(jacobi_evd_blk_kernel<true>), bytes2, use);
-    double* g = use ? nullptr : work.get<double>((size_t)2 * mp * mp);
+    double* scratch = work.get<double>(2 * (size_t)m * m + 2 * (size_t)mp * mp + 8);
+    const int* gate = nullptr;
+    if (m <= 128 && !two_sided) {
+        double* R = scratch;
+        double* Ri = R + (size_t)m * m;
+        int* info = reinterpret_cast<int*>(scratch + 2 * (size_t)m * m + 2 * (size_t)mp * mp);
+        chol_inv_upper(m, K, R, Ri, info, work, st);  // m <= 128: no work-buffer use
+        svd_reg(m, R, /*trans=*/1, vals, W, info, /*square=*/1, st);
+        gate = info;
+    }
+    double* g = use ? nullptr : scratch + 2 * (size_t)m * m;
     static const int debug = std::getenv("WC4DVAR_DEBUG_JACOBI") ? 1 : 0;
     (use ? jacobi_evd_blk_kernel<true> : jacobi_evd_blk_kernel<false>)<<<1, kEvdThreads, sh, st>>>(
-        m, K, vals, W, g, use, debug);
+        m, K, vals, W, g, use, debug, gate);
     W4_LAUNCH();
 }
 
 void svd_left_desc(int m, const double* X, double* sigma, double* U, DevBuf& work,
                    cudaStream_t st) {
     require(m <= 512, "svd_left_desc: m too large");
+    static const bool two_phase = [] {
+        const char* e = std::getenv("WC4DVAR_SVD");
+        return e && std::strcmp(e, "jacobi") == 0;
+    }();
+    if (m <= 128 && !two_phase) return svd_reg(m, X, 0, sigma, U, nullptr, 0, st);
     int use = 0;
     const size_t bytes = sizeof(double) * m * m;
     const size_t sh = setup_smem(reinterpret_cast<const void*>(jacobi_svd_kernel<true>), bytes, use);

@@ -115,3 +115,30 @@ def test_chol_inv_fused_vs_torch(m):
     assert np.abs(Ri @ R - np.eye(m)).max() <= 1e-12
     with pytest.raises(W.NumericalError):
         D.DeviceOps(0).chol_inv(_dev(G - 2 * np.abs(G).max() * np.eye(m)))
+
+
+@pytest.mark.parametrize("m", [1, 2, 7, 20, 64, 100, 128, 129])
+def test_small_evd_svd_vs_lapack(m):
+    """sym_evd_desc (Cholesky + register one-sided Jacobi for SPD, two-sided Jacobi fallback
+    for indefinite input) and svd_left_desc against LAPACK: values 1e-12 relative to the
+    largest, vectors through the projector of well-separated leading pairs."""
+    rng = np.random.default_rng(100 + m)
+    ops = D.DeviceOps(0)
+    Q, _ = np.linalg.qr(rng.standard_normal((m, m)))
+    for spd in (True, False):
+        lam = np.linspace(1.0, 50.0, m) if spd else np.linspace(-20.0, 30.0, m)
+        K = (Q * lam) @ Q.T
+        vals, V = ops.eigh_desc(_dev(K))
+        vals, V = vals.cpu().numpy(), V.cpu().numpy()
+        ref = np.sort(lam)[::-1]
+        assert np.abs(vals - ref).max() <= 1e-12 * np.abs(ref).max(), (spd, np.abs(vals - ref).max())
+        assert np.abs(V.T @ V - np.eye(m)).max() <= 1e-12
+        assert np.abs(K @ V - V * vals).max() <= 1e-11 * np.abs(ref).max()
+    X = rng.standard_normal((m, m))
+    s, U = ops.svd_left(_dev(X))
+    s, U = s.cpu().numpy(), U.cpu().numpy()
+    sref = np.linalg.svd(X, compute_uv=False)
+    assert np.abs(s - sref).max() <= 1e-12 * sref.max()
+    assert np.abs(U.T @ U - np.eye(m)).max() <= 1e-12
+    # U diag(s) is X's column space image: X X^T U = U diag(s^2)
+    assert np.abs(X @ X.T @ U - U * s * s).max() <= 1e-11 * sref.max() ** 2
