@@ -826,53 +826,67 @@ __global__ void __launch_bounds__(kThreads)
 }
 
 // ---------------------------------------------------------------- one-sided Jacobi, one barrier
-// Left singular vectors / values of X (m <= 128), or of X^T (trans), by cyclic one-sided
-// Jacobi in round-robin order.  One 8-lane group per column pair: the group loads both
-// columns into registers (lane l owns the row pairs 2l + 16t, 2l + 16t + 1: LDS.128, and a
-// group's 8 lanes cover 128 contiguous bytes, so the four groups of a warp hit disjoint bank
-// passes), reduces the three dot products with width-8 shuffles, rotates in registers and
-// stores back -- one barrier per round and no SMEM rotation tables (the two-phase
-// jacobi_svd_kernel needs two barriers, a table round trip and a second pass over X).
-// Rotation and threshold as jacobi_svd_kernel (m eps relative, squared test).
-// gate (optional): run only if *gate == 0 (the Cholesky feeding sym_evd_desc succeeded).
-// square: write sigma^2 (eigenvalues of X X^T) instead of sigma.
+// Left singular vectors / values of X (m <= 128), or of X^T (trans), by one-sided Jacobi in
+// the odd-even transposition ordering (Brent-Luk): positions 0..mp-1 on a line; even steps
+// rotate the column pairs at positions (2k, 2k+1), odd steps (2k+1, 2k+2), and every rotated
+// pair swaps positions, so after mp steps every pair of columns has met exactly once (a
+// sweep).  Group k (8 lanes) owns the pair of step parity; a column pair lives in
+// REGISTERS (lane l holds row pairs 2l + 16t: LDS.128 / STS.128) and between steps each
+// group keeps one of its columns and trades the other with one neighbour through a
+// double-buffered SMEM mailbox: one column out and one in per step (the round-robin order
+// moves both) and one barrier per step.  The group reduces the three dot products with
+// width-8 shuffles and rotates in registers; rotation and threshold as jacobi_svd_kernel
+// (m eps relative, squared test).  gate (optional): run only if *gate == 0 (the Cholesky
+// feeding sym_evd_desc succeeded).  square: write sigma^2 (eigenvalues of X X^T).
 template <int RP>  // row pairs per lane: rows covered = 16 RP >= m
 __global__ void __launch_bounds__(512)
     svd_reg_kernel(int m, const double* __restrict__ Xin, int trans, double* __restrict__ sigma,
                    double* __restrict__ U, const int* __restrict__ gate, int square, int debug) {
     if (gate && *gate != 0) return;
-    extern __shared__ __align__(16) double X[];  // ld x mp column-major, ld = 16 RP, zero padded
+    extern __shared__ __align__(16) double sm[];
     constexpr int ld = 16 * RP;
+    const int tid = threadIdx.x, nt = blockDim.x;
+    const int mp = m + (m & 1), np = mp / 2, L = np - 1;
+    double* X = sm;                              // ld x mp staging (load / final), zero padded
+    double* mbox = sm;                           // [2][np][ld] mailboxes, aliasing X (unused
+                                                 // while the columns live in registers)
+    double* park = sm + (size_t)ld * mp;         // [2][ld]: group 0's and group L's parked column
     __shared__ double nrm[128];
     __shared__ int rank_of[128];
-    const int tid = threadIdx.x, nt = blockDim.x;
-    const int mp = m + (m & 1);
+    __shared__ int mid[2][64];
     for (int e = tid; e < ld * mp; e += nt) {
         const int i = e % ld, j = e / ld;
         X[e] = (i < m && j < m) ? (trans ? Xin[j + (size_t)i * m] : Xin[i + (size_t)j * m]) : 0.0;
     }
     __syncthreads();
-    const int g = tid >> 3, gl = tid & 7;
-    int a = g, b = mp - 1 - g;  // round-robin players (rr_pair, r advancing by one per round)
-    const bool active = g < mp / 2;
+    const int k = tid >> 3, gl = tid & 7;
+    const bool active = k < np;
+    double2 a[RP], b[RP];
+    int ia = 2 * k, ib = 2 * k + 1, ipk = -1;  // column ids (id m = odd-m phantom)
+#pragma unroll
+    for (int t = 0; t < RP; ++t) {
+        a[t] = active ? *reinterpret_cast<const double2*>(X + (size_t)ia * ld + 2 * gl + 16 * t)
+                      : make_double2(0.0, 0.0);
+        b[t] = active ? *reinterpret_cast<const double2*>(X + (size_t)ib * ld + 2 * gl + 16 * t)
+                      : make_double2(0.0, 0.0);
+    }
+    __syncthreads();  // X is read: the mailboxes may overwrite it
+    const double thr = mp * DBL_EPSILON;
+    int step = 0;
     for (int sweep = 0; sweep < 60 && m > 1; ++sweep) {
         int rotated = 0;
-        for (int r = 0; r < mp - 1; ++r) {
-            const int p = a < b ? a : b, q = a < b ? b : a;
-            double2 xp[RP], xq[RP];
+        for (int ss = 0; ss < mp; ++ss, ++step) {
+            const bool odd = step & 1;
+            const bool work = active && !(odd && k == L);
             double al0 = 0.0, al1 = 0.0, be0 = 0.0, be1 = 0.0, ga0 = 0.0, ga1 = 0.0;
-            const double* cp = X + (size_t)p * ld + 2 * gl;
-            const double* cq = X + (size_t)q * ld + 2 * gl;
 #pragma unroll
             for (int t = 0; t < RP; ++t) {
-                xp[t] = active ? *reinterpret_cast<const double2*>(cp + 16 * t) : make_double2(0.0, 0.0);
-                xq[t] = active ? *reinterpret_cast<const double2*>(cq + 16 * t) : make_double2(0.0, 0.0);
-                al0 = fma(xp[t].x, xp[t].x, al0);
-                al1 = fma(xp[t].y, xp[t].y, al1);
-                be0 = fma(xq[t].x, xq[t].x, be0);
-                be1 = fma(xq[t].y, xq[t].y, be1);
-                ga0 = fma(xp[t].x, xq[t].x, ga0);
-                ga1 = fma(xp[t].y, xq[t].y, ga1);
+                al0 = fma(a[t].x, a[t].x, al0);
+                al1 = fma(a[t].y, a[t].y, al1);
+                be0 = fma(b[t].x, b[t].x, be0);
+                be1 = fma(b[t].y, b[t].y, be1);
+                ga0 = fma(a[t].x, b[t].x, ga0);
+                ga1 = fma(a[t].y, b[t].y, ga1);
             }
             double al = al0 + al1, be = be0 + be1, ga = ga0 + ga1;
 #pragma unroll
@@ -881,34 +895,93 @@ __global__ void __launch_bounds__(512)
                 be += __shfl_xor_sync(0xffffffffu, be, o, 8);
                 ga += __shfl_xor_sync(0xffffffffu, ga, o, 8);
             }
-            const double thr = mp * DBL_EPSILON;
-            if (active && q < m && ga != 0.0 && ga * ga > thr * thr * (al * be)) {
+            if (work && ga != 0.0 && ga * ga > thr * thr * (al * be)) {
                 const double h = be - al, g2 = 2.0 * ga;
                 const double tt = (h >= 0.0 ? g2 : -g2) / (fabs(h) + sqrt(h * h + g2 * g2));
                 const double c = rsqrt(1.0 + tt * tt);
                 const double sn = tt * c;
                 rotated = 1;
-                double* wp = X + (size_t)p * ld + 2 * gl;
-                double* wq = X + (size_t)q * ld + 2 * gl;
 #pragma unroll
                 for (int t = 0; t < RP; ++t) {
-                    double2 np, nq;
-                    np.x = c * xp[t].x - sn * xq[t].x;
-                    np.y = c * xp[t].y - sn * xq[t].y;
-                    nq.x = sn * xp[t].x + c * xq[t].x;
-                    nq.y = sn * xp[t].y + c * xq[t].y;
-                    *reinterpret_cast<double2*>(wp + 16 * t) = np;
-                    *reinterpret_cast<double2*>(wq + 16 * t) = nq;
+                    const double2 x = a[t], y = b[t];
+                    a[t] = make_double2(c * x.x - sn * y.x, c * x.y - sn * y.y);
+                    b[t] = make_double2(sn * x.x + c * y.x, sn * x.y + c * y.y);
                 }
             }
-            a = a == 0 ? 0 : (a == mp - 1 ? 1 : a + 1);
-            b = b == 0 ? 0 : (b == mp - 1 ? 1 : b + 1);
+            if (np == 1) continue;  // a single pair never moves
+            // positions swap after the step; then hand one column to a neighbour:
+            //   even -> odd: keep a, send b left (group 0 parks it), receive b from the right
+            //                (the last group parks a and idles);
+            //   odd -> even: keep b, send a right (the last group takes its park as b),
+            //                receive a from the left (group 0 takes its park as a).
+            const int par = step & 1;
+            double* mb = mbox + (size_t)par * np * ld;
+            if (active) {
+                // even: every group but 0 sends b to k - 1; odd: every group but L sends a to k + 1
+                const int dst = !odd ? (k > 0 ? k - 1 : -1) : (k < L ? k + 1 : -1);
+                if (dst >= 0) {
+                    double* o = mb + (size_t)dst * ld + 2 * gl;
+                    if (!odd) {
+#pragma unroll
+                        for (int t = 0; t < RP; ++t) *reinterpret_cast<double2*>(o + 16 * t) = b[t];
+                    } else {
+#pragma unroll
+                        for (int t = 0; t < RP; ++t) *reinterpret_cast<double2*>(o + 16 * t) = a[t];
+                    }
+                    if (gl == 0) mid[par][dst] = !odd ? ib : ia;
+                }
+            }
             __syncthreads();
+            if (active) {
+                const double2* in = reinterpret_cast<const double2*>(mb + (size_t)k * ld + 2 * gl);
+                double2* pkb = reinterpret_cast<double2*>(park + (k == 0 ? 0 : ld) + 2 * gl);
+                if (!odd) {
+                    if (k == 0) {  // park b (position 0 idles in odd steps)
+#pragma unroll
+                        for (int t = 0; t < RP; ++t) pkb[8 * t] = b[t];
+                        ipk = ib;
+                    }
+                    if (k == L) {  // park a, idle
+#pragma unroll
+                        for (int t = 0; t < RP; ++t) pkb[8 * t] = a[t];
+                        ipk = ia;
+                    } else {       // receive b from the right
+#pragma unroll
+                        for (int t = 0; t < RP; ++t) b[t] = in[8 * t];
+                        ib = mid[par][k];
+                    }
+                } else {
+                    if (k == L) {  // b <- park, receive a from the left
+#pragma unroll
+                        for (int t = 0; t < RP; ++t) b[t] = pkb[8 * t];
+                        ib = ipk;
+                    }
+                    if (k == 0) {  // a <- park
+#pragma unroll
+                        for (int t = 0; t < RP; ++t) a[t] = pkb[8 * t];
+                        ia = ipk;
+                    } else {
+#pragma unroll
+                        for (int t = 0; t < RP; ++t) a[t] = in[8 * t];
+                        ia = mid[par][k];
+                    }
+                }
+            }
         }
         const int any = __syncthreads_or(rotated);
         if (debug && tid == 0) printf("svd_reg m=%d sweep %d rotated %d\n", m, sweep, any);
         if (!any) break;
     }
+    // back to X by column id (the odd-m phantom column is dropped); a parked column (odd
+    // sweep end never happens: mp is even, so every sweep ends after an odd step) is none
+    if (active) {
+#pragma unroll
+        for (int t = 0; t < RP; ++t) {
+            if (ia < m) *reinterpret_cast<double2*>(X + (size_t)ia * ld + 2 * gl + 16 * t) = a[t];
+            if (ib < m) *reinterpret_cast<double2*>(X + (size_t)ib * ld + 2 * gl + 16 * t) = b[t];
+        }
+    }
+    __syncthreads();
     const int wid = tid >> 5, lane = tid & 31, nw = nt >> 5;
     for (int j = wid; j < m; j += nw) {
         double s2 = 0.0;
@@ -935,7 +1008,7 @@ template <int RP>
 void launch_svd_reg(int m, const double* X, int trans, double* sigma, double* U, const int* gate,
                     int square, cudaStream_t st) {
     const int mp = m + (m & 1);
-    const size_t smem = sizeof(double) * (size_t)(16 * RP) * mp;
+    const size_t smem = sizeof(double) * (size_t)(16 * RP) * (mp + 2);
     auto kern = svd_reg_kernel<RP>;
     cudaFuncAttributes fa;
     W4_CUDA(cudaFuncGetAttributes(&fa, kern));

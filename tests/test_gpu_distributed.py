@@ -142,3 +142,4 @@ def test_small_evd_svd_vs_lapack(m):
     assert np.abs(U.T @ U - np.eye(m)).max() <= 1e-12
     # U diag(s) is X's column space image: X X^T U = U diag(s^2)
     assert np.abs(X @ X.T @ U - U * s * s).max() <= 1e-11 * sref.max() ** 2
+
