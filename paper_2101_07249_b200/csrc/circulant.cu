@@ -149,13 +149,11 @@ void CirculantPlan::apply(bool inv, int N, const double* V, int64_t ldv, int64_t
     require(sb && sq, "apply_D_half_inv: inverse factors were not provided");
     const int64_t dim = n * (N + 1);
     const int64_t ncols = (int64_t)(N + 1) * m;
-    // WC4DVAR_FFT4=1 selects the fused four-step path (fft4.cu).  Round-1 measurement at
-    // C4 (n = 1e6, m = 64): 46 ms per D^1/2 vs 25 ms for batched cuFFT -- the three passes
-    // run at ~1.3 TB/s (one 512-thread CTA per SM, load / FFT / store phases not overlapped),
-    // so cuFFT stays the default until the passes are double-buffered.
+    // The fused four-step path (fft4.cu) runs whenever n has a compiled split; WC4DVAR_FFT4=0
+    // forces batched cuFFT (the fallback for every other n).
     static const bool use_f4 = [] {
         const char* e = std::getenv("WC4DVAR_FFT4");
-        return e && std::atoi(e) != 0;
+        return !e || std::atoi(e) != 0;
     }();
     if (use_f4 && impl->f4.ready()) {
         impl->f4.apply(inv, N, V, ldv, m, out, ldo, add, ldadd, status, zbuf, impl->pairbuf, st);

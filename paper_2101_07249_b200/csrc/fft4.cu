@@ -1,412 +1,664 @@
-// Fused four-step FFT for the circulant D^{1/2} (EXTENSION, BASELINE configs 3-5).
+// Fused four-step FFT convolution for the circulant D^{1/2} (EXTENSION, BASELINE configs 3-5).
 //
 // D^{1/2} of a periodic-grid SOAR factor is a circulant convolution whose spectrum lam is
 // real and even.  Two real window columns x1, x2 that use the same factor therefore go
 // through ONE complex transform: z = x1 + i x2, D^{1/2}x1 = Re IFFT(lam FFT z),
 // D^{1/2}x2 = Im IFFT(lam FFT z).  The length-N transform is the four-step split
-// N = N1 N2 (index n = n1 + N1 n2, frequency k = k2 + N2 k1):
-//   pass A   : per n1, FFT_N2 over n2 (strided gather), times w_N^{n1 k2}        -> Y
-//   pass B   : per k2, FFT_N1 over n1, times lam[k2 + N2 k1], IFFT_N1, times
-//              w_N^{-n1 k2}                                                      -> Y (in place)
-//   pass A^-1: per n1, IFFT_N2 over k2, / N, real / imaginary parts (+ v) -> two outputs
-// Every FFT of length <= 4096 runs in SMEM as Stockham radix-{8,5,4,3,2} stages.  HBM sees
-// three read + write passes over the (complex) pair data instead of the ~7 of
-// D2Z -> product -> Z2D with multi-pass library FFTs.
+// N = N1 N2 (index j = j1 + N1 j2, frequency k = k2 + N2 k1):
+//   pass A : per j1, FFT_N2 over j2 (strided), times w_N^{j1 k2}                  -> Y[j1 + N1 k2]
+//   pass B : per k2, FFT_N1 over j1 (contiguous), times lam[k2 + N2 k1] / N,
+//            IFFT_N1, times w_N^{-j1 k2}                                           -> Y (in place)
+//   pass C : per j1, IFFT_N2 over k2, real / imaginary parts (+ v)                 -> two outputs
+//
+// B200 design:
+//  * ONE persistent kernel runs all three passes as a ticketed dataflow.  Work items are
+//    issued in steps {A(g), B(g-1), C(g-2)} over groups g of column pairs; an item waits on
+//    a per-group completion counter of the pass before it (all such items hold smaller
+//    tickets, so the wait never deadlocks).  Four Y slots rotate, so the working set of
+//    a step (4 groups x 16 N bytes) stays in L2: HBM sees one read of V (and of the add
+//    term) and one write of the output per column; Y round-trips through L2 only.
+//  * Every FFT is a Stockham sequence of register-resident radix-R stages (R in 5..20,
+//    composite radices as in-register Cooley-Tukey over hard-coded radix-2/4/5/8
+//    butterflies).  The first stage loads straight from global memory and the last stage
+//    stores straight to global memory, so a length-L sequence with s stages costs s - 1
+//    SMEM exchanges; pass B turns around in registers (forward last stage, spectrum
+//    product, inverse first stage) without an exchange.
+//  * Stage twiddles w_M^{r jm} come from one w_L^e table per length (only e < ~400 is
+//    touched, so it stays in L1) raised to the r-th power in registers; the four-step
+//    twiddles w_N^p come from a two-level (p >> 10, p & 1023) table.
+//  * 200 threads and <= 64000 B of SMEM per CTA for every item kind; two CTAs per SM (the
+//    128-register budget of a radix-20 stage).
 #include "fft4.cuh"
 
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <vector>
 
 namespace w4 {
 namespace {
 
-constexpr int kFftThreads = 512;
-constexpr int kFftMaxElems = 4096;  // cnt * L per CTA (bounds the per-thread butterflies)
+constexpr int kNT = 200;      // threads per CTA (every item kind)
+constexpr int kCtaPerSm = 2;  // CTAs per SM (register budget)
+constexpr int kSlots = 4;     // Y slots in flight: A(g) reuses the slot of C(g - 4), two steps earlier
+
+__constant__ double2 c_w400[400];  // exp(-2 pi i e / 400): every in-register DFT twiddle
 
 __device__ __forceinline__ double2 cmul(double2 a, double2 b) {
-    return make_double2(a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x);
+    return make_double2(fma(a.x, b.x, -a.y * b.y), fma(a.x, b.y, a.y * b.x));
 }
 __device__ __forceinline__ double2 cadd(double2 a, double2 b) { return make_double2(a.x + b.x, a.y + b.y); }
 __device__ __forceinline__ double2 csub(double2 a, double2 b) { return make_double2(a.x - b.x, a.y - b.y); }
+__device__ __forceinline__ double2 conj2(double2 a) { return make_double2(a.x, -a.y); }
 // multiply by -i (forward) or +i (inverse)
-__device__ __forceinline__ double2 rot(double2 a, bool inv) {
-    return inv ? make_double2(-a.y, a.x) : make_double2(a.y, -a.x);
+template <bool INV>
+__device__ __forceinline__ double2 rot(double2 a) {
+    return INV ? make_double2(-a.y, a.x) : make_double2(a.y, -a.x);
 }
 
-// DFT_R of v in place: X_k = sum_r v_r exp(-+2 pi i r k / R)  (- forward, + inverse)
-template <int R>
-__device__ __forceinline__ void dft(double2 (&v)[R], bool inv);
-
-template <>
-__device__ __forceinline__ void dft<2>(double2 (&v)[2], bool) {
-    const double2 a = v[0], b = v[1];
-    v[0] = cadd(a, b);
-    v[1] = csub(a, b);
-}
-template <>
-__device__ __forceinline__ void dft<4>(double2 (&v)[4], bool inv) {
-    const double2 t0 = cadd(v[0], v[2]), t1 = csub(v[0], v[2]);
-    const double2 t2 = cadd(v[1], v[3]), t3 = rot(csub(v[1], v[3]), inv);
-    v[0] = cadd(t0, t2);
-    v[2] = csub(t0, t2);
-    v[1] = cadd(t1, t3);
-    v[3] = csub(t1, t3);
-}
-template <>
-__device__ __forceinline__ void dft<8>(double2 (&v)[8], bool inv) {
-    double2 e[4] = {v[0], v[2], v[4], v[6]}, o[4] = {v[1], v[3], v[5], v[7]};
-    dft<4>(e, inv);
-    dft<4>(o, inv);
-    constexpr double h = 0.70710678118654752440;  // 1/sqrt(2)
-    // o_k *= w8^k, w8 = exp(-+ i pi / 4)
-    const double sg = inv ? 1.0 : -1.0;
-    o[1] = make_double2(h * (o[1].x - sg * o[1].y), h * (o[1].y + sg * o[1].x));
-    o[2] = rot(o[2], inv);
-    o[3] = make_double2(h * (-o[3].x - sg * o[3].y), h * (-o[3].y + sg * o[3].x));
-#pragma unroll
-    for (int k = 0; k < 4; ++k) {
-        v[k] = cadd(e[k], o[k]);
-        v[k + 4] = csub(e[k], o[k]);
-    }
-}
-template <>
-__device__ __forceinline__ void dft<3>(double2 (&v)[3], bool inv) {
-    constexpr double s = 0.86602540378443864676;  // sin(2 pi / 3)
-    const double2 t1 = cadd(v[1], v[2]), t2 = csub(v[1], v[2]);
-    const double2 m1 = make_double2(v[0].x - 0.5 * t1.x, v[0].y - 0.5 * t1.y);
-    const double2 m2 = rot(make_double2(s * t2.x, s * t2.y), inv);
-    v[0] = cadd(v[0], t1);
-    v[1] = cadd(m1, m2);
-    v[2] = csub(m1, m2);
-}
-template <>
-__device__ __forceinline__ void dft<5>(double2 (&v)[5], bool inv) {
-    constexpr double c1 = 0.30901699437494742410, c2 = -0.80901699437494742410;  // cos 2pi/5, cos 4pi/5
-    constexpr double s1 = 0.95105651629515357212, s2 = 0.58778525229247312917;   // sin 2pi/5, sin 4pi/5
-    const double2 t1 = cadd(v[1], v[4]), t2 = cadd(v[2], v[3]);
-    const double2 t3 = csub(v[1], v[4]), t4 = csub(v[2], v[3]);
-    const double2 x0 = v[0];
-    const double2 a1 = make_double2(x0.x + c1 * t1.x + c2 * t2.x, x0.y + c1 * t1.y + c2 * t2.y);
-    const double2 a2 = make_double2(x0.x + c2 * t1.x + c1 * t2.x, x0.y + c2 * t1.y + c1 * t2.y);
-    const double2 b1 = rot(make_double2(s1 * t3.x + s2 * t4.x, s1 * t3.y + s2 * t4.y), inv);
-    const double2 b2 = rot(make_double2(s2 * t3.x - s1 * t4.x, s2 * t3.y - s1 * t4.y), inv);
-    v[0] = make_double2(x0.x + t1.x + t2.x, x0.y + t1.y + t2.y);
-    v[1] = cadd(a1, b1);
-    v[4] = csub(a1, b1);
-    v[2] = cadd(a2, b2);
-    v[3] = csub(a2, b2);
-}
-
-// SMEM slot of sequence element i: one pad slot per 8 elements, so the stride-R writes of
-// a Stockham stage (Ns = 1: consecutive butterflies write 8 R bytes apart) spread over all
-// eight 16-byte bank groups instead of piling on one.
-__device__ __forceinline__ int pd(int i) { return i + (i >> 3); }
-
-// One Stockham stage over cnt SMEM sequences (row stride LS): read every butterfly's
-// inputs, barrier, write the outputs in place.  MAXB bounds butterflies per thread:
-// cnt * L / R <= MAXB * kFftThreads.
-template <int R, int MAXB>
-__device__ __noinline__ void fft_stage(double2* buf, int cnt, int L, int LS, int Ns,
-                                          const double2* __restrict__ tw, bool inv) {
-    const int tid = threadIdx.x;
-    const int nb = L / R, total = cnt * nb;
-    double2 v[MAXB][R];
-    int dst[MAXB], row[MAXB];
-#pragma unroll
-    for (int b = 0; b < MAXB; ++b) {
-        const int q = tid + b * kFftThreads;
-        dst[b] = -1;
-        if (q < total) {
-            const int s = q / nb, j = q - s * nb;
-            const int jm = j % Ns;
-            const double2* src = buf + s * LS;
-#pragma unroll
-            for (int r = 0; r < R; ++r) {
-                double2 x = src[pd(j + r * nb)];
-                if (r > 0 && Ns > 1) {
-                    double2 w = __ldg(tw + jm * R + r);
-                    if (inv) w.y = -w.y;
-                    x = cmul(x, w);
-                }
-                v[b][r] = x;
-            }
-            dft<R>(v[b], inv);
-            dst[b] = (j - jm) * R + jm;  // (j / Ns) Ns R + j % Ns
-            row[b] = s * LS;
-        }
-    }
-    __syncthreads();
-#pragma unroll
-    for (int b = 0; b < MAXB; ++b)
-        if (dst[b] >= 0) {
-#pragma unroll
-            for (int r = 0; r < R; ++r) buf[row[b] + pd(dst[b] + r * Ns)] = v[b][r];
-        }
-    __syncthreads();
-}
-
-__device__ void fft_seq(double2* buf, const SeqPlan& p, int LS, bool inv) {
-    for (int s = 0; s < p.nst; ++s) {
-        const int R = p.radix[s], Ns = p.ns[s];
-        const double2* tw = p.tw[s];
-        switch (R) {
-            // MAXB = ceil(kFftMaxElems / (R kFftThreads))
-            case 8: fft_stage<8, 1>(buf, p.cnt, p.L, LS, Ns, tw, inv); break;
-            case 5: fft_stage<5, 2>(buf, p.cnt, p.L, LS, Ns, tw, inv); break;
-            case 4: fft_stage<4, 2>(buf, p.cnt, p.L, LS, Ns, tw, inv); break;
-            case 3: fft_stage<3, 3>(buf, p.cnt, p.L, LS, Ns, tw, inv); break;
-            default: fft_stage<2, 4>(buf, p.cnt, p.L, LS, Ns, tw, inv); break;
-        }
-    }
-}
-
-// w_N^{p}, p in [0, N): hi[p >> 10] * lo[p & 1023]
-__device__ __forceinline__ double2 twiddle_n(int64_t p, const double2* __restrict__ lo,
-                                             const double2* __restrict__ hi, bool conj) {
-    double2 w = cmul(__ldg(hi + (p >> 10)), __ldg(lo + (p & 1023)));
-    if (conj) w.y = -w.y;
+// w_R^{e} (conjugated for the inverse), e a compile-time constant after unrolling
+template <int R, bool INV>
+__device__ __forceinline__ double2 wr(int e) {
+    double2 w = c_w400[(e % R) * (400 / R)];
+    if (INV) w.y = -w.y;
     return w;
 }
 
-// window column c of the (Nsw+1)m view
-__device__ __forceinline__ int64_t vcol(int64_t c, int per, int64_t ld, int64_t n) {
-    return (c / per) * ld + (c % per) * n;
+template <int R, bool INV>
+__device__ __forceinline__ void dft(double2 (&v)[R]);
+
+// In-register Cooley-Tukey DFT_{R1 R2}: input n = R2 n1 + n2, output k = k1 + R1 k2.
+template <int R1, int R2, bool INV>
+__device__ __forceinline__ void dft_ct(double2 (&v)[R1 * R2]) {
+    constexpr int R = R1 * R2;
+    double2 a[R2][R1];
+#pragma unroll
+    for (int n2 = 0; n2 < R2; ++n2) {
+#pragma unroll
+        for (int n1 = 0; n1 < R1; ++n1) a[n2][n1] = v[R2 * n1 + n2];
+        dft<R1, INV>(a[n2]);
+        if (n2 > 0) {
+#pragma unroll
+            for (int k1 = 1; k1 < R1; ++k1) a[n2][k1] = cmul(a[n2][k1], wr<R, INV>(n2 * k1));
+        }
+    }
+#pragma unroll
+    for (int k1 = 0; k1 < R1; ++k1) {
+        double2 b[R2];
+#pragma unroll
+        for (int n2 = 0; n2 < R2; ++n2) b[n2] = a[n2][k1];
+        dft<R2, INV>(b);
+#pragma unroll
+        for (int k2 = 0; k2 < R2; ++k2) v[k1 + R1 * k2] = b[k2];
+    }
 }
 
-struct PassArgs {
-    SeqPlan p;        // the length this pass transforms
-    int N1, N2;
-    int64_t N;
-    const int2* pairs;
-    int per;
-    const double2* tlo;
-    const double2* thi;
+// X_k = sum_r v_r exp(-+2 pi i r k / R)  (- forward, + inverse), in place
+template <int R, bool INV>
+__device__ __forceinline__ void dft(double2 (&v)[R]) {
+    if constexpr (R == 2) {
+        const double2 a = v[0], b = v[1];
+        v[0] = cadd(a, b);
+        v[1] = csub(a, b);
+    } else if constexpr (R == 4) {
+        const double2 t0 = cadd(v[0], v[2]), t1 = csub(v[0], v[2]);
+        const double2 t2 = cadd(v[1], v[3]), t3 = rot<INV>(csub(v[1], v[3]));
+        v[0] = cadd(t0, t2);
+        v[2] = csub(t0, t2);
+        v[1] = cadd(t1, t3);
+        v[3] = csub(t1, t3);
+    } else if constexpr (R == 5) {
+        constexpr double c1 = 0.30901699437494742410, c2 = -0.80901699437494742410;  // cos 2pi/5, cos 4pi/5
+        constexpr double s1 = 0.95105651629515357212, s2 = 0.58778525229247312917;   // sin 2pi/5, sin 4pi/5
+        const double2 t1 = cadd(v[1], v[4]), t2 = cadd(v[2], v[3]);
+        const double2 t3 = csub(v[1], v[4]), t4 = csub(v[2], v[3]);
+        const double2 x0 = v[0];
+        const double2 a1 = make_double2(fma(c2, t2.x, fma(c1, t1.x, x0.x)), fma(c2, t2.y, fma(c1, t1.y, x0.y)));
+        const double2 a2 = make_double2(fma(c1, t2.x, fma(c2, t1.x, x0.x)), fma(c1, t2.y, fma(c2, t1.y, x0.y)));
+        const double2 b1 = rot<INV>(make_double2(fma(s2, t4.x, s1 * t3.x), fma(s2, t4.y, s1 * t3.y)));
+        const double2 b2 = rot<INV>(make_double2(fma(-s1, t4.x, s2 * t3.x), fma(-s1, t4.y, s2 * t3.y)));
+        v[0] = make_double2(x0.x + t1.x + t2.x, x0.y + t1.y + t2.y);
+        v[1] = cadd(a1, b1);
+        v[4] = csub(a1, b1);
+        v[2] = cadd(a2, b2);
+        v[3] = csub(a2, b2);
+    } else if constexpr (R == 8) {
+        double2 e[4] = {v[0], v[2], v[4], v[6]}, o[4] = {v[1], v[3], v[5], v[7]};
+        dft<4, INV>(e);
+        dft<4, INV>(o);
+        constexpr double h = 0.70710678118654752440;  // 1/sqrt(2)
+        const double sg = INV ? 1.0 : -1.0;           // o_k *= w8^k, w8 = exp(-+ i pi / 4)
+        o[1] = make_double2(h * (o[1].x - sg * o[1].y), h * (o[1].y + sg * o[1].x));
+        o[2] = rot<INV>(o[2]);
+        o[3] = make_double2(h * (-o[3].x - sg * o[3].y), h * (-o[3].y + sg * o[3].x));
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            v[k] = cadd(e[k], o[k]);
+            v[k + 4] = csub(e[k], o[k]);
+        }
+    } else if constexpr (R == 10) {
+        dft_ct<2, 5, INV>(v);
+    } else if constexpr (R == 16) {
+        dft_ct<4, 4, INV>(v);
+    } else if constexpr (R == 20) {
+        dft_ct<4, 5, INV>(v);
+    } else if constexpr (R == 25) {
+        dft_ct<5, 5, INV>(v);
+    } else {
+        static_assert(R == 0, "unsupported radix");
+    }
+}
+
+// v[r] *= w^r, r = 1..R-1 (w^r by repeated multiplication: <= R ulp, far inside the
+// 1e-12 parity tolerance)
+template <int R>
+__device__ __forceinline__ void twiddle_pow(double2 (&v)[R], double2 w) {
+    double2 c = w;
+#pragma unroll
+    for (int r = 1; r < R; ++r) {
+        v[r] = cmul(v[r], c);
+        if (r + 1 < R) c = cmul(c, w);
+    }
+}
+
+// ---- tile views --------------------------------------------------------------------
+// Column tile (passes A / C): TC sequences (consecutive j1), length L along the strided
+// index; SMEM i-major, lanes sequence-fast, so every access is a contiguous run.
+template <int L_, int TC>
+struct ColView {
+    static constexpr int L = L_, S = TC, SMEM = L_ * TC;
+    template <int R>
+    __device__ static __forceinline__ void map(int q, int& seq, int& j) {
+        seq = q % TC;
+        j = q / TC;
+    }
+    __device__ static __forceinline__ int addr(int seq, int i) { return i * TC + seq; }
+};
+// Row tile (pass B): S contiguous rows of length L; lanes index-fast.  One pad slot per 32
+// elements breaks the stride-R store pattern of the first stages.
+template <int L_, int S_>
+struct RowView {
+    static constexpr int L = L_, S = S_, LP = L_ + L_ / 32 + 1, SMEM = S_ * LP;
+    template <int R>
+    __device__ static __forceinline__ void map(int q, int& seq, int& j) {
+        seq = q / (L_ / R);
+        j = q - seq * (L_ / R);
+    }
+    __device__ static __forceinline__ int addr(int seq, int i) { return seq * LP + i + (i >> 5); }
 };
 
-// Element loops run in batches of kB per thread with every load of the batch issued before
-// the first use (kB * kFftThreads = kFftMaxElems covers a whole CTA tile in one batch), so
-// each thread keeps kB global requests in flight instead of one.
-constexpr int kB = kFftMaxElems / kFftThreads;
+template <class V, int R>
+struct Shape {
+    static constexpr int LR = V::L / R;
+    static constexpr int NB = V::S * LR;  // butterflies per stage
+    static constexpr int BPT = (NB + kNT - 1) / kNT;
+    static constexpr bool FULL = NB % kNT == 0;
+};
 
-__global__ void __launch_bounds__(kFftThreads, 1) fft4_pass_a(const PassArgs pa, const double* __restrict__ V,
-                                                            int64_t ldv, double2* __restrict__ Y) {
-    extern __shared__ double2 fsm[];
-    __shared__ SeqPlan sp;
-    if (threadIdx.x == 0) sp = pa.p;
-    const int cnt = pa.p.cnt, L = pa.p.L, LS = pd(L) + 1, total = cnt * L;
-    const int a0 = blockIdx.x * cnt, na = min(cnt, pa.N1 - a0);
-    const int2 cp = pa.pairs[blockIdx.y];
-    const double* x1 = V + vcol(cp.x, pa.per, ldv, pa.N);
-    const double* x2 = cp.y >= 0 ? V + vcol(cp.y, pa.per, ldv, pa.N) : x1;
-    const bool two = cp.y >= 0;
-    for (int base = threadIdx.x; base < total; base += kB * kFftThreads) {
-        double2 z[kB];
+// ---- Stockham stages ---------------------------------------------------------------
+// Stage of radix R after NS = R_0 ... R_{s-1}: butterfly j reads x[j + r L/R], multiplies
+// by w_{NS R}^{r (j % NS)}, DFT_R, writes y[(j - j % NS) R + j % NS + r NS].
+
+// first stage (NS = 1): inputs from ld(seq, index)
+template <class V, int R, bool INV, class Ld>
+__device__ __forceinline__ void stage_first(double2* sm, Ld ld) {
+    using SH = Shape<V, R>;
+    double2 v[SH::BPT][R];
 #pragma unroll
-        for (int u = 0; u < kB; ++u) {
-            const int idx = base + u * kFftThreads;
-            const int a = idx % cnt, n2 = idx / cnt;
-            const bool ok = idx < total && a < na;
-            const int64_t g = ok ? a0 + a + (int64_t)pa.N1 * n2 : 0;
-            z[u] = make_double2(ok ? x1[g] : 0.0, ok && two ? x2[g] : 0.0);
+    for (int b = 0; b < SH::BPT; ++b) {
+        const int q = threadIdx.x + b * kNT;
+        if (SH::FULL || q < SH::NB) {
+            int seq, j;
+            V::template map<R>(q, seq, j);
+#pragma unroll
+            for (int r = 0; r < R; ++r) v[b][r] = ld(seq, j + r * SH::LR);
         }
+    }
 #pragma unroll
-        for (int u = 0; u < kB; ++u) {
-            const int idx = base + u * kFftThreads;
-            if (idx < total) fsm[(idx % cnt) * LS + pd(idx / cnt)] = z[u];
+    for (int b = 0; b < SH::BPT; ++b) {
+        const int q = threadIdx.x + b * kNT;
+        if (SH::FULL || q < SH::NB) {
+            int seq, j;
+            V::template map<R>(q, seq, j);
+            dft<R, INV>(v[b]);
+#pragma unroll
+            for (int r = 0; r < R; ++r) sm[V::addr(seq, j * R + r)] = v[b][r];
         }
     }
     __syncthreads();
-    fft_seq(fsm, sp, LS, false);
-    double2* Yp = Y + (int64_t)blockIdx.y * pa.N;
-    for (int base = threadIdx.x; base < total; base += kB * kFftThreads) {
-        double2 w[kB];
+}
+
+// read + twiddle + DFT of one stage into registers; tw = w_L^e table (w_{NS R}^{jm} =
+// w_L^{jm L / (NS R)})
+template <class V, int R, int NS, bool INV>
+__device__ __forceinline__ void stage_read(const double2* sm, const double2* __restrict__ tw,
+                                           double2 (&v)[Shape<V, R>::BPT][R]) {
+    using SH = Shape<V, R>;
 #pragma unroll
-        for (int u = 0; u < kB; ++u) {  // n1 k2 < N: no reduction needed
-            const int idx = base + u * kFftThreads;
-            const int64_t a = idx % cnt, k2 = idx / cnt;
-            w[u] = idx < total ? twiddle_n((a0 + a) * k2, pa.tlo, pa.thi, false) : make_double2(0.0, 0.0);
+    for (int b = 0; b < SH::BPT; ++b) {
+        const int q = threadIdx.x + b * kNT;
+        if (SH::FULL || q < SH::NB) {
+            int seq, j;
+            V::template map<R>(q, seq, j);
+#pragma unroll
+            for (int r = 0; r < R; ++r) v[b][r] = sm[V::addr(seq, j + r * SH::LR)];
         }
+    }
 #pragma unroll
-        for (int u = 0; u < kB; ++u) {
-            const int idx = base + u * kFftThreads;
-            const int a = idx % cnt, k2 = idx / cnt;
-            if (idx < total && a < na) Yp[a0 + a + (int64_t)pa.N1 * k2] = cmul(fsm[a * LS + pd(k2)], w[u]);
+    for (int b = 0; b < SH::BPT; ++b) {
+        const int q = threadIdx.x + b * kNT;
+        if (SH::FULL || q < SH::NB) {
+            int seq, j;
+            V::template map<R>(q, seq, j);
+            if (NS > 1) {
+                const int jm = j % NS;
+                double2 w = __ldg(tw + jm * (V::L / (NS * R)));
+                if (INV) w.y = -w.y;
+                twiddle_pow<R>(v[b], w);
+            }
+            dft<R, INV>(v[b]);
         }
     }
 }
 
-__global__ void __launch_bounds__(kFftThreads, 1) fft4_pass_b(const PassArgs pa, const double* __restrict__ lamB,
-                                                            const double* __restrict__ lamQ, double2* __restrict__ Y) {
-    extern __shared__ double2 fsm[];
-    __shared__ SeqPlan sp;
-    if (threadIdx.x == 0) sp = pa.p;
-    const int cnt = pa.p.cnt, L = pa.p.L, LS = pd(L) + 1, total = cnt * L;  // L = N1
-    const int k0 = blockIdx.x * cnt, nk = min(cnt, pa.N2 - k0);
-    const int2 cp = pa.pairs[blockIdx.y];
-    const double* lam = (cp.x % pa.per == 0) ? lamB : lamQ;  // transposed: lamT[k1 + N1 k2]
-    double2* Yp = Y + (int64_t)blockIdx.y * pa.N;
-    for (int base = threadIdx.x; base < total; base += kB * kFftThreads) {
-        double2 z[kB];
+template <class V, int R, int NS>
+__device__ __forceinline__ void stage_write(double2* sm, const double2 (&v)[Shape<V, R>::BPT][R]) {
+    using SH = Shape<V, R>;
 #pragma unroll
-        for (int u = 0; u < kB; ++u) {
-            const int idx = base + u * kFftThreads;
-            const int r = idx / L, n1 = idx - r * L;
-            z[u] = (idx < total && r < nk) ? Yp[n1 + (int64_t)L * (k0 + r)] : make_double2(0.0, 0.0);
-        }
+    for (int b = 0; b < SH::BPT; ++b) {
+        const int q = threadIdx.x + b * kNT;
+        if (SH::FULL || q < SH::NB) {
+            int seq, j;
+            V::template map<R>(q, seq, j);
+            const int jm = j % NS, base = (j - jm) * R + jm;
 #pragma unroll
-        for (int u = 0; u < kB; ++u) {
-            const int idx = base + u * kFftThreads;
-            if (idx < total) fsm[(idx / L) * LS + pd(idx % L)] = z[u];
-        }
-    }
-    __syncthreads();
-    fft_seq(fsm, sp, LS, false);
-    for (int base = threadIdx.x; base < total; base += kB * kFftThreads) {
-        double l[kB];
-#pragma unroll
-        for (int u = 0; u < kB; ++u) {
-            const int idx = base + u * kFftThreads;
-            const int r = idx / L, k1 = idx - r * L;
-            l[u] = (idx < total && r < nk) ? __ldg(lam + k1 + (int64_t)L * (k0 + r)) : 0.0;
-        }
-#pragma unroll
-        for (int u = 0; u < kB; ++u) {
-            const int idx = base + u * kFftThreads;
-            if (idx >= total) continue;
-            double2& zz = fsm[(idx / L) * LS + pd(idx % L)];
-            zz = make_double2(l[u] * zz.x, l[u] * zz.y);
-        }
-    }
-    __syncthreads();
-    fft_seq(fsm, sp, LS, true);
-    for (int base = threadIdx.x; base < total; base += kB * kFftThreads) {
-        double2 w[kB];
-#pragma unroll
-        for (int u = 0; u < kB; ++u) {
-            const int idx = base + u * kFftThreads;
-            const int64_t r = idx / L, n1 = idx - r * L;
-            w[u] = idx < total ? twiddle_n(n1 * (k0 + r), pa.tlo, pa.thi, true) : make_double2(0.0, 0.0);
-        }
-#pragma unroll
-        for (int u = 0; u < kB; ++u) {
-            const int idx = base + u * kFftThreads;
-            const int r = idx / L, n1 = idx - r * L;
-            if (idx < total && r < nk) Yp[n1 + (int64_t)L * (k0 + r)] = cmul(fsm[r * LS + pd(n1)], w[u]);
+            for (int r = 0; r < R; ++r) sm[V::addr(seq, base + r * NS)] = v[b][r];
         }
     }
 }
 
-__global__ void __launch_bounds__(kFftThreads, 1) fft4_pass_a_inv(const PassArgs pa, const double2* __restrict__ Y,
-                                                                double* __restrict__ out, int64_t ldo,
-                                                                const double* __restrict__ add, int64_t ldadd,
-                                                                unsigned* status) {
-    extern __shared__ double2 fsm[];
-    __shared__ SeqPlan sp;
-    if (threadIdx.x == 0) sp = pa.p;
-    const int cnt = pa.p.cnt, L = pa.p.L, LS = pd(L) + 1, total = cnt * L;  // L = N2
-    const int a0 = blockIdx.x * cnt, na = min(cnt, pa.N1 - a0);
-    const int2 cp = pa.pairs[blockIdx.y];
-    const double2* Yp = Y + (int64_t)blockIdx.y * pa.N;
-    for (int base = threadIdx.x; base < total; base += kB * kFftThreads) {
-        double2 z[kB];
+template <class V, int R, int NS, bool INV>
+__device__ __forceinline__ void stage_mid(double2* sm, const double2* __restrict__ tw) {
+    double2 v[Shape<V, R>::BPT][R];
+    stage_read<V, R, NS, INV>(sm, tw, v);
+    __syncthreads();
+    stage_write<V, R, NS>(sm, v);
+    __syncthreads();
+}
+
+template <int... R>
+struct RL {};
+template <class V, bool INV, int NS, class List>
+struct Mids;
+template <class V, bool INV, int NS>
+struct Mids<V, INV, NS, RL<>> {
+    static constexpr int NS_OUT = NS;
+    __device__ static __forceinline__ void run(double2*, const double2*) {}
+};
+template <class V, bool INV, int NS, int R, int... Rest>
+struct Mids<V, INV, NS, RL<R, Rest...>> {
+    static constexpr int NS_OUT = Mids<V, INV, NS * R, RL<Rest...>>::NS_OUT;
+    __device__ static __forceinline__ void run(double2* sm, const double2* tw) {
+        stage_mid<V, R, NS, INV>(sm, tw);
+        Mids<V, INV, NS * R, RL<Rest...>>::run(sm, tw);
+    }
+};
+
+// last stage (NS R = L): outputs at index j + r L/R go to st(seq, j, v[R])
+template <class V, int R, bool INV, class St>
+__device__ __forceinline__ void stage_last(const double2* sm, const double2* __restrict__ tw, St st) {
+    using SH = Shape<V, R>;
+    double2 v[SH::BPT][R];
+    stage_read<V, R, SH::LR, INV>(sm, tw, v);
 #pragma unroll
-        for (int u = 0; u < kB; ++u) {
-            const int idx = base + u * kFftThreads;
-            const int a = idx % cnt, k2 = idx / cnt;
-            z[u] = (idx < total && a < na) ? Yp[a0 + a + (int64_t)pa.N1 * k2] : make_double2(0.0, 0.0);
+    for (int b = 0; b < SH::BPT; ++b) {
+        const int q = threadIdx.x + b * kNT;
+        if (SH::FULL || q < SH::NB) {
+            int seq, j;
+            V::template map<R>(q, seq, j);
+            st(seq, j, v[b]);
         }
+    }
+}
+
+// forward last stage, spectrum product mul(seq, j, v[R]) on index j + r L/R, inverse first
+// stage (same butterfly positions), exchange
+template <class V, int R, class Mul>
+__device__ __forceinline__ void stage_turn(double2* sm, const double2* __restrict__ tw, Mul mul) {
+    using SH = Shape<V, R>;
+    double2 v[SH::BPT][R];
+    stage_read<V, R, SH::LR, false>(sm, tw, v);
 #pragma unroll
-        for (int u = 0; u < kB; ++u) {
-            const int idx = base + u * kFftThreads;
-            if (idx < total) fsm[(idx % cnt) * LS + pd(idx / cnt)] = z[u];
+    for (int b = 0; b < SH::BPT; ++b) {
+        const int q = threadIdx.x + b * kNT;
+        if (SH::FULL || q < SH::NB) {
+            int seq, j;
+            V::template map<R>(q, seq, j);
+            mul(seq, j, v[b]);
+            dft<R, true>(v[b]);
         }
     }
     __syncthreads();
-    fft_seq(fsm, sp, LS, true);
-    double* o1 = out + vcol(cp.x, pa.per, ldo, pa.N);
-    double* o2 = cp.y >= 0 ? out + vcol(cp.y, pa.per, ldo, pa.N) : nullptr;
-    const double* d1 = add ? add + vcol(cp.x, pa.per, ldadd, pa.N) : nullptr;
-    const double* d2 = (add && cp.y >= 0) ? add + vcol(cp.y, pa.per, ldadd, pa.N) : nullptr;
-    const double inv_n = 1.0 / (double)pa.N;
+    stage_write<V, R, 1>(sm, v);
+    __syncthreads();
+}
+
+// ---- plans ---------------------------------------------------------------------------
+// N1: contiguous length (pass B, S rows per item), radices B0, BM..., BL (BMr = BM reversed).
+// N2: strided length (passes A / C, TC columns per item), radices A0, AM..., AL.
+struct PlanE6 {  // n = 1e6 (C4)
+    static constexpr int N1 = 4000, N2 = 250, TC = 16, S = 1;
+    static constexpr int A0 = 10, AL = 5, B0 = 20, BL = 10;
+    using AM = RL<5>;
+    using AMr = RL<5>;
+    using BM = RL<20>;
+    using BMr = RL<20>;
+};
+struct Plan2E6 {  // n = 2e6 (C5)
+    static constexpr int N1 = 4000, N2 = 500, TC = 8, S = 1;
+    static constexpr int A0 = 10, AL = 10, B0 = 20, BL = 10;
+    using AM = RL<5>;
+    using AMr = RL<5>;
+    using BM = RL<20>;
+    using BMr = RL<20>;
+};
+struct PlanE5 {  // n = 1e5 (C3)
+    static constexpr int N1 = 400, N2 = 250, TC = 16, S = 10;
+    static constexpr int A0 = 10, AL = 5, B0 = 20, BL = 20;
+    using AM = RL<5>;
+    using AMr = RL<5>;
+    using BM = RL<>;
+    using BMr = RL<>;
+};
+struct PlanE4 {  // n = 1e4 (parity tests; partial stages)
+    static constexpr int N1 = 400, N2 = 25, TC = 16, S = 5;
+    static constexpr int A0 = 5, AL = 5, B0 = 20, BL = 20;
+    using AM = RL<>;
+    using AMr = RL<>;
+    using BM = RL<>;
+    using BMr = RL<>;
+};
+
+struct Job {
+    const double* V;
+    int64_t ldv;
+    double* out;
+    int64_t ldo;
+    const double* add;
+    int64_t ldadd;
+    unsigned* status;
+    const int2* pairs;
+    int np, per, G, ngroups;
+    const double* lamB;  // lamT[k1 + N1 k2] = lam[k2 + N2 k1] / N
+    const double* lamQ;
+    double2* Y;          // kSlots x G x N
+    const double2* tw1;  // w_N1^e
+    const double2* tw2;  // w_N2^e
+    const double2* tlo;  // w_N^{p & 1023}
+    const double2* thi;  // w_N^{(p >> 10) 1024}
+    unsigned* ctr;       // [0] ticket, [1 + 3 g + phase] completed items of group g
+};
+
+__device__ __forceinline__ double2 wN(const Job& jb, int64_t p) {  // w_N^p, 0 <= p < N
+    return cmul(__ldg(jb.thi + (p >> 10)), __ldg(jb.tlo + (p & 1023)));
+}
+
+// window column c of the (Nsw+1)m view
+__device__ __forceinline__ int64_t vcol(int c, int per, int64_t ld, int64_t n) {
+    return (int64_t)(c / per) * ld + (int64_t)(c % per) * n;
+}
+
+__device__ __forceinline__ unsigned ld_relaxed(const unsigned* p) {
+    unsigned v;
+    asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void red_release(unsigned* p) {
+    asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(p) : "memory");
+}
+
+template <class P>
+__device__ __forceinline__ void item_a(const Job& jb, double2* sm, int p, int tile) {
+    using VA = ColView<P::N2, P::TC>;
+    constexpr int64_t N = (int64_t)P::N1 * P::N2;
+    const int2 cp = jb.pairs[p];
+    const double* x1 = jb.V + vcol(cp.x, jb.per, jb.ldv, N);
+    const double* x2 = cp.y >= 0 ? jb.V + vcol(cp.y, jb.per, jb.ldv, N) : nullptr;
+    double2* Yp = jb.Y + ((int64_t)((p / jb.G) % kSlots) * jb.G + p % jb.G) * N;
+    const int j10 = tile * P::TC;
+    if (x2) {
+        stage_first<VA, P::A0, false>(sm, [&](int seq, int i) {
+            const int64_t g = j10 + seq + (int64_t)P::N1 * i;
+            return make_double2(__ldcs(x1 + g), __ldcs(x2 + g));
+        });
+    } else {
+        stage_first<VA, P::A0, false>(sm, [&](int seq, int i) {
+            return make_double2(__ldcs(x1 + j10 + seq + (int64_t)P::N1 * i), 0.0);
+        });
+    }
+    Mids<VA, false, P::A0, typename P::AM>::run(sm, jb.tw2);
+    constexpr int LR = P::N2 / P::AL;
+    stage_last<VA, P::AL, false>(sm, jb.tw2, [&](int seq, int j, double2(&v)[P::AL]) {
+        const int64_t j1 = j10 + seq;
+        double2 w = wN(jb, j1 * j);
+        const double2 ws = wN(jb, j1 * LR);
+#pragma unroll
+        for (int r = 0; r < P::AL; ++r) {
+            __stcg(Yp + j1 + (int64_t)P::N1 * (j + r * LR), cmul(v[r], w));
+            if (r + 1 < P::AL) w = cmul(w, ws);
+        }
+    });
+}
+
+template <class P>
+__device__ __forceinline__ void item_b(const Job& jb, double2* sm, int p, int rowblk) {
+    using VB = RowView<P::N1, P::S>;
+    constexpr int64_t N = (int64_t)P::N1 * P::N2;
+    const int2 cp = jb.pairs[p];
+    const double* lam = (cp.x % jb.per == 0) ? jb.lamB : jb.lamQ;
+    double2* Yp = jb.Y + ((int64_t)((p / jb.G) % kSlots) * jb.G + p % jb.G) * N;
+    const int k20 = rowblk * P::S;
+    stage_first<VB, P::B0, false>(sm, [&](int seq, int i) {
+        return __ldcg(Yp + (int64_t)P::N1 * (k20 + seq) + i);
+    });
+    Mids<VB, false, P::B0, typename P::BM>::run(sm, jb.tw1);
+    constexpr int LRt = P::N1 / P::BL;
+    stage_turn<VB, P::BL>(sm, jb.tw1, [&](int seq, int j, double2(&v)[P::BL]) {
+        const double* lr = lam + (int64_t)P::N1 * (k20 + seq) + j;
+#pragma unroll
+        for (int r = 0; r < P::BL; ++r) {
+            const double l = __ldg(lr + r * LRt);
+            v[r] = make_double2(l * v[r].x, l * v[r].y);
+        }
+    });
+    Mids<VB, true, P::BL, typename P::BMr>::run(sm, jb.tw1);
+    constexpr int LR = P::N1 / P::B0;
+    stage_last<VB, P::B0, true>(sm, jb.tw1, [&](int seq, int j, double2(&v)[P::B0]) {
+        const int64_t k2 = k20 + seq;
+        double2 w = conj2(wN(jb, j * k2));
+        const double2 ws = conj2(wN(jb, LR * k2));
+        double2* yr = Yp + (int64_t)P::N1 * k2 + j;
+#pragma unroll
+        for (int r = 0; r < P::B0; ++r) {
+            __stcg(yr + r * LR, cmul(v[r], w));
+            if (r + 1 < P::B0) w = cmul(w, ws);
+        }
+    });
+}
+
+template <class P>
+__device__ __forceinline__ void item_c(const Job& jb, double2* sm, int p, int tile) {
+    using VA = ColView<P::N2, P::TC>;
+    constexpr int64_t N = (int64_t)P::N1 * P::N2;
+    const int2 cp = jb.pairs[p];
+    const double2* Yp = jb.Y + ((int64_t)((p / jb.G) % kSlots) * jb.G + p % jb.G) * N;
+    const int j10 = tile * P::TC;
+    stage_first<VA, P::AL, true>(sm, [&](int seq, int i) {
+        return __ldcg(Yp + j10 + seq + (int64_t)P::N1 * i);
+    });
+    Mids<VA, true, P::AL, typename P::AMr>::run(sm, jb.tw2);
+    double* o1 = jb.out + vcol(cp.x, jb.per, jb.ldo, N) + j10;
+    double* o2 = cp.y >= 0 ? jb.out + vcol(cp.y, jb.per, jb.ldo, N) + j10 : nullptr;
+    const double* d1 = jb.add ? jb.add + vcol(cp.x, jb.per, jb.ldadd, N) + j10 : nullptr;
+    const double* d2 = (jb.add && cp.y >= 0) ? jb.add + vcol(cp.y, jb.per, jb.ldadd, N) + j10 : nullptr;
+    constexpr int LR = P::N2 / P::A0;
     bool bad = false;
-    for (int base = threadIdx.x; base < total; base += kB * kFftThreads) {
-        double ad1[kB], ad2[kB];
+    stage_last<VA, P::A0, true>(sm, jb.tw2, [&](int seq, int j, double2(&v)[P::A0]) {
+        // add-term loads all issued before the first store (out may alias add, so the
+        // compiler cannot hoist them across the stores itself)
+        double a1[P::A0], a2[P::A0];
 #pragma unroll
-        for (int u = 0; u < kB; ++u) {  // addend loads first (out = v + D^{1/2} s, operators.cpp:141)
-            const int idx = base + u * kFftThreads;
-            const int a = idx % cnt, n2 = idx / cnt;
-            const bool ok = idx < total && a < na;
-            const int64_t g = ok ? a0 + a + (int64_t)pa.N1 * n2 : 0;
-            ad1[u] = (ok && d1) ? d1[g] : 0.0;
-            ad2[u] = (ok && d2) ? d2[g] : 0.0;
+        for (int r = 0; r < P::A0; ++r) {
+            const int64_t g = seq + (int64_t)P::N1 * (j + r * LR);
+            a1[r] = d1 ? __ldcs(d1 + g) : 0.0;
+            a2[r] = d2 ? __ldcs(d2 + g) : 0.0;
         }
 #pragma unroll
-        for (int u = 0; u < kB; ++u) {
-            const int idx = base + u * kFftThreads;
-            const int a = idx % cnt, n2 = idx / cnt;
-            if (idx >= total || a >= na) continue;
-            const int64_t g = a0 + a + (int64_t)pa.N1 * n2;
-            const double2 z = fsm[a * LS + pd(n2)];
-            double y1 = z.x * inv_n, y2 = z.y * inv_n;
-            if (d1) {
-                y1 = ad1[u] + y1;
+        for (int r = 0; r < P::A0; ++r) {
+            const int64_t g = seq + (int64_t)P::N1 * (j + r * LR);
+            double y1 = v[r].x, y2 = v[r].y;
+            if (d1) {  // out = v + D^{1/2} s (operators.cpp:141)
+                y1 = a1[r] + y1;
                 bad |= !isfinite(y1);
             }
-            o1[g] = y1;
+            __stcs(o1 + g, y1);
             if (o2) {
                 if (d2) {
-                    y2 = ad2[u] + y2;
+                    y2 = a2[r] + y2;
                     bad |= !isfinite(y2);
                 }
-                o2[g] = y2;
+                __stcs(o2 + g, y2);
             }
         }
-    }
-    if (status && __syncthreads_or(bad) && threadIdx.x == 0) atomicOr(status, ST_OUT_NONFINITE);
+    });
+    if (jb.status && bad) atomicOr(jb.status, ST_OUT_NONFINITE);
 }
 
-// lamT[k1 + N1 k2] = Re spec[min(k, N - k)], k = k2 + N2 k1 (real even spectrum)
+template <class P>
+__global__ void __launch_bounds__(kNT, kCtaPerSm) fftconv_kernel(const Job jb) {
+    extern __shared__ double2 sm[];
+    __shared__ unsigned s_ticket;
+    constexpr int nA1 = P::N1 / P::TC, nB1 = P::N2 / P::S;  // items per pair
+    const int nA = jb.G * nA1, nB = jb.G * nB1, nC = nA;
+    const unsigned stepN = (unsigned)(nA + nB + nC);
+    const unsigned total = stepN * (unsigned)(jb.ngroups + 2);
+    // decode ticket t into (phase, group, item): step s = {A(s), B(s - 1), C(s - 2)}
+    auto decode = [&](unsigned t, int& phase, int& g, int& r) {
+        const int s = (int)(t / stepN);
+        r = (int)(t - (unsigned)s * stepN);
+        if (r < nA) {
+            phase = 0;
+            g = s;
+        } else if (r < nA + nB) {
+            phase = 1;
+            g = s - 1;
+            r -= nA;
+        } else {
+            phase = 2;
+            g = s - 2;
+            r -= nA + nB;
+        }
+    };
+    unsigned next = 0;
+    if (threadIdx.x == 0) next = atomicAdd(jb.ctr, 1u);
+    for (;;) {
+        if (threadIdx.x == 0) {
+            // dependency: A(g) reuses the Y slot of C(g - kSlots); B(g) needs A(g); C(g) needs
+            // B(g).  Relaxed polling, then one acquire fence.
+            if (next < total) {
+                int phase, g, r;
+                decode(next, phase, g, r);
+                const unsigned* dep = nullptr;
+                unsigned need = 0;
+                if (g >= 0 && g < jb.ngroups) {
+                    if (phase == 0 && g >= kSlots) {
+                        dep = jb.ctr + 1 + 3 * (g - kSlots) + 2;
+                        need = (unsigned)nC;
+                    } else if (phase == 1) {
+                        dep = jb.ctr + 1 + 3 * g + 0;
+                        need = (unsigned)nA;
+                    } else if (phase == 2) {
+                        dep = jb.ctr + 1 + 3 * g + 1;
+                        need = (unsigned)nB;
+                    }
+                }
+                if (dep) {
+                    while (ld_relaxed(dep) < need) __nanosleep(64);
+                    asm volatile("fence.acq_rel.gpu;" ::: "memory");
+                }
+            }
+            s_ticket = next;
+        }
+        __syncthreads();  // ticket published, dependency met, previous item's SMEM reads done
+        const unsigned t = s_ticket;
+        if (t >= total) break;
+        if (threadIdx.x == 0) next = atomicAdd(jb.ctr, 1u);  // prefetch: consumed after this item
+        int phase, g, r;
+        decode(t, phase, g, r);
+        const bool valid = g >= 0 && g < jb.ngroups;
+        if (valid) {
+            // pair index and the item inside it; groups are G consecutive pairs
+            const int per_pair = phase == 1 ? nB1 : nA1;
+            const int p = g * jb.G + r / per_pair, idx = r % per_pair;
+            if (p < jb.np) {  // the last group may be partial
+                if (phase == 0)
+                    item_a<P>(jb, sm, p, idx);
+                else if (phase == 1)
+                    item_b<P>(jb, sm, p, idx);
+                else
+                    item_c<P>(jb, sm, p, idx);
+            }
+        }
+        __syncthreads();  // every store of the item issued; s_ticket read by every thread
+        if (threadIdx.x == 0 && valid) red_release(jb.ctr + 1 + 3 * g + phase);
+    }
+}
+
+// lamT[k1 + N1 k2] = Re spec[min(k, N - k)] / N, k = k2 + N2 k1 (real even spectrum)
 __global__ void build_lam_kernel(int64_t N, int N1, int N2, const double2* __restrict__ spec, double* __restrict__ lamT) {
+    const double inv_n = 1.0 / (double)N;
     for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < N; e += (int64_t)gridDim.x * blockDim.x) {
         const int64_t k1 = e % N1, k2 = e / N1;
         const int64_t k = k2 + (int64_t)N2 * k1;
-        lamT[e] = spec[k <= N - k ? k : N - k].x;
+        lamT[e] = spec[k <= N - k ? k : N - k].x * inv_n;
     }
 }
 
-bool smooth(int64_t L) {
-    for (int r : {2, 3, 5})
-        while (L % r == 0) L /= r;
-    return L == 1;
+template <class P>
+constexpr size_t smem_bytes() {
+    return sizeof(double2) * (size_t)std::max(ColView<P::N2, P::TC>::SMEM, RowView<P::N1, P::S>::SMEM);
 }
 
-// radices 8, 5, 4, 3, 2 greedily (largest butterflies first)
-bool build_seq(int L, SeqPlan& p, std::vector<double2>& tab, std::vector<int64_t>& offs) {
-    p.L = L;
-    p.nst = 0;
-    p.cnt = std::max(1, std::min(8, kFftMaxElems / L));
-    int rem = L, Ns = 1;
-    for (int r : {8, 5, 4, 3, 2}) {
-        while (rem % r == 0) {
-            if (p.nst >= 12) return false;
-            p.radix[p.nst] = r;
-            p.ns[p.nst] = Ns;
-            offs.push_back((int64_t)tab.size());
-            const long double two_pi = 6.283185307179586476925286766559L;
-            for (int jm = 0; jm < Ns; ++jm)
-                for (int q = 0; q < r; ++q) {
-                    const int64_t k = ((int64_t)q * jm) % ((int64_t)Ns * r);
-                    const long double ang = -two_pi * (long double)k / (long double)(Ns * r);
-                    tab.push_back(make_double2((double)cosl(ang), (double)sinl(ang)));
-                }
-            ++p.nst;
-            Ns *= r;
-            rem /= r;
-        }
+template <class P>
+void launch(const Job& jb, cudaStream_t st) {
+    constexpr size_t sm = smem_bytes<P>();
+    static_assert(sm <= 227 * 1024 / kCtaPerSm, "fftconv tile exceeds the per-CTA SMEM budget");
+    static bool attr = false;
+    if (!attr) {
+        W4_CUDA(cudaFuncSetAttribute(fftconv_kernel<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+        attr = true;
     }
-    return rem == 1;
+    int dev = 0, nsm = kSMs, occ = 0;
+    W4_CUDA(cudaGetDevice(&dev));
+    W4_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
+    W4_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fftconv_kernel<P>, kNT, sm));
+    const int64_t items = (int64_t)(jb.ngroups + 2) * jb.G * (2 * (P::N1 / P::TC) + P::N2 / P::S);
+    const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(items, (int64_t)nsm * std::max(occ, 1)));
+    fftconv_kernel<P><<<grid, kNT, sm, st>>>(jb);
+    W4_LAUNCH();
 }
+
+struct PlanInfo {
+    int64_t N1, N2;
+    size_t smem;
+    void (*run)(const Job&, cudaStream_t);
+};
+const PlanInfo kPlans[] = {
+    {PlanE6::N1, PlanE6::N2, smem_bytes<PlanE6>(), launch<PlanE6>},
+    {Plan2E6::N1, Plan2E6::N2, smem_bytes<Plan2E6>(), launch<Plan2E6>},
+    {PlanE5::N1, PlanE5::N2, smem_bytes<PlanE5>(), launch<PlanE5>},
+    {PlanE4::N1, PlanE4::N2, smem_bytes<PlanE4>(), launch<PlanE4>},
+};
 
 }  // namespace
 
@@ -417,52 +669,61 @@ Fft4::~Fft4() {
 }
 
 bool Fft4::init(int64_t N, const double2* const spec_half[4], cudaStream_t st) {
-    if (N < 64 || !smooth(N)) return false;
-    int best1 = 0;
-    const double rt = std::sqrt((double)N);
-    for (int64_t d = 2; d <= kFftMaxElems && d < N; ++d) {
-        if (N % d) continue;
-        const int64_t e = N / d;
-        if (e > kFftMaxElems || !smooth(d) || !smooth(e)) continue;
-        if (!best1 || std::fabs((double)d - rt) < std::fabs((double)best1 - rt)) best1 = (int)d;
-    }
-    if (!best1) return false;
-    const int N1 = best1, N2 = (int)(N / best1);
-    std::vector<double2> tab;
-    std::vector<int64_t> o1, o2;
-    SeqPlan p1, p2;
-    if (!build_seq(N1, p1, tab, o1) || !build_seq(N2, p2, tab, o2)) return false;
-    // four-step twiddles w_N^p = hi[p >> 10] * lo[p & 1023]
-    const int64_t off_lo = (int64_t)tab.size();
+    int plan = -1;
+    for (int i = 0; i < (int)(sizeof(kPlans) / sizeof(kPlans[0])); ++i)
+        if (kPlans[i].N1 * kPlans[i].N2 == N) plan = i;
+    if (plan < 0) return false;
+    const int64_t N1 = kPlans[plan].N1, N2 = kPlans[plan].N2;
     const long double two_pi = 6.283185307179586476925286766559L;
-    for (int q = 0; q < 1024; ++q) {
-        const long double ang = -two_pi * (long double)(q % N) / (long double)N;
-        tab.push_back(make_double2((double)cosl(ang), (double)sinl(ang)));
+    // in-register DFT twiddles (constant bank), once per process
+    static bool cw = false;
+    if (!cw) {
+        double2 w[400];
+        for (int e = 0; e < 400; ++e) {
+            const long double a = -two_pi * (long double)e / 400.0L;
+            w[e] = make_double2((double)cosl(a), (double)sinl(a));
+        }
+        W4_CUDA(cudaMemcpyToSymbol(c_w400, w, sizeof(w)));
+        cw = true;
     }
-    const int64_t off_hi = (int64_t)tab.size();
+    std::vector<double2> tab;
+    auto push_len = [&](int64_t L) {
+        const int64_t off = (int64_t)tab.size();
+        for (int64_t e = 0; e < L; ++e) {
+            const long double a = -two_pi * (long double)e / (long double)L;
+            tab.push_back(make_double2((double)cosl(a), (double)sinl(a)));
+        }
+        return off;
+    };
+    const int64_t o1 = push_len(N1), o2 = push_len(N2);
+    const int64_t olo = (int64_t)tab.size();
+    for (int q = 0; q < 1024; ++q) {
+        const long double a = -two_pi * (long double)(q % N) / (long double)N;
+        tab.push_back(make_double2((double)cosl(a), (double)sinl(a)));
+    }
+    const int64_t ohi = (int64_t)tab.size();
     for (int64_t h = 0; h <= N / 1024; ++h) {
-        const long double ang = -two_pi * (long double)((h * 1024) % N) / (long double)N;
-        tab.push_back(make_double2((double)cosl(ang), (double)sinl(ang)));
+        const long double a = -two_pi * (long double)((h * 1024) % N) / (long double)N;
+        tab.push_back(make_double2((double)cosl(a), (double)sinl(a)));
     }
     W4_CUDA(cudaMalloc(&tables_, sizeof(double2) * tab.size()));
     W4_CUDA(cudaMemcpyAsync(tables_, tab.data(), sizeof(double2) * tab.size(), cudaMemcpyHostToDevice, st));
-    for (int s = 0; s < p1.nst; ++s) p1.tw[s] = tables_ + o1[s];
-    for (int s = 0; s < p2.nst; ++s) p2.tw[s] = tables_ + o2[s];
-    tw_lo_ = tables_ + off_lo;
-    tw_hi_ = tables_ + off_hi;
+    tw1_ = tables_ + o1;
+    tw2_ = tables_ + o2;
+    tlo_ = tables_ + olo;
+    thi_ = tables_ + ohi;
     for (int i = 0; i < 4; ++i) {
         if (!spec_half[i]) continue;
         W4_CUDA(cudaMalloc(&lam_[i], sizeof(double) * N));
-        build_lam_kernel<<<(unsigned)std::min<int64_t>(cdiv(N, 256), 4096), 256, 0, st>>>(N, N1, N2, spec_half[i],
-                                                                                            lam_[i]);
+        build_lam_kernel<<<(unsigned)std::min<int64_t>(cdiv(N, 256), 4096), 256, 0, st>>>(N, (int)N1, (int)N2,
+                                                                                            spec_half[i], lam_[i]);
         W4_LAUNCH();
     }
     W4_CUDA(cudaStreamSynchronize(st));  // tab is freed on return
     N_ = N;
     N1_ = N1;
     N2_ = N2;
-    p1_ = p1;
-    p2_ = p2;
+    plan_ = plan;
     return true;
 }
 
@@ -474,6 +735,7 @@ void Fft4::apply(bool inv, int Nsw, const double* V, int64_t ldv, int64_t m, dou
     require(lamB && lamQ, "apply_D_half_inv: inverse factors were not provided");
     const int per = Nsw + 1;
     const int64_t ncols = (int64_t)per * m;
+    require(ncols < (int64_t)1 << 30, "circulant apply: too many columns");
     // pair window columns that use the same factor: the i = 0 blocks (B) and the rest (Q)
     std::vector<int2> pairs;
     for (int kind = 0; kind < 2; ++kind) {
@@ -489,8 +751,7 @@ void Fft4::apply(bool inv, int Nsw, const double* V, int64_t ldv, int64_t m, dou
         }
         if (pend >= 0) pairs.push_back(make_int2((int)pend, -1));
     }
-    const int64_t np = (int64_t)pairs.size();
-    require(ncols < (int64_t)1 << 31, "circulant apply: too many columns");
+    const int np = (int)pairs.size();
     // the pair table depends only on (m, Nsw): upload once per shape (the caller holds the
     // operator lock, so the cache is not shared between concurrent applies)
     int2* dpairs = pairbuf.get<int2>((size_t)np);
@@ -501,27 +762,20 @@ void Fft4::apply(bool inv, int Nsw, const double* V, int64_t ldv, int64_t m, dou
         pairs_per_ = per;
         pairs_ptr_ = dpairs;
     }
-    double2* Y = ybuf.get<double2>((size_t)np * N_);
-    PassArgs pa{p2_, N1_, N2_, N_, dpairs, per, tw_lo_, tw_hi_};
-    const size_t sm2 = sizeof(double2) * (size_t)p2_.cnt * (p2_.L + p2_.L / 8 + 1);
-    const size_t sm1 = sizeof(double2) * (size_t)p1_.cnt * (p1_.L + p1_.L / 8 + 1);
-    static bool attr = false;
-    if (!attr) {
-        W4_CUDA(cudaFuncSetAttribute(fft4_pass_a, cudaFuncAttributeMaxDynamicSharedMemorySize, 80 * 1024));
-        W4_CUDA(cudaFuncSetAttribute(fft4_pass_b, cudaFuncAttributeMaxDynamicSharedMemorySize, 80 * 1024));
-        W4_CUDA(cudaFuncSetAttribute(fft4_pass_a_inv, cudaFuncAttributeMaxDynamicSharedMemorySize, 80 * 1024));
-        attr = true;
-    }
-    const dim3 ga((unsigned)cdiv(N1_, p2_.cnt), (unsigned)np);
-    fft4_pass_a<<<ga, kFftThreads, sm2, st>>>(pa, V, ldv, Y);
-    W4_LAUNCH();
-    PassArgs pb = pa;
-    pb.p = p1_;
-    const dim3 gb((unsigned)cdiv(N2_, p1_.cnt), (unsigned)np);
-    fft4_pass_b<<<gb, kFftThreads, sm1, st>>>(pb, lamB, lamQ, Y);
-    W4_LAUNCH();
-    fft4_pass_a_inv<<<ga, kFftThreads, sm2, st>>>(pa, Y, out, ldo, add, ldadd, add ? status : nullptr);
-    W4_LAUNCH();
+    // G pairs per group: the Y slots (kSlots G 16 N bytes) stay within ~64 MB of L2
+    static const int g_env = [] {
+        const char* e = std::getenv("WC4DVAR_FFT_G");
+        return e ? std::atoi(e) : 0;
+    }();
+    int G = g_env > 0 ? g_env : (int)std::max<int64_t>(1, (64ll << 20) / (kSlots * 16 * N_));
+    G = std::min(G, np);
+    const int ngroups = (np + G - 1) / G;
+    double2* Y = ybuf.get<double2>((size_t)kSlots * G * N_);
+    unsigned* ctr = ctr_.get<unsigned>((size_t)1 + 3 * ngroups);
+    W4_CUDA(cudaMemsetAsync(ctr, 0, sizeof(unsigned) * (1 + 3 * (size_t)ngroups), st));
+    Job jb{V, ldv, out, ldo, add, ldadd, add ? status : nullptr, dpairs, np, per, G, ngroups,
+           lamB, lamQ, Y, tw1_, tw2_, tlo_, thi_, ctr};
+    kPlans[plan_].run(jb, st);
 }
 
 }  // namespace w4
