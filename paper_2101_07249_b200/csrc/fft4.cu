@@ -38,9 +38,12 @@
 namespace w4 {
 namespace {
 
-constexpr int kNT = 200;      // threads per CTA (every item kind)
+constexpr int kNT = 200;       // threads per CTA (butterfly mapping, every item kind)
+constexpr int kThreads = kNT;
 constexpr int kCtaPerSm = 2;  // CTAs per SM (register budget)
 constexpr int kSlots = 4;     // Y slots in flight: A(g) reuses the slot of C(g - 4), two steps earlier
+
+__device__ __forceinline__ void cbar() { __syncthreads(); }
 
 __constant__ double2 c_w400[400];  // exp(-2 pi i e / 400): every in-register DFT twiddle
 
@@ -225,7 +228,7 @@ __device__ __forceinline__ void stage_first(double2* sm, Ld ld) {
             for (int r = 0; r < R; ++r) sm[V::addr(seq, j * R + r)] = v[b][r];
         }
     }
-    __syncthreads();
+    cbar();
 }
 
 // read + twiddle + DFT of one stage into registers; tw = w_L^e table (w_{NS R}^{jm} =
@@ -281,13 +284,14 @@ template <class V, int R, int NS, bool INV>
 __device__ __forceinline__ void stage_mid(double2* sm, const double2* __restrict__ tw) {
     double2 v[Shape<V, R>::BPT][R];
     stage_read<V, R, NS, INV>(sm, tw, v);
-    __syncthreads();
+    cbar();
     stage_write<V, R, NS>(sm, v);
-    __syncthreads();
+    cbar();
 }
 
 template <int... R>
 struct RL {};
+
 template <class V, bool INV, int NS, class List>
 struct Mids;
 template <class V, bool INV, int NS>
@@ -338,9 +342,9 @@ __device__ __forceinline__ void stage_turn(double2* sm, const double2* __restric
             dft<R, true>(v[b]);
         }
     }
-    __syncthreads();
+    cbar();
     stage_write<V, R, 1>(sm, v);
-    __syncthreads();
+    cbar();
 }
 
 // ---- plans ---------------------------------------------------------------------------
@@ -397,6 +401,7 @@ struct Job {
     const double2* tlo;  // w_N^{p & 1023}
     const double2* thi;  // w_N^{(p >> 10) 1024}
     unsigned* ctr;       // [0] ticket, [1 + 3 g + phase] completed items of group g
+    int l2hint;          // evict_last policy on Y + discard after pass C (WC4DVAR_FFT_L2HINT)
 };
 
 __device__ __forceinline__ double2 wN(const Job& jb, int64_t p) {  // w_N^p, 0 <= p < N
@@ -413,6 +418,31 @@ __device__ __forceinline__ unsigned ld_relaxed(const unsigned* p) {
     asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
     return v;
 }
+// Y traffic stays in L2: stores / in-place loads with an evict_last policy, and pass C
+// discards each Y line after its last read (no write-back of dead data)
+__device__ __forceinline__ uint64_t policy_evict_last() {
+    uint64_t p;
+    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+    return p;
+}
+__device__ __forceinline__ double2 ld_y(const double2* a, uint64_t pol) {
+    if (!pol) return __ldcg(a);
+    double2 v;
+    asm volatile("ld.global.cg.L2::cache_hint.v2.f64 {%0, %1}, [%2], %3;" : "=d"(v.x), "=d"(v.y) : "l"(a), "l"(pol));
+    return v;
+}
+__device__ __forceinline__ void st_y(double2* a, double2 v, uint64_t pol) {
+    // no memory clobber: the compiler may keep interleaving the SMEM reads of later
+    // butterflies with these stores; the volatile cbar() that ends the item orders them
+    if (!pol) {
+        __stcg(a, v);
+        return;
+    }
+    asm volatile("st.global.cg.L2::cache_hint.v2.f64 [%0], {%1, %2}, %3;" ::"l"(a), "d"(v.x), "d"(v.y), "l"(pol));
+}
+__device__ __forceinline__ void discard_l2(const void* a) {
+    asm volatile("discard.global.L2 [%0], 128;" ::"l"(a) : "memory");
+}
 __device__ __forceinline__ void red_release(unsigned* p) {
     asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(p) : "memory");
 }
@@ -426,6 +456,7 @@ __device__ __forceinline__ void item_a(const Job& jb, double2* sm, int p, int ti
     const double* x2 = cp.y >= 0 ? jb.V + vcol(cp.y, jb.per, jb.ldv, N) : nullptr;
     double2* Yp = jb.Y + ((int64_t)((p / jb.G) % kSlots) * jb.G + p % jb.G) * N;
     const int j10 = tile * P::TC;
+    const uint64_t pol = jb.l2hint ? policy_evict_last() : 0;
     if (x2) {
         stage_first<VA, P::A0, false>(sm, [&](int seq, int i) {
             const int64_t g = j10 + seq + (int64_t)P::N1 * i;
@@ -444,7 +475,7 @@ __device__ __forceinline__ void item_a(const Job& jb, double2* sm, int p, int ti
         const double2 ws = wN(jb, j1 * LR);
 #pragma unroll
         for (int r = 0; r < P::AL; ++r) {
-            __stcg(Yp + j1 + (int64_t)P::N1 * (j + r * LR), cmul(v[r], w));
+            st_y(Yp + j1 + (int64_t)P::N1 * (j + r * LR), cmul(v[r], w), pol);
             if (r + 1 < P::AL) w = cmul(w, ws);
         }
     });
@@ -458,8 +489,9 @@ __device__ __forceinline__ void item_b(const Job& jb, double2* sm, int p, int ro
     const double* lam = (cp.x % jb.per == 0) ? jb.lamB : jb.lamQ;
     double2* Yp = jb.Y + ((int64_t)((p / jb.G) % kSlots) * jb.G + p % jb.G) * N;
     const int k20 = rowblk * P::S;
+    const uint64_t pol = jb.l2hint ? policy_evict_last() : 0;
     stage_first<VB, P::B0, false>(sm, [&](int seq, int i) {
-        return __ldcg(Yp + (int64_t)P::N1 * (k20 + seq) + i);
+        return ld_y(Yp + (int64_t)P::N1 * (k20 + seq) + i, pol);
     });
     Mids<VB, false, P::B0, typename P::BM>::run(sm, jb.tw1);
     constexpr int LRt = P::N1 / P::BL;
@@ -480,7 +512,7 @@ __device__ __forceinline__ void item_b(const Job& jb, double2* sm, int p, int ro
         double2* yr = Yp + (int64_t)P::N1 * k2 + j;
 #pragma unroll
         for (int r = 0; r < P::B0; ++r) {
-            __stcg(yr + r * LR, cmul(v[r], w));
+            st_y(yr + r * LR, cmul(v[r], w), pol);
             if (r + 1 < P::B0) w = cmul(w, ws);
         }
     });
@@ -496,6 +528,13 @@ __device__ __forceinline__ void item_c(const Job& jb, double2* sm, int p, int ti
     stage_first<VA, P::AL, true>(sm, [&](int seq, int i) {
         return __ldcg(Yp + j10 + seq + (int64_t)P::N1 * i);
     });
+    if (jb.l2hint) {  // this tile's Y lines are dead: drop them from L2 without a write-back
+        static_assert((P::TC * 16) % 128 == 0, "column tile must cover whole 128-byte lines");
+        constexpr int lpr = P::TC * 16 / 128;
+        const char* base = reinterpret_cast<const char*>(Yp + j10);
+        for (int e = threadIdx.x; e < P::N2 * lpr; e += kNT)
+                discard_l2(base + (int64_t)(e / lpr) * P::N1 * 16 + (e % lpr) * 128);
+    }
     Mids<VA, true, P::AL, typename P::AMr>::run(sm, jb.tw2);
     double* o1 = jb.out + vcol(cp.x, jb.per, jb.ldo, N) + j10;
     double* o2 = cp.y >= 0 ? jb.out + vcol(cp.y, jb.per, jb.ldo, N) + j10 : nullptr;
@@ -535,7 +574,7 @@ __device__ __forceinline__ void item_c(const Job& jb, double2* sm, int p, int ti
 }
 
 template <class P>
-__global__ void __launch_bounds__(kNT, kCtaPerSm) fftconv_kernel(const Job jb) {
+__global__ void __launch_bounds__(kThreads, kCtaPerSm) fftconv_kernel(const Job jb) {
     extern __shared__ double2 sm[];
     __shared__ unsigned s_ticket;
     constexpr int nA1 = P::N1 / P::TC, nB1 = P::N2 / P::S;  // items per pair
@@ -559,40 +598,52 @@ __global__ void __launch_bounds__(kNT, kCtaPerSm) fftconv_kernel(const Job jb) {
             r -= nA + nB;
         }
     };
-    unsigned next = 0;
-    if (threadIdx.x == 0) next = atomicAdd(jb.ctr, 1u);
+    // counter item t waits for: A(g) reuses the Y slot of C(g - kSlots); B(g) needs A(g);
+    // C(g) needs B(g).  Every awaited item holds a smaller ticket, and a CTA holds at most
+    // one unstarted (prefetched) ticket while it runs a smaller one, so the smallest
+    // unfinished ticket always progresses: no deadlock.
+    auto dependency = [&](unsigned t, const unsigned*& dep, unsigned& need) {
+        dep = nullptr;
+        need = 0;
+        if (t >= total) return;
+        int phase, g, r;
+        decode(t, phase, g, r);
+        if (g < 0 || g >= jb.ngroups) return;
+        if (phase == 0 && g >= kSlots) {
+            dep = jb.ctr + 1 + 3 * (g - kSlots) + 2;
+            need = (unsigned)nC;
+        } else if (phase == 1) {
+            dep = jb.ctr + 1 + 3 * g + 0;
+            need = (unsigned)nA;
+        } else if (phase == 2) {
+            dep = jb.ctr + 1 + 3 * g + 1;
+            need = (unsigned)nB;
+        }
+    };
+    // thread 0 owns the schedule: `next` is fetched one item ahead and its dependency
+    // counter is read at the end of the current item, so both round trips overlap work
+    unsigned next = 0, seen = 0, need = 0;
+    const unsigned* dep = nullptr;
+    if (threadIdx.x == 0) {
+        next = atomicAdd(jb.ctr, 1u);
+        dependency(next, dep, need);
+        if (dep) seen = ld_relaxed(dep);
+    }
     for (;;) {
         if (threadIdx.x == 0) {
-            // dependency: A(g) reuses the Y slot of C(g - kSlots); B(g) needs A(g); C(g) needs
-            // B(g).  Relaxed polling, then one acquire fence.
-            if (next < total) {
-                int phase, g, r;
-                decode(next, phase, g, r);
-                const unsigned* dep = nullptr;
-                unsigned need = 0;
-                if (g >= 0 && g < jb.ngroups) {
-                    if (phase == 0 && g >= kSlots) {
-                        dep = jb.ctr + 1 + 3 * (g - kSlots) + 2;
-                        need = (unsigned)nC;
-                    } else if (phase == 1) {
-                        dep = jb.ctr + 1 + 3 * g + 0;
-                        need = (unsigned)nA;
-                    } else if (phase == 2) {
-                        dep = jb.ctr + 1 + 3 * g + 1;
-                        need = (unsigned)nB;
-                    }
+            if (dep)
+                while (seen < need) {
+                    __nanosleep(64);
+                    seen = ld_relaxed(dep);
                 }
-                if (dep) {
-                    while (ld_relaxed(dep) < need) __nanosleep(64);
-                    asm volatile("fence.acq_rel.gpu;" ::: "memory");
-                }
-            }
             s_ticket = next;
         }
-        __syncthreads();  // ticket published, dependency met, previous item's SMEM reads done
+        // Y is written with st.cg, published by red.release and read with ld.cg (L2, the
+        // coherence point) only after thread 0 observed the counter and this barrier
+        __syncthreads();
         const unsigned t = s_ticket;
         if (t >= total) break;
-        if (threadIdx.x == 0) next = atomicAdd(jb.ctr, 1u);  // prefetch: consumed after this item
+        if (threadIdx.x == 0) next = atomicAdd(jb.ctr, 1u);
         int phase, g, r;
         decode(t, phase, g, r);
         const bool valid = g >= 0 && g < jb.ngroups;
@@ -601,15 +652,20 @@ __global__ void __launch_bounds__(kNT, kCtaPerSm) fftconv_kernel(const Job jb) {
             const int per_pair = phase == 1 ? nB1 : nA1;
             const int p = g * jb.G + r / per_pair, idx = r % per_pair;
             if (p < jb.np) {  // the last group may be partial
-                if (phase == 0)
+                if (phase == 0) {
                     item_a<P>(jb, sm, p, idx);
-                else if (phase == 1)
+                } else if (phase == 1) {
                     item_b<P>(jb, sm, p, idx);
-                else
+                } else {
                     item_c<P>(jb, sm, p, idx);
+                }
             }
         }
-        __syncthreads();  // every store of the item issued; s_ticket read by every thread
+        if (threadIdx.x == 0) {
+            dependency(next, dep, need);
+            if (dep) seen = ld_relaxed(dep);
+        }
+        __syncthreads();  // every store of the item issued; s_ticket read; SMEM free
         if (threadIdx.x == 0 && valid) red_release(jb.ctr + 1 + 3 * g + phase);
     }
 }
@@ -641,10 +697,10 @@ void launch(const Job& jb, cudaStream_t st) {
     int dev = 0, nsm = kSMs, occ = 0;
     W4_CUDA(cudaGetDevice(&dev));
     W4_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
-    W4_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fftconv_kernel<P>, kNT, sm));
+    W4_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fftconv_kernel<P>, kThreads, sm));
     const int64_t items = (int64_t)(jb.ngroups + 2) * jb.G * (2 * (P::N1 / P::TC) + P::N2 / P::S);
     const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(items, (int64_t)nsm * std::max(occ, 1)));
-    fftconv_kernel<P><<<grid, kNT, sm, st>>>(jb);
+    fftconv_kernel<P><<<grid, kThreads, sm, st>>>(jb);
     W4_LAUNCH();
 }
 
@@ -773,8 +829,12 @@ void Fft4::apply(bool inv, int Nsw, const double* V, int64_t ldv, int64_t m, dou
     double2* Y = ybuf.get<double2>((size_t)kSlots * G * N_);
     unsigned* ctr = ctr_.get<unsigned>((size_t)1 + 3 * ngroups);
     W4_CUDA(cudaMemsetAsync(ctr, 0, sizeof(unsigned) * (1 + 3 * (size_t)ngroups), st));
+    static const int l2hint = [] {
+        const char* e = std::getenv("WC4DVAR_FFT_L2HINT");
+        return e ? std::atoi(e) : 1;
+    }();
     Job jb{V, ldv, out, ldo, add, ldadd, add ? status : nullptr, dpairs, np, per, G, ngroups,
-           lamB, lamQ, Y, tw1_, tw2_, tlo_, thi_, ctr};
+           lamB, lamQ, Y, tw1_, tw2_, tlo_, thi_, ctr, l2hint};
     kPlans[plan_].run(jb, st);
 }
 
