@@ -70,8 +70,18 @@ typedef struct {
     double diffusion;    /* ADVDIFF: nu dt / dx^2 */
     double dt;           /* LORENZ96 */
     /* LORENZ96: host pointer to N*substeps stage sets, each [x1|x2|x3|x4] of
-     * 4n doubles (Lorenz96Stages::at, models.cpp:80-87), sub-step-major. */
+     * 4n doubles (Lorenz96Stages::at, models.cpp:80-87), sub-step-major.  NULL
+     * when `trajectory` is given instead. */
     const double* stages;
+    /* LORENZ96 alternative (Lorenz96Linearized ctor, operators.cpp:44-51): the
+     * linearisation trajectory, n x (N*substeps + 1) col-major with leading
+     * dimension ld_trajectory, host memory or (trajectory_on_device = 1) device
+     * memory on the operator's device; the stages are computed on the device. */
+    const double* trajectory;
+    int64_t ld_trajectory;
+    double forcing;
+    int32_t trajectory_on_device;
+    int32_t reserved2;
 } wc4dvar_model_desc;
 
 /* ObservationNetwork (models.hpp:45-56): observed times ascending, observed
@@ -154,6 +164,29 @@ int wc4dvar_gpu_probe_dmma_peak(int device, double* tflops);
 /* Bit-exact with the reference stream (mt19937_64 + Box-Muller on glibc libm),
  * column-major fill.  Host output. */
 int wc4dvar_gpu_gaussian_matrix(int64_t rows, int64_t cols, uint64_t seed, double* out);
+
+/* ------------------------------------------------------------------------- */
+/* Lorenz-96 nonlinear model on the device                   */
+/* ------------------------------------------------------------------------- */
+/* lorenz96_step (models.cpp:72-78, RK4 of lorenz96_rhs models.cpp:59-70)
+ * applied `spinup` times to x0 (n), then the next `steps` states: traj is
+ * n x (steps + 1) col-major (ld >= n), column 0 the spun-up state.  Bitwise
+ * equal to the reference's (non-FMA) arithmetic.  Host pointers. */
+int wc4dvar_gpu_l96_trajectory(int64_t n, double forcing, double dt, const double* x0,
+                               int64_t spinup, int64_t steps, double* traj, int64_t ldt,
+                               int device);
+/* Same with device pointers, enqueued on `stream`. */
+int wc4dvar_gpu_l96_trajectory_dev(int64_t n, double forcing, double dt, const double* x0,
+                                   int64_t spinup, int64_t steps, double* traj, int64_t ldt,
+                                   int device, void* stream);
+/* AssimilationSystem::integrate_p (assimilation.cpp:21-33) for Lorenz-96 with
+ * `substeps` RK4 steps per window interval (1 = reference): p is the window
+ * control vector n(N+1); traj n x (N substeps + 1) holds every sub-step state,
+ * x_0 = p_0 and the end of interval i gets + p_i.  A non-finite interval end
+ * is NumericalError "integrate_p: non-finite trajectory at step i". */
+int wc4dvar_gpu_l96_integrate_p(int64_t n, int32_t N, int32_t substeps, double forcing,
+                                double dt, const double* p, double* traj, int64_t ldt,
+                                int device);
 
 /* ------------------------------------------------------------------------- */
 /* Randomized eigenpairs (randevd.hpp:24-41)                                  */

@@ -9,7 +9,7 @@ from .wc4dvar import (  # noqa: F401
     LinearOperator, LmpFactor, NumericalError, ObservationNetwork, PcgOptions, PcgResult,
     QuadraticCost, RitzPairs, SketchConfig, assemble_dense, build_spectral_lmp, gaussian_matrix,
     last_sketch_timing, nystrom, pcg_split, probe_dmma_peak, rayleigh_ritz, revd, revd_ritzit,
-    sketch_eigenpairs, version, LIB_PATH, SIGNATURES, Lorenz96Linearized, lorenz96_rhs,
-    lorenz96_stages, lorenz96_step, lorenz96_trajectory, InnerLoopReport, PrecondSpec, SolverSpec,
+    sketch_eigenpairs, version, LIB_PATH, SIGNATURES, Lorenz96Linearized,
+    lorenz96_trajectory, lorenz96_trajectory_device, integrate_p, InnerLoopReport, PrecondSpec, SolverSpec,
     run_inner_loop,
 )

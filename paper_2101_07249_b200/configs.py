@@ -127,9 +127,10 @@ def lorenz96_workload(name, n, N, s, m, k, forcing=8.0, dt=0.025, spinup=1000, L
     subwindow; linearisation trajectory from a seeded N(0,1) state spun up `spinup` steps
     (composed from the reference primitives NormalStream::draw and lorenz96_step, SURVEY
     §0.2-4); B = SOAR(L) circulant, Q = 0.1 B, R = 0.04 I, every other variable observed."""
-    from .wc4dvar import Lorenz96Linearized, gaussian_matrix, lorenz96_trajectory
+    from .wc4dvar import Lorenz96Linearized, gaussian_matrix, lorenz96_trajectory_device
     x0 = gaussian_matrix(n, 1, L96_X0_SEED)[:, 0]
-    traj = lorenz96_trajectory(x0, forcing, dt, spinup, N * s)
+    # spin-up, trajectory and stages stay on the device (SURVEY §8(f)-1)
+    traj = lorenz96_trajectory_device(x0, forcing, dt, spinup, N * s)
     model = Lorenz96Linearized(traj, forcing, dt, s)
     net = ObservationNetwork.build(n, N, 2, 1)
     col = soar_first_column(1.0, L, n)

@@ -7,6 +7,7 @@
 #include <sstream>
 #include <vector>
 
+#include "l96.cuh"
 #include "lmp_pcg.cuh"
 #include "ops.cuh"
 #include "pcg.cuh"
@@ -98,8 +99,10 @@ int wc4dvar_gpu_hessian_create(const wc4dvar_model_desc* model, const wc4dvar_ne
     require(net->n == model->n && net->N == model->N, "HessianOperator: network/window mismatch");
     require(model->kind >= WC4DVAR_MODEL_IDENTITY && model->kind <= WC4DVAR_MODEL_LORENZ96,
             "HessianOperator: unknown model kind");
-    require(model->kind != WC4DVAR_MODEL_LORENZ96 || (model->stages && model->dt > 0.0),
-            "Lorenz96Linearized: stages and dt are required");
+    require(model->kind != WC4DVAR_MODEL_LORENZ96 || ((model->stages || model->trajectory) && model->dt > 0.0),
+            "Lorenz96Linearized: stages (or the trajectory) and dt are required");
+    require(model->kind != WC4DVAR_MODEL_LORENZ96 || model->stages || model->ld_trajectory >= model->n,
+            "Lorenz96Linearized: ld_trajectory < n");
     require(model->kind != WC4DVAR_MODEL_LORENZ96 || model->n >= 4, "Lorenz96Model: n must be >= 4");
     require(bh->kind == WC4DVAR_COV_DENSE || bh->kind == WC4DVAR_COV_CIRCULANT,
             "HessianOperator: unknown covariance representation");
@@ -129,7 +132,28 @@ int wc4dvar_gpu_hessian_create(const wc4dvar_model_desc* model, const wc4dvar_ne
     h->md.d = model->diffusion;
     h->md.dt = model->dt;
     if (model->kind == WC4DVAR_MODEL_LORENZ96) {
-        h->d_stages = dev_upload(model->stages, (size_t)N * model->substeps * 4 * n, st);
+        const int64_t nst = (int64_t)N * model->substeps;
+        if (model->stages) {
+            h->d_stages = dev_upload(model->stages, (size_t)nst * 4 * n, st);
+        } else {
+            // Lorenz96Linearized ctor (operators.cpp:44-51): stages of trajectory columns
+            // 0 .. N s - 1, computed on the device
+            W4_CUDA(cudaMalloc(&h->d_stages, sizeof(double) * std::max<size_t>((size_t)nst * 4 * n, 1)));
+            const double* tr = model->trajectory;
+            int64_t ldt = model->ld_trajectory;
+            double* tmp = nullptr;
+            if (!model->trajectory_on_device) {
+                W4_CUDA(cudaMalloc(&tmp, sizeof(double) * (size_t)n * (nst + 1)));
+                h2d_block(tmp, model->trajectory, n, nst + 1, ldt, st);
+                tr = tmp;
+                ldt = n;
+            }
+            l96_stages_dev(n, model->forcing, model->dt, tr, ldt, nst, h->d_stages, st);
+            if (tmp) {
+                W4_CUDA(cudaStreamSynchronize(st));
+                cudaFree(tmp);
+            }
+        }
         h->md.stages = h->d_stages;
     }
     h->times.assign(net->times, net->times + net->n_times);
@@ -359,6 +383,64 @@ int wc4dvar_gpu_probe_dmma_peak(int device, double* tflops) {
     require(tflops != nullptr, "probe_dmma_peak: null");
     DeviceGuard g(device);
     *tflops = w4::probe_dmma_tflops();
+    W4_API_END
+}
+
+int wc4dvar_gpu_l96_trajectory_dev(int64_t n, double forcing, double dt, const double* x0, int64_t spinup,
+                                   int64_t steps, double* traj, int64_t ldt, int device, void* stream) {
+    W4_API_BEGIN
+    require(n >= 4, "lorenz96_rhs: n must be >= 4");
+    require(spinup >= 0 && steps >= 0 && ldt >= n && x0 && traj, "l96_trajectory: bad arguments");
+    DeviceGuard g(device);
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    DevBuf work;
+    l96_trajectory_dev(n, forcing, dt, x0, spinup, steps, traj, ldt, spinup > 1 ? work.get<double>(n) : nullptr, st);
+    W4_CUDA(cudaStreamSynchronize(st));  // work is released on return
+    W4_API_END
+}
+
+int wc4dvar_gpu_l96_trajectory(int64_t n, double forcing, double dt, const double* x0, int64_t spinup,
+                               int64_t steps, double* traj, int64_t ldt, int device) {
+    W4_API_BEGIN
+    require(n >= 4, "lorenz96_rhs: n must be >= 4");
+    require(spinup >= 0 && steps >= 0 && ldt >= n && x0 && traj, "l96_trajectory: bad arguments");
+    DeviceGuard g(device);
+    cudaStream_t st = nullptr;
+    W4_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+    std::unique_ptr<CUstream_st, void (*)(cudaStream_t)> sguard(st, [](cudaStream_t s) { cudaStreamDestroy(s); });
+    DevBuf dx0, dtraj, work;
+    double* x = dx0.get<double>(n);
+    double* tr = dtraj.get<double>((size_t)n * (steps + 1));
+    W4_CUDA(cudaMemcpyAsync(x, x0, sizeof(double) * n, cudaMemcpyHostToDevice, st));
+    l96_trajectory_dev(n, forcing, dt, x, spinup, steps, tr, n, spinup > 1 ? work.get<double>(n) : nullptr, st);
+    d2h_block(traj, ldt, tr, n, steps + 1, st);
+    W4_CUDA(cudaStreamSynchronize(st));
+    W4_API_END
+}
+
+int wc4dvar_gpu_l96_integrate_p(int64_t n, int32_t N, int32_t substeps, double forcing, double dt, const double* p,
+                                double* traj, int64_t ldt, int device) {
+    W4_API_BEGIN
+    require(n >= 4, "lorenz96_rhs: n must be >= 4");
+    require(N >= 0 && substeps >= 1 && ldt >= n && p && traj, "integrate_p: bad arguments");
+    DeviceGuard g(device);
+    cudaStream_t st = nullptr;
+    W4_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+    std::unique_ptr<CUstream_st, void (*)(cudaStream_t)> sguard(st, [](cudaStream_t s) { cudaStreamDestroy(s); });
+    const int64_t cols = (int64_t)N * substeps + 1;
+    DevBuf dp, dtraj, dstat;
+    double* pd = dp.get<double>((size_t)n * (N + 1));
+    double* tr = dtraj.get<double>((size_t)n * cols);
+    unsigned* stat = dstat.get<unsigned>(std::max(N, 1));
+    W4_CUDA(cudaMemsetAsync(stat, 0, sizeof(unsigned) * std::max(N, 1), st));
+    W4_CUDA(cudaMemcpyAsync(pd, p, sizeof(double) * n * (N + 1), cudaMemcpyHostToDevice, st));
+    l96_integrate_p_dev(n, N, substeps, forcing, dt, pd, tr, n, stat, st);
+    std::vector<unsigned> hs(std::max(N, 1));
+    W4_CUDA(cudaMemcpyAsync(hs.data(), stat, sizeof(unsigned) * hs.size(), cudaMemcpyDeviceToHost, st));
+    d2h_block(traj, ldt, tr, n, cols, st);
+    W4_CUDA(cudaStreamSynchronize(st));
+    for (int i = 0; i < N; ++i)
+        if (hs[i]) throw NumericalError("integrate_p: non-finite trajectory at step " + std::to_string(i + 1));
     W4_API_END
 }
 

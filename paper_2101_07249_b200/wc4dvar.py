@@ -50,7 +50,9 @@ class ModelDesc(ctypes.Structure):
     _fields_ = [("kind", ctypes.c_int32), ("N", ctypes.c_int32), ("n", _i64),
                 ("substeps", ctypes.c_int32), ("reserved", ctypes.c_int32),
                 ("courant", ctypes.c_double), ("diffusion", ctypes.c_double),
-                ("dt", ctypes.c_double), ("stages", _dp)]
+                ("dt", ctypes.c_double), ("stages", _dp), ("trajectory", _dp), ("ld_trajectory", _i64),
+                ("forcing", ctypes.c_double), ("trajectory_on_device", ctypes.c_int32),
+                ("reserved2", ctypes.c_int32)]
 
 
 class NetworkDesc(ctypes.Structure):
@@ -103,6 +105,12 @@ SIGNATURES = {
     "wc4dvar_gpu_op_profile_read": (ctypes.c_int, [_vp, _dp, ctypes.POINTER(_i64)]),
     "wc4dvar_gpu_probe_dmma_peak": (ctypes.c_int, [ctypes.c_int, ctypes.POINTER(ctypes.c_double)]),
     "wc4dvar_gpu_gaussian_matrix": (ctypes.c_int, [_i64, _i64, ctypes.c_uint64, _dp]),
+    "wc4dvar_gpu_l96_trajectory": (ctypes.c_int, [_i64, ctypes.c_double, ctypes.c_double, _dp, _i64, _i64, _dp,
+                                                  _i64, ctypes.c_int]),
+    "wc4dvar_gpu_l96_trajectory_dev": (ctypes.c_int, [_i64, ctypes.c_double, ctypes.c_double, _vp, _i64, _i64,
+                                                      _vp, _i64, ctypes.c_int, _vp]),
+    "wc4dvar_gpu_l96_integrate_p": (ctypes.c_int, [_i64, ctypes.c_int32, ctypes.c_int32, ctypes.c_double,
+                                                   ctypes.c_double, _dp, _dp, _i64, ctypes.c_int]),
     "wc4dvar_gpu_sketch": (ctypes.c_int, [_vp, ctypes.POINTER(SketchDesc), _dp, _dp, _i64, _dp,
                                           ctypes.POINTER(_i64)]),
     "wc4dvar_gpu_sketch_dev": (ctypes.c_int, [_vp, ctypes.POINTER(SketchDesc), _vp, _vp, _i64, _vp,
@@ -244,6 +252,8 @@ class LinearizedModel:
     diffusion: float = 0.0
     dt: float = 0.0
     stages: Optional[np.ndarray] = None
+    trajectory: Optional[object] = None  # L96: n x (N s + 1) numpy array or device tensor (steps+1, n)
+    forcing: float = 0.0
 
 
 def IdentityLinearized(n: int, N: int) -> LinearizedModel:
@@ -260,51 +270,57 @@ def AdvDiffLinearized(n: int, N: int, courant: float, diffusion: float, substeps
     return LinearizedModel("advdiff", n, N, substeps, courant, diffusion)
 
 
-def lorenz96_rhs(x: np.ndarray, forcing: float) -> np.ndarray:
-    """models.cpp:59-70 (same evaluation order, vectorised)."""
-    xm2, xm1, xp1 = np.roll(x, 2), np.roll(x, 1), np.roll(x, -1)
-    return -xm2 * xm1 + xm1 * xp1 - x + forcing
-
-
-def lorenz96_step(x: np.ndarray, forcing: float, dt: float) -> np.ndarray:
-    """models.cpp:72-78 (RK4)."""
-    k1 = lorenz96_rhs(x, forcing)
-    k2 = lorenz96_rhs(x + 0.5 * dt * k1, forcing)
-    k3 = lorenz96_rhs(x + 0.5 * dt * k2, forcing)
-    k4 = lorenz96_rhs(x + dt * k3, forcing)
-    return x + (dt / 6.0) * (k1 + 2.0 * k2 + 2.0 * k3 + k4)
-
-
-def lorenz96_stages(x: np.ndarray, forcing: float, dt: float) -> np.ndarray:
-    """Lorenz96Stages::at, models.cpp:80-87 -> [x1 | x2 | x3 | x4]."""
-    x1 = x
-    x2 = x + 0.5 * dt * lorenz96_rhs(x1, forcing)
-    x3 = x + 0.5 * dt * lorenz96_rhs(x2, forcing)
-    x4 = x + dt * lorenz96_rhs(x3, forcing)
-    return np.concatenate([x1, x2, x3, x4])
-
-
-def Lorenz96Linearized(trajectory: np.ndarray, forcing: float, dt: float, substeps: int = 1):
-    """operators.cpp:44-51: stages precomputed on the host at construction, as in the
-    reference.  ``trajectory`` holds N*s + 1 states (n x (N*s+1)); s = 1 is the reference."""
-    trajectory = np.asarray(trajectory, dtype=np.float64)
-    require(trajectory.ndim == 2 and trajectory.shape[1] >= 2, "Lorenz96Linearized: trajectory too short")
-    n, total = trajectory.shape[0], trajectory.shape[1] - 1
+def Lorenz96Linearized(trajectory, forcing: float, dt: float, substeps: int = 1):
+    """operators.cpp:44-51: the operator stores the RK4 stages of every trajectory column;
+    the library computes them on the device at construction (wc4dvar_model_desc.trajectory).
+    ``trajectory`` is an n x (N*s+1) host array, or a device tensor of shape (N*s+1, n)
+    (each row one state, i.e. the same column-major block) from lorenz96_trajectory_device;
+    s = 1 is the reference."""
+    if isinstance(trajectory, np.ndarray) or not hasattr(trajectory, "data_ptr"):
+        trajectory = np.asfortranarray(trajectory, dtype=np.float64)
+        require(trajectory.ndim == 2 and trajectory.shape[1] >= 2, "Lorenz96Linearized: trajectory too short")
+        n, total = trajectory.shape[0], trajectory.shape[1] - 1
+    else:
+        require(trajectory.dim() == 2 and trajectory.shape[0] >= 2, "Lorenz96Linearized: trajectory too short")
+        require(trajectory.is_contiguous(), "Lorenz96Linearized: device trajectory must be contiguous")
+        n, total = trajectory.shape[1], trajectory.shape[0] - 1
     require(total % substeps == 0, "Lorenz96Linearized: trajectory/sub-step mismatch")
-    stages = np.concatenate([lorenz96_stages(trajectory[:, c], forcing, dt) for c in range(total)])
-    return LinearizedModel("l96", n, total // substeps, substeps, dt=dt, stages=stages)
+    return LinearizedModel("l96", n, total // substeps, substeps, dt=dt, trajectory=trajectory, forcing=forcing)
 
 
-def lorenz96_trajectory(x0: np.ndarray, forcing: float, dt: float, spinup: int, steps: int) -> np.ndarray:
-    """Spin x0 up for `spinup` RK4 steps, then return the next `steps` + 1 states (n x (steps+1))."""
-    x = np.asarray(x0, dtype=np.float64)
-    for _ in range(spinup):
-        x = lorenz96_step(x, forcing, dt)
-    traj = np.empty((len(x), steps + 1))
-    traj[:, 0] = x
-    for c in range(steps):
-        x = lorenz96_step(x, forcing, dt)
-        traj[:, c + 1] = x
+def lorenz96_trajectory(x0, forcing: float, dt: float, spinup: int, steps: int, device: int = 0) -> np.ndarray:
+    """Spin x0 up for `spinup` RK4 steps (lorenz96_step, models.cpp:72-78), then return the
+    next `steps` + 1 states as an n x (steps+1) host array; integrated on the device
+    (wc4dvar_gpu_l96_trajectory), bitwise equal to the reference arithmetic."""
+    x0 = np.ascontiguousarray(x0, dtype=np.float64)
+    n = len(x0)
+    traj = np.empty((n, steps + 1), order="F")
+    _check(lib.wc4dvar_gpu_l96_trajectory(n, forcing, dt, _p(x0), spinup, steps, _p(traj), n, device))
+    return traj
+
+
+def lorenz96_trajectory_device(x0, forcing: float, dt: float, spinup: int, steps: int, device: int = 0):
+    """lorenz96_trajectory kept on the device: a (steps+1, n) float64 tensor (row c = state c),
+    ready for Lorenz96Linearized without a host round trip."""
+    import torch
+    x0 = torch.as_tensor(np.ascontiguousarray(x0, dtype=np.float64)).to(f"cuda:{device}")
+    n = x0.numel()
+    traj = torch.empty((steps + 1, n), dtype=torch.float64, device=x0.device)
+    stream = torch.cuda.current_stream(x0.device)
+    _check(lib.wc4dvar_gpu_l96_trajectory_dev(n, forcing, dt, ctypes.c_void_p(x0.data_ptr()), spinup, steps,
+                                              ctypes.c_void_p(traj.data_ptr()), n, device,
+                                              ctypes.c_void_p(stream.cuda_stream)))
+    return traj
+
+
+def integrate_p(p, n: int, N: int, forcing: float, dt: float, substeps: int = 1, device: int = 0) -> np.ndarray:
+    """AssimilationSystem::integrate_p (assimilation.cpp:21-33) for Lorenz-96, on the device:
+    x_0 = p_0, x_{i+1} = M^s(x_i) + p_{i+1}; returns every sub-step state, n x (N s + 1)
+    (s = 1: the reference's n x (N+1)).  NumericalError on a non-finite interval end."""
+    p = np.ascontiguousarray(p, dtype=np.float64)
+    require(p.size == n * (N + 1), "integrate_p: control vector length mismatch")
+    traj = np.empty((n, N * substeps + 1), order="F")
+    _check(lib.wc4dvar_gpu_l96_integrate_p(n, N, substeps, forcing, dt, _p(p), _p(traj), n, device))
     return traj
 
 
@@ -423,6 +439,19 @@ class HessianOperator(LinearOperator):
         md.courant, md.diffusion, md.dt = model.courant, model.diffusion, model.dt
         st = arr(model.stages)
         md.stages = _p(st)
+        tr = model.trajectory
+        if tr is not None and st is None:
+            if isinstance(tr, np.ndarray):
+                tr = arr(tr)
+                md.trajectory, md.ld_trajectory, md.trajectory_on_device = _p(tr), tr.shape[0], 0
+            else:
+                require(tr.device.index == device, "HessianOperator: trajectory on another device")
+                keep.append(tr)
+                md.trajectory = ctypes.cast(ctypes.c_void_p(tr.data_ptr()), _dp)
+                md.ld_trajectory, md.trajectory_on_device = tr.shape[1], 1
+                import torch
+                torch.cuda.current_stream(tr.device).synchronize()  # the library uses its own stream
+            md.forcing = model.forcing
         nd = NetworkDesc()
         times = arr(np.asarray(net.times, dtype=np.int32), np.int32)
         points = arr(np.asarray(net.points, dtype=np.int32), np.int32)

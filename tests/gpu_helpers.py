@@ -6,6 +6,10 @@ import paper_2101_07249_b200 as W
 
 
 def oracle_model(m: W.LinearizedModel) -> O.LinearizedModel:
+    if m.kind == "l96" and m.stages is None:  # stages built on the device from the trajectory
+        tr = m.trajectory
+        tr = tr if isinstance(tr, np.ndarray) else tr.cpu().numpy().T
+        return O.Lorenz96Linearized(tr, m.forcing, m.dt, m.substeps)
     return O.LinearizedModel(m.kind, m.n, m.N, m.substeps, m.courant, m.diffusion, m.dt, m.stages)
 
 
