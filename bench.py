@@ -261,6 +261,8 @@ def run_ours(args):
     extras = {}
     if not args.no_extras and rank == 0:
         extras = run_extras(W, configs, wl, op, Om, dev)
+        if world == 1:
+            extras["large_configs"] = run_large(W, configs, dmma_peak, hbm_peak)
 
     if rank == 0:
         line = {
@@ -326,6 +328,57 @@ def run_extras(W, configs, wl, op, Om, dev):
         r = W.pcg_split(op, b, f, opts=W.PcgOptions(max_iter=500, rel_tol=1e-6))
         out["pcg"][method] = {"ms": 1e3 * (time.perf_counter() - t0), "iterations": r.history.iterations,
                               "converged": r.history.converged}
+    return out
+
+
+def run_large(W, configs, peak_tfs, hbm_gbs):
+    """BASELINE configs[2] (C3, Lorenz-96 n=1e5) and configs[3] (C4, adv-diff n=1e6,
+    circulant factors) block applies at m = 64 on one GPU: device-drawn N(0,1) Omega (torch,
+    throughput only; parity at these shapes is property-based in tests/), CUDA-event timing,
+    per-stage split, and the SURVEY §8(d) roofline t_roof = max(B/BW, F/P) per block with
+    B = 8 (3 n_A + 2 q) m and F = (F_model + F_cov) m."""
+    import torch
+    out = {}
+    for name, mk in (("C3", lambda: configs.config3()), ("C4", lambda: configs.config4(64))):
+        try:
+            wl = mk()
+            t0 = time.perf_counter()
+            op = wl.hessian(0)
+            setup_s = time.perf_counter() - t0
+            m, nA, q = 64, op.dim(), wl.net.q
+            n, N, s = wl.model.n, wl.model.N, wl.model.substeps
+            g = torch.Generator(device="cuda").manual_seed(1)
+            V = torch.randn(m, nA, dtype=torch.float64, device="cuda", generator=g)
+            Y = torch.empty_like(V)
+            sp = torch.cuda.current_stream().cuda_stream
+            op.apply_block_dev(V, Y, sp)
+            op.profile(True)
+            torch.cuda.synchronize()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            reps = 3
+            e0.record()
+            for _ in range(reps):
+                op.apply_block_dev(V, Y, sp)
+            e1.record()
+            torch.cuda.synchronize()
+            ms = e0.elapsed_time(e1) / reps
+            st, calls = op.profile_read()
+            op.profile(False)
+            f_model = (92.0 if wl.model.kind == "l96" else 10.0) * N * s * n
+            f_cov = 2.0 * (N + 1) * (5.0 * n * math.log2(n) + n)
+            t_f = (f_model + f_cov) * m / (peak_tfs * 1e12)
+            t_b = 8.0 * (3 * nA + 2 * q) * m / (hbm_gbs * 1e9)
+            t_roof = max(t_f, t_b) * 1e3
+            out[name] = {"workload": wl.name, "m": m, "ms_per_apply": ms, "columns_per_s": m / (ms * 1e-3),
+                         "stage_ms": {"d_half_in": st[0] / max(calls, 1), "sweep": st[1] / max(calls, 1),
+                                      "d_half_out_plus_identity": st[2] / max(calls, 1)},
+                         "roofline": {"t_roof_ms": t_roof, "bound": "fp64" if t_f >= t_b else "hbm",
+                                      "frac": t_roof / ms},
+                         "operator_setup_s": setup_s, "omega": "device N(0,1) (torch), seed 1"}
+            del V, Y, op
+            torch.cuda.empty_cache()
+        except Exception as e:  # report, do not fail the headline line
+            out[name] = {"error": f"{type(e).__name__}: {e}"[:300]}
     return out
 
 

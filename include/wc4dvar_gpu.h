@@ -150,6 +150,21 @@ int wc4dvar_gpu_hessian_piece_dev(wc4dvar_op* op, int which, const double* V, in
 /* Stage profiling of HessianOperator block applies (CUDA events around the
  * D^{1/2} GEMM, the fused sweep and the final D^{1/2} GEMM + identity term).
  * enable != 0 resets the accumulators; read returns ms[3] summed over calls. */
+/* HessianOperator::observation_range (operators.cpp:146-154): W (dim x q, ldw) =
+ * D^{1/2} L^{-T} H^T [e_1 .. e_q], computed as one block adjoint sweep of the q
+ * unit observations.  Host / device (_dev, on `stream`) outputs. */
+int wc4dvar_gpu_observation_range(wc4dvar_op* op, double* W, int64_t ldw);
+int wc4dvar_gpu_observation_range_dev(wc4dvar_op* op, double* W, int64_t ldw, void* stream);
+
+/* clustered_spectrum (spectrum.cpp:31-64) of the (LMP-preconditioned) Hessian:
+ * the q + k eigenvalues of C^T A C on span([W | U]) in decreasing order
+ * (*n_nonunit = q + k, nonunit holds them) and the multiplicity dim - (q + k) of
+ * the eigenvalue 1 elsewhere.  precond NULL = no preconditioner; obs_range NULL =
+ * computed (observation_range).  Counts q + k operator applies. */
+int wc4dvar_gpu_clustered_spectrum(wc4dvar_op* op, const struct wc4dvar_lmp* precond,
+                                   const double* obs_range, int64_t ldw, double* nonunit,
+                                   int64_t* n_nonunit, int64_t* unit_multiplicity);
+
 int wc4dvar_gpu_op_profile(wc4dvar_op* op, int enable);
 int wc4dvar_gpu_op_profile_read(wc4dvar_op* op, double* ms3, int64_t* calls);
 

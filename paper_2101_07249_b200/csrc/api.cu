@@ -337,6 +337,69 @@ int wc4dvar_gpu_hessian_piece_dev(wc4dvar_op* op, int which, const double* V, in
     W4_API_END
 }
 
+int wc4dvar_gpu_observation_range_dev(wc4dvar_op* op, double* W, int64_t ldw, void* stream) {
+    W4_API_BEGIN
+    HessianOp* h = dynamic_cast<HessianOp*>(op);
+    require(h != nullptr, "observation_range: operator is not a HessianOperator");
+    require(ldw >= op->dim && (W || h->nd.q == 0), "observation_range: bad output");
+    std::lock_guard<std::recursive_mutex> lk(op->mu);
+    DeviceGuard g(op->device);
+    cudaStream_t st = pick(op, stream);
+    op->reset_status(st);
+    h->observation_range_dev(W, ldw, st);
+    op->check_status(st);
+    W4_API_END
+}
+
+int wc4dvar_gpu_observation_range(wc4dvar_op* op, double* W, int64_t ldw) {
+    W4_API_BEGIN
+    HessianOp* h = dynamic_cast<HessianOp*>(op);
+    require(h != nullptr, "observation_range: operator is not a HessianOperator");
+    require(ldw >= op->dim && (W || h->nd.q == 0), "observation_range: bad output");
+    std::lock_guard<std::recursive_mutex> lk(op->mu);
+    DeviceGuard g(op->device);
+    const int64_t q = h->nd.q;
+    if (q == 0) return WC4DVAR_OK;
+    double* dw = op->out_buf.get<double>((size_t)op->dim * q);
+    const int rc = wc4dvar_gpu_observation_range_dev(op, dw, op->dim, nullptr);
+    if (rc != WC4DVAR_OK) return rc;
+    d2h_block(W, ldw, dw, op->dim, q, op->stream);
+    W4_CUDA(cudaStreamSynchronize(op->stream));
+    W4_API_END
+}
+
+int wc4dvar_gpu_clustered_spectrum(wc4dvar_op* op, const wc4dvar_lmp* precond, const double* obs_range,
+                                   int64_t ldw, double* nonunit, int64_t* n_nonunit, int64_t* unit_multiplicity) {
+    W4_API_BEGIN
+    HessianOp* h = dynamic_cast<HessianOp*>(op);
+    require(h != nullptr, "clustered_spectrum: operator is not a HessianOperator");
+    require(nonunit && n_nonunit && unit_multiplicity, "clustered_spectrum: null output");
+    require(!obs_range || ldw >= op->dim, "clustered_spectrum: observation range mismatch");
+    require(!precond || precond->n == op->dim, "clustered_spectrum: preconditioner dimension mismatch");
+    require(!precond || precond->device == op->device, "clustered_spectrum: preconditioner on another device");
+    std::lock_guard<std::recursive_mutex> lk(op->mu);
+    DeviceGuard g(op->device);
+    cudaStream_t st = op->stream;
+    const int64_t n = op->dim, q = h->nd.q;
+    const int64_t k = precond ? precond->k : 0;  // identity LMP: k = 0 (spectrum.cpp:36)
+    double* W = op->in_buf.get<double>((size_t)n * std::max<int64_t>(q, 1));
+    if (obs_range) {
+        h2d_block(W, obs_range, n, q, ldw, st);
+    } else {
+        op->reset_status(st);
+        h->observation_range_dev(W, n, st);
+        op->check_status(st);
+    }
+    if (precond && k) W4_CUDA(cudaStreamSynchronize(precond->stream));  // U / T built on the LMP stream
+    double* vals = op->out_buf.get<double>((size_t)std::max<int64_t>(q + k, 1));
+    clustered_spectrum_dev(*op, W, q, precond ? precond->U : nullptr, k, precond ? precond->T : nullptr, vals, st);
+    W4_CUDA(cudaMemcpyAsync(nonunit, vals, sizeof(double) * (q + k), cudaMemcpyDeviceToHost, st));
+    W4_CUDA(cudaStreamSynchronize(st));
+    *n_nonunit = q + k;
+    *unit_multiplicity = n - (q + k);
+    W4_API_END
+}
+
 int wc4dvar_gpu_hessian_piece(wc4dvar_op* op, int which, const double* V, int64_t ldv, int64_t m,
                               double* out, int64_t ldo) {
     W4_API_BEGIN

@@ -162,6 +162,32 @@ void HessianOp::apply_block_dev(const double* V, int64_t ldv, int64_t m, double*
     prof_pending = prof;
 }
 
+namespace {
+__global__ void identity_kernel(int64_t q, double* Y) {
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < q * q; e += (int64_t)gridDim.x * blockDim.x)
+        Y[e] = (e % (q + 1) == 0) ? 1.0 : 0.0;
+}
+}  // namespace
+
+void HessianOp::observation_range_dev(double* W, int64_t ldw, cudaStream_t st) {
+    const int64_t q = nd.q;
+    if (q == 0) return;
+    double* Y = y_ws.get<double>((size_t)q * q);
+    identity_kernel<<<(unsigned)std::min<int64_t>(cdiv(q * q, 256), 4096), 256, 0, st>>>(q, Y);
+    W4_LAUNCH();
+    double* S = t_ws.get<double>((size_t)dim * q);
+    // s = L^{-T} H^T e_r for all r at once (observe_adjoint, models.cpp:193-201)
+    SweepArgs a;
+    a.Y = Y;
+    a.S = S;
+    a.lds = dim;
+    a.do_adj = true;
+    a.adj_obs = true;
+    a.m = q;
+    sweep(md, nd, a, d_status, st, &sweep_ws);
+    d_half(false, S, dim, q, W, ldw, nullptr, 0, d_status, st);
+}
+
 void HessianOp::piece_dev(int which, const double* V, int64_t ldv, int64_t m, double* out,
                           int64_t ldo, cudaStream_t st) {
     if (m == 0) return;

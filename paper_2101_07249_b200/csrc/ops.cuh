@@ -83,6 +83,9 @@ struct HessianOp final : wc4dvar_op {
     // which: WC4DVAR_LINV / LINVT / D_HALF / D_HALF_INV (block forms).
     void piece_dev(int which, const double* V, int64_t ldv, int64_t m, double* out, int64_t ldo,
                    cudaStream_t st);
+    // HessianOperator::observation_range (operators.cpp:146-154): W (n_A x q, ldw) =
+    // D^{1/2} L^{-T} H^T [e_1 .. e_q], one block adjoint sweep of the q unit observations.
+    void observation_range_dev(double* W, int64_t ldw, cudaStream_t st);
     // out = D^{1/2} V (+ add) for an n_A x m block; inverse factors when inv.
     void d_half(bool inv, const double* V, int64_t ldv, int64_t m, double* out, int64_t ldo,
                 const double* add, int64_t ldadd, unsigned* status, cudaStream_t st);

@@ -20,6 +20,7 @@
 #include "smallla.cuh"
 
 namespace w4 {
+void gaussian_fill(int64_t count, uint64_t seed, double* out);
 namespace {
 
 enum {
@@ -203,6 +204,98 @@ void rr_core(Ctx& c, const double* Z, int64_t m, int64_t keep, double* U_out, in
 }
 
 }  // namespace
+
+void clustered_spectrum_dev(wc4dvar_op& op, const double* Wobs, int64_t q, const double* U, int64_t k,
+                            const double* T, double* vals_out, cudaStream_t st) {
+    const int64_t n = op.dim;
+    const int64_t m = q + k;
+    require(m >= 1 && m <= n, "clustered_spectrum: q + k must lie in [1, dim]");
+    require(m <= 512, "clustered_spectrum: q + k above 512 is not supported by the device small-matrix kernels");
+    Timer tm(st, false);
+    Ctx c{op, st, n, tm, op.pool, op.h_int};
+    // B = [W | U] (spectrum.cpp:38-41)
+    double* B = c.buf(P_Y, n * m);
+    if (q) W4_CUDA(cudaMemcpyAsync(B, Wobs, sizeof(double) * n * q, cudaMemcpyDeviceToDevice, st));
+    if (k) W4_CUDA(cudaMemcpyAsync(B + n * q, U, sizeof(double) * n * k, cudaMemcpyDeviceToDevice, st));
+    // Orthonormal Q with q + k columns spanning span(B) (spectrum.cpp:45-46: Householder Q).
+    // CholQR2 when B has full numerical rank; otherwise CholQR2 of the r pivot columns,
+    // completed by Gaussian directions orthogonalised against them -- C^T A C is the
+    // identity on that complement, as on the Householder completion.
+    double* G = c.buf(P_G, m * m);
+    c.gram(B, m, B, m, G);
+    int* perm = nullptr;
+    const int r = c.rank_probe(G, m, &perm);
+    if (r == 0) throw NumericalError("clustered_spectrum: observation range and LMP vectors are zero");
+    double* Q = c.buf(P_Z, n * m);
+    if (r == m) {
+        if (!c.cholqr2(B, m, Q, nullptr, G))
+            throw NumericalError("clustered_spectrum: basis too ill-conditioned for CholQR2");
+    } else {
+        double* Bp = c.buf(P_SEL, n * m);
+        gather_cols(n, r, B, n, perm, Bp, n, st);
+        if (!c.cholqr2(Bp, r, Q, nullptr, nullptr))
+            throw NumericalError("clustered_spectrum: basis too ill-conditioned for CholQR2");
+        const int64_t e = m - r;
+        std::vector<double> hz((size_t)n * e);
+        gaussian_fill(n * e, 1, hz.data());  // NormalStream(1): deterministic completion
+        double* Z = Bp;                       // Bp is dead once Q[:, :r] exists
+        W4_CUDA(cudaMemcpyAsync(Z, hz.data(), sizeof(double) * n * e, cudaMemcpyHostToDevice, st));
+        double* P = c.buf(P_TMP, (size_t)r * e);
+        for (int pass = 0; pass < 2; ++pass) {  // Z -= Q_r (Q_r^T Z), twice
+            c.gram(Q, r, Z, e, P);
+            GemmPass gp;
+            gp.A = Q;
+            gp.lda = n;
+            gp.M = n;
+            gp.K = r;
+            gp.ncols = e;
+            gp.alpha = -1.0;
+            gp.in = ColMap::plain(P, r);
+            gp.out = ColMap::plain(Z, n);
+            gp.add = ColMap::plain(Z, n);
+            gemm_nn(&gp, 1, nullptr, st);
+        }
+        if (!c.cholqr2(Z, e, Q + n * r, nullptr, nullptr))
+            throw NumericalError("clustered_spectrum: completion basis breakdown");
+        W4_CUDA(cudaStreamSynchronize(st));  // hz is released on return
+    }
+    // Y = C^T A C Q (spectrum.cpp:48-55), C = I - U T U^T (compact WY)
+    auto apply_lmp = [&](const double* X, double* out, bool transpose) {
+        double* G1 = c.buf(P_TMP, 2 * (size_t)k * m);
+        double* G2 = G1 + k * m;
+        c.gram(U, k, X, m, G1);  // U^T X
+        small_gemm(transpose, false, (int)k, (int)m, (int)k, 1.0, T, (int)k, G1, (int)k, 0.0, G2, (int)k, st);
+        GemmPass gp;
+        gp.A = U;
+        gp.lda = n;
+        gp.M = n;
+        gp.K = k;
+        gp.ncols = m;
+        gp.alpha = -1.0;
+        gp.in = ColMap::plain(G2, k);
+        gp.out = ColMap::plain(out, n);
+        gp.add = ColMap::plain(X, n);
+        gemm_nn(&gp, 1, nullptr, st);
+    };
+    double* V1 = c.buf(P_F, n * m);
+    const double* CQ = Q;
+    if (k) {
+        apply_lmp(Q, V1, false);
+        CQ = V1;
+    }
+    double* AV = c.buf(P_AZ, n * m);
+    c.apply(CQ, m, AV);
+    const double* Y = AV;
+    if (k) {
+        apply_lmp(AV, V1, true);
+        Y = V1;
+    }
+    // K = sym(Q^T Y), eigenvalues decreasing (spectrum.cpp:56-62)
+    double* K = c.buf(P_K, m * m);
+    c.gram(Q, m, Y, m, K);
+    double* Wv = c.buf(P_W, m * m);
+    sym_evd_desc((int)m, K, vals_out, Wv, c.pool[P_SMALLWS], st);
+}
 
 void rayleigh_ritz_dev(wc4dvar_op& op, const double* Z, int64_t ldz, int64_t m, double* U_out,
                        int64_t ldu, double* theta_out, cudaStream_t st) {

@@ -101,6 +101,10 @@ SIGNATURES = {
     "wc4dvar_gpu_op_apply_block_dev": (ctypes.c_int, [_vp, _vp, _i64, _i64, _vp, _i64, _vp]),
     "wc4dvar_gpu_hessian_piece": (ctypes.c_int, [_vp, ctypes.c_int, _dp, _i64, _i64, _dp, _i64]),
     "wc4dvar_gpu_hessian_piece_dev": (ctypes.c_int, [_vp, ctypes.c_int, _vp, _i64, _i64, _vp, _i64, _vp]),
+    "wc4dvar_gpu_observation_range": (ctypes.c_int, [_vp, _dp, _i64]),
+    "wc4dvar_gpu_observation_range_dev": (ctypes.c_int, [_vp, _vp, _i64, _vp]),
+    "wc4dvar_gpu_clustered_spectrum": (ctypes.c_int, [_vp, _vp, _dp, _i64, _dp, ctypes.POINTER(_i64),
+                                                      ctypes.POINTER(_i64)]),
     "wc4dvar_gpu_op_profile": (ctypes.c_int, [_vp, ctypes.c_int]),
     "wc4dvar_gpu_op_profile_read": (ctypes.c_int, [_vp, _dp, ctypes.POINTER(_i64)]),
     "wc4dvar_gpu_probe_dmma_peak": (ctypes.c_int, [ctypes.c_int, ctypes.POINTER(ctypes.c_double)]),
@@ -492,6 +496,15 @@ class HessianOperator(LinearOperator):
         _check(lib.wc4dvar_gpu_hessian_piece(self._h, which, _p(v), v.shape[0], m, _p(out), v.shape[0]))
         return out
 
+    def observation_range(self) -> np.ndarray:
+        """operators.cpp:146-154: D^{1/2} L^{-T} H^T [e_1..e_q] (dim x q), one block
+        adjoint sweep on the device."""
+        q = self.net.q
+        W = np.empty((self.dim(), q), order="F")
+        if q:
+            _check(lib.wc4dvar_gpu_observation_range(self.handle, _p(W), self.dim()))
+        return W
+
     def apply_Linv(self, p):
         """operators.cpp:79-89 (vector or block)."""
         return self._piece(0, "apply_Linv", p)
@@ -786,8 +799,51 @@ class SolverSpec:
 
 
 @dataclass
+class ClusteredSpectrum:
+    """spectrum.hpp:13-24: the eigenvalues of the (preconditioned) Hessian that can differ
+    from 1 (decreasing) and the multiplicity of the unit cluster."""
+
+    nonunit: np.ndarray
+    unit_multiplicity: int
+
+    def min_eigenvalue(self) -> float:
+        """spectrum.cpp:9-13"""
+        m = 1.0 if self.unit_multiplicity > 0 else math.inf
+        return min(m, float(self.nonunit.min())) if len(self.nonunit) else m
+
+    def max_eigenvalue(self) -> float:
+        """spectrum.cpp:15-19"""
+        m = 1.0 if self.unit_multiplicity > 0 else -math.inf
+        return max(m, float(self.nonunit.max())) if len(self.nonunit) else m
+
+    def full(self) -> np.ndarray:
+        """spectrum.cpp:21-29: every eigenvalue, decreasing."""
+        return np.sort(np.concatenate([self.nonunit, np.ones(self.unit_multiplicity)]))[::-1]
+
+
+def clustered_spectrum(op: "HessianOperator", precond: Optional["LmpFactor"] = None,
+                       obs_range: Optional[np.ndarray] = None) -> ClusteredSpectrum:
+    """spectrum.cpp:31-64 on the device: orthonormal basis of [W | U], C^T A C on it (q + k
+    block applies), symmetric EVD of the projected matrix."""
+    require(isinstance(op, HessianOperator), "clustered_spectrum: operator is not a HessianOperator")
+    k = precond.k() if (precond is not None and not precond.is_identity()) else 0
+    q = op.net.q
+    W = None
+    if obs_range is not None:
+        W = np.asfortranarray(obs_range, dtype=np.float64)
+        require(W.shape[0] == op.dim(), "clustered_spectrum: observation range mismatch")
+        q = W.shape[1]
+    vals = np.empty(max(q + k, 1))
+    nn, unit = _i64(0), _i64(0)
+    _check(lib.wc4dvar_gpu_clustered_spectrum(op.handle, precond.handle if k else None, _p(W),
+                                              W.shape[0] if W is not None else op.dim(), _p(vals),
+                                              ctypes.byref(nn), ctypes.byref(unit)))
+    return ClusteredSpectrum(vals[:nn.value].copy(), int(unit.value))
+
+
+@dataclass
 class InnerLoopReport:
-    """assimilation.hpp:86-97 (without the desk-scale preconditioned extremes)."""
+    """assimilation.hpp:86-97."""
 
     delta_p: np.ndarray
     delta_p_tilde: np.ndarray
@@ -797,10 +853,11 @@ class InnerLoopReport:
     converged: bool
     precond: PrecondSpec
     ritz_values: np.ndarray
+    preconditioned_extremes: Optional[tuple] = None  # (min, max) when dim <= dense_cap
 
 
 def run_inner_loop(hessian: HessianOperator, b, d, precond: PrecondSpec, solver: SolverSpec,
-                   omega: Optional[np.ndarray] = None) -> InnerLoopReport:
+                   omega: Optional[np.ndarray] = None, dense_cap: int = 4096) -> InnerLoopReport:
     """run_inner_loop, assimilation.cpp:192-253, from the innovations b (control space) and
     d (observation space) of compute_innovations (assimilation.cpp:119-128): QuadraticCost
     -> randomized LMP -> split PCG on the cost's RHS -> delta_p = D^{1/2} x."""
@@ -814,9 +871,13 @@ def run_inner_loop(hessian: HessianOperator, b, d, precond: PrecondSpec, solver:
     opts = PcgOptions(solver.max_iter, solver.rel_tol, solver.reorthogonalize,
                       cost if solver.record_cost else None)
     sol = pcg_split(hessian, cost.rhs(), factor, None, opts)
+    extremes = None
+    if hessian.dim() <= dense_cap:  # desk-scale diagnostic (assimilation.cpp:248-251)
+        cs = clustered_spectrum(hessian, factor)
+        extremes = (cs.min_eigenvalue(), cs.max_eigenvalue())
     return InnerLoopReport(hessian.apply_D_half(sol.x), sol.x, sol.history.quadratic_costs,
                            sol.history.residual_norms, sol.history.iterations, sol.history.converged,
-                           precond, ritz)
+                           precond, ritz, extremes)
 
 
 def pcg_split(op: LinearOperator, b, precond: Optional[LmpFactor] = None, x0=None,
