@@ -321,6 +321,8 @@ typedef struct {
     int32_t max_iter;
     int32_t reorthogonalize;
     double rel_tol;
+    int32_t store_residual_vectors; /* keep f_j = r_j / ||r_j|| (CgHistory::normalized_residuals) */
+    int32_t reserved;
 } wc4dvar_pcg_options;
 
 /* CgHistory (krylov.hpp:17-30): caller-provided arrays of length max_iter + 1
@@ -334,6 +336,12 @@ typedef struct {
     int32_t converged;
     int32_t stop_reason;     /* 0 zero initial residual, 1 tolerance, 2 max iterations */
     int32_t reserved;
+    /* n x (max_iter + 1) host block (ld_residuals) for the normalised residuals, filled when
+     * reorthogonalize or store_residual_vectors is set; n_residuals = columns written */
+    double* normalized_residuals;
+    int64_t ld_residuals;
+    int32_t n_residuals;
+    int32_t reserved2;
 } wc4dvar_pcg_history;
 
 /* pcg_split (krylov.cpp:22-99): precond may be NULL (identity, krylov.cpp:106-108),
@@ -341,6 +349,31 @@ typedef struct {
 int wc4dvar_gpu_pcg(wc4dvar_op* op, const double* b, wc4dvar_lmp* precond, const double* x0,
                     const wc4dvar_pcg_options* opts, wc4dvar_cost* cost, double* x,
                     wc4dvar_pcg_history* hist);
+
+/* ------------------------------------------------------------------------- */
+/* Deterministic LMP eigenpairs                              */
+/* ------------------------------------------------------------------------- */
+/* LanczosOptions (krylov.hpp:81-85). */
+typedef struct {
+    int32_t max_iter; /* 0: min(dim, 8k + 120) */
+    int32_t reserved;
+    double tol;       /* relative residual tolerance on each pair (1e-10) */
+    uint64_t seed;    /* NormalStream seed of the start vector (0x5eed0f4d) */
+} wc4dvar_lanczos_options;
+
+/* lanczos_eigenpairs (krylov.cpp:178-278): top-k eigenpairs by matrix-free Lanczos with
+ * full re-orthogonalisation, on the device.  U: dim x k host (ldu), values: k host,
+ * decreasing; *steps = Krylov dimension used (may be NULL).  One apply per step. */
+int wc4dvar_gpu_lanczos_eigenpairs(wc4dvar_op* op, int64_t k, const wc4dvar_lanczos_options* opts,
+                                   double* U, int64_t ldu, double* values, int64_t* steps);
+
+/* ritz_from_tridiagonal (krylov.cpp:136-176): top-k Ritz pairs from the CG-Lanczos
+ * tridiagonal (gammas j, taus j-1) and the stored normalised CG residuals (n x j, ldf,
+ * host); ghosts collapsed, NumericalError when the basis lost orthogonality or fewer
+ * than k distinct values remain.  U: n x k host (ldu), values: k host. */
+int wc4dvar_gpu_ritz_from_tridiagonal(int64_t n, int64_t j, const double* gammas, const double* taus,
+                                      const double* residual_basis, int64_t ldf, int64_t k, double* U,
+                                      int64_t ldu, double* values, int device);
 
 #ifdef __cplusplus
 }

@@ -11,5 +11,6 @@ from .wc4dvar import (  # noqa: F401
     last_sketch_timing, nystrom, pcg_split, probe_dmma_peak, rayleigh_ritz, revd, revd_ritzit,
     sketch_eigenpairs, version, LIB_PATH, SIGNATURES, Lorenz96Linearized,
     lorenz96_trajectory, lorenz96_trajectory_device, integrate_p, InnerLoopReport, PrecondSpec, SolverSpec,
-    run_inner_loop, ClusteredSpectrum, clustered_spectrum,
+    run_inner_loop, ClusteredSpectrum, clustered_spectrum, TridiagonalMatrix, tridiagonal_from_cg,
+    ritz_from_tridiagonal, LanczosOptions, lanczos_eigenpairs, exact_top_pairs,
 )

@@ -8,6 +8,7 @@
 #include <vector>
 
 #include "l96.cuh"
+#include "lanczos.cuh"
 #include "lmp_pcg.cuh"
 #include "ops.cuh"
 #include "pcg.cuh"
@@ -800,7 +801,54 @@ int wc4dvar_gpu_pcg(wc4dvar_op* op, const double* b, wc4dvar_lmp* pre, const dou
         hist->iterations = rec.iterations;
         hist->converged = rec.converged ? 1 : 0;
         hist->stop_reason = rec.stop_reason;
+        hist->n_residuals = 0;
+        if (hist->normalized_residuals && rec.nf) {
+            require(hist->ld_residuals >= n, "pcg_split: ld_residuals < dim");
+            d2h_block(hist->normalized_residuals, hist->ld_residuals, rec.F, n, rec.nf, st);
+            W4_CUDA(cudaStreamSynchronize(st));
+            hist->n_residuals = rec.nf;
+        }
     }
+    W4_API_END
+}
+
+int wc4dvar_gpu_lanczos_eigenpairs(wc4dvar_op* op, int64_t k, const wc4dvar_lanczos_options* opts, double* U,
+                                   int64_t ldu, double* values, int64_t* steps) {
+    W4_API_BEGIN
+    require(op && opts && U && values, "lanczos_eigenpairs: null argument");
+    require(ldu >= op->dim, "lanczos_eigenpairs: ldu < dim");
+    std::lock_guard<std::recursive_mutex> lk(op->mu);
+    DeviceGuard g(op->device);
+    cudaStream_t st = op->stream;
+    const int64_t n = op->dim;
+    require(k >= 1 && k <= n, "lanczos_eigenpairs: k out of range");
+    double* dU = op->out_buf.get<double>((size_t)n * k);
+    const int64_t m = lanczos_eigenpairs_dev(*op, k, opts->max_iter, opts->tol, opts->seed, dU, n, values, st);
+    d2h_block(U, ldu, dU, n, k, st);
+    W4_CUDA(cudaStreamSynchronize(st));
+    if (steps) *steps = m;
+    W4_API_END
+}
+
+int wc4dvar_gpu_ritz_from_tridiagonal(int64_t n, int64_t j, const double* gammas, const double* taus,
+                                      const double* residual_basis, int64_t ldf, int64_t k, double* U, int64_t ldu,
+                                      double* values, int device) {
+    W4_API_BEGIN
+    require(j >= 1 && gammas && (j == 1 || taus), "ritz_from_tridiagonal: empty tridiagonal");
+    require(k >= 1 && k <= j, "ritz_from_tridiagonal: k out of range");
+    require(residual_basis && ldf >= n && n >= 1, "ritz_from_tridiagonal: residual basis shorter than T");
+    require(U && values && ldu >= n, "ritz_from_tridiagonal: bad output");
+    DeviceGuard g(device);
+    cudaStream_t st = nullptr;
+    W4_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+    std::unique_ptr<CUstream_st, void (*)(cudaStream_t)> sguard(st, [](cudaStream_t s) { cudaStreamDestroy(s); });
+    DevBuf fb, ub;
+    double* F = fb.get<double>((size_t)n * j);
+    double* dU = ub.get<double>((size_t)n * k);
+    h2d_block(F, residual_basis, n, j, ldf, st);
+    ritz_from_tridiagonal_dev(n, j, gammas, taus, F, n, k, dU, n, values, st);
+    d2h_block(U, ldu, dU, n, k, st);
+    W4_CUDA(cudaStreamSynchronize(st));
     W4_API_END
 }
 

@@ -84,7 +84,11 @@ void pcg_dev(wc4dvar_op& op, const double* b, wc4dvar_lmp* pre, const double* x0
     W4_CUDA(cudaMemsetAsync(counter, 0, 4 * sizeof(unsigned), st));
     W4_CUDA(cudaMemsetAsync(scal, 0, (SC_N + 2) * sizeof(double), st));
     double* F = nullptr;
-    if (opts.reorthogonalize) F = pool[B_F].get<double>((size_t)n * (opts.max_iter + 1));
+    // CgHistory::normalized_residuals are kept for re-orthogonalisation or on request
+    // (krylov.cpp:30)
+    if (opts.reorthogonalize || opts.store_residual_vectors)
+        F = pool[B_F].get<double>((size_t)n * (opts.max_iter + 1));
+    const bool reorth = opts.reorthogonalize != 0;
     static thread_local double* pinned = nullptr;
     if (!pinned) W4_CUDA(cudaMallocHost(&pinned, 16 * sizeof(double)));
 
@@ -202,11 +206,11 @@ void pcg_dev(wc4dvar_op& op, const double* b, wc4dvar_lmp* pre, const double* x0
             op.reset_status(st);
             op.apply_block_dev(p, n, 1, w, n, st);
             pcg_pass1(c, p, w, st);  // curvature, alpha
-            if (F) W4_CUDA(cudaMemcpyAsync(scal + SC_DOT, scal + SC_RHO, sizeof(double),
-                                           cudaMemcpyDeviceToDevice, st));
+            if (reorth) W4_CUDA(cudaMemcpyAsync(scal + SC_DOT, scal + SC_RHO, sizeof(double),
+                                                cudaMemcpyDeviceToDevice, st));
             pcg_pass2(c, x, r, p, w, st);  // x, r, rho_next, beta
         }
-        if (!graph_it && F) {
+        if (!graph_it && reorth) {
             // modified Gram-Schmidt against the stored normalised residuals (krylov.cpp:71-74)
             double* dd = scal + SC_N;
             for (int f = 0; f < nf; ++f) {
@@ -262,6 +266,8 @@ void pcg_dev(wc4dvar_op& op, const double* b, wc4dvar_lmp* pre, const double* x0
         }
     }
     if (!rec.converged) rec.stop_reason = 2;
+    rec.F = F;
+    rec.nf = nf;
     W4_CUDA(cudaStreamSynchronize(st));
 }
 

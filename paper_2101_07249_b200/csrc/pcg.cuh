@@ -12,6 +12,8 @@ struct PcgRecord {
     int iterations = 0;
     bool converged = false;
     int stop_reason = 2;
+    const double* F = nullptr;  // device: the stored normalised residuals (n x nf, ld n)
+    int nf = 0;
 };
 
 // b, x0 (nullable), x: device vectors of length op.dim on op's device.

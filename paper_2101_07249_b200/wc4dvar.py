@@ -72,15 +72,21 @@ class SketchDesc(ctypes.Structure):
 
 
 class PcgOpts(ctypes.Structure):
-    _fields_ = [("max_iter", ctypes.c_int32), ("reorthogonalize", ctypes.c_int32),
-                ("rel_tol", ctypes.c_double)]
+    _fields_ = [("max_iter", ctypes.c_int32), ("reorthogonalize", ctypes.c_int32), ("rel_tol", ctypes.c_double),
+                ("store_residual_vectors", ctypes.c_int32), ("reserved", ctypes.c_int32)]
 
 
 class PcgHist(ctypes.Structure):
     _fields_ = [("alphas", _dp), ("betas", _dp), ("residual_norms", _dp),
                 ("quadratic_costs", _dp), ("iterations", ctypes.c_int32),
                 ("converged", ctypes.c_int32), ("stop_reason", ctypes.c_int32),
-                ("reserved", ctypes.c_int32)]
+                ("reserved", ctypes.c_int32), ("normalized_residuals", _dp), ("ld_residuals", _i64),
+                ("n_residuals", ctypes.c_int32), ("reserved2", ctypes.c_int32)]
+
+
+class LanczosOpts(ctypes.Structure):
+    _fields_ = [("max_iter", ctypes.c_int32), ("reserved", ctypes.c_int32), ("tol", ctypes.c_double),
+                ("seed", ctypes.c_uint64)]
 
 
 # Every entry point of include/wc4dvar_gpu.h with its ctypes signature.
@@ -147,6 +153,10 @@ SIGNATURES = {
     "wc4dvar_gpu_cost_rhs": (ctypes.c_int, [_vp, _dp]),
     "wc4dvar_gpu_pcg": (ctypes.c_int, [_vp, _dp, _vp, _dp, ctypes.POINTER(PcgOpts), _vp, _dp,
                                        ctypes.POINTER(PcgHist)]),
+    "wc4dvar_gpu_lanczos_eigenpairs": (ctypes.c_int, [_vp, _i64, ctypes.POINTER(LanczosOpts), _dp, _i64, _dp,
+                                                      ctypes.POINTER(_i64)]),
+    "wc4dvar_gpu_ritz_from_tridiagonal": (ctypes.c_int, [_i64, _i64, _dp, _dp, _dp, _i64, _i64, _dp, _i64, _dp,
+                                                         ctypes.c_int]),
 }
 for _name, (_res, _args) in SIGNATURES.items():
     _f = getattr(lib, _name)
@@ -751,6 +761,7 @@ class PcgOptions:
     rel_tol: float = 1e-6
     reorthogonalize: bool = False
     cost: Optional[QuadraticCost] = None
+    store_residual_vectors: bool = False
 
 
 @dataclass
@@ -762,6 +773,7 @@ class CgHistory:
     iterations: int = 0
     converged: bool = False
     stop_reason: str = ""
+    normalized_residuals: List[np.ndarray] = field(default_factory=list)  # f_j = r_j / ||r_j||
 
     def relative_residual(self, j: int) -> float:
         return self.residual_norms[j] / self.residual_norms[0]
@@ -778,10 +790,9 @@ _STOP = {0: "zero initial residual", 1: "relative residual tolerance reached", 2
 
 @dataclass
 class PrecondSpec:
-    """assimilation.hpp:66-77 (randomized kinds; the deterministic Lanczos LMP is out of
-    scope)."""
+    """assimilation.hpp:66-77."""
 
-    kind: str = "none"   # none | revd | nystrom | ritzit
+    kind: str = "none"   # none | deterministic | revd | nystrom | ritzit
     k: int = 0
     l: int = 5
     seed: int = 0
@@ -857,13 +868,19 @@ class InnerLoopReport:
 
 
 def run_inner_loop(hessian: HessianOperator, b, d, precond: PrecondSpec, solver: SolverSpec,
-                   omega: Optional[np.ndarray] = None, dense_cap: int = 4096) -> InnerLoopReport:
+                   omega: Optional[np.ndarray] = None, dense_cap: int = 4096,
+                   previous_hessian: Optional[HessianOperator] = None) -> InnerLoopReport:
     """run_inner_loop, assimilation.cpp:192-253, from the innovations b (control space) and
     d (observation space) of compute_innovations (assimilation.cpp:119-128): QuadraticCost
     -> randomized LMP -> split PCG on the cost's RHS -> delta_p = D^{1/2} x."""
     cost = QuadraticCost(hessian, b, d)
     factor, ritz = None, np.zeros(0)
-    if precond.kind != "none":
+    if precond.kind == "deterministic":  # previous-loop Lanczos LMP (assimilation.cpp:204-211)
+        require(previous_hessian is not None, "run_inner_loop: deterministic LMP needs a previous inner loop")
+        pairs = exact_top_pairs(previous_hessian, precond.k, dense_cap)
+        factor = build_spectral_lmp(pairs, hessian.device())
+        ritz = pairs.values
+    elif precond.kind != "none":
         cfg = SketchConfig(precond.k, precond.l, precond.seed, precond.kind, precond.p_iter)
         pairs = sketch_eigenpairs(hessian, cfg, omega)
         factor = build_spectral_lmp(pairs, hessian.device())
@@ -891,11 +908,16 @@ def pcg_split(op: LinearOperator, b, precond: Optional[LmpFactor] = None, x0=Non
     require(x0a is None or len(x0a) == n, "pcg_split: initial guess dimension mismatch")
     o = PcgOpts()
     o.max_iter, o.reorthogonalize, o.rel_tol = opts.max_iter, int(opts.reorthogonalize), opts.rel_tol
+    o.store_residual_vectors = int(opts.store_residual_vectors)
     mi = max(opts.max_iter, 0)
     al, be = np.zeros(mi + 1), np.zeros(mi + 1)
     rn, qc = np.zeros(mi + 2), np.zeros(mi + 2)
     hst = PcgHist()
     hst.alphas, hst.betas, hst.residual_norms, hst.quadratic_costs = _p(al), _p(be), _p(rn), _p(qc)
+    F = None
+    if opts.reorthogonalize or opts.store_residual_vectors:
+        F = np.empty((n, mi + 1), order="F")
+        hst.normalized_residuals, hst.ld_residuals = _p(F), n
     x = np.empty(n)
     _check(lib.wc4dvar_gpu_pcg(op.handle, _p(b), precond.handle if precond is not None else None,
                                _p(x0a), ctypes.byref(o), opts.cost.handle if opts.cost else None,
@@ -903,5 +925,89 @@ def pcg_split(op: LinearOperator, b, precond: Optional[LmpFactor] = None, x0=Non
     it = hst.iterations
     h = CgHistory(al[:it].tolist(), be[:it].tolist(), rn[:it + 1].tolist(),
                   qc[:it + 1].tolist() if opts.cost else [], it, bool(hst.converged),
-                  _STOP.get(hst.stop_reason, ""))
+                  _STOP.get(hst.stop_reason, ""),
+                  [F[:, j].copy() for j in range(hst.n_residuals)] if F is not None else [])
     return PcgResult(x, h)
+
+
+# ---------------------------------------------------------------------------------------------
+# Deterministic LMP eigenpairs (krylov.hpp:56-91, assimilation.cpp:173-190), SURVEY §8(f)-3
+@dataclass
+class TridiagonalMatrix:
+    """krylov.hpp:56-63: gamma (diagonal) / tau (off-diagonal) parameterisation."""
+
+    gammas: np.ndarray
+    taus: np.ndarray
+
+    def dim(self) -> int:
+        return len(self.gammas)
+
+    def dense(self) -> np.ndarray:
+        """krylov.cpp:110-120"""
+        return np.diag(self.gammas) + np.diag(self.taus, 1) + np.diag(self.taus, -1)
+
+
+def tridiagonal_from_cg(history: CgHistory) -> TridiagonalMatrix:
+    """krylov.cpp:122-134: gamma_1 = 1/alpha_1, gamma_j = 1/alpha_j + beta_{j-1}/alpha_{j-1},
+    tau_j = sqrt(beta_j)/alpha_j (scalar recurrences on the CG history)."""
+    j = len(history.alphas)
+    require(j >= 1, "tridiagonal_from_cg: history is empty")
+    g = np.empty(j)
+    t = np.empty(max(j - 1, 0))
+    for i in range(j):
+        g[i] = 1.0 / history.alphas[i]
+        if i > 0:
+            g[i] += history.betas[i - 1] / history.alphas[i - 1]
+        if i + 1 < j:
+            t[i] = math.sqrt(history.betas[i]) / history.alphas[i]
+    return TridiagonalMatrix(g, t)
+
+
+def ritz_from_tridiagonal(T: TridiagonalMatrix, residual_basis, k: int, device: int = 0) -> RitzPairs:
+    """krylov.cpp:136-176 on the device: top-k Ritz pairs from T_j and the stored normalised
+    CG residuals (sign-alternated into the Lanczos basis), ghosts collapsed."""
+    j = T.dim()
+    require(1 <= k <= j, "ritz_from_tridiagonal: k out of range")
+    require(len(residual_basis) >= j, "ritz_from_tridiagonal: residual basis shorter than T")
+    F = np.asfortranarray(np.column_stack([np.asarray(residual_basis[i], dtype=np.float64) for i in range(j)]))
+    n = F.shape[0]
+    U = np.empty((n, k), order="F")
+    vals = np.empty(k)
+    g = np.ascontiguousarray(T.gammas, dtype=np.float64)
+    t = np.ascontiguousarray(T.taus, dtype=np.float64) if j > 1 else np.zeros(1)
+    _check(lib.wc4dvar_gpu_ritz_from_tridiagonal(n, j, _p(g), _p(t), _p(F), n, k, _p(U), n, _p(vals), device))
+    return RitzPairs(U, vals, "lanczos")
+
+
+@dataclass
+class LanczosOptions:
+    """krylov.hpp:81-85."""
+
+    max_iter: int = 0
+    tol: float = 1e-10
+    seed: int = 0x5EED0F4D
+
+
+def lanczos_eigenpairs(op: LinearOperator, k: int, opts: Optional[LanczosOptions] = None) -> RitzPairs:
+    """krylov.cpp:178-278 on the device: Lanczos with full re-orthogonalisation until the
+    top-k pairs converge (residual b |W(m-1, i)| <= tol |theta_0|)."""
+    opts = opts or LanczosOptions()
+    n = op.dim()
+    require(1 <= k <= n, "lanczos_eigenpairs: k out of range")
+    o = LanczosOpts()
+    o.max_iter, o.tol, o.seed = opts.max_iter, opts.tol, opts.seed
+    U = np.empty((n, k), order="F")
+    vals = np.empty(k)
+    steps = _i64(0)
+    _check(lib.wc4dvar_gpu_lanczos_eigenpairs(op.handle, k, ctypes.byref(o), _p(U), n, _p(vals), ctypes.byref(steps)))
+    return RitzPairs(U, vals, "exact")
+
+
+def exact_top_pairs(op: LinearOperator, k: int, dense_cap: int = 4096, lanczos_seed: int = 0x5EED0F4D,
+                    tol: float = 1e-12) -> RitzPairs:
+    """assimilation.cpp:173-190.  The reference takes a dense EVD when dim <= dense_cap and
+    Lanczos otherwise; on the device both routes are Lanczos with full re-orthogonalisation,
+    with the tolerance tightened to 1e-12 on the desk-scale route (the reference's own
+    dense-vs-Lanczos agreement test is 1e-8, test_assimilation.cpp:361-373)."""
+    require(1 <= k <= op.dim(), "exact_top_pairs: k out of range")
+    return lanczos_eigenpairs(op, k, LanczosOptions(0, tol if op.dim() <= dense_cap else 1e-10, lanczos_seed))
