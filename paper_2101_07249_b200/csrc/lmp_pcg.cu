@@ -43,25 +43,36 @@ __global__ void __launch_bounds__(kBlock)
     const int64_t rem_rows = c.n - row0;
     const int rows = (int)(rem_rows < RB ? rem_rows : RB);
 
-    // Stage this CTA's U rows once (coalesced per column).
+    // Stage this CTA's U rows once (coalesced per column) with cp.async: every copy of the
+    // thread is in flight at once instead of one L2 round trip per element.
     for (int e = tid; e < k * RB; e += kBlock) {
         const int i = e / RB, rr = e % RB;
-        Us[i * ks + rr] = rr < rows ? c.U[row0 + rr + (int64_t)i * c.ldu] : 0.0;
+        if (rr < rows) {
+            const unsigned d = static_cast<unsigned>(__cvta_generic_to_shared(Us + i * ks + rr));
+            asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(d),
+                         "l"(c.U + row0 + rr + (int64_t)i * c.ldu));
+        } else {
+            Us[i * ks + rr] = 0.0;
+        }
     }
+    asm volatile("cp.async.wait_all;\n" ::: "memory");
     // Coefficients for the U-apply: APPLY uses op(T) gin, P2 uses T^T g, P3 uses T h.
     if (MODE == M_APPLY || MODE == M_APPLY_T || MODE == M_P2 || MODE == M_P3) {
         const double* gv = (MODE == M_APPLY || MODE == M_APPLY_T) ? A.gin
                            : (MODE == M_P2)                     ? c.g
                                                                 : c.h;
         const bool trans = (MODE == M_APPLY_T || MODE == M_P2);
-        for (int i = tid; i < k; i += kBlock) {
+        // one warp per coefficient, lanes stride j (independent L2 loads, fixed-order tree)
+        const int warp = tid >> 5, lane = tid & 31;
+        for (int i = warp; i < k; i += kBlock / 32) {
             double s = 0.0;
             if (trans) {  // (T^T g)_i = sum_{j<=i} T[j,i] g_j
-                for (int j = 0; j <= i; ++j) s += c.T[j + (int64_t)i * k] * gv[j];
+                for (int j = lane; j <= i; j += 32) s += c.T[j + (int64_t)i * k] * gv[j];
             } else {      // (T h)_i = sum_{j>=i} T[i,j] h_j
-                for (int j = i; j < k; ++j) s += c.T[i + (int64_t)j * k] * gv[j];
+                for (int j = i + lane; j < k; j += 32) s += c.T[i + (int64_t)j * k] * gv[j];
             }
-            ys[i] = s;
+            s = warp_sum(s);
+            if (lane == 0) ys[i] = s;
         }
     }
     __syncthreads();
@@ -139,9 +150,19 @@ __global__ void __launch_bounds__(kBlock)
     double* res = (MODE == M_UTV) ? A.out : (MODE == M_P1 ? c.g : c.h);
     // final sums over the CTAs' partials: one warp per entry, lanes stride the CTAs (the
     // loads of a lane are independent, so they pipeline instead of forming one long chain)
+    // (each lane issues its up-to-8 loads per 256-CTA chunk before summing them in order)
     for (int i = tid >> 5; i <= k; i += kBlock / 32) {
         double s = 0.0;
-        for (unsigned b = tid & 31; b < gridDim.x; b += 32) s += __ldcg(c.partial + (int64_t)b * (k + 1) + i);
+        for (unsigned b0 = tid & 31; b0 < gridDim.x; b0 += 256) {
+            double v[8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+                const unsigned b = b0 + 32 * u;
+                v[u] = b < gridDim.x ? __ldcg(c.partial + (int64_t)b * (k + 1) + i) : 0.0;
+            }
+#pragma unroll
+            for (int u = 0; u < 8; ++u) s += v[u];
+        }
         s = warp_sum(s);
         if ((tid & 31) == 0) res[i] = s;
     }

@@ -8,6 +8,7 @@
 #include <cmath>
 #include <cstdlib>
 #include <sstream>
+#include <vector>
 
 #include "lmp_pcg.cuh"
 
@@ -51,6 +52,33 @@ __global__ void scale_copy_kernel(int64_t n, const double* __restrict__ r, const
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
          i += (int64_t)gridDim.x * blockDim.x)
         f[i] = r[i] * inv;
+}
+
+// Device-side loop control for iterations 2.. of the unpreconditioned-cost path: record
+// alpha / beta / |r| of iteration j, stop (condition 0) on an error, on convergence or at
+// max_iter.  state = {j, err, status, converged}.
+__global__ void pcg_loop_check_kernel(cudaGraphConditionalHandle h, const double* __restrict__ scal,
+                                      const unsigned* __restrict__ status, int* state, double* alphas,
+                                      double* betas, double* res, double r0, double tol, int max_iter) {
+    const int j = state[0] + 1;
+    state[0] = j;
+    const unsigned s = *status;
+    const double curv = scal[SC_CURV], alpha = scal[SC_ALPHA], rn = scal[SC_RHO_NEXT], beta = scal[SC_BETA];
+    int err = 0;
+    if (s) err = 1;
+    else if (!isfinite(curv) || curv <= 0.0 || !isfinite(alpha) || !isfinite(beta)) err = 2;
+    if (err) {
+        state[1] = err;
+        state[2] = (int)s;
+        cudaGraphSetConditional(h, 0);
+        return;
+    }
+    alphas[j - 1] = alpha;
+    betas[j - 1] = beta;
+    res[j] = sqrt(rn);
+    const bool conv = sqrt(rn) / r0 <= tol;
+    if (conv) state[3] = 1;
+    cudaGraphSetConditional(h, (conv || j >= max_iter) ? 0u : 1u);
 }
 
 void check_finite(double v, const char* what, int it) {
@@ -181,7 +209,119 @@ void pcg_dev(wc4dvar_op& op, const double* b, wc4dvar_lmp* pre, const double* x0
         W4_CUDA(cudaMemcpyAsync(op.h_status, op.d_status, sizeof(unsigned), cudaMemcpyDeviceToHost, st));
         W4_CUDA(cudaMemcpyAsync(pinned, scal, SC_N * sizeof(double), cudaMemcpyDeviceToHost, st));
     };
+    // Iterations 2.. can run as ONE graph launch: a conditional WHILE node whose body is the
+    // iteration plus a check kernel that records alpha / beta / |r| on the device and stops
+    // the loop; the host reads the history once at the end.  Used when nothing needs the
+    // host per iteration (no cost recorder, no re-orthogonalisation, no profiling).
+    // WC4DVAR_PCG_DEVLOOP=0 keeps the per-iteration graph + host check.
+    static const bool devloop_env = [] {
+        const char* e = std::getenv("WC4DVAR_PCG_DEVLOOP");
+        return !(e && std::atoi(e) == 0);
+    }();
+    const bool dev_loop = use_graph && devloop_env && !cost;
+    // returns false when the loop graph could not be built (the host loop then continues)
+    auto run_dev_loop = [&](int j0) -> bool {
+        const int left = opts.max_iter - j0 + 1;
+        DevBuf rec_buf;
+        double* hist = rec_buf.get<double>((size_t)3 * (opts.max_iter + 2) + 4);
+        double* d_al = hist;
+        double* d_be = hist + (opts.max_iter + 2);
+        double* d_rs = hist + 2 * (opts.max_iter + 2);
+        int* state = reinterpret_cast<int*>(hist + 3 * (opts.max_iter + 2));
+        std::vector<int> st0 = {j0 - 1, 0, 0, 0};
+        W4_CUDA(cudaMemcpyAsync(state, st0.data(), sizeof(int) * 4, cudaMemcpyHostToDevice, st));
+        W4_CUDA(cudaStreamSynchronize(st));
+        cudaGraph_t g = nullptr, bodyg = nullptr;
+        cudaGraphExec_t ex = nullptr;
+        bool ok = cudaGraphCreate(&g, 0) == cudaSuccess;
+        cudaGraphConditionalHandle h{};
+        if (ok) ok = cudaGraphConditionalHandleCreate(&h, g, 1, cudaGraphCondAssignDefault) == cudaSuccess;
+        cudaGraphNode_t node;
+        cudaGraphNodeParams cp = {};
+        if (ok) {
+            cp.type = cudaGraphNodeTypeConditional;
+            cp.conditional.handle = h;
+            cp.conditional.type = cudaGraphCondTypeWhile;
+            cp.conditional.size = 1;
+            ok = cudaGraphAddNode(&node, g, nullptr, 0, &cp) == cudaSuccess;
+        }
+        if (ok) {
+            bodyg = cp.conditional.phGraph_out[0];
+            ok = cudaStreamBeginCaptureToGraph(st, bodyg, nullptr, nullptr, 0, cudaStreamCaptureModeRelaxed) ==
+                 cudaSuccess;
+            if (ok) {
+                try {
+                    op.reset_status(st);
+                    op.apply_block_dev(p, n, 1, w, n, st);
+                    pcg_pass1(c, p, w, st);
+                    pcg_pass2(c, x, r, p, w, st);
+                    pcg_pass3(c, r, p, st);
+                    pcg_loop_check_kernel<<<1, 1, 0, st>>>(h, scal, op.d_status, state, d_al, d_be, d_rs, r0,
+                                                           opts.rel_tol, opts.max_iter);
+                } catch (...) {
+                    ok = false;
+                }
+                cudaGraph_t cap = nullptr;
+                if (cudaStreamEndCapture(st, &cap) != cudaSuccess) ok = false;
+            }
+        }
+        if (ok) ok = cudaGraphInstantiate(&ex, g, 0) == cudaSuccess;
+        if (!ok) {
+            cudaGetLastError();  // clear a sticky capture / instantiate error
+            if (ex) cudaGraphExecDestroy(ex);
+            if (g) cudaGraphDestroy(g);
+            return false;
+        }
+        W4_CUDA(cudaGraphLaunch(ex, st));
+        std::vector<int> hs(4);
+        W4_CUDA(cudaMemcpyAsync(hs.data(), state, sizeof(int) * 4, cudaMemcpyDeviceToHost, st));
+        W4_CUDA(cudaStreamSynchronize(st));
+        cudaGraphExecDestroy(ex);
+        cudaGraphDestroy(g);
+        const int jl = hs[0];  // last iteration executed
+        const int done_ok = hs[1] ? jl - 1 : jl;
+        op.applies += jl - j0 + 1;
+        std::vector<double> ha(left + 1), hb(left + 1), hr(left + 2);
+        if (done_ok >= j0) {
+            W4_CUDA(cudaMemcpyAsync(ha.data(), d_al + j0 - 1, sizeof(double) * (done_ok - j0 + 1),
+                                    cudaMemcpyDeviceToHost, st));
+            W4_CUDA(cudaMemcpyAsync(hb.data(), d_be + j0 - 1, sizeof(double) * (done_ok - j0 + 1),
+                                    cudaMemcpyDeviceToHost, st));
+            W4_CUDA(cudaMemcpyAsync(hr.data(), d_rs + j0, sizeof(double) * (done_ok - j0 + 1),
+                                    cudaMemcpyDeviceToHost, st));
+        }
+        W4_CUDA(cudaStreamSynchronize(st));
+        for (int jj = j0; jj <= done_ok; ++jj) {
+            rec.alphas.push_back(ha[jj - j0]);
+            rec.betas.push_back(hb[jj - j0]);
+            rec.residual_norms.push_back(hr[jj - j0]);
+            rec.iterations = jj;
+        }
+        if (hs[1]) {  // reproduce the host loop's checks and messages for iteration jl
+            const unsigned s = (unsigned)hs[2];
+            if (s & ST_FWD_NONFINITE) throw NumericalError("hessian apply: non-finite value after forward sweep");
+            if (s & ST_ADJ_NONFINITE) throw NumericalError("hessian apply: non-finite value after adjoint sweep");
+            if (s & ST_OUT_NONFINITE) throw NumericalError("hessian apply: non-finite result");
+            read_scal();
+            const double curv = pinned[SC_CURV];
+            check_finite(curv, "curvature", jl);
+            if (curv <= 0.0) {
+                std::ostringstream m;
+                m << "pcg_split: p^T A p = " << curv << " at iteration " << jl
+                  << "; operator lost positive definiteness";
+                throw NumericalError(m.str());
+            }
+            check_finite(pinned[SC_ALPHA], "alpha", jl);
+            check_finite(pinned[SC_BETA], "beta", jl);
+        }
+        if (hs[3]) {
+            rec.converged = true;
+            rec.stop_reason = 1;
+        }
+        return true;
+    };
     for (int j = 1; j <= opts.max_iter; ++j) {
+        if (dev_loop && j == 2 && run_dev_loop(j)) break;
         op.applies += 1;  // the single operator apply of this iteration (krylov.cpp:56)
         // iteration 1 runs eagerly (it grows the workspaces; no allocation under capture)
         const bool graph_it = use_graph && j > 1;
