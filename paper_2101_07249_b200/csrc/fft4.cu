@@ -402,6 +402,8 @@ struct Job {
     const double2* thi;  // w_N^{(p >> 10) 1024}
     unsigned* ctr;       // [0] ticket, [1 + 3 g + phase] completed items of group g
     int l2hint;          // evict_last policy on Y + discard after pass C (WC4DVAR_FFT_L2HINT)
+    int phase_mask;      // profiling aid (WC4DVAR_FFT_PHASES, default 7): passes whose items run
+    int sub;             // tiles per ticket (WC4DVAR_FFT_SUB)
 };
 
 __device__ __forceinline__ double2 wN(const Job& jb, int64_t p) {  // w_N^p, 0 <= p < N
@@ -577,7 +579,11 @@ template <class P>
 __global__ void __launch_bounds__(kThreads, kCtaPerSm) fftconv_kernel(const Job jb) {
     extern __shared__ double2 sm[];
     __shared__ unsigned s_ticket;
-    constexpr int nA1 = P::N1 / P::TC, nB1 = P::N2 / P::S;  // items per pair
+    // a ticket covers `sub` consecutive tiles (A / C) or row blocks (B) of one pair: fewer
+    // tickets, so the per-ticket cost (ticket atomic, dependency read, two barriers, the
+    // completion release) is paid once per `sub` tiles
+    constexpr int tA = P::N1 / P::TC, tB = P::N2 / P::S;  // tiles / row blocks per pair
+    const int nA1 = (tA + jb.sub - 1) / jb.sub, nB1 = (tB + jb.sub - 1) / jb.sub;  // tickets per pair
     const int nA = jb.G * nA1, nB = jb.G * nB1, nC = nA;
     const unsigned stepN = (unsigned)(nA + nB + nC);
     const unsigned total = stepN * (unsigned)(jb.ngroups + 2);
@@ -651,13 +657,17 @@ __global__ void __launch_bounds__(kThreads, kCtaPerSm) fftconv_kernel(const Job 
             // pair index and the item inside it; groups are G consecutive pairs
             const int per_pair = phase == 1 ? nB1 : nA1;
             const int p = g * jb.G + r / per_pair, idx = r % per_pair;
-            if (p < jb.np) {  // the last group may be partial
-                if (phase == 0) {
-                    item_a<P>(jb, sm, p, idx);
-                } else if (phase == 1) {
-                    item_b<P>(jb, sm, p, idx);
-                } else {
-                    item_c<P>(jb, sm, p, idx);
+            if (p < jb.np && ((jb.phase_mask >> phase) & 1)) {  // the last group may be partial
+                const int u0 = idx * jb.sub, u1 = min(u0 + jb.sub, phase == 1 ? tB : tA);
+                for (int u = u0; u < u1; ++u) {
+                    if (u > u0) __syncthreads();  // the previous tile's last stage read SMEM
+                    if (phase == 0) {
+                        item_a<P>(jb, sm, p, u);
+                    } else if (phase == 1) {
+                        item_b<P>(jb, sm, p, u);
+                    } else {
+                        item_c<P>(jb, sm, p, u);
+                    }
                 }
             }
         }
@@ -698,7 +708,8 @@ void launch(const Job& jb, cudaStream_t st) {
     W4_CUDA(cudaGetDevice(&dev));
     W4_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
     W4_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fftconv_kernel<P>, kThreads, sm));
-    const int64_t items = (int64_t)(jb.ngroups + 2) * jb.G * (2 * (P::N1 / P::TC) + P::N2 / P::S);
+    const int64_t items = (int64_t)(jb.ngroups + 2) * jb.G *
+                          (2 * ((P::N1 / P::TC + jb.sub - 1) / jb.sub) + (P::N2 / P::S + jb.sub - 1) / jb.sub);
     const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(items, (int64_t)nsm * std::max(occ, 1)));
     fftconv_kernel<P><<<grid, kThreads, sm, st>>>(jb);
     W4_LAUNCH();
@@ -833,8 +844,16 @@ void Fft4::apply(bool inv, int Nsw, const double* V, int64_t ldv, int64_t m, dou
         const char* e = std::getenv("WC4DVAR_FFT_L2HINT");
         return e ? std::atoi(e) : 1;
     }();
+    static const int phase_mask = [] {
+        const char* e = std::getenv("WC4DVAR_FFT_PHASES");
+        return e ? std::atoi(e) : 7;
+    }();
+    static const int sub = [] {
+        const char* e = std::getenv("WC4DVAR_FFT_SUB");
+        return e ? std::max(1, std::atoi(e)) : 1;
+    }();
     Job jb{V, ldv, out, ldo, add, ldadd, add ? status : nullptr, dpairs, np, per, G, ngroups,
-           lamB, lamQ, Y, tw1_, tw2_, tlo_, thi_, ctr, l2hint};
+           lamB, lamQ, Y, tw1_, tw2_, tlo_, thi_, ctr, l2hint, phase_mask, sub};
     kPlans[plan_].run(jb, st);
 }
 
