@@ -150,6 +150,11 @@ int wc4dvar_gpu_hessian_piece_dev(wc4dvar_op* op, int which, const double* V, in
 /* Stage profiling of HessianOperator block applies (CUDA events around the
  * D^{1/2} GEMM, the fused sweep and the final D^{1/2} GEMM + identity term).
  * enable != 0 resets the accumulators; read returns ms[3] summed over calls. */
+/* observe (models.cpp:184-192) with the operator's network: y (q, network order) =
+ * H traj for a window trajectory traj (n(N+1), i.e. n x (N+1) col-major).  Host / device. */
+int wc4dvar_gpu_observe(wc4dvar_op* op, const double* traj, double* y);
+int wc4dvar_gpu_observe_dev(wc4dvar_op* op, const double* traj, double* y, void* stream);
+
 /* HessianOperator::observation_range (operators.cpp:146-154): W (dim x q, ldw) =
  * D^{1/2} L^{-T} H^T [e_1 .. e_q], computed as one block adjoint sweep of the q
  * unit observations.  Host / device (_dev, on `stream`) outputs. */

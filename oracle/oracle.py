@@ -1049,3 +1049,85 @@ class QuadraticCost:
 
     def gradient(self, x):
         return self.op.apply(x) - self.rhs()
+
+
+# ---------------------------------------------------------------------------
+# Outer loop and twin data (proj/src/assimilation.cpp:11-128, 255-263), SURVEY §8(f)-4.
+# Test infrastructure: the checker for paper_2101_07249_b200/assimilation.py.
+# ---------------------------------------------------------------------------
+@dataclass
+class AssimSystem:
+    """assimilation.hpp:19-37 (plain fields; factors are oracle CovarianceFactors)."""
+
+    kind: str          # "advection" | "lorenz96"
+    n: int
+    N: int
+    dt: float
+    dx: float
+    net: ObservationNetwork
+    bh: CovarianceFactor
+    qh: CovarianceFactor
+    sigma_obs: float
+    courant: float = 0.0
+    forcing: float = 8.0
+    spinup_steps: int = 500
+
+    def model_step(self, x):
+        """assimilation.cpp:11-19"""
+        if self.kind == "advection":
+            return advection_step(x, self.courant)
+        return lorenz96_step(x, self.forcing, self.dt)
+
+    def integrate_p(self, p) -> np.ndarray:
+        """assimilation.cpp:21-33"""
+        n = self.n
+        traj = np.empty((n, self.N + 1))
+        traj[:, 0] = p[:n]
+        for i in range(self.N):
+            traj[:, i + 1] = self.model_step(traj[:, i]) + p[(i + 1) * n:(i + 2) * n]
+            if not np.all(np.isfinite(traj[:, i + 1])):
+                raise NumericalError(f"integrate_p: non-finite trajectory at step {i + 1}")
+        return traj
+
+    def hessian(self, traj, threads: int = 8) -> "HessianOperator":
+        """assimilation.cpp:35-50"""
+        model = (AdvectionLinearized(self.n, self.N, self.courant) if self.kind == "advection"
+                 else Lorenz96Linearized(traj, self.forcing, self.dt))
+        return HessianOperator(model, self.net, self.bh, self.qh, self.sigma_obs, threads=threads)
+
+
+def generate_twin(sys: AssimSystem, seeds=(1, 2, 3), noise_scale: float = 1.0, truth_model_error: bool = False):
+    """assimilation.cpp:75-110 (seeds = background, observations, model_error).
+    Returns (truth, background, y)."""
+    n = sys.n
+    if sys.kind == "advection":
+        x0 = np.array([6.0 * math.exp(-0.5 * ((j * sys.dx - 0.5) / 0.1) ** 2) for j in range(n)])
+    else:
+        x0 = np.full(n, sys.forcing)
+        x0[0] += 0.01
+        for _ in range(sys.spinup_steps):
+            x0 = lorenz96_step(x0, sys.forcing, sys.dt)
+    truth = np.empty((n, sys.N + 1))
+    truth[:, 0] = x0
+    mn = NormalStream(seeds[2])
+    for i in range(sys.N):
+        nxt = sys.model_step(truth[:, i])
+        if truth_model_error and noise_scale > 0.0:
+            nxt = nxt + noise_scale * sys.qh.apply(mn.draw(n))
+        if not np.all(np.isfinite(nxt)):
+            raise NumericalError("generate_twin: truth integration became non-finite")
+        truth[:, i + 1] = nxt
+    bg = truth[:, 0].copy()
+    if noise_scale > 0.0:
+        bg = bg + noise_scale * sys.bh.apply(NormalStream(seeds[0]).draw(n))
+    y = observe(truth.reshape(-1, order="F"), sys.net)
+    if noise_scale > 0.0:
+        y = y + noise_scale * sys.sigma_obs * NormalStream(seeds[1]).draw(len(y))
+    return truth, bg, y
+
+
+def compute_innovations(sys: AssimSystem, p, traj, background, y):
+    """assimilation.cpp:120-128 -> (b, d)."""
+    b = -np.asarray(p, dtype=np.float64)
+    b[:sys.n] = background - traj[:, 0]
+    return b, y - observe(traj.reshape(-1, order="F"), sys.net)

@@ -164,6 +164,8 @@ int wc4dvar_gpu_hessian_create(const wc4dvar_model_desc* model, const wc4dvar_ne
     for (int b = 0; b < net->n_points; ++b) pmap[net->points[b]] = b;
     h->d_slot = dev_upload(slot.data(), slot.size(), st);
     h->d_pmap = dev_upload(pmap.data(), pmap.size(), st);
+    h->d_times = dev_upload(h->times.data(), h->times.size(), st);
+    h->d_points = dev_upload(h->points.data(), h->points.size(), st);
     h->nd.n_times = net->n_times;
     h->nd.n_points = net->n_points;
     h->nd.q = (int64_t)net->n_times * net->n_points;
@@ -335,6 +337,35 @@ int wc4dvar_gpu_hessian_piece_dev(wc4dvar_op* op, int which, const double* V, in
     op->reset_status(st);
     h->piece_dev(which, src, lds, m, out, ldo, st);
     W4_CUDA(cudaStreamSynchronize(st));
+    W4_API_END
+}
+
+int wc4dvar_gpu_observe_dev(wc4dvar_op* op, const double* traj, double* y, void* stream) {
+    W4_API_BEGIN
+    HessianOp* h = dynamic_cast<HessianOp*>(op);
+    require(h != nullptr, "observe: operator is not a HessianOperator");
+    require(traj && (y || h->nd.q == 0), "observe: null argument");
+    std::lock_guard<std::recursive_mutex> lk(op->mu);
+    DeviceGuard g(op->device);
+    h->observe_dev(traj, y, pick(op, stream));
+    W4_API_END
+}
+
+int wc4dvar_gpu_observe(wc4dvar_op* op, const double* traj, double* y) {
+    W4_API_BEGIN
+    HessianOp* h = dynamic_cast<HessianOp*>(op);
+    require(h != nullptr, "observe: operator is not a HessianOperator");
+    require(traj && (y || h->nd.q == 0), "observe: null argument");
+    std::lock_guard<std::recursive_mutex> lk(op->mu);
+    DeviceGuard g(op->device);
+    const int64_t q = h->nd.q;
+    if (q == 0) return WC4DVAR_OK;
+    double* dt = op->in_buf.get<double>((size_t)op->dim);
+    double* dy = op->out_buf.get<double>((size_t)q);
+    W4_CUDA(cudaMemcpyAsync(dt, traj, sizeof(double) * op->dim, cudaMemcpyHostToDevice, op->stream));
+    h->observe_dev(dt, dy, op->stream);
+    W4_CUDA(cudaMemcpyAsync(y, dy, sizeof(double) * q, cudaMemcpyDeviceToHost, op->stream));
+    W4_CUDA(cudaStreamSynchronize(op->stream));
     W4_API_END
 }
 

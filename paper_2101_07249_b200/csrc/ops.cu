@@ -89,6 +89,8 @@ HessianOp::~HessianOp() {
         if (p) cudaFree(p);
     if (d_slot) cudaFree(d_slot);
     if (d_pmap) cudaFree(d_pmap);
+    if (d_times) cudaFree(d_times);
+    if (d_points) cudaFree(d_points);
     delete circ;
 }
 
@@ -168,6 +170,26 @@ __global__ void identity_kernel(int64_t q, double* Y) {
         Y[e] = (e % (q + 1) == 0) ? 1.0 : 0.0;
 }
 }  // namespace
+
+namespace {
+// y[a np + b] = traj[times[a] n + points[b]]  (network order, models.cpp:184-192)
+__global__ void observe_kernel(int64_t n, int np, int64_t q, const int* __restrict__ times,
+                               const int* __restrict__ points, const double* __restrict__ traj,
+                               double* __restrict__ y) {
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < q; e += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t a = e / np, b = e - a * np;
+        y[e] = traj[(int64_t)times[a] * n + points[b]];
+    }
+}
+}  // namespace
+
+void HessianOp::observe_dev(const double* traj, double* y, cudaStream_t st) {
+    const int64_t q = nd.q;
+    if (q == 0) return;
+    observe_kernel<<<(unsigned)std::min<int64_t>(cdiv(q, 256), 4096), 256, 0, st>>>(n, nd.n_points, q, d_times,
+                                                                                      d_points, traj, y);
+    W4_LAUNCH();
+}
 
 void HessianOp::observation_range_dev(double* W, int64_t ldw, cudaStream_t st) {
     const int64_t q = nd.q;

@@ -70,6 +70,8 @@ struct HessianOp final : wc4dvar_op {
     bool sym[4] = {false, false, false, false};  // b_half, q_half, b_half_inv, q_half_inv == ^T
     int* d_slot = nullptr;
     int* d_pmap = nullptr;
+    int* d_times = nullptr;   // network times / points (device copies, observe)
+    int* d_points = nullptr;
     double* d_stages = nullptr;
     std::vector<int> times, points;
     DevBuf t_ws, y_ws, sweep_ws;
@@ -86,6 +88,8 @@ struct HessianOp final : wc4dvar_op {
     // HessianOperator::observation_range (operators.cpp:146-154): W (n_A x q, ldw) =
     // D^{1/2} L^{-T} H^T [e_1 .. e_q], one block adjoint sweep of the q unit observations.
     void observation_range_dev(double* W, int64_t ldw, cudaStream_t st);
+    // observe (models.cpp:184-192): y = H traj (window trajectory, network order)
+    void observe_dev(const double* traj, double* y, cudaStream_t st);
     // out = D^{1/2} V (+ add) for an n_A x m block; inverse factors when inv.
     void d_half(bool inv, const double* V, int64_t ldv, int64_t m, double* out, int64_t ldo,
                 const double* add, int64_t ldadd, unsigned* status, cudaStream_t st);

@@ -107,6 +107,8 @@ SIGNATURES = {
     "wc4dvar_gpu_op_apply_block_dev": (ctypes.c_int, [_vp, _vp, _i64, _i64, _vp, _i64, _vp]),
     "wc4dvar_gpu_hessian_piece": (ctypes.c_int, [_vp, ctypes.c_int, _dp, _i64, _i64, _dp, _i64]),
     "wc4dvar_gpu_hessian_piece_dev": (ctypes.c_int, [_vp, ctypes.c_int, _vp, _i64, _i64, _vp, _i64, _vp]),
+    "wc4dvar_gpu_observe": (ctypes.c_int, [_vp, _dp, _dp]),
+    "wc4dvar_gpu_observe_dev": (ctypes.c_int, [_vp, _vp, _vp, _vp]),
     "wc4dvar_gpu_observation_range": (ctypes.c_int, [_vp, _dp, _i64]),
     "wc4dvar_gpu_observation_range_dev": (ctypes.c_int, [_vp, _vp, _i64, _vp]),
     "wc4dvar_gpu_clustered_spectrum": (ctypes.c_int, [_vp, _vp, _dp, _i64, _dp, ctypes.POINTER(_i64),
@@ -505,6 +507,15 @@ class HessianOperator(LinearOperator):
         out = np.empty_like(v)
         _check(lib.wc4dvar_gpu_hessian_piece(self._h, which, _p(v), v.shape[0], m, _p(out), v.shape[0]))
         return out
+
+    def observe(self, traj) -> np.ndarray:
+        """observe (models.cpp:184-192) with this operator's network, on the device."""
+        traj = np.ascontiguousarray(np.asarray(traj, dtype=np.float64).reshape(-1, order="F"))
+        require(len(traj) == self.dim(), "observe: trajectory length mismatch")
+        y = np.empty(self.net.q)
+        if self.net.q:
+            _check(lib.wc4dvar_gpu_observe(self.handle, _p(traj), _p(y)))
+        return y
 
     def observation_range(self) -> np.ndarray:
         """operators.cpp:146-154: D^{1/2} L^{-T} H^T [e_1..e_q] (dim x q), one block
