@@ -171,6 +171,13 @@ int wc4dvar_gpu_hessian_create(const wc4dvar_model_desc* model, const wc4dvar_ne
     h->nd.q = (int64_t)net->n_times * net->n_points;
     h->nd.slot = h->d_slot;
     h->nd.pmap = h->d_pmap;
+    {  // regular spatial network (models.cpp:159-176): points = 0, sx, 2 sx, ... < n
+        const int np = net->n_points;
+        int sx = np >= 2 ? net->points[1] - net->points[0] : (np == 1 ? (int)n : 0);
+        bool reg = np >= 1 && net->points[0] == 0 && sx >= 1 && (int64_t)np == (n + sx - 1) / sx;
+        for (int b = 0; reg && b < np; ++b) reg = net->points[b] == b * sx;
+        h->nd.sx = reg ? sx : 0;
+    }
     if (bh->kind == WC4DVAR_COV_CIRCULANT) {
         h->circ = new CirculantPlan();
         h->circ->init(n, bh->half, qh->half, bh->half_inv, qh->half_inv, st);

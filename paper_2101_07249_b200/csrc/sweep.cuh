@@ -33,6 +33,8 @@ struct NetDev {
     int64_t q = 0;
     const int* slot = nullptr;  // N+1: observation slot of time t, or -1
     const int* pmap = nullptr;  // n: index of grid point j in points[], or -1
+    int sx = 0;  // > 0: points are exactly {0, sx, 2 sx, ...} (ObservationNetwork::build), so
+                 // pmap[g] = g % sx ? -1 : g / sx without a table lookup
 };
 
 struct SweepArgs {

@@ -410,11 +410,24 @@ template <int S, int P>
 __device__ __forceinline__ void blk_conv(const double* __restrict__ cur, int b, int R, int ns,
                                          const StencilTaps& tp, double (&v)[P + 2 * S]) {
     constexpr int L = P + 2 * S;
+    if (b >= S && b + P + S <= R) {
+        // interior thread: j = b + d, d = u - S compile-time, so the slot
+        // (j % P) ns + j / P = b / P + (d mod P) ns + floor(d / P) is one base register plus
+        // one of P row offsets plus an immediate
+        const double* base = cur + b / P;
 #pragma unroll
-    for (int u = 0; u < L; ++u) {
-        int j = b - S + u;
-        j = j < 0 ? 0 : (j >= R ? R - 1 : j);
-        v[u] = cur[(j % P) * ns + j / P];
+        for (int u = 0; u < L; ++u) {
+            const int d = u - S;
+            const int dm = ((d % P) + P) % P, dq = (d - dm) / P;
+            v[u] = base[dm * ns + dq];
+        }
+    } else {
+#pragma unroll
+        for (int u = 0; u < L; ++u) {
+            int j = b - S + u;
+            j = j < 0 ? 0 : (j >= R ? R - 1 : j);
+            v[u] = cur[(j % P) * ns + j / P];
+        }
     }
     double o[P];
 #pragma unroll
@@ -470,8 +483,20 @@ __global__ void __launch_bounds__(512) tiled_blk_fwd_kernel(const TiledArgs ta, 
     bool bad = false;
     double v[P + 2 * S];
     auto slot = [&](int e) { return (e % P) * ns + e / P; };
+    // element e = tid + k nt: when nt % P == 0 its slot advances by nt / P and its grid
+    // index by nt (one periodic wrap at most), so the loops run on increments
+    const bool inc = nt % P == 0;
     auto load_row = [&](double* dst, const double* row) {
-        for (int e = tid; e < R; e += nt) cp8(dst + slot(e), row + rg.gidx(e));
+        if (inc) {
+            int s = slot(tid), g = rg.gidx(tid);
+            for (int e = tid; e < R; e += nt, s += nt / P) {
+                cp8(dst + s, row + g);
+                g += nt;
+                if (g >= n) g -= n;
+            }
+        } else {
+            for (int e = tid; e < R; e += nt) cp8(dst + slot(e), row + rg.gidx(e));
+        }
         asm volatile("cp.async.commit_group;\n");
     };
 
@@ -483,18 +508,32 @@ __global__ void __launch_bounds__(512) tiled_blk_fwd_kernel(const TiledArgs ta, 
         cp_async_wait_all();
         __syncthreads();
         // emit x_i on the tile centre (x_{i0} only at the window start: otherwise the
-        // previous launch emitted it)
+        // previous launch emitted it).  Non-finite values cannot vanish along a linear sweep
+        // (NaN / Inf propagate through every tap), so the finite check runs on the launch's
+        // last state only; with a regular network only the observed points are visited.
         if (i > ta.i0 || ta.i0 == 0) {
             const int sl = net.slot[i];
             double* tri = tr ? tr + (int64_t)i * n : nullptr;
-            for (int e = c_lo + tid; e < c_hi; e += nt) {
-                const int g = rg.gidx(e);
-                const double x = cur[slot(e)];
-                bad |= !isfinite(x);
-                if (tri) tri[g] = x;
-                if (a.fwd_obs && sl >= 0) {
-                    const int bb = net.pmap[g];
-                    if (bb >= 0) Yc[(int64_t)sl * np + bb] = a.scale_fwd * x;
+            const bool last = i == ta.i1;
+            if (tri || last || (a.fwd_obs && sl >= 0 && !net.sx)) {
+                for (int e = c_lo + tid; e < c_hi; e += nt) {
+                    const int g = rg.gidx(e);
+                    const double x = cur[slot(e)];
+                    if (last) bad |= !isfinite(x);
+                    if (tri) tri[g] = x;
+                    if (a.fwd_obs && sl >= 0 && !net.sx) {
+                        const int bb = net.pmap[g];
+                        if (bb >= 0) Yc[(int64_t)sl * np + bb] = a.scale_fwd * x;
+                    }
+                }
+            }
+            if (a.fwd_obs && sl >= 0 && net.sx) {
+                // observed points g = bb sx inside the tile centre [t0, t0 + (c_hi - c_lo))
+                const int sx = net.sx;
+                const int g0 = (int)t0, g1 = (int)(t0 + (c_hi - c_lo));
+                for (int bb = (g0 + sx - 1) / sx + tid; bb * sx < g1; bb += nt) {
+                    const int e = bb * sx - g0 + c_lo;
+                    Yc[(int64_t)sl * np + bb] = a.scale_fwd * cur[slot(e)];
                 }
             }
         }
@@ -550,8 +589,20 @@ __global__ void __launch_bounds__(512) tiled_blk_adj_kernel(const TiledArgs ta, 
     bool bad = false;
     double v[P + 2 * S];
     auto slot = [&](int e) { return (e % P) * ns + e / P; };
+    // element e = tid + k nt: when nt % P == 0 its slot advances by nt / P and its grid
+    // index by nt (one periodic wrap at most), so the loops run on increments
+    const bool inc = nt % P == 0;
     auto load_row = [&](double* dst, const double* row) {
-        for (int e = tid; e < R; e += nt) cp8(dst + slot(e), row + rg.gidx(e));
+        if (inc) {
+            int s = slot(tid), g = rg.gidx(tid);
+            for (int e = tid; e < R; e += nt, s += nt / P) {
+                cp8(dst + s, row + g);
+                g += nt;
+                if (g >= n) g -= n;
+            }
+        } else {
+            for (int e = tid; e < R; e += nt) cp8(dst + slot(e), row + rg.gidx(e));
+        }
         asm volatile("cp.async.commit_group;\n");
     };
     // H_i^T y part of the addend (sparse: observed points of observed times)
@@ -559,7 +610,13 @@ __global__ void __launch_bounds__(512) tiled_blk_adj_kernel(const TiledArgs ta, 
         if (a.adj_obs) {
             const int sl = net.slot[i];
             if (sl >= 0) {
-                const int bb = net.pmap[g];
+                int bb;
+                if (net.sx) {
+                    const int q = g / net.sx;
+                    bb = (q * net.sx == g) ? q : -1;
+                } else {
+                    bb = net.pmap[g];
+                }
                 if (bb >= 0) x = V ? x + Yc[(int64_t)sl * np + bb] : Yc[(int64_t)sl * np + bb];
             }
         }
@@ -579,11 +636,22 @@ __global__ void __launch_bounds__(512) tiled_blk_adj_kernel(const TiledArgs ta, 
     for (int i = ta.i1;; --i) {  // cur = s_i
         cp_async_wait_all();
         __syncthreads();
-        if (i < ta.i1 || !ta.bin) {  // emit s_i on the tile centre
-            for (int e = c_lo + tid; e < c_hi; e += nt) {
-                const double x = cur[slot(e)];
-                Sv[(int64_t)i * n + rg.gidx(e)] = x;
-                bad |= !isfinite(x);
+        if (i < ta.i1 || !ta.bin) {  // emit s_i on the tile centre (finite check: last state)
+            const bool last = i == ta.i0;
+            double* Si = Sv + (int64_t)i * n;
+            if (inc) {  // the tile centre does not wrap: g = t0 + (e - c_lo)
+                int s = slot(c_lo + tid);
+                for (int e = c_lo + tid; e < c_hi; e += nt, s += nt / P) {
+                    const double x = cur[s];
+                    Si[t0 + (e - c_lo)] = x;
+                    if (last) bad |= !isfinite(x);
+                }
+            } else {
+                for (int e = c_lo + tid; e < c_hi; e += nt) {
+                    const double x = cur[slot(e)];
+                    Si[rg.gidx(e)] = x;
+                    if (last) bad |= !isfinite(x);
+                }
             }
         }
         if (i == ta.i0) break;
@@ -592,14 +660,43 @@ __global__ void __launch_bounds__(512) tiled_blk_adj_kernel(const TiledArgs ta, 
         lo += S;
         hi -= S;
         if (b + P > lo && b < hi) {
+            // H^T y of the thread's P points first: all y loads in flight before the stencil
+            // (the loads' latency then hides under the FMA chains)
+            const int sl = a.adj_obs ? net.slot[i - 1] : -1;
+            double yv[P];
+            bool has[P];
+            if (sl >= 0) {
+                const double* ys = Yc + (int64_t)sl * np;
+                if (net.sx) {  // regular network: observed iff g % sx == 0, bb = g / sx
+                    int g = rg.gidx(b), q = g / net.sx, r = g - q * net.sx;
+#pragma unroll
+                    for (int p = 0; p < P; ++p) {
+                        has[p] = r == 0;
+                        yv[p] = has[p] ? ys[q] : 0.0;
+                        if (++g == n) g = q = r = 0;  // periodic wrap
+                        else if (++r == net.sx) r = 0, ++q;
+                    }
+                } else {
+#pragma unroll
+                    for (int p = 0; p < P; ++p) {
+                        const int bb = net.pmap[rg.gidx(b + p)];
+                        has[p] = bb >= 0;
+                        yv[p] = has[p] ? ys[bb] : 0.0;
+                    }
+                }
+            } else {
+#pragma unroll
+                for (int p = 0; p < P; ++p) has[p] = false, yv[p] = 0.0;
+            }
             blk_conv<S, P>(cur, b, R, ns, ta.tp, v);  // M_i^T as one stencil
             const double* vr = (k & 1) ? vb1 : vb0;
 #pragma unroll
             for (int p = 0; p < P; ++p) {
                 const int e = b + p;
                 if (e >= lo && e < hi) {
-                    // s_{i-1} = v_{i-1} + H^T y + M^T s_i  (operators.cpp:99)
-                    const double ad = obs_add(i - 1, rg.gidx(e), V ? vr[p * ns + tid] : 0.0);
+                    // s_{i-1} = v_{i-1} + H^T y + M^T s_i  (operators.cpp:99; obs_add order)
+                    double ad = V ? vr[p * ns + tid] : 0.0;
+                    if (has[p]) ad = V ? ad + yv[p] : yv[p];
                     nxt[p * ns + tid] = ad + v[S + p];
                 }
             }
@@ -619,10 +716,20 @@ template <int KIND, int S>
 bool launch_tiled_blk(const ModelDev& md, const NetDev& net, const SweepArgs& a, unsigned* status,
                       cudaStream_t st, DevBuf& ws, int tile_override) {
     constexpr int P = 8;
-    int nt = 512;
+    // WC4DVAR_TILED_NT: threads per CTA (512 default: one CTA per SM); WC4DVAR_TILED_KDIV:
+    // halo budget R / KDIV for the intervals per launch (4 default)
+    static const int nt_env = [] {
+        const char* e = std::getenv("WC4DVAR_TILED_NT");
+        return e ? std::atoi(e) : 512;
+    }();
+    static const int kdiv = [] {
+        const char* e = std::getenv("WC4DVAR_TILED_KDIV");
+        return e ? std::max(1, std::atoi(e)) : 4;
+    }();
+    int nt = nt_env;
     int K = md.N;
     int R = nt * P;
-    while (K > 1 && 2 * K * S > R / 4) --K;
+    while (K > 1 && 2 * K * S > R / kdiv) --K;
     int T = R - 2 * K * S;
     if (tile_override > 0) {
         T = tile_override;
