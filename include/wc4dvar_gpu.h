@@ -380,6 +380,28 @@ int wc4dvar_gpu_ritz_from_tridiagonal(int64_t n, int64_t j, const double* gammas
                                       const double* residual_basis, int64_t ldf, int64_t k, double* U,
                                       int64_t ldu, double* values, int device);
 
+/* ------------------------------------------------------------------------- */
+/* Multi-GPU plumbing for a C++ host                    */
+/* ------------------------------------------------------------------------- */
+/* NCCL communicator (NCCL resolved at run time: libnccl.so.2).  Rank 0 makes the
+ * 128-byte id and the caller broadcasts it out of band, as with ncclGetUniqueId. */
+typedef struct wc4dvar_comm wc4dvar_comm;
+int wc4dvar_gpu_comm_unique_id(unsigned char* id128);
+int wc4dvar_gpu_comm_create(const unsigned char* id128, int rank, int size, int device, wc4dvar_comm** out);
+int wc4dvar_gpu_comm_destroy(wc4dvar_comm* comm);
+/* In-place sum of the m x m Gram-type partials (Y^T Y, Z^T A Z, Z^T E1, U^T v, ...). */
+int wc4dvar_gpu_comm_allreduce_sum(wc4dvar_comm* comm, double* buf, int64_t count, void* stream);
+int wc4dvar_gpu_comm_allgather(wc4dvar_comm* comm, const double* send, int64_t count, double* recv,
+                               void* stream);
+/* The column <-> row transposes of the row-sharded sketches: an nrows x ncols block,
+ * balanced partitions (part r = [total r / G, total (r+1) / G)); rank r holds columns
+ * part_r(ncols) (cols: nrows x m_r, ld nrows) or rows part_r(nrows) (rows: R_r x ncols,
+ * ld R_r).  Grouped NCCL send / recv on `stream`. */
+int wc4dvar_gpu_comm_cols_to_rows(wc4dvar_comm* comm, const double* cols, int64_t nrows, int64_t ncols,
+                                  double* rows, void* stream);
+int wc4dvar_gpu_comm_rows_to_cols(wc4dvar_comm* comm, const double* rows, int64_t nrows, int64_t ncols,
+                                  double* cols, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

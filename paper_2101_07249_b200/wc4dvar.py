@@ -155,6 +155,14 @@ SIGNATURES = {
     "wc4dvar_gpu_cost_rhs": (ctypes.c_int, [_vp, _dp]),
     "wc4dvar_gpu_pcg": (ctypes.c_int, [_vp, _dp, _vp, _dp, ctypes.POINTER(PcgOpts), _vp, _dp,
                                        ctypes.POINTER(PcgHist)]),
+    "wc4dvar_gpu_comm_unique_id": (ctypes.c_int, [ctypes.c_char_p]),
+    "wc4dvar_gpu_comm_create": (ctypes.c_int, [ctypes.c_char_p, ctypes.c_int, ctypes.c_int, ctypes.c_int,
+                                               ctypes.POINTER(_vp)]),
+    "wc4dvar_gpu_comm_destroy": (ctypes.c_int, [_vp]),
+    "wc4dvar_gpu_comm_allreduce_sum": (ctypes.c_int, [_vp, _vp, _i64, _vp]),
+    "wc4dvar_gpu_comm_allgather": (ctypes.c_int, [_vp, _vp, _i64, _vp, _vp]),
+    "wc4dvar_gpu_comm_cols_to_rows": (ctypes.c_int, [_vp, _vp, _i64, _i64, _vp, _vp]),
+    "wc4dvar_gpu_comm_rows_to_cols": (ctypes.c_int, [_vp, _vp, _i64, _i64, _vp, _vp]),
     "wc4dvar_gpu_lanczos_eigenpairs": (ctypes.c_int, [_vp, _i64, ctypes.POINTER(LanczosOpts), _dp, _i64, _dp,
                                                       ctypes.POINTER(_i64)]),
     "wc4dvar_gpu_ritz_from_tridiagonal": (ctypes.c_int, [_i64, _i64, _dp, _dp, _dp, _i64, _i64, _dp, _i64, _dp,
