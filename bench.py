@@ -332,20 +332,22 @@ def run_extras(W, configs, wl, op, Om, dev):
 
 
 def run_large(W, configs, peak_tfs, hbm_gbs):
-    """BASELINE configs[2] (C3, Lorenz-96 n=1e5) and configs[3] (C4, adv-diff n=1e6,
-    circulant factors) block applies at m = 64 on one GPU: device-drawn N(0,1) Omega (torch,
+    """BASELINE configs[2] (C3, Lorenz-96 n=1e5), configs[3] (C4, adv-diff n=1e6, circulant
+    factors) block applies at m = 64 and configs[4] (C5, Lorenz-96 n=2e6, Nsw=20) at one
+    rank's 32-column share of its 8-GPU sketch, on one GPU: device-drawn N(0,1) Omega (torch,
     throughput only; parity at these shapes is property-based in tests/), CUDA-event timing,
     per-stage split, and the SURVEY §8(d) roofline t_roof = max(B/BW, F/P) per block with
     B = 8 (3 n_A + 2 q) m and F = (F_model + F_cov) m."""
     import torch
     out = {}
-    for name, mk in (("C3", lambda: configs.config3()), ("C4", lambda: configs.config4(64))):
+    for name, mk in (("C3", lambda: configs.config3()), ("C4", lambda: configs.config4(64)),
+                     ("C5", lambda: configs.config5(32))):
         try:
             wl = mk()
             t0 = time.perf_counter()
             op = wl.hessian(0)
             setup_s = time.perf_counter() - t0
-            m, nA, q = 64, op.dim(), wl.net.q
+            m, nA, q = wl.m, op.dim(), wl.net.q  # C5: one rank's 32-column share of the 8-GPU sketch
             n, N, s = wl.model.n, wl.model.N, wl.model.substeps
             g = torch.Generator(device="cuda").manual_seed(1)
             V = torch.randn(m, nA, dtype=torch.float64, device="cuda", generator=g)
