@@ -295,7 +295,13 @@ __global__ void __launch_bounds__(kThreads) tiled_adj_kernel(const TiledArgs ta,
         if (a.adj_obs) {
             const int sl = net.slot[i];
             if (sl >= 0) {
-                const int bb = net.pmap[g];
+                int bb;
+                if (net.sx) {
+                    const int q = g / net.sx;
+                    bb = q * net.sx == g ? q : -1;
+                } else {
+                    bb = net.pmap[g];
+                }
                 if (bb >= 0) x = V ? x + Yc[(int64_t)sl * np + bb] : Yc[(int64_t)sl * np + bb];
             }
         }
@@ -966,6 +972,14 @@ __global__ void __launch_bounds__(CB * NTC, 65536 / (CB * NTC * 128)) l96_blk_fw
     }
     int pb = 0;
     for (int i = ta.i0; i < ta.i1; ++i) {
+        // forcing X_{i+1} of this interval's end, loaded now so its latency hides under the
+        // s RK4 steps
+        double xf[P];
+        if (live) {
+            const double* Xn = X + (int64_t)(i + 1) * n;
+#pragma unroll
+            for (int p = 0; p < P; ++p) xf[p] = Xn[rg.gidx(b + p)];
+        }
         for (int k = 0; k < s; ++k) {
             // RK4 TL step (models.cpp:120-128)
             l96_publish<P, Lay::NTC>(ex + (pb * CB + cg) * LD + G, b, cur);
@@ -1012,19 +1026,24 @@ __global__ void __launch_bounds__(CB * NTC, 65536 / (CB * NTC * 128)) l96_blk_fw
         }
         // x_{i+1} = M_i x_i + X_{i+1}  (operators.cpp:88)
         if (live) {
-            const double* Xn = X + (int64_t)(i + 1) * n;
             const int sl = net.slot[i + 1];
             double* trn = tr ? tr + (int64_t)(i + 1) * n : nullptr;
 #pragma unroll
             for (int p = 0; p < P; ++p) {
                 const int e = b + p;
                 const int g = rg.gidx(e);
-                cur[p] = cur[p] + Xn[g];
+                cur[p] = cur[p] + xf[p];
                 if (e >= c_lo && e < c_hi) {
                     bad |= !isfinite(cur[p]);
                     if (trn) trn[g] = cur[p];
                     if (a.fwd_obs && sl >= 0) {
-                        const int bb = net.pmap[g];
+                        int bb;
+                        if (net.sx) {
+                            const int q = g / net.sx;
+                            bb = q * net.sx == g ? q : -1;
+                        } else {
+                            bb = net.pmap[g];
+                        }
                         if (bb >= 0) Yc[(int64_t)sl * np + bb] = a.scale_fwd * cur[p];
                     }
                 }
@@ -1111,6 +1130,12 @@ __global__ void __launch_bounds__(CB * NTC, 65536 / (CB * NTC * 128)) l96_blk_ad
     }
     int pb = 0;
     for (int i = ta.i1 - 1; i >= ta.i0; --i) {
+        // v_i + H_i^T y of this interval's end, loaded now (latency hidden by the s steps)
+        double adv[P];
+        if (live) {
+#pragma unroll
+            for (int p = 0; p < P; ++p) adv[p] = addend(i, rg.gidx(b + p));
+        }
         for (int kk = 0; kk < s; ++kk) {
             // RK4 adjoint step (models.cpp:130-148)
             l96_publish<P, Lay::NTC>(ex + (pb * CB + cg) * LD + G, b, cur);
@@ -1161,7 +1186,7 @@ __global__ void __launch_bounds__(CB * NTC, 65536 / (CB * NTC * 128)) l96_blk_ad
             for (int p = 0; p < P; ++p) {
                 const int e = b + p;
                 const int g = rg.gidx(e);
-                cur[p] = addend(i, g) + cur[p];
+                cur[p] = adv[p] + cur[p];
                 if (e >= c_lo && e < c_hi) {
                     Sv[(int64_t)i * n + g] = cur[p];
                     bad |= !isfinite(cur[p]);
