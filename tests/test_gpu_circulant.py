@@ -117,3 +117,22 @@ print(json.dumps([relerr(g.apply_block(V), o.apply_block(V)),
     import json
     e_apply, e_inv = json.loads(p.stdout.strip().splitlines()[-1])
     assert e_apply <= 1e-12 and e_inv <= 1e-10, (e_apply, e_inv)
+
+
+def test_pcg_with_fused_fft_operator_vs_oracle():
+    """Split PCG (iterations 2.. as one conditional-graph launch) on an operator whose
+    D^{1/2} is the fused four-step FFT (n = 1e4): same step sizes and iterate as the oracle,
+    with and without a Nystrom LMP."""
+    n, N = 10000, 2
+    bh, qh = circ_factors(n, 5.0)
+    g, o = pair(W.AdvDiffLinearized(n, N, 0.5, 0.2, 3), W.ObservationNetwork.build(n, N, 4, 1), bh, qh, 0.1)
+    b = O.NormalStream(2).draw(g.dim())
+    pg = W.sketch_eigenpairs(g, W.SketchConfig(8, 4, 1, "nystrom"))
+    po = O.sketch_eigenpairs(o, O.SketchConfig(8, 4, 1, "nystrom"))
+    for fg, fo in ((None, None), (W.build_spectral_lmp(pg), O.build_spectral_lmp(po))):
+        # a fixed 20 iterations (the oracle's direct O(n^2) convolution bounds the budget)
+        rg = W.pcg_split(g, b, fg, opts=W.PcgOptions(max_iter=20, rel_tol=0.0))
+        ro = O.pcg_split(o, b, fo, opts=O.PcgOptions(max_iter=20, rel_tol=0.0))
+        assert rg.history.iterations == ro.history.iterations == 20
+        assert np.allclose(rg.history.alphas, ro.history.alphas, rtol=1e-9, atol=0.0)
+        assert relerr(rg.x, ro.x) <= 1e-9
