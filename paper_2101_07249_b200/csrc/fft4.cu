@@ -296,12 +296,10 @@ template <class V, bool INV, int NS, class List>
 struct Mids;
 template <class V, bool INV, int NS>
 struct Mids<V, INV, NS, RL<>> {
-    static constexpr int NS_OUT = NS;
     __device__ static __forceinline__ void run(double2*, const double2*) {}
 };
 template <class V, bool INV, int NS, int R, int... Rest>
 struct Mids<V, INV, NS, RL<R, Rest...>> {
-    static constexpr int NS_OUT = Mids<V, INV, NS * R, RL<Rest...>>::NS_OUT;
     __device__ static __forceinline__ void run(double2* sm, const double2* tw) {
         stage_mid<V, R, NS, INV>(sm, tw);
         Mids<V, INV, NS * R, RL<Rest...>>::run(sm, tw);
