@@ -53,3 +53,14 @@ def test_no_cpu_fallback_without_gpu():
     import paper_2101_07249_b200 as w
     with pytest.raises(w.DeviceError):
         w.DenseOperator(np.eye(4))
+
+
+def test_cpp_host_header_compiles():
+    """include/wc4dvar_gpu.hpp (the C++ mirror of the reference API) and its test program
+    compile and link against the library without a GPU."""
+    out = "/tmp/_w4_test_cpp_api"
+    cmd = ["g++", "-std=c++17", "-O1", "-Wall", "-Werror", "-I", os.path.join(ROOT, "include"),
+           os.path.join(ROOT, "tests", "cpp", "test_cpp_api.cpp"), "-L", os.path.join(ROOT, "paper_2101_07249_b200"),
+           "-lwc4dvar_gpu", "-L", os.path.join(ROOT, "oracle"), "-loracle", "-o", out]
+    r = subprocess.run(cmd, capture_output=True, text=True)
+    assert r.returncode == 0, r.stderr[-3000:]
