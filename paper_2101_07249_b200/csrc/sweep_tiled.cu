@@ -798,7 +798,10 @@ struct L96Lay {
     static constexpr int NTC = NTC_;              // threads per column
     static constexpr int NT = CB * NTC;           // threads per CTA
     static constexpr int R = NTC * kL96P;         // region points
-    static constexpr int LD = kL96P * (NTC + 2);  // row size in doubles
+    // row size in doubles, padded so consecutive exchange rows start 8 / CB bank groups
+    // apart -- with column-fast lanes (lane = j CB + column) a quarter warp's 8 STS / LDS.128
+    // then hit 8 distinct 16-byte bank groups
+    static constexpr int LD = kL96P * (NTC + 2) + 2 * (8 / (CB < 8 ? CB : 8));
     // 4 stage ring buffers + 2 x CB exchange rows
     static constexpr size_t smem_bytes = sizeof(double) * (4 * LD + 2 * CB * LD);
 };
@@ -923,7 +926,9 @@ __global__ void __launch_bounds__(CB * NTC, 65536 / (CB * NTC * 128)) l96_blk_fw
     const TileGeom& geo = ta.geo;
     const int n = (int)md.n;
     const int tid = threadIdx.x, nt = blockDim.x;
-    const int cg = tid / Lay::NTC, b = (tid % Lay::NTC) * P;
+    // column-fast lanes: the CB threads that own the same points of different columns are
+    // adjacent, so their stage-slice loads (same addresses) are served as SMEM broadcasts
+    const int cg = tid % CB, b = (tid / CB) * P;
     const int64_t col = (int64_t)blockIdx.x * CB + cg;
     const bool live = col < a.m;
     const int64_t t0 = (int64_t)blockIdx.y * geo.T;
@@ -1073,7 +1078,9 @@ __global__ void __launch_bounds__(CB * NTC, 65536 / (CB * NTC * 128)) l96_blk_ad
     const TileGeom& geo = ta.geo;
     const int n = (int)md.n;
     const int tid = threadIdx.x, nt = blockDim.x;
-    const int cg = tid / Lay::NTC, b = (tid % Lay::NTC) * P;
+    // column-fast lanes: the CB threads that own the same points of different columns are
+    // adjacent, so their stage-slice loads (same addresses) are served as SMEM broadcasts
+    const int cg = tid % CB, b = (tid / CB) * P;
     const int64_t col = (int64_t)blockIdx.x * CB + cg;
     const bool live = col < a.m;
     const int64_t t0 = (int64_t)blockIdx.y * geo.T;
