@@ -828,8 +828,10 @@ template <int P, int NTC>
 __device__ __forceinline__ void l96_publish(double* exr, int b, const double (&v)[P]) {
     double2* r2 = reinterpret_cast<double2*>(exr);
     const int j = b / P;
-#pragma unroll
-    for (int k = 0; k < P / 2; ++k) r2[l96_slot<NTC>(k, j)] = make_double2(v[2 * k], v[2 * k + 1]);
+    // neighbours read only the first and the last point pair of a thread (the TL / adjoint
+    // halos are 2 + 1 points), so only those two pairs are published
+    r2[l96_slot<NTC>(0, j)] = make_double2(v[0], v[1]);
+    r2[l96_slot<NTC>(P / 2 - 1, j)] = make_double2(v[P - 2], v[P - 1]);
 }
 
 template <int P, int NTC>
