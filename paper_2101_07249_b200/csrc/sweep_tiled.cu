@@ -1269,6 +1269,10 @@ bool try_l96_blk(const ModelDev& md, const NetDev& net, const SweepArgs& a, unsi
         return e ? std::atoi(e) : 4;
     }();
     if (mode == 0 || (mode < 0 && !tiled_regime)) return false;
+    // a single column (PCG, Lanczos) on the 4-column shape would leave 3 / 4 of every CTA
+    // idle: one column per CTA, 256 threads
+    if (a.m == 1 && !std::getenv("WC4DVAR_L96_CB") && launch_l96_blk<1, 256>(md, net, a, status, st, ws))
+        return true;
     switch (cb) {
         case 1: return launch_l96_blk<2, 256>(md, net, a, status, st, ws);
         case 2: return launch_l96_blk<4, 128>(md, net, a, status, st, ws);
