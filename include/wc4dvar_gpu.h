@@ -185,6 +185,23 @@ int wc4dvar_gpu_probe_dmma_peak(int device, double* tflops);
  * column-major fill.  Host output. */
 int wc4dvar_gpu_gaussian_matrix(int64_t rows, int64_t cols, uint64_t seed, double* out);
 
+/* Device NormalStream with MT19937-64 jump-ahead (random.hpp:14-42; randevd.cpp:16-21;
+ * SURVEY §7 hard part 3).  out (rows x cols, ldo; device memory on `device`) = rows
+ * [row0, row0 + rows) x columns [col0, col0 + cols) of gaussian_matrix(n_total, *, seed),
+ * i.e. entry (i, j) is normal number n_total j + i of NormalStream(seed): column shards
+ * (multi-GPU A*Omega) and row shards (row-sharded ritzit) of the reference's single serial
+ * stream.  Raw engine outputs are bit-exact with libstdc++ std::mt19937_64; the normals
+ * use the device log / cos / sqrt (within a few ulp of glibc's).  Enqueued on `stream`. */
+int wc4dvar_gpu_gaussian_block_dev(int64_t n_total, int64_t row0, int64_t rows, int64_t col0,
+                                   int64_t cols, uint64_t seed, double* out, int64_t ldo,
+                                   int device, void* stream);
+/* Test hook: `count` raw std::mt19937_64(seed) outputs starting at draw `offset` (both even),
+ * generated on the device from a jump-ahead state (device pointer `out`). */
+int wc4dvar_gpu_mt19937_raw_dev(uint64_t seed, uint64_t offset, int64_t count, uint64_t* out,
+                                int device, void* stream);
+/* Host twin of the jump-ahead (same polynomial arithmetic), for the CPU test suite. */
+int wc4dvar_gpu_mt19937_raw_host(uint64_t seed, uint64_t offset, int64_t count, uint64_t* out);
+
 /* ------------------------------------------------------------------------- */
 /* Lorenz-96 nonlinear model on the device                   */
 /* ------------------------------------------------------------------------- */

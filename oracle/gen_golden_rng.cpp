@@ -60,8 +60,54 @@ int main() {
             sum += last;
             sum2 += last * last;
         }
-        std::printf("  \"seed7_1e6\": {\"sum\": %.17g, \"sum2\": %.17g, \"last\": %.17g}\n", sum,
+        std::printf("  \"seed7_1e6\": {\"sum\": %.17g, \"sum2\": %.17g, \"last\": %.17g},\n", sum,
                     sum2, last);
+    }
+    // Jump-ahead pins (SURVEY §7 hard part 3): raw outputs at large offsets (discard), and the
+    // first normals of far columns / a row block of a gaussian_matrix.
+    {
+        const unsigned long long offs1[] = {2, 310, 312, 314, 624, 19936, 19938, 1000002ULL,
+                                            34000000ULL, 123456788ULL, 8670000000ULL};
+        std::printf("  \"raw_at\": {\"1\": {");
+        const size_t no = sizeof(offs1) / sizeof(offs1[0]);
+        for (size_t k = 0; k < no; ++k) {
+            std::mt19937_64 gen(1);
+            gen.discard(offs1[k]);
+            std::printf("\"%llu\": [", offs1[k]);
+            for (int i = 0; i < 8; ++i)
+                std::printf("\"%llu\"%s", (unsigned long long)gen(), i + 1 < 8 ? ", " : "");
+            std::printf("]%s", k + 1 < no ? ", " : "");
+        }
+        std::printf("}, \"5\": {");
+        {
+            std::mt19937_64 gen(5);
+            gen.discard(100000000ULL);
+            std::printf("\"100000000\": [");
+            for (int i = 0; i < 8; ++i)
+                std::printf("\"%llu\"%s", (unsigned long long)gen(), i + 1 < 8 ? ", " : "");
+            std::printf("]");
+        }
+        std::printf("}},\n");
+    }
+    {
+        // columns 1, 2, 255 of gaussian_matrix(17000000, 256, 1) (the C4 sketch): first 4 normals
+        const unsigned long long rows = 17000000ULL;
+        const int cols[] = {1, 2, 255};
+        std::printf("  \"gaussian_cols_rows17e6_seed1\": {");
+        for (int c = 0; c < 3; ++c) {
+            std::mt19937_64 gen(1);
+            gen.discard(2ULL * rows * (unsigned long long)cols[c]);
+            std::printf("\"%d\": [", cols[c]);
+            for (int i = 0; i < 4; ++i) std::printf("%.17g%s", next_normal(gen), i + 1 < 4 ? ", " : "");
+            std::printf("]%s", c + 1 < 3 ? ", " : "");
+        }
+        std::printf("},\n");
+        // rows 500000..500003 of column 3 of gaussian_matrix(1000003, *, 1)
+        std::mt19937_64 gen(1);
+        gen.discard(2ULL * (1000003ULL * 3ULL + 500000ULL));
+        std::printf("  \"gaussian_rows_n1000003_col3_row500000_seed1\": [");
+        for (int i = 0; i < 4; ++i) std::printf("%.17g%s", next_normal(gen), i + 1 < 4 ? ", " : "");
+        std::printf("]\n");
     }
     std::printf("}\n");
     return 0;

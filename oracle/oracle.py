@@ -530,6 +530,8 @@ _lib.orc_hessian_apply.argtypes = [_HP, _dp, _dp]
 _lib.orc_hessian_apply.restype = ctypes.c_int
 _lib.orc_hessian_apply_block.argtypes = [_HP, _i64, _dp, _dp, ctypes.c_int]
 _lib.orc_hessian_apply_block.restype = ctypes.c_int
+_lib.orc_hessian_sweeps_block.argtypes = [_HP, _i64, _dp, ctypes.c_int]
+_lib.orc_hessian_sweeps_block.restype = ctypes.c_int
 _MODEL_CODES = {"identity": 0, "advection": 1, "advdiff": 2, "l96": 3}
 _STAGE_MSG = {
     1: "hessian apply: non-finite value after forward sweep",
@@ -559,6 +561,7 @@ class HessianOperator(LinearOperator):
         self.sigma_obs_ = sigma_obs
         self.threads = threads
         self._keep = []
+        self._fft = {}
 
         def keep(a, dtype=np.float64):
             a = np.ascontiguousarray(a, dtype=dtype)
@@ -628,6 +631,62 @@ class HessianOperator(LinearOperator):
                                               threads or self.threads)
             if st:
                 raise NumericalError(_STAGE_MSG[st])
+        return out
+
+    def apply_D_half_block(self, V, inv: bool = False, threads: Optional[int] = None) -> np.ndarray:
+        """apply_D_half / _inv (operators.cpp:103-125) on a whole block.  The window block
+        V (dim x m) is viewed as the n x (N+1)m matrix of its n-blocks; the dense factor is
+        then ONE GEMM over that view (what operators.cpp:107-111 does per column, as
+        Q^{1/2} [v_1 .. v_N]), multithreaded BLAS.  The circulant EXTENSION is one batched
+        real FFT convolution (scipy.fft, `threads` workers): C^{1/2} = F^{-1} diag(lambda) F
+        with lambda = DFT of the factor's first column (real: the column is symmetric)."""
+        import scipy.fft
+        V = np.asfortranarray(V, dtype=np.float64)
+        n, N = self.model.n, self.model.N
+        m = V.shape[1]
+        X = V.reshape((n, (N + 1) * m), order="F")
+        b = self.b_half.half_inv if inv else self.b_half.half
+        qf = self.q_half.half_inv if inv else self.q_half.half
+        first = np.arange(m) * (N + 1)
+        if self.b_half.kind == "dense":
+            out = np.asfortranarray(qf @ X) if N > 0 else np.empty_like(X, order="F")
+            out[:, first] = b @ X[:, first]
+        else:
+            key = ("lam", inv)
+            if key not in self._fft:
+                self._fft[key] = (np.real(scipy.fft.rfft(b)), np.real(scipy.fft.rfft(qf)))
+            lb, lq = self._fft[key]
+            w = threads or self.threads or 1
+            # X^T is the C-contiguous ((N+1)m, n) matrix of the n-blocks: row i + (N+1) j is
+            # block i of column j
+            F = scipy.fft.rfft(X.T, axis=1, workers=w)
+            F3 = F.reshape((m, N + 1, F.shape[1]))
+            F3[:, 0, :] *= lb
+            F3[:, 1:, :] *= lq
+            out = scipy.fft.irfft(F, n=n, axis=1, workers=w).T
+        return out.reshape((n * (N + 1), m), order="F")
+
+    def apply_block_fast(self, V, threads: Optional[int] = None) -> np.ndarray:
+        """HessianOperator::apply (operators.cpp:127-144) on a block, batched for the CPU
+        baseline: D^{1/2} of the whole block (apply_D_half_block), then the per-column
+        sweeps L^{-T} H^T R^{-1} H L^{-1} in C with the apply_block column fan-out
+        (threads.cpp:25-44), then out = V + D^{1/2} S.  Same arithmetic as apply_block up
+        to the summation order of the factor products."""
+        V = np.asfortranarray(V, dtype=np.float64)
+        require(V.shape[0] == self.dim(), "LinearOperator::apply_block: dimension mismatch")
+        m = V.shape[1]
+        self._applies += m
+        if m == 0:
+            return np.empty_like(V, order="F")
+        w = threads or self.threads or 1
+        T = np.asfortranarray(self.apply_D_half_block(V, False, w))
+        st = _lib.orc_hessian_sweeps_block(ctypes.byref(self._h), m, _ptr(T), w)
+        if st:
+            raise NumericalError(_STAGE_MSG[st])
+        out = self.apply_D_half_block(T, False, w)
+        out += V
+        if not np.isfinite(out).all():
+            raise NumericalError(_STAGE_MSG[3])
         return out
 
     def observation_range(self) -> np.ndarray:

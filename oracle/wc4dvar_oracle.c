@@ -429,6 +429,30 @@ done:
     return status;
 }
 
+/* The middle of HessianOperator::apply (operators.cpp:129-140) for one column:
+ * s = L^{-T} H^T R^{-1} H L^{-1} t, in place on t.  Used by the batched CPU baseline
+ * (oracle.py HessianOperator.apply_block_fast), which applies D^{1/2} to the whole block
+ * at once (one GEMM, operators.cpp:107-111, or the circulant FFT EXTENSION) and runs
+ * these sweeps with the same column fan-out as apply_block.  status as orc_hessian_apply. */
+int orc_hessian_sweeps(const orc_hessian* h, double* t) {
+    const int64_t dim = h->n * (h->N + 1);
+    const int64_t q = (int64_t)h->n_times * h->n_points;
+    const double r_inv = 1.0 / (h->sigma_obs * h->sigma_obs);
+    double* traj = (double*)malloc(sizeof(double) * (dim + q + 1));
+    double* y = traj + dim;
+    int status = 0;
+    orc_apply_Linv(h, t, traj);
+    if (!all_finite(traj, dim)) { status = 1; goto done; }
+    orc_observe(h, traj, y);
+    for (int64_t k = 0; k < q; ++k) y[k] *= r_inv;
+    orc_observe_adjoint(h, y, traj); /* reuse traj as the scattered vector */
+    orc_apply_LinvT(h, traj, t);
+    if (!all_finite(t, dim)) status = 2;
+done:
+    free(traj);
+    return status;
+}
+
 /* LinearOperator::apply_block, operators.cpp:9-19, with the parallel_for
  * work-stealing fan-out of proj/src/threads.cpp:25-44 (atomic next index,
  * disjoint output columns, bitwise independent of the worker count). */
@@ -438,6 +462,7 @@ typedef struct {
     double* out;
     int64_t m;
     int64_t next;
+    int sweeps_only; /* 1: out[:, j] = sweeps(out[:, j]) in place (orc_hessian_sweeps) */
     pthread_mutex_t lock;
     int status;
 } block_ctx;
@@ -450,7 +475,8 @@ static void* block_worker(void* arg) {
         const int64_t j = c->next++;
         pthread_mutex_unlock(&c->lock);
         if (j >= c->m) return NULL;
-        const int st = orc_hessian_apply(c->h, c->V + j * dim, c->out + j * dim);
+        const int st = c->sweeps_only ? orc_hessian_sweeps(c->h, c->out + j * dim)
+                                      : orc_hessian_apply(c->h, c->V + j * dim, c->out + j * dim);
         if (st) {
             pthread_mutex_lock(&c->lock);
             if (!c->status) c->status = st;
@@ -459,8 +485,8 @@ static void* block_worker(void* arg) {
     }
 }
 
-int orc_hessian_apply_block(const orc_hessian* h, int64_t m, const double* V, double* out,
-                            int threads) {
+static int run_block(const orc_hessian* h, int64_t m, const double* V, double* out, int threads,
+                     int sweeps_only) {
     block_ctx c;
     c.h = h;
     c.V = V;
@@ -468,6 +494,7 @@ int orc_hessian_apply_block(const orc_hessian* h, int64_t m, const double* V, do
     c.m = m;
     c.next = 0;
     c.status = 0;
+    c.sweeps_only = sweeps_only;
     pthread_mutex_init(&c.lock, NULL);
     int workers = threads < 1 ? 1 : threads;
     if (workers > m) workers = (int)m;
@@ -481,6 +508,16 @@ int orc_hessian_apply_block(const orc_hessian* h, int64_t m, const double* V, do
     }
     pthread_mutex_destroy(&c.lock);
     return c.status;
+}
+
+int orc_hessian_apply_block(const orc_hessian* h, int64_t m, const double* V, double* out,
+                            int threads) {
+    return run_block(h, m, V, out, threads, 0);
+}
+
+/* orc_hessian_sweeps on every column of T (dim x m, in place), column fan-out. */
+int orc_hessian_sweeps_block(const orc_hessian* h, int64_t m, double* T, int threads) {
+    return run_block(h, m, NULL, T, threads, 1);
 }
 
 /* ------------------------------------------------------------------------- */

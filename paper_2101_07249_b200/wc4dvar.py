@@ -125,6 +125,10 @@ SIGNATURES = {
                                                    ctypes.c_double, _dp, _dp, _i64, ctypes.c_int]),
     "wc4dvar_gpu_sketch": (ctypes.c_int, [_vp, ctypes.POINTER(SketchDesc), _dp, _dp, _i64, _dp,
                                           ctypes.POINTER(_i64)]),
+    "wc4dvar_gpu_gaussian_block_dev": (ctypes.c_int, [_i64, _i64, _i64, _i64, _i64, ctypes.c_uint64, _vp, _i64,
+                                                      ctypes.c_int, _vp]),
+    "wc4dvar_gpu_mt19937_raw_dev": (ctypes.c_int, [ctypes.c_uint64, ctypes.c_uint64, _i64, _vp, ctypes.c_int, _vp]),
+    "wc4dvar_gpu_mt19937_raw_host": (ctypes.c_int, [ctypes.c_uint64, ctypes.c_uint64, _i64, _vp]),
     "wc4dvar_gpu_sketch_dev": (ctypes.c_int, [_vp, ctypes.POINTER(SketchDesc), _vp, _vp, _i64, _vp,
                                               ctypes.POINTER(_i64), _vp]),
     "wc4dvar_gpu_rayleigh_ritz": (ctypes.c_int, [_vp, _dp, _i64, _i64, _dp, _i64, _dp]),
@@ -224,6 +228,34 @@ def gaussian_matrix(rows: int, cols: int, seed: int) -> np.ndarray:
 # ---------------------------------------------------------------------------
 # Descriptors (models.hpp, covariance.hpp, operators.hpp)
 # ---------------------------------------------------------------------------
+def gaussian_block_dev(out, n_total: int, seed: int, row0: int = 0, col0: int = 0, stream=None) -> None:
+    """Device NormalStream with jump-ahead (wc4dvar_gpu_gaussian_block_dev): fills the torch
+    CUDA tensor ``out`` (shape (cols, rows), row j = column col0 + j of the column-major
+    sketch) with rows [row0, row0 + rows) of columns [col0, col0 + cols) of
+    gaussian_matrix(n_total, *, seed) (randevd.cpp:16-21)."""
+    cols, rows = out.shape
+    require(out.stride(1) == 1, "gaussian_block_dev: rows must be contiguous")
+    _check(lib.wc4dvar_gpu_gaussian_block_dev(n_total, row0, rows, col0, cols, seed, out.data_ptr(),
+                                              out.stride(0) if cols > 1 else rows, out.device.index,
+                                              None if stream is None else stream))
+
+
+def mt19937_raw_host(seed: int, offset: int, count: int) -> np.ndarray:
+    """Raw std::mt19937_64(seed) outputs from draw `offset` via the library's host jump-ahead."""
+    out = np.empty(count, dtype=np.uint64)
+    _check(lib.wc4dvar_gpu_mt19937_raw_host(seed, offset, count, out.ctypes.data_as(_vp)))
+    return out
+
+
+def mt19937_raw_dev(seed: int, offset: int, count: int, device: int = 0) -> np.ndarray:
+    """Raw outputs generated on the device from a jump-ahead state (test hook)."""
+    import torch
+    t = torch.empty(count, dtype=torch.int64, device=f"cuda:{device}")
+    _check(lib.wc4dvar_gpu_mt19937_raw_dev(seed, offset, count, t.data_ptr(), device, None))
+    torch.cuda.synchronize(device)
+    return t.cpu().numpy().view(np.uint64)
+
+
 @dataclass
 class ObservationNetwork:
     """models.hpp:45-56; build rule of models.cpp:159-176."""
