@@ -1,14 +1,25 @@
 #!/usr/bin/env python
-"""Benchmark of the randomized-LMP hot path on BASELINE.json configs[1] (C2).
+"""Benchmark of the randomized-LMP hot path on the largest single-GPU BASELINE config.
 
 Metric (BASELINE.json): "Hessian-block apply columns/s and LMP build ms; fraction of HBM
-roofline".  One step = one block product A*Omega of the first-level-preconditioned
-inner-loop Hessian (operators.cpp:127-144) with an n_A x m Gaussian sketch, m = 100,
-n_A = 2000 * 21 = 42 000 (advection-diffusion, 10 TL sub-steps per subwindow, dense SOAR
-B^{1/2}, Q^{1/2}).  Multi-GPU: the sketch columns shard by rank with no data-path
-collective (weak scaling, each rank applies its own 100-column block).
+roofline".  Headline workload: configs[3] (C4) -- advection-diffusion n = 1e6, Nsw = 16,
+10 TL sub-steps per subwindow (n_A = 1.7e7), circulant SOAR L = 50 B^{1/2} / Q^{1/2}, every
+10th point observed -- with the widest sketch k = 256 columns.  One step = one block
+product A*Omega (operators.cpp:127-144) of the 256-column sketch drawn from the
+reference's NormalStream(1) (device jump-ahead generator, random.hpp:14-42).
+Multi-GPU: the 256 columns of the ONE global sketch shard across ranks (strong scaling,
+no data-path collective); `value` is whole-job columns/s, timed on the device as the max
+over ranks.
 
-  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+Secondary keys (N = 1 only): per-config applies (C2, C3, C5 rank share), LMP build ms
+(REVD / Nystrom / ritzit at C2, C3 and C4 k = 256), LMP-PCG time-to-solution (C2, C3, C4),
+and the CPU baseline (oracle port, all host cores, bounded column sample).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--no-extras]
+
+`--gpus N` without torchrun re-launches itself under torch.distributed.run with N ranks.
+`--impl reference` times the CPU oracle port of the same path (the reference itself is
+not buildable here: Eigen is absent) WITHOUT importing the product package.
 """
 from __future__ import annotations
 
@@ -16,6 +27,7 @@ import argparse
 import json
 import math
 import os
+import socket
 import statistics
 import subprocess
 import sys
@@ -25,8 +37,12 @@ import time
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
-METRIC = "Hessian-block apply columns/s (A*Omega, C2); LMP build ms"
+METRIC = "Hessian-block apply columns/s (A*Omega, C4 n_A=1.7e7, k=256); LMP build ms"
 UNIT = "columns/s"
+M_GLOBAL = 256           # C4 sketch width (the widest of BASELINE configs[3]'s k in {16, 64, 256})
+OMEGA_SEED = 1           # the reference's sketch_base = 1 (proj/configs/advection.cfg:39)
+RHS_SEED = 2
+CPU_SAMPLE_COLS = 16     # CPU legs: columns of the same sketch per step
 
 
 def parse():
@@ -35,13 +51,23 @@ def parse():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
-    ap.add_argument("--no-extras", action="store_true", help="skip LMP-build / PCG timings")
+    ap.add_argument("--no-extras", action="store_true", help="headline only (no secondary configs / LMP / PCG)")
     return ap.parse_args()
 
 
 def env_rank():
     return (int(os.environ.get("RANK", "0")), int(os.environ.get("WORLD_SIZE", "1")),
             int(os.environ.get("LOCAL_RANK", "0")))
+
+
+def spawn_ranks(n: int) -> int:
+    """`bench.py --gpus N` outside torchrun: re-launch under torch.distributed.run."""
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr=127.0.0.1", f"--master-port={port}", os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd)
 
 
 class ClockSampler:
@@ -99,106 +125,108 @@ class ClockSampler:
                 "reasons": sorted(reasons), "samples": len(sm)}
 
 
-def build_workload():
-    from paper_2101_07249_b200 import configs
-    return configs.config2()
-
-
-def algorithmic_counts(wl, m):
-    n, N, q = wl.model.n, wl.model.N, wl.net.q
+def c4_counts(n=1_000_000, N=16, s=10, q=1_600_000, m=M_GLOBAL):
+    """SURVEY §8(d) per-column algorithmic counts for C4, times m columns."""
     nA = n * (N + 1)
-    s = wl.model.substeps
-    flops_gemm = 2.0 * n * n * (N + 1) * m             # one D^{1/2} application (B and Q blocks)
-    flops_model = 10.0 * N * s * n * m                  # adv-diff TL + adjoint stencils
-    bytes_step = 8.0 * (3 * nA * m + 2 * q * m + 4 * n * n)  # v twice, Av once, y w+r, factors
-    return nA, flops_gemm, flops_model, bytes_step
+    fft_launch = (N + 1) * m * (5.0 * n * math.log2(n) + n)      # one D^{1/2} (real-FFT convention)
+    flops = (10.0 * N * s * n + 2.0 * (N + 1) * (5.0 * n * math.log2(n) + n)) * m
+    bytes_ = 8.0 * (3 * nA + 2 * q) * m
+    return nA, fft_launch, flops, bytes_
 
 
-def gemm_traffic():
-    """DRAM bytes per launch of the D^1/2 GEMM from the committed `ncu --set full` capture
-    (dram__bytes_read.sum + dram__bytes_write.sum, averaged over the captured launches)."""
-    path = os.path.join(ROOT, "profiles", "r01_gemm_sym_stream_k.json")
+def profile_traffic(name: str, kernel: str):
+    """DRAM bytes per launch of `kernel` from a committed `ncu --set full` summary."""
+    path = os.path.join(ROOT, "profiles", name)
     try:
-        ks = [k for k in json.load(open(path))["kernels"] if "gemm_sym_ws" in k["kernel"]]
+        ks = [k for k in json.load(open(path))["kernels"] if kernel in k["kernel"]]
         return sum(k["traffic_bytes"] for k in ks) / len(ks), os.path.relpath(path, ROOT)
     except (OSError, KeyError, ValueError, ZeroDivisionError):
         return None, None
 
 
-def cpu_reference(wl, columns, threads, seed_cols_offset=0):
-    """Time the oracle port of HessianOperator::apply_block (the reference's column
-    fan-out over std::thread, threads.cpp:25-44) on `columns` sketch columns."""
+# ------------------------------------------------------------------------------ reference
+def oracle_c4(threads: int, cols: int):
+    """The C4 operator and the first `cols` columns of the same NormalStream(1) sketch, from
+    the CPU oracle alone (oracle/workloads.py: never imports the product package)."""
     from oracle import oracle as O
-    o = O.HessianOperator(
-        O.LinearizedModel(wl.model.kind, wl.model.n, wl.model.N, wl.model.substeps, wl.model.courant,
-                          wl.model.diffusion),
-        O.ObservationNetwork(wl.net.n, wl.net.N, wl.net.space_stride, wl.net.time_stride,
-                             list(wl.net.times), list(wl.net.points), wl.net.q),
-        O.CovarianceFactor(wl.b_half.half, wl.b_half.half_inv),
-        O.CovarianceFactor(wl.q_half.half, wl.q_half.half_inv), wl.sigma_obs, threads=threads)
-    V = O.gaussian_matrix(o.dim(), columns, 1)
-    t0 = time.perf_counter()
-    o.apply_block(V)
-    return time.perf_counter() - t0
+    from oracle import workloads as OW
+    wl = OW.config4(M_GLOBAL, threads=threads)
+    V = O.gaussian_matrix(wl.dim, cols, OMEGA_SEED)
+    return wl, V
 
 
 def run_reference(args):
     rank, world, _ = env_rank()
     if rank != 0:
         return 0
-    wl = build_workload()
     threads = os.cpu_count() or 1
-    m = wl.m
-    cols = min(m, max(8, 2 * threads))
+    cols = CPU_SAMPLE_COLS
+    wl, V = oracle_c4(threads, cols)
     for _ in range(args.warmup):
-        cpu_reference(wl, cols, threads)
-    secs = [cpu_reference(wl, cols, threads) for _ in range(args.steps)]
+        wl.op.apply_block_fast(V, threads)
+    secs = []
+    for _ in range(args.steps):
+        t0 = time.perf_counter()
+        wl.op.apply_block_fast(V, threads)
+        secs.append(time.perf_counter() - t0)
     total = sum(secs)
     value = cols * args.steps / total
+    sample = (f"{cols} of the {M_GLOBAL} sketch columns per step (columns 0..{cols - 1} of NormalStream(1)); "
+              f"oracle port of HessianOperator::apply_block (reference not buildable: Eigen absent): "
+              f"circulant D^1/2 as a batched real FFT (scipy.fft, {threads} workers), TL/adjoint sweeps in C "
+              f"with the reference's column fan-out over {threads} threads")
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * total / args.steps,
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-        "data": "synthetic (seeded N(0,1) sketch, BASELINE configs[1] operator)",
-        "config": {"workload": wl.name, "n": wl.model.n, "Nsw": wl.model.N, "substeps": wl.model.substeps,
-                   "n_A": wl.dim, "sketch_columns": m, "q": wl.net.q},
-        "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port",
-                         "sample": f"{cols} of {m} sketch columns per step, oracle/wc4dvar_oracle.c "
-                                   f"(reference not buildable: Eigen absent), pthread column fan-out"},
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (NormalStream(1) sketch, BASELINE configs[3] operator)",
+        "config": {"workload": wl.name, "n": wl.n, "Nsw": wl.N, "substeps": wl.substeps, "n_A": wl.dim,
+                   "sketch_columns": M_GLOBAL, "q": wl.q, "covariance": wl.covariance},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port", "sample": sample},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
-    print(json.dumps(line))
+    print(json.dumps(line), flush=True)
     return 0
 
 
+# ------------------------------------------------------------------------------ ours
 def run_ours(args):
     import numpy as np
     import torch
 
     rank, world, local = env_rank()
+    if args.gpus != world:
+        raise SystemExit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}")
+    if M_GLOBAL % world:
+        raise SystemExit(f"bench.py: {M_GLOBAL} sketch columns do not split over {world} ranks")
     torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
     dist = None
     if world > 1:
         import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        dist.init_process_group("nccl", device_id=dev)
 
     import paper_2101_07249_b200 as W
     from paper_2101_07249_b200 import configs
 
-    wl = build_workload()
-    m = wl.m
+    m = M_GLOBAL // world
+    wl = configs.config4(M_GLOBAL)
     op = wl.hessian(local)
     nA = op.dim()
-    # this rank's columns [rank*m, (rank+1)*m) of the global sketch stream (column-major fill)
-    Om = W.gaussian_matrix(nA, (rank + 1) * m, configs.OMEGA_SEED)[:, rank * m:]
-    dev = torch.device("cuda", local)
-    V = torch.from_numpy(np.ascontiguousarray(Om.T)).to(dev)  # (m, nA) row-major == column-major Omega
-    out = torch.empty_like(V)
-    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)  # 256 MiB > 126 MB L2
     stream = torch.cuda.current_stream(dev)
     sp = stream.cuda_stream
+    # this rank's columns [rank m, (rank + 1) m) of gaussian_matrix(n_A, 256, 1)
+    V = torch.empty((m, nA), dtype=torch.float64, device=dev)
+    W.gaussian_block_dev(V, nA, OMEGA_SEED, col0=rank * m, stream=sp)
+    out = torch.empty_like(V)
+    fp64_peak = W.probe_dmma_peak(local)
 
-    dmma_peak = W.probe_dmma_peak(local)
+    def maxrank(x):
+        if not dist:
+            return x
+        t = torch.tensor([x], device=dev, dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
 
     for _ in range(max(args.warmup, 3)):
         op.apply_block_dev(V, out, sp)
@@ -210,182 +238,243 @@ def run_ours(args):
     if dist:
         dist.barrier()
     torch.cuda.synchronize()
+    l0 = W.launch_count()
     with ClockSampler(local) as clk:
         for i in range(args.steps):
-            flush.fill_(float(i))  # L2 flush between timed steps (excluded from step time)
             starts[i].record(stream)
             op.apply_block_dev(V, out, sp)
             ends[i].record(stream)
         torch.cuda.synchronize()
+    launches = W.launch_count() - l0
     if dist:
         dist.barrier()
     step_ms = [s.elapsed_time(e) for s, e in zip(starts, ends)]
-    total_ms = sum(step_ms)
+    total_ms = maxrank(sum(step_ms))
     stage_ms, calls = op.profile_read()
     op.profile(False)
-    if dist:
-        t = torch.tensor([total_ms], device=dev, dtype=torch.float64)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        total_ms = float(t.item())
-    value = world * m * args.steps / (total_ms / 1e3)
+    value = M_GLOBAL * args.steps / (total_ms / 1e3)
+    step_mean_ms = total_ms / args.steps
+    clocks = clk.summary()
 
-    # ---- e2e: the public C-ABI with HOST buffers (pinned), H2D + D2H inside the timed region
-    Vh = torch.from_numpy(np.ascontiguousarray(Om.T)).pin_memory()
-    Oh = torch.empty_like(Vh).pin_memory()
-    op.apply_block_host_ptr(Vh.data_ptr(), nA, m, Oh.data_ptr(), nA)
-    if dist:
-        dist.barrier()
-    t0 = time.perf_counter()
-    for _ in range(args.steps):
-        op.apply_block_host_ptr(Vh.data_ptr(), nA, m, Oh.data_ptr(), nA)
-    e2e_s = time.perf_counter() - t0
-    if dist:
-        t = torch.tensor([e2e_s], device=dev, dtype=torch.float64)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        e2e_s = float(t.item())
-    e2e_value = world * m * args.steps / e2e_s
-
-    # ---- roofline of the dominant kernel (the D^{1/2} DMMA GEMM)
-    nA_, flops_gemm, flops_model, bytes_step = algorithmic_counts(wl, m)
-    gemm_ms = (stage_ms[0] + stage_ms[2]) / (2 * max(calls, 1))
-    achieved_tf = flops_gemm / (gemm_ms * 1e-3) / 1e12
-    traffic, traffic_src = gemm_traffic()
+    # ---- roofline of the dominant kernel: the fused FFT convolution (circulant D^{1/2})
+    _, fft_flops_launch, flops_step, bytes_step = c4_counts(m=m)
+    fft_ms = stage_ms[0] / max(calls, 1)   # the first D^{1/2}: one fftconv_kernel launch
+    achieved = fft_flops_launch / (fft_ms * 1e-3) / 1e12
+    traffic, traffic_src = profile_traffic("r02_c4_fftconv.json", "fftconv")
     try:
         peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
     except Exception:
         peaks = {}
     hbm_peak = peaks.get("hbm_gbs", 6650.0)
-    step_mean_ms = total_ms / args.steps
-    clocks = clk.summary()
+    t_roof = max(flops_step / (fp64_peak * 1e12), bytes_step / (hbm_peak * 1e9)) * 1e3
 
-    extras = {}
-    if not args.no_extras and rank == 0:
-        extras = run_extras(W, configs, wl, op, Om, dev)
-        if world == 1:
-            extras["large_configs"] = run_large(W, configs, dmma_peak, hbm_peak)
+    # ---- e2e: the reference-facing C-ABI (wc4dvar_gpu_op_apply_block) with pinned HOST buffers
+    Vh = torch.empty((m, nA), dtype=torch.float64, pin_memory=True)
+    Vh.copy_(V)
+    Oh = torch.empty((m, nA), dtype=torch.float64, pin_memory=True)
+    del V, out
+    torch.cuda.empty_cache()
+    op.apply_block_host_ptr(Vh.data_ptr(), nA, m, Oh.data_ptr(), nA)
+    if dist:
+        dist.barrier()
+    e2e_steps = max(2, min(args.steps, 5))
+    t0 = time.perf_counter()
+    for _ in range(e2e_steps):
+        op.apply_block_host_ptr(Vh.data_ptr(), nA, m, Oh.data_ptr(), nA)
+    e2e_s = maxrank(time.perf_counter() - t0)
+    e2e_value = M_GLOBAL * e2e_steps / e2e_s
+    check = float(Oh[0, :4].sum())  # read back (the step's result on the host)
+    del Vh, Oh
 
+    line = None
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": step_mean_ms, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-            "data": "synthetic (seeded N(0,1) sketch from the reference NormalStream, BASELINE configs[1] operator)",
-            "config": {"workload": wl.name, "n": wl.model.n, "Nsw": wl.model.N, "substeps": wl.model.substeps,
-                       "n_A": nA, "sketch_columns_per_gpu": m, "q": wl.net.q, "covariance": "dense SOAR",
-                       "parallelism": f"column-sharded x{world}",
-                       "l2": "flushed between timed steps (256 MiB write), flush excluded from step time"},
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (seeded N(0,1) sketch = the reference NormalStream(1) stream, generated on the "
+                    "device with MT19937-64 jump-ahead; BASELINE configs[3] operator)",
+            "config": {"workload": wl.name.replace("-m256", "") + "-k256", "n": wl.model.n, "Nsw": wl.model.N,
+                       "substeps": wl.model.substeps, "n_A": nA, "sketch_columns": M_GLOBAL,
+                       "sketch_columns_per_gpu": m, "q": wl.net.q, "covariance": "circulant SOAR L=50",
+                       "parallelism": f"column-sharded x{world} (one global sketch)",
+                       "l2": "inputs larger than L2 (sketch block %.1f GB per GPU); no flush" % (8e-9 * nA * m)},
             "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": 8 * nA * m,
-                    "d2h_bytes_per_step": 8 * nA * m},
-            "gpu_launches": 3 * args.steps,
-            "roofline": {"bound": "tensor", "achieved": achieved_tf, "peak": dmma_peak, "unit": "TFLOP/s",
-                         "frac": achieved_tf / dmma_peak, "traffic": traffic,
-                         "traffic_source": traffic_src,
-                         "kernel": "gemm_sym_ws_kernel (D^1/2 block-diagonal DMMA GEMM, stream-K)",
-                         "flops_per_launch": flops_gemm, "launch_ms": gemm_ms,
-                         "peak_source": "measured in this run: all-SM mma.sync.f64 probe "
-                                        "(MEASURED_PEAKS.json has bf16/HBM only)"},
-            "hbm_roofline": {"bytes_per_step": bytes_step, "achieved_gbs": bytes_step / (step_mean_ms * 1e-3) / 1e9,
-                             "peak_gbs": hbm_peak, "frac": bytes_step / (step_mean_ms * 1e-3) / 1e9 / hbm_peak,
-                             "note": "C2 is fp64-compute bound (dense D^1/2 is 99% of flops)"},
+                    "d2h_bytes_per_step": 8 * nA * m, "steps": e2e_steps,
+                    "path": "wc4dvar_gpu_op_apply_block (host pointers, pinned): two-slot chunk ring, H2D / "
+                            "compute / D2H on three streams", "checksum": check},
+            "gpu_launches": launches,
+            "roofline": {"bound": "fp64", "achieved": achieved, "peak": fp64_peak, "unit": "TFLOP/s",
+                         "frac": achieved / fp64_peak, "traffic": traffic, "traffic_source": traffic_src,
+                         "kernel": "fftconv_kernel (circulant D^1/2: fused four-step FFT convolution)",
+                         "flops_per_launch": fft_flops_launch, "launch_ms": fft_ms,
+                         "flops_per_unit": "(N+1)(5 n log2 n + n) per sketch column (real-FFT convention, SURVEY §8(d))",
+                         "peak_source": "measured in this run: all-SM mma.sync.f64 probe (the FP64 FMA pipe "
+                                        "measures the same ~36-37 TF/s, profiles/r01_fp64_pipes_probe.txt)"},
+            "apply_roofline": {"t_roof_ms": t_roof, "frac": t_roof / step_mean_ms,
+                               "bound": "fp64" if flops_step / (fp64_peak * 1e12) >= bytes_step / (hbm_peak * 1e9)
+                               else "hbm",
+                               "flops_per_step": flops_step, "bytes_per_step": bytes_step,
+                               "hbm_gbs": bytes_step / (step_mean_ms * 1e-3) / 1e9, "hbm_peak_gbs": hbm_peak,
+                               "hbm_frac": bytes_step / (step_mean_ms * 1e-3) / 1e9 / hbm_peak},
             "stage_ms": {"d_half_in": stage_ms[0] / max(calls, 1), "sweep": stage_ms[1] / max(calls, 1),
                          "d_half_out_plus_identity": stage_ms[2] / max(calls, 1)},
             "clocks": clocks,
         }
+    del op
+    torch.cuda.empty_cache()
+
+    if not args.no_extras and rank == 0 and world == 1:
+        extras = {}
+        for key, fn in (("configs", lambda: run_configs(W, configs, fp64_peak, hbm_peak)),
+                        ("lmp", lambda: run_lmp(W, configs, dev)),
+                        ("cpu_baseline", lambda: cpu_baseline())):
+            try:
+                extras[key] = fn()
+            except Exception as e:  # report, never lose the headline line
+                extras[key] = {"error": f"{type(e).__name__}: {e}"[:400]}
+            torch.cuda.empty_cache()
+        cb = extras.pop("cpu_baseline")
+        line["cpu_baseline"] = cb
         line.update(extras)
-        if world == 1:
-            threads = os.cpu_count() or 1
-            cols = min(m, max(8, 2 * threads))
-            secs = cpu_reference(wl, cols, threads)
-            line["cpu_baseline"] = {"value": cols / secs, "unit": UNIT, "cores": threads, "kind": "port",
-                                    "sample": f"{cols} of {m} sketch columns, oracle/wc4dvar_oracle.c "
-                                              f"(reference not buildable: Eigen absent), pthread column fan-out"}
-        print(json.dumps(line))
+    if rank == 0:
+        print(json.dumps(line), flush=True)
     if dist:
         dist.destroy_process_group()
     return 0
 
 
-def run_extras(W, configs, wl, op, Om, dev):
-    """LMP build ms per method (Omega resident on device -> U, Theta on device) and
-    LMP-PCG time/iterations on the same operator."""
-    import numpy as np
-    import torch
-    out = {"lmp_build_ms": {}, "lmp_build_stage_ms": {}, "pcg": {}}
-    nA = op.dim()
-    k, l = wl.k, wl.m - wl.k
-    pairs = {}
-    for method in ("revd", "nystrom", "ritzit"):
-        cfg = W.SketchConfig(k, l, configs.OMEGA_SEED, method, 1)
-        W.sketch_eigenpairs(op, cfg, Om)  # warm (grows the sketch workspaces)
-        pairs[method] = W.sketch_eigenpairs(op, cfg, Om)
-        t = W.last_sketch_timing()  # the second, warm call
-        out["lmp_build_ms"][method] = t["total_ms"]
-        out["lmp_build_stage_ms"][method] = {kk: v for kk, v in t.items() if kk != "total_ms"}
-    b = W.gaussian_matrix(nA, 1, configs.RHS_SEED)[:, 0]
-    for method in ("none", "revd", "nystrom", "ritzit"):
-        f = None if method == "none" else W.build_spectral_lmp(pairs[method])
-        t0 = time.perf_counter()
-        r = W.pcg_split(op, b, f, opts=W.PcgOptions(max_iter=500, rel_tol=1e-6))
-        out["pcg"][method] = {"ms": 1e3 * (time.perf_counter() - t0), "iterations": r.history.iterations,
-                              "converged": r.history.converged}
-    return out
+def cpu_baseline():
+    threads = os.cpu_count() or 1
+    wl, V = oracle_c4(threads, CPU_SAMPLE_COLS)
+    wl.op.apply_block_fast(V, threads)
+    t0 = time.perf_counter()
+    wl.op.apply_block_fast(V, threads)
+    secs = time.perf_counter() - t0
+    return {"value": CPU_SAMPLE_COLS / secs, "unit": UNIT, "cores": threads, "kind": "port",
+            "sample": f"{CPU_SAMPLE_COLS} of the {M_GLOBAL} C4 sketch columns (NormalStream(1) columns 0..15), "
+                      f"one warm apply; oracle port (reference not buildable: Eigen absent): batched real-FFT "
+                      f"circulant D^1/2 (scipy.fft, {threads} workers) + C sweeps, {threads}-thread column fan-out"}
 
 
-def run_large(W, configs, peak_tfs, hbm_gbs):
-    """BASELINE configs[2] (C3, Lorenz-96 n=1e5), configs[3] (C4, adv-diff n=1e6, circulant
-    factors) block applies at m = 64 and configs[4] (C5, Lorenz-96 n=2e6, Nsw=20) at one
-    rank's 32-column share of its 8-GPU sketch, on one GPU: device-drawn N(0,1) Omega (torch,
-    throughput only; parity at these shapes is property-based in tests/), CUDA-event timing,
-    per-stage split, and the SURVEY §8(d) roofline t_roof = max(B/BW, F/P) per block with
-    B = 8 (3 n_A + 2 q) m and F = (F_model + F_cov) m."""
+def _apply_timing(W, wl, m, fp64_peak, hbm_peak, reps=3):
     import torch
+    op = wl.hessian(0)
+    nA, q = op.dim(), wl.net.q
+    n, N, s = wl.model.n, wl.model.N, wl.model.substeps
+    V = torch.empty((m, nA), dtype=torch.float64, device="cuda")
+    W.gaussian_block_dev(V, nA, OMEGA_SEED)
+    Y = torch.empty_like(V)
+    sp = torch.cuda.current_stream().cuda_stream
+    for _ in range(2):
+        op.apply_block_dev(V, Y, sp)
+    op.profile(True)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(reps):
+        op.apply_block_dev(V, Y, sp)
+    e1.record()
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / reps
+    st, calls = op.profile_read()
+    op.profile(False)
+    if wl.b_half.kind == "dense":
+        f_cov = 4.0 * n * n * (N + 1)
+    else:
+        f_cov = 2.0 * (N + 1) * (5.0 * n * math.log2(n) + n)
+    f_model = (92.0 if wl.model.kind == "l96" else 10.0) * N * s * n
+    t_f = (f_model + f_cov) * m / (fp64_peak * 1e12)
+    t_b = 8.0 * (3 * nA + 2 * q) * m / (hbm_peak * 1e9)
+    t_roof = max(t_f, t_b) * 1e3
+    return {"workload": wl.name, "m": m, "ms_per_apply": ms, "columns_per_s": m / (ms * 1e-3),
+            "stage_ms": {"d_half_in": st[0] / max(calls, 1), "sweep": st[1] / max(calls, 1),
+                         "d_half_out_plus_identity": st[2] / max(calls, 1)},
+            "roofline": {"t_roof_ms": t_roof, "bound": "fp64" if t_f >= t_b else "hbm", "frac": t_roof / ms}}
+
+
+def run_configs(W, configs, fp64_peak, hbm_peak):
+    """Block applies of the other BASELINE configs (N = 1): C2 (dense SOAR, m = 100), C3
+    (Lorenz-96, m = 64), C4 at k = 16 / 64, and C5 at one rank's 32-column share of its
+    8-GPU sketch."""
     out = {}
-    for name, mk in (("C3", lambda: configs.config3()), ("C4", lambda: configs.config4(64)),
-                     ("C5", lambda: configs.config5(32))):
+    for name, mk, m in (("C2", configs.config2, 100), ("C3", configs.config3, 64),
+                        ("C4_k16", lambda: configs.config4(16), 16), ("C4_k64", lambda: configs.config4(64), 64),
+                        ("C5_rank_share", lambda: configs.config5(32), 32)):
         try:
-            wl = mk()
-            t0 = time.perf_counter()
-            op = wl.hessian(0)
-            setup_s = time.perf_counter() - t0
-            m, nA, q = wl.m, op.dim(), wl.net.q  # C5: one rank's 32-column share of the 8-GPU sketch
-            n, N, s = wl.model.n, wl.model.N, wl.model.substeps
-            g = torch.Generator(device="cuda").manual_seed(1)
-            V = torch.randn(m, nA, dtype=torch.float64, device="cuda", generator=g)
-            Y = torch.empty_like(V)
-            sp = torch.cuda.current_stream().cuda_stream
-            op.apply_block_dev(V, Y, sp)
-            op.profile(True)
-            torch.cuda.synchronize()
-            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            reps = 3
-            e0.record()
-            for _ in range(reps):
-                op.apply_block_dev(V, Y, sp)
-            e1.record()
-            torch.cuda.synchronize()
-            ms = e0.elapsed_time(e1) / reps
-            st, calls = op.profile_read()
-            op.profile(False)
-            f_model = (92.0 if wl.model.kind == "l96" else 10.0) * N * s * n
-            f_cov = 2.0 * (N + 1) * (5.0 * n * math.log2(n) + n)
-            t_f = (f_model + f_cov) * m / (peak_tfs * 1e12)
-            t_b = 8.0 * (3 * nA + 2 * q) * m / (hbm_gbs * 1e9)
-            t_roof = max(t_f, t_b) * 1e3
-            out[name] = {"workload": wl.name, "m": m, "ms_per_apply": ms, "columns_per_s": m / (ms * 1e-3),
-                         "stage_ms": {"d_half_in": st[0] / max(calls, 1), "sweep": st[1] / max(calls, 1),
-                                      "d_half_out_plus_identity": st[2] / max(calls, 1)},
-                         "roofline": {"t_roof_ms": t_roof, "bound": "fp64" if t_f >= t_b else "hbm",
-                                      "frac": t_roof / ms},
-                         "operator_setup_s": setup_s, "omega": "device N(0,1) (torch), seed 1"}
-            del V, Y, op
-            torch.cuda.empty_cache()
-        except Exception as e:  # report, do not fail the headline line
+            out[name] = _apply_timing(W, mk(), m, fp64_peak, hbm_peak)
+        except Exception as e:
             out[name] = {"error": f"{type(e).__name__}: {e}"[:300]}
     return out
 
 
+def run_lmp(W, configs, dev):
+    """LMP build ms (Omega resident on the device -> U, Theta on the device; second, warm call)
+    per method, and LMP-PCG time-to-solution to relative residual 1e-6 (krylov.cpp:22-99)."""
+    import numpy as np
+    import torch
+    res = {}
+    for name, mk, pcg_methods, max_iter in (
+            ("C2", configs.config2, ("none", "revd", "nystrom", "ritzit"), 1000),
+            ("C3", configs.config3, ("none", "nystrom"), 500),
+            ("C4_k256", lambda: configs.config4(256), ("none", "nystrom"), 300)):
+        r = {"build_ms": {}, "build_stage_ms": {}, "pcg": {}}
+        try:
+            wl = mk()
+            op = wl.hessian(0)
+            nA, m, k = op.dim(), wl.m, wl.k
+            r.update({"workload": wl.name, "m": m, "k": k})
+            Om = torch.empty((m, nA), dtype=torch.float64, device=dev)
+            W.gaussian_block_dev(Om, nA, OMEGA_SEED)
+            U = torch.empty((k, nA), dtype=torch.float64, device=dev)
+            th = torch.empty(k, dtype=torch.float64, device=dev)
+            kept = {}
+            for method in ("revd", "ritzit", "nystrom"):
+                cfg = W.SketchConfig(k, m - k, OMEGA_SEED, method, 1)
+                W.sketch_eigenpairs_dev(op, cfg, Om, U, th)          # warm (grows workspaces)
+                torch.cuda.synchronize()
+                t0 = time.perf_counter()
+                kk = W.sketch_eigenpairs_dev(op, cfg, Om, U, th)
+                torch.cuda.synchronize()
+                wall = 1e3 * (time.perf_counter() - t0)
+                t = W.last_sketch_timing()
+                r["build_ms"][method] = t["total_ms"]
+                r["build_stage_ms"][method] = dict({kk_: v for kk_, v in t.items() if kk_ != "total_ms"},
+                                                   wall_ms=wall)
+                r.setdefault("theta_head", {})[method] = th[:3].cpu().tolist()
+                if method in pcg_methods:
+                    if method == "nystrom":   # last: free the sketch blocks before the factor copies U
+                        del Om
+                        op.release_workspaces()
+                        torch.cuda.empty_cache()
+                    kept[method] = W.build_spectral_lmp_dev(U, th, kk, 0)
+            del U, th
+            op.release_workspaces()
+            torch.cuda.empty_cache()
+            b = torch.empty((1, nA), dtype=torch.float64, device=dev)
+            W.gaussian_block_dev(b, nA, RHS_SEED)
+            bh = b[0].cpu().numpy()
+            del b
+            for method in pcg_methods:
+                f = kept.get(method)
+                t0 = time.perf_counter()
+                pr = W.pcg_split(op, bh, f, opts=W.PcgOptions(max_iter=max_iter, rel_tol=1e-6))
+                ms = 1e3 * (time.perf_counter() - t0)
+                r["pcg"][method] = {"ms": ms, "iterations": pr.history.iterations,
+                                    "converged": pr.history.converged,
+                                    "ms_per_iteration": ms / max(pr.history.iterations, 1)}
+            del kept, op
+        except Exception as e:
+            r["error"] = f"{type(e).__name__}: {e}"[:400]
+        torch.cuda.empty_cache()
+        res[name] = r
+    return res
+
+
 def main():
     args = parse()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        return spawn_ranks(args.gpus)
     if args.impl == "reference":
         return run_reference(args)
     return run_ours(args)

@@ -47,6 +47,9 @@ const char* wc4dvar_gpu_last_error(void);
 /* Library version string and the compiled device architecture ("sm_100a"). */
 const char* wc4dvar_gpu_version(void);
 
+/* Number of kernel launches this library has issued (bench.py's gpu_launches). */
+int64_t wc4dvar_gpu_launch_count(void);
+
 /* ------------------------------------------------------------------------- */
 /* Operator descriptors                                                       */
 /* ------------------------------------------------------------------------- */
@@ -128,6 +131,11 @@ int64_t wc4dvar_gpu_op_dim(const wc4dvar_op* op);
 int64_t wc4dvar_gpu_op_apply_count(const wc4dvar_op* op);
 void wc4dvar_gpu_op_reset_apply_count(wc4dvar_op* op);
 int wc4dvar_gpu_op_device(const wc4dvar_op* op);
+
+/* Frees the operator's grow-only device workspaces (block-apply, sketch and PCG buffers);
+ * they re-grow on the next call.  Lets a caller bound peak HBM between the sketch (two
+ * n x (k+l) blocks) and the solve (SURVEY §7 hard part 7). */
+int wc4dvar_gpu_op_release_workspaces(wc4dvar_op* op);
 
 /* LinearOperator::apply (operators.hpp:23) and apply_block (operators.hpp:30,
  * operators.cpp:9-19).  Column-major V (dim x m, ldv), out (dim x m, ldo). */

@@ -13,5 +13,5 @@ from .wc4dvar import (  # noqa: F401
     lorenz96_trajectory, lorenz96_trajectory_device, integrate_p, InnerLoopReport, PrecondSpec, SolverSpec,
     run_inner_loop, ClusteredSpectrum, clustered_spectrum, TridiagonalMatrix, tridiagonal_from_cg,
     ritz_from_tridiagonal, LanczosOptions, lanczos_eigenpairs, exact_top_pairs,
-    gaussian_block_dev, mt19937_raw_host, mt19937_raw_dev,
+    gaussian_block_dev, mt19937_raw_host, mt19937_raw_dev, sketch_eigenpairs_dev, launch_count, build_spectral_lmp_dev,
 )

@@ -38,6 +38,11 @@ using namespace w4;
         return WC4DVAR_DEVICE;             \
     }
 
+namespace w4 {
+void gaussian_block_dev(int64_t n_total, int64_t row0, int64_t rows, int64_t col0, int64_t cols,
+                        uint64_t seed, double* out, int64_t ldo, bool raw, cudaStream_t st);
+}
+
 namespace {
 
 thread_local SketchTiming g_sketch_timing;
@@ -236,6 +241,16 @@ void wc4dvar_gpu_op_reset_apply_count(wc4dvar_op* op) {
 }
 int wc4dvar_gpu_op_device(const wc4dvar_op* op) { return op ? op->device : -1; }
 
+int wc4dvar_gpu_op_release_workspaces(wc4dvar_op* op) {
+    W4_API_BEGIN
+    require(op != nullptr, "release_workspaces: null operator");
+    std::lock_guard<std::recursive_mutex> lk(op->mu);
+    DeviceGuard g(op->device);
+    W4_CUDA(cudaStreamSynchronize(op->stream));
+    op->release_workspaces();
+    W4_API_END
+}
+
 int wc4dvar_gpu_op_apply_block(wc4dvar_op* op, const double* V, int64_t ldv, int64_t m,
                                double* out, int64_t ldo) {
     W4_API_BEGIN
@@ -247,40 +262,52 @@ int wc4dvar_gpu_op_apply_block(wc4dvar_op* op, const double* V, int64_t ldv, int
     op->applies += m;
     if (m == 0 || op->dim == 0) return WC4DVAR_OK;
     cudaStream_t st = op->stream;
-    double* din = op->in_buf.get<double>((size_t)op->dim * m);
-    double* dout = op->out_buf.get<double>((size_t)op->dim * m);
-    // Copy/compute overlap for wide blocks: the columns go in `nch` chunks; chunk c+1's
-    // host->device copy and chunk c-1's device->host copy run on their own streams while
-    // chunk c computes.  Each column's arithmetic is unchanged (bitwise).
-    // WC4DVAR_PIPELINE_CHUNKS (default 2; 1 = off), engaged for m >= 32.
+    // Copy/compute pipeline for wide blocks: the columns go through a two-slot device ring
+    // in `nch` chunks; chunk c+1's host->device copy and chunk c-1's device->host copy run
+    // on their own streams while chunk c computes.  Each column's arithmetic is unchanged
+    // (bitwise), and the device staging stays bounded (2 x 2 slots of <= kStageBytes) for
+    // blocks far larger than HBM headroom (C4: n_A x 256 = 34.8 GB each way).
+    // WC4DVAR_PIPELINE_CHUNKS (default 2; 1 = off) is the chunk count below that bound.
     static const int chunks_env = [] {
         const char* e = std::getenv("WC4DVAR_PIPELINE_CHUNKS");
         return e ? std::atoi(e) : 2;
     }();
-    const int nch = (m >= 32 && !op->prof) ? std::max(1, std::min(chunks_env, 4)) : 1;
+    constexpr size_t kStageBytes = size_t(4) << 30;
+    const int64_t cmax = std::max<int64_t>(1, (int64_t)(kStageBytes / (sizeof(double) * (size_t)op->dim)));
+    int64_t nch = cdiv(m, cmax);
+    if (nch == 1 && m >= 32 && chunks_env > 1) nch = std::min<int64_t>(chunks_env, 4);
+    if (op->prof && m <= cmax) nch = 1;  // stage timers see one apply
     if (nch > 1) {
         op->ensure_pipeline();
         op->reset_status(st);
-        int64_t cb[5];
-        for (int c = 0; c <= nch; ++c) cb[c] = m * c / nch;
-        for (int c = 0; c < nch; ++c) {
-            h2d_block(din + cb[c] * op->dim, V + cb[c] * ldv, op->dim, cb[c + 1] - cb[c], ldv, op->pipe_in);
-            W4_CUDA(cudaEventRecord(op->pipe_ev[c], op->pipe_in));
-        }
-        for (int c = 0; c < nch; ++c) {
-            W4_CUDA(cudaStreamWaitEvent(st, op->pipe_ev[c], 0));
-            op->apply_block_dev(din + cb[c] * op->dim, op->dim, cb[c + 1] - cb[c], dout + cb[c] * op->dim,
-                                op->dim, st);
-            W4_CUDA(cudaEventRecord(op->pipe_ev[4 + c], st));
-        }
-        for (int c = 0; c < nch; ++c) {
-            W4_CUDA(cudaStreamWaitEvent(op->pipe_out, op->pipe_ev[4 + c], 0));
-            d2h_block(out + cb[c] * ldo, ldo, dout + cb[c] * op->dim, op->dim, cb[c + 1] - cb[c], op->pipe_out);
+        const int64_t cw = cdiv(m, nch);
+        double* din = op->in_buf.get<double>((size_t)op->dim * cw * 2);
+        double* dout = op->out_buf.get<double>((size_t)op->dim * cw * 2);
+        cudaEvent_t* in_ready = op->pipe_ev;       // [0, 2)
+        cudaEvent_t* computed = op->pipe_ev + 2;   // [2, 4)
+        cudaEvent_t* drained = op->pipe_ev + 4;    // [4, 6)
+        for (int64_t c = 0; c < nch; ++c) {
+            const int slot = (int)(c & 1);
+            const int64_t c0 = m * c / nch, w = m * (c + 1) / nch - c0;
+            double* di = din + (size_t)slot * op->dim * cw;
+            double* dq = dout + (size_t)slot * op->dim * cw;
+            if (c >= 2) W4_CUDA(cudaStreamWaitEvent(op->pipe_in, computed[slot], 0));
+            h2d_block(di, V + c0 * ldv, op->dim, w, ldv, op->pipe_in);
+            W4_CUDA(cudaEventRecord(in_ready[slot], op->pipe_in));
+            W4_CUDA(cudaStreamWaitEvent(st, in_ready[slot], 0));
+            if (c >= 2) W4_CUDA(cudaStreamWaitEvent(st, drained[slot], 0));
+            op->apply_block_dev(di, op->dim, w, dq, op->dim, st);
+            W4_CUDA(cudaEventRecord(computed[slot], st));
+            W4_CUDA(cudaStreamWaitEvent(op->pipe_out, computed[slot], 0));
+            d2h_block(out + c0 * ldo, ldo, dq, op->dim, w, op->pipe_out);
+            W4_CUDA(cudaEventRecord(drained[slot], op->pipe_out));
         }
         W4_CUDA(cudaStreamSynchronize(op->pipe_out));
         op->check_status(st);
         return WC4DVAR_OK;
     }
+    double* din = op->in_buf.get<double>((size_t)op->dim * m);
+    double* dout = op->out_buf.get<double>((size_t)op->dim * m);
     h2d_block(din, V, op->dim, m, ldv, st);
     op->reset_status(st);
     op->apply_block_dev(din, op->dim, m, dout, op->dim, st);
@@ -581,16 +608,14 @@ int wc4dvar_gpu_sketch(wc4dvar_op* op, const wc4dvar_sketch_config* cfg, const d
     DeviceGuard g(op->device);
     const int64_t n = op->dim;
     cudaStream_t st = op->stream;
-    std::vector<double> hom;
-    if (!omega) {
-        hom.resize(n * m);
-        w4::gaussian_fill(n * m, cfg->seed, hom.data());
-        omega = hom.data();
-    }
     double* dom = op->in_buf.get<double>((size_t)n * m);
     double* dU = op->out_buf.get<double>((size_t)n * cfg->target_rank + cfg->target_rank);
     double* dth = dU + (size_t)n * cfg->target_rank;
-    h2d_block(dom, omega, n, m, n, st);
+    if (omega) {
+        h2d_block(dom, omega, n, m, n, st);
+    } else {  // gaussian_matrix(dim, k + l, seed) drawn on the device (jump-ahead NormalStream)
+        w4::gaussian_block_dev(n, 0, n, 0, m, cfg->seed, dom, n, false, st);
+    }
     g_sketch_timing = SketchTiming{};
     const int64_t kk = sketch_dev(*op, *cfg, dom, dU, n, dth, st, &g_sketch_timing);
     d2h_block(U, ldu, dU, n, kk, st);

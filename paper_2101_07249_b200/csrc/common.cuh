@@ -3,6 +3,7 @@
 
 #include <cuda_runtime.h>
 
+#include <atomic>
 #include <cstdint>
 #include <stdexcept>
 #include <string>
@@ -33,8 +34,13 @@ inline void require(bool cond, const std::string& what) {
             throw ::w4::DeviceError(std::string(#expr) + ": " + cudaGetErrorString(_e)); \
     } while (0)
 
+// Kernel launches issued by this library (wc4dvar_gpu_launch_count): every launch site
+// is followed by W4_LAUNCH().
+extern std::atomic<long long> g_launch_count;
+
 #define W4_LAUNCH()                                                                      \
     do {                                                                                 \
+        ::w4::g_launch_count.fetch_add(1, std::memory_order_relaxed);                    \
         cudaError_t _e = cudaGetLastError();                                             \
         if (_e != cudaSuccess)                                                           \
             throw ::w4::DeviceError(std::string("kernel launch (") + __FILE__ + ":" +       \
@@ -59,6 +65,11 @@ struct DevBuf {
     size_t bytes = 0;
     ~DevBuf() {
         if (p) cudaFree(p);
+    }
+    void release() {
+        if (p) cudaFree(p);
+        p = nullptr;
+        bytes = 0;
     }
     template <class T>
     T* get(size_t count) {

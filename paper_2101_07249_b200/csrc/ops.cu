@@ -10,6 +10,8 @@
 
 namespace w4 {
 
+std::atomic<long long> g_launch_count{0};
+
 namespace {
 thread_local std::string g_last_error;
 }
@@ -18,6 +20,8 @@ void set_last_error(const std::string& msg) { g_last_error = msg; }
 const char* last_error_cstr() { return g_last_error.c_str(); }
 
 }  // namespace w4
+
+extern "C" int64_t wc4dvar_gpu_launch_count(void) { return w4::g_launch_count.load(); }
 
 using namespace w4;
 

@@ -42,6 +42,12 @@ struct wc4dvar_op {
     void ensure_pipeline();
 
     virtual ~wc4dvar_op();
+    // Frees every grow-only workspace (they re-grow on the next call).
+    virtual void release_workspaces() {
+        in_buf.release();
+        out_buf.release();
+        for (auto& b : pool) b.release();
+    }
     // Block apply on device pointers; does not count and does not synchronise.
     virtual void apply_block_dev(const double* V, int64_t ldv, int64_t m, double* out, int64_t ldo,
                                  cudaStream_t st) = 0;
@@ -75,6 +81,12 @@ struct HessianOp final : wc4dvar_op {
     double* d_stages = nullptr;
     std::vector<int> times, points;
     DevBuf t_ws, y_ws, sweep_ws;
+    void release_workspaces() override {
+        wc4dvar_op::release_workspaces();
+        t_ws.release();
+        y_ws.release();
+        sweep_ws.release();
+    }
     CirculantPlan* circ = nullptr;  // WC4DVAR_COV_CIRCULANT factors
     DevBuf circ_z, circ_x;
 

@@ -82,6 +82,7 @@ struct Ctx {
     Timer& tm;
     DevBuf* pool;
     int* h_int;  // pinned scratch
+    int shifted_calls = 0;  // orth() calls that needed shifted CholQR3
 
     double* buf(int id, size_t count) { return pool[id].get<double>(count); }
 
@@ -120,9 +121,11 @@ struct Ctx {
         gemm_nn(&p, 1, nullptr, st);
     }
 
-    // CholQR2: Q (n x m) with Y = Q R; G0 = Y^T Y may be supplied.  Returns false on a
-    // Cholesky breakdown (caller raises the method-specific NumericalError).
-    bool cholqr2(const double* Y, int64_t m, double* Q, double* R_out, const double* G0) {
+    // CholQR2: Q (n x m) with Y = Q R; G0 = Y^T Y may be supplied.  Q may alias Y (Y is
+    // dead once Q1 = Y R1^{-1} exists); `scratch` (n x m) holds Q1 and must alias neither.
+    // Returns false on a Cholesky breakdown (caller raises the method-specific
+    // NumericalError).
+    bool cholqr2(const double* Y, int64_t m, double* Q, double* R_out, const double* G0, double* scratch) {
         tm.begin(T_ORTH);
         double* G = buf(P_G, m * m);
         if (G0) {
@@ -136,7 +139,7 @@ struct Ctx {
         int* info = reinterpret_cast<int*>(buf(P_INT, 4 + 2 * m));
         chol_inv_upper((int)m, G, R1, R1i, info, pool[P_SMALLWS], st);
         if (read_int(info)) return false;
-        double* Q1 = buf(P_Q1, n * m);
+        double* Q1 = scratch;
         tall_times_small(Y, m, R1i, m, m, Q1, n);
         double* G2 = buf(P_G2, m * m);
         gram(Q1, m, Q1, m, G2);
@@ -147,6 +150,55 @@ struct Ctx {
         tall_times_small(Q1, m, R2i, m, m, Q, n);
         if (R_out) small_gemm(false, false, (int)m, (int)m, (int)m, 1.0, R2, (int)m, R1, (int)m, 0.0,
                               R_out, (int)m, st);
+        tm.end();
+        return true;
+    }
+
+    // Orthonormal basis Q of span(Y) (full column rank) with Y = Q R: CholQR2, falling back
+    // to shifted CholQR3 (Fukaya, Kannan, Nakatsukasa, Yamamoto, Yanagisawa 2020) when the
+    // Gram is too ill-conditioned for a plain Cholesky (cond(Y) >~ 1e8; the reference's
+    // Householder QR accepts any full-rank Y).  Q may alias Y; `scratch` aliases neither.
+    // Returns false only if the shifted variant breaks down too.
+    bool orth(const double* Y, int64_t m, double* Q, double* R_out, const double* G0, double* scratch) {
+        if (cholqr2(Y, m, Q, R_out, G0, scratch)) return true;
+        ++shifted_calls;
+        tm.begin(T_ORTH);
+        double* G = buf(P_G, m * m);
+        gram(Y, m, Y, m, G);  // cholqr2 may have overwritten P_G
+        std::vector<double> hG((size_t)m * m);
+        W4_CUDA(cudaMemcpyAsync(hG.data(), G, sizeof(double) * m * m, cudaMemcpyDeviceToHost, st));
+        W4_CUDA(cudaStreamSynchronize(st));
+        double tr = 0.0;
+        for (int64_t i = 0; i < m; ++i) tr += hG[i + i * m];
+        // shift s = 11 (m n + m (m + 1)) u ||Y||_2^2, with trace(G) >= ||Y||_2^2
+        const double shift = 11.0 * ((double)m * (double)n + (double)m * (m + 1)) * 1.1102230246251565e-16 * tr;
+        for (int64_t i = 0; i < m; ++i) hG[i + i * m] += shift;
+        W4_CUDA(cudaMemcpyAsync(G, hG.data(), sizeof(double) * m * m, cudaMemcpyHostToDevice, st));
+        double* Rs = buf(P_R1, m * m);
+        double* Rsi = buf(P_R1I, m * m);
+        int* info = reinterpret_cast<int*>(buf(P_INT, 4 + 2 * m));
+        chol_inv_upper((int)m, G, Rs, Rsi, info, pool[P_SMALLWS], st);
+        if (read_int(info)) return false;
+        tall_times_small(Y, m, Rsi, m, m, scratch, n);  // Q1 = Y Rs^{-1}; Y is dead after this
+        double* Racc = buf(P_TMP, 2 * m * m);
+        double* Rtmp = Racc + m * m;
+        W4_CUDA(cudaMemcpyAsync(Racc, Rs, sizeof(double) * m * m, cudaMemcpyDeviceToDevice, st));
+        double* src = scratch;
+        double* dst = Q;  // Q is free: either Y's own (dead) buffer or a separate output
+        for (int pass = 0; pass < 2; ++pass) {
+            double* G2 = buf(P_G2, m * m);
+            gram(src, m, src, m, G2);
+            double* R2 = buf(P_R2, m * m);
+            double* R2i = buf(P_R2I, m * m);
+            chol_inv_upper((int)m, G2, R2, R2i, info, pool[P_SMALLWS], st);
+            if (read_int(info)) return false;
+            tall_times_small(src, m, R2i, m, m, dst, n);
+            small_gemm(false, false, (int)m, (int)m, (int)m, 1.0, R2, (int)m, Racc, (int)m, 0.0, Rtmp, (int)m, st);
+            std::swap(Racc, Rtmp);
+            std::swap(src, dst);
+        }
+        if (src != Q) W4_CUDA(cudaMemcpyAsync(Q, src, sizeof(double) * n * m, cudaMemcpyDeviceToDevice, st));
+        if (R_out) W4_CUDA(cudaMemcpyAsync(R_out, Racc, sizeof(double) * m * m, cudaMemcpyDeviceToDevice, st));
         tm.end();
         return true;
     }
@@ -175,7 +227,7 @@ __global__ void square_head_kernel(int k, const double* __restrict__ s, double* 
 }
 
 void rr_core(Ctx& c, const double* Z, int64_t m, int64_t keep, double* U_out, int64_t ldu,
-             double* theta_out) {
+             double* theta_out, double* AZ) {
     const int64_t n = c.n;
     // Gram defect check (randevd.cpp:50-52)
     c.tm.begin(T_GEMM);
@@ -188,7 +240,6 @@ void rr_core(Ctx& c, const double* Z, int64_t m, int64_t keep, double* U_out, in
     W4_CUDA(cudaStreamSynchronize(c.st));
     c.tm.end();
     if (!(hd <= 1e-8)) throw NumericalError("rayleigh_ritz: Z is not orthonormal");
-    double* AZ = c.buf(P_AZ, n * m);
     c.apply(Z, m, AZ);  // second block product
     c.tm.begin(T_GEMM);
     double* K = c.buf(P_K, m * m);
@@ -228,12 +279,12 @@ void clustered_spectrum_dev(wc4dvar_op& op, const double* Wobs, int64_t q, const
     if (r == 0) throw NumericalError("clustered_spectrum: observation range and LMP vectors are zero");
     double* Q = c.buf(P_Z, n * m);
     if (r == m) {
-        if (!c.cholqr2(B, m, Q, nullptr, G))
+        if (!c.orth(B, m, Q, nullptr, G, c.buf(P_Q1, n * m)))
             throw NumericalError("clustered_spectrum: basis too ill-conditioned for CholQR2");
     } else {
         double* Bp = c.buf(P_SEL, n * m);
         gather_cols(n, r, B, n, perm, Bp, n, st);
-        if (!c.cholqr2(Bp, r, Q, nullptr, nullptr))
+        if (!c.orth(Bp, r, Q, nullptr, nullptr, c.buf(P_Q1, n * m)))
             throw NumericalError("clustered_spectrum: basis too ill-conditioned for CholQR2");
         const int64_t e = m - r;
         std::vector<double> hz((size_t)n * e);
@@ -255,7 +306,7 @@ void clustered_spectrum_dev(wc4dvar_op& op, const double* Wobs, int64_t q, const
             gp.add = ColMap::plain(Z, n);
             gemm_nn(&gp, 1, nullptr, st);
         }
-        if (!c.cholqr2(Z, e, Q + n * r, nullptr, nullptr))
+        if (!c.orth(Z, e, Q + n * r, nullptr, nullptr, c.buf(P_Q1, n * m)))
             throw NumericalError("clustered_spectrum: completion basis breakdown");
         W4_CUDA(cudaStreamSynchronize(st));  // hz is released on return
     }
@@ -302,7 +353,7 @@ void rayleigh_ritz_dev(wc4dvar_op& op, const double* Z, int64_t ldz, int64_t m, 
     require(ldz == op.dim, "rayleigh_ritz: Z must be contiguous (ld = dim)");
     Timer tm(st, false);
     Ctx c{op, st, op.dim, tm, op.pool, op.h_int};
-    rr_core(c, Z, m, m, U_out, ldu, theta_out);
+    rr_core(c, Z, m, m, U_out, ldu, theta_out, c.buf(P_AZ, op.dim * m));
 }
 
 int64_t sketch_dev(wc4dvar_op& op, const wc4dvar_sketch_config& cfg, const double* omega,
@@ -320,9 +371,16 @@ int64_t sketch_dev(wc4dvar_op& op, const wc4dvar_sketch_config& cfg, const doubl
     Ctx c{op, st, n, tm, op.pool, op.h_int};
     int64_t produced = 0;
 
+    // Memory plan (SURVEY §7 hard part 7): besides the caller's Omega and U and the
+    // operator's apply workspace, a sketch holds TWO n x m blocks (bufA, bufB): the
+    // orthonormalisations run with Q aliasing their input and the other block as scratch,
+    // and each block product writes into whichever block is dead.  C4 at m = 256:
+    // Omega + 2 blocks + workspace + U = 4.5 x 34.8 GB.
+    double* bufA = c.buf(P_Y, n * m);
+    double* bufB = c.buf(P_Z, n * m);
     if (cfg.method == WC4DVAR_SKETCH_REVD) {
         // randevd.cpp:62-80
-        double* Y = c.buf(P_Y, n * m);
+        double* Y = bufA;
         c.apply(omega, m, Y);
         tm.begin(T_GEMM);
         double* G = c.buf(P_G, m * m);
@@ -334,14 +392,14 @@ int64_t sketch_dev(wc4dvar_op& op, const wc4dvar_sketch_config& cfg, const doubl
             msg << "revd: sample matrix rank collapsed to " << r << " of " << m << " columns";
             throw NumericalError(msg.str());
         }
-        double* Z = c.buf(P_Z, n * m);
-        if (!c.cholqr2(Y, m, Z, nullptr, G))
+        double* Z = bufA;  // householder_q(Y), randevd.cpp:74
+        if (!c.orth(Y, m, Z, nullptr, G, bufB))
             throw NumericalError("revd: sample matrix is numerically rank deficient (CholQR breakdown)");
-        rr_core(c, Z, m, k, U_out, ldu, theta_out);
+        rr_core(c, Z, m, k, U_out, ldu, theta_out, bufB);
         produced = k;
     } else if (cfg.method == WC4DVAR_SKETCH_NYSTROM) {
         // randevd.cpp:82-114
-        double* Y = c.buf(P_Y, n * m);
+        double* Y = bufA;
         c.apply(omega, m, Y);
         tm.begin(T_GEMM);
         double* G = c.buf(P_G, m * m);
@@ -349,16 +407,16 @@ int64_t sketch_dev(wc4dvar_op& op, const wc4dvar_sketch_config& cfg, const doubl
         int* perm = nullptr;
         const int r = c.rank_probe(G, m, &perm);
         if (r == 0) throw NumericalError("nystrom: sample matrix is zero");
-        double* Z = c.buf(P_Z, n * m);
-        const double* Ysrc = Y;
-        if (r < m) {
-            double* Ysel = c.buf(P_SEL, n * r);
-            gather_cols(n, r, Y, n, perm, Ysel, n, st);
-            Ysrc = Ysel;
+        double* Z = bufA;
+        double* other = bufB;
+        if (r < m) {  // the r pivot columns span the kept subspace (randevd.cpp:89-92)
+            gather_cols(n, r, Y, n, perm, bufB, n, st);
+            Z = bufB;
+            other = bufA;
         }
-        if (!c.cholqr2(Ysrc, r, Z, nullptr, r < m ? nullptr : G))
+        if (!c.orth(Z, r, Z, nullptr, r < m ? nullptr : G, other))
             throw NumericalError("nystrom: sample matrix is numerically rank deficient (CholQR breakdown)");
-        double* E1 = c.buf(P_AZ, n * r);
+        double* E1 = other;
         c.apply(Z, r, E1);
         tm.begin(T_GEMM);
         double* E2 = c.buf(P_K, r * r);
@@ -374,11 +432,10 @@ int64_t sketch_dev(wc4dvar_op& op, const wc4dvar_sketch_config& cfg, const doubl
                 "indefinite. Increase the oversampling parameter or use revd for indefinite "
                 "spectra.");
         tm.begin(T_GEMM);
-        double* F = c.buf(P_F, n * r);
+        double* F = Z;  // Z is dead once E2 exists
         c.tall_times_small(E1, r, Rui, r, r, F, n);  // F = E1 U^{-1}, randevd.cpp:104-105
-        double* QF = c.buf(P_Y, n * r);              // Y no longer needed
         double* RF = c.buf(P_R, r * r);
-        if (!c.cholqr2(F, r, QF, RF, nullptr))
+        if (!c.orth(F, r, F, RF, nullptr, E1))
             throw NumericalError("nystrom: factor F is numerically rank deficient (CholQR breakdown)");
         tm.begin(T_SMALL);
         double* sig = c.buf(P_VALS, r);
@@ -386,26 +443,27 @@ int64_t sketch_dev(wc4dvar_op& op, const wc4dvar_sketch_config& cfg, const doubl
         svd_left_desc((int)r, RF, sig, W, op.pool[P_SMALLWS], st);
         const int64_t keep = std::min<int64_t>(k, r);
         tm.begin(T_GEMM);
-        c.tall_times_small(QF, r, W, r, keep, U_out, ldu);
+        c.tall_times_small(F, r, W, r, keep, U_out, ldu);
         square_head_kernel<<<1, 512, 0, st>>>((int)keep, sig, theta_out);
         W4_LAUNCH();
         tm.end();
         produced = keep;
     } else if (cfg.method == WC4DVAR_SKETCH_RITZIT) {
         // randevd.cpp:116-136 (+ p_iter EXTENSION)
-        double* G3 = c.buf(P_Z, n * m);
-        if (!c.cholqr2(omega, m, G3, nullptr, nullptr))
+        double* G3 = bufA;
+        if (!c.orth(omega, m, G3, nullptr, nullptr, bufB))
             throw NumericalError("revd_ritzit: Gaussian sample is numerically rank deficient");
-        double* Y3 = c.buf(P_Y, n * m);
+        double* Y3 = bufB;
         c.apply(G3, m, Y3);
         for (int it = 1; it < std::max(cfg.p_iter, 1); ++it) {
-            if (!c.cholqr2(Y3, m, G3, nullptr, nullptr))
+            if (!c.orth(Y3, m, Y3, nullptr, nullptr, G3))
                 throw NumericalError("revd_ritzit: QR of the sample matrix is rank deficient");
+            std::swap(G3, Y3);  // the basis now lives in the old Y3 block
             c.apply(G3, m, Y3);
         }
-        double* Z3 = c.buf(P_Z, n * m);
+        double* Z3 = Y3;
         double* R3 = c.buf(P_R, m * m);
-        if (!c.cholqr2(Y3, m, Z3, R3, nullptr))
+        if (!c.orth(Y3, m, Z3, R3, nullptr, G3))
             throw NumericalError("revd_ritzit: QR of the sample matrix is rank deficient");
         // min |R_ii| <= 1e-14 max |R_ii| (randevd.cpp:125-127)
         std::vector<double> hR(m * m);

@@ -125,6 +125,8 @@ SIGNATURES = {
                                                    ctypes.c_double, _dp, _dp, _i64, ctypes.c_int]),
     "wc4dvar_gpu_sketch": (ctypes.c_int, [_vp, ctypes.POINTER(SketchDesc), _dp, _dp, _i64, _dp,
                                           ctypes.POINTER(_i64)]),
+    "wc4dvar_gpu_launch_count": (ctypes.c_int64, []),
+    "wc4dvar_gpu_op_release_workspaces": (ctypes.c_int, [_vp]),
     "wc4dvar_gpu_gaussian_block_dev": (ctypes.c_int, [_i64, _i64, _i64, _i64, _i64, ctypes.c_uint64, _vp, _i64,
                                                       ctypes.c_int, _vp]),
     "wc4dvar_gpu_mt19937_raw_dev": (ctypes.c_int, [ctypes.c_uint64, ctypes.c_uint64, _i64, _vp, ctypes.c_int, _vp]),
@@ -228,6 +230,11 @@ def gaussian_matrix(rows: int, cols: int, seed: int) -> np.ndarray:
 # ---------------------------------------------------------------------------
 # Descriptors (models.hpp, covariance.hpp, operators.hpp)
 # ---------------------------------------------------------------------------
+def launch_count() -> int:
+    """Kernel launches issued by the library so far (wc4dvar_gpu_launch_count)."""
+    return int(lib.wc4dvar_gpu_launch_count())
+
+
 def gaussian_block_dev(out, n_total: int, seed: int, row0: int = 0, col0: int = 0, stream=None) -> None:
     """Device NormalStream with jump-ahead (wc4dvar_gpu_gaussian_block_dev): fills the torch
     CUDA tensor ``out`` (shape (cols, rows), row j = column col0 + j of the column-major
@@ -427,6 +434,10 @@ class LinearOperator:
         _check(lib.wc4dvar_gpu_op_apply_block(self._h, _p(V), V.shape[0], V.shape[1], _p(out),
                                               out.shape[0]))
         return out
+
+    def release_workspaces(self) -> None:
+        """Free the operator's grow-only device workspaces (wc4dvar_gpu_op_release_workspaces)."""
+        _check(lib.wc4dvar_gpu_op_release_workspaces(self._h))
 
     def profile(self, enable: bool = True) -> None:
         _check(lib.wc4dvar_gpu_op_profile(self._h, int(enable)))
@@ -666,6 +677,20 @@ def sketch_eigenpairs(op: LinearOperator, cfg: SketchConfig, omega: Optional[np.
     return RitzPairs(U[:, :k].copy(order="F"), th[:k].copy(), cfg.method if cfg.method != "ritzit" else "ritzit")
 
 
+def sketch_eigenpairs_dev(op: LinearOperator, cfg: SketchConfig, omega, U, theta, stream=None) -> int:
+    """Device-resident sketch_eigenpairs (wc4dvar_gpu_sketch_dev) on torch CUDA tensors in the
+    (columns, rows) layout: omega (k+l, dim), U (>= k, dim), theta (>= k).  Returns the number
+    of pairs written (Nystrom caps it at the detected rank)."""
+    d = cfg._desc()
+    n = op.dim()
+    require(tuple(omega.shape) == (cfg.sample_size(), n) and omega.stride(1) == 1, "sketch: omega shape mismatch")
+    require(U.shape[1] == n and U.shape[0] >= cfg.target_rank and U.stride(1) == 1, "sketch: U shape mismatch")
+    kout = _i64(0)
+    _check(lib.wc4dvar_gpu_sketch_dev(op.handle, ctypes.byref(d), omega.data_ptr(), U.data_ptr(), U.stride(0),
+                                      theta.data_ptr(), ctypes.byref(kout), None if stream is None else stream))
+    return kout.value
+
+
 def revd(op, cfg, omega=None):
     """randevd.cpp:62-80."""
     return sketch_eigenpairs(op, SketchConfig(cfg.target_rank, cfg.oversample, cfg.seed, "revd", cfg.p_iter), omega)
@@ -762,6 +787,17 @@ def build_spectral_lmp(pairs: RitzPairs, device: int = 0) -> LmpFactor:
     _check(lib.wc4dvar_gpu_lmp_build(U.shape[0], len(th), _p(U) if len(th) else None, U.shape[0],
                                      _p(th) if len(th) else None, device, ctypes.byref(h)))
     return LmpFactor(h, U.shape[0], U, th)
+
+
+def build_spectral_lmp_dev(U, theta, k: int, device: int = 0) -> LmpFactor:
+    """build_spectral_lmp (lmp.cpp:35-52) from device-resident Ritz pairs: torch CUDA tensors
+    U (>= k, dim) (row j = vector j) and theta (>= k); the factor copies them."""
+    n = U.shape[1]
+    require(U.stride(1) == 1, "build_spectral_lmp: U rows must be contiguous")
+    h = _vp()
+    _check(lib.wc4dvar_gpu_lmp_build_dev(n, k, U.data_ptr() if k else None, U.stride(0),
+                                         theta.data_ptr() if k else None, device, ctypes.byref(h)))
+    return LmpFactor(h, n, None, np.zeros(k))
 
 
 # ---------------------------------------------------------------------------
