@@ -562,6 +562,9 @@ class HessianOperator(LinearOperator):
         self.threads = threads
         self._keep = []
         self._fft = {}
+        # fast = True routes apply / apply_block through apply_block_fast (batched D^{1/2}:
+        # BLAS GEMM or real FFT); the default per-column C path is the reference's loop order.
+        self.fast = False
 
         def keep(a, dtype=np.float64):
             a = np.ascontiguousarray(a, dtype=dtype)
@@ -614,6 +617,8 @@ class HessianOperator(LinearOperator):
         return self._call("apply_D_half_inv", v)
 
     def _apply(self, v):
+        if self.fast:
+            return self.apply_block_fast(v.reshape(-1, 1), self.threads, count=False)[:, 0]
         out = np.empty_like(v)
         st = _lib.orc_hessian_apply(ctypes.byref(self._h), _ptr(v), _ptr(out))
         if st:
@@ -621,6 +626,8 @@ class HessianOperator(LinearOperator):
         return out
 
     def apply_block(self, V, threads: Optional[int] = None):
+        if self.fast:
+            return self.apply_block_fast(V, threads)
         V = np.asfortranarray(V, dtype=np.float64)
         require(V.shape[0] == self.dim(), "LinearOperator::apply_block: dimension mismatch")
         out = np.empty_like(V, order="F")
@@ -666,7 +673,7 @@ class HessianOperator(LinearOperator):
             out = scipy.fft.irfft(F, n=n, axis=1, workers=w).T
         return out.reshape((n * (N + 1), m), order="F")
 
-    def apply_block_fast(self, V, threads: Optional[int] = None) -> np.ndarray:
+    def apply_block_fast(self, V, threads: Optional[int] = None, count: bool = True) -> np.ndarray:
         """HessianOperator::apply (operators.cpp:127-144) on a block, batched for the CPU
         baseline: D^{1/2} of the whole block (apply_D_half_block), then the per-column
         sweeps L^{-T} H^T R^{-1} H L^{-1} in C with the apply_block column fan-out
@@ -675,7 +682,8 @@ class HessianOperator(LinearOperator):
         V = np.asfortranarray(V, dtype=np.float64)
         require(V.shape[0] == self.dim(), "LinearOperator::apply_block: dimension mismatch")
         m = V.shape[1]
-        self._applies += m
+        if count:
+            self._applies += m
         if m == 0:
             return np.empty_like(V, order="F")
         w = threads or self.threads or 1
