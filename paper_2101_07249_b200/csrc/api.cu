@@ -458,7 +458,13 @@ int wc4dvar_gpu_clustered_spectrum(wc4dvar_op* op, const wc4dvar_lmp* precond, c
     }
     if (precond && k) W4_CUDA(cudaStreamSynchronize(precond->stream));  // U / T built on the LMP stream
     double* vals = op->out_buf.get<double>((size_t)std::max<int64_t>(q + k, 1));
-    clustered_spectrum_dev(*op, W, q, precond ? precond->U : nullptr, k, precond ? precond->T : nullptr, vals, st);
+    double* Ucol = nullptr;  // the spectrum's tall GEMMs take U column-major
+    if (k) {
+        W4_CUDA(cudaMallocAsync(&Ucol, sizeof(double) * n * k, st));
+        lmp_unblock_U(n, (int)k, precond->U, Ucol, n, st);
+    }
+    clustered_spectrum_dev(*op, W, q, Ucol, k, precond ? precond->T : nullptr, vals, st);
+    if (Ucol) W4_CUDA(cudaFreeAsync(Ucol, st));
     W4_CUDA(cudaMemcpyAsync(nonunit, vals, sizeof(double) * (q + k), cudaMemcpyDeviceToHost, st));
     W4_CUDA(cudaStreamSynchronize(st));
     *n_nonunit = q + k;
@@ -688,14 +694,26 @@ static int lmp_build_impl(int64_t n, int64_t k, const double* U, int64_t ldu, co
         m << "build_spectral_lmp: nonpositive Ritz value " << mn;
         throw NumericalError(m.str());
     }
-    W4_CUDA(cudaMalloc(&f->U, sizeof(double) * n * k));
+    // U is kept in the row-tile blocked layout of the PCG row passes (lmp_block_U); a
+    // column-major device copy (the caller's, or a staging upload) feeds U^T U and the
+    // blocking kernel.
+    W4_CUDA(cudaMalloc(&f->U, sizeof(double) * lmp_blocked_size(n, (int)k)));
     W4_CUDA(cudaMalloc(&f->theta, sizeof(double) * k));
     W4_CUDA(cudaMalloc(&f->T, sizeof(double) * k * k));
-    W4_CUDA(cudaMemcpy2DAsync(f->U, n * 8, U, ldu * 8, n * 8, k,
-                              dev_ptrs ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, st));
+    const double* Ucol = U;
+    int64_t ldc = ldu;
+    double* staged = nullptr;
+    if (!dev_ptrs) {
+        W4_CUDA(cudaMallocAsync(&staged, sizeof(double) * n * k, st));
+        W4_CUDA(cudaMemcpy2DAsync(staged, n * 8, U, ldu * 8, n * 8, k, cudaMemcpyHostToDevice, st));
+        Ucol = staged;
+        ldc = n;
+    }
+    lmp_block_U(n, (int)k, Ucol, ldc, f->U, st);
     W4_CUDA(cudaMemcpyAsync(f->theta, th.data(), sizeof(double) * k, cudaMemcpyHostToDevice, st));
     double* S = f->tmp.get<double>((size_t)k * k + 1);
-    gemm_tn(n, k, k, f->U, n, f->U, n, 1.0, S, k, f->partial, st);
+    gemm_tn(n, k, k, Ucol, ldc, Ucol, ldc, 1.0, S, k, f->partial, st);
+    if (staged) W4_CUDA(cudaFreeAsync(staged, st));
     double* dd = S + k * k;
     defect_max((int)k, S, dd, st);
     double defect = 0;
@@ -749,8 +767,9 @@ int wc4dvar_gpu_lmp_apply(wc4dvar_lmp* f, int transpose, const double* v, double
     c.k = f->k;
     c.U = f->U;
     c.ldu = n;
+    c.blk_rb = lmp_tile_rows(f->k);
     c.T = f->T;
-    c.partial = f->partial.get<double>((size_t)(cdiv(n, 32) + 1) * (f->k + 1));
+    c.partial = f->partial.get<double>((size_t)std::min<int64_t>(cdiv(n, 32) + 1, 2048) * (f->k + 1));
     c.counter = f->counter;
     rowpass_utv(c, dv, nullptr, nullptr, gk, st);
     rowpass_apply(c, transpose != 0, dv, gk, dout, st);

@@ -128,8 +128,8 @@ struct Work {
     }
     // a . b (deterministic row pass) -> host
     double dot(const double* a, const double* b) {
-        const int64_t maxgrid = cdiv(n, 32) + 1;
-        RowPassCtx c{n, 0, nullptr, n, nullptr, part.get<double>((size_t)maxgrid),
+        const int64_t maxgrid = std::min<int64_t>(cdiv(n, 32) + 1, 2048);
+        RowPassCtx c{n, 0, nullptr, n, 0, nullptr, part.get<double>((size_t)maxgrid),
                      cnt.get<unsigned>(4), scal.get<double>(SC_N), nullptr, nullptr};
         W4_CUDA(cudaMemsetAsync(c.counter, 0, 4 * sizeof(unsigned), st));
         double* out = scal.get<double>(SC_N) + SC_N - 1;

@@ -1,6 +1,10 @@
 // Compact-WY spectral LMP and fused PCG row passes (see lmp_pcg.cuh).
 #include "lmp_pcg.cuh"
 
+#include <algorithm>
+
+#include "bulk.cuh"
+
 namespace w4 {
 namespace {
 
@@ -26,45 +30,78 @@ struct PassArgs {
     const double* w;
 };
 
-template <int MODE>
-__global__ void __launch_bounds__(kBlock)
-    rowpass_kernel(const RowPassCtx c, const PassArgs A, int RB) {
-    extern __shared__ double sm[];
-    const int k = c.k;
-    const int ks = RB + 1;
-    double* Us = sm;                        // k x (RB+1)
-    double* es = Us + (size_t)k * ks;       // RB
-    double* ys = es + RB;                   // k
-    __shared__ double wred[kBlock / 32];
+// Persistent row-pass kernel: a fixed grid (one CTA per SM) walks the row tiles; each
+// tile's U rows (k column segments of RB contiguous doubles) and its vector segments land in
+// shared memory by cp.async.bulk on an mbarrier, double-buffered, so the next tile streams
+// from HBM while this one computes.  Column dots accumulate in registers across every tile
+// a CTA owns (lane-strided rows, fixed order), so the cross-CTA reduction is over gridDim
+// partials only.  Tiles that are partial or misaligned load with plain cooperative loads.
+constexpr int kRP = 256;
+constexpr int kStageDoubles = 12 * 1024;  // 96 KB per stage (U tile + vector segments)
+
+__host__ __device__ constexpr int nvec_of(int mode) {
+    return mode == M_UTV ? 3 : (mode == M_APPLY || mode == M_APPLY_T) ? 1 : mode == M_P1 ? 2 : mode == M_P2 ? 4 : 2;
+}
+
+template <int MODE, int NACC>
+__global__ void __launch_bounds__(kRP, 1)
+    rowpass_kernel(const RowPassCtx c, const PassArgs A, int RB, int nparts, int bulk) {
+    extern __shared__ __align__(16) double sm[];
+    __shared__ __align__(8) uint64_t bars[2];
+    __shared__ double wred[kRP / 32];
     __shared__ int is_last;
+    constexpr int NV = nvec_of(MODE);
+    const int k = c.k;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int64_t n = c.n;
+    const int64_t ntiles = (n + RB - 1) / RB;
+    const int stage_d = k * RB + NV * RB;
+    double* stg[2] = {sm, sm + stage_d};
+    double* ys = sm + 2 * stage_d;          // k (coefficients of the row dots)
+    double* es = ys + ((k + 1) & ~1);       // RB (per-row values of the column dots)
+    double* rp = es + RB;                   // nparts x RB (row-dot partials)
+    const double* vsrc[4];
+    if (MODE == M_UTV) { vsrc[0] = A.v; vsrc[1] = A.a; vsrc[2] = A.b; vsrc[3] = nullptr; }
+    else if (MODE == M_APPLY || MODE == M_APPLY_T) { vsrc[0] = A.v; vsrc[1] = vsrc[2] = vsrc[3] = nullptr; }
+    else if (MODE == M_P1) { vsrc[0] = A.w; vsrc[1] = A.p; vsrc[2] = vsrc[3] = nullptr; }
+    else if (MODE == M_P2) { vsrc[0] = A.w; vsrc[1] = A.x; vsrc[2] = A.p; vsrc[3] = A.r; }
+    else { vsrc[0] = A.r; vsrc[1] = A.p; vsrc[2] = vsrc[3] = nullptr; }
 
-    const int tid = threadIdx.x;
-    const int64_t row0 = (int64_t)blockIdx.x * RB;
-    const int64_t rem_rows = c.n - row0;
-    const int rows = (int)(rem_rows < RB ? rem_rows : RB);
-
-    // Stage this CTA's U rows once (coalesced per column) with cp.async: every copy of the
-    // thread is in flight at once instead of one L2 round trip per element.
-    for (int e = tid; e < k * RB; e += kBlock) {
-        const int i = e / RB, rr = e % RB;
-        if (rr < rows) {
-            const unsigned d = static_cast<unsigned>(__cvta_generic_to_shared(Us + i * ks + rr));
-            asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(d),
-                         "l"(c.U + row0 + rr + (int64_t)i * c.ldu));
-        } else {
-            Us[i * ks + rr] = 0.0;
+    auto tile_rows = [&](int64_t t) { return (int)min((int64_t)RB, n - t * RB); };
+    auto is_bulk = [&](int64_t t) { return bulk && tile_rows(t) == RB; };
+    // warp 0: arm the stage's barrier and issue the tile's bulk copies
+    auto issue = [&](int64_t t, int s) {
+        if (t >= ntiles || !is_bulk(t)) return;
+        const int64_t row0 = t * RB;
+        int nv = 0;
+#pragma unroll
+        for (int v = 0; v < NV; ++v) nv += vsrc[v] != nullptr;
+        if (lane == 0) {
+            fence_proxy_async_smem();
+            mbar_arrive_expect_tx(&bars[s], (unsigned)(sizeof(double) * RB * (k + nv)));
         }
+        __syncwarp();
+        if (c.blk_rb) {  // the whole tile is one contiguous k x RB block
+            if (lane == 0 && k > 0)
+                bulk_g2s(stg[s], c.U + t * (int64_t)k * RB, (unsigned)(sizeof(double) * RB * k), &bars[s]);
+        } else {
+            for (int i = lane; i < k; i += 32)
+                bulk_g2s(stg[s] + (size_t)i * RB, c.U + row0 + (int64_t)i * c.ldu, sizeof(double) * RB, &bars[s]);
+        }
+        if (lane < NV && vsrc[lane])
+            bulk_g2s(stg[s] + (size_t)(k + lane) * RB, vsrc[lane] + row0, sizeof(double) * RB, &bars[s]);
+    };
+
+    if (tid == 0) {
+        mbar_init(&bars[0], 1);
+        mbar_init(&bars[1], 1);
+        fence_mbar_init();
     }
-    asm volatile("cp.async.wait_all;\n" ::: "memory");
     // Coefficients for the U-apply: APPLY uses op(T) gin, P2 uses T^T g, P3 uses T h.
     if (MODE == M_APPLY || MODE == M_APPLY_T || MODE == M_P2 || MODE == M_P3) {
-        const double* gv = (MODE == M_APPLY || MODE == M_APPLY_T) ? A.gin
-                           : (MODE == M_P2)                     ? c.g
-                                                                : c.h;
+        const double* gv = (MODE == M_APPLY || MODE == M_APPLY_T) ? A.gin : (MODE == M_P2) ? c.g : c.h;
         const bool trans = (MODE == M_APPLY_T || MODE == M_P2);
-        // one warp per coefficient, lanes stride j (independent L2 loads, fixed-order tree)
-        const int warp = tid >> 5, lane = tid & 31;
-        for (int i = warp; i < k; i += kBlock / 32) {
+        for (int i = warp; i < k; i += kRP / 32) {
             double s = 0.0;
             if (trans) {  // (T^T g)_i = sum_{j<=i} T[j,i] g_j
                 for (int j = lane; j <= i; j += 32) s += c.T[j + (int64_t)i * k] * gv[j];
@@ -76,70 +113,112 @@ __global__ void __launch_bounds__(kBlock)
         }
     }
     __syncthreads();
+    if (warp == 0) {
+        issue(blockIdx.x, 0);
+        issue((int64_t)blockIdx.x + gridDim.x, 1);
+    }
+    double alpha = 0.0, beta = 0.0;
+    if (MODE == M_P2) alpha = c.scal[SC_ALPHA];
+    if (MODE == M_P3) beta = c.scal[SC_BETA];
 
+    double acc[NACC > 0 ? NACC : 1];
+#pragma unroll
+    for (int j = 0; j < (NACC > 0 ? NACC : 1); ++j) acc[j] = 0.0;
     double dotc = 0.0;
-    if (tid < RB) {
-        const int rr = tid;
-        const int64_t row = row0 + rr;
-        const bool live = rr < rows;
-        double e = 0.0;
-        if (MODE == M_UTV) {
-            if (live) {
-                e = A.v[row];
-                if (A.a) dotc = A.a[row] * A.b[row];
+    unsigned phase[2] = {0u, 0u};
+    const int part = tid / RB, prow = tid - part * RB;
+
+    for (int64_t it = 0;; ++it) {
+        const int64_t t = blockIdx.x + it * (int64_t)gridDim.x;
+        if (t >= ntiles) break;
+        const int s = (int)(it & 1);
+        const int64_t row0 = t * RB;
+        const int rows = tile_rows(t);
+        double* Us = stg[s];
+        double* Vs = Us + (size_t)k * RB;
+        if (is_bulk(t)) {
+            mbar_wait(&bars[s], phase[s]);
+            phase[s] ^= 1u;
+        } else {
+            for (int e = tid; e < k * RB; e += kRP) {
+                const int i = e / RB, r = e - i * RB;
+                Us[e] = c.blk_rb ? c.U[t * (int64_t)k * RB + e]
+                                 : (r < rows ? c.U[row0 + r + (int64_t)i * c.ldu] : 0.0);
             }
-        } else if (MODE == M_APPLY || MODE == M_APPLY_T) {
-            if (live) {
-                double s = 0.0;
-                for (int i = 0; i < k; ++i) s += Us[i * ks + rr] * ys[i];
-                A.out[row] = A.v[row] - s;
+            for (int e = tid; e < NV * RB; e += kRP) {
+                const int v = e / RB, r = e - v * RB;
+                Vs[e] = (r < rows && vsrc[v]) ? vsrc[v][row0 + r] : 0.0;
             }
-        } else if (MODE == M_P1) {
-            if (live) {
-                e = A.w[row];
-                dotc = A.p[row] * e;
+            __syncthreads();
+        }
+        // ---- row dots s_r = sum_i U[r, i] ys[i] (nparts column ranges, fixed-order combine)
+        if (MODE == M_APPLY || MODE == M_APPLY_T || MODE == M_P2 || MODE == M_P3) {
+            if (part < nparts && prow < rows) {
+                const int i0 = part * k / nparts, i1 = (part + 1) * k / nparts;
+                double sacc = 0.0;
+                for (int i = i0; i < i1; ++i) sacc += Us[(size_t)i * RB + prow] * ys[i];
+                rp[part * RB + prow] = sacc;
             }
-        } else if (MODE == M_P2) {
-            if (live) {
-                const double alpha = c.scal[SC_ALPHA];
-                double s = 0.0;
-                for (int i = 0; i < k; ++i) s += Us[i * ks + rr] * ys[i];
-                const double ctw = A.w[row] - s;          // C^T w
-                A.x[row] = A.x[row] + alpha * A.p[row];   // x += alpha p
-                const double rn = A.r[row] - alpha * ctw; // r -= alpha C^T w
+            __syncthreads();
+        }
+        if (tid < rows) {
+            const int r = tid;
+            const int64_t row = row0 + r;
+            double sr = 0.0;
+            if (MODE == M_APPLY || MODE == M_APPLY_T || MODE == M_P2 || MODE == M_P3)
+                for (int p = 0; p < nparts; ++p) sr += rp[p * RB + r];
+            double e = 0.0;
+            if (MODE == M_UTV) {
+                e = Vs[r];
+                if (vsrc[1]) dotc += Vs[RB + r] * Vs[2 * RB + r];
+            } else if (MODE == M_APPLY || MODE == M_APPLY_T) {
+                A.out[row] = Vs[r] - sr;
+            } else if (MODE == M_P1) {
+                e = Vs[r];                    // w
+                dotc += Vs[RB + r] * e;       // p . w
+            } else if (MODE == M_P2) {
+                const double ctw = Vs[r] - sr;                   // C^T w
+                A.x[row] = Vs[RB + r] + alpha * Vs[2 * RB + r];  // x += alpha p
+                const double rn = Vs[3 * RB + r] - alpha * ctw;  // r -= alpha C^T w
                 A.r[row] = rn;
                 e = rn;
-                dotc = rn * rn;
+                dotc += rn * rn;
+            } else {
+                A.p[row] = (Vs[r] - sr) + beta * Vs[RB + r];  // p = C r + beta p
             }
-        } else if (MODE == M_P3) {
-            if (live) {
-                const double beta = c.scal[SC_BETA];
-                double s = 0.0;
-                for (int i = 0; i < k; ++i) s += Us[i * ks + rr] * ys[i];
-                A.p[row] = (A.r[row] - s) + beta * A.p[row];  // p = C r + beta p
+            if (MODE == M_UTV || MODE == M_P1 || MODE == M_P2) es[r] = e;
+        }
+        if (MODE == M_UTV || MODE == M_P1 || MODE == M_P2) {
+            __syncthreads();
+            // column dots: warp w owns columns w + 8 j, lanes stride the tile's rows
+            for (int r = lane; r < rows; r += 32) {
+                const double er = es[r];
+                const double* ur = Us + (size_t)warp * RB + r;
+#pragma unroll
+                for (int j = 0; j < NACC; ++j)
+                    if (warp + 8 * j < k) acc[j] += ur[(size_t)8 * j * RB] * er;
             }
         }
-        es[rr] = e;
+        __syncthreads();  // stage s and es / rp are free
+        if (warp == 0) issue(t + 2 * (int64_t)gridDim.x, s);
     }
     if (MODE == M_APPLY || MODE == M_APPLY_T || MODE == M_P3) return;
 
-    // Reduction: column i of U against es (fixed order), plus the block dot.
-    double d = warp_sum(dotc);
-    if ((tid & 31) == 0) wred[tid >> 5] = d;
-    __syncthreads();
-    double* part = c.partial + (int64_t)blockIdx.x * (k + 1);
-    // one warp per U column: lanes stride the CTA's rows, then a shuffle tree (fixed order)
-    for (int i = tid >> 5; i < k; i += kBlock / 32) {
-        double s = 0.0;
-        const double* col = Us + i * ks;
-        for (int rr = tid & 31; rr < rows; rr += 32) s += col[rr] * es[rr];
-        s = warp_sum(s);
-        if ((tid & 31) == 0) part[i] = s;
+    // per-CTA partials: column dots (fixed shuffle tree) and the row dot
+    double* partial = c.partial + (int64_t)blockIdx.x * (k + 1);
+#pragma unroll
+    for (int j = 0; j < NACC; ++j) {
+        const int i = warp + 8 * j;
+        const double s = warp_sum(acc[j]);
+        if (i < k && lane == 0) partial[i] = s;
     }
+    const double d = warp_sum(dotc);
+    if (lane == 0) wred[warp] = d;
+    __syncthreads();
     if (tid == 0) {
         double s = 0.0;
-        for (int w = 0; w < kBlock / 32; ++w) s += wred[w];
-        part[k] = s;
+        for (int w = 0; w < kRP / 32; ++w) s += wred[w];
+        partial[k] = s;
     }
     __threadfence();
     __syncthreads();
@@ -148,23 +227,11 @@ __global__ void __launch_bounds__(kBlock)
     if (!is_last) return;
     __threadfence();
     double* res = (MODE == M_UTV) ? A.out : (MODE == M_P1 ? c.g : c.h);
-    // final sums over the CTAs' partials: one warp per entry, lanes stride the CTAs (the
-    // loads of a lane are independent, so they pipeline instead of forming one long chain)
-    // (each lane issues its up-to-8 loads per 256-CTA chunk before summing them in order)
-    for (int i = tid >> 5; i <= k; i += kBlock / 32) {
+    for (int i = warp; i <= k; i += kRP / 32) {
         double s = 0.0;
-        for (unsigned b0 = tid & 31; b0 < gridDim.x; b0 += 256) {
-            double v[8];
-#pragma unroll
-            for (int u = 0; u < 8; ++u) {
-                const unsigned b = b0 + 32 * u;
-                v[u] = b < gridDim.x ? __ldcg(c.partial + (int64_t)b * (k + 1) + i) : 0.0;
-            }
-#pragma unroll
-            for (int u = 0; u < 8; ++u) s += v[u];
-        }
+        for (unsigned b = lane; b < gridDim.x; b += 32) s += __ldcg(c.partial + (int64_t)b * (k + 1) + i);
         s = warp_sum(s);
-        if ((tid & 31) == 0) res[i] = s;
+        if (lane == 0) res[i] = s;
     }
     __syncthreads();
     if (tid == 0) {
@@ -183,25 +250,72 @@ __global__ void __launch_bounds__(kBlock)
 }
 
 int pick_rb(int k) {
-    if (k <= 0) return kBlock;
-    int rb = (int)((160 * 1024 / 8) / k) - 1;
-    if (rb > kBlock) rb = kBlock;
-    rb = (rb / 32) * 32;
-    if (rb < 32) rb = 32;
+    int rb = kStageDoubles / (k + 4);
+    rb = (rb / 16) * 16;
+    if (rb > kRP) rb = kRP;
+    if (rb < 16) rb = 16;
     return rb;
+}
+
+bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
+
+template <int MODE, int NACC>
+void launch_pass_n(const RowPassCtx& c, const PassArgs& a, cudaStream_t st) {
+    const int RB = c.blk_rb ? c.blk_rb : pick_rb(c.k);
+    const int nparts = std::max(1, std::min(c.k > 0 ? c.k : 1, kRP / RB));
+    constexpr int NV = nvec_of(MODE);
+    const size_t smem =
+        sizeof(double) * (2 * ((size_t)c.k * RB + (size_t)NV * RB) + ((c.k + 1) & ~1) + RB + (size_t)nparts * RB);
+    auto kern = rowpass_kernel<MODE, NACC>;
+    static int configured = 0;
+    if (smem > 48 * 1024 && (size_t)configured < smem) {
+        W4_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        configured = (int)smem;
+    }
+    const double* vs[4] = {a.v, a.a, a.b, nullptr};
+    if (MODE == M_P1) { vs[0] = a.w; vs[1] = a.p; vs[2] = nullptr; }
+    if (MODE == M_P2) { vs[0] = a.w; vs[1] = a.x; vs[2] = a.p; vs[3] = a.r; }
+    if (MODE == M_P3) { vs[0] = a.r; vs[1] = a.p; vs[2] = nullptr; }
+    if (MODE == M_APPLY || MODE == M_APPLY_T) { vs[1] = vs[2] = nullptr; }
+    bool bulk = (RB % 2 == 0) && (c.k == 0 || ((c.blk_rb || c.ldu % 2 == 0) && aligned16(c.U)));
+    for (const double* v : vs) bulk = bulk && (v == nullptr || aligned16(v));
+    static int nsm = 0;
+    if (!nsm) {
+        int dev = 0;
+        W4_CUDA(cudaGetDevice(&dev));
+        W4_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
+    }
+    const int64_t ntiles = cdiv(c.n, RB);
+    const int64_t grid = std::max<int64_t>(1, std::min<int64_t>({ntiles, (int64_t)nsm, cdiv(c.n, 32) + 1}));
+    kern<<<(unsigned)grid, kRP, smem, st>>>(c, a, RB, nparts, bulk ? 1 : 0);
+    W4_LAUNCH();
 }
 
 template <int MODE>
 void launch_pass(const RowPassCtx& c, const PassArgs& a, cudaStream_t st) {
     if (c.n == 0) return;
-    const int RB = pick_rb(c.k);
-    const size_t smem = sizeof(double) * ((size_t)c.k * (RB + 1) + RB + c.k);
-    auto kern = rowpass_kernel<MODE>;
-    if (smem + 1024 > 48 * 1024)  // + the kernel's static reduction scratch
-        W4_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    const int64_t grid = cdiv(c.n, RB);
-    kern<<<(unsigned)grid, kBlock, smem, st>>>(c, a, RB);
-    W4_LAUNCH();
+    if (MODE == M_APPLY || MODE == M_APPLY_T || MODE == M_P3) return launch_pass_n<MODE, 0>(c, a, st);
+    const int need = (c.k + 7) / 8;
+    if (need <= 0) return launch_pass_n<MODE, 0>(c, a, st);
+    if (need <= 1) return launch_pass_n<MODE, 1>(c, a, st);
+    if (need <= 2) return launch_pass_n<MODE, 2>(c, a, st);
+    if (need <= 4) return launch_pass_n<MODE, 4>(c, a, st);
+    if (need <= 8) return launch_pass_n<MODE, 8>(c, a, st);
+    if (need <= 16) return launch_pass_n<MODE, 16>(c, a, st);
+    if (need <= 32) return launch_pass_n<MODE, 32>(c, a, st);
+    return launch_pass_n<MODE, 64>(c, a, st);
+}
+
+__global__ void block_U_kernel(int64_t n, int k, int rb, const double* __restrict__ U, int64_t ldu,
+                               double* __restrict__ B, int64_t total, int to_blocked) {
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t tile = e / ((int64_t)k * rb);
+        const int64_t w = e - tile * (int64_t)k * rb;
+        const int64_t i = w / rb, r = w - i * rb;
+        const int64_t row = tile * rb + r;
+        if (to_blocked) B[e] = row < n ? U[row + i * ldu] : 0.0;
+        else if (row < n) const_cast<double*>(U)[row + i * ldu] = B[e];
+    }
 }
 
 __global__ void build_T_kernel(int k, const double* __restrict__ S, const double* __restrict__ th,
@@ -283,6 +397,29 @@ __global__ void defect_kernel(int k, const double* __restrict__ S, double* out) 
 void lmp_build_T(int k, const double* S, const double* theta, double* T, cudaStream_t st) {
     if (k == 0) return;
     build_T_kernel<<<1, 256, 0, st>>>(k, S, theta, T);
+    W4_LAUNCH();
+}
+
+int lmp_tile_rows(int k) { return pick_rb(k); }
+
+int64_t lmp_blocked_size(int64_t n, int k) {
+    const int rb = pick_rb(k);
+    return cdiv(n, rb) * rb * (int64_t)k;
+}
+
+void lmp_block_U(int64_t n, int k, const double* U, int64_t ldu, double* Ublk, cudaStream_t st) {
+    const int64_t total = lmp_blocked_size(n, k);
+    if (!total) return;
+    block_U_kernel<<<(unsigned)std::min<int64_t>(cdiv(total, 256), 8 * kSMs), 256, 0, st>>>(n, k, pick_rb(k), U, ldu,
+                                                                                             Ublk, total, 1);
+    W4_LAUNCH();
+}
+
+void lmp_unblock_U(int64_t n, int k, const double* Ublk, double* U, int64_t ldu, cudaStream_t st) {
+    const int64_t total = lmp_blocked_size(n, k);
+    if (!total) return;
+    block_U_kernel<<<(unsigned)std::min<int64_t>(cdiv(total, 256), 8 * kSMs), 256, 0, st>>>(
+        n, k, pick_rb(k), U, ldu, const_cast<double*>(Ublk), total, 0);
     W4_LAUNCH();
 }
 

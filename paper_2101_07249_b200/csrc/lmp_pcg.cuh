@@ -24,6 +24,7 @@ struct RowPassCtx {
     int k = 0;
     const double* U = nullptr;
     int64_t ldu = 0;
+    int blk_rb = 0;             // > 0: U is row-tile blocked (lmp_block_U with rb = blk_rb)
     const double* T = nullptr;  // k x k upper
     double* partial = nullptr;  // grid x (k+1)
     unsigned* counter = nullptr;
@@ -31,6 +32,14 @@ struct RowPassCtx {
     double* g = nullptr;        // k+1 reduction result
     double* h = nullptr;        // k+1 reduction result
 };
+
+// Row-tile height of the PCG row passes for rank k, and the LMP factor's blocked copy of
+// U: tile t (rows [t rb, (t+1) rb), zero-padded past n) is the contiguous rb x k
+// column-major block at Ublk + t k rb, so a pass streams each tile with ONE bulk copy.
+int lmp_tile_rows(int k);
+int64_t lmp_blocked_size(int64_t n, int k);
+void lmp_block_U(int64_t n, int k, const double* U, int64_t ldu, double* Ublk, cudaStream_t st);
+void lmp_unblock_U(int64_t n, int k, const double* Ublk, double* U, int64_t ldu, cudaStream_t st);
 
 // out[k] = U^T v, out[k] (dot) = a . b (a/b may be NULL -> 0); deterministic.
 void rowpass_utv(const RowPassCtx& c, const double* v, const double* a, const double* b,

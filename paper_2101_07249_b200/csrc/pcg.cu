@@ -103,7 +103,7 @@ void pcg_dev(wc4dvar_op& op, const double* b, wc4dvar_lmp* pre, const double* x0
     double* p = pool[B_P].get<double>(n);
     double* w = pool[B_W].get<double>(n);
     double* tmp = pool[B_TMP].get<double>(n);
-    const int64_t maxgrid = cdiv(n, 32) + 1;
+    const int64_t maxgrid = std::min<int64_t>(cdiv(n, 32) + 1, 2048);
     double* part = pool[B_PART].get<double>((size_t)maxgrid * (k + 1));
     double* scal = pool[B_SCAL].get<double>(SC_N + 2);
     double* g = pool[B_G].get<double>(k + 1);
@@ -125,6 +125,7 @@ void pcg_dev(wc4dvar_op& op, const double* b, wc4dvar_lmp* pre, const double* x0
     c.k = k;
     c.U = pre ? pre->U : nullptr;
     c.ldu = n;
+    c.blk_rb = pre && pre->k ? lmp_tile_rows(pre->k) : 0;
     c.T = pre ? pre->T : nullptr;
     c.partial = part;
     c.counter = counter;
@@ -141,7 +142,7 @@ void pcg_dev(wc4dvar_op& op, const double* b, wc4dvar_lmp* pre, const double* x0
     bool x0_zero = true;
     if (x0) {
         // isZero(0.0): every entry exactly zero (checked on device)
-        rowpass_utv(RowPassCtx{n, 0, nullptr, n, nullptr, part, counter, scal, g, h}, x0, x0, x0,
+        rowpass_utv(RowPassCtx{n, 0, nullptr, n, 0, nullptr, part, counter, scal, g, h}, x0, x0, x0,
                     tmp, st);  // tmp[0] = x0 . x0
         double hv = 0;
         W4_CUDA(cudaMemcpyAsync(&hv, tmp, sizeof(double), cudaMemcpyDeviceToHost, st));
