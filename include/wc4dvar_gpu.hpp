@@ -259,16 +259,53 @@ inline std::unique_ptr<LmpFactor> build_spectral_lmp(const RitzPairs& pairs, int
     return std::unique_ptr<LmpFactor>(new LmpFactor(pairs, device));
 }
 
+// ---------------------------------------------------------------- assimilation.hpp
+// QuadraticCost (assimilation.hpp:82-97, assimilation.cpp:130-150): J(x) = 1/2 |x - D^{-1/2} b|^2
+// + 1/2 sigma_o^-2 |H L^{-1} D^{1/2} x - d|^2, evaluated on the device.  Passed to pcg_split
+// through PcgOptions::cost_eval it records the cost every iteration, as run_inner_loop does
+// with record_cost = true (assimilation.hpp:112, assimilation.cpp:235).
+class QuadraticCost {
+public:
+    QuadraticCost(const HessianOperator& op, const Vector& b, const Vector& d) : dim_(op.dim()) {
+        if ((Index)b.size() != op.dim()) throw std::invalid_argument("QuadraticCost: background length mismatch");
+        if ((Index)d.size() != op.network().q) throw std::invalid_argument("QuadraticCost: innovation length mismatch");
+        check(wc4dvar_gpu_cost_create(op.handle(), b.data(), d.data(), &h_));
+    }
+    ~QuadraticCost() {
+        if (h_) wc4dvar_gpu_cost_destroy(h_);
+    }
+    QuadraticCost(const QuadraticCost&) = delete;
+    QuadraticCost& operator=(const QuadraticCost&) = delete;
+    double operator()(const Vector& x) const {
+        if ((Index)x.size() != dim_) throw std::invalid_argument("QuadraticCost: dimension mismatch");
+        double v = 0.0;
+        check(wc4dvar_gpu_cost_eval(h_, x.data(), &v));
+        return v;
+    }
+    // rhs = D^{-1/2} b + sigma_o^-2 D^{1/2} L^{-T} H^T d (assimilation.cpp:142-146)
+    Vector rhs() const {
+        Vector r((size_t)dim_);
+        check(wc4dvar_gpu_cost_rhs(h_, r.data()));
+        return r;
+    }
+    wc4dvar_cost* handle() const { return h_; }
+
+private:
+    Index dim_;
+    wc4dvar_cost* h_ = nullptr;
+};
+
 // ---------------------------------------------------------------- krylov.hpp
 struct PcgOptions {  // krylov.hpp:32-38
     int max_iter = 100;
     double rel_tol = 1e-6;
     bool reorthogonalize = false;
     bool store_residual_vectors = false;
+    const QuadraticCost* cost_eval = nullptr;  // krylov.hpp:37 (the reference's std::function hook)
 };
 
 struct CgHistory {  // krylov.hpp:17-30
-    std::vector<double> alphas, betas, residual_norms;
+    std::vector<double> alphas, betas, residual_norms, quadratic_costs;
     int iterations = 0;
     bool converged = false;
     std::string stop_reason;
@@ -288,11 +325,12 @@ inline PcgResult pcg_split(const LinearOperator& op, const Vector& b, const LmpF
     if (!x0.empty() && (Index)x0.size() != n)
         throw std::invalid_argument("pcg_split: initial guess dimension mismatch");
     const int mi = opts.max_iter > 0 ? opts.max_iter : 0;
-    std::vector<double> al(mi + 1), be(mi + 1), rn(mi + 2);
+    std::vector<double> al(mi + 1), be(mi + 1), rn(mi + 2), qc(mi + 2);
     wc4dvar_pcg_history h{};
     h.alphas = al.data();
     h.betas = be.data();
     h.residual_norms = rn.data();
+    h.quadratic_costs = qc.data();
     wc4dvar_pcg_options o{};
     o.max_iter = opts.max_iter;
     o.reorthogonalize = opts.reorthogonalize ? 1 : 0;
@@ -301,7 +339,9 @@ inline PcgResult pcg_split(const LinearOperator& op, const Vector& b, const LmpF
     PcgResult r;
     r.x.resize((size_t)n);
     check(wc4dvar_gpu_pcg(op.handle(), b.data(), precond ? precond->handle() : nullptr,
-                          x0.empty() ? nullptr : x0.data(), &o, nullptr, r.x.data(), &h));
+                          x0.empty() ? nullptr : x0.data(), &o, opts.cost_eval ? opts.cost_eval->handle() : nullptr,
+                          r.x.data(), &h));
+    if (opts.cost_eval) r.history.quadratic_costs.assign(qc.begin(), qc.begin() + h.iterations + 1);
     r.history.alphas.assign(al.begin(), al.begin() + h.iterations);
     r.history.betas.assign(be.begin(), be.begin() + h.iterations);
     r.history.residual_norms.assign(rn.begin(), rn.begin() + h.iterations + 1);

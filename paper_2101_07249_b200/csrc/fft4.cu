@@ -573,8 +573,8 @@ __device__ __forceinline__ void item_c(const Job& jb, double2* sm, int p, int ti
     if (jb.status && bad) atomicOr(jb.status, ST_OUT_NONFINITE);
 }
 
-template <class P>
-__global__ void __launch_bounds__(kThreads, kCtaPerSm) fftconv_kernel(const Job jb) {
+template <class P, int CPS>
+__global__ void __launch_bounds__(kThreads, CPS) fftconv_kernel(const Job jb) {
     extern __shared__ double2 sm[];
     __shared__ unsigned s_ticket;
     // a ticket covers `sub` consecutive tiles (A / C) or row blocks (B) of one pair: fewer
@@ -635,11 +635,15 @@ __global__ void __launch_bounds__(kThreads, kCtaPerSm) fftconv_kernel(const Job 
     }
     for (;;) {
         if (threadIdx.x == 0) {
-            if (dep)
+            if (dep) {
                 while (seen < need) {
                     __nanosleep(64);
                     seen = ld_relaxed(dep);
                 }
+                // acquire: pairs with the producers' red.release, so the Y lines they wrote
+                // are visible to this CTA's loads after the barrier below
+                asm volatile("fence.acq_rel.gpu;" ::: "memory");
+            }
             s_ticket = next;
         }
         // Y is written with st.cg, published by red.release and read with ld.cg (L2, the
@@ -693,24 +697,37 @@ constexpr size_t smem_bytes() {
     return sizeof(double2) * (size_t)std::max(ColView<P::N2, P::TC>::SMEM, RowView<P::N1, P::S>::SMEM);
 }
 
-template <class P>
-void launch(const Job& jb, cudaStream_t st) {
+template <class P, int CPS>
+void launch_cps(const Job& jb, cudaStream_t st) {
     constexpr size_t sm = smem_bytes<P>();
-    static_assert(sm <= 227 * 1024 / kCtaPerSm, "fftconv tile exceeds the per-CTA SMEM budget");
+    static_assert(sm <= 227 * 1024 / 2, "fftconv tile exceeds the per-CTA SMEM budget");
     static bool attr = false;
     if (!attr) {
-        W4_CUDA(cudaFuncSetAttribute(fftconv_kernel<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+        W4_CUDA(cudaFuncSetAttribute(fftconv_kernel<P, CPS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
         attr = true;
     }
     int dev = 0, nsm = kSMs, occ = 0;
     W4_CUDA(cudaGetDevice(&dev));
     W4_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
-    W4_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fftconv_kernel<P>, kThreads, sm));
+    W4_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fftconv_kernel<P, CPS>, kThreads, sm));
     const int64_t items = (int64_t)(jb.ngroups + 2) * jb.G *
                           (2 * ((P::N1 / P::TC + jb.sub - 1) / jb.sub) + (P::N2 / P::S + jb.sub - 1) / jb.sub);
     const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(items, (int64_t)nsm * std::max(occ, 1)));
-    fftconv_kernel<P><<<grid, kThreads, sm, st>>>(jb);
+    fftconv_kernel<P, CPS><<<grid, kThreads, sm, st>>>(jb);
     W4_LAUNCH();
+}
+
+// WC4DVAR_FFT_CPS: register budget as CTAs per SM (1: ~250 registers, no spills; 2: 128
+// registers (default); 3: ~104 registers)
+template <class P>
+void launch(const Job& jb, cudaStream_t st) {
+    static const int cps = [] {
+        const char* e = std::getenv("WC4DVAR_FFT_CPS");
+        return e ? std::atoi(e) : kCtaPerSm;
+    }();
+    if (cps == 1) return launch_cps<P, 1>(jb, st);
+    if (cps == 3) return launch_cps<P, 3>(jb, st);
+    return launch_cps<P, 2>(jb, st);
 }
 
 struct PlanInfo {

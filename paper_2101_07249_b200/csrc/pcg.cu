@@ -10,6 +10,7 @@
 #include <sstream>
 #include <vector>
 
+#include "gemm.cuh"
 #include "lmp_pcg.cuh"
 
 namespace w4 {
@@ -21,29 +22,6 @@ __global__ void reorth_fix_kernel(double* scal, const double* h, int k) {
     scal[SC_RHO_NEXT] = rn;
     scal[SC_BETA] = rn / scal[SC_DOT];
     scal[SC_RHO] = rn;
-}
-
-__global__ void dot_kernel(int64_t n, const double* __restrict__ a, const double* __restrict__ b,
-                           double* out) {
-    __shared__ double red[32];
-    double s = 0.0;
-    for (int64_t i = threadIdx.x; i < n; i += blockDim.x) s += a[i] * b[i];
-    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = s;
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        double t = 0.0;
-        for (unsigned w = 0; w < blockDim.x / 32; ++w) t += red[w];
-        *out = t;
-    }
-}
-
-__global__ void axpy_dev_kernel(int64_t n, const double* __restrict__ coef, double sign,
-                                const double* __restrict__ f, double* __restrict__ r) {
-    const double c = sign * (*coef);
-    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
-         i += (int64_t)gridDim.x * blockDim.x)
-        r[i] -= c * f[i];
 }
 
 __global__ void scale_copy_kernel(int64_t n, const double* __restrict__ r, const double* rho,
@@ -97,7 +75,7 @@ void pcg_dev(wc4dvar_op& op, const double* b, wc4dvar_lmp* pre, const double* x0
     const int64_t n = op.dim;
     const int k = pre ? pre->k : 0;
     require(!pre || pre->k == 0 || pre->n == n, "pcg_split: preconditioner dimension mismatch");
-    enum { B_R = 0, B_P, B_W, B_TMP, B_PART, B_SCAL, B_G, B_H, B_F, B_CNT };
+    enum { B_R = 0, B_P, B_W, B_TMP, B_PART, B_SCAL, B_G, B_H, B_F, B_CNT, B_GWS, B_HF };
     DevBuf* pool = op.pool + 20;  // pool[0..19] belong to the sketch workspaces
     double* r = pool[B_R].get<double>(n);
     double* p = pool[B_P].get<double>(n);
@@ -114,8 +92,19 @@ void pcg_dev(wc4dvar_op& op, const double* b, wc4dvar_lmp* pre, const double* x0
     double* F = nullptr;
     // CgHistory::normalized_residuals are kept for re-orthogonalisation or on request
     // (krylov.cpp:30)
-    if (opts.reorthogonalize || opts.store_residual_vectors)
+    if (opts.reorthogonalize || opts.store_residual_vectors) {
+        // the n x (max_iter + 1) residual store must fit beside the operator's workspaces
+        size_t free_b = 0, total_b = 0;
+        W4_CUDA(cudaMemGetInfo(&free_b, &total_b));
+        const double need = 8.0 * (double)n * (double)(opts.max_iter + 1);
+        if (need > 0.9 * (double)(free_b + pool[B_F].bytes)) {
+            std::ostringstream m;
+            m << "pcg_split: the stored residual basis (" << need / 1e9 << " GB for " << opts.max_iter + 1
+              << " vectors of " << n << ") does not fit in device memory; lower max_iter";
+            throw InvalidArgument(m.str());
+        }
         F = pool[B_F].get<double>((size_t)n * (opts.max_iter + 1));
+    }
     const bool reorth = opts.reorthogonalize != 0;
     static thread_local double* pinned = nullptr;
     if (!pinned) W4_CUDA(cudaMallocHost(&pinned, 16 * sizeof(double)));
@@ -352,14 +341,25 @@ void pcg_dev(wc4dvar_op& op, const double* b, wc4dvar_lmp* pre, const double* x0
             pcg_pass2(c, x, r, p, w, st);  // x, r, rho_next, beta
         }
         if (!graph_it && reorth) {
-            // modified Gram-Schmidt against the stored normalised residuals (krylov.cpp:71-74)
-            double* dd = scal + SC_N;
-            for (int f = 0; f < nf; ++f) {
-                dot_kernel<<<1, 1024, 0, st>>>(n, F + (int64_t)f * n, r, dd);
-                axpy_dev_kernel<<<(unsigned)std::min<int64_t>(cdiv(n, 256), 1184), 256, 0, st>>>(
-                    n, dd, 1.0, F + (int64_t)f * n, r);
+            // re-orthogonalisation against the stored normalised residuals (krylov.cpp:71-74):
+            // the reference's modified Gram-Schmidt becomes classical Gram-Schmidt applied
+            // twice (CGS2, as stable as MGS) -- per pass one DMMA Gram h = F^T r and one
+            // DMMA update r -= F h over the whole n x nf store, instead of 2 nf launches
+            double* hf = pool[B_HF].get<double>((size_t)nf + 1);
+            for (int pass = 0; pass < 2 && nf > 0; ++pass) {
+                gemm_tn(n, nf, 1, F, n, r, n, 1.0, hf, nf, pool[B_GWS], st);
+                GemmPass gp;
+                gp.A = F;
+                gp.lda = n;
+                gp.M = n;
+                gp.K = nf;
+                gp.ncols = 1;
+                gp.alpha = -1.0;
+                gp.in = ColMap::plain(hf, nf);
+                gp.out = ColMap::plain(r, n);
+                gp.add = ColMap::plain(r, n);
+                gemm_nn(&gp, 1, nullptr, st);
             }
-            W4_LAUNCH();
             rowpass_utv(c, r, r, r, h, st);
             reorth_fix_kernel<<<1, 1, 0, st>>>(scal, h, k);
             W4_LAUNCH();

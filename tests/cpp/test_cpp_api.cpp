@@ -163,6 +163,24 @@ static void test_hessian_vs_oracle() {
     const ClusteredSpectrum cs = clustered_spectrum(op);
     CHECK(cs.unit_multiplicity == op.dim() - net.q);
     CHECK(cs.min_eigenvalue() >= 1.0 - 1e-12);
+    // QuadraticCost recorded every PCG iteration (record_cost, assimilation.hpp:112,
+    // assimilation.cpp:235): the cost of the CG iterates never increases (test_krylov.cpp:100-115)
+    Vector bg((size_t)op.dim()), d((size_t)net.q);
+    orc_gaussian_matrix(op.dim(), 1, 21, bg.data());
+    orc_gaussian_matrix(net.q, 1, 22, d.data());
+    const QuadraticCost J(op, bg, d);
+    PcgOptions co;
+    co.max_iter = 40;
+    co.rel_tol = 1e-10;
+    co.cost_eval = &J;
+    const PcgResult pr = pcg_split(op, J.rhs(), nullptr, {}, co);
+    CHECK(pr.history.quadratic_costs.size() == (size_t)pr.history.iterations + 1);
+    bool mono = true;
+    for (size_t j = 1; j < pr.history.quadratic_costs.size(); ++j)
+        mono = mono && pr.history.quadratic_costs[j] <= pr.history.quadratic_costs[j - 1] * (1 + 1e-12);
+    CHECK(mono);
+    CHECK(std::fabs(J(pr.x) - pr.history.quadratic_costs.back()) <= 1e-12 * std::fabs(J(pr.x)));
+    CHECK(throws_as<std::invalid_argument>([&] { QuadraticCost bad(op, bg, Vector(3)); }));
 }
 
 static void test_sketches_and_pcg() {

@@ -28,6 +28,11 @@ void run(int warps_per_sm) {
     const int threads = 32 * warps_per_sm;  // one block per SM
     const int iters = 4096;
     k<CH><<<148, threads>>>(64, sink);
+    if (cudaDeviceSynchronize() != cudaSuccess || cudaGetLastError() != cudaSuccess) {
+        printf("warps/SM %2d chains %2d : launch failed\n", warps_per_sm, CH);
+        cudaFree(sink);
+        return;
+    }
     cudaEvent_t e0, e1;
     cudaEventCreate(&e0);
     cudaEventCreate(&e1);
@@ -35,6 +40,14 @@ void run(int warps_per_sm) {
     k<CH><<<148, threads>>>(iters, sink);
     cudaEventRecord(e1);
     cudaEventSynchronize(e1);
+    // a launch that does not fit (registers x threads) fails without running: report it
+    // instead of dividing the flop count by a zero-length interval
+    const cudaError_t err = cudaGetLastError();
+    if (err != cudaSuccess) {
+        printf("warps/SM %2d chains %2d : launch failed (%s)\n", warps_per_sm, CH, cudaGetErrorString(err));
+        cudaFree(sink);
+        return;
+    }
     float ms;
     cudaEventElapsedTime(&ms, e0, e1);
     const double flops = 148.0 * warps_per_sm * iters * CH * 2.0 * 16 * 8 * 4;
