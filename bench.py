@@ -410,14 +410,17 @@ def run_configs(W, configs, fp64_peak, hbm_peak):
 
 def run_lmp(W, configs, dev):
     """LMP build ms (Omega resident on the device -> U, Theta on the device; second, warm call)
-    per method, and LMP-PCG time-to-solution to relative residual 1e-6 (krylov.cpp:22-99)."""
+    per method, and LMP-PCG time-to-solution to relative residual 1e-6 (krylov.cpp:22-99).
+    C5_k64 is BASELINE configs[4]'s inner loop on ONE GPU with a 64-column Nystrom / REVD
+    sketch (the k = 256 sketch needs 4 x 86 GB blocks: the 8-GPU configuration)."""
     import numpy as np
     import torch
     res = {}
     for name, mk, pcg_methods, max_iter in (
             ("C2", configs.config2, ("none", "revd", "nystrom", "ritzit"), 1000),
             ("C3", configs.config3, ("none", "nystrom"), 500),
-            ("C4_k256", lambda: configs.config4(256), ("none", "nystrom"), 300)):
+            ("C4_k256", lambda: configs.config4(256), ("none", "nystrom"), 300),
+            ("C5_k64", lambda: configs.config5(64), ("none", "revd", "nystrom"), 100)):
         r = {"build_ms": {}, "build_stage_ms": {}, "pcg": {}}
         try:
             wl = mk()
@@ -429,7 +432,8 @@ def run_lmp(W, configs, dev):
             U = torch.empty((k, nA), dtype=torch.float64, device=dev)
             th = torch.empty(k, dtype=torch.float64, device=dev)
             kept = {}
-            for method in ("revd", "ritzit", "nystrom"):
+            methods = ("revd", "ritzit", "nystrom") if name != "C5_k64" else ("revd", "nystrom")
+            for method in methods:
                 cfg = W.SketchConfig(k, m - k, OMEGA_SEED, method, 1)
                 W.sketch_eigenpairs_dev(op, cfg, Om, U, th)          # warm (grows workspaces)
                 torch.cuda.synchronize()
@@ -443,7 +447,7 @@ def run_lmp(W, configs, dev):
                                                    wall_ms=wall)
                 r.setdefault("theta_head", {})[method] = th[:3].cpu().tolist()
                 if method in pcg_methods:
-                    if method == "nystrom":   # last: free the sketch blocks before the factor copies U
+                    if method == methods[-1]:   # last: free the sketch blocks before the factor copies U
                         del Om
                         op.release_workspaces()
                         torch.cuda.empty_cache()

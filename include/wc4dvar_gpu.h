@@ -149,7 +149,10 @@ int wc4dvar_gpu_op_apply_block_dev(wc4dvar_op* op, const double* V, int64_t ldv,
  * which = 0 apply_Linv (operators.cpp:79-89), 1 apply_LinvT (:91-101),
  *         2 apply_D_half (:103-113), 3 apply_D_half_inv (:115-125).
  * These do not count as operator applies, as in the reference. */
-enum { WC4DVAR_LINV = 0, WC4DVAR_LINVT = 1, WC4DVAR_D_HALF = 2, WC4DVAR_D_HALF_INV = 3 };
+enum { WC4DVAR_LINV = 0, WC4DVAR_LINVT = 1, WC4DVAR_D_HALF = 2, WC4DVAR_D_HALF_INV = 3,
+       /* the middle of HessianOperator::apply (operators.cpp:132-141):
+        * L^{-T} H^T R^{-1} H L^{-1} v, no D^{1/2} (row-sharded apply, distributed.py) */
+       WC4DVAR_SWEEPS = 4 };
 int wc4dvar_gpu_hessian_piece(wc4dvar_op* op, int which, const double* V, int64_t ldv,
                               int64_t m, double* out, int64_t ldo);
 int wc4dvar_gpu_hessian_piece_dev(wc4dvar_op* op, int which, const double* V, int64_t ldv,
@@ -177,6 +180,13 @@ int wc4dvar_gpu_observation_range_dev(wc4dvar_op* op, double* W, int64_t ldw, vo
 int wc4dvar_gpu_clustered_spectrum(wc4dvar_op* op, const struct wc4dvar_lmp* precond,
                                    const double* obs_range, int64_t ldw, double* nonunit,
                                    int64_t* n_nonunit, int64_t* unit_multiplicity);
+
+/* One covariance factor of the operator (which = 0: B^{1/2}, 1: Q^{1/2}; inv != 0: the
+ * inverse factor; CovarianceFactor::half / half_inv, covariance.hpp:31-38) applied to c
+ * n-vectors X (n x c, ldx) -> out (n x c, ldo), device pointers on `stream`: the local step
+ * of the block-sharded D^{1/2} in the row-sharded Hessian apply. */
+int wc4dvar_gpu_factor_apply_dev(wc4dvar_op* op, int which, int inv, const double* X, int64_t ldx,
+                                 int64_t c, double* out, int64_t ldo, void* stream);
 
 int wc4dvar_gpu_op_profile(wc4dvar_op* op, int enable);
 int wc4dvar_gpu_op_profile_read(wc4dvar_op* op, double* ms3, int64_t* calls);

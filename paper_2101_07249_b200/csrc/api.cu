@@ -351,8 +351,8 @@ int wc4dvar_gpu_hessian_piece_dev(wc4dvar_op* op, int which, const double* V, in
     W4_API_BEGIN
     HessianOp* h = dynamic_cast<HessianOp*>(op);
     require(h != nullptr, "hessian piece: operator is not a HessianOperator");
-    static const char* names[] = {"apply_Linv", "apply_LinvT", "apply_D_half", "apply_D_half_inv"};
-    require(which >= 0 && which <= 3, "hessian piece: unknown selector");
+    static const char* names[] = {"apply_Linv", "apply_LinvT", "apply_D_half", "apply_D_half_inv", "sweeps"};
+    require(which >= 0 && which <= 4, "hessian piece: unknown selector");
     require(m >= 0 && ldv >= op->dim && ldo >= op->dim,
             std::string(names[which]) + ": window length mismatch");
     std::lock_guard<std::recursive_mutex> lk(op->mu);
@@ -370,6 +370,29 @@ int wc4dvar_gpu_hessian_piece_dev(wc4dvar_op* op, int which, const double* V, in
     }
     op->reset_status(st);
     h->piece_dev(which, src, lds, m, out, ldo, st);
+    if (which == WC4DVAR_SWEEPS) op->check_status(st);  // the apply's stage-tagged finite checks
+    else W4_CUDA(cudaStreamSynchronize(st));
+    W4_API_END
+}
+
+int wc4dvar_gpu_factor_apply_dev(wc4dvar_op* op, int which, int inv, const double* X, int64_t ldx, int64_t c,
+                                 double* out, int64_t ldo, void* stream) {
+    W4_API_BEGIN
+    HessianOp* h = dynamic_cast<HessianOp*>(op);
+    require(h != nullptr, "factor apply: operator is not a HessianOperator");
+    require(which == 0 || which == 1, "factor apply: which must be 0 (B) or 1 (Q)");
+    require(c >= 0 && ldx >= h->n && ldo >= h->n && (c == 0 || (X && out)), "factor apply: bad arguments");
+    std::lock_guard<std::recursive_mutex> lk(op->mu);
+    DeviceGuard g(op->device);
+    cudaStream_t st = pick(op, stream);
+    const double* src = X;
+    if (overlaps(X, ldx, c, out, ldo, c, h->n)) {
+        double* tmp = op->in_buf.get<double>((size_t)h->n * c);
+        W4_CUDA(cudaMemcpy2DAsync(tmp, h->n * 8, X, ldx * 8, h->n * 8, c, cudaMemcpyDeviceToDevice, st));
+        src = tmp;
+        ldx = h->n;
+    }
+    h->factor_apply(which, inv != 0, src, ldx, c, out, ldo, st);
     W4_CUDA(cudaStreamSynchronize(st));
     W4_API_END
 }

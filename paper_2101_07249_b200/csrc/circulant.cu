@@ -142,9 +142,10 @@ void CirculantPlan::init(int64_t n, const double* h_b, const double* h_q, const 
 
 void CirculantPlan::apply(bool inv, int N, const double* V, int64_t ldv, int64_t m, double* out,
                           int64_t ldo, const double* add, int64_t ldadd, unsigned* status,
-                          DevBuf& zbuf, DevBuf& xbuf, cudaStream_t st) {
+                          DevBuf& zbuf, DevBuf& xbuf, cudaStream_t st, int only) {
     const int64_t n = impl->n, nh = n / 2 + 1;
-    const double2* sb = spec[inv ? 2 : 0];
+    // only = 0 / 1: every column uses the B / Q factor (callers pass N = 0)
+    const double2* sb = spec[inv ? (only == 1 ? 3 : 2) : (only == 1 ? 1 : 0)];
     const double2* sq = spec[inv ? 3 : 1];
     require(sb && sq, "apply_D_half_inv: inverse factors were not provided");
     const int64_t dim = n * (N + 1);
@@ -156,7 +157,7 @@ void CirculantPlan::apply(bool inv, int N, const double* V, int64_t ldv, int64_t
         return !e || std::atoi(e) != 0;
     }();
     if (use_f4 && impl->f4.ready()) {
-        impl->f4.apply(inv, N, V, ldv, m, out, ldo, add, ldadd, status, zbuf, impl->pairbuf, st);
+        impl->f4.apply(inv, N, V, ldv, m, out, ldo, add, ldadd, status, zbuf, impl->pairbuf, st, only);
         return;
     }
     // contiguous real input (the FFT plan assumes column distance n)

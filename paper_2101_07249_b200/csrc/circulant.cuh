@@ -21,7 +21,7 @@ struct CirculantPlan {
     // out = D^{1/2} V (+ add) for an n(N+1) x m block (inverse factors when inv).
     void apply(bool inv, int N, const double* V, int64_t ldv, int64_t m, double* out, int64_t ldo,
                const double* add, int64_t ldadd, unsigned* status, DevBuf& zbuf, DevBuf& xbuf,
-               cudaStream_t st);
+               cudaStream_t st, int only = -1);
 };
 
 }  // namespace w4

@@ -811,8 +811,9 @@ bool Fft4::init(int64_t N, const double2* const spec_half[4], cudaStream_t st) {
 
 void Fft4::apply(bool inv, int Nsw, const double* V, int64_t ldv, int64_t m, double* out, int64_t ldo,
                  const double* add, int64_t ldadd, unsigned* status, DevBuf& ybuf, DevBuf& pairbuf,
-                 cudaStream_t st) {
-    const double* lamB = lam_[inv ? 2 : 0];
+                 cudaStream_t st, int only) {
+    // only = 0 / 1: every column uses the B / Q factor (callers pass Nsw = 0)
+    const double* lamB = lam_[inv ? (only == 1 ? 3 : 2) : (only == 1 ? 1 : 0)];
     const double* lamQ = lam_[inv ? 3 : 1];
     require(lamB && lamQ, "apply_D_half_inv: inverse factors were not provided");
     const int per = Nsw + 1;

@@ -20,7 +20,7 @@ public:
     // out = D^{1/2} V (+ add) for an N(Nsw+1) x m block; spectra 0/1 (2/3 when inv) = B / Q.
     void apply(bool inv, int Nsw, const double* V, int64_t ldv, int64_t m, double* out, int64_t ldo,
                const double* add, int64_t ldadd, unsigned* status, DevBuf& ybuf, DevBuf& pairbuf,
-               cudaStream_t st);
+               cudaStream_t st, int only = -1);
 
 private:
     int plan_ = -1;

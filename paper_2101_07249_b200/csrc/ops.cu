@@ -137,6 +137,27 @@ void HessianOp::d_half(bool inv, const double* V, int64_t ldv, int64_t m, double
     gemm_nn(ps, np, status, st);
 }
 
+void HessianOp::factor_apply(int which, bool inv, const double* X, int64_t ldx, int64_t c, double* out,
+                             int64_t ldo, cudaStream_t st) {
+    if (c == 0) return;
+    if (cov_kind == WC4DVAR_COV_CIRCULANT) {
+        circ->apply(inv, 0, X, ldx, c, out, ldo, nullptr, 0, nullptr, circ_z, circ_x, st, which);
+        return;
+    }
+    const double* F = which == 0 ? (inv ? b_half_inv : b_half) : (inv ? q_half_inv : q_half);
+    require(F, "apply_D_half_inv: inverse factors were not provided");
+    GemmPass p;
+    p.A = F;
+    p.lda = n;
+    p.M = n;
+    p.K = n;
+    p.ncols = c;
+    p.in = ColMap::plain(X, ldx);
+    p.out = ColMap::plain(out, ldo);
+    p.symA = sym[which == 0 ? (inv ? 2 : 0) : (inv ? 3 : 1)];
+    gemm_nn(&p, 1, nullptr, st);
+}
+
 void HessianOp::apply_block_dev(const double* V, int64_t ldv, int64_t m, double* out, int64_t ldo,
                                 cudaStream_t st) {
     if (m == 0) return;
@@ -236,6 +257,21 @@ void HessianOp::piece_dev(int which, const double* V, int64_t ldv, int64_t m, do
             a.do_adj = true;
             sweep(md, nd, a, d_status, st, &sweep_ws);
             break;
+        case WC4DVAR_SWEEPS: {  // L^{-T} H^T R^{-1} H L^{-1} v (operators.cpp:132-141)
+            const int64_t q = nd.q;
+            a.X = V;
+            a.ldx = ldv;
+            a.Y = q > 0 ? y_ws.get<double>((size_t)q * m) : nullptr;
+            a.scale_fwd = 1.0 / (sigma_obs * sigma_obs);
+            a.do_fwd = true;
+            a.fwd_obs = q > 0;
+            a.S = out;
+            a.lds = ldo;
+            a.do_adj = true;
+            a.adj_obs = q > 0;
+            sweep(md, nd, a, d_status, st, &sweep_ws);
+            break;
+        }
         case WC4DVAR_D_HALF:
         case WC4DVAR_D_HALF_INV:
             d_half(which == WC4DVAR_D_HALF_INV, V, ldv, m, out, ldo, nullptr, 0, nullptr, st);

@@ -103,6 +103,10 @@ struct HessianOp final : wc4dvar_op {
     // observe (models.cpp:184-192): y = H traj (window trajectory, network order)
     void observe_dev(const double* traj, double* y, cudaStream_t st);
     // out = D^{1/2} V (+ add) for an n_A x m block; inverse factors when inv.
+    // One covariance factor (which = 0: B^{1/2}, 1: Q^{1/2}; their inverses when inv) on c
+    // n-vectors: the block-sharded D^{1/2} of the row-sharded apply (distributed.py).
+    void factor_apply(int which, bool inv, const double* X, int64_t ldx, int64_t c, double* out, int64_t ldo,
+                      cudaStream_t st);
     void d_half(bool inv, const double* V, int64_t ldv, int64_t m, double* out, int64_t ldo,
                 const double* add, int64_t ldadd, unsigned* status, cudaStream_t st);
 };

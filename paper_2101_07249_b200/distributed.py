@@ -448,9 +448,12 @@ class DistPcgResult:
 
 def dist_pcg(apply_rows: Callable[[torch.Tensor], torch.Tensor], b_rows: torch.Tensor,
              U_rows: Optional[torch.Tensor], theta: Optional[torch.Tensor], max_iter: int = 100,
-             rel_tol: float = 1e-6, ops=TorchOps) -> DistPcgResult:
+             rel_tol: float = 1e-6, ops=TorchOps, comm=None) -> DistPcgResult:
     """Row-sharded split PCG (krylov.cpp:22-99) with the compact-WY spectral LMP: every dot
-    product and every U^T v of an iteration is one all-reduce of (k + 1) doubles."""
+    product and every U^T v of an iteration is one all-reduce of (k + 1) doubles.  Any row
+    partition works (contiguous rows, or the spatial slabs of RowShardedHessian) as long as
+    b, U and apply_rows use the same one."""
+    allreduce_sum = comm.allreduce_sum if comm is not None else globals()["allreduce_sum"]
     k = 0 if U_rows is None else U_rows.shape[1]
     if k:
         c = 1.0 - 1.0 / torch.sqrt(theta)
@@ -505,3 +508,283 @@ def dist_pcg(apply_rows: Callable[[torch.Tensor], torch.Tensor], b_rows: torch.T
         rho = rn
     res.x_rows = x
     return res
+
+
+# ----------------------------------------------------------------------------- row-sharded apply
+class TorchComm:
+    """torch.distributed (NCCL on GPU ranks, gloo on CPU ranks) for the row-sharded apply."""
+
+    def world_rank(self):
+        return _world_rank()
+
+    def alltoall(self, recv: List[torch.Tensor], send: List[torch.Tensor]) -> None:
+        world, rank = _world_rank()
+        if world == 1:
+            recv[0].copy_(send[0])
+            return
+        _alltoall(recv, send)
+
+    def allreduce_sum(self, t: torch.Tensor) -> torch.Tensor:
+        return allreduce_sum(t)
+
+
+class ThreadComm:
+    """In-process ranks (one host thread each) sharing one device: the same collectives as
+    TorchComm through a barrier and a mailbox, deterministic rank order.  Used to run the
+    multi-rank device path on a single GPU (no kernel waits on another rank's kernel: each
+    exchange completes on the host between launches)."""
+
+    def __init__(self, world: int):
+        import threading
+        self.world = world
+        self._bar = threading.Barrier(world)
+        self._box = {}
+
+    def bind(self, rank: int) -> "ThreadComm._Rank":
+        return ThreadComm._Rank(self, rank)
+
+    class _Rank:
+        def __init__(self, hub, rank):
+            self.hub, self.rank = hub, rank
+
+        def world_rank(self):
+            return self.hub.world, self.rank
+
+        def alltoall(self, recv, send):
+            h = self.hub
+            for q, sd in enumerate(send):
+                h._box[(self.rank, q)] = sd.clone() if sd.numel() else sd
+            if any(sd.is_cuda for sd in send):
+                torch.cuda.synchronize()
+            h._bar.wait()
+            for q, rv in enumerate(recv):
+                if rv.numel():
+                    rv.copy_(h._box[(q, self.rank)])
+            if recv and recv[0].is_cuda:
+                torch.cuda.synchronize()
+            h._bar.wait()
+
+        def allreduce_sum(self, t):
+            h = self.hub
+            h._box[("ar", self.rank)] = t.clone()
+            if t.is_cuda:
+                torch.cuda.synchronize()
+            h._bar.wait()
+            acc = h._box[("ar", 0)].clone()
+            for q in range(1, h.world):
+                acc += h._box[("ar", q)]
+            h._bar.wait()
+            t.copy_(acc)
+            return t
+
+
+def window_halo(kind: str, N: int, s: int) -> int:
+    """Stencil reach (grid points) of one forward + adjoint window sweep (N intervals of s
+    TL sub-steps): a slab extended by this many points on each side computes its own points
+    of L^{-T} H^T R^{-1} H L^{-1} exactly with no further exchange.  s_0 on the slab needs
+    s_i (and so H^T y_i, i.e. the forward state x_i) within i r_adj of it, while the forward
+    state x_i is exact within H - i r_fwd of the slab: per side H >= N (r_fwd + r_adj), with
+    (r_fwd, r_adj) per interval = the TL step's reach on that side and the adjoint's.
+    Upwind advection (models.cpp:27-45): (s, 0) left, (0, s) right -> N s; advection-
+    diffusion: (s, s) -> 2 N s; the RK4 Lorenz-96 Jacobian (models.cpp:92-116, radius 2
+    left / 1 right per stage, 4 stages per step): (8 s, 4 s) left, (4 s, 8 s) right -> 12 N s,
+    plus 8 points for the RK4 stages recomputed on the slab from its trajectory rows (three
+    dependent right-hand sides, models.cpp:80-87)."""
+    if kind == "identity":
+        return 0
+    if kind == "advection":
+        return N * s
+    if kind == "advdiff":
+        return 2 * N * s
+    if kind == "l96":
+        return 12 * N * s + 8
+    raise ValueError(f"window_halo: unknown model {kind}")
+
+
+@dataclass
+class SlabGeometry:
+    """Spatial decomposition for the row-sharded Hessian apply: rank r owns
+    grid points [a, b) of EVERY window block (N + 1 blocks of n points); a local vector is
+    the (N + 1) x n_loc block-major array.  The sweeps run on the slab extended by `halo`
+    points per side as a periodic domain of n_ext = n_loc + 2 halo points."""
+    n: int
+    N: int
+    world: int
+    rank: int
+    halo: int
+
+    @property
+    def a(self) -> int:
+        return row_range(self.n, self.world, self.rank)[0]
+
+    @property
+    def b(self) -> int:
+        return row_range(self.n, self.world, self.rank)[1]
+
+    @property
+    def n_loc(self) -> int:
+        return self.b - self.a
+
+    @property
+    def n_ext(self) -> int:
+        return self.n_loc + 2 * self.halo
+
+    def ext_points(self, rank: Optional[int] = None) -> torch.Tensor:
+        """Global grid index of every extended-slab point of `rank` (periodic)."""
+        r = self.rank if rank is None else rank
+        a, b = row_range(self.n, self.world, r)
+        return (torch.arange(a - self.halo, b + self.halo, dtype=torch.int64) % self.n)
+
+    def owner(self, g: torch.Tensor) -> torch.Tensor:
+        bounds = torch.tensor([row_range(self.n, self.world, r)[1] for r in range(self.world)], dtype=torch.int64)
+        return torch.bucketize(g, bounds, right=True)
+
+    def window_indices(self) -> torch.Tensor:
+        """Indices into a full window vector (n (N+1)) of this rank's local vector."""
+        j = torch.arange(self.a, self.b, dtype=torch.int64)
+        return (torch.arange(self.N + 1, dtype=torch.int64)[:, None] * self.n + j[None, :]).reshape(-1)
+
+
+def slab_network(points, times, n: int, geom: SlabGeometry):
+    """The observation network restricted to the extended slab, in local (extended) indices:
+    (local points, times).  Observation times are unchanged."""
+    pts = set(int(p) for p in points)
+    g = geom.ext_points().tolist()
+    return [j for j, gj in enumerate(g) if gj in pts], list(times)
+
+
+class RowShardedHessian:
+    """HessianOperator::apply (operators.cpp:127-144) on spatial slabs, one rank per GPU:
+
+      t = D^{1/2} v   -- block-sharded: an all-to-all turns slabs into whole window blocks,
+                         each rank applies B^{1/2} / Q^{1/2} to its blocks, and a second
+                         all-to-all returns slabs;
+      s = L^{-T} H^T R^{-1} H L^{-1} t
+                      -- ONE halo exchange of t (window_halo points per side, every block),
+                         then the whole forward + adjoint window sweep on the extended slab
+                         with no further communication (the halo is the stencil reach);
+      out = v + D^{1/2} s.
+
+    `ops` supplies the local steps: factor(X (c, n), which) and sweeps(T_ext (N+1, n_ext)).
+    The DEVICE backend is `DeviceSlabOps` (library kernels through the C-ABI); tests inject a
+    CPU backend built on the oracle."""
+
+    def __init__(self, geom: SlabGeometry, ops, comm=None):
+        self.geom, self.ops = geom, ops
+        self.comm = comm if comm is not None else TorchComm()
+        g = geom
+        self.blocks = [column_range(g.N + 1, g.world, r) for r in range(g.world)]
+        self.slabs = [row_range(g.n, g.world, r) for r in range(g.world)]
+        # halo exchange plan: for every rank q, the positions of its extended slab owned by
+        # each rank (the same plan on every rank, so sender and receiver agree on the order)
+        self._ext_src = []   # per q: list over r of (ext positions j, global indices)
+        for q in range(g.world):
+            gq = g.ext_points(q)
+            own = g.owner(gq)
+            self._ext_src.append([(torch.nonzero(own == r).reshape(-1), gq[own == r]) for r in range(g.world)])
+
+    # -- D^{1/2}: slabs -> whole blocks -> factor -> slabs
+    def d_half(self, x: torch.Tensor) -> torch.Tensor:
+        g = self.geom
+        n_loc = g.n_loc
+        send = [x[i0:i1].reshape(-1) for (i0, i1) in self.blocks]
+        my0, my1 = self.blocks[g.rank]
+        nb = my1 - my0
+        recv = [torch.empty(nb * (b - a), dtype=x.dtype, device=x.device) for (a, b) in self.slabs]
+        self.comm.alltoall(recv, send)
+        full = torch.empty((nb, g.n), dtype=x.dtype, device=x.device)
+        for (a, b), rv in zip(self.slabs, recv):
+            full[:, a:b] = rv.reshape(nb, b - a)
+        out = torch.empty_like(full)
+        if nb:
+            if my0 == 0:  # block 0 takes B^{1/2} (operators.cpp:106), the rest Q^{1/2} (:110)
+                out[:1] = self.ops.factor(full[:1], 0)
+                if nb > 1:
+                    out[1:] = self.ops.factor(full[1:], 1)
+            else:
+                out[:] = self.ops.factor(full, 1)
+        send2 = [out[:, a:b].reshape(-1).contiguous() for (a, b) in self.slabs]
+        recv2 = [torch.empty((i1 - i0) * n_loc, dtype=x.dtype, device=x.device) for (i0, i1) in self.blocks]
+        self.comm.alltoall(recv2, send2)
+        return torch.cat([rv.reshape(-1, n_loc) for rv in recv2], dim=0)
+
+    # -- halo exchange: the extended slab of every block
+    def extend(self, t: torch.Tensor) -> torch.Tensor:
+        g = self.geom
+        a = g.a
+        send = []
+        for q in range(g.world):  # what q's extended slab needs from this rank
+            _, gidx = self._ext_src[q][g.rank]
+            send.append(t[:, (gidx - a).to(t.device)].reshape(-1).contiguous())
+        recv = [torch.empty(g.N + 1, len(self._ext_src[g.rank][r][0]), dtype=t.dtype, device=t.device).reshape(-1)
+                for r in range(g.world)]
+        self.comm.alltoall(recv, send)
+        ext = torch.empty((g.N + 1, g.n_ext), dtype=t.dtype, device=t.device)
+        for r in range(g.world):
+            pos, _ = self._ext_src[g.rank][r]
+            ext[:, pos.to(t.device)] = recv[r].reshape(g.N + 1, -1)
+        return ext
+
+    def apply(self, v: torch.Tensor) -> torch.Tensor:
+        """v: (N+1, n_loc) local slab of one window vector -> A v on the same slab."""
+        g = self.geom
+        t = self.d_half(v)
+        s_ext = self.ops.sweeps(self.extend(t))
+        s = s_ext[:, g.halo:g.halo + g.n_loc].contiguous()
+        return v + self.d_half(s)
+
+    def apply_rows(self, v_flat: torch.Tensor) -> torch.Tensor:
+        """dist_pcg's callback: the flattened slab (block-major) in, the same out."""
+        g = self.geom
+        return self.apply(v_flat.reshape(g.N + 1, g.n_loc)).reshape(-1)
+
+
+class DeviceSlabOps:
+    """The row-sharded apply's local steps on this rank's GPU, through the C-ABI: the factor
+    applies on an operator holding the n-point covariance factors, and the sweeps
+    (WC4DVAR_SWEEPS piece) on an operator built for the extended slab: the same model on
+    n_ext points (for Lorenz-96 the linearisation trajectory's extended-slab rows), the
+    network's observed points inside the slab and R^{-1}."""
+
+    def __init__(self, model, net, b_half, q_half, sigma_obs: float, geom: SlabGeometry, device: int = 0):
+        from . import wc4dvar as w
+        self.w = w
+        self.geom = geom
+        n, N = model.n, model.N
+        # D^{1/2}: the full-size factors on a minimal operator (identity model, no network)
+        self.fop = w.HessianOperator(w.IdentityLinearized(n, 1), w.ObservationNetwork.empty(n, 1), b_half, q_half,
+                                     sigma_obs, device)
+        ne = geom.n_ext
+        pts, times = slab_network(net.points, net.times, n, geom)
+        snet = w.ObservationNetwork(ne, N, 1, 1, list(times), list(pts), len(times) * len(pts))
+        if model.kind == "l96" and model.stages is not None:  # host stages (N s, 4 n)
+            idx = geom.ext_points().numpy()
+            st = model.stages.reshape(-1, 4, n)[:, :, idx].reshape(-1, 4 * ne)
+            smodel = w.LinearizedModel("l96", ne, N, model.substeps, dt=model.dt, stages=st)
+        elif model.kind == "l96":
+            tr = model.trajectory
+            idx = geom.ext_points()
+            if isinstance(tr, torch.Tensor):     # device (steps + 1, n) row-major
+                tslab = tr[:, idx.to(tr.device)].contiguous()
+            else:                                # host n x (steps + 1)
+                tslab = tr[idx.numpy(), :]
+            smodel = w.Lorenz96Linearized(tslab, model.forcing, model.dt, model.substeps)
+        else:
+            smodel = w.LinearizedModel(model.kind, ne, N, model.substeps, model.courant, model.diffusion)
+        unit = torch.zeros(ne, dtype=torch.float64)
+        unit[0] = 1.0
+        eye = w.CovarianceFactor(unit.numpy(), unit.numpy(), kind="circulant")  # unused by the sweeps
+        self.sop = w.HessianOperator(smodel, snet, eye, eye, sigma_obs, device)
+
+    def factor(self, X: torch.Tensor, which: int) -> torch.Tensor:
+        X = X.contiguous()
+        out = torch.empty_like(X)
+        self.fop.factor_apply_dev(which, False, X, out, ctypes.c_void_p(torch.cuda.current_stream().cuda_stream))
+        return out
+
+    def sweeps(self, T: torch.Tensor) -> torch.Tensor:
+        g = self.geom
+        V = T.reshape(1, -1).contiguous()  # one window column of the extended slab
+        out = torch.empty_like(V)
+        self.sop.piece_dev(4, V, out, ctypes.c_void_p(torch.cuda.current_stream().cuda_stream))
+        return out.reshape(g.N + 1, g.n_ext)

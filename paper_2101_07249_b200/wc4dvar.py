@@ -126,6 +126,7 @@ SIGNATURES = {
     "wc4dvar_gpu_sketch": (ctypes.c_int, [_vp, ctypes.POINTER(SketchDesc), _dp, _dp, _i64, _dp,
                                           ctypes.POINTER(_i64)]),
     "wc4dvar_gpu_launch_count": (ctypes.c_int64, []),
+    "wc4dvar_gpu_factor_apply_dev": (ctypes.c_int, [_vp, ctypes.c_int, ctypes.c_int, _vp, _i64, _i64, _vp, _i64, _vp]),
     "wc4dvar_gpu_op_release_workspaces": (ctypes.c_int, [_vp]),
     "wc4dvar_gpu_gaussian_block_dev": (ctypes.c_int, [_i64, _i64, _i64, _i64, _i64, ctypes.c_uint64, _vp, _i64,
                                                       ctypes.c_int, _vp]),
@@ -558,6 +559,28 @@ class HessianOperator(LinearOperator):
         out = np.empty_like(v)
         _check(lib.wc4dvar_gpu_hessian_piece(self._h, which, _p(v), v.shape[0], m, _p(out), v.shape[0]))
         return out
+
+    def sweeps(self, v):
+        """L^{-T} H^T R^{-1} H L^{-1} v: the middle of apply (operators.cpp:132-141), no D^{1/2}."""
+        return self._piece(4, "sweeps", v)
+
+    def piece_dev(self, which: int, V, out, stream=None) -> None:
+        """Device-resident hessian piece (0 Linv, 1 LinvT, 2 D^{1/2}, 3 D^{-1/2}, 4 sweeps) on
+        torch CUDA tensors in the (columns, rows) layout."""
+        m, dim = V.shape
+        require(dim == self.dim() and tuple(out.shape) == (m, dim), "hessian piece: shape mismatch")
+        _check(lib.wc4dvar_gpu_hessian_piece_dev(self._h, which, V.data_ptr(), V.stride(0) if m > 1 else dim, m,
+                                                 out.data_ptr(), out.stride(0) if m > 1 else dim,
+                                                 None if stream is None else stream))
+
+    def factor_apply_dev(self, which: int, inv: bool, X, out, stream=None) -> None:
+        """B^{1/2} (which 0) or Q^{1/2} (which 1), or their inverses, on the rows of the torch
+        CUDA tensor X (c, n) -> out (c, n) (wc4dvar_gpu_factor_apply_dev)."""
+        c, n = X.shape
+        require(n == self.state_size() and tuple(out.shape) == (c, n), "factor apply: shape mismatch")
+        _check(lib.wc4dvar_gpu_factor_apply_dev(self._h, which, int(inv), X.data_ptr(), X.stride(0) if c > 1 else n,
+                                                c, out.data_ptr(), out.stride(0) if c > 1 else n,
+                                                None if stream is None else stream))
 
     def observe(self, traj) -> np.ndarray:
         """observe (models.cpp:184-192) with this operator's network, on the device."""

@@ -143,3 +143,55 @@ def test_small_evd_svd_vs_lapack(m):
     # U diag(s) is X's column space image: X X^T U = U diag(s^2)
     assert np.abs(X @ X.T @ U - U * s * s).max() <= 1e-11 * sref.max() ** 2
 
+
+
+@pytest.mark.parametrize("case", ["advdiff-dense", "advdiff-circulant", "lorenz96"])
+@pytest.mark.parametrize("world", [2, 3])
+def test_row_sharded_apply_device(case, world):
+    """The row-sharded Hessian apply (spatial slabs, block-sharded D^{1/2}, one halo exchange,
+    distributed.RowShardedHessian) on the DEVICE backend: `world` ranks as host threads on
+    one GPU (ThreadComm; every exchange completes on the host between launches), each with
+    its own C-ABI handles (factor apply + the WC4DVAR_SWEEPS piece on its extended slab),
+    against the single-handle block apply."""
+    import threading
+
+    from paper_2101_07249_b200.distributed import (DeviceSlabOps, RowShardedHessian, SlabGeometry, ThreadComm,
+                                                   window_halo)
+    if case == "advdiff-dense":
+        wl = configs.small_advdiff(n=96, N=5, s=3)
+    elif case == "advdiff-circulant":
+        wl = configs.Workload("c", W.AdvDiffLinearized(400, 6, 0.5, 0.2, 4), W.ObservationNetwork.build(400, 6, 3, 1),
+                              configs.circulant_sqrt(configs.soar_first_column(1.0, 6.0, 400)),
+                              configs.circulant_sqrt(configs.soar_first_column(0.3, 6.0, 400)), 0.1, 6, 3)
+    else:
+        wl = configs.lorenz96_workload("l96", 300, 3, 2, 6, 3, spinup=50)
+    g = wl.hessian(0)
+    nA, n, N = g.dim(), wl.model.n, wl.model.N
+    V = torch.from_numpy(O.gaussian_matrix(nA, 2, 23).T.copy()).cuda()
+    ref = torch.empty_like(V)
+    g.apply_block_dev(V, ref)
+    torch.cuda.synchronize()
+    hub = ThreadComm(world)
+    errs, outs = [], {}
+
+    def run(rank):
+        try:
+            geom = SlabGeometry(n, N, world, rank, window_halo(wl.model.kind, N, wl.model.substeps))
+            ops = DeviceSlabOps(wl.model, wl.net, wl.b_half, wl.q_half, wl.sigma_obs, geom, 0)
+            rsh = RowShardedHessian(geom, ops, hub.bind(rank))
+            idx = geom.window_indices().cuda()
+            for c in range(2):
+                outs[(rank, c)] = (rsh.apply(V[c][idx].reshape(N + 1, geom.n_loc)).reshape(-1), idx)
+        except Exception as e:  # surfaced below
+            errs.append(e)
+
+    th = [threading.Thread(target=run, args=(r,)) for r in range(world)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join()
+    assert not errs, errs
+    scale = ref.abs().max()
+    for (rank, c), (out, idx) in outs.items():
+        err = float((out - ref[c][idx]).abs().max() / scale)
+        assert err <= 1e-13, (case, rank, c, err)
