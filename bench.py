@@ -418,8 +418,8 @@ def run_lmp(W, configs, dev):
     res = {}
     for name, mk, pcg_methods, max_iter in (
             ("C2", configs.config2, ("none", "revd", "nystrom", "ritzit"), 1000),
-            ("C3", configs.config3, ("none", "nystrom"), 500),
-            ("C4_k256", lambda: configs.config4(256), ("none", "nystrom"), 300),
+            ("C3", configs.config3, ("none", "nystrom"), 20000),
+            ("C4_k256", lambda: configs.config4(256), ("none", "nystrom"), 2000),
             ("C5_k64", lambda: configs.config5(64), ("none", "revd", "nystrom"), 100)):
         r = {"build_ms": {}, "build_stage_ms": {}, "pcg": {}}
         try:

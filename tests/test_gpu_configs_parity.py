@@ -130,6 +130,24 @@ class _Variant(O.LinearOperator):
         return out.reshape(-1, order="F") + v
 
 
+class _NoisyLmp:
+    """The oracle LMP with last-bit noise of relative size `noise` (the measured device-vs-
+    oracle one-apply discrepancy of the factor) on every apply / apply_transpose."""
+
+    def __init__(self, base, seed, noise):
+        self.base, self.noise = base, noise
+        self.s = O.NormalStream(seed)
+
+    def _n(self, y):
+        return y + self.noise * np.abs(y).max() * self.s.draw(len(y))
+
+    def apply(self, v):
+        return self._n(self.base.apply(v))
+
+    def apply_transpose(self, v):
+        return self._n(self.base.apply_transpose(v))
+
+
 def _pcg_case(name, g, o, b, fg, fo, delta, max_iter=2000):
     """Device PCG vs the oracle PCG (same preconditioner).  The bound is the north star's
     (iterations within 1, x within 1e-9) wherever it holds.  Otherwise the case also runs
@@ -147,8 +165,11 @@ def _pcg_case(name, g, o, b, fg, fo, delta, max_iter=2000):
     if it_d <= 1 and dx <= 1e-9:
         print(msg + " -> strict bound holds (iterations within 1, x within 1e-9)")
         return
+    # the LMP discrepancy of one apply (compact-WY on the device vs rank-1 updates here)
+    dl = max(relerr(fg.apply_transpose(b), fo.apply_transpose(b)), 2.2e-16) if fo is not None else 0.0
     runs = [ro, O.pcg_split(_Variant(o), b, fo, opts=O.PcgOptions(**opts))]
-    runs += [O.pcg_split(_Variant(o, sd, delta), b, fo, opts=O.PcgOptions(**opts)) for sd in (11, 12, 13)]
+    runs += [O.pcg_split(_Variant(o, sd, delta), b, _NoisyLmp(fo, sd + 50, dl) if fo is not None else None,
+                         opts=O.PcgOptions(**opts)) for sd in (11, 12, 13)]
     its = [r.history.iterations for r in runs]
     # the spread is the largest pairwise distance among the five equally valid oracle runs
     sp_it = max(its) - min(its)
