@@ -1164,9 +1164,17 @@ void gemm_nn(const GemmPass* passes, int npass, unsigned* status, cudaStream_t s
         W4_LAUNCH();
         return;
     }
-    // Tile shape: big tiles when there are enough of them to fill the chip twice.
+    // Tile shape: big tiles when there are enough of them to fill the chip twice; 128 x 128
+    // tiles with 16 warps for the tall x (>= 128 wide) products of the sketches (Y R^{-1},
+    // Z W at k + l = 256: WC4DVAR_GEMM_NN = 1 forces the 128 x 64 shape, 2 the 128 x 128 one)
+    static const int nn_env = [] {
+        const char* e = std::getenv("WC4DVAR_GEMM_NN");
+        return e ? std::atoi(e) : 0;
+    }();
     const bool big = cdiv(maxM, 128) * cdiv(total_cols, 64) >= 2 * kSMs;
-    const int BMv = big ? 128 : 64, BNv = big ? 64 : 32;
+    const bool huge = vec2 && big && (nn_env == 2 || (nn_env == 0 && total_cols >= 128 &&
+                                                        cdiv(maxM, 128) * cdiv(total_cols, 128) >= 2 * kSMs));
+    const int BMv = big ? 128 : 64, BNv = huge ? 128 : (big ? 64 : 32);
     int64_t start = 0;
     for (int i = 0; i < 2; ++i) {
         tab.tile_start[i] = start;
@@ -1179,7 +1187,9 @@ void gemm_nn(const GemmPass* passes, int npass, unsigned* status, cudaStream_t s
     }
     tab.tile_start[2] = start;
     if (start == 0) return;
-    if (big) {
+    if (huge) {
+        launch_nn<128, 128, 4, 4, 3, 2>(tab, start, status, stream);
+    } else if (big) {
         if (vec2) launch_nn<128, 64, 4, 2, 3, 2>(tab, start, status, stream);
         else launch_nn<128, 64, 4, 2, 3, 1>(tab, start, status, stream);
     } else {
@@ -1192,9 +1202,20 @@ void gemm_tn(int64_t R, int64_t m1, int64_t m2, const double* A, int64_t lda, co
              int64_t ldb, double alpha, double* C, int64_t ldc, DevBuf& work,
              cudaStream_t stream) {
     if (m1 == 0 || m2 == 0) return;
-    constexpr int BM = 64, BN = 64;
+    // tile variant (WC4DVAR_GEMM_TN, default 0 = by shape): 1: 64x64 / 4 warps / 4 stages,
+    // 2: 64x64 / 8 warps, 3: 128x64 / 8 warps / 3 stages, 4: 128x128 / 16 warps / 3 stages
+    static const int var_env = [] {
+        const char* e = std::getenv("WC4DVAR_GEMM_TN");
+        return e ? std::atoi(e) : 0;
+    }();
+    int var = var_env;
+    // measured (C4 n = 1.7e7, m = 256): 128x128 / 16 warps 28.2 TF/s vs 64x64 / 4 warps ~17;
+    // at m = 64 (C3) the 64x64 tiles win (25 vs 7 TF/s: a 128-wide tile is half empty)
+    if (var == 0) var = (m1 >= 128 && m2 >= 128) ? 4 : (m1 >= 128 ? 3 : 1);
+    const int BM = (var >= 3) ? 128 : 64, BN = (var == 4) ? 128 : 64;
+    const int ctas_per_sm = (var == 4) ? 1 : 2;
     const int64_t tiles = cdiv(m1, BM) * cdiv(m2, BN);
-    int64_t nsplit = cdiv(2 * kSMs, tiles);
+    int64_t nsplit = cdiv((int64_t)ctas_per_sm * kSMs, tiles);
     const int64_t min_rows = 256;
     if (nsplit * min_rows > R) nsplit = cdiv(R, min_rows);
     if (nsplit < 1) nsplit = 1;
@@ -1205,10 +1226,16 @@ void gemm_tn(int64_t R, int64_t m1, int64_t m2, const double* A, int64_t lda, co
     const bool vec2 = aligned16(A) && aligned16(B) && lda % 2 == 0 && ldb % 2 == 0;
     if (R == 0) {
         W4_CUDA(cudaMemsetAsync(w, 0, sizeof(double) * m1 * m2, stream));
-    } else if (vec2) {
-        launch_tn<BM, BN, 2, 2, 4, 2>(R, m1, m2, A, lda, B, ldb, w, rows_per_split, nsplit, stream);
+    } else if (!vec2) {
+        launch_tn<64, 64, 2, 2, 4, 1>(R, m1, m2, A, lda, B, ldb, w, rows_per_split, nsplit, stream);
+    } else if (var == 2) {
+        launch_tn<64, 64, 2, 4, 4, 2>(R, m1, m2, A, lda, B, ldb, w, rows_per_split, nsplit, stream);
+    } else if (var == 3) {
+        launch_tn<128, 64, 4, 2, 3, 2>(R, m1, m2, A, lda, B, ldb, w, rows_per_split, nsplit, stream);
+    } else if (var == 4) {
+        launch_tn<128, 128, 4, 4, 3, 2>(R, m1, m2, A, lda, B, ldb, w, rows_per_split, nsplit, stream);
     } else {
-        launch_tn<BM, BN, 2, 2, 4, 1>(R, m1, m2, A, lda, B, ldb, w, rows_per_split, nsplit, stream);
+        launch_tn<64, 64, 2, 2, 4, 2>(R, m1, m2, A, lda, B, ldb, w, rows_per_split, nsplit, stream);
     }
     const int64_t e = m1 * m2;
     reduce_splits_kernel<<<(unsigned)cdiv(e, 256), 256, 0, stream>>>(m1, m2, nsplit, w, alpha, C,
