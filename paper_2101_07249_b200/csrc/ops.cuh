@@ -22,7 +22,7 @@ struct wc4dvar_op {
     unsigned* h_status = nullptr;  // pinned mirror
     int* h_int = nullptr;          // pinned scratch for small device->host reads
     w4::DevBuf in_buf, out_buf;
-    w4::DevBuf pool[32];           // [0,20) sketch, [20,32) PCG workspaces
+    w4::DevBuf pool[40];           // [0,24) sketch, [24,40) PCG workspaces
 
     // Stage profiling (wc4dvar_gpu_op_profile): events around the apply's kernels.
     bool prof = false;

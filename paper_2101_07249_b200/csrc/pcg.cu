@@ -76,7 +76,7 @@ void pcg_dev(wc4dvar_op& op, const double* b, wc4dvar_lmp* pre, const double* x0
     const int k = pre ? pre->k : 0;
     require(!pre || pre->k == 0 || pre->n == n, "pcg_split: preconditioner dimension mismatch");
     enum { B_R = 0, B_P, B_W, B_TMP, B_PART, B_SCAL, B_G, B_H, B_F, B_CNT, B_GWS, B_HF };
-    DevBuf* pool = op.pool + 20;  // pool[0..19] belong to the sketch workspaces
+    DevBuf* pool = op.pool + 24;  // pool[0..23] belong to the sketch workspaces
     double* r = pool[B_R].get<double>(n);
     double* p = pool[B_P].get<double>(n);
     double* w = pool[B_W].get<double>(n);

@@ -21,12 +21,16 @@
 
 namespace w4 {
 void gaussian_fill(int64_t count, uint64_t seed, double* out);
+int colpiv_rank_dd(int64_t n, int m, const double* Y, int64_t ld, int* perm_dev, int* rank_dev, int* rank_host,
+                   DevBuf& work, cudaStream_t st);
 namespace {
 
 enum {
     P_Y = 0, P_Z, P_Q1, P_AZ, P_F, P_G, P_R1, P_R1I, P_G2, P_R2, P_R2I, P_R, P_K, P_W,
-    P_VALS, P_INT, P_TMP, P_SEL, P_GEMMWS, P_SMALLWS, P_COUNT
+    P_VALS, P_INT, P_TMP, P_SEL, P_GEMMWS, P_SMALLWS, P_DDWS, P_COUNT
 };
+
+static_assert(P_COUNT <= 24, "sketch workspaces must stay below the PCG pool range (ops.cuh)");
 
 struct Timer {
     cudaStream_t st;
@@ -83,6 +87,7 @@ struct Ctx {
     DevBuf* pool;
     int* h_int;  // pinned scratch
     int shifted_calls = 0;  // orth() calls that needed shifted CholQR3
+    int dd_rank_calls = 0;  // rank probes decided on the double-double Gram
 
     double* buf(int id, size_t count) { return pool[id].get<double>(count); }
 
@@ -203,14 +208,22 @@ struct Ctx {
         return true;
     }
 
-    // rank probe: pivoted Cholesky of G (m x m); perm to P_INT[4..]
-    int rank_probe(const double* G, int64_t m, int** perm_out) {
+    // Rank probe of ColPivHouseholderQR (randevd.cpp:67-73, 89-92); perm to P_INT[4..].
+    // Fast path: a pivoted Cholesky of the double Gram G with a Gram-noise tolerance; it is
+    // conclusive when it finds full rank (cond(Y) <~ 1e6).  Otherwise, when Y is given, the
+    // rank is decided by Eigen's own rule on a double-double Gram (rank_dd.cu), so an
+    // ill-conditioned but full-rank sample (cond up to ~1/(m eps)) is accepted as Eigen does.
+    int rank_probe(const double* G, int64_t m, int** perm_out, const double* Y = nullptr) {
         tm.begin(T_SMALL);
         int* ints = reinterpret_cast<int*>(buf(P_INT, 4 + 2 * m));
         int* perm = ints + 4;
         const double tol_rel = 32.0 * std::sqrt((double)n) * 2.220446049250313e-16;
         pivoted_chol_rank((int)m, G, tol_rel, ints + 1, perm, pool[P_SMALLWS], st);
-        const int r = read_int(ints + 1);
+        int r = read_int(ints + 1);
+        if (r < m && Y) {
+            ++dd_rank_calls;
+            r = colpiv_rank_dd(n, (int)m, Y, n, perm, ints + 1, h_int, pool[P_DDWS], st);
+        }
         tm.end();
         *perm_out = perm;
         return r;
@@ -386,7 +399,7 @@ int64_t sketch_dev(wc4dvar_op& op, const wc4dvar_sketch_config& cfg, const doubl
         double* G = c.buf(P_G, m * m);
         c.gram(Y, m, Y, m, G);
         int* perm = nullptr;
-        const int r = c.rank_probe(G, m, &perm);
+        const int r = c.rank_probe(G, m, &perm, Y);
         if (r < m) {
             std::ostringstream msg;
             msg << "revd: sample matrix rank collapsed to " << r << " of " << m << " columns";
@@ -405,7 +418,7 @@ int64_t sketch_dev(wc4dvar_op& op, const wc4dvar_sketch_config& cfg, const doubl
         double* G = c.buf(P_G, m * m);
         c.gram(Y, m, Y, m, G);
         int* perm = nullptr;
-        const int r = c.rank_probe(G, m, &perm);
+        const int r = c.rank_probe(G, m, &perm, Y);
         if (r == 0) throw NumericalError("nystrom: sample matrix is zero");
         double* Z = bufA;
         double* other = bufB;
