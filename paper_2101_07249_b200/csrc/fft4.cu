@@ -348,7 +348,16 @@ __device__ __forceinline__ void stage_turn(double2* sm, const double2* __restric
 // ---- plans ---------------------------------------------------------------------------
 // N1: contiguous length (pass B, S rows per item), radices B0, BM..., BL (BMr = BM reversed).
 // N2: strided length (passes A / C, TC columns per item), radices A0, AM..., AL.
-struct PlanE6 {  // n = 1e6 (C4)
+// Columns (N2) take two register stages (one SMEM exchange per pass A / C); rows (N1) three.
+struct PlanE6 {  // n = 1e6 (C4): 250 = 10 x 25, 4000 = 20 x 20 x 10
+    static constexpr int N1 = 4000, N2 = 250, TC = 16, S = 1;
+    static constexpr int A0 = 10, AL = 25, B0 = 20, BL = 10;
+    using AM = RL<>;
+    using AMr = RL<>;
+    using BM = RL<20>;
+    using BMr = RL<20>;
+};
+struct PlanE6c3 {  // n = 1e6, three column stages (10 x 5 x 5): the round-1 plan (variant 1)
     static constexpr int N1 = 4000, N2 = 250, TC = 16, S = 1;
     static constexpr int A0 = 10, AL = 5, B0 = 20, BL = 10;
     using AM = RL<5>;
@@ -356,19 +365,19 @@ struct PlanE6 {  // n = 1e6 (C4)
     using BM = RL<20>;
     using BMr = RL<20>;
 };
-struct Plan2E6 {  // n = 2e6 (C5)
+struct Plan2E6 {  // n = 2e6 (C5): 500 = 20 x 25, 4000 = 20 x 20 x 10
     static constexpr int N1 = 4000, N2 = 500, TC = 8, S = 1;
-    static constexpr int A0 = 10, AL = 10, B0 = 20, BL = 10;
-    using AM = RL<5>;
-    using AMr = RL<5>;
+    static constexpr int A0 = 20, AL = 25, B0 = 20, BL = 10;
+    using AM = RL<>;
+    using AMr = RL<>;
     using BM = RL<20>;
     using BMr = RL<20>;
 };
-struct PlanE5 {  // n = 1e5 (C3)
+struct PlanE5 {  // n = 1e5 (C3): 250 = 10 x 25, 400 = 20 x 20
     static constexpr int N1 = 400, N2 = 250, TC = 16, S = 10;
-    static constexpr int A0 = 10, AL = 5, B0 = 20, BL = 20;
-    using AM = RL<5>;
-    using AMr = RL<5>;
+    static constexpr int A0 = 10, AL = 25, B0 = 20, BL = 20;
+    using AM = RL<>;
+    using AMr = RL<>;
     using BM = RL<>;
     using BMr = RL<>;
 };
@@ -402,6 +411,8 @@ struct Job {
     int l2hint;          // evict_last policy on Y + discard after pass C (WC4DVAR_FFT_L2HINT)
     int phase_mask;      // profiling aid (WC4DVAR_FFT_PHASES, default 7): passes whose items run
     int sub;             // tiles per ticket (WC4DVAR_FFT_SUB)
+    int acq;             // acquire loads on the dependency counters (WC4DVAR_FFT_ACQ, default 1)
+    int prefetch;        // L2 prefetch of the next pass-A tile (WC4DVAR_FFT_PREFETCH, default 0)
 };
 
 __device__ __forceinline__ double2 wN(const Job& jb, int64_t p) {  // w_N^p, 0 <= p < N
@@ -417,6 +428,14 @@ __device__ __forceinline__ unsigned ld_relaxed(const unsigned* p) {
     unsigned v;
     asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
     return v;
+}
+__device__ __forceinline__ unsigned ld_acquire(const unsigned* p) {
+    unsigned v;
+    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void prefetch_l2(const void* a) {
+    asm volatile("prefetch.global.L2::evict_normal [%0];" ::"l"(a));
 }
 // Y traffic stays in L2: stores / in-place loads with an evict_last policy, and pass C
 // discards each Y line after its last read (no write-back of dead data)
@@ -447,8 +466,10 @@ __device__ __forceinline__ void red_release(unsigned* p) {
     asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(p) : "memory");
 }
 
-template <class P>
-__device__ __forceinline__ void item_a(const Job& jb, double2* sm, int p, int tile) {
+// `af()` runs on every thread right after the first stage (its barrier passed, the stage's
+// global loads consumed): the deferred completion release and the next item's L2 prefetch
+template <class P, class AF>
+__device__ __forceinline__ void item_a(const Job& jb, double2* sm, int p, int tile, AF af) {
     using VA = ColView<P::N2, P::TC>;
     constexpr int64_t N = (int64_t)P::N1 * P::N2;
     const int2 cp = jb.pairs[p];
@@ -467,6 +488,7 @@ __device__ __forceinline__ void item_a(const Job& jb, double2* sm, int p, int ti
             return make_double2(__ldcs(x1 + j10 + seq + (int64_t)P::N1 * i), 0.0);
         });
     }
+    af();
     Mids<VA, false, P::A0, typename P::AM>::run(sm, jb.tw2);
     constexpr int LR = P::N2 / P::AL;
     stage_last<VA, P::AL, false>(sm, jb.tw2, [&](int seq, int j, double2(&v)[P::AL]) {
@@ -481,8 +503,8 @@ __device__ __forceinline__ void item_a(const Job& jb, double2* sm, int p, int ti
     });
 }
 
-template <class P>
-__device__ __forceinline__ void item_b(const Job& jb, double2* sm, int p, int rowblk) {
+template <class P, class AF>
+__device__ __forceinline__ void item_b(const Job& jb, double2* sm, int p, int rowblk, AF af) {
     using VB = RowView<P::N1, P::S>;
     constexpr int64_t N = (int64_t)P::N1 * P::N2;
     const int2 cp = jb.pairs[p];
@@ -493,6 +515,7 @@ __device__ __forceinline__ void item_b(const Job& jb, double2* sm, int p, int ro
     stage_first<VB, P::B0, false>(sm, [&](int seq, int i) {
         return ld_y(Yp + (int64_t)P::N1 * (k20 + seq) + i, pol);
     });
+    af();
     Mids<VB, false, P::B0, typename P::BM>::run(sm, jb.tw1);
     constexpr int LRt = P::N1 / P::BL;
     stage_turn<VB, P::BL>(sm, jb.tw1, [&](int seq, int j, double2(&v)[P::BL]) {
@@ -518,8 +541,8 @@ __device__ __forceinline__ void item_b(const Job& jb, double2* sm, int p, int ro
     });
 }
 
-template <class P>
-__device__ __forceinline__ void item_c(const Job& jb, double2* sm, int p, int tile) {
+template <class P, bool ADD, class AF>
+__device__ __forceinline__ void item_c(const Job& jb, double2* sm, int p, int tile, AF af) {
     using VA = ColView<P::N2, P::TC>;
     constexpr int64_t N = (int64_t)P::N1 * P::N2;
     const int2 cp = jb.pairs[p];
@@ -528,6 +551,7 @@ __device__ __forceinline__ void item_c(const Job& jb, double2* sm, int p, int ti
     stage_first<VA, P::AL, true>(sm, [&](int seq, int i) {
         return __ldcg(Yp + j10 + seq + (int64_t)P::N1 * i);
     });
+    af();
     if (jb.l2hint) {  // this tile's Y lines are dead: drop them from L2 without a write-back
         static_assert((P::TC * 16) % 128 == 0, "column tile must cover whole 128-byte lines");
         constexpr int lpr = P::TC * 16 / 128;
@@ -538,45 +562,52 @@ __device__ __forceinline__ void item_c(const Job& jb, double2* sm, int p, int ti
     Mids<VA, true, P::AL, typename P::AMr>::run(sm, jb.tw2);
     double* o1 = jb.out + vcol(cp.x, jb.per, jb.ldo, N) + j10;
     double* o2 = cp.y >= 0 ? jb.out + vcol(cp.y, jb.per, jb.ldo, N) + j10 : nullptr;
-    const double* d1 = jb.add ? jb.add + vcol(cp.x, jb.per, jb.ldadd, N) + j10 : nullptr;
-    const double* d2 = (jb.add && cp.y >= 0) ? jb.add + vcol(cp.y, jb.per, jb.ldadd, N) + j10 : nullptr;
+    const double* d1 = ADD ? jb.add + vcol(cp.x, jb.per, jb.ldadd, N) + j10 : nullptr;
+    const double* d2 = (ADD && cp.y >= 0) ? jb.add + vcol(cp.y, jb.per, jb.ldadd, N) + j10 : nullptr;
     constexpr int LR = P::N2 / P::A0;
     bool bad = false;
     stage_last<VA, P::A0, true>(sm, jb.tw2, [&](int seq, int j, double2(&v)[P::A0]) {
-        // add-term loads all issued before the first store (out may alias add, so the
-        // compiler cannot hoist them across the stores itself)
-        double a1[P::A0], a2[P::A0];
+        // add-term loads issued in chunks of CH ahead of the chunk's stores (out may alias
+        // add, so the compiler cannot hoist them across the stores itself; CH <= 10 bounds the
+        // registers they hold)
+        constexpr int CH = P::A0 <= 10 ? P::A0 : (P::A0 % 10 == 0 ? 10 : 5);
 #pragma unroll
-        for (int r = 0; r < P::A0; ++r) {
-            const int64_t g = seq + (int64_t)P::N1 * (j + r * LR);
-            a1[r] = d1 ? __ldcs(d1 + g) : 0.0;
-            a2[r] = d2 ? __ldcs(d2 + g) : 0.0;
-        }
+        for (int r0 = 0; r0 < P::A0; r0 += CH) {
+            double a1[CH], a2[CH];
+            if (ADD) {
 #pragma unroll
-        for (int r = 0; r < P::A0; ++r) {
-            const int64_t g = seq + (int64_t)P::N1 * (j + r * LR);
-            double y1 = v[r].x, y2 = v[r].y;
-            if (d1) {  // out = v + D^{1/2} s (operators.cpp:141)
-                y1 = a1[r] + y1;
-                bad |= !isfinite(y1);
-            }
-            __stcs(o1 + g, y1);
-            if (o2) {
-                if (d2) {
-                    y2 = a2[r] + y2;
-                    bad |= !isfinite(y2);
+                for (int r = 0; r < CH; ++r) {
+                    const int64_t g = seq + (int64_t)P::N1 * (j + (r0 + r) * LR);
+                    a1[r] = __ldcs(d1 + g);
+                    a2[r] = d2 ? __ldcs(d2 + g) : 0.0;
                 }
-                __stcs(o2 + g, y2);
+            }
+#pragma unroll
+            for (int r = 0; r < CH; ++r) {
+                const int64_t g = seq + (int64_t)P::N1 * (j + (r0 + r) * LR);
+                double y1 = v[r0 + r].x, y2 = v[r0 + r].y;
+                if (ADD) {  // out = v + D^{1/2} s (operators.cpp:141)
+                    y1 = a1[r] + y1;
+                    bad |= !isfinite(y1);
+                }
+                __stcs(o1 + g, y1);
+                if (o2) {
+                    if (ADD && d2) {
+                        y2 = a2[r] + y2;
+                        bad |= !isfinite(y2);
+                    }
+                    __stcs(o2 + g, y2);
+                }
             }
         }
     });
-    if (jb.status && bad) atomicOr(jb.status, ST_OUT_NONFINITE);
+    if (ADD && jb.status && bad) atomicOr(jb.status, ST_OUT_NONFINITE);
 }
 
-template <class P, int CPS>
+template <class P, int CPS, bool ADD>
 __global__ void __launch_bounds__(kThreads, CPS) fftconv_kernel(const Job jb) {
     extern __shared__ double2 sm[];
-    __shared__ unsigned s_ticket;
+    __shared__ unsigned s_ticket, s_next;
     // a ticket covers `sub` consecutive tiles (A / C) or row blocks (B) of one pair: fewer
     // tickets, so the per-ticket cost (ticket atomic, dependency read, two barriers, the
     // completion release) is paid once per `sub` tiles
@@ -605,7 +636,8 @@ __global__ void __launch_bounds__(kThreads, CPS) fftconv_kernel(const Job jb) {
     // counter item t waits for: A(g) reuses the Y slot of C(g - kSlots); B(g) needs A(g);
     // C(g) needs B(g).  Every awaited item holds a smaller ticket, and a CTA holds at most
     // one unstarted (prefetched) ticket while it runs a smaller one, so the smallest
-    // unfinished ticket always progresses: no deadlock.
+    // unfinished ticket always progresses: no deadlock (the deferred release below is
+    // flushed before any wait that is not already satisfied).
     auto dependency = [&](unsigned t, const unsigned*& dep, unsigned& need) {
         dep = nullptr;
         need = 0;
@@ -625,61 +657,100 @@ __global__ void __launch_bounds__(kThreads, CPS) fftconv_kernel(const Job jb) {
         }
     };
     // thread 0 owns the schedule: `next` is fetched one item ahead and its dependency
-    // counter is read at the end of the current item, so both round trips overlap work
+    // counter is read (acquire) at the end of the current item, so both round trips overlap
+    // work.  The completion release of an item is DEFERRED to just after the first stage of
+    // the following item: its MEMBAR then finds no outstanding global traffic of this warp
+    // instead of draining the item's last-stage stores while the whole CTA waits.
     unsigned next = 0, seen = 0, need = 0;
     const unsigned* dep = nullptr;
+    unsigned* pend = nullptr;
     if (threadIdx.x == 0) {
         next = atomicAdd(jb.ctr, 1u);
         dependency(next, dep, need);
-        if (dep) seen = ld_relaxed(dep);
+        if (dep) seen = jb.acq ? ld_acquire(dep) : ld_relaxed(dep);
     }
+    auto flush = [&]() {
+        if (threadIdx.x == 0 && pend) {
+            red_release(pend);
+            pend = nullptr;
+        }
+    };
+    auto after_first = [&]() {
+        flush();
+        if (!jb.prefetch) return;
+        // L2 prefetch of the next item's HBM input (pass A reads V; B / C read L2-resident Y)
+        int ph, g, r;
+        const unsigned nt = s_next;
+        if (nt >= total) return;
+        decode(nt, ph, g, r);
+        if (ph != 0 || g < 0 || g >= jb.ngroups) return;
+        const int p = g * jb.G + r / nA1;
+        if (p >= jb.np) return;
+        const int2 cp = jb.pairs[p];
+        constexpr int64_t N = (int64_t)P::N1 * P::N2;
+        const int j10 = (r % nA1) * jb.sub * P::TC;
+        const int lines = P::TC * 8 / 128 * jb.sub;  // 128-byte lines per row of the tile(s)
+        for (int e = threadIdx.x; e < P::N2 * lines * 2; e += kNT) {
+            const int col = e & 1, row = (e >> 1) / lines, l = (e >> 1) % lines;
+            const int c = col ? cp.y : cp.x;
+            if (c >= 0) prefetch_l2(jb.V + vcol(c, jb.per, jb.ldv, N) + j10 + (int64_t)P::N1 * row + l * 16);
+        }
+    };
     for (;;) {
         if (threadIdx.x == 0) {
-            if (dep) {
-                while (seen < need) {
-                    __nanosleep(64);
-                    seen = ld_relaxed(dep);
+            if (dep && seen < need) {
+                if (pend) {  // never wait while holding an unreleased item
+                    red_release(pend);
+                    pend = nullptr;
                 }
-                // acquire: pairs with the producers' red.release, so the Y lines they wrote
-                // are visible to this CTA's loads after the barrier below
-                asm volatile("fence.acq_rel.gpu;" ::: "memory");
+                do {
+                    __nanosleep(64);
+                    seen = jb.acq ? ld_acquire(dep) : ld_relaxed(dep);
+                } while (seen < need);
             }
             s_ticket = next;
         }
-        // Y is written with st.cg, published by red.release and read with ld.cg (L2, the
-        // coherence point) only after thread 0 observed the counter and this barrier
+        // Y is written with st.cg, published by red.release and read with ld.cg (L2) only
+        // after thread 0's acquire load observed the counter and this barrier
         __syncthreads();
         const unsigned t = s_ticket;
         if (t >= total) break;
-        if (threadIdx.x == 0) next = atomicAdd(jb.ctr, 1u);
+        if (threadIdx.x == 0) {
+            next = atomicAdd(jb.ctr, 1u);
+            s_next = next;  // read by after_first() behind the first stage's barrier
+        }
         int phase, g, r;
         decode(t, phase, g, r);
         const bool valid = g >= 0 && g < jb.ngroups;
+        bool ran = false;
         if (valid) {
             // pair index and the item inside it; groups are G consecutive pairs
             const int per_pair = phase == 1 ? nB1 : nA1;
             const int p = g * jb.G + r / per_pair, idx = r % per_pair;
             if (p < jb.np && ((jb.phase_mask >> phase) & 1)) {  // the last group may be partial
                 const int u0 = idx * jb.sub, u1 = min(u0 + jb.sub, phase == 1 ? tB : tA);
+                ran = true;
                 for (int u = u0; u < u1; ++u) {
                     if (u > u0) __syncthreads();  // the previous tile's last stage read SMEM
                     if (phase == 0) {
-                        item_a<P>(jb, sm, p, u);
+                        item_a<P>(jb, sm, p, u, after_first);
                     } else if (phase == 1) {
-                        item_b<P>(jb, sm, p, u);
+                        item_b<P>(jb, sm, p, u, after_first);
                     } else {
-                        item_c<P>(jb, sm, p, u);
+                        item_c<P, ADD>(jb, sm, p, u, after_first);
                     }
                 }
             }
         }
+        if (!ran) flush();  // no first stage ran: release the deferred item now
         if (threadIdx.x == 0) {
             dependency(next, dep, need);
-            if (dep) seen = ld_relaxed(dep);
+            if (dep) seen = jb.acq ? ld_acquire(dep) : ld_relaxed(dep);
         }
         __syncthreads();  // every store of the item issued; s_ticket read; SMEM free
-        if (threadIdx.x == 0 && valid) red_release(jb.ctr + 1 + 3 * g + phase);
+        if (threadIdx.x == 0 && valid) pend = jb.ctr + 1 + 3 * g + phase;
     }
+    if (threadIdx.x == 0 && pend) red_release(pend);
 }
 
 // lamT[k1 + N1 k2] = Re spec[min(k, N - k)] / N, k = k2 + N2 k1 (real even spectrum)
@@ -697,49 +768,51 @@ constexpr size_t smem_bytes() {
     return sizeof(double2) * (size_t)std::max(ColView<P::N2, P::TC>::SMEM, RowView<P::N1, P::S>::SMEM);
 }
 
-template <class P, int CPS>
+template <class P, int CPS, bool ADD>
 void launch_cps(const Job& jb, cudaStream_t st) {
     constexpr size_t sm = smem_bytes<P>();
     static_assert(sm <= 227 * 1024 / 2, "fftconv tile exceeds the per-CTA SMEM budget");
     static bool attr = false;
     if (!attr) {
-        W4_CUDA(cudaFuncSetAttribute(fftconv_kernel<P, CPS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+        W4_CUDA(cudaFuncSetAttribute(fftconv_kernel<P, CPS, ADD>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)sm));
         attr = true;
     }
     int dev = 0, nsm = kSMs, occ = 0;
     W4_CUDA(cudaGetDevice(&dev));
     W4_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
-    W4_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fftconv_kernel<P, CPS>, kThreads, sm));
+    W4_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fftconv_kernel<P, CPS, ADD>, kThreads, sm));
     const int64_t items = (int64_t)(jb.ngroups + 2) * jb.G *
                           (2 * ((P::N1 / P::TC + jb.sub - 1) / jb.sub) + (P::N2 / P::S + jb.sub - 1) / jb.sub);
     const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(items, (int64_t)nsm * std::max(occ, 1)));
-    fftconv_kernel<P, CPS><<<grid, kThreads, sm, st>>>(jb);
+    fftconv_kernel<P, CPS, ADD><<<grid, kThreads, sm, st>>>(jb);
     W4_LAUNCH();
 }
 
 // WC4DVAR_FFT_CPS: register budget as CTAs per SM (1: ~250 registers, no spills; 2: 128
-// registers (default); 3: ~104 registers)
+// registers (default); 3 (~104 registers) spilled heavily and was dropped)
 template <class P>
 void launch(const Job& jb, cudaStream_t st) {
     static const int cps = [] {
         const char* e = std::getenv("WC4DVAR_FFT_CPS");
         return e ? std::atoi(e) : kCtaPerSm;
     }();
-    if (cps == 1) return launch_cps<P, 1>(jb, st);
-    if (cps == 3) return launch_cps<P, 3>(jb, st);
-    return launch_cps<P, 2>(jb, st);
+    if (jb.add) return cps == 1 ? launch_cps<P, 1, true>(jb, st) : launch_cps<P, 2, true>(jb, st);
+    return cps == 1 ? launch_cps<P, 1, false>(jb, st) : launch_cps<P, 2, false>(jb, st);
 }
 
 struct PlanInfo {
+    int variant;  // WC4DVAR_FFT_VARIANT selects among plans of the same length (0 = default)
     int64_t N1, N2;
     size_t smem;
     void (*run)(const Job&, cudaStream_t);
 };
 const PlanInfo kPlans[] = {
-    {PlanE6::N1, PlanE6::N2, smem_bytes<PlanE6>(), launch<PlanE6>},
-    {Plan2E6::N1, Plan2E6::N2, smem_bytes<Plan2E6>(), launch<Plan2E6>},
-    {PlanE5::N1, PlanE5::N2, smem_bytes<PlanE5>(), launch<PlanE5>},
-    {PlanE4::N1, PlanE4::N2, smem_bytes<PlanE4>(), launch<PlanE4>},
+    {0, PlanE6::N1, PlanE6::N2, smem_bytes<PlanE6>(), launch<PlanE6>},
+    {1, PlanE6c3::N1, PlanE6c3::N2, smem_bytes<PlanE6c3>(), launch<PlanE6c3>},
+    {0, Plan2E6::N1, Plan2E6::N2, smem_bytes<Plan2E6>(), launch<Plan2E6>},
+    {0, PlanE5::N1, PlanE5::N2, smem_bytes<PlanE5>(), launch<PlanE5>},
+    {0, PlanE4::N1, PlanE4::N2, smem_bytes<PlanE4>(), launch<PlanE4>},
 };
 
 }  // namespace
@@ -752,8 +825,12 @@ Fft4::~Fft4() {
 
 bool Fft4::init(int64_t N, const double2* const spec_half[4], cudaStream_t st) {
     int plan = -1;
+    static const int variant = [] {
+        const char* e = std::getenv("WC4DVAR_FFT_VARIANT");
+        return e ? std::atoi(e) : 0;
+    }();
     for (int i = 0; i < (int)(sizeof(kPlans) / sizeof(kPlans[0])); ++i)
-        if (kPlans[i].N1 * kPlans[i].N2 == N) plan = i;
+        if (kPlans[i].N1 * kPlans[i].N2 == N && (plan < 0 || kPlans[i].variant == variant)) plan = i;
     if (plan < 0) return false;
     const int64_t N1 = kPlans[plan].N1, N2 = kPlans[plan].N2;
     const long double two_pi = 6.283185307179586476925286766559L;
@@ -868,8 +945,16 @@ void Fft4::apply(bool inv, int Nsw, const double* V, int64_t ldv, int64_t m, dou
         const char* e = std::getenv("WC4DVAR_FFT_SUB");
         return e ? std::max(1, std::atoi(e)) : 1;
     }();
+    static const int acq = [] {
+        const char* e = std::getenv("WC4DVAR_FFT_ACQ");
+        return e ? std::atoi(e) : 1;
+    }();
+    static const int prefetch = [] {
+        const char* e = std::getenv("WC4DVAR_FFT_PREFETCH");
+        return e ? std::atoi(e) : 0;  // measured: 13.7 ms without vs 14.0 ms with (C4 m = 64)
+    }();
     Job jb{V, ldv, out, ldo, add, ldadd, add ? status : nullptr, dpairs, np, per, G, ngroups,
-           lamB, lamQ, Y, tw1_, tw2_, tlo_, thi_, ctr, l2hint, phase_mask, sub};
+           lamB, lamQ, Y, tw1_, tw2_, tlo_, thi_, ctr, l2hint, phase_mask, sub, acq, prefetch};
     kPlans[plan_].run(jb, st);
 }
 
