@@ -456,26 +456,57 @@ __device__ __forceinline__ void cp8(double* dst, const double* src) {
     asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(d), "l"(src));
 }
 
+// Row loads of the blocked tiles: element e = tid + k nt (k < P) of a region row goes to
+// slot(e).  With nt % P == 0 (every launch shape but test overrides) the slot is
+// s0 + k nt / P and the grid index is fixed per thread, so the per-element work is one
+// address IMAD and the cp.async; the periodic wrap is resolved once per launch.
+template <int P, int NT>
+struct RowPlan {
+    int s0;      // slot of element tid
+    int goff[P]; // grid index of element tid + k nt
+    bool fast;   // nt % P == 0 && R == nt P
+    __device__ void init(const Region& rg, int R, int tid, int nt, int ns) {
+        fast = nt % P == 0 && R == nt * P;
+        s0 = (tid % P) * ns + tid / P;
+#pragma unroll
+        for (int k = 0; k < P; ++k) goff[k] = rg.gidx(min(tid + k * nt, R - 1));
+    }
+    template <class Slot>
+    __device__ __forceinline__ void load(double* dst, const double* row, const Region& rg, int R, int tid, int nt,
+                                         Slot slot) const {
+        if (fast) {
+            const int step = (NT ? NT : nt) / P;
+#pragma unroll
+            for (int k = 0; k < P; ++k) cp8(dst + s0 + k * step, row + goff[k]);
+        } else {
+            for (int e = tid; e < R; e += nt) cp8(dst + slot(e), row + rg.gidx(e));
+        }
+        asm volatile("cp.async.commit_group;\n");
+    }
+};
+
 // Each CTA runs intervals i0..i1 of one tile of one column.  Per interval: one barrier,
 // then (a) a coalesced pass that emits the previous state's tile centre (finite check,
 // trajectory, observations -- stores coalesced instead of stride-P per thread), (b) the
 // next interval's forcing row issued by cp.async into a double buffer (lands while the S
-// sub-steps compute), (c) the register-blocked advance.
-template <int KIND, int S, int P>
+// sub-steps compute), (c) the register-blocked advance.  Every thread advances all its P
+// points every interval: points that left the valid region (S per side per interval) only
+// ever feed other invalid points and are never emitted, so no per-point validity test is
+// needed.  NT = threads per CTA as a compile-time constant (0: blockDim.x).
+template <int KIND, int S, int P, int NT>
 __global__ void __launch_bounds__(512) tiled_blk_fwd_kernel(const TiledArgs ta, unsigned* status) {
     extern __shared__ double sm[];
-    const ModelDev& md = ta.md;
     const NetDev& net = ta.net;
     const SweepArgs& a = ta.a;
     const TileGeom& geo = ta.geo;
     const int R = geo.R;
-    const int tid = threadIdx.x, nt = blockDim.x;
+    const int tid = threadIdx.x, nt = NT ? NT : blockDim.x;
     const int ns = nt + 2, RS = P * ns;
     double* cur = sm;
     double* nxt = sm + RS;
     double* const fx0 = sm + 2 * RS;  // forcing X_{i+1}, prefetched (double buffer)
     double* const fx1 = sm + 3 * RS;
-    const int n = (int)md.n;
+    const int n = (int)ta.md.n;
     const int64_t col = blockIdx.x;
     const int64_t t0 = (int64_t)blockIdx.y * geo.T;
     const Region rg{R, false, (int)(t0 - geo.HL), n};
@@ -489,27 +520,16 @@ __global__ void __launch_bounds__(512) tiled_blk_fwd_kernel(const TiledArgs ta, 
     bool bad = false;
     double v[P + 2 * S];
     auto slot = [&](int e) { return (e % P) * ns + e / P; };
-    // element e = tid + k nt: when nt % P == 0 its slot advances by nt / P and its grid
-    // index by nt (one periodic wrap at most), so the loops run on increments
-    const bool inc = nt % P == 0;
-    auto load_row = [&](double* dst, const double* row) {
-        if (inc) {
-            int s = slot(tid), g = rg.gidx(tid);
-            for (int e = tid; e < R; e += nt, s += nt / P) {
-                cp8(dst + s, row + g);
-                g += nt;
-                if (g >= n) g -= n;
-            }
-        } else {
-            for (int e = tid; e < R; e += nt) cp8(dst + slot(e), row + rg.gidx(e));
-        }
-        asm volatile("cp.async.commit_group;\n");
-    };
+    RowPlan<P, NT> rp;
+    rp.init(rg, R, tid, nt, ns);
+    // regular network: observed points g = bb sx of the tile centre [g0, g1), bb from bb0
+    const int sx = net.sx;
+    const int g0 = (int)t0, g1 = (int)(t0 + (c_hi - c_lo));
+    const int bb0 = sx ? (g0 + sx - 1) / sx : 0;
 
-    if (ta.i1 > ta.i0) load_row(fx0, X + (int64_t)(ta.i0 + 1) * n);
+    if (ta.i1 > ta.i0) rp.load(fx0, X + (int64_t)(ta.i0 + 1) * n, rg, R, tid, nt, slot);
     const double* src = ta.bin ? ta.bin + col * n : X;  // x_0 = X_0
     for (int e = tid; e < R; e += nt) cur[slot(e)] = src[rg.gidx(e)];
-    int lo = 0, hi = R;
     for (int i = ta.i0;; ++i) {
         cp_async_wait_all();
         __syncthreads();
@@ -521,43 +541,31 @@ __global__ void __launch_bounds__(512) tiled_blk_fwd_kernel(const TiledArgs ta, 
             const int sl = net.slot[i];
             double* tri = tr ? tr + (int64_t)i * n : nullptr;
             const bool last = i == ta.i1;
-            if (tri || last || (a.fwd_obs && sl >= 0 && !net.sx)) {
+            if (tri || last || (a.fwd_obs && sl >= 0 && !sx)) {
                 for (int e = c_lo + tid; e < c_hi; e += nt) {
                     const int g = rg.gidx(e);
                     const double x = cur[slot(e)];
                     if (last) bad |= !isfinite(x);
                     if (tri) tri[g] = x;
-                    if (a.fwd_obs && sl >= 0 && !net.sx) {
+                    if (a.fwd_obs && sl >= 0 && !sx) {
                         const int bb = net.pmap[g];
                         if (bb >= 0) Yc[(int64_t)sl * np + bb] = a.scale_fwd * x;
                     }
                 }
             }
-            if (a.fwd_obs && sl >= 0 && net.sx) {
-                // observed points g = bb sx inside the tile centre [t0, t0 + (c_hi - c_lo))
-                const int sx = net.sx;
-                const int g0 = (int)t0, g1 = (int)(t0 + (c_hi - c_lo));
-                for (int bb = (g0 + sx - 1) / sx + tid; bb * sx < g1; bb += nt) {
-                    const int e = bb * sx - g0 + c_lo;
-                    Yc[(int64_t)sl * np + bb] = a.scale_fwd * cur[slot(e)];
-                }
+            if (a.fwd_obs && sl >= 0 && sx) {
+                double* ys = Yc + (int64_t)sl * np;
+                for (int bb = bb0 + tid; bb * sx < g1; bb += nt) ys[bb] = a.scale_fwd * cur[slot(bb * sx - g0 + c_lo)];
             }
         }
         if (i == ta.i1) break;
         const int k = i - ta.i0;
-        if (i + 2 <= ta.i1) load_row((k & 1) ? fx0 : fx1, X + (int64_t)(i + 2) * n);
-        lo += S;
-        hi -= S;
-        if (b + P > lo && b < hi) {
-            blk_conv<S, P>(cur, b, R, ns, ta.tp, v);  // M_i = the S-step TL as one stencil
-            const double* f = (k & 1) ? fx1 : fx0;
+        if (i + 2 <= ta.i1) rp.load((k & 1) ? fx0 : fx1, X + (int64_t)(i + 2) * n, rg, R, tid, nt, slot);
+        blk_conv<S, P>(cur, b, R, ns, ta.tp, v);  // M_i = the S-step TL as one stencil
+        const double* f = (k & 1) ? fx1 : fx0;
 #pragma unroll
-            for (int p = 0; p < P; ++p) {
-                const int e = b + p;
-                if (e >= lo && e < hi)  // x_{i+1} = M_i x_i + X_{i+1}  (operators.cpp:88)
-                    nxt[p * ns + tid] = v[S + p] + f[p * ns + tid];
-            }
-        }
+        for (int p = 0; p < P; ++p)  // x_{i+1} = M_i x_i + X_{i+1}  (operators.cpp:88)
+            nxt[p * ns + tid] = v[S + p] + f[p * ns + tid];
         double* t = cur;
         cur = nxt;
         nxt = t;
@@ -567,21 +575,20 @@ __global__ void __launch_bounds__(512) tiled_blk_fwd_kernel(const TiledArgs ta, 
     if (__syncthreads_or(bad) && tid == 0) atomicOr(status, ST_FWD_NONFINITE);
 }
 
-template <int KIND, int S, int P>
+template <int KIND, int S, int P, int NT>
 __global__ void __launch_bounds__(512) tiled_blk_adj_kernel(const TiledArgs ta, unsigned* status) {
     extern __shared__ double sm[];
-    const ModelDev& md = ta.md;
     const NetDev& net = ta.net;
     const SweepArgs& a = ta.a;
     const TileGeom& geo = ta.geo;
     const int R = geo.R;
-    const int tid = threadIdx.x, nt = blockDim.x;
+    const int tid = threadIdx.x, nt = NT ? NT : blockDim.x;
     const int ns = nt + 2, RS = P * ns;
     double* cur = sm;
     double* nxt = sm + RS;
     double* const vb0 = sm + 2 * RS;  // v_{i-1} rows, prefetched (double buffer)
     double* const vb1 = sm + 3 * RS;
-    const int n = (int)md.n;
+    const int n = (int)ta.md.n;
     const int64_t col = blockIdx.x;
     const int64_t t0 = (int64_t)blockIdx.y * geo.T;
     const Region rg{R, false, (int)(t0 - geo.HR), n};
@@ -595,22 +602,8 @@ __global__ void __launch_bounds__(512) tiled_blk_adj_kernel(const TiledArgs ta, 
     bool bad = false;
     double v[P + 2 * S];
     auto slot = [&](int e) { return (e % P) * ns + e / P; };
-    // element e = tid + k nt: when nt % P == 0 its slot advances by nt / P and its grid
-    // index by nt (one periodic wrap at most), so the loops run on increments
-    const bool inc = nt % P == 0;
-    auto load_row = [&](double* dst, const double* row) {
-        if (inc) {
-            int s = slot(tid), g = rg.gidx(tid);
-            for (int e = tid; e < R; e += nt, s += nt / P) {
-                cp8(dst + s, row + g);
-                g += nt;
-                if (g >= n) g -= n;
-            }
-        } else {
-            for (int e = tid; e < R; e += nt) cp8(dst + slot(e), row + rg.gidx(e));
-        }
-        asm volatile("cp.async.commit_group;\n");
-    };
+    RowPlan<P, NT> rp;
+    if (V) rp.init(rg, R, tid, nt, ns);
     // H_i^T y part of the addend (sparse: observed points of observed times)
     auto obs_add = [&](int i, int g, double x) -> double {
         if (a.adj_obs) {
@@ -628,8 +621,14 @@ __global__ void __launch_bounds__(512) tiled_blk_adj_kernel(const TiledArgs ta, 
         }
         return x;
     };
+    // regular network: the thread's first point g_b = q_b sx + r_b (interval-invariant)
+    const int sx = net.sx;
+    const int g_b = rg.gidx(b < R ? b : R - 1);
+    const int q_b = sx ? g_b / sx : 0, r_b = sx ? g_b - q_b * sx : 0;
+    // tile centre rows are contiguous in the grid (no wrap): g = t0 + (e - c_lo)
+    const bool inc = nt % P == 0;
 
-    if (V && ta.i1 > ta.i0) load_row(vb0, V + (int64_t)(ta.i1 - 1) * n);
+    if (V && ta.i1 > ta.i0) rp.load(vb0, V + (int64_t)(ta.i1 - 1) * n, rg, R, tid, nt, slot);
     if (ta.bin) {
         for (int e = tid; e < R; e += nt) cur[slot(e)] = ta.bin[col * n + rg.gidx(e)];
     } else {  // s_N = v_N + H_N^T y
@@ -638,14 +637,13 @@ __global__ void __launch_bounds__(512) tiled_blk_adj_kernel(const TiledArgs ta, 
             cur[slot(e)] = obs_add(ta.i1, g, V ? V[(int64_t)ta.i1 * n + g] : 0.0);
         }
     }
-    int lo = 0, hi = R;
     for (int i = ta.i1;; --i) {  // cur = s_i
         cp_async_wait_all();
         __syncthreads();
         if (i < ta.i1 || !ta.bin) {  // emit s_i on the tile centre (finite check: last state)
             const bool last = i == ta.i0;
             double* Si = Sv + (int64_t)i * n;
-            if (inc) {  // the tile centre does not wrap: g = t0 + (e - c_lo)
+            if (inc) {
                 int s = slot(c_lo + tid);
                 for (int e = c_lo + tid; e < c_hi; e += nt, s += nt / P) {
                     const double x = cur[s];
@@ -662,50 +660,43 @@ __global__ void __launch_bounds__(512) tiled_blk_adj_kernel(const TiledArgs ta, 
         }
         if (i == ta.i0) break;
         const int k = ta.i1 - i;
-        if (V && i - 2 >= ta.i0) load_row((k & 1) ? vb0 : vb1, V + (int64_t)(i - 2) * n);
-        lo += S;
-        hi -= S;
-        if (b + P > lo && b < hi) {
-            // H^T y of the thread's P points first: all y loads in flight before the stencil
-            // (the loads' latency then hides under the FMA chains)
-            const int sl = a.adj_obs ? net.slot[i - 1] : -1;
-            double yv[P];
-            bool has[P];
-            if (sl >= 0) {
-                const double* ys = Yc + (int64_t)sl * np;
-                if (net.sx) {  // regular network: observed iff g % sx == 0, bb = g / sx
-                    int g = rg.gidx(b), q = g / net.sx, r = g - q * net.sx;
+        if (V && i - 2 >= ta.i0) rp.load((k & 1) ? vb0 : vb1, V + (int64_t)(i - 2) * n, rg, R, tid, nt, slot);
+        // H^T y of the thread's P points first: all y loads in flight before the stencil
+        // (the loads' latency then hides under the FMA chains)
+        const int sl = a.adj_obs ? net.slot[i - 1] : -1;
+        double yv[P];
+        bool has[P];
+        if (sl >= 0) {
+            const double* ys = Yc + (int64_t)sl * np;
+            if (sx) {  // regular network: observed iff g % sx == 0, bb = g / sx
+                int g = g_b, q = q_b, r = r_b;
 #pragma unroll
-                    for (int p = 0; p < P; ++p) {
-                        has[p] = r == 0;
-                        yv[p] = has[p] ? ys[q] : 0.0;
-                        if (++g == n) g = q = r = 0;  // periodic wrap
-                        else if (++r == net.sx) r = 0, ++q;
-                    }
-                } else {
-#pragma unroll
-                    for (int p = 0; p < P; ++p) {
-                        const int bb = net.pmap[rg.gidx(b + p)];
-                        has[p] = bb >= 0;
-                        yv[p] = has[p] ? ys[bb] : 0.0;
-                    }
+                for (int p = 0; p < P; ++p) {
+                    has[p] = r == 0;
+                    yv[p] = has[p] ? ys[q] : 0.0;
+                    if (++g == n) g = q = r = 0;  // periodic wrap
+                    else if (++r == sx) r = 0, ++q;
                 }
             } else {
 #pragma unroll
-                for (int p = 0; p < P; ++p) has[p] = false, yv[p] = 0.0;
-            }
-            blk_conv<S, P>(cur, b, R, ns, ta.tp, v);  // M_i^T as one stencil
-            const double* vr = (k & 1) ? vb1 : vb0;
-#pragma unroll
-            for (int p = 0; p < P; ++p) {
-                const int e = b + p;
-                if (e >= lo && e < hi) {
-                    // s_{i-1} = v_{i-1} + H^T y + M^T s_i  (operators.cpp:99; obs_add order)
-                    double ad = V ? vr[p * ns + tid] : 0.0;
-                    if (has[p]) ad = V ? ad + yv[p] : yv[p];
-                    nxt[p * ns + tid] = ad + v[S + p];
+                for (int p = 0; p < P; ++p) {
+                    const int bb = net.pmap[rg.gidx(min(b + p, R - 1))];
+                    has[p] = bb >= 0;
+                    yv[p] = has[p] ? ys[bb] : 0.0;
                 }
             }
+        } else {
+#pragma unroll
+            for (int p = 0; p < P; ++p) has[p] = false, yv[p] = 0.0;
+        }
+        blk_conv<S, P>(cur, b, R, ns, ta.tp, v);  // M_i^T as one stencil
+        const double* vr = (k & 1) ? vb1 : vb0;
+#pragma unroll
+        for (int p = 0; p < P; ++p) {
+            // s_{i-1} = v_{i-1} + H^T y + M^T s_i  (operators.cpp:99; obs_add order)
+            double ad = V ? vr[p * ns + tid] : 0.0;
+            if (has[p]) ad = V ? ad + yv[p] : yv[p];
+            nxt[p * ns + tid] = ad + v[S + p];
         }
         double* t = cur;
         cur = nxt;
@@ -748,8 +739,8 @@ bool launch_tiled_blk(const ModelDev& md, const NetDev& net, const SweepArgs& a,
     if (nt > 512 || T <= 0 || R > md.n) return false;
     TileGeom geo{T, K * S, K * S, R, false, cdiv(md.n, T)};
     const size_t smem = sizeof(double) * 4 * (size_t)P * (nt + 2);  // cur, nxt, 2 prefetch rows
-    auto fk = tiled_blk_fwd_kernel<KIND, S, P>;
-    auto ak = tiled_blk_adj_kernel<KIND, S, P>;
+    auto fk = nt == 512 ? tiled_blk_fwd_kernel<KIND, S, P, 512> : tiled_blk_fwd_kernel<KIND, S, P, 0>;
+    auto ak = nt == 512 ? tiled_blk_adj_kernel<KIND, S, P, 512> : tiled_blk_adj_kernel<KIND, S, P, 0>;
     W4_CUDA(cudaFuncSetAttribute(fk, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     W4_CUDA(cudaFuncSetAttribute(ak, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     const int nl = (int)cdiv(md.N, K);
