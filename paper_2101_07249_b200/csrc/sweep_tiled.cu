@@ -457,27 +457,28 @@ __device__ __forceinline__ void cp8(double* dst, const double* src) {
 }
 
 // Row loads of the blocked tiles: element e = tid + k nt (k < P) of a region row goes to
-// slot(e).  With nt % P == 0 (every launch shape but test overrides) the slot is
-// s0 + k nt / P and the grid index is fixed per thread, so the per-element work is one
-// address IMAD and the cp.async; the periodic wrap is resolved once per launch.
+// slot(e).  With nt % P == 0 and a region that does not cross the periodic boundary (every
+// tile but the first and last of a column), the slot is s0 + k nt / P and the grid index
+// origin + tid + k nt, so the loop is cp.async with immediate offsets on both sides.
 template <int P, int NT>
 struct RowPlan {
-    int s0;      // slot of element tid
-    int goff[P]; // grid index of element tid + k nt
-    bool fast;   // nt % P == 0 && R == nt P
+    int s0;    // slot of element tid
+    int g0;    // grid index of element tid
+    bool fast;
     __device__ void init(const Region& rg, int R, int tid, int nt, int ns) {
-        fast = nt % P == 0 && R == nt * P;
+        fast = nt % P == 0 && R == nt * P && rg.origin >= 0 && rg.origin + R <= rg.n;
         s0 = (tid % P) * ns + tid / P;
-#pragma unroll
-        for (int k = 0; k < P; ++k) goff[k] = rg.gidx(min(tid + k * nt, R - 1));
+        g0 = rg.origin + tid;
     }
     template <class Slot>
     __device__ __forceinline__ void load(double* dst, const double* row, const Region& rg, int R, int tid, int nt,
                                          Slot slot) const {
         if (fast) {
-            const int step = (NT ? NT : nt) / P;
+            const int w = NT ? NT : nt;
+            const double* src = row + g0;
+            double* d = dst + s0;
 #pragma unroll
-            for (int k = 0; k < P; ++k) cp8(dst + s0 + k * step, row + goff[k]);
+            for (int k = 0; k < P; ++k) cp8(d + k * (w / P), src + k * w);
         } else {
             for (int e = tid; e < R; e += nt) cp8(dst + slot(e), row + rg.gidx(e));
         }
@@ -494,7 +495,7 @@ struct RowPlan {
 // ever feed other invalid points and are never emitted, so no per-point validity test is
 // needed.  NT = threads per CTA as a compile-time constant (0: blockDim.x).
 template <int KIND, int S, int P, int NT>
-__global__ void __launch_bounds__(512) tiled_blk_fwd_kernel(const TiledArgs ta, unsigned* status) {
+__global__ void __launch_bounds__(NT ? NT : 512, NT == 256 ? 2 : 1) tiled_blk_fwd_kernel(const TiledArgs ta, unsigned* status) {
     extern __shared__ double sm[];
     const NetDev& net = ta.net;
     const SweepArgs& a = ta.a;
@@ -576,7 +577,7 @@ __global__ void __launch_bounds__(512) tiled_blk_fwd_kernel(const TiledArgs ta, 
 }
 
 template <int KIND, int S, int P, int NT>
-__global__ void __launch_bounds__(512) tiled_blk_adj_kernel(const TiledArgs ta, unsigned* status) {
+__global__ void __launch_bounds__(NT ? NT : 512, NT == 256 ? 2 : 1) tiled_blk_adj_kernel(const TiledArgs ta, unsigned* status) {
     extern __shared__ double sm[];
     const NetDev& net = ta.net;
     const SweepArgs& a = ta.a;
@@ -625,6 +626,13 @@ __global__ void __launch_bounds__(512) tiled_blk_adj_kernel(const TiledArgs ta, 
     const int sx = net.sx;
     const int g_b = rg.gidx(b < R ? b : R - 1);
     const int q_b = sx ? g_b / sx : 0, r_b = sx ? g_b - q_b * sx : 0;
+    // H^T y fast path (no addend v, regular network with sx >= P / 2, region not wrapping):
+    // the thread's observed points are op and op + sx (< P), y indices qf, qf + 1.  The
+    // stencil result is stored first and y added in place by the owner thread: y + M^T s
+    // either way (addition commutes), without per-point selects.
+    const bool fobs_ok = !V && sx >= P / 2 && rg.origin >= 0 && rg.origin + R <= n;
+    const int op = sx ? (sx - r_b) % sx : P;
+    const int qf = q_b + (r_b ? 1 : 0);
     // tile centre rows are contiguous in the grid (no wrap): g = t0 + (e - c_lo)
     const bool inc = nt % P == 0;
 
@@ -664,9 +672,17 @@ __global__ void __launch_bounds__(512) tiled_blk_adj_kernel(const TiledArgs ta, 
         // H^T y of the thread's P points first: all y loads in flight before the stencil
         // (the loads' latency then hides under the FMA chains)
         const int sl = a.adj_obs ? net.slot[i - 1] : -1;
+        const bool fobs = fobs_ok && sl >= 0;
+        double y0 = 0.0, y1 = 0.0;
         double yv[P];
         bool has[P];
-        if (sl >= 0) {
+        if (fobs) {
+            const double* ys = Yc + (int64_t)sl * np;
+            if (op < P) y0 = ys[qf];
+            if (op + sx < P) y1 = ys[qf + 1];
+#pragma unroll
+            for (int p = 0; p < P; ++p) has[p] = false, yv[p] = 0.0;
+        } else if (sl >= 0) {
             const double* ys = Yc + (int64_t)sl * np;
             if (sx) {  // regular network: observed iff g % sx == 0, bb = g / sx
                 int g = g_b, q = q_b, r = r_b;
@@ -691,12 +707,19 @@ __global__ void __launch_bounds__(512) tiled_blk_adj_kernel(const TiledArgs ta, 
         }
         blk_conv<S, P>(cur, b, R, ns, ta.tp, v);  // M_i^T as one stencil
         const double* vr = (k & 1) ? vb1 : vb0;
+        if (fobs) {
 #pragma unroll
-        for (int p = 0; p < P; ++p) {
-            // s_{i-1} = v_{i-1} + H^T y + M^T s_i  (operators.cpp:99; obs_add order)
-            double ad = V ? vr[p * ns + tid] : 0.0;
-            if (has[p]) ad = V ? ad + yv[p] : yv[p];
-            nxt[p * ns + tid] = ad + v[S + p];
+            for (int p = 0; p < P; ++p) nxt[p * ns + tid] = v[S + p];
+            if (op < P) nxt[op * ns + tid] += y0;
+            if (op + sx < P) nxt[(op + sx) * ns + tid] += y1;
+        } else {
+#pragma unroll
+            for (int p = 0; p < P; ++p) {
+                // s_{i-1} = v_{i-1} + H^T y + M^T s_i  (operators.cpp:99; obs_add order)
+                double ad = V ? vr[p * ns + tid] : 0.0;
+                if (has[p]) ad = V ? ad + yv[p] : yv[p];
+                nxt[p * ns + tid] = ad + v[S + p];
+            }
         }
         double* t = cur;
         cur = nxt;
@@ -713,11 +736,13 @@ template <int KIND, int S>
 bool launch_tiled_blk(const ModelDev& md, const NetDev& net, const SweepArgs& a, unsigned* status,
                       cudaStream_t st, DevBuf& ws, int tile_override) {
     constexpr int P = 8;
-    // WC4DVAR_TILED_NT: threads per CTA (512 default: one CTA per SM); WC4DVAR_TILED_KDIV:
-    // halo budget R / KDIV for the intervals per launch (4 default)
+    // WC4DVAR_TILED_NT: threads per CTA (256 default: two CTAs per SM, whose interval
+    // barriers interleave -- C4 m = 64 sweeps 8.6 vs 9.3 ms with one 512-thread CTA); both
+    // widths have compile-time instantiations.  WC4DVAR_TILED_KDIV: halo budget R / KDIV for
+    // the intervals per launch (4 default)
     static const int nt_env = [] {
         const char* e = std::getenv("WC4DVAR_TILED_NT");
-        return e ? std::atoi(e) : 512;
+        return e ? std::atoi(e) : 256;
     }();
     static const int kdiv = [] {
         const char* e = std::getenv("WC4DVAR_TILED_KDIV");
@@ -739,8 +764,10 @@ bool launch_tiled_blk(const ModelDev& md, const NetDev& net, const SweepArgs& a,
     if (nt > 512 || T <= 0 || R > md.n) return false;
     TileGeom geo{T, K * S, K * S, R, false, cdiv(md.n, T)};
     const size_t smem = sizeof(double) * 4 * (size_t)P * (nt + 2);  // cur, nxt, 2 prefetch rows
-    auto fk = nt == 512 ? tiled_blk_fwd_kernel<KIND, S, P, 512> : tiled_blk_fwd_kernel<KIND, S, P, 0>;
-    auto ak = nt == 512 ? tiled_blk_adj_kernel<KIND, S, P, 512> : tiled_blk_adj_kernel<KIND, S, P, 0>;
+    auto fk = nt == 512 ? tiled_blk_fwd_kernel<KIND, S, P, 512>
+              : nt == 256 ? tiled_blk_fwd_kernel<KIND, S, P, 256> : tiled_blk_fwd_kernel<KIND, S, P, 0>;
+    auto ak = nt == 512 ? tiled_blk_adj_kernel<KIND, S, P, 512>
+              : nt == 256 ? tiled_blk_adj_kernel<KIND, S, P, 256> : tiled_blk_adj_kernel<KIND, S, P, 0>;
     W4_CUDA(cudaFuncSetAttribute(fk, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     W4_CUDA(cudaFuncSetAttribute(ak, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     const int nl = (int)cdiv(md.N, K);
