@@ -41,7 +41,7 @@ namespace {
 constexpr int kNT = 200;       // threads per CTA (butterfly mapping, every item kind)
 constexpr int kThreads = kNT;
 constexpr int kCtaPerSm = 2;  // CTAs per SM (register budget)
-constexpr int kSlots = 4;     // Y slots in flight: A(g) reuses the slot of C(g - 4), two steps earlier
+constexpr int kSlots = 4;     // Y slots in flight (default): A(g) reuses the slot of C(g - 4), two steps earlier
 
 __device__ __forceinline__ void cbar() { __syncthreads(); }
 
@@ -412,6 +412,7 @@ struct Job {
     int phase_mask;      // profiling aid (WC4DVAR_FFT_PHASES, default 7): passes whose items run
     int sub;             // tiles per ticket (WC4DVAR_FFT_SUB)
     int acq;             // acquire loads on the dependency counters (WC4DVAR_FFT_ACQ, default 1)
+    int slots;           // Y slots (WC4DVAR_FFT_SLOTS, default kSlots; >= 3)
     int prefetch;        // L2 prefetch of the next pass-A tile (WC4DVAR_FFT_PREFETCH, default 0)
 };
 
@@ -475,7 +476,7 @@ __device__ __forceinline__ void item_a(const Job& jb, double2* sm, int p, int ti
     const int2 cp = jb.pairs[p];
     const double* x1 = jb.V + vcol(cp.x, jb.per, jb.ldv, N);
     const double* x2 = cp.y >= 0 ? jb.V + vcol(cp.y, jb.per, jb.ldv, N) : nullptr;
-    double2* Yp = jb.Y + ((int64_t)((p / jb.G) % kSlots) * jb.G + p % jb.G) * N;
+    double2* Yp = jb.Y + ((int64_t)((p / jb.G) % jb.slots) * jb.G + p % jb.G) * N;
     const int j10 = tile * P::TC;
     const uint64_t pol = jb.l2hint ? policy_evict_last() : 0;
     if (x2) {
@@ -509,7 +510,7 @@ __device__ __forceinline__ void item_b(const Job& jb, double2* sm, int p, int ro
     constexpr int64_t N = (int64_t)P::N1 * P::N2;
     const int2 cp = jb.pairs[p];
     const double* lam = (cp.x % jb.per == 0) ? jb.lamB : jb.lamQ;
-    double2* Yp = jb.Y + ((int64_t)((p / jb.G) % kSlots) * jb.G + p % jb.G) * N;
+    double2* Yp = jb.Y + ((int64_t)((p / jb.G) % jb.slots) * jb.G + p % jb.G) * N;
     const int k20 = rowblk * P::S;
     const uint64_t pol = jb.l2hint ? policy_evict_last() : 0;
     stage_first<VB, P::B0, false>(sm, [&](int seq, int i) {
@@ -546,7 +547,7 @@ __device__ __forceinline__ void item_c(const Job& jb, double2* sm, int p, int ti
     using VA = ColView<P::N2, P::TC>;
     constexpr int64_t N = (int64_t)P::N1 * P::N2;
     const int2 cp = jb.pairs[p];
-    const double2* Yp = jb.Y + ((int64_t)((p / jb.G) % kSlots) * jb.G + p % jb.G) * N;
+    const double2* Yp = jb.Y + ((int64_t)((p / jb.G) % jb.slots) * jb.G + p % jb.G) * N;
     const int j10 = tile * P::TC;
     stage_first<VA, P::AL, true>(sm, [&](int seq, int i) {
         return __ldcg(Yp + j10 + seq + (int64_t)P::N1 * i);
@@ -645,8 +646,8 @@ __global__ void __launch_bounds__(kThreads, CPS) fftconv_kernel(const Job jb) {
         int phase, g, r;
         decode(t, phase, g, r);
         if (g < 0 || g >= jb.ngroups) return;
-        if (phase == 0 && g >= kSlots) {
-            dep = jb.ctr + 1 + 3 * (g - kSlots) + 2;
+        if (phase == 0 && g >= jb.slots) {
+            dep = jb.ctr + 1 + 3 * (g - jb.slots) + 2;
             need = (unsigned)nC;
         } else if (phase == 1) {
             dep = jb.ctr + 1 + 3 * g + 0;
@@ -927,10 +928,14 @@ void Fft4::apply(bool inv, int Nsw, const double* V, int64_t ldv, int64_t m, dou
         const char* e = std::getenv("WC4DVAR_FFT_G");
         return e ? std::atoi(e) : 0;
     }();
-    int G = g_env > 0 ? g_env : (int)std::max<int64_t>(1, (64ll << 20) / (kSlots * 16 * N_));
+    static const int slots = [] {
+        const char* e = std::getenv("WC4DVAR_FFT_SLOTS");
+        return e ? std::max(3, std::atoi(e)) : kSlots;
+    }();
+    int G = g_env > 0 ? g_env : (int)std::max<int64_t>(1, (64ll << 20) / (slots * 16 * N_));
     G = std::min(G, np);
     const int ngroups = (np + G - 1) / G;
-    double2* Y = ybuf.get<double2>((size_t)kSlots * G * N_);
+    double2* Y = ybuf.get<double2>((size_t)slots * G * N_);
     unsigned* ctr = ctr_.get<unsigned>((size_t)1 + 3 * ngroups);
     W4_CUDA(cudaMemsetAsync(ctr, 0, sizeof(unsigned) * (1 + 3 * (size_t)ngroups), st));
     static const int l2hint = [] {
@@ -954,7 +959,7 @@ void Fft4::apply(bool inv, int Nsw, const double* V, int64_t ldv, int64_t m, dou
         return e ? std::atoi(e) : 0;  // measured: 13.7 ms without vs 14.0 ms with (C4 m = 64)
     }();
     Job jb{V, ldv, out, ldo, add, ldadd, add ? status : nullptr, dpairs, np, per, G, ngroups,
-           lamB, lamQ, Y, tw1_, tw2_, tlo_, thi_, ctr, l2hint, phase_mask, sub, acq, prefetch};
+           lamB, lamQ, Y, tw1_, tw2_, tlo_, thi_, ctr, l2hint, phase_mask, sub, acq, slots, prefetch};
     kPlans[plan_].run(jb, st);
 }
 
