@@ -448,11 +448,17 @@ class DistPcgResult:
 
 def dist_pcg(apply_rows: Callable[[torch.Tensor], torch.Tensor], b_rows: torch.Tensor,
              U_rows: Optional[torch.Tensor], theta: Optional[torch.Tensor], max_iter: int = 100,
-             rel_tol: float = 1e-6, ops=TorchOps, comm=None) -> DistPcgResult:
+             rel_tol: float = 1e-6, ops=TorchOps, comm=None, check_every: int = 8) -> DistPcgResult:
     """Row-sharded split PCG (krylov.cpp:22-99) with the compact-WY spectral LMP: every dot
     product and every U^T v of an iteration is one all-reduce of (k + 1) doubles.  Any row
     partition works (contiguous rows, or the spatial slabs of RowShardedHessian) as long as
-    b, U and apply_rows use the same one."""
+    b, U and apply_rows use the same one.
+
+    The loop keeps alpha / beta / rho, the stop test and the curvature check on the device
+    (no host round trip per iteration): the host looks at the device flags every
+    `check_every` iterations.  Iterations issued after the one that converged (or failed)
+    run masked -- alpha is zeroed, r and rho are frozen -- so x, the residual history and the
+    iteration count are exactly those of the per-iteration loop (krylov.cpp:92-95)."""
     allreduce_sum = comm.allreduce_sum if comm is not None else globals()["allreduce_sum"]
     k = 0 if U_rows is None else U_rows.shape[1]
     if k:
@@ -486,26 +492,51 @@ def dist_pcg(apply_rows: Callable[[torch.Tensor], torch.Tensor], b_rows: torch.T
     if r0 == 0.0:
         res.converged = True
         return res
-    rho = float(rho)
+    dev, dt = b_rows.device, b_rows.dtype
+    zero = torch.zeros((), dtype=dt, device=dev)
+    done = torch.zeros((), dtype=torch.bool, device=dev)      # converged or failed
+    conv = torch.zeros((), dtype=torch.bool, device=dev)
+    fail_at = torch.zeros((), dtype=torch.int64, device=dev)  # first iteration with curv <= 0
+    curv_bad = torch.zeros((), dtype=dt, device=dev)
+    hist = []
+    check_every = max(1, int(check_every))
+    j_issued = 0
     for j in range(1, max_iter + 1):
         w = apply_rows(p)
         g, curv = utv_dot(w, p)
-        curv = float(curv)
-        if not math.isfinite(curv) or curv <= 0.0:
-            raise NumericalError(f"pcg_split: p^T A p = {curv} at iteration {j}")
-        alpha = rho / curv
+        active = ~done
+        bad = active & (~torch.isfinite(curv) | (curv <= 0.0))
+        fail_at = torch.where(bad, torch.full_like(fail_at, j), fail_at)
+        curv_bad = torch.where(bad, curv, curv_bad)
+        done = done | bad
+        live = ~done
+        alpha = torch.where(live, rho / curv, zero)
         x = x + alpha * p
         r = r - alpha * Ct(w, g)
         h, rn = utv_dot(r, r)
-        rn = float(rn)
+        rn = torch.where(live, rn, rho)
         beta = rn / rho
-        res.residual_norms.append(math.sqrt(rn))
-        res.iterations = j
-        if math.sqrt(rn) / r0 <= rel_tol:
-            res.converged = True
-            break
+        hist.append(torch.where(live, torch.sqrt(rn), zero))
+        now = live & (torch.sqrt(rn) / r0 <= rel_tol)
+        conv = conv | now
+        done = done | now
         p = C(r, h) + beta * p
         rho = rn
+        j_issued = j
+        if j % check_every == 0 or j == max_iter:
+            if bool(done):  # the one host sync per `check_every` iterations
+                break
+    fj = int(fail_at)
+    if fj:
+        cv = float(curv_bad)
+        raise NumericalError(f"pcg_split: p^T A p = {cv} at iteration {fj}")
+    hv = torch.stack(hist).cpu().tolist() if hist else []
+    nlive = j_issued
+    if bool(conv):
+        nlive = next(i for i, v in enumerate(hv, 1) if v / r0 <= rel_tol)
+    res.residual_norms += hv[:nlive]
+    res.iterations = nlive
+    res.converged = bool(conv)
     res.x_rows = x
     return res
 

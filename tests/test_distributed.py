@@ -106,6 +106,17 @@ def _body_revd_pcg(rank, world):
     assert res.converged and abs(res.iterations - oref.history.iterations) <= 1
     x = all_gather_cat(res.x_rows, rsz).numpy()
     assert np.abs(x - oref.x).max() <= 1e-9 * np.abs(oref.x).max()
+    # the device-side stop test (host check every 8 / 5 iterations, later iterations masked)
+    # reproduces the per-iteration loop exactly: same iterations, residuals and x bits
+    for ce in (5, 8):
+        r1 = dist_pcg(apply_rows, torch.from_numpy(b[ra:rb].copy()), U_rows, theta, 200, 1e-10, check_every=1)
+        r2 = dist_pcg(apply_rows, torch.from_numpy(b[ra:rb].copy()), U_rows, theta, 200, 1e-10, check_every=ce)
+        assert r1.iterations == r2.iterations == res.iterations and r1.converged and r2.converged
+        assert r1.residual_norms == r2.residual_norms
+        assert torch.equal(r1.x_rows, r2.x_rows)
+    # max_iter reached without convergence: every issued iteration is live
+    r3 = dist_pcg(apply_rows, torch.from_numpy(b[ra:rb].copy()), U_rows, theta, 3, 1e-14, check_every=8)
+    assert not r3.converged and r3.iterations == 3 and len(r3.residual_norms) == 4
 
 
 def _gather_rows(U_rows, n_, world):
