@@ -137,7 +137,8 @@ __global__ void __launch_bounds__(WM * WN * 32)
 #pragma unroll
             for (int v = 0; v < 4; ++v) acc[i][j][v] = 0.0;
 
-    const int64_t ktiles = (K + BK - 1) / BK;
+    const int64_t kend = P.upper_tri ? (n0 + BN < K ? n0 + BN : K) : K;
+    const int64_t ktiles = (kend + BK - 1) / BK;
 
     auto load_stage = [&](int stage, int64_t kt) {
         const int64_t k0 = kt * BK;
@@ -938,7 +939,7 @@ template <int BM, int BN, int WM, int WN, int STAGES, int VEC>
 __global__ void __launch_bounds__(WM * WN * 32)
     gemm_tn_kernel(int64_t R, int64_t m1, int64_t m2, const double* __restrict__ A, int64_t lda,
                    const double* __restrict__ B, int64_t ldb, int64_t rows_per_split,
-                   int64_t tiles_m, int64_t tiles_n, double* __restrict__ work) {
+                   int64_t tiles_m, int64_t tiles_n, double* __restrict__ work, bool sym) {
     constexpr int NT = WM * WN * 32;
     constexpr int WTM = BM / WM, WTN = BN / WN;
     constexpr int MI = WTM / 16, NI = WTN / 8;
@@ -947,10 +948,25 @@ __global__ void __launch_bounds__(WM * WN * 32)
     double* As = smem;
     double* Bs = smem + STAGES * A_ELEMS;
 
+    // tile t of a split: plain (tm, tn) grid, or with sym the upper-triangle tiles
+    // (tm <= tn) of a square grid enumerated column by column
     const int64_t t = blockIdx.x;
-    const int64_t tm = t % tiles_m;
-    const int64_t tn = (t / tiles_m) % tiles_n;
-    const int64_t split = t / (tiles_m * tiles_n);
+    int64_t tm, tn, split;
+    if (sym) {
+        const int64_t ntri = tiles_m * (tiles_m + 1) / 2;
+        split = t / ntri;
+        int64_t u = t - split * ntri;
+        tn = 0;
+        while (u > tn) {
+            u -= tn + 1;
+            ++tn;
+        }
+        tm = u;
+    } else {
+        tm = t % tiles_m;
+        tn = (t / tiles_m) % tiles_n;
+        split = t / (tiles_m * tiles_n);
+    }
     const int64_t i0 = tm * BM, j0 = tn * BN;
     const int64_t r_begin = split * rows_per_split;
     const int64_t r_end = min(R, r_begin + rows_per_split);
@@ -1064,25 +1080,29 @@ __global__ void __launch_bounds__(WM * WN * 32)
 
 __global__ void reduce_splits_kernel(int64_t m1, int64_t m2, int64_t nsplit,
                                      const double* __restrict__ work, double alpha,
-                                     double* __restrict__ C, int64_t ldc) {
-    const int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+                                     double* __restrict__ C, int64_t ldc, int sym_bm) {
+    int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (e >= m1 * m2) return;
+    const int64_t r0 = e % m1, c0 = e / m1;
+    const int64_t out = r0 + c0 * ldc;
+    // Gram: the partials of a tile below the diagonal were never computed; read the mirror
+    if (sym_bm && r0 / sym_bm > c0 / sym_bm) e = c0 + r0 * m1;
     double s = 0.0;
     for (int64_t k = 0; k < nsplit; ++k) s += work[k * m1 * m2 + e];  // fixed order
-    const int64_t r = e % m1, c = e / m1;
-    C[c * ldc + r] = alpha * s;
+    C[out] = alpha * s;
 }
 
 template <int BM, int BN, int WM, int WN, int STAGES, int VEC>
 void launch_tn(int64_t R, int64_t m1, int64_t m2, const double* A, int64_t lda, const double* B,
                int64_t ldb, double* work, int64_t rows_per_split, int64_t nsplit,
-               cudaStream_t stream) {
+               cudaStream_t stream, bool sym = false) {
     const size_t smem = sizeof(double) * STAGES * (BM * KS + BN * KS);
     auto kern = gemm_tn_kernel<BM, BN, WM, WN, STAGES, VEC>;
     configure_smem(reinterpret_cast<const void*>(kern), smem);
     const int64_t tm = cdiv(m1, BM), tn = cdiv(m2, BN);
-    kern<<<(unsigned)(tm * tn * nsplit), WM * WN * 32, smem, stream>>>(
-        R, m1, m2, A, lda, B, ldb, rows_per_split, tm, tn, work);
+    const int64_t tiles = sym ? tm * (tm + 1) / 2 : tm * tn;
+    kern<<<(unsigned)(tiles * nsplit), WM * WN * 32, smem, stream>>>(
+        R, m1, m2, A, lda, B, ldb, rows_per_split, tm, tn, work, sym);
     W4_LAUNCH();
 }
 
@@ -1214,8 +1234,18 @@ void gemm_tn(int64_t R, int64_t m1, int64_t m2, const double* A, int64_t lda, co
     if (var == 0) var = (m1 >= 128 && m2 >= 128) ? 4 : (m1 >= 128 ? 3 : 1);
     const int BM = (var >= 3) ? 128 : 64, BN = (var == 4) ? 128 : 64;
     const int ctas_per_sm = (var == 4) ? 1 : 2;
-    const int64_t tiles = cdiv(m1, BM) * cdiv(m2, BN);
-    int64_t nsplit = cdiv((int64_t)ctas_per_sm * kSMs, tiles);
+    // Gram (A^T A): upper-triangle tiles only (square tiles; WC4DVAR_GEMM_SYRK=0 disables)
+    static const bool syrk_env = [] {
+        const char* e = std::getenv("WC4DVAR_GEMM_SYRK");
+        return !(e && std::atoi(e) == 0);
+    }();
+    const bool vec2 = aligned16(A) && aligned16(B) && lda % 2 == 0 && ldb % 2 == 0;
+    const bool sym = syrk_env && A == B && m1 == m2 && lda == ldb && BM == BN && vec2 && var != 2 &&
+                     cdiv(m1, BM) > 1;
+    const int64_t tiles = sym ? cdiv(m1, BM) * (cdiv(m1, BM) + 1) / 2 : cdiv(m1, BM) * cdiv(m2, BN);
+    // (sym: whole waves -- floor -- so no split lands in a one-CTA tail wave)
+    int64_t nsplit = sym ? std::max<int64_t>(1, (int64_t)ctas_per_sm * kSMs / tiles)
+                         : cdiv((int64_t)ctas_per_sm * kSMs, tiles);
     const int64_t min_rows = 256;
     if (nsplit * min_rows > R) nsplit = cdiv(R, min_rows);
     if (nsplit < 1) nsplit = 1;
@@ -1223,7 +1253,6 @@ void gemm_tn(int64_t R, int64_t m1, int64_t m2, const double* A, int64_t lda, co
     rows_per_split = cdiv(rows_per_split, BK) * BK;
     nsplit = R > 0 ? cdiv(R, rows_per_split) : 1;
     double* w = work.get<double>((size_t)(nsplit * m1 * m2));
-    const bool vec2 = aligned16(A) && aligned16(B) && lda % 2 == 0 && ldb % 2 == 0;
     if (R == 0) {
         W4_CUDA(cudaMemsetAsync(w, 0, sizeof(double) * m1 * m2, stream));
     } else if (!vec2) {
@@ -1233,13 +1262,13 @@ void gemm_tn(int64_t R, int64_t m1, int64_t m2, const double* A, int64_t lda, co
     } else if (var == 3) {
         launch_tn<128, 64, 4, 2, 3, 2>(R, m1, m2, A, lda, B, ldb, w, rows_per_split, nsplit, stream);
     } else if (var == 4) {
-        launch_tn<128, 128, 4, 4, 3, 2>(R, m1, m2, A, lda, B, ldb, w, rows_per_split, nsplit, stream);
+        launch_tn<128, 128, 4, 4, 3, 2>(R, m1, m2, A, lda, B, ldb, w, rows_per_split, nsplit, stream, sym);
     } else {
-        launch_tn<64, 64, 2, 2, 4, 2>(R, m1, m2, A, lda, B, ldb, w, rows_per_split, nsplit, stream);
+        launch_tn<64, 64, 2, 2, 4, 2>(R, m1, m2, A, lda, B, ldb, w, rows_per_split, nsplit, stream, sym);
     }
     const int64_t e = m1 * m2;
     reduce_splits_kernel<<<(unsigned)cdiv(e, 256), 256, 0, stream>>>(m1, m2, nsplit, w, alpha, C,
-                                                                        ldc);
+                                                                        ldc, (sym && R > 0) ? BM : 0);
     W4_LAUNCH();
 }
 

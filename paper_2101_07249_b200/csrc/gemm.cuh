@@ -45,6 +45,10 @@ struct GemmPass {
     ColMap out;   // M-long columns
     ColMap add;   // optional addend (base == nullptr: none)
     bool symA = false;  // A == A^T bitwise (enables the k-contiguous LDS.128 kernel)
+    bool upper_tri = false;  // B (the `in` columns) is upper triangular: column c has zeros
+                             // below row c, so an output tile of columns [n0, n0 + BN) stops
+                             // its k loop at n0 + BN (whole zero k-tiles skipped: the same
+                             // bits, Y R^{-1} at about 3/4 of the flops)
 };
 
 // Launch one or two passes in a single kernel.  status (optional) gets
@@ -52,7 +56,10 @@ struct GemmPass {
 void gemm_nn(const GemmPass* passes, int npass, unsigned* status, cudaStream_t stream);
 
 // C (m1 x m2, ldc) = alpha * A^T B, A: R x m1 (lda), B: R x m2 (ldb).
-// work: scratch device buffer (grown as needed).
+// work: scratch device buffer (grown as needed).  When B == A (same pointer, m2 == m1,
+// ldb == lda) the product is a Gram matrix: only the tiles on and above the diagonal are
+// computed and the reduction mirrors them (bitwise the full product: the DMMA sums of
+// (r, c) and (c, r) multiply the same pairs in the same k order).
 void gemm_tn(int64_t R, int64_t m1, int64_t m2, const double* A, int64_t lda, const double* B,
              int64_t ldb, double alpha, double* C, int64_t ldc, DevBuf& work, cudaStream_t stream);
 

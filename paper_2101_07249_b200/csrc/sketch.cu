@@ -112,10 +112,11 @@ struct Ctx {
         gemm_tn(n, m1, m2, A, n, B, n, 1.0, G, m1, pool[P_GEMMWS], st);
     }
 
-    // C (n x ncols) = A (n x K) * B (K x ncols, ld K)
+    // C (n x ncols) = A (n x K) * B (K x ncols, ld K); tri: B is upper triangular (R^{-1})
     void tall_times_small(const double* A, int64_t K, const double* B, int64_t ldb, int64_t ncols,
-                          double* C, int64_t ldc) {
+                          double* C, int64_t ldc, bool tri = false) {
         GemmPass p;
+        p.upper_tri = tri;
         p.A = A;
         p.lda = n;
         p.M = n;
@@ -145,14 +146,14 @@ struct Ctx {
         chol_inv_upper((int)m, G, R1, R1i, info, pool[P_SMALLWS], st);
         if (read_int(info)) return false;
         double* Q1 = scratch;
-        tall_times_small(Y, m, R1i, m, m, Q1, n);
+        tall_times_small(Y, m, R1i, m, m, Q1, n, true);
         double* G2 = buf(P_G2, m * m);
         gram(Q1, m, Q1, m, G2);
         double* R2 = buf(P_R2, m * m);
         double* R2i = buf(P_R2I, m * m);
         chol_inv_upper((int)m, G2, R2, R2i, info, pool[P_SMALLWS], st);
         if (read_int(info)) return false;
-        tall_times_small(Q1, m, R2i, m, m, Q, n);
+        tall_times_small(Q1, m, R2i, m, m, Q, n, true);
         if (R_out) small_gemm(false, false, (int)m, (int)m, (int)m, 1.0, R2, (int)m, R1, (int)m, 0.0,
                               R_out, (int)m, st);
         tm.end();
@@ -184,7 +185,7 @@ struct Ctx {
         int* info = reinterpret_cast<int*>(buf(P_INT, 4 + 2 * m));
         chol_inv_upper((int)m, G, Rs, Rsi, info, pool[P_SMALLWS], st);
         if (read_int(info)) return false;
-        tall_times_small(Y, m, Rsi, m, m, scratch, n);  // Q1 = Y Rs^{-1}; Y is dead after this
+        tall_times_small(Y, m, Rsi, m, m, scratch, n, true);  // Q1 = Y Rs^{-1}; Y is dead after this
         double* Racc = buf(P_TMP, 2 * m * m);
         double* Rtmp = Racc + m * m;
         W4_CUDA(cudaMemcpyAsync(Racc, Rs, sizeof(double) * m * m, cudaMemcpyDeviceToDevice, st));
@@ -197,7 +198,7 @@ struct Ctx {
             double* R2i = buf(P_R2I, m * m);
             chol_inv_upper((int)m, G2, R2, R2i, info, pool[P_SMALLWS], st);
             if (read_int(info)) return false;
-            tall_times_small(src, m, R2i, m, m, dst, n);
+            tall_times_small(src, m, R2i, m, m, dst, n, true);
             small_gemm(false, false, (int)m, (int)m, (int)m, 1.0, R2, (int)m, Racc, (int)m, 0.0, Rtmp, (int)m, st);
             std::swap(Racc, Rtmp);
             std::swap(src, dst);
@@ -446,7 +447,7 @@ int64_t sketch_dev(wc4dvar_op& op, const wc4dvar_sketch_config& cfg, const doubl
                 "spectra.");
         tm.begin(T_GEMM);
         double* F = Z;  // Z is dead once E2 exists
-        c.tall_times_small(E1, r, Rui, r, r, F, n);  // F = E1 U^{-1}, randevd.cpp:104-105
+        c.tall_times_small(E1, r, Rui, r, r, F, n, true);  // F = E1 U^{-1}, randevd.cpp:104-105
         double* RF = c.buf(P_R, r * r);
         if (!c.orth(F, r, F, RF, nullptr, E1))
             throw NumericalError("nystrom: factor F is numerically rank deficient (CholQR breakdown)");
