@@ -345,6 +345,81 @@ __device__ __forceinline__ void stage_turn(double2* sm, const double2* __restric
     cbar();
 }
 
+// ---- in-place row stages (pass B) ----------------------------------------------------
+// Pass B as an in-place Cooley-Tukey sequence: the forward transform is decimation in
+// frequency (natural order in, digit-reversed spectrum out), the spectrum product uses a
+// lam table stored in that digit-reversed order, and the inverse is decimation in time
+// (digit-reversed in, natural order out) -- no permutation anywhere.  Every stage reads
+// and writes the SAME slots, so a thread finishes its butterflies (load, DFT, store) with no
+// barrier between the reads and the writes: one barrier per stage instead of the two of a
+// Stockham stage (pass B: 4 barriers instead of 7).
+// Butterfly (seq, b, q) of a stage with radix R and span M owns the row elements
+// e = b R M + q + k M, k < R.  DIF: DFT_R, then output k times w_{RM}^{q k}; DIT: input k
+// times w_{RM}^{-q k}, then IDFT_R.
+template <class V, int R, int M>
+struct Ip {
+    static constexpr int PR = V::L / R;  // butterflies per row
+    static constexpr int NB = V::S * PR;
+    __device__ static __forceinline__ void map(int u, int& seq, int& e0, int& q) {
+        seq = u / PR;
+        const int w = u - seq * PR;
+        q = w % M;
+        e0 = (w / M) * (R * M) + q;
+    }
+};
+
+template <class V, int R, int M, bool INV>
+__device__ __forceinline__ void ip_stage(double2* sm, const double2* __restrict__ tw) {
+    using IP = Ip<V, R, M>;
+    constexpr int BPT = (IP::NB + kNT - 1) / kNT;
+#pragma unroll
+    for (int it = 0; it < BPT; ++it) {
+        const int u = threadIdx.x + it * kNT;
+        if (IP::NB % kNT != 0 && u >= IP::NB) break;
+        int seq, e0, q;
+        IP::map(u, seq, e0, q);
+        double2 v[R];
+#pragma unroll
+        for (int k = 0; k < R; ++k) v[k] = sm[V::addr(seq, e0 + k * M)];
+        double2 w = make_double2(1.0, 0.0);
+        if (M > 1) {
+            w = __ldg(tw + q * (V::L / (R * M)));  // w_{RM}^q = w_L^{q L / (R M)}
+            if (INV) w.y = -w.y;
+        }
+        if (INV && M > 1) twiddle_pow<R>(v, w);
+        dft<R, INV>(v);
+        if (!INV && M > 1) twiddle_pow<R>(v, w);
+#pragma unroll
+        for (int k = 0; k < R; ++k) sm[V::addr(seq, e0 + k * M)] = v[k];
+    }
+    cbar();
+}
+
+template <class V, bool INV, int M, class List>
+struct IpMids;
+template <class V, bool INV, int M>
+struct IpMids<V, INV, M, RL<>> {
+    static constexpr int Mout = M;
+    __device__ static __forceinline__ void run(double2*, const double2*) {}
+};
+// forward (DIF): spans shrink, M -> M / R; inverse (DIT): spans grow, M -> M R
+template <class V, int M, int R, int... Rest>
+struct IpMids<V, false, M, RL<R, Rest...>> {
+    static constexpr int Mout = IpMids<V, false, M / R, RL<Rest...>>::Mout;
+    __device__ static __forceinline__ void run(double2* sm, const double2* tw) {
+        ip_stage<V, R, M / R, false>(sm, tw);
+        IpMids<V, false, M / R, RL<Rest...>>::run(sm, tw);
+    }
+};
+template <class V, int M, int R, int... Rest>
+struct IpMids<V, true, M, RL<R, Rest...>> {
+    static constexpr int Mout = IpMids<V, true, M * R, RL<Rest...>>::Mout;
+    __device__ static __forceinline__ void run(double2* sm, const double2* tw) {
+        ip_stage<V, R, M, true>(sm, tw);
+        IpMids<V, true, M * R, RL<Rest...>>::run(sm, tw);
+    }
+};
+
 // ---- plans ---------------------------------------------------------------------------
 // N1: contiguous length (pass B, S rows per item), radices B0, BM..., BL (BMr = BM reversed).
 // N2: strided length (passes A / C, TC columns per item), radices A0, AM..., AL.
@@ -413,6 +488,7 @@ struct Job {
     int sub;             // tiles per ticket (WC4DVAR_FFT_SUB)
     int acq;             // acquire loads on the dependency counters (WC4DVAR_FFT_ACQ, default 1)
     int slots;           // Y slots (WC4DVAR_FFT_SLOTS, default kSlots; >= 3)
+    int ipb;             // pass B in place (DIF / DIT, digit-reversed lam); 0 = Stockham
     int prefetch;        // L2 prefetch of the next pass-A tile (WC4DVAR_FFT_PREFETCH, default 0)
 };
 
@@ -542,6 +618,102 @@ __device__ __forceinline__ void item_b(const Job& jb, double2* sm, int p, int ro
     });
 }
 
+// pass B, in-place form (see ip_stage); lam is the digit-reversed table (lam_rev_kernel)
+template <class P, class AF>
+__device__ __forceinline__ void item_b_ip(const Job& jb, double2* sm, int p, int rowblk, AF af) {
+    using VB = RowView<P::N1, P::S>;
+    constexpr int64_t N = (int64_t)P::N1 * P::N2;
+    constexpr int L = P::N1;
+    const int2 cp = jb.pairs[p];
+    const double* lam = (cp.x % jb.per == 0) ? jb.lamB : jb.lamQ;
+    double2* Yp = jb.Y + ((int64_t)((p / jb.G) % jb.slots) * jb.G + p % jb.G) * N;
+    const int k20 = rowblk * P::S;
+    const uint64_t pol = jb.l2hint ? policy_evict_last() : 0;
+    // DIF stage 1 (radix B0, span M1 = L / B0): natural-order loads from Y
+    {
+        constexpr int R = P::B0, M = L / P::B0;
+        using IP = Ip<VB, R, M>;
+        constexpr int BPT = (IP::NB + kNT - 1) / kNT;
+#pragma unroll
+        for (int it = 0; it < BPT; ++it) {
+            const int u = threadIdx.x + it * kNT;
+            if (IP::NB % kNT != 0 && u >= IP::NB) break;
+            int seq, e0, q;
+            IP::map(u, seq, e0, q);
+            const double2* yr = Yp + (int64_t)P::N1 * (k20 + seq) + e0;
+            double2 v[R];
+#pragma unroll
+            for (int k = 0; k < R; ++k) v[k] = ld_y(yr + k * M, pol);
+            dft<R, false>(v);
+            twiddle_pow<R>(v, __ldg(jb.tw1 + q));  // w_L^{q k}
+#pragma unroll
+            for (int k = 0; k < R; ++k) sm[VB::addr(seq, e0 + k * M)] = v[k];
+        }
+        cbar();
+    }
+    af();
+    using FM = IpMids<VB, false, L / P::B0, typename P::BM>;
+    FM::run(sm, jb.tw1);
+    static_assert(FM::Mout == P::BL, "pass B radices must multiply to N1");
+    // last DIF stage (radix BL, span 1) + spectrum product + first DIT stage, in registers
+    {
+        constexpr int R = P::BL;
+        using IP = Ip<VB, R, 1>;
+        constexpr int BPT = (IP::NB + kNT - 1) / kNT;
+#pragma unroll
+        for (int it = 0; it < BPT; ++it) {
+            const int u = threadIdx.x + it * kNT;
+            if (IP::NB % kNT != 0 && u >= IP::NB) break;
+            int seq, e0, q;
+            IP::map(u, seq, e0, q);
+            double2 v[R];
+#pragma unroll
+            for (int k = 0; k < R; ++k) v[k] = sm[VB::addr(seq, e0 + k)];
+            dft<R, false>(v);
+            const double* lr = lam + (int64_t)P::N1 * (k20 + seq) + e0;
+#pragma unroll
+            for (int k = 0; k < R; ++k) {
+                const double l = __ldg(lr + k);
+                v[k] = make_double2(l * v[k].x, l * v[k].y);
+            }
+            dft<R, true>(v);
+#pragma unroll
+            for (int k = 0; k < R; ++k) sm[VB::addr(seq, e0 + k)] = v[k];
+        }
+        cbar();
+    }
+    using IM = IpMids<VB, true, P::BL, typename P::BMr>;
+    IM::run(sm, jb.tw1);
+    static_assert(IM::Mout == L / P::B0, "pass B radices must multiply to N1");
+    // last DIT stage (radix B0, span L / B0): conjugate four-step twiddle, natural-order store
+    {
+        constexpr int R = P::B0, M = L / P::B0;
+        using IP = Ip<VB, R, M>;
+        constexpr int BPT = (IP::NB + kNT - 1) / kNT;
+#pragma unroll
+        for (int it = 0; it < BPT; ++it) {
+            const int u = threadIdx.x + it * kNT;
+            if (IP::NB % kNT != 0 && u >= IP::NB) break;
+            int seq, e0, q;
+            IP::map(u, seq, e0, q);
+            double2 v[R];
+#pragma unroll
+            for (int k = 0; k < R; ++k) v[k] = sm[VB::addr(seq, e0 + k * M)];
+            twiddle_pow<R>(v, conj2(__ldg(jb.tw1 + q)));
+            dft<R, true>(v);
+            const int64_t k2 = k20 + seq;
+            double2 w = conj2(wN(jb, e0 * k2));
+            const double2 ws = conj2(wN(jb, M * k2));
+            double2* yr = Yp + (int64_t)P::N1 * k2 + e0;
+#pragma unroll
+            for (int k = 0; k < R; ++k) {
+                st_y(yr + k * M, cmul(v[k], w), pol);
+                if (k + 1 < R) w = cmul(w, ws);
+            }
+        }
+    }
+}
+
 template <class P, bool ADD, class AF>
 __device__ __forceinline__ void item_c(const Job& jb, double2* sm, int p, int tile, AF af) {
     using VA = ColView<P::N2, P::TC>;
@@ -605,7 +777,7 @@ __device__ __forceinline__ void item_c(const Job& jb, double2* sm, int p, int ti
     if (ADD && jb.status && bad) atomicOr(jb.status, ST_OUT_NONFINITE);
 }
 
-template <class P, int CPS, bool ADD>
+template <class P, int CPS, bool ADD, bool IPB>
 __global__ void __launch_bounds__(kThreads, CPS) fftconv_kernel(const Job jb) {
     extern __shared__ double2 sm[];
     __shared__ unsigned s_ticket, s_next;
@@ -736,7 +908,8 @@ __global__ void __launch_bounds__(kThreads, CPS) fftconv_kernel(const Job jb) {
                     if (phase == 0) {
                         item_a<P>(jb, sm, p, u, after_first);
                     } else if (phase == 1) {
-                        item_b<P>(jb, sm, p, u, after_first);
+                        if (IPB) item_b_ip<P>(jb, sm, p, u, after_first);
+                        else item_b<P>(jb, sm, p, u, after_first);
                     } else {
                         item_c<P, ADD>(jb, sm, p, u, after_first);
                     }
@@ -764,29 +937,53 @@ __global__ void build_lam_kernel(int64_t N, int N1, int N2, const double2* __res
     }
 }
 
+// in-place pass B: lamR[e + N1 k2] = lam at row frequency f(e), the digit reversal of the
+// DIF radix sequence rad[0..nr) (rad[0] first): e = sum d_i M_i (M_i = span of stage i),
+// f = sum d_i P_i (P_i = rad[0] ... rad[i-1])
+struct Radices {
+    int r[4];
+    int n;
+};
+__global__ void build_lam_rev_kernel(int64_t N, int N1, int N2, Radices rd, const double2* __restrict__ spec,
+                                     double* __restrict__ lamR) {
+    const double inv_n = 1.0 / (double)N;
+    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < N; t += (int64_t)gridDim.x * blockDim.x) {
+        const int e = (int)(t % N1);
+        const int64_t k2 = t / N1;
+        int span = N1, pw = 1, f = 0;
+        for (int i = 0; i < rd.n; ++i) {
+            span /= rd.r[i];
+            f += ((e / span) % rd.r[i]) * pw;
+            pw *= rd.r[i];
+        }
+        const int64_t k = k2 + (int64_t)N2 * f;
+        lamR[t] = spec[k <= N - k ? k : N - k].x * inv_n;
+    }
+}
+
 template <class P>
 constexpr size_t smem_bytes() {
     return sizeof(double2) * (size_t)std::max(ColView<P::N2, P::TC>::SMEM, RowView<P::N1, P::S>::SMEM);
 }
 
-template <class P, int CPS, bool ADD>
+template <class P, int CPS, bool ADD, bool IPB>
 void launch_cps(const Job& jb, cudaStream_t st) {
     constexpr size_t sm = smem_bytes<P>();
     static_assert(sm <= 227 * 1024 / 2, "fftconv tile exceeds the per-CTA SMEM budget");
     static bool attr = false;
     if (!attr) {
-        W4_CUDA(cudaFuncSetAttribute(fftconv_kernel<P, CPS, ADD>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        W4_CUDA(cudaFuncSetAttribute(fftconv_kernel<P, CPS, ADD, IPB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      (int)sm));
         attr = true;
     }
     int dev = 0, nsm = kSMs, occ = 0;
     W4_CUDA(cudaGetDevice(&dev));
     W4_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
-    W4_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fftconv_kernel<P, CPS, ADD>, kThreads, sm));
+    W4_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fftconv_kernel<P, CPS, ADD, IPB>, kThreads, sm));
     const int64_t items = (int64_t)(jb.ngroups + 2) * jb.G *
                           (2 * ((P::N1 / P::TC + jb.sub - 1) / jb.sub) + (P::N2 / P::S + jb.sub - 1) / jb.sub);
     const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(items, (int64_t)nsm * std::max(occ, 1)));
-    fftconv_kernel<P, CPS, ADD><<<grid, kThreads, sm, st>>>(jb);
+    fftconv_kernel<P, CPS, ADD, IPB><<<grid, kThreads, sm, st>>>(jb);
     W4_LAUNCH();
 }
 
@@ -798,22 +995,26 @@ void launch(const Job& jb, cudaStream_t st) {
         const char* e = std::getenv("WC4DVAR_FFT_CPS");
         return e ? std::atoi(e) : kCtaPerSm;
     }();
-    if (jb.add) return cps == 1 ? launch_cps<P, 1, true>(jb, st) : launch_cps<P, 2, true>(jb, st);
-    return cps == 1 ? launch_cps<P, 1, false>(jb, st) : launch_cps<P, 2, false>(jb, st);
+    if (cps == 3) {  // register budget experiment (in-place pass B only)
+        if (jb.ipb) return jb.add ? launch_cps<P, 3, true, true>(jb, st) : launch_cps<P, 3, false, true>(jb, st);
+    }
+    if (jb.ipb) return jb.add ? launch_cps<P, 2, true, true>(jb, st) : launch_cps<P, 2, false, true>(jb, st);
+    return jb.add ? launch_cps<P, 2, true, false>(jb, st) : launch_cps<P, 2, false, false>(jb, st);
 }
 
 struct PlanInfo {
     int variant;  // WC4DVAR_FFT_VARIANT selects among plans of the same length (0 = default)
+    Radices brad; // pass-B (row) DIF radices, first stage first
     int64_t N1, N2;
     size_t smem;
     void (*run)(const Job&, cudaStream_t);
 };
 const PlanInfo kPlans[] = {
-    {0, PlanE6::N1, PlanE6::N2, smem_bytes<PlanE6>(), launch<PlanE6>},
-    {1, PlanE6c3::N1, PlanE6c3::N2, smem_bytes<PlanE6c3>(), launch<PlanE6c3>},
-    {0, Plan2E6::N1, Plan2E6::N2, smem_bytes<Plan2E6>(), launch<Plan2E6>},
-    {0, PlanE5::N1, PlanE5::N2, smem_bytes<PlanE5>(), launch<PlanE5>},
-    {0, PlanE4::N1, PlanE4::N2, smem_bytes<PlanE4>(), launch<PlanE4>},
+    {0, {{20, 20, 10, 0}, 3}, PlanE6::N1, PlanE6::N2, smem_bytes<PlanE6>(), launch<PlanE6>},
+    {1, {{20, 20, 10, 0}, 3}, PlanE6c3::N1, PlanE6c3::N2, smem_bytes<PlanE6c3>(), launch<PlanE6c3>},
+    {0, {{20, 20, 10, 0}, 3}, Plan2E6::N1, Plan2E6::N2, smem_bytes<Plan2E6>(), launch<Plan2E6>},
+    {0, {{20, 20, 0, 0}, 2}, PlanE5::N1, PlanE5::N2, smem_bytes<PlanE5>(), launch<PlanE5>},
+    {0, {{20, 20, 0, 0}, 2}, PlanE4::N1, PlanE4::N2, smem_bytes<PlanE4>(), launch<PlanE4>},
 };
 
 }  // namespace
@@ -872,11 +1073,20 @@ bool Fft4::init(int64_t N, const double2* const spec_half[4], cudaStream_t st) {
     tw2_ = tables_ + o2;
     tlo_ = tables_ + olo;
     thi_ = tables_ + ohi;
+    // pass B in place (default) or as Stockham stages (WC4DVAR_FFT_IPB=0): the lam layout follows
+    static const int ipb_env = [] {
+        const char* e = std::getenv("WC4DVAR_FFT_IPB");
+        return e ? std::atoi(e) : 1;
+    }();
+    ipb_ = ipb_env;
     for (int i = 0; i < 4; ++i) {
         if (!spec_half[i]) continue;
         W4_CUDA(cudaMalloc(&lam_[i], sizeof(double) * N));
-        build_lam_kernel<<<(unsigned)std::min<int64_t>(cdiv(N, 256), 4096), 256, 0, st>>>(N, (int)N1, (int)N2,
-                                                                                            spec_half[i], lam_[i]);
+        const unsigned g = (unsigned)std::min<int64_t>(cdiv(N, 256), 4096);
+        if (ipb_)
+            build_lam_rev_kernel<<<g, 256, 0, st>>>(N, (int)N1, (int)N2, kPlans[plan].brad, spec_half[i], lam_[i]);
+        else
+            build_lam_kernel<<<g, 256, 0, st>>>(N, (int)N1, (int)N2, spec_half[i], lam_[i]);
         W4_LAUNCH();
     }
     W4_CUDA(cudaStreamSynchronize(st));  // tab is freed on return
@@ -959,7 +1169,7 @@ void Fft4::apply(bool inv, int Nsw, const double* V, int64_t ldv, int64_t m, dou
         return e ? std::atoi(e) : 0;  // measured: 13.7 ms without vs 14.0 ms with (C4 m = 64)
     }();
     Job jb{V, ldv, out, ldo, add, ldadd, add ? status : nullptr, dpairs, np, per, G, ngroups,
-           lamB, lamQ, Y, tw1_, tw2_, tlo_, thi_, ctr, l2hint, phase_mask, sub, acq, slots, prefetch};
+           lamB, lamQ, Y, tw1_, tw2_, tlo_, thi_, ctr, l2hint, phase_mask, sub, acq, slots, ipb_, prefetch};
     kPlans[plan_].run(jb, st);
 }
 

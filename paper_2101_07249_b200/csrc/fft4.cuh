@@ -24,6 +24,7 @@ public:
 
 private:
     int plan_ = -1;
+    int ipb_ = 1;                // pass B in place (the lam tables are in its digit-reversed order)
     int64_t N_ = 0, N1_ = 0, N2_ = 0;
     double2* tables_ = nullptr;  // w_N1^e, w_N2^e (stage twiddles) + two-level w_N^p
     const double2* tw1_ = nullptr;
