@@ -266,13 +266,21 @@ int wc4dvar_gpu_op_apply_block(wc4dvar_op* op, const double* V, int64_t ldv, int
     // in `nch` chunks; chunk c+1's host->device copy and chunk c-1's device->host copy run
     // on their own streams while chunk c computes.  Each column's arithmetic is unchanged
     // (bitwise), and the device staging stays bounded (2 x 2 slots of <= kStageBytes) for
-    // blocks far larger than HBM headroom (C4: n_A x 256 = 34.8 GB each way).
+    // blocks far larger than HBM headroom (C4: n_A x 256 = 34.8 GB each way, PCIe-bound:
+    // 48 GB/s per direction with both directions busy, tools/pcie_probe.py).
     // WC4DVAR_PIPELINE_CHUNKS (default 2; 1 = off) is the chunk count below that bound.
     static const int chunks_env = [] {
         const char* e = std::getenv("WC4DVAR_PIPELINE_CHUNKS");
         return e ? std::atoi(e) : 2;
     }();
-    constexpr size_t kStageBytes = size_t(4) << 30;
+    // WC4DVAR_PIPELINE_STAGE_MB: device bytes per chunk slot (default 512; C4 k = 256 e2e step
+    // 840 / 778 / 749 ms at 4096 / 1024 / 512 MB against a 722 ms PCIe floor): small enough that
+    // the ramp (first H2D) and the tail (last compute + D2H) are short against a step of
+    // full-duplex PCIe traffic, large enough that every chunk fills the GPU (C4: 3 columns)
+    static const size_t kStageBytes = [] {
+        const char* e = std::getenv("WC4DVAR_PIPELINE_STAGE_MB");
+        return (size_t)(e ? std::max(64, std::atoi(e)) : 512) << 20;
+    }();
     const int64_t cmax = std::max<int64_t>(1, (int64_t)(kStageBytes / (sizeof(double) * (size_t)op->dim)));
     int64_t nch = cdiv(m, cmax);
     if (nch == 1 && m >= 32 && chunks_env > 1) nch = std::min<int64_t>(chunks_env, 4);
