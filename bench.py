@@ -134,6 +134,16 @@ def c4_counts(n=1_000_000, N=16, s=10, q=1_600_000, m=M_GLOBAL):
     return nA, fft_launch, flops, bytes_
 
 
+def c4_config(world: int, m_per_gpu: int) -> dict:
+    """The `config` object of both arms (identical keys and values at the same N)."""
+    n, N, s, q = 1_000_000, 16, 10, 1_600_000
+    nA = n * (N + 1)
+    return {"workload": "C4-advdiff-n1e6-N16-s10-k256", "n": n, "Nsw": N, "substeps": s, "n_A": nA,
+            "sketch_columns": M_GLOBAL, "sketch_columns_per_gpu": m_per_gpu, "q": q,
+            "covariance": "circulant SOAR L=50", "parallelism": f"column-sharded x{world} (one global sketch)",
+            "l2": "inputs larger than L2 (sketch block %.1f GB per GPU); no flush" % (8e-9 * nA * m_per_gpu)}
+
+
 def profile_traffic(name: str, kernel: str):
     """DRAM bytes per launch of `kernel` from a committed `ncu --set full` summary."""
     path = os.path.join(ROOT, "profiles", name)
@@ -162,6 +172,8 @@ def run_reference(args):
     threads = os.cpu_count() or 1
     cols = CPU_SAMPLE_COLS
     wl, V = oracle_c4(threads, cols)
+    cfg = c4_config(world, M_GLOBAL // world)
+    assert (wl.n, wl.N, wl.substeps, wl.dim, wl.q) == (cfg["n"], cfg["Nsw"], cfg["substeps"], cfg["n_A"], cfg["q"])
     for _ in range(args.warmup):
         wl.op.apply_block_fast(V, threads)
     secs = []
@@ -180,8 +192,7 @@ def run_reference(args):
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * total / args.steps,
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (NormalStream(1) sketch, BASELINE configs[3] operator)",
-        "config": {"workload": wl.name, "n": wl.n, "Nsw": wl.N, "substeps": wl.substeps, "n_A": wl.dim,
-                   "sketch_columns": M_GLOBAL, "q": wl.q, "covariance": wl.covariance},
+        "config": cfg,
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port", "sample": sample},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
@@ -294,11 +305,7 @@ def run_ours(args):
             "scaling": "strong", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (seeded N(0,1) sketch = the reference NormalStream(1) stream, generated on the "
                     "device with MT19937-64 jump-ahead; BASELINE configs[3] operator)",
-            "config": {"workload": wl.name.replace("-m256", "") + "-k256", "n": wl.model.n, "Nsw": wl.model.N,
-                       "substeps": wl.model.substeps, "n_A": nA, "sketch_columns": M_GLOBAL,
-                       "sketch_columns_per_gpu": m, "q": wl.net.q, "covariance": "circulant SOAR L=50",
-                       "parallelism": f"column-sharded x{world} (one global sketch)",
-                       "l2": "inputs larger than L2 (sketch block %.1f GB per GPU); no flush" % (8e-9 * nA * m)},
+            "config": c4_config(world, m),
             "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": 8 * nA * m,
                     "d2h_bytes_per_step": 8 * nA * m, "steps": e2e_steps,
                     "path": "wc4dvar_gpu_op_apply_block (host pointers, pinned): two-slot chunk ring, H2D / "
