@@ -10,6 +10,37 @@
 namespace w4 {
 namespace {
 
+// Jacobi rotation (c, s) of the 2x2 problem (h = beta - alpha, g = 2 gamma or gamma): t =
+// sgn(h) g / (|h| + sqrt(h^2 + g^2)), c = 1 / sqrt(1 + t^2), s = t c.  The IEEE sqrt and
+// division sit on the serial path of every Jacobi step, so they are replaced by the MUFU
+// approximations refined with two Newton steps (1-ulp class): c^2 + s^2 = 1 holds to working
+// precision whatever the rounding of t, so the rotation stays orthogonal.
+__device__ __forceinline__ double rcp_nr(double x) {
+    double y;
+    asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
+    double e = fma(-x, y, 1.0);
+    y = fma(y, e, y);
+    e = fma(-x, y, 1.0);
+    return fma(y, e, y);
+}
+__device__ __forceinline__ double rsqrt_nr(double x) {
+    double y;
+    asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
+    const double hx = 0.5 * x;
+    double r = fma(-hx * y, y, 0.5);
+    y = fma(y, r, y);
+    r = fma(-hx * y, y, 0.5);
+    return fma(y, r, y);
+}
+__device__ __forceinline__ void jacobi_rot(double h, double g, double& c, double& s) {
+    const double x = fma(h, h, g * g);
+    const double d = x * rsqrt_nr(x);
+    const double t = (h >= 0.0 ? g : -g) * rcp_nr(fabs(h) + d);
+    c = rsqrt_nr(fma(t, t, 1.0));
+    s = t * c;
+}
+
+
 constexpr int kThreads = 1024;
 constexpr size_t kSmemMax = 200 * 1024;
 
@@ -395,14 +426,12 @@ __global__ void __launch_bounds__(kEvdThreads)
                 // pure eps threshold lets roundoff re-create above-threshold entries so the
                 // sweep never goes quiet.
                 // (squared test, no sqrt).  Rotation t = sgn(tau)/(|tau| + sqrt(1 + tau^2)),
-                // tau = h / g, rewritten as sgn(h) g / (|h| + sqrt(h^2 + g^2)): one division
-                // and one square root on this serial path, c = rsqrt(1 + t^2).
+                // tau = h / g, rewritten as sgn(h) g / (|h| + sqrt(h^2 + g^2)), c = 1 / sqrt(1
+                // + t^2) (jacobi_rot: Newton-refined MUFU reciprocal / rsqrt on this serial path).
                 const double thr = mp * DBL_EPSILON;
                 if (apq != 0.0 && apq * apq > thr * thr * fabs(app * aqq)) {
                     const double h = aqq - app, g = 2.0 * apq;
-                    const double t = (h >= 0.0 ? g : -g) / (fabs(h) + sqrt(h * h + g * g));
-                    c = rsqrt(1.0 + t * t);
-                    s = t * c;
+                    jacobi_rot(h, g, c, s);
                     rotated = 1;
                 }
                 cs_c[k] = c;
@@ -776,9 +805,7 @@ __global__ void __launch_bounds__(kThreads)
                     const double thr = mp * DBL_EPSILON;
                     if (ga != 0.0 && ga * ga > thr * thr * (al * be)) {
                         const double h = be - al, g = 2.0 * ga;
-                        const double t = (h >= 0.0 ? g : -g) / (fabs(h) + sqrt(h * h + g * g));
-                        c = rsqrt(1.0 + t * t);
-                        s = t * c;
+                        jacobi_rot(h, g, c, s);
                         rotated = 1;
                     }
                 }
@@ -897,9 +924,8 @@ __global__ void __launch_bounds__(512)
             }
             if (work && ga != 0.0 && ga * ga > thr * thr * (al * be)) {
                 const double h = be - al, g2 = 2.0 * ga;
-                const double tt = (h >= 0.0 ? g2 : -g2) / (fabs(h) + sqrt(h * h + g2 * g2));
-                const double c = rsqrt(1.0 + tt * tt);
-                const double sn = tt * c;
+                double c, sn;
+                jacobi_rot(h, g2, c, sn);
                 rotated = 1;
 #pragma unroll
                 for (int t = 0; t < RP; ++t) {
