@@ -1,6 +1,8 @@
 // Single-CTA dense kernels on the (k+l)-dimension (see smallla.cuh).
 #include "smallla.cuh"
 
+#include <cooperative_groups.h>
+
 #include <algorithm>
 #include <cfloat>
 #include <cstdio>
@@ -1030,6 +1032,197 @@ __global__ void __launch_bounds__(512)
     }
 }
 
+// ---------------------------------------------------------------- one-sided Jacobi on a cluster
+// The same Brent-Luk odd-even transposition Jacobi as svd_reg_kernel for 128 < m <= 256: one
+// WARP per column pair (lane l holds rows 2l + 64t, 2l + 1 + 64t, t < 4: 16 doubles), 128
+// warps on a cluster of four 1024-thread CTAs.  Between steps a group keeps one column and
+// hands the other to its neighbour group through a double-buffered mailbox in the
+// destination CTA's shared memory (distributed shared memory: st.shared::cluster through
+// map_shared_rank), then one cluster barrier (arrive.release / wait.acquire).  The whole
+// 256 x 256 problem stays on chip: no global-memory traffic per step (the single-CTA
+// jacobi kernels stream a 512 KB matrix through L2 every round at these sizes).
+constexpr int kCjCtas = 4, kCjWarps = 32, kCjRP = 4, kCjLd = 256;
+
+__global__ void __cluster_dims__(kCjCtas, 1, 1) __launch_bounds__(kCjWarps * 32, 1)
+    svd_cluster_kernel(int m, const double* __restrict__ Xin, int trans, double* __restrict__ sigma,
+                       double* __restrict__ U, const int* __restrict__ gate, int square,
+                       double* __restrict__ Xs, double* __restrict__ nrm, int* __restrict__ rank_of,
+                       int debug) {
+    namespace cg = cooperative_groups;
+    cg::cluster_group cluster = cg::this_cluster();
+    if (gate && *gate != 0) return;  // uniform across the cluster
+    extern __shared__ __align__(16) double csm[];
+    double* mbox = csm;                                  // [2][kCjWarps][kCjLd] (this CTA's groups)
+    double* park = csm + 2 * kCjWarps * kCjLd;           // [2][kCjLd]: groups 0 / L park a column
+    __shared__ int mid[2][kCjWarps];
+    __shared__ int any_s;
+    const int crank = (int)cluster.block_rank();
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const int k = crank * kCjWarps + w;                  // this warp's group (column pair)
+    const int mp = m + (m & 1), np = mp / 2, L = np - 1;
+    const bool active = k < np;
+    double2 a[kCjRP], b[kCjRP];
+    int ia = 2 * k, ib = 2 * k + 1, ipk = -1;            // column ids (id m: odd-m phantom)
+    auto elem = [&](int i, int j) -> double {
+        if (i >= m || j >= m) return 0.0;
+        return trans ? Xin[j + (size_t)i * m] : Xin[i + (size_t)j * m];
+    };
+#pragma unroll
+    for (int t = 0; t < kCjRP; ++t) {
+        const int i = 2 * lane + 64 * t;
+        a[t] = active ? make_double2(elem(i, ia), elem(i + 1, ia)) : make_double2(0.0, 0.0);
+        b[t] = active ? make_double2(elem(i, ib), elem(i + 1, ib)) : make_double2(0.0, 0.0);
+    }
+    const double thr = mp * DBL_EPSILON;
+    int step = 0;
+    for (int sweep = 0; sweep < 60 && m > 1; ++sweep) {
+        int rotated = 0;
+        for (int ss = 0; ss < mp; ++ss, ++step) {
+            const bool odd = step & 1;
+            const bool work = active && !(odd && k == L);
+            double al = 0.0, be = 0.0, ga = 0.0;
+#pragma unroll
+            for (int t = 0; t < kCjRP; ++t) {
+                al = fma(a[t].x, a[t].x, fma(a[t].y, a[t].y, al));
+                be = fma(b[t].x, b[t].x, fma(b[t].y, b[t].y, be));
+                ga = fma(a[t].x, b[t].x, fma(a[t].y, b[t].y, ga));
+            }
+            al = warp_sum(al);
+            be = warp_sum(be);
+            ga = warp_sum(ga);
+            if (work && ga != 0.0 && ga * ga > thr * thr * (al * be)) {
+                double c, sn;
+                jacobi_rot(be - al, 2.0 * ga, c, sn);
+                rotated = 1;
+#pragma unroll
+                for (int t = 0; t < kCjRP; ++t) {
+                    const double2 x = a[t], y = b[t];
+                    a[t] = make_double2(c * x.x - sn * y.x, c * x.y - sn * y.y);
+                    b[t] = make_double2(sn * x.x + c * y.x, sn * x.y + c * y.y);
+                }
+            }
+            if (np == 1) continue;
+            // even -> odd: keep a, send b to k - 1 (group 0 parks b), receive b from k + 1 (group L
+            // parks a); odd -> even: keep b, send a to k + 1 (group L takes its park as b),
+            // receive a from k - 1 (group 0 takes its park as a) -- as svd_reg_kernel
+            const int par = step & 1;
+            if (active) {
+                const int dst = !odd ? (k > 0 ? k - 1 : -1) : (k < L ? k + 1 : -1);
+                if (dst >= 0) {
+                    const int dr = dst / kCjWarps, dl = dst % kCjWarps;
+                    double* o = cluster.map_shared_rank(mbox + ((size_t)par * kCjWarps + dl) * kCjLd, dr);
+#pragma unroll
+                    for (int t = 0; t < kCjRP; ++t)
+                        *reinterpret_cast<double2*>(o + 2 * lane + 64 * t) = !odd ? b[t] : a[t];
+                    if (lane == 0) *cluster.map_shared_rank(&mid[par][dl], dr) = !odd ? ib : ia;
+                }
+            }
+            cluster.sync();
+            if (active) {
+                const double* in = mbox + ((size_t)par * kCjWarps + w) * kCjLd + 2 * lane;
+                double* pk = park + (k == 0 ? 0 : kCjLd) + 2 * lane;
+                if (!odd) {
+                    if (k == 0) {
+#pragma unroll
+                        for (int t = 0; t < kCjRP; ++t) *reinterpret_cast<double2*>(pk + 64 * t) = b[t];
+                        ipk = ib;
+                    }
+                    if (k == L) {
+#pragma unroll
+                        for (int t = 0; t < kCjRP; ++t) *reinterpret_cast<double2*>(pk + 64 * t) = a[t];
+                        ipk = ia;
+                    } else {
+#pragma unroll
+                        for (int t = 0; t < kCjRP; ++t) b[t] = *reinterpret_cast<const double2*>(in + 64 * t);
+                        ib = mid[par][w];
+                    }
+                } else {
+                    if (k == L) {
+#pragma unroll
+                        for (int t = 0; t < kCjRP; ++t) b[t] = *reinterpret_cast<const double2*>(pk + 64 * t);
+                        ib = ipk;
+                    }
+                    if (k == 0) {
+#pragma unroll
+                        for (int t = 0; t < kCjRP; ++t) a[t] = *reinterpret_cast<const double2*>(pk + 64 * t);
+                        ia = ipk;
+                    } else {
+#pragma unroll
+                        for (int t = 0; t < kCjRP; ++t) a[t] = *reinterpret_cast<const double2*>(in + 64 * t);
+                        ia = mid[par][w];
+                    }
+                }
+            }
+        }
+        // cluster-wide "any rotation this sweep": OR into CTA 0's flag
+        if (threadIdx.x == 0) any_s = 0;
+        cluster.sync();
+        const int anyc = __syncthreads_or(rotated);
+        if (threadIdx.x == 0 && anyc) atomicOr(cluster.map_shared_rank(&any_s, 0), 1);
+        cluster.sync();
+        const int any = *cluster.map_shared_rank(&any_s, 0);
+        if (debug && crank == 0 && threadIdx.x == 0) printf("svd_cluster m=%d sweep %d rotated %d\n", m, sweep, any);
+        cluster.sync();  // every CTA has read the flag before it is reset
+        if (!any) break;
+    }
+    // columns back by id (the phantom column dropped), then norms, ranks and the output
+    if (active) {
+#pragma unroll
+        for (int t = 0; t < kCjRP; ++t) {
+            const int i = 2 * lane + 64 * t;
+            if (ia < m) {
+                if (i < m) Xs[i + (size_t)ia * m] = a[t].x;
+                if (i + 1 < m) Xs[i + 1 + (size_t)ia * m] = a[t].y;
+            }
+            if (ib < m) {
+                if (i < m) Xs[i + (size_t)ib * m] = b[t].x;
+                if (i + 1 < m) Xs[i + 1 + (size_t)ib * m] = b[t].y;
+            }
+        }
+    }
+    cluster.sync();
+    const int gw = k, nw = kCjCtas * kCjWarps;
+    for (int j = gw; j < m; j += nw) {
+        double s2 = 0.0;
+        for (int i = lane; i < m; i += 32) s2 += Xs[i + (size_t)j * m] * Xs[i + (size_t)j * m];
+        s2 = warp_sum(s2);
+        if (lane == 0) nrm[j] = sqrt(s2);
+    }
+    cluster.sync();
+    const int gt = crank * blockDim.x + threadIdx.x, gn = kCjCtas * blockDim.x;
+    for (int i = gt; i < m; i += gn) {
+        const double ni = nrm[i];
+        int rk = 0;
+        for (int j = 0; j < m; ++j) rk += (nrm[j] > ni) || (nrm[j] == ni && j < i);
+        rank_of[i] = rk;
+        sigma[rk] = square ? ni * ni : ni;
+    }
+    cluster.sync();
+    for (int e = gt; e < m * m; e += gn) {
+        const int i = e % m, j = e / m;
+        const double sj = nrm[j];
+        U[i + (size_t)rank_of[j] * m] = sj > 0.0 ? Xs[e] / sj : 0.0;
+    }
+}
+
+// ws: m^2 + 2 m + 8 doubles of device scratch
+void launch_svd_cluster(int m, const double* X, int trans, double* sigma, double* U, const int* gate, int square,
+                        double* ws, cudaStream_t st) {
+    const size_t smem = sizeof(double) * (size_t)(2 * kCjWarps * kCjLd + 2 * kCjLd);
+    static bool attr = false;
+    if (!attr) {
+        W4_CUDA(cudaFuncSetAttribute(svd_cluster_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        attr = true;
+    }
+    double* Xs = ws;
+    double* nrm = Xs + (size_t)m * m;
+    int* rank_of = reinterpret_cast<int*>(nrm + m);
+    static const int debug = std::getenv("WC4DVAR_DEBUG_JACOBI") ? 1 : 0;
+    svd_cluster_kernel<<<kCjCtas, kCjWarps * 32, smem, st>>>(m, X, trans, sigma, U, gate, square, Xs, nrm, rank_of,
+                                                            debug);
+    W4_LAUNCH();
+}
+
 template <int RP>
 void launch_svd_reg(int m, const double* X, int trans, double* sigma, double* U, const int* gate,
                     int square, cudaStream_t st) {
@@ -1096,13 +1289,19 @@ size_t setup_smem(const void* kern, size_t bytes, int& use_smem) {
 
 }  // namespace
 
-void chol_upper(int m, const double* G, double* R, int* info, DevBuf& work, cudaStream_t st) {
+// gws: m^2 doubles of device scratch, used when the matrix does not fit shared memory
+void chol_upper_ws(int m, const double* G, double* R, int* info, double* gws, cudaStream_t st) {
     int use = 0;
     const size_t bytes = sizeof(double) * m * m;
     const size_t sh = setup_smem(reinterpret_cast<const void*>(chol_kernel<true>), bytes, use);
-    double* g = use ? nullptr : work.get<double>((size_t)m * m);
-    (use ? chol_kernel<true> : chol_kernel<false>)<<<1, kThreads, sh, st>>>(m, G, R, info, g, use);
+    (use ? chol_kernel<true> : chol_kernel<false>)<<<1, kThreads, sh, st>>>(m, G, R, info, use ? nullptr : gws, use);
     W4_LAUNCH();
+}
+
+void chol_upper(int m, const double* G, double* R, int* info, DevBuf& work, cudaStream_t st) {
+    int use = 0;
+    setup_smem(reinterpret_cast<const void*>(chol_kernel<true>), sizeof(double) * m * m, use);
+    chol_upper_ws(m, G, R, info, use ? nullptr : work.get<double>((size_t)m * m), st);
 }
 
 void chol_inv_upper(int m, const double* G, double* R, double* Rinv, int* info, DevBuf& work,
@@ -1179,8 +1378,21 @@ void sym_evd_desc(int m, const double* K, double* vals, double* W, DevBuf& work,
     const size_t bytes2 = sizeof(double) * 2 * mp * mp;
     int use = 0;
     const size_t sh = setup_smem(reinterpret_cast<const void*>(jacobi_evd_blk_kernel<true>), bytes2, use);
-    double* scratch = work.get<double>(2 * (size_t)m * m + 2 * (size_t)mp * mp + 8);
+    // cluster-Jacobi scratch (128 < m <= 256): m^2 + 2m + 8, then m^2 for the Cholesky
+    const size_t cl_ws = 2 * (size_t)m * m + 2 * (size_t)m + 8;
+    double* scratch = work.get<double>(2 * (size_t)m * m + 2 * (size_t)mp * mp + 8 + cl_ws);
     const int* gate = nullptr;
+    if (m > 128 && m <= 256 && !two_sided) {
+        // K = R^T R (Cholesky), eigenvectors = left singular vectors of R^T by the cluster
+        // one-sided Jacobi (eigenvalues sigma^2); the two-sided kernel below runs only if the
+        // Cholesky broke down (indefinite K)
+        double* R = scratch;
+        int* info = reinterpret_cast<int*>(scratch + 2 * (size_t)m * m + 2 * (size_t)mp * mp);
+        double* cws = scratch + 2 * (size_t)m * m + 2 * (size_t)mp * mp + 8;
+        chol_upper_ws(m, K, R, info, cws + (size_t)m * m + 2 * (size_t)m + 8, st);
+        launch_svd_cluster(m, R, /*trans=*/1, vals, W, info, /*square=*/1, cws, st);
+        gate = info;
+    }
     if (m <= 128 && !two_sided) {
         double* R = scratch;
         double* Ri = R + (size_t)m * m;
@@ -1204,6 +1416,9 @@ void svd_left_desc(int m, const double* X, double* sigma, double* U, DevBuf& wor
         return e && std::strcmp(e, "jacobi") == 0;
     }();
     if (m <= 128 && !two_phase) return svd_reg(m, X, 0, sigma, U, nullptr, 0, st);
+    if (m <= 256 && !two_phase)
+        return launch_svd_cluster(m, X, 0, sigma, U, nullptr, 0, work.get<double>((size_t)m * m + 2 * (size_t)m + 8),
+                                  st);
     int use = 0;
     const size_t bytes = sizeof(double) * m * m;
     const size_t sh = setup_smem(reinterpret_cast<const void*>(jacobi_svd_kernel<true>), bytes, use);

@@ -117,10 +117,11 @@ def test_chol_inv_fused_vs_torch(m):
         D.DeviceOps(0).chol_inv(_dev(G - 2 * np.abs(G).max() * np.eye(m)))
 
 
-@pytest.mark.parametrize("m", [1, 2, 7, 20, 64, 100, 128, 129])
+@pytest.mark.parametrize("m", [1, 2, 7, 20, 64, 100, 128, 129, 200, 255, 256])
 def test_small_evd_svd_vs_lapack(m):
-    """sym_evd_desc (Cholesky + register one-sided Jacobi for SPD, two-sided Jacobi fallback
-    for indefinite input) and svd_left_desc against LAPACK: values 1e-12 relative to the
+    """sym_evd_desc (Cholesky + one-sided Jacobi for SPD -- register kernel for m <= 128, the
+    4-CTA cluster kernel for 128 < m <= 256 -- with the two-sided Jacobi fallback for
+    indefinite input) and svd_left_desc against LAPACK: values 1e-12 relative to the
     largest, vectors through the projector of well-separated leading pairs."""
     rng = np.random.default_rng(100 + m)
     ops = D.DeviceOps(0)
