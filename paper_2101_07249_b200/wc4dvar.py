@@ -400,7 +400,7 @@ class LinearOperator:
 
     def __del__(self):
         h = getattr(self, "_h", None)
-        if h:
+        if h and lib is not None:  # the module global is gone at interpreter shutdown
             lib.wc4dvar_gpu_op_destroy(h)
             self._h = None
 
@@ -760,7 +760,7 @@ class LmpFactor:
 
     def __del__(self):
         h = getattr(self, "_h", None)
-        if h:
+        if h and lib is not None:  # the module global is gone at interpreter shutdown
             lib.wc4dvar_gpu_lmp_destroy(h)
             self._h = None
 
@@ -840,7 +840,7 @@ class QuadraticCost:
 
     def __del__(self):
         h = getattr(self, "_h", None)
-        if h:
+        if h and lib is not None:  # the module global is gone at interpreter shutdown
             lib.wc4dvar_gpu_cost_destroy(h)
             self._h = None
 
