@@ -410,30 +410,22 @@ __global__ void __launch_bounds__(kThreads) tiled_adj_kernel(const TiledArgs ta,
 // sub-step).  Region R = nt * P = T + 2 K S; the valid region shrinks by S per side per
 // interval.
 //
-// Gather P + 2S region values (clamped lanes feed only discarded points) and apply the fused
-// S-step stencil; results in v[S .. S+P).
+// Gather P + 2S region values and apply the fused S-step stencil; results in v[S .. S+P).
+// Rows carry GO >= ceil(S / P) guard slots on each side (`cur` points at the first region
+// slot), so EVERY thread gathers with one base register and immediate offsets: no clamped
+// edge path, whose two divergent warps per CTA used to hold every interval barrier (C4
+// sweeps 7.4 -> 5.9 ms at m = 64).  Guard slots hold whatever was there; they only feed
+// points outside the valid region, which are never emitted.
 template <int S, int P>
-__device__ __forceinline__ void blk_conv(const double* __restrict__ cur, int b, int R, int ns,
-                                         const StencilTaps& tp, double (&v)[P + 2 * S]) {
+__device__ __forceinline__ void blk_conv(const double* __restrict__ cur, int b, int ns, const StencilTaps& tp,
+                                           double (&v)[P + 2 * S]) {
     constexpr int L = P + 2 * S;
-    if (b >= S && b + P + S <= R) {
-        // interior thread: j = b + d, d = u - S compile-time, so the slot
-        // (j % P) ns + j / P = b / P + (d mod P) ns + floor(d / P) is one base register plus
-        // one of P row offsets plus an immediate
-        const double* base = cur + b / P;
+    const double* base = cur + b / P;
 #pragma unroll
-        for (int u = 0; u < L; ++u) {
-            const int d = u - S;
-            const int dm = ((d % P) + P) % P, dq = (d - dm) / P;
-            v[u] = base[dm * ns + dq];
-        }
-    } else {
-#pragma unroll
-        for (int u = 0; u < L; ++u) {
-            int j = b - S + u;
-            j = j < 0 ? 0 : (j >= R ? R - 1 : j);
-            v[u] = cur[(j % P) * ns + j / P];
-        }
+    for (int u = 0; u < L; ++u) {
+        const int d = u - S;
+        const int dm = ((d % P) + P) % P, dq = (d - dm) / P;
+        v[u] = base[dm * ns + dq];
     }
     double o[P];
 #pragma unroll
@@ -465,9 +457,9 @@ struct RowPlan {
     int s0;    // slot of element tid
     int g0;    // grid index of element tid
     bool fast;
-    __device__ void init(const Region& rg, int R, int tid, int nt, int ns) {
+    __device__ void init(const Region& rg, int R, int tid, int nt, int ns, int go) {
         fast = nt % P == 0 && R == nt * P && rg.origin >= 0 && rg.origin + R <= rg.n;
-        s0 = (tid % P) * ns + tid / P;
+        s0 = (tid % P) * ns + tid / P + go;
         g0 = rg.origin + tid;
     }
     template <class Slot>
@@ -502,7 +494,8 @@ __global__ void __launch_bounds__(NT ? NT : 512, NT == 256 ? 2 : 1) tiled_blk_fw
     const TileGeom& geo = ta.geo;
     const int R = geo.R;
     const int tid = threadIdx.x, nt = NT ? NT : blockDim.x;
-    const int ns = nt + 2, RS = P * ns;
+    constexpr int GO = (S + P - 1) / P;  // guard slots per row side
+    const int ns = nt + 2 + 2 * GO, RS = P * ns;
     double* cur = sm;
     double* nxt = sm + RS;
     double* const fx0 = sm + 2 * RS;  // forcing X_{i+1}, prefetched (double buffer)
@@ -520,9 +513,9 @@ __global__ void __launch_bounds__(NT ? NT : 512, NT == 256 ? 2 : 1) tiled_blk_fw
     const int b = tid * P;
     bool bad = false;
     double v[P + 2 * S];
-    auto slot = [&](int e) { return (e % P) * ns + e / P; };
+    auto slot = [&](int e) { return (e % P) * ns + e / P + GO; };
     RowPlan<P, NT> rp;
-    rp.init(rg, R, tid, nt, ns);
+    rp.init(rg, R, tid, nt, ns, GO);
     // regular network: observed points g = bb sx of the tile centre [g0, g1), bb from bb0
     const int sx = net.sx;
     const int g0 = (int)t0, g1 = (int)(t0 + (c_hi - c_lo));
@@ -562,11 +555,11 @@ __global__ void __launch_bounds__(NT ? NT : 512, NT == 256 ? 2 : 1) tiled_blk_fw
         if (i == ta.i1) break;
         const int k = i - ta.i0;
         if (i + 2 <= ta.i1) rp.load((k & 1) ? fx0 : fx1, X + (int64_t)(i + 2) * n, rg, R, tid, nt, slot);
-        blk_conv<S, P>(cur, b, R, ns, ta.tp, v);  // M_i = the S-step TL as one stencil
+        blk_conv<S, P>(cur + GO, b, ns, ta.tp, v);  // M_i = the S-step TL as one stencil
         const double* f = (k & 1) ? fx1 : fx0;
 #pragma unroll
         for (int p = 0; p < P; ++p)  // x_{i+1} = M_i x_i + X_{i+1}  (operators.cpp:88)
-            nxt[p * ns + tid] = v[S + p] + f[p * ns + tid];
+            nxt[p * ns + tid + GO] = v[S + p] + f[p * ns + tid + GO];
         double* t = cur;
         cur = nxt;
         nxt = t;
@@ -584,7 +577,8 @@ __global__ void __launch_bounds__(NT ? NT : 512, NT == 256 ? 2 : 1) tiled_blk_ad
     const TileGeom& geo = ta.geo;
     const int R = geo.R;
     const int tid = threadIdx.x, nt = NT ? NT : blockDim.x;
-    const int ns = nt + 2, RS = P * ns;
+    constexpr int GO = (S + P - 1) / P;  // guard slots per row side
+    const int ns = nt + 2 + 2 * GO, RS = P * ns;
     double* cur = sm;
     double* nxt = sm + RS;
     double* const vb0 = sm + 2 * RS;  // v_{i-1} rows, prefetched (double buffer)
@@ -602,9 +596,9 @@ __global__ void __launch_bounds__(NT ? NT : 512, NT == 256 ? 2 : 1) tiled_blk_ad
     const int b = tid * P;
     bool bad = false;
     double v[P + 2 * S];
-    auto slot = [&](int e) { return (e % P) * ns + e / P; };
+    auto slot = [&](int e) { return (e % P) * ns + e / P + GO; };
     RowPlan<P, NT> rp;
-    if (V) rp.init(rg, R, tid, nt, ns);
+    if (V) rp.init(rg, R, tid, nt, ns, GO);
     // H_i^T y part of the addend (sparse: observed points of observed times)
     auto obs_add = [&](int i, int g, double x) -> double {
         if (a.adj_obs) {
@@ -705,20 +699,20 @@ __global__ void __launch_bounds__(NT ? NT : 512, NT == 256 ? 2 : 1) tiled_blk_ad
 #pragma unroll
             for (int p = 0; p < P; ++p) has[p] = false, yv[p] = 0.0;
         }
-        blk_conv<S, P>(cur, b, R, ns, ta.tp, v);  // M_i^T as one stencil
+        blk_conv<S, P>(cur + GO, b, ns, ta.tp, v);  // M_i^T as one stencil
         const double* vr = (k & 1) ? vb1 : vb0;
         if (fobs) {
 #pragma unroll
-            for (int p = 0; p < P; ++p) nxt[p * ns + tid] = v[S + p];
-            if (op < P) nxt[op * ns + tid] += y0;
-            if (op + sx < P) nxt[(op + sx) * ns + tid] += y1;
+            for (int p = 0; p < P; ++p) nxt[p * ns + tid + GO] = v[S + p];
+            if (op < P) nxt[op * ns + tid + GO] += y0;
+            if (op + sx < P) nxt[(op + sx) * ns + tid + GO] += y1;
         } else {
 #pragma unroll
             for (int p = 0; p < P; ++p) {
                 // s_{i-1} = v_{i-1} + H^T y + M^T s_i  (operators.cpp:99; obs_add order)
-                double ad = V ? vr[p * ns + tid] : 0.0;
+                double ad = V ? vr[p * ns + tid + GO] : 0.0;
                 if (has[p]) ad = V ? ad + yv[p] : yv[p];
-                nxt[p * ns + tid] = ad + v[S + p];
+                nxt[p * ns + tid + GO] = ad + v[S + p];
             }
         }
         double* t = cur;
@@ -763,7 +757,7 @@ bool launch_tiled_blk(const ModelDev& md, const NetDev& net, const SweepArgs& a,
     }
     if (nt > 512 || T <= 0 || R > md.n) return false;
     TileGeom geo{T, K * S, K * S, R, false, cdiv(md.n, T)};
-    const size_t smem = sizeof(double) * 4 * (size_t)P * (nt + 2);  // cur, nxt, 2 prefetch rows
+    const size_t smem = sizeof(double) * 4 * (size_t)P * (nt + 2 + 2 * ((S + P - 1) / P));  // cur, nxt, 2 prefetch rows
     auto fk = nt == 512 ? tiled_blk_fwd_kernel<KIND, S, P, 512>
               : nt == 256 ? tiled_blk_fwd_kernel<KIND, S, P, 256> : tiled_blk_fwd_kernel<KIND, S, P, 0>;
     auto ak = nt == 512 ? tiled_blk_adj_kernel<KIND, S, P, 512>
