@@ -271,7 +271,7 @@ def run_ours(args):
     _, fft_flops_launch, flops_step, bytes_step = c4_counts(m=m)
     fft_ms = stage_ms[0] / max(calls, 1)   # the first D^{1/2}: one fftconv_kernel launch
     achieved = fft_flops_launch / (fft_ms * 1e-3) / 1e12
-    traffic, traffic_src = profile_traffic("r02b_c4_fftconv_m256.json", "PlanE6, 2, 0")
+    traffic, traffic_src = profile_traffic("r02d_c4_fftconv_m256.json", "PlanE6, 2, 0")
     try:
         peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
     except Exception:
