@@ -987,17 +987,11 @@ void launch_cps(const Job& jb, cudaStream_t st) {
     W4_LAUNCH();
 }
 
-// WC4DVAR_FFT_CPS: register budget as CTAs per SM (1: ~250 registers, no spills; 2: 128
-// registers (default); 3 (~104 registers) spilled heavily and was dropped)
+// Two CTAs per SM (128 registers).  Measured and dropped: one CTA per SM (~250 registers,
+// no spills: 19.7-20.6 vs 13.7 ms per C4 m = 64 D^{1/2}) and three (~104 registers, heavy
+// spills: 23.7 vs 13.0 ms).
 template <class P>
 void launch(const Job& jb, cudaStream_t st) {
-    static const int cps = [] {
-        const char* e = std::getenv("WC4DVAR_FFT_CPS");
-        return e ? std::atoi(e) : kCtaPerSm;
-    }();
-    if (cps == 3) {  // register budget experiment (in-place pass B only)
-        if (jb.ipb) return jb.add ? launch_cps<P, 3, true, true>(jb, st) : launch_cps<P, 3, false, true>(jb, st);
-    }
     if (jb.ipb) return jb.add ? launch_cps<P, 2, true, true>(jb, st) : launch_cps<P, 2, false, true>(jb, st);
     return jb.add ? launch_cps<P, 2, true, false>(jb, st) : launch_cps<P, 2, false, false>(jb, st);
 }
