@@ -36,6 +36,12 @@ __device__ __forceinline__ double rsqrt_nr(double x) {
 }
 __device__ __forceinline__ void jacobi_rot(double h, double g, double& c, double& s) {
     const double x = fma(h, h, g * g);
+    if (!(x > 1e-280 && x < 1e280)) {  // far outside the sketch range: IEEE path (no ftz / overflow)
+        const double t = (h >= 0.0 ? g : -g) / (fabs(h) + sqrt(h * h + g * g));
+        c = rsqrt(1.0 + t * t);
+        s = t * c;
+        return;
+    }
     const double d = x * rsqrt_nr(x);
     const double t = (h >= 0.0 ? g : -g) * rcp_nr(fabs(h) + d);
     c = rsqrt_nr(fma(t, t, 1.0));
