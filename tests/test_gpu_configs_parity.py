@@ -96,6 +96,25 @@ def test_c2_sketch_vs_oracle(c2, method):
     assert pg.orthonormality_defect() <= 1e-12
 
 
+@pytest.mark.parametrize("method", METHODS)
+def test_c2_operator_wide_sketch_vs_oracle(c2, method):
+    """k + l = 256 on the C2 operator (k = 128): the widest sketch shape of BASELINE configs[3],
+    at a size the oracle can check -- the upper-triangle Gram tiles, the triangular Y R^{-1}
+    products and the 4-CTA cluster Jacobi EVD / SVD (128 < m <= 256) against LAPACK."""
+    wl, g, o, _, b = c2
+    k, m = 128, 256
+    omega = O.gaussian_matrix(g.dim(), m, configs.OMEGA_SEED)
+    cfg = dict(target_rank=k, oversample=m - k, seed=configs.OMEGA_SEED, method=method)
+    pg = W.sketch_eigenpairs(g, W.SketchConfig(**cfg), omega)
+    po = O.sketch_eigenpairs(o, O.SketchConfig(**cfg), omega)
+    assert pg.k() == po.k() == k
+    ev = relerr(pg.values, po.values)
+    la = _lmp_action_err(pg, po, b)
+    print(f"C2 k+l=256 {method}: Ritz values rel err {ev:.2e}, LMP action rel err {la:.2e}")
+    assert ev <= 1e-10
+    assert pg.orthonormality_defect() <= 1e-12
+
+
 class _Variant(O.LinearOperator):
     """An equally valid fp64 implementation of the oracle operator, used to MEASURE how far
     rounding alone moves a long CG run: `noise` > 0 adds last-bit noise of that relative
