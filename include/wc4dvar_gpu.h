@@ -188,6 +188,17 @@ int wc4dvar_gpu_clustered_spectrum(wc4dvar_op* op, const struct wc4dvar_lmp* pre
 int wc4dvar_gpu_factor_apply_dev(wc4dvar_op* op, int which, int inv, const double* X, int64_t ldx,
                                  int64_t c, double* out, int64_t ldo, void* stream);
 
+/* Fourier-space form of HessianOperator::apply (operators.cpp:127-144), an execution
+ * strategy with the same result to rounding: for a periodic constant-coefficient TL model
+ * (advection / advection-diffusion, models.cpp:27-45), circulant covariance factors and the
+ * regular network of ObservationNetwork::build (models.cpp:159-176) every factor of A but the
+ * observation mask is diagonal in the DFT basis, so the block apply runs as one forward
+ * transform, the window recurrences per frequency class and one inverse transform.
+ * mode = 1 / 0 switches it on / off for this operator (on is refused with status 1 when the
+ * operator is not eligible), mode < 0 only queries; *active (optional) receives the state.
+ * Eligible operators start with it on unless WC4DVAR_SPECTRAL=0. */
+int wc4dvar_gpu_op_spectral(wc4dvar_op* op, int mode, int* active);
+
 int wc4dvar_gpu_op_profile(wc4dvar_op* op, int enable);
 int wc4dvar_gpu_op_profile_read(wc4dvar_op* op, double* ms3, int64_t* calls);
 

@@ -186,6 +186,7 @@ int wc4dvar_gpu_hessian_create(const wc4dvar_model_desc* model, const wc4dvar_ne
     if (bh->kind == WC4DVAR_COV_CIRCULANT) {
         h->circ = new CirculantPlan();
         h->circ->init(n, bh->half, qh->half, bh->half_inv, qh->half_inv, st);
+        h->setup_spectral(st);
         W4_CUDA(cudaStreamSynchronize(st));
         *out = h.release();
         return WC4DVAR_OK;
@@ -518,6 +519,24 @@ int wc4dvar_gpu_hessian_piece(wc4dvar_op* op, int which, const double* V, int64_
     if (rc != WC4DVAR_OK) return rc;
     d2h_block(out, ldo, dout, op->dim, m, op->stream);
     W4_CUDA(cudaStreamSynchronize(op->stream));
+    W4_API_END
+}
+
+int wc4dvar_gpu_op_spectral(wc4dvar_op* op, int mode, int* active) {
+    W4_API_BEGIN
+    require(op != nullptr, "op_spectral: null operator");
+    std::lock_guard<std::recursive_mutex> lk(op->mu);
+    HessianOp* h = dynamic_cast<HessianOp*>(op);
+    if (mode >= 0) {
+        require(h != nullptr || mode == 0, "op_spectral: not a HessianOperator");
+        if (h) {
+            require(mode == 0 || h->d_mhat != nullptr,
+                    "op_spectral: operator is not eligible (needs a periodic stencil model, circulant "
+                    "factors with a fused transform and a regular network whose stride divides n)");
+            h->spectral = mode != 0;
+        }
+    }
+    if (active) *active = (h && h->spectral) ? 1 : 0;
     W4_API_END
 }
 

@@ -140,6 +140,8 @@ void CirculantPlan::init(int64_t n, const double* h_b, const double* h_q, const 
     impl->f4.init(n, sp, st);  // leaves f4 unready when n has no suitable split
 }
 
+Fft4* CirculantPlan::spectral_fft() { return impl->f4.spectral_ready() ? &impl->f4 : nullptr; }
+
 void CirculantPlan::apply(bool inv, int N, const double* V, int64_t ldv, int64_t m, double* out,
                           int64_t ldo, const double* add, int64_t ldadd, unsigned* status,
                           DevBuf& zbuf, DevBuf& xbuf, cudaStream_t st, int only) {

@@ -5,6 +5,8 @@
 
 namespace w4 {
 
+class Fft4;
+
 struct CirculantPlan {
     struct Impl;
     Impl* impl;
@@ -22,6 +24,8 @@ struct CirculantPlan {
     void apply(bool inv, int N, const double* V, int64_t ldv, int64_t m, double* out, int64_t ldo,
                const double* add, int64_t ldadd, unsigned* status, DevBuf& zbuf, DevBuf& xbuf,
                cudaStream_t st, int only = -1);
+    // the fused four-step transform when it can run the spectral modes (spectral.cu), else null
+    Fft4* spectral_fft();
 };
 
 }  // namespace w4

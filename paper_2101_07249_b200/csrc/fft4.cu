@@ -490,6 +490,7 @@ struct Job {
     int slots;           // Y slots (WC4DVAR_FFT_SLOTS, default kSlots; >= 3)
     int ipb;             // pass B in place (DIF / DIT, digit-reversed lam); 0 = Stockham
     int prefetch;        // L2 prefetch of the next pass-A tile (WC4DVAR_FFT_PREFETCH, default 0)
+    double2* Z;          // spectral modes: np x N spectra in pass B's digit-reversed row order
 };
 
 __device__ __forceinline__ double2 wN(const Job& jb, int64_t p) {  // w_N^p, 0 <= p < N
@@ -714,6 +715,132 @@ __device__ __forceinline__ void item_b_ip(const Job& jb, double2* sm, int p, int
     }
 }
 
+// ---- spectral modes (forward-only / inverse-only transforms) -----------------------------
+// MODE 1 (forward): passes A and B', where B' is the DIF half of pass B and leaves the
+// UNSCALED spectrum of pair p in Z[p N + e + N1 k2] (frequency k2 + N2 f(e), f the digit
+// reversal of the row radices).  MODE 2 (inverse): B'' reads such a spectrum, runs the DIT
+// half of pass B into the Y slot, pass C finishes.  The window recurrence between the two
+// runs on the spectra (spectral.cu).
+template <class P, class AF>
+__device__ __forceinline__ void item_b_fwd(const Job& jb, double2* sm, int p, int rowblk, AF af) {
+    using VB = RowView<P::N1, P::S>;
+    constexpr int64_t N = (int64_t)P::N1 * P::N2;
+    constexpr int L = P::N1;
+    double2* Yp = jb.Y + ((int64_t)((p / jb.G) % jb.slots) * jb.G + p % jb.G) * N;
+    const int k20 = rowblk * P::S;
+    const uint64_t pol = jb.l2hint ? policy_evict_last() : 0;
+    {
+        constexpr int R = P::B0, M = L / P::B0;
+        using IP = Ip<VB, R, M>;
+        constexpr int BPT = (IP::NB + kNT - 1) / kNT;
+#pragma unroll
+        for (int it = 0; it < BPT; ++it) {
+            const int u = threadIdx.x + it * kNT;
+            if (IP::NB % kNT != 0 && u >= IP::NB) break;
+            int seq, e0, q;
+            IP::map(u, seq, e0, q);
+            const double2* yr = Yp + (int64_t)P::N1 * (k20 + seq) + e0;
+            double2 v[R];
+#pragma unroll
+            for (int k = 0; k < R; ++k) v[k] = ld_y(yr + k * M, pol);
+            dft<R, false>(v);
+            twiddle_pow<R>(v, __ldg(jb.tw1 + q));
+#pragma unroll
+            for (int k = 0; k < R; ++k) sm[VB::addr(seq, e0 + k * M)] = v[k];
+        }
+        cbar();
+    }
+    af();
+    if (jb.l2hint) {  // these Y rows are dead: drop them from L2 without a write-back
+        static_assert((P::N1 * 16) % 128 == 0, "rows must cover whole 128-byte lines");
+        constexpr int lpr = P::N1 * 16 / 128;
+        const char* base = reinterpret_cast<const char*>(Yp + (int64_t)P::N1 * k20);
+        for (int e = threadIdx.x; e < P::S * lpr; e += kNT) discard_l2(base + (int64_t)e * 128);
+    }
+    using FM = IpMids<VB, false, L / P::B0, typename P::BM>;
+    FM::run(sm, jb.tw1);
+    {
+        constexpr int R = P::BL;
+        using IP = Ip<VB, R, 1>;
+        constexpr int BPT = (IP::NB + kNT - 1) / kNT;
+        double2* zp = jb.Z + (int64_t)p * N;
+#pragma unroll
+        for (int it = 0; it < BPT; ++it) {
+            const int u = threadIdx.x + it * kNT;
+            if (IP::NB % kNT != 0 && u >= IP::NB) break;
+            int seq, e0, q;
+            IP::map(u, seq, e0, q);
+            double2 v[R];
+#pragma unroll
+            for (int k = 0; k < R; ++k) v[k] = sm[VB::addr(seq, e0 + k)];
+            dft<R, false>(v);
+            double2* zr = zp + (int64_t)P::N1 * (k20 + seq) + e0;
+#pragma unroll
+            for (int k = 0; k < R; ++k) zr[k] = v[k];
+        }
+    }
+}
+
+template <class P, class AF>
+__device__ __forceinline__ void item_b_inv(const Job& jb, double2* sm, int p, int rowblk, AF af) {
+    using VB = RowView<P::N1, P::S>;
+    constexpr int64_t N = (int64_t)P::N1 * P::N2;
+    constexpr int L = P::N1;
+    double2* Yp = jb.Y + ((int64_t)((p / jb.G) % jb.slots) * jb.G + p % jb.G) * N;
+    const int k20 = rowblk * P::S;
+    const uint64_t pol = jb.l2hint ? policy_evict_last() : 0;
+    {
+        constexpr int R = P::BL;
+        using IP = Ip<VB, R, 1>;
+        constexpr int BPT = (IP::NB + kNT - 1) / kNT;
+        const double2* zp = jb.Z + (int64_t)p * N;
+#pragma unroll
+        for (int it = 0; it < BPT; ++it) {
+            const int u = threadIdx.x + it * kNT;
+            if (IP::NB % kNT != 0 && u >= IP::NB) break;
+            int seq, e0, q;
+            IP::map(u, seq, e0, q);
+            const double2* zr = zp + (int64_t)P::N1 * (k20 + seq) + e0;
+            double2 v[R];
+#pragma unroll
+            for (int k = 0; k < R; ++k) v[k] = __ldg(zr + k);
+            dft<R, true>(v);
+#pragma unroll
+            for (int k = 0; k < R; ++k) sm[VB::addr(seq, e0 + k)] = v[k];
+        }
+        cbar();
+    }
+    af();
+    using IM = IpMids<VB, true, P::BL, typename P::BMr>;
+    IM::run(sm, jb.tw1);
+    {
+        constexpr int R = P::B0, M = L / P::B0;
+        using IP = Ip<VB, R, M>;
+        constexpr int BPT = (IP::NB + kNT - 1) / kNT;
+#pragma unroll
+        for (int it = 0; it < BPT; ++it) {
+            const int u = threadIdx.x + it * kNT;
+            if (IP::NB % kNT != 0 && u >= IP::NB) break;
+            int seq, e0, q;
+            IP::map(u, seq, e0, q);
+            double2 v[R];
+#pragma unroll
+            for (int k = 0; k < R; ++k) v[k] = sm[VB::addr(seq, e0 + k * M)];
+            twiddle_pow<R>(v, conj2(__ldg(jb.tw1 + q)));
+            dft<R, true>(v);
+            const int64_t k2 = k20 + seq;
+            double2 w = conj2(wN(jb, e0 * k2));
+            const double2 ws = conj2(wN(jb, M * k2));
+            double2* yr = Yp + (int64_t)P::N1 * k2 + e0;
+#pragma unroll
+            for (int k = 0; k < R; ++k) {
+                st_y(yr + k * M, cmul(v[k], w), pol);
+                if (k + 1 < R) w = cmul(w, ws);
+            }
+        }
+    }
+}
+
 template <class P, bool ADD, class AF>
 __device__ __forceinline__ void item_c(const Job& jb, double2* sm, int p, int tile, AF af) {
     using VA = ColView<P::N2, P::TC>;
@@ -777,7 +904,9 @@ __device__ __forceinline__ void item_c(const Job& jb, double2* sm, int p, int ti
     if (ADD && jb.status && bad) atomicOr(jb.status, ST_OUT_NONFINITE);
 }
 
-template <class P, int CPS, bool ADD, bool IPB>
+// MODE 0: the full convolution (A, B, C).  MODE 1: forward transform (A, B'); MODE 2: inverse
+// transform (B'', C) -- the phase a mode lacks has no tickets.
+template <class P, int CPS, bool ADD, bool IPB, int MODE>
 __global__ void __launch_bounds__(kThreads, CPS) fftconv_kernel(const Job jb) {
     extern __shared__ double2 sm[];
     __shared__ unsigned s_ticket, s_next;
@@ -786,7 +915,7 @@ __global__ void __launch_bounds__(kThreads, CPS) fftconv_kernel(const Job jb) {
     // completion release) is paid once per `sub` tiles
     constexpr int tA = P::N1 / P::TC, tB = P::N2 / P::S;  // tiles / row blocks per pair
     const int nA1 = (tA + jb.sub - 1) / jb.sub, nB1 = (tB + jb.sub - 1) / jb.sub;  // tickets per pair
-    const int nA = jb.G * nA1, nB = jb.G * nB1, nC = nA;
+    const int nA = MODE == 2 ? 0 : jb.G * nA1, nB = jb.G * nB1, nC = MODE == 1 ? 0 : jb.G * nA1;
     const unsigned stepN = (unsigned)(nA + nB + nC);
     const unsigned total = stepN * (unsigned)(jb.ngroups + 2);
     // decode ticket t into (phase, group, item): step s = {A(s), B(s - 1), C(s - 2)}
@@ -818,9 +947,14 @@ __global__ void __launch_bounds__(kThreads, CPS) fftconv_kernel(const Job jb) {
         int phase, g, r;
         decode(t, phase, g, r);
         if (g < 0 || g >= jb.ngroups) return;
-        if (phase == 0 && g >= jb.slots) {
-            dep = jb.ctr + 1 + 3 * (g - jb.slots) + 2;
-            need = (unsigned)nC;
+        if (phase == 0 && g >= jb.slots) {  // slot reuse: its last reader is C (B' when forward-only)
+            dep = jb.ctr + 1 + 3 * (g - jb.slots) + (MODE == 1 ? 1 : 2);
+            need = (unsigned)(MODE == 1 ? nB : nC);
+        } else if (phase == 1 && MODE == 2) {
+            if (g >= jb.slots) {
+                dep = jb.ctr + 1 + 3 * (g - jb.slots) + 2;
+                need = (unsigned)nC;
+            }
         } else if (phase == 1) {
             dep = jb.ctr + 1 + 3 * g + 0;
             need = (unsigned)nA;
@@ -908,7 +1042,9 @@ __global__ void __launch_bounds__(kThreads, CPS) fftconv_kernel(const Job jb) {
                     if (phase == 0) {
                         item_a<P>(jb, sm, p, u, after_first);
                     } else if (phase == 1) {
-                        if (IPB) item_b_ip<P>(jb, sm, p, u, after_first);
+                        if (MODE == 1) item_b_fwd<P>(jb, sm, p, u, after_first);
+                        else if (MODE == 2) item_b_inv<P>(jb, sm, p, u, after_first);
+                        else if (IPB) item_b_ip<P>(jb, sm, p, u, after_first);
                         else item_b<P>(jb, sm, p, u, after_first);
                     } else {
                         item_c<P, ADD>(jb, sm, p, u, after_first);
@@ -966,24 +1102,24 @@ constexpr size_t smem_bytes() {
     return sizeof(double2) * (size_t)std::max(ColView<P::N2, P::TC>::SMEM, RowView<P::N1, P::S>::SMEM);
 }
 
-template <class P, int CPS, bool ADD, bool IPB>
+template <class P, int CPS, bool ADD, bool IPB, int MODE>
 void launch_cps(const Job& jb, cudaStream_t st) {
     constexpr size_t sm = smem_bytes<P>();
     static_assert(sm <= 227 * 1024 / 2, "fftconv tile exceeds the per-CTA SMEM budget");
     static bool attr = false;
     if (!attr) {
-        W4_CUDA(cudaFuncSetAttribute(fftconv_kernel<P, CPS, ADD, IPB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     (int)sm));
+        W4_CUDA(cudaFuncSetAttribute(fftconv_kernel<P, CPS, ADD, IPB, MODE>,
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
         attr = true;
     }
     int dev = 0, nsm = kSMs, occ = 0;
     W4_CUDA(cudaGetDevice(&dev));
     W4_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
-    W4_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fftconv_kernel<P, CPS, ADD, IPB>, kThreads, sm));
+    W4_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fftconv_kernel<P, CPS, ADD, IPB, MODE>, kThreads, sm));
     const int64_t items = (int64_t)(jb.ngroups + 2) * jb.G *
                           (2 * ((P::N1 / P::TC + jb.sub - 1) / jb.sub) + (P::N2 / P::S + jb.sub - 1) / jb.sub);
     const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(items, (int64_t)nsm * std::max(occ, 1)));
-    fftconv_kernel<P, CPS, ADD, IPB><<<grid, kThreads, sm, st>>>(jb);
+    fftconv_kernel<P, CPS, ADD, IPB, MODE><<<grid, kThreads, sm, st>>>(jb);
     W4_LAUNCH();
 }
 
@@ -992,8 +1128,16 @@ void launch_cps(const Job& jb, cudaStream_t st) {
 // spills: 23.7 vs 13.0 ms).
 template <class P>
 void launch(const Job& jb, cudaStream_t st) {
-    if (jb.ipb) return jb.add ? launch_cps<P, 2, true, true>(jb, st) : launch_cps<P, 2, false, true>(jb, st);
-    return jb.add ? launch_cps<P, 2, true, false>(jb, st) : launch_cps<P, 2, false, false>(jb, st);
+    if (jb.ipb) return jb.add ? launch_cps<P, 2, true, true, 0>(jb, st) : launch_cps<P, 2, false, true, 0>(jb, st);
+    return jb.add ? launch_cps<P, 2, true, false, 0>(jb, st) : launch_cps<P, 2, false, false, 0>(jb, st);
+}
+template <class P>
+void launch_fwd(const Job& jb, cudaStream_t st) {
+    launch_cps<P, 2, false, true, 1>(jb, st);
+}
+template <class P>
+void launch_inv(const Job& jb, cudaStream_t st) {
+    return jb.add ? launch_cps<P, 2, true, true, 2>(jb, st) : launch_cps<P, 2, false, true, 2>(jb, st);
 }
 
 struct PlanInfo {
@@ -1002,14 +1146,18 @@ struct PlanInfo {
     int64_t N1, N2;
     size_t smem;
     void (*run)(const Job&, cudaStream_t);
+    void (*run_fwd)(const Job&, cudaStream_t);  // spectral modes
+    void (*run_inv)(const Job&, cudaStream_t);
 };
+#define W4_PLAN(P) P::N1, P::N2, smem_bytes<P>(), launch<P>, launch_fwd<P>, launch_inv<P>
 const PlanInfo kPlans[] = {
-    {0, {{20, 20, 10, 0}, 3}, PlanE6::N1, PlanE6::N2, smem_bytes<PlanE6>(), launch<PlanE6>},
-    {1, {{20, 20, 10, 0}, 3}, PlanE6c3::N1, PlanE6c3::N2, smem_bytes<PlanE6c3>(), launch<PlanE6c3>},
-    {0, {{20, 20, 10, 0}, 3}, Plan2E6::N1, Plan2E6::N2, smem_bytes<Plan2E6>(), launch<Plan2E6>},
-    {0, {{20, 20, 0, 0}, 2}, PlanE5::N1, PlanE5::N2, smem_bytes<PlanE5>(), launch<PlanE5>},
-    {0, {{20, 20, 0, 0}, 2}, PlanE4::N1, PlanE4::N2, smem_bytes<PlanE4>(), launch<PlanE4>},
+    {0, {{20, 20, 10, 0}, 3}, W4_PLAN(PlanE6)},
+    {1, {{20, 20, 10, 0}, 3}, W4_PLAN(PlanE6c3)},
+    {0, {{20, 20, 10, 0}, 3}, W4_PLAN(Plan2E6)},
+    {0, {{20, 20, 0, 0}, 2}, W4_PLAN(PlanE5)},
+    {0, {{20, 20, 0, 0}, 2}, W4_PLAN(PlanE4)},
 };
+#undef W4_PLAN
 
 }  // namespace
 
@@ -1094,38 +1242,63 @@ bool Fft4::init(int64_t N, const double2* const spec_half[4], cudaStream_t st) {
 void Fft4::apply(bool inv, int Nsw, const double* V, int64_t ldv, int64_t m, double* out, int64_t ldo,
                  const double* add, int64_t ldadd, unsigned* status, DevBuf& ybuf, DevBuf& pairbuf,
                  cudaStream_t st, int only) {
+    run(0, inv, Nsw, V, ldv, m, out, ldo, add, ldadd, status, nullptr, ybuf, pairbuf, st, only);
+}
+
+void Fft4::forward(int Nsw, const double* V, int64_t ldv, int64_t m, double2* Z, DevBuf& ybuf, cudaStream_t st) {
+    run(1, false, Nsw, V, ldv, m, nullptr, 0, nullptr, 0, nullptr, Z, ybuf, spair_, st, -1);
+}
+
+void Fft4::inverse(int Nsw, const double2* Z, int64_t m, double* out, int64_t ldo, const double* add,
+                   int64_t ldadd, unsigned* status, DevBuf& ybuf, cudaStream_t st) {
+    run(2, false, Nsw, nullptr, 0, m, out, ldo, add, ldadd, status, const_cast<double2*>(Z), ybuf, spair_, st, -1);
+}
+
+void Fft4::run(int mode, bool inv, int Nsw, const double* V, int64_t ldv, int64_t m, double* out, int64_t ldo,
+               const double* add, int64_t ldadd, unsigned* status, double2* Z, DevBuf& ybuf, DevBuf& pairbuf,
+               cudaStream_t st, int only) {
     // only = 0 / 1: every column uses the B / Q factor (callers pass Nsw = 0)
     const double* lamB = lam_[inv ? (only == 1 ? 3 : 2) : (only == 1 ? 1 : 0)];
     const double* lamQ = lam_[inv ? 3 : 1];
-    require(lamB && lamQ, "apply_D_half_inv: inverse factors were not provided");
+    require(mode != 0 || (lamB && lamQ), "apply_D_half_inv: inverse factors were not provided");
+    require(mode == 0 || ipb_, "spectral transforms need the in-place pass B");
     const int per = Nsw + 1;
     const int64_t ncols = (int64_t)per * m;
     require(ncols < (int64_t)1 << 30, "circulant apply: too many columns");
-    // pair window columns that use the same factor: the i = 0 blocks (B) and the rest (Q)
     std::vector<int2> pairs;
-    for (int kind = 0; kind < 2; ++kind) {
-        int64_t pend = -1;
-        for (int64_t c = 0; c < ncols; ++c) {
-            if ((c % per == 0) != (kind == 0)) continue;
-            if (pend < 0) {
-                pend = c;
-            } else {
-                pairs.push_back(make_int2((int)pend, (int)c));
-                pend = -1;
+    if (mode == 0) {
+        // pair window columns that use the same factor: the i = 0 blocks (B) and the rest (Q)
+        for (int kind = 0; kind < 2; ++kind) {
+            int64_t pend = -1;
+            for (int64_t c = 0; c < ncols; ++c) {
+                if ((c % per == 0) != (kind == 0)) continue;
+                if (pend < 0) {
+                    pend = c;
+                } else {
+                    pairs.push_back(make_int2((int)pend, (int)c));
+                    pend = -1;
+                }
             }
+            if (pend >= 0) pairs.push_back(make_int2((int)pend, -1));
         }
-        if (pend >= 0) pairs.push_back(make_int2((int)pend, -1));
+    } else {
+        // spectral modes: pair p = jj per + i packs window block i of sketch columns 2 jj and
+        // 2 jj + 1, so the window recurrence runs on the packed spectra (it is complex-linear)
+        for (int64_t jj = 0; jj < (m + 1) / 2; ++jj)
+            for (int i = 0; i < per; ++i)
+                pairs.push_back(make_int2((int)(2 * jj * per + i), 2 * jj + 1 < m ? (int)((2 * jj + 1) * per + i) : -1));
     }
     const int np = (int)pairs.size();
-    // the pair table depends only on (m, Nsw): upload once per shape (the caller holds the
-    // operator lock, so the cache is not shared between concurrent applies)
-    int2* dpairs = pairbuf.get<int2>((size_t)np);
-    if (pairs_m_ != m || pairs_per_ != per || pairs_ptr_ != dpairs) {
+    // the pair table depends only on (m, Nsw, pairing): upload once per shape (the caller holds
+    // the operator lock, so the cache is not shared between concurrent applies)
+    const int pkind = mode == 0 ? 0 : 1;  // each pairing keeps its own table and cache
+    int2* dpairs = (pkind ? spair_ : pairbuf).get<int2>((size_t)np);
+    if (pairs_m_[pkind] != m || pairs_per_[pkind] != per || pairs_ptr_[pkind] != dpairs) {
         W4_CUDA(cudaMemcpyAsync(dpairs, pairs.data(), sizeof(int2) * np, cudaMemcpyHostToDevice, st));
         W4_CUDA(cudaStreamSynchronize(st));  // pairs (pageable) is consumed before it goes away
-        pairs_m_ = m;
-        pairs_per_ = per;
-        pairs_ptr_ = dpairs;
+        pairs_m_[pkind] = m;
+        pairs_per_[pkind] = per;
+        pairs_ptr_[pkind] = dpairs;
     }
     // G pairs per group: the Y slots (kSlots G 16 N bytes) stay within ~64 MB of L2
     static const int g_env = [] {
@@ -1163,8 +1336,48 @@ void Fft4::apply(bool inv, int Nsw, const double* V, int64_t ldv, int64_t m, dou
         return e ? std::atoi(e) : 0;  // measured: 13.7 ms without vs 14.0 ms with (C4 m = 64)
     }();
     Job jb{V, ldv, out, ldo, add, ldadd, add ? status : nullptr, dpairs, np, per, G, ngroups,
-           lamB, lamQ, Y, tw1_, tw2_, tlo_, thi_, ctr, l2hint, phase_mask, sub, acq, slots, ipb_, prefetch};
-    kPlans[plan_].run(jb, st);
+           lamB, lamQ, Y, tw1_, tw2_, tlo_, thi_, ctr, l2hint, phase_mask, sub, acq, slots, ipb_, prefetch, Z};
+    if (mode == 0) kPlans[plan_].run(jb, st);
+    else if (mode == 1) kPlans[plan_].run_fwd(jb, st);
+    else kPlans[plan_].run_inv(jb, st);
+}
+
+// ---- spectral window support (spectral.cu) -------------------------------------------------
+namespace {
+// mhat[e + N1 k2] = (lft w^k + mid + rgt w^-k)^s, w = exp(-2 pi i / N), k = k2 + N2 f(e): the
+// Fourier symbol of s sub-steps of the periodic 3-point TL step y_j = lft x_{j-1} + mid x_j +
+// rgt x_{j+1} (models.cpp:27-45), in the row order pass B' leaves the spectra in
+__global__ void build_symbol_kernel(int64_t N, int N1, int N2, Radices rd, double lft, double mid, double rgt,
+                                    int s, double2* __restrict__ mhat) {
+    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < N; t += (int64_t)gridDim.x * blockDim.x) {
+        const int e = (int)(t % N1);
+        const int64_t k2 = t / N1;
+        int span = N1, pw = 1, f = 0;
+        for (int i = 0; i < rd.n; ++i) {
+            span /= rd.r[i];
+            f += ((e / span) % rd.r[i]) * pw;
+            pw *= rd.r[i];
+        }
+        const int64_t k = k2 + (int64_t)N2 * f;
+        double sn, cs;
+        sincospi(2.0 * (double)k / (double)N, &sn, &cs);  // w^k = cs - i sn
+        const double2 one = make_double2(fma(lft + rgt, cs, mid), (rgt - lft) * sn);
+        double2 acc = one;
+        for (int i = 1; i < s; ++i) acc = cmul(acc, one);
+        mhat[t] = acc;
+    }
+}
+}  // namespace
+
+int Fft4::last_radix() const {
+    const Radices& r = kPlans[plan_].brad;
+    return r.r[r.n - 1];
+}
+
+void Fft4::build_symbol(double lft, double mid, double rgt, int s, double2* mhat, cudaStream_t st) const {
+    const unsigned g = (unsigned)std::min<int64_t>(cdiv(N_, 256), 4096);
+    build_symbol_kernel<<<g, 256, 0, st>>>(N_, (int)N1_, (int)N2_, kPlans[plan_].brad, lft, mid, rgt, s, mhat);
+    W4_LAUNCH();
 }
 
 }  // namespace w4

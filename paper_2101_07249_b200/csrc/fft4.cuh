@@ -22,7 +22,24 @@ public:
                const double* add, int64_t ldadd, unsigned* status, DevBuf& ybuf, DevBuf& pairbuf,
                cudaStream_t st, int only = -1);
 
+    // Spectral modes (see spectral.cu).  forward: Z[(jj (Nsw+1) + i) N + t] = unscaled DFT of
+    // window block i of sketch columns 2 jj (real part) and 2 jj + 1 (imaginary part), t the
+    // row order of pass B' (frequency k2 + N2 f(e) at t = e + N1 k2).  inverse: out = add +
+    // IDFT of such spectra (unnormalised).
+    bool spectral_ready() const { return plan_ >= 0 && ipb_; }
+    void forward(int Nsw, const double* V, int64_t ldv, int64_t m, double2* Z, DevBuf& ybuf, cudaStream_t st);
+    void inverse(int Nsw, const double2* Z, int64_t m, double* out, int64_t ldo, const double* add, int64_t ldadd,
+                 unsigned* status, DevBuf& ybuf, cudaStream_t st);
+    int last_radix() const;  // radix of the last DIF row stage: its outputs are contiguous in t
+    // forward-factor spectra / N in the same row order (0: B^{1/2}, 1: Q^{1/2})
+    const double* lam(int which) const { return lam_[which]; }
+    // Fourier symbol of s sub-steps of the 3-point TL step, in the same row order
+    void build_symbol(double lft, double mid, double rgt, int s, double2* mhat, cudaStream_t st) const;
+
 private:
+    void run(int mode, bool inv, int Nsw, const double* V, int64_t ldv, int64_t m, double* out, int64_t ldo,
+             const double* add, int64_t ldadd, unsigned* status, double2* Z, DevBuf& ybuf, DevBuf& pairbuf,
+             cudaStream_t st, int only);
     int plan_ = -1;
     int ipb_ = 1;                // pass B in place (the lam tables are in its digit-reversed order)
     int64_t N_ = 0, N1_ = 0, N2_ = 0;
@@ -33,9 +50,10 @@ private:
     const double2* thi_ = nullptr;
     double* lam_[4] = {nullptr, nullptr, nullptr, nullptr};  // real spectra / N, transposed order
     DevBuf ctr_;                 // ticket + per-group completion counters
-    int64_t pairs_m_ = -1;       // shape of the uploaded column-pair table
-    int pairs_per_ = -1;
-    const void* pairs_ptr_ = nullptr;
+    int64_t pairs_m_[2] = {-1, -1};  // shape of the uploaded column-pair tables (convolution / spectral)
+    int pairs_per_[2] = {-1, -1};
+    const void* pairs_ptr_[2] = {nullptr, nullptr};
+    DevBuf spair_;               // pair table of the spectral modes
 };
 
 }  // namespace w4

@@ -3,10 +3,13 @@
 
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <sstream>
 
+#include "fft4.cuh"
 #include "lmp_pcg.cuh"
+#include "spectral.cuh"
 
 namespace w4 {
 
@@ -95,7 +98,40 @@ HessianOp::~HessianOp() {
     if (d_pmap) cudaFree(d_pmap);
     if (d_times) cudaFree(d_times);
     if (d_points) cudaFree(d_points);
+    if (d_mhat) cudaFree(d_mhat);
     delete circ;
+}
+
+// The Fourier-space apply needs: a fused transform with the in-place pass B, a TL step that
+// is a periodic constant-coefficient stencil, and the regular network of
+// ObservationNetwork::build (models.cpp:159-176) with a stride that divides n and the last
+// row radix.  WC4DVAR_SPECTRAL=0 keeps the grid-space path (two convolutions + sweeps).
+void HessianOp::setup_spectral(cudaStream_t st) {
+    spectral = false;
+    static const bool enabled = [] {
+        const char* e = std::getenv("WC4DVAR_SPECTRAL");
+        return !e || std::atoi(e) != 0;
+    }();
+    if (cov_kind != WC4DVAR_COV_CIRCULANT || !circ) return;
+    Fft4* f4 = circ->spectral_fft();
+    if (!f4) return;
+    if (md.kind != WC4DVAR_MODEL_IDENTITY && md.kind != WC4DVAR_MODEL_ADVECTION && md.kind != WC4DVAR_MODEL_ADVDIFF)
+        return;
+    if (nd.q == 0 || nd.sx <= 0 || n % nd.sx != 0) return;
+    if (!spectral_window_supported(nd.sx, f4->last_radix(), N + 1)) return;
+    // one sub-step: coefficients of x_{j-1}, x_j, x_{j+1} (models.cpp:27-45), as stencil_power
+    double lft = 0.0, mid = 1.0, rgt = 0.0;
+    if (md.kind == WC4DVAR_MODEL_ADVECTION) {
+        lft = md.c;
+        mid = 1.0 - md.c;
+    } else if (md.kind == WC4DVAR_MODEL_ADVDIFF) {
+        lft = md.c + md.d;
+        mid = 1.0 - md.c - 2.0 * md.d;
+        rgt = md.d;
+    }
+    W4_CUDA(cudaMalloc(&d_mhat, sizeof(double2) * (size_t)n));
+    f4->build_symbol(lft, mid, rgt, md.kind == WC4DVAR_MODEL_IDENTITY ? 1 : md.s, d_mhat, st);
+    spectral = enabled;  // d_mhat != nullptr marks the operator eligible (wc4dvar_gpu_op_spectral)
 }
 
 void HessianOp::d_half(bool inv, const double* V, int64_t ldv, int64_t m, double* out,
@@ -161,6 +197,34 @@ void HessianOp::factor_apply(int which, bool inv, const double* X, int64_t ldx, 
 void HessianOp::apply_block_dev(const double* V, int64_t ldv, int64_t m, double* out, int64_t ldo,
                                 cudaStream_t st) {
     if (m == 0) return;
+    if (spectral) {
+        // DFT -> window recurrences per frequency class -> inverse DFT (+ v); see spectral.cu
+        Fft4* f4 = circ->spectral_fft();
+        const int64_t npc = (m + 1) / 2;
+        double2* Z = t_ws.get<double2>((size_t)npc * (N + 1) * n);
+        prof_mark(0, st);
+        f4->forward(N, V, ldv, m, Z, circ_z, st);
+        prof_mark(1, st);
+        SpectralArgs sa;
+        sa.Z = Z;
+        sa.N = n;
+        sa.per = N + 1;
+        sa.npc = npc;
+        sa.lamB = f4->lam(0);
+        sa.lamQ = f4->lam(1);
+        sa.mhat = d_mhat;
+        sa.slot = nd.slot;
+        sa.RL = f4->last_radix();
+        sa.sx = nd.sx;
+        sa.r_inv = 1.0 / (sigma_obs * sigma_obs);
+        sa.status = d_status;
+        spectral_window(sa, st);
+        prof_mark(2, st);
+        f4->inverse(N, Z, m, out, ldo, V, ldv, d_status, circ_z, st);
+        prof_mark(3, st);
+        prof_pending = prof;
+        return;
+    }
     const int64_t q = nd.q;
     double* T = t_ws.get<double>((size_t)dim * m);
     double* Y = q > 0 ? y_ws.get<double>((size_t)q * m) : nullptr;

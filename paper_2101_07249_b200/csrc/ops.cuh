@@ -89,6 +89,11 @@ struct HessianOp final : wc4dvar_op {
     }
     CirculantPlan* circ = nullptr;  // WC4DVAR_COV_CIRCULANT factors
     DevBuf circ_z, circ_x;
+    // Fourier-space apply (spectral.cu): periodic constant-coefficient model, circulant factors
+    // and a regular observation network; d_mhat = symbol of one window interval
+    bool spectral = false;
+    double2* d_mhat = nullptr;
+    void setup_spectral(cudaStream_t st);
 
     ~HessianOp() override;
     const char* kind_name() const override { return "HessianOperator"; }

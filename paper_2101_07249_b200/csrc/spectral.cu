@@ -1,0 +1,149 @@
+// The sweeps of HessianOperator::apply (operators.cpp:132-141) in Fourier space.
+//
+// For a periodic constant-coefficient TL model (advection / advection-diffusion,
+// models.cpp:27-45) every operator between the two D^{1/2} of
+//     A v = v + D^{1/2} L^{-T} H^T R^{-1} H L^{-1} D^{1/2} v
+// is diagonal in the DFT basis except the observation mask, and the mask of a regular network
+// (points 0, sx, 2 sx, ...; models.cpp:159-176) only couples the sx frequencies
+// k, k + n/sx, ..., k + (sx-1) n/sx:  (mask x)^(k) = (1/sx) sum_a x^(k + a n/sx).  With circulant
+// covariance factors the whole product is therefore
+//     forward DFT -> [ per frequency class: lam, forward recurrence x_i = Mhat x_{i-1} + t_i,
+//                      class sums at the observed times, adjoint recurrence
+//                      z_i = conj(Mhat) z_{i+1} + H^T y_i, lam ] -> inverse DFT,
+// ONE forward and ONE inverse transform per column instead of the two full convolutions and
+// the two stencil sweeps of the grid-space path (half the FFT work, and a (2s+1)-tap stencil
+// per interval becomes one complex multiply).  This file is the bracketed middle step.
+//
+// Layout (Fft4::forward): the spectrum of window block i of the packed sketch-column pair jj
+// is Z[(jj per + i) N + t]; the last DIF row stage of pass B has radix RL and span 1, and its
+// output digit is the MOST significant digit of the frequency, so the sx coupled frequencies
+// of a class are the entries t = b RL + c + a (RL / sx), a < sx, of one butterfly b: a class is
+// a short strided run inside one 16 RL-byte segment.  One thread owns one frequency for the
+// whole window (consecutive threads, consecutive t: every load and store is a full coalesced
+// line): it streams the per blocks once forwards, keeping the state x in registers, and once
+// backwards, writing lam z_i in place.  The class sums of the forward pass go through SMEM:
+// every thread publishes x_i, and after the interval's one barrier the first T / sx threads
+// add up one class each into sums[i][class], which the backward pass reads back.  HBM
+// traffic: one read and one write of Z.  Both packed columns ride through as real /
+// imaginary parts: every step is complex-linear with real grid-space operators.
+#include "spectral.cuh"
+
+namespace w4 {
+namespace {
+
+constexpr int kSpecThreads = 320;  // a multiple of 32 and of every row radix (10, 20)
+constexpr int kDepth = 4;          // window blocks in flight per thread (forward pass)
+
+__device__ __forceinline__ double2 cmul(double2 a, double2 b) {
+    return make_double2(fma(a.x, b.x, -a.y * b.y), fma(a.x, b.y, a.y * b.x));
+}
+__device__ __forceinline__ double2 cmulc(double2 a, double2 b) {  // conj(a) b
+    return make_double2(fma(a.x, b.x, a.y * b.y), fma(a.x, b.y, -a.y * b.x));
+}
+
+__global__ void __launch_bounds__(kSpecThreads, 4) spectral_window_kernel(const SpectralArgs a) {
+    extern __shared__ double2 sm[];
+    const int T = kSpecThreads, t = threadIdx.x;
+    const int cps = a.RL / a.sx;  // classes per butterfly
+    const int ncl = T / a.sx;     // classes per CTA
+    double2* xbuf = sm;           // [2][T] states of the current / previous interval
+    double2* sums = sm + 2 * T;   // [per][ncl] class sums
+    const int64_t pos = blockIdx.x * (int64_t)T + t;
+    const bool act = pos < a.N;   // T and N are multiples of RL: classes are wholly in or out
+    double2* Z = a.Z + (int64_t)blockIdx.y * a.per * a.N + pos;
+    double2 M = make_double2(0.0, 0.0);
+    double lq = 0.0, lb = 0.0;
+    if (act) {
+        M = __ldg(a.mhat + pos);
+        lq = __ldg(a.lamQ + pos);
+        lb = __ldg(a.lamB + pos);
+    }
+    // scale of H^T R^{-1} H in this basis: 1 / sx from the mask, r_inv, and N because both lam
+    // tables carry the 1 / N of the transform pair
+    const double scale = a.r_inv * (double)a.N / (double)a.sx;
+    bool bad_f = false;
+    // traj = L^{-1} D^{1/2} v (operators.cpp:131-132); sums = H traj per class
+    double2 x = make_double2(0.0, 0.0);
+    double2 ring[kDepth];
+#pragma unroll
+    for (int d = 0; d < kDepth; ++d)
+        ring[d] = (act && d < a.per) ? __ldcs(Z + (int64_t)d * a.N) : make_double2(0.0, 0.0);
+    const int sb = (t / cps) * a.RL + t % cps;  // first member of the class thread t < ncl adds up
+    for (int i0 = 0; i0 < a.per; i0 += kDepth) {
+        double2 cur[kDepth];
+#pragma unroll
+        for (int d = 0; d < kDepth; ++d) {
+            cur[d] = ring[d];
+            const int in = i0 + kDepth + d;
+            ring[d] = (act && in < a.per) ? __ldcs(Z + (int64_t)in * a.N) : make_double2(0.0, 0.0);
+        }
+#pragma unroll
+        for (int d = 0; d < kDepth; ++d) {
+            const int i = i0 + d;
+            if (i >= a.per) break;
+            const double l = i == 0 ? lb : lq;
+            const double2 mx = cmul(M, x);  // x is zero before the first block
+            x = make_double2(fma(l, cur[d].x, mx.x), fma(l, cur[d].y, mx.y));
+            xbuf[(i & 1) * T + t] = x;
+            __syncthreads();
+            if (t < ncl) {
+                const double2* xb = xbuf + (i & 1) * T + sb;
+                double2 sum = make_double2(0.0, 0.0);
+                for (int e = 0; e < a.sx; ++e) {
+                    const double2 v = xb[e * cps];
+                    sum.x += v.x;
+                    sum.y += v.y;
+                }
+                bad_f |= !isfinite(sum.x + sum.y);
+                sums[i * ncl + t] = sum;
+            }
+        }
+    }
+    __syncthreads();
+    // s = L^{-T} H^T R^{-1} H traj (operators.cpp:136-140), then D^{1/2} s per block
+    const int r = t % a.RL;
+    const int mycl = (t / a.RL) * cps + r % cps;
+    double2 z = make_double2(0.0, 0.0);
+    for (int i = a.per - 1; i >= 0; --i) {
+        const double2 mz = cmulc(M, z);  // z is zero before the last block
+        z = mz;
+        if (__ldg(a.slot + i) >= 0) {
+            const double2 sum = sums[i * ncl + mycl];
+            z = make_double2(fma(scale, sum.x, mz.x), fma(scale, sum.y, mz.y));
+        }
+        const double l = i == 0 ? lb : lq;
+        if (act) __stcs(Z + (int64_t)i * a.N, make_double2(l * z.x, l * z.y));
+    }
+    const bool bad_a = !isfinite(z.x + z.y);  // a non-finite z_i propagates down to z_0
+    if (a.status && (bad_f || bad_a))
+        atomicOr(a.status, (bad_f ? ST_FWD_NONFINITE : 0u) | (bad_a ? ST_ADJ_NONFINITE : 0u));
+}
+
+size_t smem_for(int sx, int per) {
+    return sizeof(double2) * ((size_t)2 * kSpecThreads + (size_t)per * (kSpecThreads / sx));
+}
+
+}  // namespace
+
+bool spectral_window_supported(int sx, int RL, int per) {
+    if (sx < 1 || RL <= 0 || RL % sx != 0 || kSpecThreads % RL != 0) return false;
+    return smem_for(sx, per) <= 200 * 1024;
+}
+
+void spectral_window(const SpectralArgs& a, cudaStream_t st) {
+    require(spectral_window_supported(a.sx, a.RL, a.per) && a.N % a.RL == 0,
+            "spectral window: unsupported network or window");
+    require(a.npc <= 65535, "spectral window: too many columns");
+    if (a.npc == 0) return;
+    const size_t smem = smem_for(a.sx, a.per);
+    static bool attr = false;
+    if (!attr) {
+        W4_CUDA(cudaFuncSetAttribute(spectral_window_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+        attr = true;
+    }
+    const dim3 grid((unsigned)cdiv(a.N, (int64_t)kSpecThreads), (unsigned)a.npc);
+    spectral_window_kernel<<<grid, kSpecThreads, smem, st>>>(a);
+    W4_LAUNCH();
+}
+
+}  // namespace w4

@@ -113,6 +113,7 @@ SIGNATURES = {
     "wc4dvar_gpu_observation_range_dev": (ctypes.c_int, [_vp, _vp, _i64, _vp]),
     "wc4dvar_gpu_clustered_spectrum": (ctypes.c_int, [_vp, _vp, _dp, _i64, _dp, ctypes.POINTER(_i64),
                                                       ctypes.POINTER(_i64)]),
+    "wc4dvar_gpu_op_spectral": (ctypes.c_int, [_vp, ctypes.c_int, ctypes.POINTER(ctypes.c_int)]),
     "wc4dvar_gpu_op_profile": (ctypes.c_int, [_vp, ctypes.c_int]),
     "wc4dvar_gpu_op_profile_read": (ctypes.c_int, [_vp, _dp, ctypes.POINTER(_i64)]),
     "wc4dvar_gpu_probe_dmma_peak": (ctypes.c_int, [ctypes.c_int, ctypes.POINTER(ctypes.c_double)]),
@@ -439,6 +440,13 @@ class LinearOperator:
     def release_workspaces(self) -> None:
         """Free the operator's grow-only device workspaces (wc4dvar_gpu_op_release_workspaces)."""
         _check(lib.wc4dvar_gpu_op_release_workspaces(self._h))
+
+    def spectral(self, mode: int = -1) -> bool:
+        """Fourier-space apply (wc4dvar_gpu_op_spectral): mode 1 / 0 switches it on / off,
+        -1 queries; returns whether it is active."""
+        active = ctypes.c_int(0)
+        _check(lib.wc4dvar_gpu_op_spectral(self._h, int(mode), ctypes.byref(active)))
+        return bool(active.value)
 
     def profile(self, enable: bool = True) -> None:
         _check(lib.wc4dvar_gpu_op_profile(self._h, int(enable)))
