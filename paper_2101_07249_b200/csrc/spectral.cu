@@ -28,11 +28,13 @@
 // imaginary parts: every step is complex-linear with real grid-space operators.
 #include "spectral.cuh"
 
+#include "bulk.cuh"
+
 namespace w4 {
 namespace {
 
 constexpr int kSpecThreads = 320;  // a multiple of 32 and of every row radix (10, 20)
-constexpr int kDepth = 4;          // window blocks in flight per thread (forward pass)
+constexpr int kDepth = 8;          // window blocks in flight per CTA (forward pass; a power of two)
 
 __device__ __forceinline__ double2 cmul(double2 a, double2 b) {
     return make_double2(fma(a.x, b.x, -a.y * b.y), fma(a.x, b.y, a.y * b.x));
@@ -41,16 +43,34 @@ __device__ __forceinline__ double2 cmulc(double2 a, double2 b) {  // conj(a) b
     return make_double2(fma(a.x, b.x, a.y * b.y), fma(a.x, b.y, -a.y * b.x));
 }
 
-__global__ void __launch_bounds__(kSpecThreads, 4) spectral_window_kernel(const SpectralArgs a) {
+__global__ void __launch_bounds__(kSpecThreads, 3) spectral_window_kernel(const SpectralArgs a) {
     extern __shared__ double2 sm[];
+    __shared__ uint64_t bars[kDepth];
     const int T = kSpecThreads, t = threadIdx.x;
     const int cps = a.RL / a.sx;  // classes per butterfly
     const int ncl = T / a.sx;     // classes per CTA
-    double2* xbuf = sm;           // [2][T] states of the current / previous interval
-    double2* sums = sm + 2 * T;   // [per][ncl] class sums
-    const int64_t pos = blockIdx.x * (int64_t)T + t;
+    double2* ring = sm;                   // [kDepth][T] window blocks in flight (bulk copies)
+    double2* xbuf = sm + kDepth * T;      // [2][T] states of the current / previous interval
+    double2* sums = sm + (kDepth + 2) * T;  // [per][ncl] class sums
+    const int64_t pos0 = blockIdx.x * (int64_t)T, pos = pos0 + t;
     const bool act = pos < a.N;   // T and N are multiples of RL: classes are wholly in or out
-    double2* Z = a.Z + (int64_t)blockIdx.y * a.per * a.N + pos;
+    double2* Zc = a.Z + (int64_t)blockIdx.y * a.per * a.N + pos0;  // this CTA's segment of block 0
+    double2* Z = Zc + t;
+    const unsigned seg_bytes = (unsigned)(min((int64_t)T, a.N - pos0) * sizeof(double2));
+    if (t == 0) {
+#pragma unroll
+        for (int d = 0; d < kDepth; ++d) mbar_init(&bars[d], 1);
+        fence_mbar_init();
+    }
+    __syncthreads();
+    // the forward pass streams the window through a kDepth-stage ring of bulk copies: thread 0
+    // issues one 16 T-byte copy per block, every thread waits on the stage's mbarrier
+    if (t == 0) {
+        for (int d = 0; d < kDepth && d < a.per; ++d) {
+            mbar_arrive_expect_tx(&bars[d], seg_bytes);
+            bulk_g2s(ring + d * T, Zc + (int64_t)d * a.N, seg_bytes, &bars[d]);
+        }
+    }
     double2 M = make_double2(0.0, 0.0);
     double lq = 0.0, lb = 0.0;
     if (act) {
@@ -64,39 +84,39 @@ __global__ void __launch_bounds__(kSpecThreads, 4) spectral_window_kernel(const 
     bool bad_f = false;
     // traj = L^{-1} D^{1/2} v (operators.cpp:131-132); sums = H traj per class
     double2 x = make_double2(0.0, 0.0);
-    double2 ring[kDepth];
-#pragma unroll
-    for (int d = 0; d < kDepth; ++d)
-        ring[d] = (act && d < a.per) ? __ldcs(Z + (int64_t)d * a.N) : make_double2(0.0, 0.0);
     const int sb = (t / cps) * a.RL + t % cps;  // first member of the class thread t < ncl adds up
-    for (int i0 = 0; i0 < a.per; i0 += kDepth) {
-        double2 cur[kDepth];
-#pragma unroll
-        for (int d = 0; d < kDepth; ++d) {
-            cur[d] = ring[d];
-            const int in = i0 + kDepth + d;
-            ring[d] = (act && in < a.per) ? __ldcs(Z + (int64_t)in * a.N) : make_double2(0.0, 0.0);
+    for (int i = 0; i < a.per; ++i) {
+        const int st = i & (kDepth - 1);
+        mbar_wait(&bars[st], (unsigned)(i / kDepth) & 1u);
+        const double2 y = act ? ring[st * T + t] : make_double2(0.0, 0.0);
+        const double l = i == 0 ? lb : lq;
+        const double2 mx = cmul(M, x);  // x is zero before the first block
+        x = make_double2(fma(l, y.x, mx.x), fma(l, y.y, mx.y));
+        xbuf[(i & 1) * T + t] = x;
+        __syncthreads();  // x_i published; every thread has read its ring entry
+        if (t == 0 && i + kDepth < a.per) {
+            mbar_arrive_expect_tx(&bars[st], seg_bytes);
+            bulk_g2s(ring + st * T, Zc + (int64_t)(i + kDepth) * a.N, seg_bytes, &bars[st]);
         }
-#pragma unroll
-        for (int d = 0; d < kDepth; ++d) {
-            const int i = i0 + d;
-            if (i >= a.per) break;
-            const double l = i == 0 ? lb : lq;
-            const double2 mx = cmul(M, x);  // x is zero before the first block
-            x = make_double2(fma(l, cur[d].x, mx.x), fma(l, cur[d].y, mx.y));
-            xbuf[(i & 1) * T + t] = x;
-            __syncthreads();
-            if (t < ncl) {
-                const double2* xb = xbuf + (i & 1) * T + sb;
-                double2 sum = make_double2(0.0, 0.0);
-                for (int e = 0; e < a.sx; ++e) {
-                    const double2 v = xb[e * cps];
-                    sum.x += v.x;
-                    sum.y += v.y;
-                }
-                bad_f |= !isfinite(sum.x + sum.y);
-                sums[i * ncl + t] = sum;
+        if (t < ncl) {
+            const double2* xb = xbuf + (i & 1) * T + sb;
+            double2 s0 = make_double2(0.0, 0.0), s1 = s0;  // two chains
+            int e = 0;
+            for (; e + 1 < a.sx; e += 2) {
+                const double2 v0 = xb[e * cps], v1 = xb[(e + 1) * cps];
+                s0.x += v0.x;
+                s0.y += v0.y;
+                s1.x += v1.x;
+                s1.y += v1.y;
             }
+            if (e < a.sx) {
+                const double2 v0 = xb[e * cps];
+                s0.x += v0.x;
+                s0.y += v0.y;
+            }
+            const double2 sum = make_double2(s0.x + s1.x, s0.y + s1.y);
+            bad_f |= !isfinite(sum.x + sum.y);
+            sums[i * ncl + t] = sum;
         }
     }
     __syncthreads();
@@ -120,7 +140,7 @@ __global__ void __launch_bounds__(kSpecThreads, 4) spectral_window_kernel(const 
 }
 
 size_t smem_for(int sx, int per) {
-    return sizeof(double2) * ((size_t)2 * kSpecThreads + (size_t)per * (kSpecThreads / sx));
+    return sizeof(double2) * ((size_t)(kDepth + 2) * kSpecThreads + (size_t)per * (kSpecThreads / sx));
 }
 
 }  // namespace
