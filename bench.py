@@ -267,16 +267,57 @@ def run_ours(args):
     step_mean_ms = total_ms / args.steps
     clocks = clk.summary()
 
-    # ---- roofline of the dominant kernel: the fused FFT convolution (circulant D^{1/2})
+    # ---- roofline of the dominant kernel
+    # Fourier-space apply (the default for C4): forward transform, window recurrence, inverse
+    # transform + identity; the inverse transform is the longest launch.  Its algorithmic work
+    # is HALF a convolution, (N+1) m 2.5 n log2 n flops (real-FFT convention),
+    # against 24 n_A m bytes (spectra in, v in, result out): the HBM roof binds it.
+    # Grid-space apply (WC4DVAR_SPECTRAL=0): the fused convolution, fp64-bound.
+    spectral = op.spectral()
     _, fft_flops_launch, flops_step, bytes_step = c4_counts(m=m)
-    fft_ms = stage_ms[0] / max(calls, 1)   # the first D^{1/2}: one fftconv_kernel launch
-    achieved = fft_flops_launch / (fft_ms * 1e-3) / 1e12
-    traffic, traffic_src = profile_traffic("r02d_c4_fftconv_m256.json", "PlanE6, 2, 0")
     try:
         peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
     except Exception:
         peaks = {}
     hbm_peak = peaks.get("hbm_gbs", 6650.0)
+    st3 = [x / max(calls, 1) for x in stage_ms]
+    if spectral:
+        inv_ms, fwd_ms, win_ms = st3[2], st3[0], st3[1]
+        inv_bytes, fwd_bytes, win_bytes = 24.0 * nA * m, 16.0 * nA * m, 16.0 * nA * m
+        half_flops = 0.5 * (fft_flops_launch - (wl.model.N + 1) * m * wl.model.n)
+        traffic, traffic_src = profile_traffic("r02e_c4_spectral_m256.json", "1, 1, 2>")
+        roofline = {"bound": "hbm", "achieved": inv_bytes / (inv_ms * 1e-3) / 1e9, "peak": hbm_peak, "unit": "GB/s",
+                    "frac": inv_bytes / (inv_ms * 1e-3) / 1e9 / hbm_peak, "traffic": traffic,
+                    "traffic_source": traffic_src,
+                    "kernel": "fftconv_kernel MODE 2 (inverse four-step transform of the window spectra + identity)",
+                    "bytes_per_launch": inv_bytes, "launch_ms": inv_ms,
+                    "bytes_per_unit": "24 n_A per sketch column: 8 n_A of spectra in (two columns per complex "
+                                      "transform), 8 n_A of v in, 8 n_A out",
+                    "flops_per_launch": half_flops, "fp64_tflops": half_flops / (inv_ms * 1e-3) / 1e12,
+                    "fp64_frac": half_flops / (inv_ms * 1e-3) / 1e12 / fp64_peak,
+                    "peak_source": "MEASURED_PEAKS.json hbm_gbs (sustained copy); fp64 peak measured in this run "
+                                   "(all-SM mma.sync.f64 probe)",
+                    "other_kernels": {
+                        "fftconv_kernel MODE 1 (forward transform)": {
+                            "launch_ms": fwd_ms, "bytes_per_launch": fwd_bytes,
+                            "hbm_frac": fwd_bytes / (fwd_ms * 1e-3) / 1e9 / hbm_peak,
+                            "fp64_frac": half_flops / (fwd_ms * 1e-3) / 1e12 / fp64_peak},
+                        "spectral_window_kernel (window recurrences per frequency class)": {
+                            "launch_ms": win_ms, "bytes_per_launch": win_bytes,
+                            "hbm_frac": win_bytes / (win_ms * 1e-3) / 1e9 / hbm_peak}}}
+        stage_names = ("transform_forward", "window_recurrence", "transform_inverse_plus_identity")
+    else:
+        fft_ms = st3[0]   # the first D^{1/2}: one fftconv_kernel launch
+        achieved = fft_flops_launch / (fft_ms * 1e-3) / 1e12
+        traffic, traffic_src = profile_traffic("r02d_c4_fftconv_m256.json", "PlanE6, 2, 0")
+        roofline = {"bound": "fp64", "achieved": achieved, "peak": fp64_peak, "unit": "TFLOP/s",
+                    "frac": achieved / fp64_peak, "traffic": traffic, "traffic_source": traffic_src,
+                    "kernel": "fftconv_kernel (circulant D^1/2: fused four-step FFT convolution)",
+                    "flops_per_launch": fft_flops_launch, "launch_ms": fft_ms,
+                    "flops_per_unit": "(N+1)(5 n log2 n + n) per sketch column (real-FFT convention, SURVEY §8(d))",
+                    "peak_source": "measured in this run: all-SM mma.sync.f64 probe (the FP64 FMA pipe "
+                                   "measures the same ~36-37 TF/s, profiles/r01_fp64_pipes_probe.txt)"}
+        stage_names = ("d_half_in", "sweep", "d_half_out_plus_identity")
     t_roof = max(flops_step / (fp64_peak * 1e12), bytes_step / (hbm_peak * 1e9)) * 1e3
 
     # ---- e2e: the reference-facing C-ABI (wc4dvar_gpu_op_apply_block) with pinned HOST buffers
@@ -311,21 +352,18 @@ def run_ours(args):
                     "path": "wc4dvar_gpu_op_apply_block (host pointers, pinned): two-slot chunk ring, H2D / "
                             "compute / D2H on three streams", "checksum": check},
             "gpu_launches": launches,
-            "roofline": {"bound": "fp64", "achieved": achieved, "peak": fp64_peak, "unit": "TFLOP/s",
-                         "frac": achieved / fp64_peak, "traffic": traffic, "traffic_source": traffic_src,
-                         "kernel": "fftconv_kernel (circulant D^1/2: fused four-step FFT convolution)",
-                         "flops_per_launch": fft_flops_launch, "launch_ms": fft_ms,
-                         "flops_per_unit": "(N+1)(5 n log2 n + n) per sketch column (real-FFT convention, SURVEY §8(d))",
-                         "peak_source": "measured in this run: all-SM mma.sync.f64 probe (the FP64 FMA pipe "
-                                        "measures the same ~36-37 TF/s, profiles/r01_fp64_pipes_probe.txt)"},
+            "roofline": roofline,
+            "apply_path": "fourier-space (forward transform, window recurrence per frequency class, inverse "
+                          "transform)" if spectral else "grid-space (convolution, stencil sweeps, convolution)",
             "apply_roofline": {"t_roof_ms": t_roof, "frac": t_roof / step_mean_ms,
                                "bound": "fp64" if flops_step / (fp64_peak * 1e12) >= bytes_step / (hbm_peak * 1e9)
                                else "hbm",
+                               "definition": "SURVEY §8(d) algorithmic counts of the grid-space apply (two "
+                                             "convolutions + stencil sweeps), whichever path runs",
                                "flops_per_step": flops_step, "bytes_per_step": bytes_step,
                                "hbm_gbs": bytes_step / (step_mean_ms * 1e-3) / 1e9, "hbm_peak_gbs": hbm_peak,
                                "hbm_frac": bytes_step / (step_mean_ms * 1e-3) / 1e9 / hbm_peak},
-            "stage_ms": {"d_half_in": stage_ms[0] / max(calls, 1), "sweep": stage_ms[1] / max(calls, 1),
-                         "d_half_out_plus_identity": stage_ms[2] / max(calls, 1)},
+            "stage_ms": dict(zip(stage_names, st3)),
             "clocks": clocks,
         }
     del op
@@ -386,6 +424,7 @@ def _apply_timing(W, wl, m, fp64_peak, hbm_peak, reps=3):
     ms = e0.elapsed_time(e1) / reps
     st, calls = op.profile_read()
     op.profile(False)
+    spectral = op.spectral()
     if wl.b_half.kind == "dense":
         f_cov = 4.0 * n * n * (N + 1)
     else:
@@ -395,8 +434,10 @@ def _apply_timing(W, wl, m, fp64_peak, hbm_peak, reps=3):
     t_b = 8.0 * (3 * nA + 2 * q) * m / (hbm_peak * 1e9)
     t_roof = max(t_f, t_b) * 1e3
     return {"workload": wl.name, "m": m, "ms_per_apply": ms, "columns_per_s": m / (ms * 1e-3),
-            "stage_ms": {"d_half_in": st[0] / max(calls, 1), "sweep": st[1] / max(calls, 1),
-                         "d_half_out_plus_identity": st[2] / max(calls, 1)},
+            "apply_path": "fourier-space" if spectral else "grid-space",
+            "stage_ms": dict(zip(("transform_forward", "window_recurrence", "transform_inverse_plus_identity")
+                                 if spectral else ("d_half_in", "sweep", "d_half_out_plus_identity"),
+                                 [x / max(calls, 1) for x in st])),
             "roofline": {"t_roof_ms": t_roof, "bound": "fp64" if t_f >= t_b else "hbm", "frac": t_roof / ms}}
 
 
