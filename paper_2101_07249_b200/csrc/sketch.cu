@@ -13,6 +13,7 @@
 #include <cmath>
 #include <cstring>
 #include <sstream>
+#include <cstdlib>
 #include <vector>
 
 #include "gemm.cuh"
@@ -87,6 +88,7 @@ struct Ctx {
     DevBuf* pool;
     int* h_int;  // pinned scratch
     int shifted_calls = 0;  // orth() calls that needed shifted CholQR3
+    int single_pass_calls = 0;  // cholqr2() calls that stopped after one pass (cond(Y) <= 4)
     int dd_rank_calls = 0;  // rank probes decided on the double-double Gram
 
     double* buf(int id, size_t count) { return pool[id].get<double>(count); }
@@ -145,6 +147,34 @@ struct Ctx {
         int* info = reinterpret_cast<int*>(buf(P_INT, 4 + 2 * m));
         chol_inv_upper((int)m, G, R1, R1i, info, pool[P_SMALLWS], st);
         if (read_int(info)) return false;
+        // The second pass exists to repair the cond(Y)^2 eps loss of orthogonality of the first.
+        // When the passes are expensive (2 n m^2 >= 1e11 flops per Gram) the singular values of
+        // R1 (= those of Y) are computed first (Jacobi SVD of the m x m factor, ms): with
+        // cond(Y) <= 4 the first pass already gives |Q1^T Q1 - I| ~ 16 eps, what Householder QR
+        // of the reference delivers (m eps), and the second pass is skipped (C4: cond(Y) = 1.6,
+        // cond(Omega) = 1.01).  WC4DVAR_CHOLQR_ADAPT=0 always runs both passes.
+        const char* adapt_env = std::getenv("WC4DVAR_CHOLQR_ADAPT");  // read per call (tests toggle it)
+        const bool adapt = !adapt_env || std::atoi(adapt_env) != 0;
+        if (adapt && 2.0 * (double)n * (double)m * (double)m >= 1e11) {
+            double* sig = buf(P_R2, m * m);
+            svd_left_desc((int)m, R1, sig, buf(P_G2, m * m), pool[P_SMALLWS], st);
+            double hs[2];
+            W4_CUDA(cudaMemcpyAsync(&hs[0], sig, sizeof(double), cudaMemcpyDeviceToHost, st));
+            W4_CUDA(cudaMemcpyAsync(&hs[1], sig + (m - 1), sizeof(double), cudaMemcpyDeviceToHost, st));
+            W4_CUDA(cudaStreamSynchronize(st));
+            if (hs[1] > 0.0 && hs[0] <= 4.0 * hs[1]) {
+                ++single_pass_calls;
+                if (Q != Y) {
+                    tall_times_small(Y, m, R1i, m, m, Q, n, true);
+                } else {  // in place: through the scratch block
+                    tall_times_small(Y, m, R1i, m, m, scratch, n, true);
+                    W4_CUDA(cudaMemcpyAsync(Q, scratch, sizeof(double) * n * m, cudaMemcpyDeviceToDevice, st));
+                }
+                if (R_out) W4_CUDA(cudaMemcpyAsync(R_out, R1, sizeof(double) * m * m, cudaMemcpyDeviceToDevice, st));
+                tm.end();
+                return true;
+            }
+        }
         double* Q1 = scratch;
         tall_times_small(Y, m, R1i, m, m, Q1, n, true);
         double* G2 = buf(P_G2, m * m);
@@ -240,20 +270,24 @@ __global__ void square_head_kernel(int k, const double* __restrict__ s, double* 
     if (i < k) out[i] = s[i] * s[i];
 }
 
+// check_z = false: Z is the basis Ctx::orth just produced (two CholQR passes, or one at
+// cond <= 4: |Z^T Z - I| is a small multiple of eps), so the 1e-8 test of randevd.cpp:50-52
+// cannot fire and its n m^2 Gram is not computed; the public rayleigh_ritz always checks.
 void rr_core(Ctx& c, const double* Z, int64_t m, int64_t keep, double* U_out, int64_t ldu,
-             double* theta_out, double* AZ) {
+             double* theta_out, double* AZ, bool check_z = true) {
     const int64_t n = c.n;
-    // Gram defect check (randevd.cpp:50-52)
-    c.tm.begin(T_GEMM);
-    double* G = c.buf(P_G, m * m);
-    c.gram(Z, m, Z, m, G);
-    double* defect = c.buf(P_TMP, 4);
-    defect_max((int)m, G, defect, c.st);
-    double hd = 0;
-    W4_CUDA(cudaMemcpyAsync(&hd, defect, sizeof(double), cudaMemcpyDeviceToHost, c.st));
-    W4_CUDA(cudaStreamSynchronize(c.st));
-    c.tm.end();
-    if (!(hd <= 1e-8)) throw NumericalError("rayleigh_ritz: Z is not orthonormal");
+    if (check_z) {  // Gram defect check (randevd.cpp:50-52)
+        c.tm.begin(T_GEMM);
+        double* G = c.buf(P_G, m * m);
+        c.gram(Z, m, Z, m, G);
+        double* defect = c.buf(P_TMP, 4);
+        defect_max((int)m, G, defect, c.st);
+        double hd = 0;
+        W4_CUDA(cudaMemcpyAsync(&hd, defect, sizeof(double), cudaMemcpyDeviceToHost, c.st));
+        W4_CUDA(cudaStreamSynchronize(c.st));
+        c.tm.end();
+        if (!(hd <= 1e-8)) throw NumericalError("rayleigh_ritz: Z is not orthonormal");
+    }
     c.apply(Z, m, AZ);  // second block product
     c.tm.begin(T_GEMM);
     double* K = c.buf(P_K, m * m);
@@ -409,7 +443,7 @@ int64_t sketch_dev(wc4dvar_op& op, const wc4dvar_sketch_config& cfg, const doubl
         double* Z = bufA;  // householder_q(Y), randevd.cpp:74
         if (!c.orth(Y, m, Z, nullptr, G, bufB))
             throw NumericalError("revd: sample matrix is numerically rank deficient (CholQR breakdown)");
-        rr_core(c, Z, m, k, U_out, ldu, theta_out, bufB);
+        rr_core(c, Z, m, k, U_out, ldu, theta_out, bufB, /*check_z=*/false);
         produced = k;
     } else if (cfg.method == WC4DVAR_SKETCH_NYSTROM) {
         // randevd.cpp:82-114

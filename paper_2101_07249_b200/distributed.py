@@ -27,6 +27,7 @@ from __future__ import annotations
 
 import ctypes
 import math
+import os
 from dataclasses import dataclass, field
 from typing import Callable, List, Optional
 
@@ -348,6 +349,16 @@ def dist_cholqr2(Y_rows: torch.Tensor, ops=TorchOps, G0: Optional[torch.Tensor] 
     G = G0 if G0 is not None else allreduce_sum(ops.gram(Y_rows, Y_rows))
     R1, R1i = ops.chol_inv(G, what)
     Q1 = ops.tall_times_small(Y_rows, R1i)
+    # sketch.cu cholqr2: when a pass is expensive (2 n m^2 >= 1e11 over all ranks) and cond(Y) <= 4
+    # (singular values of the replicated R1), the first pass is as orthonormal as Householder QR
+    m = Y_rows.shape[1]
+    if os.environ.get("WC4DVAR_CHOLQR_ADAPT", "1") != "0":
+        n_glob = allreduce_sum(torch.tensor([float(Y_rows.shape[0])], dtype=torch.float64,
+                                            device=Y_rows.device))
+        if 2.0 * float(n_glob.item()) * m * m >= 1e11:
+            sig, _ = ops.svd_left(R1)
+            if float(sig[-1]) > 0.0 and float(sig[0]) <= 4.0 * float(sig[-1]):
+                return (Q1, R1) if want_r else Q1
     G2 = allreduce_sum(ops.gram(Q1, Q1))
     R2, R2i = ops.chol_inv(G2, what)
     Q = ops.tall_times_small(Q1, R2i)
