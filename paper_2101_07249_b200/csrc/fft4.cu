@@ -1245,15 +1245,19 @@ void Fft4::apply(bool inv, int Nsw, const double* V, int64_t ldv, int64_t m, dou
     run(0, inv, Nsw, V, ldv, m, out, ldo, add, ldadd, status, nullptr, ybuf, pairbuf, st, only);
 }
 
-void Fft4::forward(int Nsw, const double* V, int64_t ldv, int64_t m, double2* Z, DevBuf& ybuf, cudaStream_t st) {
-    run(1, false, Nsw, V, ldv, m, nullptr, 0, nullptr, 0, nullptr, Z, ybuf, spair_, st, -1);
+void Fft4::forward(int Nsw, const double* V, int64_t ldv, int64_t m, double2* Z, DevBuf& ybuf, cudaStream_t st,
+                   bool pack_blocks) {
+    run(pack_blocks ? 3 : 1, false, Nsw, V, ldv, m, nullptr, 0, nullptr, 0, nullptr, Z, ybuf, spair_, st, -1);
 }
 
 void Fft4::inverse(int Nsw, const double2* Z, int64_t m, double* out, int64_t ldo, const double* add,
-                   int64_t ldadd, unsigned* status, DevBuf& ybuf, cudaStream_t st) {
-    run(2, false, Nsw, nullptr, 0, m, out, ldo, add, ldadd, status, const_cast<double2*>(Z), ybuf, spair_, st, -1);
+                   int64_t ldadd, unsigned* status, DevBuf& ybuf, cudaStream_t st, bool pack_blocks) {
+    run(pack_blocks ? 4 : 2, false, Nsw, nullptr, 0, m, out, ldo, add, ldadd, status, const_cast<double2*>(Z), ybuf,
+        spair_, st, -1);
 }
 
+// mode 0: convolution; 1 / 2: forward / inverse transform, sketch columns packed in pairs;
+// 3 / 4: forward / inverse transform of ONE column, window blocks packed in pairs
 void Fft4::run(int mode, bool inv, int Nsw, const double* V, int64_t ldv, int64_t m, double* out, int64_t ldo,
                const double* add, int64_t ldadd, unsigned* status, double2* Z, DevBuf& ybuf, DevBuf& pairbuf,
                cudaStream_t st, int only) {
@@ -1281,6 +1285,11 @@ void Fft4::run(int mode, bool inv, int Nsw, const double* V, int64_t ldv, int64_
             }
             if (pend >= 0) pairs.push_back(make_int2((int)pend, -1));
         }
+    } else if (mode >= 3) {
+        // one column: pair a packs its window blocks 2a (real part) and 2a + 1 (imaginary part);
+        // the window kernel separates them by Hermitian symmetry (spectral.cu)
+        require(m == 1, "block-packed transforms take one column");
+        for (int a = 0; 2 * a < per; ++a) pairs.push_back(make_int2(2 * a, 2 * a + 1 < per ? 2 * a + 1 : -1));
     } else {
         // spectral modes: pair p = jj per + i packs window block i of sketch columns 2 jj and
         // 2 jj + 1, so the window recurrence runs on the packed spectra (it is complex-linear)
@@ -1291,8 +1300,8 @@ void Fft4::run(int mode, bool inv, int Nsw, const double* V, int64_t ldv, int64_
     const int np = (int)pairs.size();
     // the pair table depends only on (m, Nsw, pairing): upload once per shape (the caller holds
     // the operator lock, so the cache is not shared between concurrent applies)
-    const int pkind = mode == 0 ? 0 : 1;  // each pairing keeps its own table and cache
-    int2* dpairs = (pkind ? spair_ : pairbuf).get<int2>((size_t)np);
+    const int pkind = mode == 0 ? 0 : (mode >= 3 ? 2 : 1);  // each pairing keeps its own table and cache
+    int2* dpairs = (pkind == 2 ? hpair_ : (pkind ? spair_ : pairbuf)).get<int2>((size_t)np);
     if (pairs_m_[pkind] != m || pairs_per_[pkind] != per || pairs_ptr_[pkind] != dpairs) {
         W4_CUDA(cudaMemcpyAsync(dpairs, pairs.data(), sizeof(int2) * np, cudaMemcpyHostToDevice, st));
         W4_CUDA(cudaStreamSynchronize(st));  // pairs (pageable) is consumed before it goes away
@@ -1338,7 +1347,7 @@ void Fft4::run(int mode, bool inv, int Nsw, const double* V, int64_t ldv, int64_
     Job jb{V, ldv, out, ldo, add, ldadd, add ? status : nullptr, dpairs, np, per, G, ngroups,
            lamB, lamQ, Y, tw1_, tw2_, tlo_, thi_, ctr, l2hint, phase_mask, sub, acq, slots, ipb_, prefetch, Z};
     if (mode == 0) kPlans[plan_].run(jb, st);
-    else if (mode == 1) kPlans[plan_].run_fwd(jb, st);
+    else if (mode == 1 || mode == 3) kPlans[plan_].run_fwd(jb, st);
     else kPlans[plan_].run_inv(jb, st);
 }
 
@@ -1368,6 +1377,12 @@ __global__ void build_symbol_kernel(int64_t N, int N1, int N2, Radices rd, doubl
     }
 }
 }  // namespace
+
+void Fft4::row_radices(int (&r)[4], int& n) const {
+    const Radices& rd = kPlans[plan_].brad;
+    for (int i = 0; i < 4; ++i) r[i] = rd.r[i];
+    n = rd.n;
+}
 
 int Fft4::last_radix() const {
     const Radices& r = kPlans[plan_].brad;

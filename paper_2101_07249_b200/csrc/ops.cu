@@ -200,6 +200,39 @@ void HessianOp::apply_block_dev(const double* V, int64_t ldv, int64_t m, double*
     if (spectral) {
         // DFT -> window recurrences per frequency class -> inverse DFT (+ v); see spectral.cu
         Fft4* f4 = circ->spectral_fft();
+        // one column (PCG, Lanczos): pack its window blocks in pairs instead of leaving every
+        // transform half empty (WC4DVAR_SPECTRAL_PACK1=0: the generic form)
+        static const bool pack1 = [] {
+            const char* e = std::getenv("WC4DVAR_SPECTRAL_PACK1");
+            return !e || std::atoi(e) != 0;
+        }();
+        if (m == 1 && pack1 && N >= 1) {
+            const int64_t npk = (N + 2) / 2;
+            double2* Zin = t_ws.get<double2>((size_t)2 * npk * n);
+            double2* Zout = Zin + npk * n;
+            prof_mark(0, st);
+            f4->forward(N, V, ldv, 1, Zin, circ_z, st, true);
+            prof_mark(1, st);
+            SpectralArgs sa;
+            sa.N = n;
+            sa.per = N + 1;
+            sa.lamB = f4->lam(0);
+            sa.lamQ = f4->lam(1);
+            sa.mhat = d_mhat;
+            sa.slot = nd.slot;
+            sa.RL = f4->last_radix();
+            sa.sx = nd.sx;
+            sa.r_inv = 1.0 / (sigma_obs * sigma_obs);
+            sa.status = d_status;
+            int rad[4], nrad = 0;
+            f4->row_radices(rad, nrad);
+            spectral_window1(sa, Zin, Zout, (int)f4->n1(), (int)f4->n2(), rad, nrad, st);
+            prof_mark(2, st);
+            f4->inverse(N, Zout, 1, out, ldo, V, ldv, d_status, circ_z, st, true);
+            prof_mark(3, st);
+            prof_pending = prof;
+            return;
+        }
         const int64_t npc = (m + 1) / 2;
         double2* Z = t_ws.get<double2>((size_t)npc * (N + 1) * n);
         prof_mark(0, st);

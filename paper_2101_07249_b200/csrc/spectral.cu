@@ -139,6 +139,123 @@ __global__ void __launch_bounds__(kSpecThreads, 3) spectral_window_kernel(const 
         atomicOr(a.status, (bad_f ? ST_FWD_NONFINITE : 0u) | (bad_a ? ST_ADJ_NONFINITE : 0u));
 }
 
+// ---- one column (PCG / Lanczos applies): window blocks packed in pairs --------------------
+// A single column would leave the imaginary half of every packed transform empty.  Instead
+// Fft4::forward(pack_blocks) packs window blocks 2a and 2a + 1 of the column as real /
+// imaginary part, P_a = v_2a + i v_2a+1, and this kernel separates the two real spectra by
+// Hermitian symmetry, v^_2a(k) = (P^_a(k) + conj P^_a(-k)) / 2, v^_2a+1(k) = (P^_a(k) -
+// conj P^_a(-k)) / (2 i), runs the same recurrences and class sums, and writes
+// lam z^_2a + i lam z^_2a+1 for the inverse transform: half the transforms of the unpacked form.
+// In the row order of pass B' (t = e + N1 k2, k = k2 + N2 f(e)) the mirror of row k2 > 0 is row
+// N2 - k2 read backwards (digit-wise complement: e' = N1 - 1 - e); row 0 mirrors into itself
+// through f.  Out of place (Zin -> Zout): a thread reads its mirror's entries.
+struct Window1Args {
+    const double2* Zin;
+    double2* Zout;
+    int npk;     // packed pairs, (per + 1) / 2
+    int N1, N2;
+    int rad[4];  // DIF row radices, first stage first
+    int nrad;
+};
+
+__device__ __forceinline__ int64_t mirror_pos(const Window1Args& w, int64_t t) {
+    const int e = (int)(t % w.N1), k2 = (int)(t / w.N1);
+    if (k2 > 0) return (int64_t)(w.N2 - k2) * w.N1 + (w.N1 - 1 - e);
+    int span = w.N1, pw = 1, k1 = 0;  // k1 = f(e)
+    for (int i = 0; i < w.nrad; ++i) {
+        span /= w.rad[i];
+        k1 += ((e / span) % w.rad[i]) * pw;
+        pw *= w.rad[i];
+    }
+    k1 = (w.N1 - k1) % w.N1;
+    span = w.N1;
+    pw = 1;
+    int em = 0;  // f^{-1}(k1)
+    for (int i = 0; i < w.nrad; ++i) {
+        span /= w.rad[i];
+        em += ((k1 / pw) % w.rad[i]) * span;
+        pw *= w.rad[i];
+    }
+    return em;
+}
+
+__global__ void __launch_bounds__(kSpecThreads) spectral_window1_kernel(const SpectralArgs a, const Window1Args w) {
+    extern __shared__ double2 sm[];
+    const int T = kSpecThreads, t = threadIdx.x;
+    const int cps = a.RL / a.sx, ncl = T / a.sx;
+    double2* xbuf = sm;          // [2][T]
+    double2* sums = sm + 2 * T;  // [per][ncl]
+    const int64_t pos = blockIdx.x * (int64_t)T + t;
+    const bool act = pos < a.N;
+    const int64_t mpos = act ? mirror_pos(w, pos) : 0;
+    double2 M = make_double2(0.0, 0.0);
+    double lq = 0.0, lb = 0.0;
+    if (act) {
+        M = __ldg(a.mhat + pos);
+        lq = __ldg(a.lamQ + pos);
+        lb = __ldg(a.lamB + pos);
+    }
+    const double scale = a.r_inv * (double)a.N / (double)a.sx;
+    const int sb = (t / cps) * a.RL + t % cps;
+    bool bad_f = false;
+    double2 x = make_double2(0.0, 0.0);
+    double2 p = make_double2(0.0, 0.0), pm = p;
+    if (act) {
+        p = __ldg(w.Zin + pos);
+        pm = __ldg(w.Zin + mpos);
+    }
+    for (int i = 0; i < a.per; ++i) {
+        double2 y;
+        if ((i & 1) == 0) {
+            y = make_double2(0.5 * (p.x + pm.x), 0.5 * (p.y - pm.y));  // (P + conj Pm) / 2
+        } else {
+            y = make_double2(0.5 * (p.y + pm.y), 0.5 * (pm.x - p.x));  // (P - conj Pm) / (2 i)
+            if (act && i + 1 < a.per) {  // next pair
+                p = __ldg(w.Zin + (int64_t)((i + 1) >> 1) * a.N + pos);
+                pm = __ldg(w.Zin + (int64_t)((i + 1) >> 1) * a.N + mpos);
+            }
+        }
+        const double l = i == 0 ? lb : lq;
+        const double2 mx = cmul(M, x);
+        x = make_double2(fma(l, y.x, mx.x), fma(l, y.y, mx.y));
+        xbuf[(i & 1) * T + t] = x;
+        __syncthreads();
+        if (t < ncl) {
+            const double2* xb = xbuf + (i & 1) * T + sb;
+            double2 sum = make_double2(0.0, 0.0);
+            for (int e = 0; e < a.sx; ++e) {
+                const double2 v = xb[e * cps];
+                sum.x += v.x;
+                sum.y += v.y;
+            }
+            bad_f |= !isfinite(sum.x + sum.y);
+            sums[i * ncl + t] = sum;
+        }
+    }
+    __syncthreads();
+    const int r = t % a.RL;
+    const int mycl = (t / a.RL) * cps + r % cps;
+    double2 z = make_double2(0.0, 0.0), odd = z;
+    for (int i = a.per - 1; i >= 0; --i) {
+        const double2 mz = cmulc(M, z);
+        z = mz;
+        if (__ldg(a.slot + i) >= 0) {
+            const double2 sum = sums[i * ncl + mycl];
+            z = make_double2(fma(scale, sum.x, mz.x), fma(scale, sum.y, mz.y));
+        }
+        const double l = i == 0 ? lb : lq;
+        const double2 o = make_double2(l * z.x, l * z.y);
+        if (i & 1) {
+            odd = o;
+        } else {  // lam z_2a + i lam z_2a+1
+            if (act) w.Zout[(int64_t)(i >> 1) * a.N + pos] = make_double2(o.x - odd.y, o.y + odd.x);
+            odd = make_double2(0.0, 0.0);
+        }
+    }
+    const bool bad_a = !isfinite(z.x + z.y);
+    if (a.status && (bad_f || bad_a)) atomicOr(a.status, (bad_f ? ST_FWD_NONFINITE : 0u) | (bad_a ? ST_ADJ_NONFINITE : 0u));
+}
+
 size_t smem_for(int sx, int per) {
     return sizeof(double2) * ((size_t)(kDepth + 2) * kSpecThreads + (size_t)per * (kSpecThreads / sx));
 }
@@ -163,6 +280,28 @@ void spectral_window(const SpectralArgs& a, cudaStream_t st) {
     }
     const dim3 grid((unsigned)cdiv(a.N, (int64_t)kSpecThreads), (unsigned)a.npc);
     spectral_window_kernel<<<grid, kSpecThreads, smem, st>>>(a);
+    W4_LAUNCH();
+}
+
+void spectral_window1(const SpectralArgs& a, const double2* Zin, double2* Zout, int N1, int N2, const int (&rad)[4],
+                      int nrad, cudaStream_t st) {
+    require(spectral_window_supported(a.sx, a.RL, a.per) && a.N % a.RL == 0,
+            "spectral window: unsupported network or window");
+    Window1Args w;
+    w.Zin = Zin;
+    w.Zout = Zout;
+    w.npk = (a.per + 1) / 2;
+    w.N1 = N1;
+    w.N2 = N2;
+    for (int i = 0; i < 4; ++i) w.rad[i] = rad[i];
+    w.nrad = nrad;
+    const size_t smem = sizeof(double2) * ((size_t)2 * kSpecThreads + (size_t)a.per * (kSpecThreads / a.sx));
+    static bool attr = false;
+    if (!attr) {
+        W4_CUDA(cudaFuncSetAttribute(spectral_window1_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+        attr = true;
+    }
+    spectral_window1_kernel<<<(unsigned)cdiv(a.N, (int64_t)kSpecThreads), kSpecThreads, smem, st>>>(a, w);
     W4_LAUNCH();
 }
 

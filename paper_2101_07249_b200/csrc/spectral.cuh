@@ -23,5 +23,9 @@ struct SpectralArgs {
 // strides the kernel is compiled for, and the SMEM limit on the window length
 bool spectral_window_supported(int sx, int RL, int per);
 void spectral_window(const SpectralArgs& a, cudaStream_t st);
+// One column with its window blocks packed in pairs (Fft4::forward(pack_blocks)): Zin -> Zout,
+// (per + 1) / 2 spectra each; a.Z / a.npc are unused.
+void spectral_window1(const SpectralArgs& a, const double2* Zin, double2* Zout, int N1, int N2, const int (&rad)[4],
+                      int nrad, cudaStream_t st);
 
 }  // namespace w4

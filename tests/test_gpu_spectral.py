@@ -54,6 +54,29 @@ def test_spectral_apply_vs_oracle(sx, m, kind):
     assert relerr(g.apply(v), o.apply(v)) <= 1e-12  # single vector: an unpaired (half-empty) packing
 
 
+def test_spectral_single_column_block_packing(monkeypatch):
+    """One column packs its window blocks in pairs and separates the spectra by Hermitian
+    symmetry (spectral_window1): odd and even block counts, the self-mirrored row k2 = 0 of the
+    digit-reversed order, against the oracle and against the generic (half-empty) packing."""
+    for n, N, sx in ((10000, 3, 10), (10000, 4, 4), (100000, 6, 10)):
+        bh, qh = circ_factors(n, 7.0)
+        model, net = W.AdvDiffLinearized(n, N, 0.5, 0.2, 3), _net(n, N, sx)
+        g, o = pair(model, net, bh, qh, 0.1)
+        assert g.spectral()
+        v = O.gaussian_matrix(g.dim(), 1, 5)[:, 0].copy()
+        ref = o.apply(v) if n <= 10000 else None
+        packed = g.apply(v)
+        monkeypatch.setenv("WC4DVAR_SPECTRAL_PACK1", "0")
+        g2 = W.HessianOperator(model, net, bh, qh, 0.1)  # the switch is read once per process: see below
+        generic = g2.apply_block(np.asfortranarray(np.stack([v, 0.5 * v], axis=1)))[:, 0]
+        monkeypatch.delenv("WC4DVAR_SPECTRAL_PACK1")
+        if ref is not None:
+            assert relerr(packed, ref) <= 1e-12
+        err = relerr(packed, generic)
+        print(f"n={n} N={N}: block-packed single column vs column-packed {err:.2e}")
+        assert err <= 1e-12
+
+
 def test_spectral_time_subsets_and_long_window():
     """Observation times that skip intervals and include time 0 (slot table), and a window longer
     than the kernel's load ring."""
