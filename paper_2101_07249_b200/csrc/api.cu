@@ -277,12 +277,13 @@ int wc4dvar_gpu_op_apply_block(wc4dvar_op* op, const double* V, int64_t ldv, int
     // WC4DVAR_PIPELINE_STAGE_MB: device bytes per chunk slot (default 512; C4 k = 256 e2e step
     // 840 / 778 / 749 ms at 4096 / 1024 / 512 MB against a 722 ms PCIe floor): small enough that
     // the ramp (first H2D) and the tail (last compute + D2H) are short against a step of
-    // full-duplex PCIe traffic, large enough that every chunk fills the GPU (C4: 3 columns)
+    // full-duplex PCIe traffic, large enough that every chunk fills the GPU (C4: 2 columns)
     static const size_t kStageBytes = [] {
         const char* e = std::getenv("WC4DVAR_PIPELINE_STAGE_MB");
         return (size_t)(e ? std::max(64, std::atoi(e)) : 512) << 20;
     }();
-    const int64_t cmax = std::max<int64_t>(1, (int64_t)(kStageBytes / (sizeof(double) * (size_t)op->dim)));
+    int64_t cmax = std::max<int64_t>(1, (int64_t)(kStageBytes / (sizeof(double) * (size_t)op->dim)));
+    if (cmax > 1 && (cmax & 1)) --cmax;  // even chunks: the Fourier-space apply packs columns in pairs
     int64_t nch = cdiv(m, cmax);
     if (nch == 1 && m >= 32 && chunks_env > 1) nch = std::min<int64_t>(chunks_env, 4);
     if (op->prof && m <= cmax) nch = 1;  // stage timers see one apply
