@@ -43,8 +43,10 @@ __host__ __device__ constexpr int nvec_of(int mode) {
     return mode == M_UTV ? 3 : (mode == M_APPLY || mode == M_APPLY_T) ? 1 : mode == M_P1 ? 2 : mode == M_P2 ? 4 : 2;
 }
 
-template <int MODE, int NACC>
-__global__ void __launch_bounds__(kRP, 1)
+// CPS: CTAs per SM.  1 when the stages hold U tiles (2 x 96 KB); without an LMP (k = 0) a tile
+// is only RB rows of 2-4 vectors, and four co-resident CTAs keep enough bytes in flight.
+template <int MODE, int NACC, int CPS = 1>
+__global__ void __launch_bounds__(kRP, CPS)
     rowpass_kernel(const RowPassCtx c, const PassArgs A, int RB, int nparts, int bulk) {
     extern __shared__ __align__(16) double sm[];
     __shared__ __align__(8) uint64_t bars[2];
@@ -286,6 +288,12 @@ void launch_pass_n(const RowPassCtx& c, const PassArgs& a, cudaStream_t st) {
         W4_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
     }
     const int64_t ntiles = cdiv(c.n, RB);
+    if (NACC == 0 && c.k == 0) {  // plain vector passes: four CTAs per SM (partials: <= 2048 CTAs)
+        const int64_t grid4 = std::max<int64_t>(1, std::min<int64_t>({ntiles, (int64_t)4 * nsm, (int64_t)2048}));
+        rowpass_kernel<MODE, 0, 4><<<(unsigned)grid4, kRP, smem, st>>>(c, a, RB, nparts, bulk ? 1 : 0);
+        W4_LAUNCH();
+        return;
+    }
     const int64_t grid = std::max<int64_t>(1, std::min<int64_t>({ntiles, (int64_t)nsm, cdiv(c.n, 32) + 1}));
     kern<<<(unsigned)grid, kRP, smem, st>>>(c, a, RB, nparts, bulk ? 1 : 0);
     W4_LAUNCH();
