@@ -28,7 +28,7 @@ namespace {
 
 enum {
     P_Y = 0, P_Z, P_Q1, P_AZ, P_F, P_G, P_R1, P_R1I, P_G2, P_R2, P_R2I, P_R, P_K, P_W,
-    P_VALS, P_INT, P_TMP, P_SEL, P_GEMMWS, P_SMALLWS, P_DDWS, P_COUNT
+    P_VALS, P_INT, P_TMP, P_SEL, P_GEMMWS, P_SMALLWS, P_DDWS, P_RA, P_RB, P_COUNT
 };
 
 static_assert(P_COUNT <= 24, "sketch workspaces must stay below the PCG pool range (ops.cuh)");
@@ -129,6 +129,46 @@ struct Ctx {
         gemm_nn(&p, 1, nullptr, st);
     }
 
+    // Adaptive CholQR test: passes are expensive (2 n m^2 >= 1e11 flops per Gram) and the
+    // singular values of R1 (those of Y; Jacobi SVD of the m x m factor) give cond(Y) <= 4.
+    bool single_pass_ok(const double* R1, int64_t m) {
+        const char* adapt_env = std::getenv("WC4DVAR_CHOLQR_ADAPT");  // read per call (tests toggle it)
+        const bool adapt = !adapt_env || std::atoi(adapt_env) != 0;
+        if (!adapt || 2.0 * (double)n * (double)m * (double)m < 1e11) return false;
+        double* sig = buf(P_R2, m * m);
+        svd_left_desc((int)m, R1, sig, buf(P_G2, m * m), pool[P_SMALLWS], st);
+        double hs[2];
+        W4_CUDA(cudaMemcpyAsync(&hs[0], sig, sizeof(double), cudaMemcpyDeviceToHost, st));
+        W4_CUDA(cudaMemcpyAsync(&hs[1], sig + (m - 1), sizeof(double), cudaMemcpyDeviceToHost, st));
+        W4_CUDA(cudaStreamSynchronize(st));
+        return hs[1] > 0.0 && hs[0] <= 4.0 * hs[1];
+    }
+
+    // Factored orthonormalisation for callers that only multiply the basis by a small matrix
+    // next (Q W = Y (R^{-1} W)): when one CholQR pass suffices, R and R^{-1} of Y = Q R are
+    // returned WITHOUT forming Q (one n x m x m product less).  false: use orth(); the Gram it
+    // computed stays in P_G for orth's G0.
+    bool orth_factored(const double* Y, int64_t m, double* R_out, double* Rinv_out) {
+        if (2.0 * (double)n * (double)m * (double)m < 1e11) return false;
+        tm.begin(T_ORTH);
+        double* G = buf(P_G, m * m);
+        gram(Y, m, Y, m, G);
+        factored_gram = G;
+        double* R1 = buf(P_R1, m * m);
+        double* R1i = buf(P_R1I, m * m);
+        int* info = reinterpret_cast<int*>(buf(P_INT, 4 + 2 * m));
+        chol_inv_upper((int)m, G, R1, R1i, info, pool[P_SMALLWS], st);
+        const bool ok = !read_int(info) && single_pass_ok(R1, m);
+        if (ok) {
+            ++single_pass_calls;
+            W4_CUDA(cudaMemcpyAsync(R_out, R1, sizeof(double) * m * m, cudaMemcpyDeviceToDevice, st));
+            W4_CUDA(cudaMemcpyAsync(Rinv_out, R1i, sizeof(double) * m * m, cudaMemcpyDeviceToDevice, st));
+        }
+        tm.end();
+        return ok;
+    }
+    const double* factored_gram = nullptr;  // Y^T Y left by the last orth_factored (for orth's G0)
+
     // CholQR2: Q (n x m) with Y = Q R; G0 = Y^T Y may be supplied.  Q may alias Y (Y is
     // dead once Q1 = Y R1^{-1} exists); `scratch` (n x m) holds Q1 and must alias neither.
     // Returns false on a Cholesky breakdown (caller raises the method-specific
@@ -148,21 +188,12 @@ struct Ctx {
         chol_inv_upper((int)m, G, R1, R1i, info, pool[P_SMALLWS], st);
         if (read_int(info)) return false;
         // The second pass exists to repair the cond(Y)^2 eps loss of orthogonality of the first.
-        // When the passes are expensive (2 n m^2 >= 1e11 flops per Gram) the singular values of
-        // R1 (= those of Y) are computed first (Jacobi SVD of the m x m factor, ms): with
-        // cond(Y) <= 4 the first pass already gives |Q1^T Q1 - I| ~ 16 eps, what Householder QR
-        // of the reference delivers (m eps), and the second pass is skipped (C4: cond(Y) = 1.6,
-        // cond(Omega) = 1.01).  WC4DVAR_CHOLQR_ADAPT=0 always runs both passes.
-        const char* adapt_env = std::getenv("WC4DVAR_CHOLQR_ADAPT");  // read per call (tests toggle it)
-        const bool adapt = !adapt_env || std::atoi(adapt_env) != 0;
-        if (adapt && 2.0 * (double)n * (double)m * (double)m >= 1e11) {
-            double* sig = buf(P_R2, m * m);
-            svd_left_desc((int)m, R1, sig, buf(P_G2, m * m), pool[P_SMALLWS], st);
-            double hs[2];
-            W4_CUDA(cudaMemcpyAsync(&hs[0], sig, sizeof(double), cudaMemcpyDeviceToHost, st));
-            W4_CUDA(cudaMemcpyAsync(&hs[1], sig + (m - 1), sizeof(double), cudaMemcpyDeviceToHost, st));
-            W4_CUDA(cudaStreamSynchronize(st));
-            if (hs[1] > 0.0 && hs[0] <= 4.0 * hs[1]) {
+        // When the passes are expensive and cond(Y) <= 4 (single_pass_ok) the first pass already
+        // gives |Q1^T Q1 - I| ~ 16 eps, what Householder QR of the reference delivers (m eps), and
+        // the second pass is skipped (C4: cond(Y) = 1.6, cond(Omega) = 1.01).
+        // WC4DVAR_CHOLQR_ADAPT=0 always runs both passes.
+        {
+            if (single_pass_ok(R1, m)) {
                 ++single_pass_calls;
                 if (Q != Y) {
                     tall_times_small(Y, m, R1i, m, m, Q, n, true);
@@ -483,15 +514,25 @@ int64_t sketch_dev(wc4dvar_op& op, const wc4dvar_sketch_config& cfg, const doubl
         double* F = Z;  // Z is dead once E2 exists
         c.tall_times_small(E1, r, Rui, r, r, F, n, true);  // F = E1 U^{-1}, randevd.cpp:104-105
         double* RF = c.buf(P_R, r * r);
-        if (!c.orth(F, r, F, RF, nullptr, E1))
+        // BDCSVD(F) = Q_F (U_R S V^T) with F = Q_F R_F: when one CholQR pass suffices Q_F is never
+        // formed, U = Q_F W = F (R_F^{-1} W)
+        double* RFi = c.buf(P_TMP, r * r);
+        const bool factored = c.orth_factored(F, r, RF, RFi);
+        if (!factored && !c.orth(F, r, F, RF, c.factored_gram, E1))
             throw NumericalError("nystrom: factor F is numerically rank deficient (CholQR breakdown)");
         tm.begin(T_SMALL);
         double* sig = c.buf(P_VALS, r);
         double* W = c.buf(P_W, r * r);
         svd_left_desc((int)r, RF, sig, W, op.pool[P_SMALLWS], st);
         const int64_t keep = std::min<int64_t>(k, r);
+        const double* Wf = W;
+        if (factored) {
+            double* S = c.buf(P_K, r * r);  // E2 is dead
+            small_gemm(false, false, (int)r, (int)keep, (int)r, 1.0, RFi, (int)r, W, (int)r, 0.0, S, (int)r, st);
+            Wf = S;
+        }
         tm.begin(T_GEMM);
-        c.tall_times_small(F, r, W, r, keep, U_out, ldu);
+        c.tall_times_small(F, r, Wf, r, keep, U_out, ldu);
         square_head_kernel<<<1, 512, 0, st>>>((int)keep, sig, theta_out);
         W4_LAUNCH();
         tm.end();
@@ -499,10 +540,20 @@ int64_t sketch_dev(wc4dvar_op& op, const wc4dvar_sketch_config& cfg, const doubl
     } else if (cfg.method == WC4DVAR_SKETCH_RITZIT) {
         // randevd.cpp:116-136 (+ p_iter EXTENSION)
         double* G3 = bufA;
-        if (!c.orth(omega, m, G3, nullptr, nullptr, bufB))
-            throw NumericalError("revd_ritzit: Gaussian sample is numerically rank deficient");
         double* Y3 = bufB;
-        c.apply(G3, m, Y3);
+        // Omega = Q R_o.  With one subspace iteration and a sample that needs one CholQR pass
+        // (cond(Omega) ~ 1.01) Q is never formed: A is linear, so Y3 = A Q = (A Omega) R_o^{-1}; the
+        // block holds A Omega and the m x m factor R_o^{-1} stays pending ("lazy") until the end.
+        double* Ro = c.buf(P_RA, m * m);
+        double* Roi = c.buf(P_RB, m * m);
+        bool lazy = std::max(cfg.p_iter, 1) == 1 && c.orth_factored(omega, m, Ro, Roi);
+        if (lazy) {
+            c.apply(omega, m, Y3);
+        } else {
+            if (!c.orth(omega, m, G3, nullptr, c.factored_gram, bufB))
+                throw NumericalError("revd_ritzit: Gaussian sample is numerically rank deficient");
+            c.apply(G3, m, Y3);
+        }
         for (int it = 1; it < std::max(cfg.p_iter, 1); ++it) {
             if (!c.orth(Y3, m, Y3, nullptr, nullptr, G3))
                 throw NumericalError("revd_ritzit: QR of the sample matrix is rank deficient");
@@ -511,8 +562,42 @@ int64_t sketch_dev(wc4dvar_op& op, const wc4dvar_sketch_config& cfg, const doubl
         }
         double* Z3 = Y3;
         double* R3 = c.buf(P_R, m * m);
-        if (!c.orth(Y3, m, Z3, R3, nullptr, G3))
-            throw NumericalError("revd_ritzit: QR of the sample matrix is rank deficient");
+        // U = Z3 W with Y3 = Z3 R3: when one CholQR pass suffices Z3 is never formed, U = Y3 (R3^{-1} W)
+        double* R3i = c.buf(P_TMP, m * m);
+        bool factored = false;
+        if (lazy) {
+            // Gram of Y3 = (A Omega) R_o^{-1} from the Gram of the block: R_o^{-T} (A Omega)^T (A Omega) R_o^{-1}
+            tm.begin(T_ORTH);
+            double* Gy = c.buf(P_G, m * m);
+            c.gram(Y3, m, Y3, m, Gy);
+            double* T1 = c.buf(P_K, m * m);
+            small_gemm(false, false, (int)m, (int)m, (int)m, 1.0, Gy, (int)m, Roi, (int)m, 0.0, T1, (int)m, st);
+            small_gemm(true, false, (int)m, (int)m, (int)m, 1.0, Roi, (int)m, T1, (int)m, 0.0, Gy, (int)m, st);
+            double* R1 = c.buf(P_R1, m * m);
+            double* R1i = c.buf(P_R1I, m * m);
+            int* info = reinterpret_cast<int*>(c.buf(P_INT, 4 + 2 * m));
+            chol_inv_upper((int)m, Gy, R1, R1i, info, op.pool[P_SMALLWS], st);
+            factored = !c.read_int(info) && c.single_pass_ok(R1, m);
+            if (factored) {  // Y3 = Z3 R3 with R3 = R1; pending factor R_o^{-1} R1^{-1}
+                ++c.single_pass_calls;
+                W4_CUDA(cudaMemcpyAsync(R3, R1, sizeof(double) * m * m, cudaMemcpyDeviceToDevice, st));
+                small_gemm(false, false, (int)m, (int)m, (int)m, 1.0, Roi, (int)m, R1i, (int)m, 0.0, R3i, (int)m, st);
+                tm.end();
+            } else {  // materialise Y3 = (A Omega) R_o^{-1} and take the general route
+                tm.end();
+                tm.begin(T_GEMM);
+                c.tall_times_small(Y3, m, Roi, m, m, G3, n, true);
+                tm.end();
+                std::swap(G3, Y3);
+                Z3 = Y3;
+                lazy = false;
+            }
+        }
+        if (!lazy) {
+            factored = c.orth_factored(Y3, m, R3, R3i);
+            if (!factored && !c.orth(Y3, m, Z3, R3, c.factored_gram, G3))
+                throw NumericalError("revd_ritzit: QR of the sample matrix is rank deficient");
+        }
         // min |R_ii| <= 1e-14 max |R_ii| (randevd.cpp:125-127)
         std::vector<double> hR(m * m);
         W4_CUDA(cudaMemcpyAsync(hR.data(), R3, sizeof(double) * m * m, cudaMemcpyDeviceToHost, st));
@@ -536,8 +621,14 @@ int64_t sketch_dev(wc4dvar_op& op, const wc4dvar_sketch_config& cfg, const doubl
                                 cudaMemcpyDeviceToHost, st));
         W4_CUDA(cudaStreamSynchronize(st));
         if (hv <= 0.0) throw NumericalError("revd_ritzit: nonpositive squared Ritz value");
+        const double* Wf = W;
+        if (factored) {
+            double* S = c.buf(P_G2, m * m);
+            small_gemm(false, false, (int)m, (int)k, (int)m, 1.0, R3i, (int)m, W, (int)m, 0.0, S, (int)m, st);
+            Wf = S;
+        }
         tm.begin(T_GEMM);
-        c.tall_times_small(Z3, m, W, m, k, U_out, ldu);
+        c.tall_times_small(Z3, m, Wf, m, k, U_out, ldu);
         sqrt_head_kernel<<<1, 512, 0, st>>>((int)k, vals, theta_out);
         W4_LAUNCH();
         tm.end();
