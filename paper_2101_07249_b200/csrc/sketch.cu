@@ -148,11 +148,15 @@ struct Ctx {
     // next (Q W = Y (R^{-1} W)): when one CholQR pass suffices, R and R^{-1} of Y = Q R are
     // returned WITHOUT forming Q (one n x m x m product less).  false: use orth(); the Gram it
     // computed stays in P_G for orth's G0.
-    bool orth_factored(const double* Y, int64_t m, double* R_out, double* Rinv_out) {
+    bool orth_factored(const double* Y, int64_t m, double* R_out, double* Rinv_out, const double* G0 = nullptr) {
         if (2.0 * (double)n * (double)m * (double)m < 1e11) return false;
         tm.begin(T_ORTH);
         double* G = buf(P_G, m * m);
-        gram(Y, m, Y, m, G);
+        if (G0) {
+            if (G0 != G) W4_CUDA(cudaMemcpyAsync(G, G0, sizeof(double) * m * m, cudaMemcpyDeviceToDevice, st));
+        } else {
+            gram(Y, m, Y, m, G);
+        }
         factored_gram = G;
         double* R1 = buf(P_R1, m * m);
         double* R1i = buf(P_R1I, m * m);
@@ -471,6 +475,34 @@ int64_t sketch_dev(wc4dvar_op& op, const wc4dvar_sketch_config& cfg, const doubl
             msg << "revd: sample matrix rank collapsed to " << r << " of " << m << " columns";
             throw NumericalError(msg.str());
         }
+        // Z = householder_q(Y) only enters through A Z = (A Y) R^{-1} (A is linear), K = Z^T A Z =
+        // R^{-T} (Y^T A Y) R^{-1} and U = Z W = Y (R^{-1} W): when one CholQR pass suffices
+        // (cond(Y) <= 4) Z is never formed and the second block product runs on Y itself.
+        double* Rl = c.buf(P_RA, m * m);
+        double* Rli = c.buf(P_RB, m * m);
+        if (c.orth_factored(Y, m, Rl, Rli, G)) {
+            double* AY = bufB;
+            c.apply(Y, m, AY);  // second block product
+            tm.begin(T_GEMM);
+            double* Kraw = c.buf(P_G2, m * m);
+            c.gram(Y, m, AY, m, Kraw);
+            tm.begin(T_SMALL);
+            double* T1 = c.buf(P_R, m * m);
+            double* K = c.buf(P_K, m * m);
+            small_gemm(false, false, (int)m, (int)m, (int)m, 1.0, Kraw, (int)m, Rli, (int)m, 0.0, T1, (int)m, st);
+            small_gemm(true, false, (int)m, (int)m, (int)m, 1.0, Rli, (int)m, T1, (int)m, 0.0, K, (int)m, st);
+            double* vals = c.buf(P_VALS, m);
+            double* W = c.buf(P_W, m * m);
+            sym_evd_desc((int)m, K, vals, W, c.pool[P_SMALLWS], st);
+            double* S = c.buf(P_G2, m * m);
+            small_gemm(false, false, (int)m, (int)k, (int)m, 1.0, Rli, (int)m, W, (int)m, 0.0, S, (int)m, st);
+            tm.begin(T_GEMM);
+            c.tall_times_small(Y, m, S, m, k, U_out, ldu);
+            W4_CUDA(cudaMemcpyAsync(theta_out, vals, sizeof(double) * k, cudaMemcpyDeviceToDevice, st));
+            tm.end();
+            tm.collect(timing);
+            return k;
+        }
         double* Z = bufA;  // householder_q(Y), randevd.cpp:74
         if (!c.orth(Y, m, Z, nullptr, G, bufB))
             throw NumericalError("revd: sample matrix is numerically rank deficient (CholQR breakdown)");
@@ -493,13 +525,27 @@ int64_t sketch_dev(wc4dvar_op& op, const wc4dvar_sketch_config& cfg, const doubl
             Z = bufB;
             other = bufA;
         }
-        if (!c.orth(Z, r, Z, nullptr, r < m ? nullptr : G, other))
+        // Full rank and one CholQR pass (cond(Y) <= 4): Z = Y R^{-1} is never formed; E1 = A Z =
+        // (A Y) R^{-1} stays lazy (the block holds A Y), E2 = Z^T E1 = R^{-T} (Y^T A Y) R^{-1}, and
+        // the pending R^{-1} joins U^{-1} in the one product that forms F.
+        double* Rl = c.buf(P_RA, m * m);
+        double* Rli = c.buf(P_RB, m * m);
+        const bool lazy = r == m && c.orth_factored(Y, m, Rl, Rli, G);
+        if (!lazy && !c.orth(Z, r, Z, nullptr, r < m ? nullptr : G, other))
             throw NumericalError("nystrom: sample matrix is numerically rank deficient (CholQR breakdown)");
         double* E1 = other;
         c.apply(Z, r, E1);
         tm.begin(T_GEMM);
         double* E2 = c.buf(P_K, r * r);
-        c.gram(Z, r, E1, r, E2);
+        if (lazy) {
+            double* E2raw = c.buf(P_G2, r * r);
+            double* T1 = c.buf(P_R, r * r);
+            c.gram(Z, r, E1, r, E2raw);
+            small_gemm(false, false, (int)r, (int)r, (int)r, 1.0, E2raw, (int)r, Rli, (int)r, 0.0, T1, (int)r, st);
+            small_gemm(true, false, (int)r, (int)r, (int)r, 1.0, Rli, (int)r, T1, (int)r, 0.0, E2, (int)r, st);
+        } else {
+            c.gram(Z, r, E1, r, E2);
+        }
         tm.begin(T_SMALL);
         double* Ru = c.buf(P_R1, r * r);
         double* Rui = c.buf(P_R1I, r * r);
@@ -512,7 +558,13 @@ int64_t sketch_dev(wc4dvar_op& op, const wc4dvar_sketch_config& cfg, const doubl
                 "spectra.");
         tm.begin(T_GEMM);
         double* F = Z;  // Z is dead once E2 exists
-        c.tall_times_small(E1, r, Rui, r, r, F, n, true);  // F = E1 U^{-1}, randevd.cpp:104-105
+        const double* Fi = Rui;
+        if (lazy) {  // F = (A Y) (R^{-1} U^{-1}): upper triangular times upper triangular
+            double* T2 = c.buf(P_G2, r * r);
+            small_gemm(false, false, (int)r, (int)r, (int)r, 1.0, Rli, (int)r, Rui, (int)r, 0.0, T2, (int)r, st);
+            Fi = T2;
+        }
+        c.tall_times_small(E1, r, Fi, r, r, F, n, true);  // F = E1 U^{-1}, randevd.cpp:104-105
         double* RF = c.buf(P_R, r * r);
         // BDCSVD(F) = Q_F (U_R S V^T) with F = Q_F R_F: when one CholQR pass suffices Q_F is never
         // formed, U = Q_F W = F (R_F^{-1} W)
