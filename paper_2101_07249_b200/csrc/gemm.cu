@@ -1220,7 +1220,7 @@ void gemm_nn(const GemmPass* passes, int npass, unsigned* status, cudaStream_t s
 
 void gemm_tn(int64_t R, int64_t m1, int64_t m2, const double* A, int64_t lda, const double* B,
              int64_t ldb, double alpha, double* C, int64_t ldc, DevBuf& work,
-             cudaStream_t stream) {
+             cudaStream_t stream, bool sym_result) {
     if (m1 == 0 || m2 == 0) return;
     // tile variant (WC4DVAR_GEMM_TN, default 0 = by shape): 1: 64x64 / 4 warps / 4 stages,
     // 2: 64x64 / 8 warps, 3: 128x64 / 8 warps / 3 stages, 4: 128x128 / 16 warps / 3 stages
@@ -1240,7 +1240,7 @@ void gemm_tn(int64_t R, int64_t m1, int64_t m2, const double* A, int64_t lda, co
         return !(e && std::atoi(e) == 0);
     }();
     const bool vec2 = aligned16(A) && aligned16(B) && lda % 2 == 0 && ldb % 2 == 0;
-    const bool sym = syrk_env && A == B && m1 == m2 && lda == ldb && BM == BN && vec2 && var != 2 &&
+    const bool sym = syrk_env && (A == B || sym_result) && m1 == m2 && lda == ldb && BM == BN && vec2 && var != 2 &&
                      cdiv(m1, BM) > 1;
     const int64_t tiles = sym ? cdiv(m1, BM) * (cdiv(m1, BM) + 1) / 2 : cdiv(m1, BM) * cdiv(m2, BN);
     // (sym: whole waves -- floor -- so no split lands in a one-CTA tail wave)

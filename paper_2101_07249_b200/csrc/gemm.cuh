@@ -60,7 +60,9 @@ void gemm_nn(const GemmPass* passes, int npass, unsigned* status, cudaStream_t s
 // ldb == lda) the product is a Gram matrix: only the tiles on and above the diagonal are
 // computed and the reduction mirrors them (bitwise the full product: the DMMA sums of
 // (r, c) and (c, r) multiply the same pairs in the same k order).
+// sym_result: the caller knows A^T B is symmetric (Y^T (A Y) for the symmetric operator A): only
+// the upper-triangle tiles are computed and mirrored, as for a Gram A^T A.
 void gemm_tn(int64_t R, int64_t m1, int64_t m2, const double* A, int64_t lda, const double* B,
-             int64_t ldb, double alpha, double* C, int64_t ldc, DevBuf& work, cudaStream_t stream);
+             int64_t ldb, double alpha, double* C, int64_t ldc, DevBuf& work, cudaStream_t stream, bool sym_result = false);
 
 }  // namespace w4

@@ -110,8 +110,9 @@ struct Ctx {
     }
 
     // G = A^T B (m1 x m2)
-    void gram(const double* A, int64_t m1, const double* B, int64_t m2, double* G) {
-        gemm_tn(n, m1, m2, A, n, B, n, 1.0, G, m1, pool[P_GEMMWS], st);
+    // sym: A^T B is known to be symmetric (upper-triangle tiles only, mirrored)
+    void gram(const double* A, int64_t m1, const double* B, int64_t m2, double* G, bool sym = false) {
+        gemm_tn(n, m1, m2, A, n, B, n, 1.0, G, m1, pool[P_GEMMWS], st, sym);
     }
 
     // C (n x ncols) = A (n x K) * B (K x ncols, ld K); tri: B is upper triangular (R^{-1})
@@ -485,7 +486,7 @@ int64_t sketch_dev(wc4dvar_op& op, const wc4dvar_sketch_config& cfg, const doubl
             c.apply(Y, m, AY);  // second block product
             tm.begin(T_GEMM);
             double* Kraw = c.buf(P_G2, m * m);
-            c.gram(Y, m, AY, m, Kraw);
+            c.gram(Y, m, AY, m, Kraw, true);  // Y^T A Y, A symmetric
             tm.begin(T_SMALL);
             double* T1 = c.buf(P_R, m * m);
             double* K = c.buf(P_K, m * m);
@@ -540,7 +541,7 @@ int64_t sketch_dev(wc4dvar_op& op, const wc4dvar_sketch_config& cfg, const doubl
         if (lazy) {
             double* E2raw = c.buf(P_G2, r * r);
             double* T1 = c.buf(P_R, r * r);
-            c.gram(Z, r, E1, r, E2raw);
+            c.gram(Z, r, E1, r, E2raw, true);  // Y^T A Y, A symmetric
             small_gemm(false, false, (int)r, (int)r, (int)r, 1.0, E2raw, (int)r, Rli, (int)r, 0.0, T1, (int)r, st);
             small_gemm(true, false, (int)r, (int)r, (int)r, 1.0, Rli, (int)r, T1, (int)r, 0.0, E2, (int)r, st);
         } else {
