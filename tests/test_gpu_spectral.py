@@ -58,7 +58,7 @@ def test_spectral_single_column_block_packing():
     """One column packs its window blocks in pairs and separates the spectra by Hermitian
     symmetry (spectral_window1): odd and even block counts, the self-mirrored row k2 = 0 of the
     digit-reversed order, against the oracle and against the generic (half-empty) packing."""
-    for n, N, sx in ((10000, 3, 10), (10000, 4, 4), (100000, 6, 10)):
+    for n, N, sx in ((10000, 3, 10), (10000, 4, 4), (100000, 6, 10), (1000000, 16, 10)):  # the last: C4's grid and window
         bh, qh = circ_factors(n, 7.0)
         model, net = W.AdvDiffLinearized(n, N, 0.5, 0.2, 3), _net(n, N, sx)
         g, o = pair(model, net, bh, qh, 0.1)
