@@ -163,6 +163,13 @@ public:
     }
     const ObservationNetwork& network() const { return net_; }
     double sigma_obs() const { return sigma_obs_; }
+    // Fourier-space form of apply / apply_block (wc4dvar_gpu_op_spectral): mode 1 / 0 switches it
+    // on / off, -1 queries; returns whether it is active (an execution strategy, same result).
+    bool spectral(int mode = -1) {
+        int active = 0;
+        check(wc4dvar_gpu_op_spectral(h_, mode, &active));
+        return active != 0;
+    }
     // operators.hpp:127-135 (not counted as applies, as in the reference)
     Vector apply_Linv(const Vector& p) const { return piece(WC4DVAR_LINV, p); }
     Vector apply_LinvT(const Vector& v) const { return piece(WC4DVAR_LINVT, v); }

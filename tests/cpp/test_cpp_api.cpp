@@ -114,6 +114,15 @@ static void test_hessian_vs_oracle() {
     const CovarianceFactor b = circulant_soar_sqrt(n, 1.0, 3.0), q = circulant_soar_sqrt(n, 0.3, 3.0);
     HessianOperator op(model, net, b, q, 0.1);
     CHECK(op.dim() == n * (N + 1));
+    // n = 40 has no fused transform: the Fourier-space form is not eligible and cannot be forced
+    CHECK(!op.spectral());
+    bool refused = false;
+    try {
+        op.spectral(1);
+    } catch (const std::invalid_argument&) {
+        refused = true;
+    }
+    CHECK(refused);
     const Index m = 5;
     Matrix V(op.dim(), m);
     orc_gaussian_matrix(op.dim(), m, 7, V.data());
