@@ -1231,7 +1231,11 @@ void gemm_tn(int64_t R, int64_t m1, int64_t m2, const double* A, int64_t lda, co
     int var = var_env;
     // measured (C4 n = 1.7e7, m = 256): 128x128 / 16 warps 28.2 TF/s vs 64x64 / 4 warps ~17;
     // at m = 64 (C3) the 64x64 tiles win (25 vs 7 TF/s: a 128-wide tile is half empty)
-    if (var == 0) var = (m1 >= 128 && m2 >= 128) ? 4 : (m1 >= 128 ? 3 : 1);
+    // symmetric results (Grams, Y^T A Y): only the upper-triangle tiles run, and 64 x 64 tiles cut
+    // more of the square (10 of 16 at m = 256) than 128 x 128 ones (3 of 4): measured 143 vs 169 ms
+    // of tall GEMMs per C4 k + l = 256 REVD
+    const bool sym_shape = (A == B || sym_result) && m1 == m2 && lda == ldb;
+    if (var == 0) var = (m1 >= 128 && m2 >= 128) ? (sym_shape ? 1 : 4) : (m1 >= 128 ? 3 : 1);
     const int BM = (var >= 3) ? 128 : 64, BN = (var == 4) ? 128 : 64;
     const int ctas_per_sm = (var == 4) ? 1 : 2;
     // Gram (A^T A): upper-triangle tiles only (square tiles; WC4DVAR_GEMM_SYRK=0 disables)
