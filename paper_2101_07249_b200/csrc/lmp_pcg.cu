@@ -2,6 +2,7 @@
 #include "lmp_pcg.cuh"
 
 #include <algorithm>
+#include <cstdlib>
 
 #include "bulk.cuh"
 
@@ -251,6 +252,100 @@ __global__ void __launch_bounds__(kRP, CPS)
     }
 }
 
+// Plain vector passes of the unpreconditioned PCG (k = 0, krylov.cpp:55-95 with C = I).  Same
+// grid, row ownership (thread tid owns row tid of tiles blockIdx.x + it gridDim.x) and
+// reduction order as rowpass_kernel<MODE, 0, 4>, so the results are bitwise the same; the
+// vectors are read straight from global memory with UN tiles of every stream in flight per
+// thread and no per-tile barrier (a 256-row tile of 2-4 vectors is too small for the
+// bulk-copy ring: one or two tiles in flight per CTA left the pass latency-bound).
+template <int MODE>
+__global__ void __launch_bounds__(kRP, 4) vecpass_kernel(const RowPassCtx c, const PassArgs A) {
+    __shared__ double wred[kRP / 32];
+    __shared__ int is_last;
+    constexpr int UN = (MODE == M_P2) ? 4 : 8;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int64_t n = c.n;
+    const int64_t stride = (int64_t)gridDim.x * kRP;
+    double alpha = 0.0, beta = 0.0;
+    if (MODE == M_P2) alpha = c.scal[SC_ALPHA];
+    if (MODE == M_P3) beta = c.scal[SC_BETA];
+    double dotc = 0.0;
+    for (int64_t base = (int64_t)blockIdx.x * kRP + tid; base < n; base += UN * stride) {
+        double v0[UN], v1[UN], v2[UN], v3[UN];
+#pragma unroll
+        for (int u = 0; u < UN; ++u) {
+            const int64_t row = base + u * stride;
+            const bool ok = row < n;
+            if (MODE == M_P1) {
+                v0[u] = ok ? __ldcs(A.w + row) : 0.0;
+                v1[u] = ok ? __ldcs(A.p + row) : 0.0;
+            } else if (MODE == M_P2) {
+                v0[u] = ok ? __ldcs(A.w + row) : 0.0;
+                v1[u] = ok ? __ldcs(A.x + row) : 0.0;
+                v2[u] = ok ? __ldcs(A.p + row) : 0.0;
+                v3[u] = ok ? __ldcs(A.r + row) : 0.0;
+            } else {
+                v0[u] = ok ? __ldcs(A.r + row) : 0.0;
+                v1[u] = ok ? __ldcs(A.p + row) : 0.0;
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < UN; ++u) {
+            const int64_t row = base + u * stride;
+            if (row >= n) continue;
+            if (MODE == M_P1) {
+                const double e = v0[u];   // w
+                dotc += v1[u] * e;        // p . w
+            } else if (MODE == M_P2) {
+                const double ctw = v0[u] - 0.0;           // C^T w with C = I
+                A.x[row] = v1[u] + alpha * v2[u];         // x += alpha p
+                const double rn = v3[u] - alpha * ctw;    // r -= alpha w
+                A.r[row] = rn;
+                dotc += rn * rn;
+            } else {
+                A.p[row] = (v0[u] - 0.0) + beta * v1[u];  // p = r + beta p
+            }
+        }
+    }
+    if (MODE == M_P3) return;
+    double* partial = c.partial + (int64_t)blockIdx.x;
+    const double d = warp_sum(dotc);
+    if (lane == 0) wred[warp] = d;
+    __syncthreads();
+    if (tid == 0) {
+        double s = 0.0;
+        for (int w = 0; w < kRP / 32; ++w) s += wred[w];
+        partial[0] = s;
+    }
+    __threadfence();
+    __syncthreads();
+    if (tid == 0) is_last = (atomicAdd(c.counter, 1u) == gridDim.x - 1);
+    __syncthreads();
+    if (!is_last) return;
+    __threadfence();
+    double* res = (MODE == M_P1) ? c.g : c.h;
+    if (warp == 0) {
+        double s = 0.0;
+        for (unsigned b = lane; b < gridDim.x; b += 32) s += __ldcg(c.partial + b);
+        s = warp_sum(s);
+        if (lane == 0) res[0] = s;
+    }
+    __syncthreads();
+    if (tid == 0) {
+        *c.counter = 0u;
+        if (MODE == M_P1) {
+            const double curv = res[0];
+            c.scal[SC_CURV] = curv;
+            c.scal[SC_ALPHA] = c.scal[SC_RHO] / curv;
+        } else {
+            const double rn = res[0];
+            c.scal[SC_RHO_NEXT] = rn;
+            c.scal[SC_BETA] = rn / c.scal[SC_RHO];
+            c.scal[SC_RHO] = rn;
+        }
+    }
+}
+
 int pick_rb(int k) {
     int rb = kStageDoubles / (k + 4);
     rb = (rb / 16) * 16;
@@ -290,6 +385,14 @@ void launch_pass_n(const RowPassCtx& c, const PassArgs& a, cudaStream_t st) {
     const int64_t ntiles = cdiv(c.n, RB);
     if (NACC == 0 && c.k == 0) {  // plain vector passes: four CTAs per SM (partials: <= 2048 CTAs)
         const int64_t grid4 = std::max<int64_t>(1, std::min<int64_t>({ntiles, (int64_t)4 * nsm, (int64_t)2048}));
+        if constexpr (MODE == M_P1 || MODE == M_P2 || MODE == M_P3) if (RB == kRP) {
+            const char* e = getenv("WC4DVAR_PCG_VECPASS");  // 0: the bulk-copy ring kernel
+            if (!(e && e[0] == '0')) {
+                vecpass_kernel<MODE><<<(unsigned)grid4, kRP, 0, st>>>(c, a);
+                W4_LAUNCH();
+                return;
+            }
+        }
         rowpass_kernel<MODE, 0, 4><<<(unsigned)grid4, kRP, smem, st>>>(c, a, RB, nparts, bulk ? 1 : 0);
         W4_LAUNCH();
         return;

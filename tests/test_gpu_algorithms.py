@@ -290,3 +290,24 @@ def test_inner_loop_vs_oracle(method, wl):
         fo_dev = O.build_spectral_lmp(O.RitzPairs(pg.vectors, pg.values))
         rod = O.pcg_split(o, b, fo_dev, opts=O.PcgOptions(**opts))
         _same_steps_parity(rg, o, b, fo_dev, delta, rod.history.iterations, (7, 6, 5))
+
+
+@pytest.mark.parametrize("mk", [configs.small_advdiff, configs.config1, configs.config2, configs.config3],
+                         ids=lambda f: f.__name__)
+def test_plain_vector_passes_bitwise_equal_ring_kernel(mk, monkeypatch):
+    """The unpreconditioned PCG passes (krylov.cpp:55-95 with C = I) run as direct-load vector
+    kernels; they keep the bulk-copy ring kernel's row ownership and reduction order, so every
+    iterate, alpha, beta and residual norm is bitwise the same (WC4DVAR_PCG_VECPASS=0 selects
+    the ring kernel).  The dims cover fewer tiles than CTAs, ragged last tiles and (C3,
+    n_A = 1.1e6) several tiles per CTA."""
+    op = mk().hessian(0)
+    b = np.asarray(W.gaussian_matrix(op.dim(), 1, 9))[:, 0].copy()
+    runs = []
+    for flag in ("0", "1"):
+        monkeypatch.setenv("WC4DVAR_PCG_VECPASS", flag)
+        runs.append(W.pcg_split(op, b, opts=W.PcgOptions(max_iter=25, rel_tol=1e-10)))
+    p0, p1 = runs
+    assert p0.history.iterations == p1.history.iterations
+    assert np.array_equal(p0.x, p1.x)
+    assert p0.history.alphas == p1.history.alphas and p0.history.betas == p1.history.betas
+    assert p0.history.residual_norms == p1.history.residual_norms
