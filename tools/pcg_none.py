@@ -12,8 +12,13 @@ for name, mk in (("C4", lambda: configs.config4(16)), ("C3", configs.config3), (
         continue
     wl = mk(); op = wl.hessian(0)
     b = np.asarray(W.gaussian_matrix(op.dim(), 1, 2))[:, 0].copy()
-    for it in range(2):
+    # two run lengths: the slope is the per-iteration cost without the fixed part (H2D of b,
+    # D2H of x through pageable numpy buffers, the first un-graphed iteration, graph build)
+    ts = {}
+    for its in (iters, iters, 2 * iters):
         t0 = time.perf_counter()
-        r = W.pcg_split(op, b, None, opts=W.PcgOptions(rel_tol=0.0, max_iter=iters))
-        dt = time.perf_counter() - t0
-    print(f"{name} none: {dt*1e3/ r.history.iterations:.3f} ms/iteration ({r.history.iterations} iterations)", flush=True)
+        r = W.pcg_split(op, b, None, opts=W.PcgOptions(rel_tol=0.0, max_iter=its))
+        ts[r.history.iterations] = time.perf_counter() - t0
+    (i1, t1), (i2, t2) = sorted(ts.items())
+    print(f"{name} none: {(t2 - t1) * 1e3 / (i2 - i1):.3f} ms/iteration (slope {i1} -> {i2} iterations; "
+          f"fixed part {(t1 - i1 * (t2 - t1) / (i2 - i1)) * 1e3:.1f} ms)", flush=True)
