@@ -1,4 +1,5 @@
-"""ncu driver: a few C2 PCG iterations WITH a Nystrom LMP (k = 50), per-iteration wall time."""
+"""ncu driver: a few PCG iterations WITH a Nystrom LMP (C2, k = 50, by default; argv[2] = C3 for
+the k = 32 Lorenz-96 configuration), per-iteration wall time."""
 import json
 import os
 import sys
@@ -11,7 +12,7 @@ import paper_2101_07249_b200 as W  # noqa: E402
 from paper_2101_07249_b200 import configs  # noqa: E402
 
 iters = int(sys.argv[1]) if len(sys.argv) > 1 else 20
-wl = configs.config2()
+wl = configs.config3() if (len(sys.argv) > 2 and sys.argv[2] == "C3") else configs.config2()
 op = wl.hessian(0)
 nA = op.dim()
 p = W.sketch_eigenpairs(op, W.SketchConfig(wl.k, wl.m - wl.k, configs.OMEGA_SEED, "nystrom"))
