@@ -28,6 +28,8 @@
 // imaginary parts: every step is complex-linear with real grid-space operators.
 #include "spectral.cuh"
 
+#include <cstdlib>
+
 #include "bulk.cuh"
 
 namespace w4 {
@@ -181,7 +183,7 @@ __device__ __forceinline__ int64_t mirror_pos(const Window1Args& w, int64_t t) {
 
 __global__ void __launch_bounds__(kSpecThreads) spectral_window1_kernel(const SpectralArgs a, const Window1Args w) {
     extern __shared__ double2 sm[];
-    const int T = kSpecThreads, t = threadIdx.x;
+    const int T = (int)blockDim.x, t = threadIdx.x;  // 160 or kSpecThreads: a multiple of RL
     const int cps = a.RL / a.sx, ncl = T / a.sx;
     double2* xbuf = sm;          // [2][T]
     double2* sums = sm + 2 * T;  // [per][ncl]
@@ -295,13 +297,22 @@ void spectral_window1(const SpectralArgs& a, const double2* Zin, double2* Zout, 
     w.N2 = N2;
     for (int i = 0; i < 4; ++i) w.rad[i] = rad[i];
     w.nrad = nrad;
-    const size_t smem = sizeof(double2) * ((size_t)2 * kSpecThreads + (size_t)a.per * (kSpecThreads / a.sx));
+    // 160-thread CTAs where the row radix allows (five warps hold whole frequency-class groups
+    // for RL = 10 and 20): the per-block barrier then spans half as many warps; the class sums
+    // and recurrences are per thread / per class, so the CTA width never changes a bit
+    static const int t_env = [] {
+        const char* e = std::getenv("WC4DVAR_SPECTRAL_W1T");
+        return e ? std::atoi(e) : 0;
+    }();
+    int T1 = (160 % a.RL == 0 && 160 % a.sx == 0) ? 160 : kSpecThreads;
+    if (t_env == kSpecThreads) T1 = kSpecThreads;
+    const size_t smem = sizeof(double2) * ((size_t)2 * T1 + (size_t)a.per * (T1 / a.sx));
     static bool attr = false;
     if (!attr) {
         W4_CUDA(cudaFuncSetAttribute(spectral_window1_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
         attr = true;
     }
-    spectral_window1_kernel<<<(unsigned)cdiv(a.N, (int64_t)kSpecThreads), kSpecThreads, smem, st>>>(a, w);
+    spectral_window1_kernel<<<(unsigned)cdiv(a.N, (int64_t)T1), T1, smem, st>>>(a, w);
     W4_LAUNCH();
 }
 
